@@ -1,0 +1,145 @@
+/*
+ * sgn_b200.h -- C ABI of the B200-native sparse Gauss-Newton (SGN) search-direction path.
+ *
+ * This is the drop-in boundary for the reference package `sgnopt` (arXiv 2107.03285).
+ * The reference is pure Python; its solver plugin surface is a set of Python callables
+ * (pkg/src/sgnopt/__init__.py:26-93).  The Python shim `paper_2107_03285_b200` re-exports
+ * those callables with identical names/arguments/errors and binds the entry points below
+ * through ctypes.  Each entry point names the reference interface it replaces.
+ *
+ * Conventions
+ *   - every call returns a status code (SGN_OK ...); details via sgn_last_error();
+ *   - "d_" pointers are device pointers owned by the caller; handles are owned by the
+ *     library and freed by *_destroy;
+ *   - every asynchronous call takes a cudaStream_t (passed as void*);  a handle is not
+ *     thread-safe: one host thread per handle;
+ *   - values are float64, matrix indices int64 on the host side (the reference's CscMatrix
+ *     uses int64 indptr/indices, pkg/src/sgnopt/sparse.py:71-72);
+ *   - KKT unknown order is the reference's (x[n_x], p[n_p], lambda[n_c]) with n_c == n_x
+ *     (pkg/src/sgnopt/sparse.py:165-194).
+ */
+#ifndef SGN_B200_H
+#define SGN_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> errors.py types (mapped in paper_2107_03285_b200/_lib.py) */
+#define SGN_OK             0
+#define SGN_SINGULAR       1   /* SingularMatrix(pivot_index)           errors.py:26-35 */
+#define SGN_NO_CONVERGENCE 2   /* NoConvergence(residual, iterations)   errors.py:46-54 */
+#define SGN_DIMENSION      3   /* DimensionMismatch                     errors.py:9     */
+#define SGN_CUDA_ERROR     4   /* CUDA runtime failure (message in sgn_last_error)      */
+#define SGN_INVALID        5   /* bad argument / unsupported input                      */
+
+/* solve flags */
+#define SGN_SOLVE_LEADING  1   /* solve only with the leading (x, lambda) block of the
+                                  factor; p unknowns are held at zero (adjoint solve)     */
+
+typedef struct sgn_symbolic_s* sgn_symbolic;
+typedef struct sgn_factor_s*   sgn_factor;
+
+typedef struct {
+    int64_t n;             /* dimension                                   */
+    int64_t n_fronts;      /* fronts (dense supernodes) in the assembly tree */
+    int64_t n_levels;      /* tree levels (height scheduling)             */
+    int64_t nnz_l;         /* stored entries of L (incl. D)               */
+    int64_t front_doubles; /* dense front storage per instance (doubles)  */
+    int64_t max_front;     /* largest front order                         */
+    int64_t max_piv;       /* largest pivot block of a front              */
+    int64_t launches;      /* kernel launches of one numeric factorization */
+    double  flops;         /* LDL^T flops of one numeric factorization    */
+    int64_t pair_mode;     /* 1 = (x_i, lambda_pi(i)) 2x2 pivots + p-root  */
+} sgn_symbolic_stats;
+
+/* ---- library ------------------------------------------------------------------- */
+const char* sgn_last_error(void);
+int sgn_version(void);
+int sgn_device_sync(void* stream);
+
+/* ---- symbolic analysis (host, once per sparsity pattern) -----------------------
+ * Replaces the ordering/symbolic half of SparseFactorization.__init__
+ * (pkg/src/sgnopt/linear_solvers.py:70-91: structural checks + SuperLU COLAMD).
+ * indptr/indices: full CSC pattern (sorted, unique rows) of a structurally symmetric
+ * matrix.  n_x > 0 selects KKT mode (x, p, lambda blocks; 2x2 pivots on matched
+ * (x_i, lambda_j) pairs, p unknowns eliminated last in one dense root front);
+ * n_x == 0 selects generic mode (1x1 pivots).  leaf_size: max unknowns in a leaf front
+ * (0 = default).  On structural singularity returns SGN_SINGULAR and *pivot_index.   */
+int sgn_symbolic_create(int64_t n, const int64_t* indptr, const int64_t* indices,
+                        int64_t n_x, int64_t n_p, int64_t n_c, int32_t leaf_size,
+                        sgn_symbolic* out, int64_t* pivot_index);
+int  sgn_symbolic_get_stats(sgn_symbolic s, sgn_symbolic_stats* out);
+/* perm[k] = original unknown eliminated at position k */
+int  sgn_symbolic_get_perm(sgn_symbolic s, int64_t* perm);
+/* front tree export for host-side verification: per front (first position, npiv, nrow,
+ * parent); rows_ptr (n_fronts+1) / rows (positions) */
+int  sgn_symbolic_get_fronts(sgn_symbolic s, int64_t* first, int64_t* npiv, int64_t* nrow,
+                             int64_t* parent, int64_t* rows_ptr, int64_t* rows);
+void sgn_symbolic_destroy(sgn_symbolic s);
+
+/* ---- numeric factorization (device) --------------------------------------------
+ * Replaces spla.splu (linear_solvers.py:87) + the stabilization of stabilized_matrix
+ * (linear_solvers.py:111-127): factors K + diag(+eps_x, 0, -eps_lambda) as
+ * P^T K P = L D L^T (multifrontal, DMMA Schur updates).  `batch` independent instances
+ * share the pattern; instance b's values start at d_values + b*values_stride.        */
+int  sgn_factor_create(sgn_symbolic s, int32_t batch, sgn_factor* out);
+int  sgn_factor_numeric(sgn_factor f, const double* d_values, int64_t values_stride,
+                        double eps_x, double eps_lambda, void* stream);
+/* synchronizes; returns SGN_SINGULAR with the first zero pivot (original index) */
+int  sgn_factor_check(sgn_factor f, void* stream, int64_t* pivot_index);
+/* x = (L D L^T)^{-1} b for every instance (b, x strided by n). Replaces
+ * SparseFactorization.solve (linear_solvers.py:93-97); `transpose` is a no-op for the
+ * symmetric factor.  flags: SGN_SOLVE_LEADING.  d_b may alias d_x.                 */
+int  sgn_factor_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, void* stream);
+void sgn_factor_destroy(sgn_factor f);
+
+/* y = K x on the full symmetric CSC pattern (which equals its CSR).  Replaces the
+ * scipy SpMV of _relative_residual / _bicgstab_refine (linear_solvers.py:105-108,178-211).
+ * flags: SGN_SOLVE_LEADING masks the p block (input and output).                   */
+int  sgn_spmv(sgn_factor f, const double* d_values, int64_t values_stride,
+              const double* d_x, double* d_y, int32_t flags, void* stream);
+
+/* Post-factor half of solve_kkt_stabilized (linear_solvers.py:130-175) with
+ * _bicgstab_refine (178-211) on the device: x0 = F^{-1} rhs; if the relative residual
+ * against the UNSHIFTED K exceeds tol run restart-free left-preconditioned BiCGSTAB,
+ * keeping the best iterate.  Per-instance results in rel_res[batch], iters[batch].
+ * Returns SGN_NO_CONVERGENCE if any instance ends above tol (d_sol then holds the best
+ * iterate, mirroring NoConvergence.best).                                          */
+int  sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_stride,
+                       const double* d_rhs, double* d_sol, double tol, int32_t max_iters,
+                       int32_t flags, double* rel_res, int32_t* iters, void* stream);
+
+/* ---- element assembly (device) --------------------------------------------------
+ * Replaces the NumPy element kernels + COO->CSC of constraint_jac_x / constraint_jac_p
+ * (spring analog: forward.py:61-111, spring_bar.py:144-156).  Per element, writes the
+ * element Hessian d2E/dx2 and mixed derivative d2E/dx dX (rest coordinates) in
+ * row-major (nd x nd) blocks, nd = nodes_per_elem * dim.                           */
+#define SGN_ELEM_SPRING     1   /* 2-node spring, any dim (forward.py:61-111)        */
+#define SGN_ELEM_NH_TRI     2   /* 3-node neo-Hookean triangle, plane strain         */
+#define SGN_ELEM_NH_TET     3   /* 4-node neo-Hookean tetrahedron                    */
+int  sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch,
+                        const int32_t* d_conn, const double* d_pos, const double* d_rest,
+                        int64_t vert_stride, const double* d_params, int64_t param_stride,
+                        double* d_hess, double* d_mixed, int64_t buf_stride, void* stream);
+/* element energies / gradients for the forward solve and line search
+ * (spring_energy/spring_gradient analog, forward.py:34-48) */
+int  sgn_element_energy_grad(int32_t elem_type, int64_t n_elems, int32_t batch,
+                             const int32_t* d_conn, const double* d_pos, const double* d_rest,
+                             int64_t vert_stride, const double* d_params, int64_t param_stride,
+                             double* d_energy, double* d_grad, int64_t buf_stride, void* stream);
+
+/* out[k] = base[k] + sum_{t in ptr[k]..ptr[k+1]} coef[t] * buf[idx[t]]  (atomic-free,
+ * fixed-order segmented sum into a precomputed CSC pattern; per instance strided).  */
+int  sgn_gather_values(int64_t n_out, int32_t batch, const double* d_base, int64_t base_stride,
+                       const int64_t* d_ptr, const int64_t* d_idx, const double* d_coef,
+                       const double* d_buf, int64_t buf_stride, double* d_out,
+                       int64_t out_stride, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGN_B200_H */

@@ -1,0 +1,17 @@
+"""B200-native sparse Gauss-Newton (SGN) search-direction path -- drop-in for sgnopt.
+
+Re-exports the reference package's solver-path names (reference
+pkg/src/sgnopt/__init__.py:9-93, hot-path subset) with identical signatures and
+error behaviour; the numerics run in hand-written sm_100a CUDA (``_sgnb200.so``).
+"""
+from .errors import (CapabilityMissing, DeviceError, DimensionMismatch, ForwardSimFailure,
+                     InfeasiblePoint, LineSearchFailure, MeritLineSearchFailure,
+                     NegativeCurvature, NoConvergence, NonSquareParamJacobian,
+                     NotPositiveDefinite, NumericalBlowup, SingularConstraintJacobian,
+                     SingularMatrix, ToolkitError, TripletIndexError)
+from .linear_solvers import (SolveReport, SparseFactorization, StabilizationConfig,
+                             factor_sparse, solve_kkt_stabilized, stabilized_matrix)
+from .sparse import (CscMatrix, TripletMatrix, csc_from_triplets, read_matrix_market, spmv,
+                     spmv_transpose, stack_kkt_blocks, write_matrix_market)
+
+__version__ = "0.1.0"

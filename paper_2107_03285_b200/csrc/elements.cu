@@ -1,0 +1,477 @@
+// Element kernels for SGN assembly on B200 (sm_100a).
+//
+// The reference's only elastic element is the 2-node spring, vectorized in NumPy
+// (pkg/src/sgnopt/forward.py:29-111: spring_gradient, spring_hessian_triplets,
+// spring_force_rest_jacobian @ spring_length_jacobian).  The BASELINE configs need
+// neo-Hookean linear triangles (plane strain) and tetrahedra, which the reference does
+// not implement; their CPU restatement lives in oracle/elements.py.
+//
+// One thread per element; each thread writes its dense element blocks
+//   hess [nd x nd] = d2E/dx2          (row-major)
+//   mixed[nd x nd] = d2E/dx dX_rest   (row = deformed dof, col = rest dof)
+// which the atomic-free gather (k_gather) sums into the KKT CSC pattern in a fixed order.
+//
+// Energy model (per element e, rest positions X, deformed x):
+//   E_e = A_e(X) * psi(F) + g * A_e(X)/nv * sum_a x_a[1]        (nv = nodes per element)
+//   psi(F) = mu/2 (tr F^T F - d) - mu ln J + lambda/2 (ln J)^2,  F = Ds Dm^{-1}
+// with A_e = det(Dm)/d! (signed measure), g = areal/volumetric load density (downward,
+// gravity along -y).  Gradient dE/dx is the equilibrium force residual c(x, p).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/sgn_b200.h"
+#include "sgn_internal.h"
+
+namespace {
+
+template <int D>
+struct Mat {
+  double a[D][D];
+};
+
+template <int D>
+__device__ __forceinline__ Mat<D> mul(const Mat<D>& x, const Mat<D>& y) {
+  Mat<D> r;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) s += x.a[i][k] * y.a[k][j];
+      r.a[i][j] = s;
+    }
+  return r;
+}
+template <int D>
+__device__ __forceinline__ Mat<D> transpose(const Mat<D>& x) {
+  Mat<D> r;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) r.a[i][j] = x.a[j][i];
+  return r;
+}
+__device__ __forceinline__ double det(const Mat<2>& m) { return m.a[0][0] * m.a[1][1] - m.a[0][1] * m.a[1][0]; }
+__device__ __forceinline__ double det(const Mat<3>& m) {
+  return m.a[0][0] * (m.a[1][1] * m.a[2][2] - m.a[1][2] * m.a[2][1]) -
+         m.a[0][1] * (m.a[1][0] * m.a[2][2] - m.a[1][2] * m.a[2][0]) +
+         m.a[0][2] * (m.a[1][0] * m.a[2][1] - m.a[1][1] * m.a[2][0]);
+}
+__device__ __forceinline__ Mat<2> inverse(const Mat<2>& m) {
+  const double id = 1.0 / det(m);
+  Mat<2> r;
+  r.a[0][0] = m.a[1][1] * id; r.a[0][1] = -m.a[0][1] * id;
+  r.a[1][0] = -m.a[1][0] * id; r.a[1][1] = m.a[0][0] * id;
+  return r;
+}
+__device__ __forceinline__ Mat<3> inverse(const Mat<3>& m) {
+  const double id = 1.0 / det(m);
+  Mat<3> r;
+  r.a[0][0] = (m.a[1][1] * m.a[2][2] - m.a[1][2] * m.a[2][1]) * id;
+  r.a[0][1] = (m.a[0][2] * m.a[2][1] - m.a[0][1] * m.a[2][2]) * id;
+  r.a[0][2] = (m.a[0][1] * m.a[1][2] - m.a[0][2] * m.a[1][1]) * id;
+  r.a[1][0] = (m.a[1][2] * m.a[2][0] - m.a[1][0] * m.a[2][2]) * id;
+  r.a[1][1] = (m.a[0][0] * m.a[2][2] - m.a[0][2] * m.a[2][0]) * id;
+  r.a[1][2] = (m.a[0][2] * m.a[1][0] - m.a[0][0] * m.a[1][2]) * id;
+  r.a[2][0] = (m.a[1][0] * m.a[2][1] - m.a[1][1] * m.a[2][0]) * id;
+  r.a[2][1] = (m.a[0][1] * m.a[2][0] - m.a[0][0] * m.a[2][1]) * id;
+  r.a[2][2] = (m.a[0][0] * m.a[1][1] - m.a[0][1] * m.a[1][0]) * id;
+  return r;
+}
+
+// first Piola stress of compressible neo-Hookean and its directional derivative
+template <int D>
+struct NhState {
+  Mat<D> F, FiT;  // F and F^{-T}
+  double lnJ;
+};
+template <int D>
+__device__ __forceinline__ Mat<D> nh_P(const NhState<D>& s, double mu, double lam) {
+  Mat<D> P;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) P.a[i][j] = mu * (s.F.a[i][j] - s.FiT.a[i][j]) + lam * s.lnJ * s.FiT.a[i][j];
+  return P;
+}
+// dP = mu dF + (mu - lam lnJ) F^{-T} dF^T F^{-T} + lam tr(F^{-1} dF) F^{-T}
+template <int D>
+__device__ __forceinline__ Mat<D> nh_dP(const NhState<D>& s, const Mat<D>& dF, double mu, double lam) {
+  const Mat<D> t1 = mul(mul(s.FiT, transpose(dF)), s.FiT);
+  double tr = 0.0;  // tr(F^{-1} dF) = sum_ij FiT_ij dF_ij
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) tr += s.FiT.a[i][j] * dF.a[i][j];
+  Mat<D> r;
+  const double c = mu - lam * s.lnJ;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) r.a[i][j] = mu * dF.a[i][j] + c * t1.a[i][j] + lam * tr * s.FiT.a[i][j];
+  return r;
+}
+
+// edge-matrix perturbation for dof (vertex a, axis i): d(D) = e_i e_{a-1}^T (a>0) or -e_i 1^T
+template <int D>
+__device__ __forceinline__ Mat<D> edge_dir(int a, int i) {
+  Mat<D> m;
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int c = 0; c < D; ++c) m.a[r][c] = 0.0;
+  if (a == 0) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) m.a[i][c] = -1.0;
+  } else {
+    m.a[i][a - 1] = 1.0;
+  }
+  return m;
+}
+
+// distribute H (d x d, columns = edge vertices 1..d) to the nv*d vertex-dof vector
+template <int D>
+__device__ __forceinline__ void distribute(const Mat<D>& H, double* out, int stride) {
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      out[((c + 1) * D + i) * stride] = H.a[i][c];
+      s += H.a[i][c];
+    }
+    out[(0 * D + i) * stride] = -s;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ double factorial_inv() { return D == 2 ? 0.5 : (1.0 / 6.0); }
+
+// neo-Hookean simplex: derivs
+template <int D>
+__device__ void nh_simplex_derivs(const double* xv, const double* Xv, double mu, double lam,
+                                  double gload, double* hess, double* mixed) {
+  constexpr int NV = D + 1, ND = NV * D;
+  Mat<D> Ds, Dm;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      Ds.a[i][c] = xv[(c + 1) * D + i] - xv[i];
+      Dm.a[i][c] = Xv[(c + 1) * D + i] - Xv[i];
+    }
+  const Mat<D> B = inverse(Dm);
+  const double A = det(Dm) * factorial_inv<D>();
+  NhState<D> s;
+  s.F = mul(Ds, B);
+  const double J = det(s.F);
+  s.lnJ = log(J);
+  s.FiT = transpose(inverse(s.F));
+  const Mat<D> P = nh_P(s, mu, lam);
+  const Mat<D> BT = transpose(B);
+  const Mat<D> PBT = mul(P, BT);
+  // hessian columns: perturb deformed dof (a, i)
+  for (int a = 0; a < NV; ++a)
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const int col = a * D + i;
+      const Mat<D> dF = mul(edge_dir<D>(a, i), B);
+      Mat<D> dH = mul(nh_dP(s, dF, mu, lam), BT);
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) dH.a[r][c] *= A;
+      distribute(dH, hess + col, ND);
+    }
+  // mixed columns: perturb rest dof (a, i)
+  for (int a = 0; a < NV; ++a)
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const int col = a * D + i;
+      const Mat<D> dDm = edge_dir<D>(a, i);
+      const Mat<D> dDmB = mul(dDm, B);
+      double trBdDm = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) trBdDm += mul(B, dDm).a[k][k];
+      const double dA = A * trBdDm;
+      Mat<D> dF = mul(s.F, dDmB);
+      Mat<D> dB = mul(B, dDmB);  // dB = -B dDm B
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) { dF.a[r][c] = -dF.a[r][c]; dB.a[r][c] = -dB.a[r][c]; }
+      const Mat<D> t2 = mul(nh_dP(s, dF, mu, lam), BT);
+      const Mat<D> t3 = mul(P, transpose(dB));
+      Mat<D> dH;
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) dH.a[r][c] = dA * PBT.a[r][c] + A * (t2.a[r][c] + t3.a[r][c]);
+      distribute(dH, mixed + col, ND);
+      // gravity load: d2/dy_a dX = g/NV * dA on every vertex's axis-1 row
+#pragma unroll
+      for (int v = 0; v < NV; ++v) mixed[(v * D + 1) * ND + col] += gload * dA / NV;
+    }
+}
+
+template <int D>
+__device__ void nh_simplex_energy_grad(const double* xv, const double* Xv, double mu, double lam,
+                                       double gload, double* energy, double* grad) {
+  constexpr int NV = D + 1;
+  Mat<D> Ds, Dm;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      Ds.a[i][c] = xv[(c + 1) * D + i] - xv[i];
+      Dm.a[i][c] = Xv[(c + 1) * D + i] - Xv[i];
+    }
+  const Mat<D> B = inverse(Dm);
+  const double A = det(Dm) * factorial_inv<D>();
+  NhState<D> s;
+  s.F = mul(Ds, B);
+  const double J = det(s.F);
+  s.lnJ = log(J);
+  double I1 = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) I1 += s.F.a[i][j] * s.F.a[i][j];
+  const double psi = 0.5 * mu * (I1 - D) - mu * s.lnJ + 0.5 * lam * s.lnJ * s.lnJ;
+  double ysum = 0.0;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) ysum += xv[v * D + 1];
+  *energy = (J > 0.0) ? A * psi + gload * A / NV * ysum : __longlong_as_double(0x7ff8000000000000ll);
+  s.FiT = transpose(inverse(s.F));
+  Mat<D> H = mul(nh_P(s, mu, lam), transpose(B));
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int c = 0; c < D; ++c) H.a[r][c] *= A;
+  distribute(H, grad, 1);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) grad[v * D + 1] += gload * A / NV;
+}
+
+// spring (any dim): E = k/2 (l - L)^2, L = |X_a - X_b|
+template <int D>
+__device__ void spring_derivs(const double* xv, const double* Xv, double k, double* hess, double* mixed) {
+  constexpr int ND = 2 * D;
+  double d[D], Dr[D], l2 = 0.0, L2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    d[i] = xv[i] - xv[D + i];
+    Dr[i] = Xv[i] - Xv[D + i];
+    l2 += d[i] * d[i];
+    L2 += Dr[i] * Dr[i];
+  }
+  const double l = sqrt(l2), L = sqrt(L2);
+  const double coef = (l - L) / l;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double oo = (d[i] / l) * (d[j] / l);
+      const double h = k * (oo + coef * ((i == j ? 1.0 : 0.0) - oo));
+      hess[i * ND + j] = h;
+      hess[(D + i) * ND + D + j] = h;
+      hess[i * ND + D + j] = -h;
+      hess[(D + i) * ND + j] = -h;
+      const double m = -k * (d[i] / l) * (Dr[j] / L);
+      mixed[i * ND + j] = m;
+      mixed[(D + i) * ND + D + j] = m;
+      mixed[i * ND + D + j] = -m;
+      mixed[(D + i) * ND + j] = -m;
+    }
+}
+
+template <int D>
+__device__ void spring_energy_grad(const double* xv, const double* Xv, double k, double* energy, double* grad) {
+  double d[D], l2 = 0.0, L2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    d[i] = xv[i] - xv[D + i];
+    const double r = Xv[i] - Xv[D + i];
+    l2 += d[i] * d[i];
+    L2 += r * r;
+  }
+  const double l = sqrt(l2), L = sqrt(L2);
+  *energy = 0.5 * k * (l - L) * (l - L);
+  const double c = k * (l - L) / l;
+#pragma unroll
+  for (int i = 0; i < D; ++i) { grad[i] = c * d[i]; grad[D + i] = -c * d[i]; }
+}
+
+// params layout per instance: [mu, lambda, gload, spring_dim] ; springs use per-element k
+template <int TYPE, int D>
+__global__ void k_elem_derivs(int64_t ne, const int32_t* __restrict__ conn, const double* __restrict__ pos,
+                              const double* __restrict__ rest, int64_t vstride,
+                              const double* __restrict__ params, int64_t pstride,
+                              double* __restrict__ hess, double* __restrict__ mixed, int64_t bstride) {
+  constexpr int NV = (TYPE == SGN_ELEM_SPRING) ? 2 : D + 1;
+  constexpr int ND = NV * D;
+  const int b = blockIdx.y;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  double xv[ND], Xv[ND];
+  const double* pb = pos + (int64_t)b * vstride;
+  const double* rb = rest + (int64_t)b * vstride;
+#pragma unroll
+  for (int a = 0; a < NV; ++a) {
+    const int64_t v = conn[e * NV + a];
+#pragma unroll
+    for (int i = 0; i < D; ++i) { xv[a * D + i] = pb[v * D + i]; Xv[a * D + i] = rb[v * D + i]; }
+  }
+  double h[ND * ND], m[ND * ND];
+  const double* pr = params + (int64_t)b * pstride;
+  if (TYPE == SGN_ELEM_SPRING) spring_derivs<D>(xv, Xv, pr[4 + e], h, m);
+  else nh_simplex_derivs<D>(xv, Xv, pr[0], pr[1], pr[2], h, m);
+  double* hb = hess + (int64_t)b * bstride + e * ND * ND;
+  double* mb = mixed + (int64_t)b * bstride + e * ND * ND;
+#pragma unroll
+  for (int k = 0; k < ND * ND; ++k) { hb[k] = h[k]; mb[k] = m[k]; }
+}
+
+template <int TYPE, int D>
+__global__ void k_elem_energy_grad(int64_t ne, const int32_t* __restrict__ conn, const double* __restrict__ pos,
+                                   const double* __restrict__ rest, int64_t vstride,
+                                   const double* __restrict__ params, int64_t pstride,
+                                   double* __restrict__ energy, double* __restrict__ grad, int64_t bstride) {
+  constexpr int NV = (TYPE == SGN_ELEM_SPRING) ? 2 : D + 1;
+  constexpr int ND = NV * D;
+  const int b = blockIdx.y;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  double xv[ND], Xv[ND];
+  const double* pb = pos + (int64_t)b * vstride;
+  const double* rb = rest + (int64_t)b * vstride;
+#pragma unroll
+  for (int a = 0; a < NV; ++a) {
+    const int64_t v = conn[e * NV + a];
+#pragma unroll
+    for (int i = 0; i < D; ++i) { xv[a * D + i] = pb[v * D + i]; Xv[a * D + i] = rb[v * D + i]; }
+  }
+  double en, g[ND];
+  const double* pr = params + (int64_t)b * pstride;
+  if (TYPE == SGN_ELEM_SPRING) spring_energy_grad<D>(xv, Xv, pr[4 + e], &en, g);
+  else nh_simplex_energy_grad<D>(xv, Xv, pr[0], pr[1], pr[2], &en, g);
+  if (energy) energy[(int64_t)b * ne + e] = en;
+  if (grad) {
+    double* gb = grad + (int64_t)b * bstride + e * ND;
+#pragma unroll
+    for (int k = 0; k < ND; ++k) gb[k] = g[k];
+  }
+}
+
+__global__ void k_gather(int64_t n_out, const double* __restrict__ base, int64_t base_stride,
+                         const int64_t* __restrict__ ptr, const int64_t* __restrict__ idx,
+                         const double* __restrict__ coef, const double* __restrict__ buf,
+                         int64_t buf_stride, double* __restrict__ out, int64_t out_stride) {
+  const int b = blockIdx.y;
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n_out) return;
+  const double* bb = buf + (int64_t)b * buf_stride;
+  double s = base ? base[(int64_t)b * base_stride + k] : 0.0;
+  const int64_t e = ptr[k + 1];
+  for (int64_t t = ptr[k]; t < e; ++t) s += (coef ? coef[t] : 1.0) * bb[idx[t]];
+  out[(int64_t)b * out_stride + k] = s;
+}
+
+}  // namespace
+
+#define ELEM_CHECK()                                                               \
+  do {                                                                             \
+    cudaError_t _e = cudaGetLastError();                                           \
+    if (_e != cudaSuccess) {                                                       \
+      sgn::last_error() = std::string("element kernel: ") + cudaGetErrorString(_e); \
+      return SGN_CUDA_ERROR;                                                       \
+    }                                                                              \
+  } while (0)
+
+extern "C" {
+
+// spring_dim: for SGN_ELEM_SPRING the spatial dimension is params[3] of instance 0 is not
+// read on the host; springs are dispatched by elem_type + 100*dim (2 or 3).
+int sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch, const int32_t* d_conn,
+                       const double* d_pos, const double* d_rest, int64_t vert_stride,
+                       const double* d_params, int64_t param_stride, double* d_hess,
+                       double* d_mixed, int64_t buf_stride, void* stream) {
+  if (n_elems == 0) return SGN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const dim3 grid((unsigned)((n_elems + 127) / 128), batch);
+  switch (elem_type) {
+    case SGN_ELEM_SPRING:
+    case SGN_ELEM_SPRING + 200:
+      k_elem_derivs<SGN_ELEM_SPRING, 2><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
+                                                              d_params, param_stride, d_hess, d_mixed, buf_stride);
+      break;
+    case SGN_ELEM_SPRING + 300:
+      k_elem_derivs<SGN_ELEM_SPRING, 3><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
+                                                              d_params, param_stride, d_hess, d_mixed, buf_stride);
+      break;
+    case SGN_ELEM_NH_TRI:
+      k_elem_derivs<SGN_ELEM_NH_TRI, 2><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
+                                                              d_params, param_stride, d_hess, d_mixed, buf_stride);
+      break;
+    case SGN_ELEM_NH_TET:
+      k_elem_derivs<SGN_ELEM_NH_TET, 3><<<grid, 64, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
+                                                             d_params, param_stride, d_hess, d_mixed, buf_stride);
+      break;
+    default:
+      sgn::last_error() = "unknown element type";
+      return SGN_INVALID;
+  }
+  ELEM_CHECK();
+  return SGN_OK;
+}
+
+int sgn_element_energy_grad(int32_t elem_type, int64_t n_elems, int32_t batch, const int32_t* d_conn,
+                            const double* d_pos, const double* d_rest, int64_t vert_stride,
+                            const double* d_params, int64_t param_stride, double* d_energy,
+                            double* d_grad, int64_t buf_stride, void* stream) {
+  if (n_elems == 0) return SGN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const dim3 grid((unsigned)((n_elems + 127) / 128), batch);
+  switch (elem_type) {
+    case SGN_ELEM_SPRING:
+    case SGN_ELEM_SPRING + 200:
+      k_elem_energy_grad<SGN_ELEM_SPRING, 2><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
+                                                                   d_params, param_stride, d_energy, d_grad, buf_stride);
+      break;
+    case SGN_ELEM_SPRING + 300:
+      k_elem_energy_grad<SGN_ELEM_SPRING, 3><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
+                                                                   d_params, param_stride, d_energy, d_grad, buf_stride);
+      break;
+    case SGN_ELEM_NH_TRI:
+      k_elem_energy_grad<SGN_ELEM_NH_TRI, 2><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
+                                                                   d_params, param_stride, d_energy, d_grad, buf_stride);
+      break;
+    case SGN_ELEM_NH_TET:
+      k_elem_energy_grad<SGN_ELEM_NH_TET, 3><<<grid, 64, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
+                                                                  d_params, param_stride, d_energy, d_grad, buf_stride);
+      break;
+    default:
+      sgn::last_error() = "unknown element type";
+      return SGN_INVALID;
+  }
+  ELEM_CHECK();
+  return SGN_OK;
+}
+
+int sgn_gather_values(int64_t n_out, int32_t batch, const double* d_base, int64_t base_stride,
+                      const int64_t* d_ptr, const int64_t* d_idx, const double* d_coef,
+                      const double* d_buf, int64_t buf_stride, double* d_out, int64_t out_stride,
+                      void* stream) {
+  if (n_out == 0) return SGN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const dim3 grid((unsigned)((n_out + 255) / 256), batch);
+  k_gather<<<grid, 256, 0, st>>>(n_out, d_base, base_stride, d_ptr, d_idx, d_coef, d_buf, buf_stride,
+                                 d_out, out_stride);
+  ELEM_CHECK();
+  return SGN_OK;
+}
+
+}  // extern "C"

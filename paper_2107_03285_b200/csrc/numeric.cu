@@ -1,0 +1,974 @@
+// Device numeric phase of the SGN KKT solver on B200 (sm_100a) + the C ABI.
+//
+// Replaces, on the GPU, the reference's SuperLU numeric LU (spla.splu, reference
+// pkg/src/sgnopt/linear_solvers.py:87), its triangular solves (linear_solvers.py:93-97),
+// the stabilization (linear_solvers.py:111-127), the relative-residual SpMV
+// (linear_solvers.py:105-108) and the BiCGSTAB refinement (linear_solvers.py:130-211).
+//
+// Factorization: multifrontal LDL^T over the host-built assembly tree (symbolic.cpp).
+// Per tree level: (1) tile-owner assembly of all fronts of the level (original entries +
+// stabilization shift + fixed-order extend-add of children update matrices -- atomic
+// free, bitwise deterministic); (2) per 32-column panel: a panel kernel (redundant
+// in-smem LDL^T of the diagonal block with 2x2 / 1x1 pivots + TRSM of a 32-row tile)
+// and a Schur-update kernel whose 32x32 tiles run on the FP64 tensor pipe
+// (mma.sync.m8n8k4.f64 -> DMMA).  Solves are level-scheduled, one CTA per front,
+// warp-shuffle diagonal blocks.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/sgn_b200.h"
+#include "sgn_internal.h"
+
+using sgn::DFront;
+using sgn::kTile;
+using sgn::Work;
+
+#define CUDA_TRY(expr)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      sgn::last_error() = std::string(#expr) + ": " + cudaGetErrorString(_e);       \
+      return SGN_CUDA_ERROR;                                                        \
+    }                                                                               \
+  } while (0)
+
+namespace {
+
+constexpr int kAsmThreads = 256;
+constexpr int kPanelThreads = 128;
+constexpr int kUpdThreads = 128;
+constexpr int kSolveThreads = 256;
+
+// ------------------------------------------------------------------------------------
+// assembly: one CTA owns one 32x32 lower tile of one front
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kAsmThreads)
+k_assemble(const Work* __restrict__ work, const DFront* __restrict__ fronts,
+           const int32_t* __restrict__ children, const int32_t* __restrict__ rel,
+           const int64_t* __restrict__ tile_ptr, const int64_t* __restrict__ tile_nnz,
+           const int32_t* __restrict__ tile_loc, const int8_t* __restrict__ kind_pos,
+           const double* __restrict__ values, int64_t vstride, double eps_x, double eps_l,
+           double* __restrict__ fstore, int64_t fstride) {
+  __shared__ double tile[kTile][kTile + 1];
+  const Work w = work[blockIdx.x];
+  const int b = blockIdx.y;
+  const DFront F = fronts[w.f];
+  const int ti = w.a, tj = w.b;
+  const int tid = threadIdx.x;
+  double* fb = fstore + (int64_t)b * fstride;
+  const double* vals = values + (int64_t)b * vstride;
+  for (int e = tid; e < kTile * kTile; e += blockDim.x) tile[e >> 5][e & 31] = 0.0;
+  __syncthreads();
+  const int64_t tid_g = F.tile_base + (int64_t)ti * (ti + 1) / 2 + tj;
+  for (int64_t e = tile_ptr[tid_g] + tid; e < tile_ptr[tid_g + 1]; e += blockDim.x) {
+    const int loc = tile_loc[e];
+    tile[loc >> 5][loc & 31] = vals[tile_nnz[e]];
+  }
+  __syncthreads();
+  if (ti == tj && tid < kTile) {
+    const int r = ti * kTile + tid;
+    if (r < F.npiv) {
+      const int8_t k = kind_pos[F.first + r];
+      if (k == 1) tile[tid][tid] += eps_x;
+      else if (k == 2) tile[tid][tid] -= eps_l;
+    }
+  }
+  const int i0 = ti * kTile, i1 = min(i0 + kTile, F.nrow);
+  const int j0 = tj * kTile, j1 = min(j0 + kTile, F.nrow);
+  for (int ci = F.child_begin; ci < F.child_end; ++ci) {
+    const DFront C = fronts[children[ci]];
+    const int cn = C.nrow - C.npiv;
+    if (cn == 0) continue;
+    const int32_t* rc = rel + C.rel_off;
+    const int r_lo = lower_bound_i32(rc, cn, i0), r_hi = lower_bound_i32(rc, cn, i1);
+    const int s_lo = lower_bound_i32(rc, cn, j0), s_hi = lower_bound_i32(rc, cn, j1);
+    const int nr = r_hi - r_lo, ns = s_hi - s_lo;
+    __syncthreads();
+    if (nr > 0 && ns > 0) {
+      const double* U = fb + C.foff;
+      const int64_t ldc = C.nrow;
+      for (int idx = tid; idx < nr * ns; idx += blockDim.x) {
+        const int r = r_lo + idx % nr, s = s_lo + idx / nr;
+        if (r >= s) {
+          const double u = U[(int64_t)(C.npiv + s) * ldc + C.npiv + r];
+          tile[rc[r] - i0][rc[s] - j0] += u;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double* Fm = fb + F.foff;
+  const int64_t ld = F.nrow;
+  for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+    const int ii = e & 31, jj = e >> 5;
+    const int gi = i0 + ii, gj = j0 + jj;
+    if (gi < i1 && gj < j1) Fm[(int64_t)gj * ld + gi] = tile[ii][jj];
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// dense LDL^T of a <=32 x 32 diagonal block in shared memory (lower part used)
+// pivtype 2: 2x2 pivots on (2t, 2t+1); D stored in place, L strictly below the blocks.
+// returns first failing local pivot via *bad (min), else leaves it
+// ------------------------------------------------------------------------------------
+__device__ void smem_ldlt(double (*D)[kTile + 1], int w, int pivtype, int* bad) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (pivtype == 2) {
+    for (int j = 0; j < w; j += 2) {
+      const double a = D[j][j], bb = D[j + 1][j], c = D[j + 1][j + 1];
+      const double det = a * c - bb * bb;
+      if (det == 0.0 || !isfinite(det)) { if (tid == 0) atomicMin(bad, j); }
+      const double ia = c / det, ib = -bb / det, ic = a / det;
+      const int m = w - j - 2;  // trailing size
+      for (int e = tid; e < m * m; e += nt) {
+        const int i = j + 2 + e % m, k = j + 2 + e / m;
+        if (i >= k) {
+          const double x0 = D[i][j], x1 = D[i][j + 1];
+          const double y0 = D[k][j], y1 = D[k][j + 1];
+          D[i][k] -= x0 * (ia * y0 + ib * y1) + x1 * (ib * y0 + ic * y1);
+        }
+      }
+      __syncthreads();
+      for (int i = j + 2 + tid; i < w; i += nt) {
+        const double x0 = D[i][j], x1 = D[i][j + 1];
+        D[i][j] = x0 * ia + x1 * ib;
+        D[i][j + 1] = x0 * ib + x1 * ic;
+      }
+      __syncthreads();
+    }
+  } else {
+    for (int j = 0; j < w; ++j) {
+      const double d = D[j][j];
+      if (d == 0.0 || !isfinite(d)) { if (tid == 0) atomicMin(bad, j); }
+      const double inv = 1.0 / d;
+      const int m = w - j - 1;
+      for (int e = tid; e < m * m; e += nt) {
+        const int i = j + 1 + e % m, k = j + 1 + e / m;
+        if (i >= k) D[i][k] -= D[i][j] * D[k][j] * inv;
+      }
+      __syncthreads();
+      for (int i = j + 1 + tid; i < w; i += nt) D[i][j] *= inv;
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPanelThreads)
+k_panel(const Work* __restrict__ work, const DFront* __restrict__ fronts,
+        const int64_t* __restrict__ perm, double* __restrict__ fstore, int64_t fstride,
+        double* __restrict__ wstore, int64_t wstride, long long* __restrict__ status) {
+  __shared__ double D[kTile][kTile + 1];
+  __shared__ double P[kTile][kTile + 1];
+  __shared__ int bad;
+  const Work wk = work[blockIdx.x];
+  const int b = blockIdx.y;
+  const DFront F = fronts[wk.f];
+  const int j0 = wk.a * kTile;
+  const int w = min(kTile, F.npiv - j0);
+  const int t = wk.b;
+  const int tid = threadIdx.x;
+  double* Fm = fstore + (int64_t)b * fstride + F.foff;
+  const int64_t ld = F.nrow;
+  if (tid == 0) bad = 1 << 30;
+  for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+    const int i = e & 31, j = e >> 5;
+    D[i][j] = (i < w && j < w && i >= j) ? Fm[(int64_t)(j0 + j) * ld + j0 + i] : 0.0;
+  }
+  __syncthreads();
+  smem_ldlt(D, w, F.pivtype, &bad);
+  if (t == 0) {
+    if (tid == 0 && bad < (1 << 30))
+      atomicMin(&status[b], (long long)perm[F.first + j0 + bad]);
+    for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+      const int i = e & 31, j = e >> 5;
+      if (i < w && j < w && i >= j) Fm[(int64_t)(j0 + j) * ld + j0 + i] = D[i][j];
+    }
+    return;
+  }
+  const int r0 = j0 + w + (t - 1) * kTile;
+  const int nr = min(kTile, F.nrow - r0);
+  for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+    const int i = e & 31, j = e >> 5;
+    P[i][j] = (i < nr && j < w) ? Fm[(int64_t)(j0 + j) * ld + r0 + i] : 0.0;
+  }
+  __syncthreads();
+  // W = P L11^{-T}: row-wise forward substitution (thread per row)
+  if (tid < nr) {
+    const int i = tid;
+    for (int c = 0; c < w; ++c) {
+      double acc = P[i][c];
+      for (int cp = 0; cp < c; ++cp) {
+        if (F.pivtype == 2 && (cp & 1) == 0 && cp + 1 == c) continue;  // D off-diagonal slot
+        acc -= P[i][cp] * D[c][cp];
+      }
+      P[i][c] = acc;
+    }
+  }
+  __syncthreads();
+  double* Wb = wstore + (int64_t)b * wstride + F.woff + (int64_t)(t - 1) * kTile * kTile;
+  for (int e = tid; e < nr * kTile; e += blockDim.x) {
+    const int i = e / kTile, c = e % kTile;
+    Wb[(int64_t)i * kTile + c] = (c < w) ? P[i][c] : 0.0;
+  }
+  // L21 = W D^{-1}
+  for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+    const int i = e & 31, c = e >> 5;
+    if (i >= nr || c >= w) continue;
+    double l;
+    if (F.pivtype == 2) {
+      const int c0 = c & ~1;
+      const double a = D[c0][c0], bb = D[c0 + 1][c0], cc = D[c0 + 1][c0 + 1];
+      const double det = a * cc - bb * bb;
+      const double x0 = P[i][c0], x1 = P[i][c0 + 1];
+      l = (c == c0) ? (x0 * cc - x1 * bb) / det : (x1 * a - x0 * bb) / det;
+    } else {
+      l = P[i][c] / D[c][c];
+    }
+    Fm[(int64_t)(j0 + c) * ld + r0 + i] = l;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Schur update of one 32x32 lower tile of the trailing matrix on the FP64 tensor pipe:
+//   C[i, j] -= sum_c L21[i, c] * W[j, c]       (W = L21 D, row-major scratch)
+// mma.sync.aligned.m8n8k4.row.col.f64: A 8x4 (row), B 4x8 (col), C 8x8.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kUpdThreads)
+k_update(const Work* __restrict__ work, const DFront* __restrict__ fronts,
+         double* __restrict__ fstore, int64_t fstride, const double* __restrict__ wstore,
+         int64_t wstride) {
+  __shared__ double As[kTile][kTile + 1];
+  __shared__ double Bs[kTile][kTile + 1];
+  const Work wk = work[blockIdx.x];
+  const int b = blockIdx.y;
+  const DFront F = fronts[wk.f];
+  const int j0 = wk.a * kTile;
+  const int w = min(kTile, F.npiv - j0);
+  const int o = j0 + w;
+  const int ti = wk.b, tj = wk.c;
+  const int rbase = o + ti * kTile, cbase = o + tj * kTile;
+  const int nr = min(kTile, F.nrow - rbase), nc = min(kTile, F.nrow - cbase);
+  const int tid = threadIdx.x;
+  double* Fm = fstore + (int64_t)b * fstride + F.foff;
+  const int64_t ld = F.nrow;
+  const double* Wb = wstore + (int64_t)b * wstride + F.woff;
+  for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+    const int i = e & 31, c = e >> 5;
+    As[i][c] = (i < nr && c < w) ? Fm[(int64_t)(j0 + c) * ld + rbase + i] : 0.0;
+  }
+  for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+    const int c = e & 31, j = e >> 5;
+    Bs[j][c] = (j < nc && c < w) ? Wb[(int64_t)(tj * kTile + j) * kTile + c] : 0.0;
+  }
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int row0 = warp * 8;
+  double acc[4][2];
+#pragma unroll
+  for (int nf = 0; nf < 4; ++nf) acc[nf][0] = acc[nf][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < kTile; kk += 4) {
+    const double a = As[row0 + g][kk + q];
+#pragma unroll
+    for (int nf = 0; nf < 4; ++nf) {
+      const double bv = Bs[nf * 8 + g][kk + q];
+      dmma_8x8x4(acc[nf][0], acc[nf][1], a, bv);
+    }
+  }
+  const int i = row0 + g;
+  if (i < nr) {
+#pragma unroll
+    for (int nf = 0; nf < 4; ++nf) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = nf * 8 + 2 * q + h;
+        if (j < nc && (ti != tj || i >= j)) Fm[(int64_t)(cbase + j) * ld + rbase + i] -= acc[nf][h];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// level-scheduled multifrontal solves (one CTA per front)
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ bool pair_skip(int pivtype, int row, int col) {
+  // in 2x2-pivot fronts L(2t+1, 2t) is structurally zero (slot holds D)
+  return pivtype == 2 && (col & 1) == 0 && row == col + 1;
+}
+
+__global__ void __launch_bounds__(kSolveThreads)
+k_fwd(const int32_t* __restrict__ flist, const DFront* __restrict__ fronts,
+      const int32_t* __restrict__ children, const int32_t* __restrict__ rel,
+      const double* __restrict__ fstore, int64_t fstride, double* __restrict__ y, int64_t n,
+      double* __restrict__ ubuf, int64_t ustride, double* __restrict__ vbuf, int64_t vstride,
+      int leading) {
+  const int b = blockIdx.y;
+  const DFront F = fronts[flist[blockIdx.x]];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* yb = y + (int64_t)b * n;
+  if (leading && F.is_root_p) return;
+  double* v = vbuf + (int64_t)b * vstride + F.voff;
+  const double* Fm = fstore + (int64_t)b * fstride + F.foff;
+  const int64_t ld = F.nrow;
+  for (int i = tid; i < F.nrow; i += blockDim.x) v[i] = (i < F.npiv) ? yb[F.first + i] : 0.0;
+  __syncthreads();
+  for (int ci = F.child_begin; ci < F.child_end; ++ci) {
+    const DFront C = fronts[children[ci]];
+    const int cn = C.nrow - C.npiv;
+    const double* uc = ubuf + (int64_t)b * ustride + C.uoff;
+    const int32_t* rc = rel + C.rel_off;
+    for (int t = tid; t < cn; t += blockDim.x) v[rc[t]] += uc[t];
+    __syncthreads();
+  }
+  for (int jb = 0; jb < F.npiv; jb += 32) {
+    const int wb = min(32, F.npiv - jb);
+    if (warp == 0) {
+      double val = (lane < wb) ? v[jb + lane] : 0.0;
+      for (int c = 0; c < wb; ++c) {
+        const double vc = __shfl_sync(0xffffffffu, val, c);
+        if (lane > c && lane < wb && !pair_skip(F.pivtype, lane, c))
+          val -= Fm[(int64_t)(jb + c) * ld + jb + lane] * vc;
+      }
+      if (lane < wb) v[jb + lane] = val;
+    }
+    __syncthreads();
+    for (int i = jb + wb + tid; i < F.nrow; i += blockDim.x) {
+      double acc = 0.0;
+      for (int c = 0; c < wb; ++c) acc += Fm[(int64_t)(jb + c) * ld + i] * v[jb + c];
+      v[i] -= acc;
+    }
+    __syncthreads();
+  }
+  // D solve, write z to y at pivot positions
+  if (F.pivtype == 2) {
+    for (int j = 2 * tid; j < F.npiv; j += 2 * blockDim.x) {
+      const double a = Fm[(int64_t)j * ld + j], bb = Fm[(int64_t)j * ld + j + 1],
+                   c = Fm[(int64_t)(j + 1) * ld + j + 1];
+      const double det = a * c - bb * bb;
+      const double x0 = v[j], x1 = v[j + 1];
+      yb[F.first + j] = (c * x0 - bb * x1) / det;
+      yb[F.first + j + 1] = (a * x1 - bb * x0) / det;
+    }
+  } else {
+    for (int j = tid; j < F.npiv; j += blockDim.x) yb[F.first + j] = v[j] / Fm[(int64_t)j * ld + j];
+  }
+  double* u = ubuf + (int64_t)b * ustride + F.uoff;
+  for (int i = F.npiv + tid; i < F.nrow; i += blockDim.x) u[i - F.npiv] = v[i];
+}
+
+__global__ void __launch_bounds__(kSolveThreads)
+k_bwd(const int32_t* __restrict__ flist, const DFront* __restrict__ fronts,
+      const int64_t* __restrict__ srows, const double* __restrict__ fstore, int64_t fstride,
+      double* __restrict__ y, int64_t n, double* __restrict__ vbuf, int64_t vstride,
+      int leading) {
+  const int b = blockIdx.y;
+  const DFront F = fronts[flist[blockIdx.x]];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  double* yb = y + (int64_t)b * n;
+  if (leading && F.is_root_p) {
+    for (int i = tid; i < F.npiv; i += blockDim.x) yb[F.first + i] = 0.0;
+    return;
+  }
+  double* v = vbuf + (int64_t)b * vstride + F.voff;
+  const double* Fm = fstore + (int64_t)b * fstride + F.foff;
+  const int64_t ld = F.nrow;
+  for (int i = tid; i < F.nrow; i += blockDim.x)
+    v[i] = (i < F.npiv) ? yb[F.first + i] : yb[srows[F.srow_off + i - F.npiv]];
+  __syncthreads();
+  const int nblk = (F.npiv + 31) / 32;
+  for (int blk = nblk - 1; blk >= 0; --blk) {
+    const int jb = blk * 32, wb = min(32, F.npiv - jb);
+    for (int c = warp; c < wb; c += nwarps) {
+      const double* col = Fm + (int64_t)(jb + c) * ld;
+      double acc = 0.0;
+      for (int i = jb + wb + lane; i < F.nrow; i += 32) acc += col[i] * v[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) v[jb + c] -= acc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double val = (lane < wb) ? v[jb + lane] : 0.0;
+      for (int c = wb - 1; c >= 0; --c) {
+        const double vc = __shfl_sync(0xffffffffu, val, c);
+        if (lane < c && !pair_skip(F.pivtype, c, lane))
+          val -= Fm[(int64_t)(jb + lane) * ld + jb + c] * vc;
+      }
+      if (lane < wb) v[jb + lane] = val;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < F.npiv; i += blockDim.x) yb[F.first + i] = v[i];
+}
+
+__global__ void k_permute_in(const double* __restrict__ x, double* __restrict__ y,
+                             const int64_t* __restrict__ perm, int64_t n) {
+  const int b = blockIdx.y;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    y[(int64_t)b * n + q] = x[(int64_t)b * n + perm[q]];
+}
+__global__ void k_permute_out(const double* __restrict__ y, double* __restrict__ x,
+                              const int64_t* __restrict__ perm, int64_t n) {
+  const int b = blockIdx.y;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    x[(int64_t)b * n + perm[q]] = y[(int64_t)b * n + q];
+}
+
+// ------------------------------------------------------------------------------------
+// SpMV on the symmetric pattern (CSC == CSR), 8 lanes per row
+// ------------------------------------------------------------------------------------
+__global__ void k_spmv(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                       const double* __restrict__ vals, int64_t vstride,
+                       const double* __restrict__ x, double* __restrict__ y, int64_t n,
+                       int64_t p_lo, int64_t p_hi) {
+  const int b = blockIdx.y;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+  const int sub = threadIdx.x & 7;
+  const bool valid = row < n;
+  const double* vb = vals + (int64_t)b * vstride;
+  const double* xb = x + (int64_t)b * n;
+  double acc = 0.0;
+  const int64_t kb = valid ? ptr[row] : 0, ke = valid ? ptr[row + 1] : 0;
+  for (int64_t k = kb + sub; k < ke; k += 8) {
+    const int32_t c = idx[k];
+    if (c >= p_lo && c < p_hi) continue;
+    acc += vb[k] * xb[c];
+  }
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  if (valid && sub == 0) y[(int64_t)b * n + row] = (row >= p_lo && row < p_hi) ? 0.0 : acc;
+}
+
+// ------------------------------------------------------------------------------------
+// deterministic batched BLAS-1 for BiCGSTAB (fixed reduction trees)
+// ------------------------------------------------------------------------------------
+constexpr int kDotBlocks = 64;
+constexpr int kDotThreads = 256;
+
+// up to 2 dot products in one pass: out[b*2+0] = a.b, out[b*2+1] = c.d (if c)
+__global__ void __launch_bounds__(kDotThreads)
+k_dot_partial(const double* __restrict__ a, const double* __restrict__ bvec,
+              const double* __restrict__ c, const double* __restrict__ d, int64_t n,
+              double* __restrict__ partial) {
+  __shared__ double s0[kDotThreads], s1[kDotThreads];
+  const int b = blockIdx.y;
+  const double* ab = a + (int64_t)b * n;
+  const double* bb = bvec + (int64_t)b * n;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    acc0 += ab[i] * bb[i];
+    if (c) acc1 += c[(int64_t)b * n + i] * d[(int64_t)b * n + i];
+  }
+  s0[threadIdx.x] = acc0;
+  s1[threadIdx.x] = acc1;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) { s0[threadIdx.x] += s0[threadIdx.x + s]; s1[threadIdx.x] += s1[threadIdx.x + s]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partial[((int64_t)b * kDotBlocks + blockIdx.x) * 2 + 0] = s0[0];
+    partial[((int64_t)b * kDotBlocks + blockIdx.x) * 2 + 1] = s1[0];
+  }
+}
+
+struct BiState {
+  double rho, alpha, omega, bnorm, best_res, res, dot0, dot1;
+  int32_t active, iters, reason, pad;
+};
+
+// reduce partials and run one scalar step of BiCGSTAB per instance.
+// step: 0 = bnorm, 1 = initial residual (res0), 2 = rho, 3 = alpha, 4 = omega, 5 = residual
+__global__ void k_dot_final(const double* __restrict__ partial, BiState* __restrict__ st,
+                            int step, double tol, int32_t it) {
+  const int b = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  double s0 = 0.0, s1 = 0.0;
+  for (int k = 0; k < kDotBlocks; ++k) {
+    s0 += partial[((int64_t)b * kDotBlocks + k) * 2 + 0];
+    s1 += partial[((int64_t)b * kDotBlocks + k) * 2 + 1];
+  }
+  BiState& S = st[b];
+  S.dot0 = s0;
+  S.dot1 = s1;
+  if (step == 0) {
+    S.bnorm = sqrt(s0);
+    S.iters = 0; S.reason = 0; S.active = 1;
+    S.rho = S.alpha = S.omega = 1.0;
+    if (S.bnorm == 0.0) { S.active = 0; S.res = 0.0; S.best_res = 0.0; S.reason = 4; }
+    return;
+  }
+  if (!S.active) return;
+  if (step == 1) {
+    S.res = sqrt(s0) / S.bnorm;
+    S.best_res = S.res;
+    if (S.res <= tol) { S.active = 0; S.reason = 1; }
+  } else if (step == 2) {
+    const double rho_new = s0;
+    if (rho_new == 0.0 || S.omega == 0.0) { S.active = 0; S.reason = 2; S.iters = it - 1; return; }
+    const double beta = (rho_new / S.rho) * (S.alpha / S.omega);
+    S.rho = rho_new;
+    S.dot1 = beta;
+  } else if (step == 3) {
+    if (s0 == 0.0) { S.active = 0; S.reason = 2; S.iters = it - 1; return; }
+    S.alpha = S.rho / s0;
+  } else if (step == 4) {
+    // s0 = t.t, s1 = t.s
+    S.omega = (s0 > 0.0) ? s1 / s0 : 0.0;
+  } else if (step == 5) {
+    S.res = sqrt(s0) / S.bnorm;
+    S.iters = it;
+    if (S.res < S.best_res) { S.best_res = S.res; S.reason = 10; /* copy best */ }
+    if (S.res <= tol) { S.active = 0; S.reason = 1; }
+  }
+}
+
+// vector kernels (each masked by the instance's active flag)
+// mode 0: out = x + a*y          (a from st field)
+__global__ void k_vec(int mode, const BiState* __restrict__ st, int64_t n,
+                      double* __restrict__ o, const double* __restrict__ x,
+                      const double* __restrict__ y, const double* __restrict__ z,
+                      double* __restrict__ o2, double* __restrict__ o3) {
+  const int b = blockIdx.y;
+  const BiState S = st[b];
+  if (mode != 9 && mode != 7 && !S.active) return;
+  const int64_t base = (int64_t)b * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = base + i;
+    switch (mode) {
+      case 0:  // r = b - Ax ;  o = x - y
+        o[k] = x[k] - y[k];
+        break;
+      case 1:  // p = r + beta (p - omega v)   beta in dot1 (set by step 2)
+        o[k] = x[k] + S.dot1 * (o[k] - S.omega * y[k]);
+        break;
+      case 2:  // s = r - alpha v
+        o[k] = x[k] - S.alpha * y[k];
+        break;
+      case 3:  // x += alpha p + omega s ; r = s - omega t   (o = x, x = p, y = s, z = t, o2 = r)
+        o[k] += S.alpha * x[k] + S.omega * y[k];
+        o2[k] = y[k] - S.omega * z[k];
+        break;
+      case 4:  // copy o = x
+        o[k] = x[k];
+        break;
+      case 7:  // best-copy when step 5 flagged a new best iterate (reason 10)
+        if (S.reason == 10) o[k] = x[k];
+        break;
+      case 9:  // unconditional copy
+        o[k] = x[k];
+        break;
+    }
+  }
+}
+
+__global__ void k_clear_reason(BiState* st) {
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0 && st[b].reason == 10) st[b].reason = 0;
+}
+
+// final select: out = (converged at last iterate) ? x : best
+__global__ void k_select(const BiState* __restrict__ st, int64_t n, const double* __restrict__ x,
+                         const double* __restrict__ best, double* __restrict__ out) {
+  const int b = blockIdx.y;
+  const BiState S = st[b];
+  const int64_t base = (int64_t)b * n;
+  const bool use_x = (S.reason == 1) || (S.reason == 4);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[base + i] = (S.reason == 4) ? 0.0 : (use_x ? x[base + i] : best[base + i]);
+}
+
+// ------------------------------------------------------------------------------------
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() { if (p) cudaFree(p); }
+  int alloc(size_t cnt) {
+    n = cnt;
+    if (cnt == 0) return 0;
+    cudaError_t e = cudaMalloc(&p, cnt * sizeof(T));
+    if (e != cudaSuccess) { sgn::last_error() = std::string("cudaMalloc: ") + cudaGetErrorString(e); return SGN_CUDA_ERROR; }
+    return 0;
+  }
+  int upload(const std::vector<T>& v) {
+    int rc = alloc(v.size());
+    if (rc) return rc;
+    if (!v.empty()) {
+      cudaError_t e = cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) { sgn::last_error() = std::string("cudaMemcpy: ") + cudaGetErrorString(e); return SGN_CUDA_ERROR; }
+    }
+    return 0;
+  }
+};
+
+}  // namespace
+
+struct sgn_symbolic_s {
+  sgn::Symbolic s;
+};
+
+struct sgn_factor_s {
+  sgn_symbolic sym = nullptr;
+  int32_t batch = 1;
+  int64_t n = 0;
+  DevBuf<DFront> fronts;
+  DevBuf<int32_t> children, rel, tile_loc, lvl_fronts, idx32;
+  DevBuf<int64_t> srows, perm, tile_ptr, tile_nnz, indptr;
+  DevBuf<int8_t> kind_pos;
+  DevBuf<Work> work;
+  DevBuf<double> fstore, wstore, ubuf, vbuf, y;
+  DevBuf<long long> status;
+  std::vector<int64_t> lvl_off;  // level -> offset into lvl_fronts
+  // BiCGSTAB workspace
+  DevBuf<double> bx, br, brh, bp, bv, bs, bt, btmp, bbest, bb, bscr, partial;
+  DevBuf<BiState> bst;
+  bool bicg_ready = false;
+};
+
+namespace {
+
+int launch_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st) {
+  const sgn::Symbolic& s = f->sym->s;
+  const int64_t n = s.n;
+  if (n == 0) return SGN_OK;
+  const dim3 pg((unsigned)std::min<int64_t>((n + 255) / 256, 1024), f->batch);
+  k_permute_in<<<pg, 256, 0, st>>>(d_b, f->y.p, f->perm.p, n);
+  const int leading = (flags & SGN_SOLVE_LEADING) ? 1 : 0;
+  for (int32_t lv = 0; lv < s.n_levels; ++lv) {
+    const int64_t cnt = f->lvl_off[lv + 1] - f->lvl_off[lv];
+    if (!cnt) continue;
+    k_fwd<<<dim3((unsigned)cnt, f->batch), kSolveThreads, 0, st>>>(
+        f->lvl_fronts.p + f->lvl_off[lv], f->fronts.p, f->children.p, f->rel.p, f->fstore.p,
+        s.front_doubles, f->y.p, n, f->ubuf.p, s.u_doubles, f->vbuf.p, s.v_doubles, leading);
+  }
+  for (int32_t lv = s.n_levels - 1; lv >= 0; --lv) {
+    const int64_t cnt = f->lvl_off[lv + 1] - f->lvl_off[lv];
+    if (!cnt) continue;
+    k_bwd<<<dim3((unsigned)cnt, f->batch), kSolveThreads, 0, st>>>(
+        f->lvl_fronts.p + f->lvl_off[lv], f->fronts.p, f->srows.p, f->fstore.p, s.front_doubles,
+        f->y.p, n, f->vbuf.p, s.v_doubles, leading);
+  }
+  k_permute_out<<<pg, 256, 0, st>>>(f->y.p, d_x, f->perm.p, n);
+  CUDA_TRY(cudaGetLastError());
+  return SGN_OK;
+}
+
+int launch_spmv(sgn_factor f, const double* vals, int64_t vstride, const double* x, double* y,
+                int32_t flags, cudaStream_t st) {
+  const sgn::Symbolic& s = f->sym->s;
+  const int64_t n = s.n;
+  if (n == 0) return SGN_OK;
+  int64_t p_lo = 0, p_hi = 0;
+  if ((flags & SGN_SOLVE_LEADING) && s.pair_mode) { p_lo = s.n_x; p_hi = s.n_x + s.n_p; }
+  const int64_t threads = n * 8;
+  k_spmv<<<dim3((unsigned)((threads + 255) / 256), f->batch), 256, 0, st>>>(
+      f->indptr.p, f->idx32.p, vals, vstride, x, y, n, p_lo, p_hi);
+  CUDA_TRY(cudaGetLastError());
+  return SGN_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+extern "C" {
+
+const char* sgn_last_error(void) { return sgn::last_error().c_str(); }
+int sgn_version(void) { return 1; }
+
+int sgn_device_sync(void* stream) {
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return SGN_OK;
+}
+
+int sgn_symbolic_create(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t n_x,
+                        int64_t n_p, int64_t n_c, int32_t leaf_size, sgn_symbolic* out,
+                        int64_t* pivot_index) {
+  try {
+    if (!out || !indptr || n < 0) { sgn::last_error() = "bad arguments"; return SGN_INVALID; }
+    auto h = std::make_unique<sgn_symbolic_s>();
+    h->s.n = n; h->s.n_x = n_x; h->s.n_p = n_p; h->s.n_c = n_c;
+    h->s.indptr.assign(indptr, indptr + n + 1);
+    const int64_t nnz = h->s.indptr[n];
+    h->s.indices.assign(indices, indices + nnz);
+    int64_t piv = -1;
+    int rc = sgn::build_symbolic(h->s, leaf_size, &piv);
+    if (pivot_index) *pivot_index = piv;
+    if (rc) return rc;
+    *out = h.release();
+    return SGN_OK;
+  } catch (const std::exception& e) {
+    sgn::last_error() = e.what();
+    return SGN_INVALID;
+  }
+}
+
+int sgn_symbolic_get_stats(sgn_symbolic h, sgn_symbolic_stats* o) {
+  const sgn::Symbolic& s = h->s;
+  o->n = s.n;
+  o->n_fronts = (int64_t)s.fronts.size();
+  o->n_levels = s.n_levels;
+  o->nnz_l = s.nnz_l;
+  o->front_doubles = s.front_doubles;
+  o->max_front = s.max_front;
+  o->max_piv = s.max_piv;
+  o->launches = (int64_t)s.launches.size();
+  o->flops = s.flops;
+  o->pair_mode = s.pair_mode ? 1 : 0;
+  return SGN_OK;
+}
+
+int sgn_symbolic_get_perm(sgn_symbolic h, int64_t* perm) {
+  std::copy(h->s.perm.begin(), h->s.perm.end(), perm);
+  return SGN_OK;
+}
+
+int sgn_symbolic_get_fronts(sgn_symbolic h, int64_t* first, int64_t* npiv, int64_t* nrow,
+                            int64_t* parent, int64_t* rows_ptr, int64_t* rows) {
+  const sgn::Symbolic& s = h->s;
+  int64_t at = 0;
+  for (size_t k = 0; k < s.fronts.size(); ++k) {
+    const sgn::Front& F = s.fronts[k];
+    if (first) first[k] = F.first;
+    if (npiv) npiv[k] = F.npiv;
+    if (nrow) nrow[k] = F.nrow;
+    if (parent) parent[k] = F.parent;
+    if (rows_ptr) rows_ptr[k] = at;
+    for (int32_t i = 0; i < F.nrow; ++i) {
+      if (rows) rows[at] = (i < F.npiv) ? F.first + i : s.srows[F.srow_off + i - F.npiv];
+      ++at;
+    }
+  }
+  if (rows_ptr) rows_ptr[s.fronts.size()] = at;
+  return SGN_OK;
+}
+
+void sgn_symbolic_destroy(sgn_symbolic h) { delete h; }
+
+int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
+  if (!h || batch < 1 || !out) { sgn::last_error() = "bad arguments"; return SGN_INVALID; }
+  auto f = std::make_unique<sgn_factor_s>();
+  f->sym = h;
+  f->batch = batch;
+  const sgn::Symbolic& s = h->s;
+  f->n = s.n;
+  std::vector<DFront> df(s.fronts.size());
+  for (size_t k = 0; k < s.fronts.size(); ++k) {
+    const sgn::Front& F = s.fronts[k];
+    DFront& d = df[k];
+    d.first = F.first; d.foff = F.foff; d.srow_off = F.srow_off; d.rel_off = F.rel_off;
+    d.uoff = F.uoff; d.woff = F.woff; d.voff = F.voff; d.tile_base = F.tile_base;
+    d.npiv = F.npiv; d.nrow = F.nrow; d.parent = F.parent; d.pivtype = F.pivtype;
+    d.child_begin = F.child_begin; d.child_end = F.child_end; d.is_root_p = F.is_root_p;
+    d.level = F.level;
+  }
+  std::vector<int32_t> lf;
+  f->lvl_off.assign(s.n_levels + 1, 0);
+  for (int32_t lv = 0; lv < s.n_levels; ++lv) {
+    f->lvl_off[lv] = (int64_t)lf.size();
+    lf.insert(lf.end(), s.level_fronts[lv].begin(), s.level_fronts[lv].end());
+  }
+  f->lvl_off[s.n_levels] = (int64_t)lf.size();
+  std::vector<int32_t> idx32(s.indices.begin(), s.indices.end());
+  int rc = 0;
+  if ((rc = f->fronts.upload(df)) || (rc = f->children.upload(s.children)) ||
+      (rc = f->rel.upload(s.rel)) || (rc = f->tile_loc.upload(s.tile_loc)) ||
+      (rc = f->lvl_fronts.upload(lf)) || (rc = f->idx32.upload(idx32)) ||
+      (rc = f->srows.upload(s.srows)) || (rc = f->perm.upload(s.perm)) ||
+      (rc = f->tile_ptr.upload(s.tile_ptr)) || (rc = f->tile_nnz.upload(s.tile_nnz)) ||
+      (rc = f->indptr.upload(s.indptr)) || (rc = f->kind_pos.upload(s.kind_pos)) ||
+      (rc = f->work.upload(s.work)))
+    return rc;
+  const size_t B = (size_t)batch;
+  if ((rc = f->fstore.alloc(B * std::max<int64_t>(s.front_doubles, 1))) ||
+      (rc = f->wstore.alloc(B * std::max<int64_t>(s.w_doubles, 1))) ||
+      (rc = f->ubuf.alloc(B * std::max<int64_t>(s.u_doubles, 1))) ||
+      (rc = f->vbuf.alloc(B * std::max<int64_t>(s.v_doubles, 1))) ||
+      (rc = f->y.alloc(B * std::max<int64_t>(s.n, 1))) || (rc = f->status.alloc(B)))
+    return rc;
+  *out = f.release();
+  return SGN_OK;
+}
+
+int sgn_factor_numeric(sgn_factor f, const double* d_values, int64_t values_stride, double eps_x,
+                       double eps_lambda, void* stream) {
+  const sgn::Symbolic& s = f->sym->s;
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    std::vector<long long> init(f->batch, (long long)INT64_MAX);
+    CUDA_TRY(cudaMemcpyAsync(f->status.p, init.data(), init.size() * sizeof(long long),
+                             cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));  // keep `init` alive until the copy is done
+  }
+  for (const sgn::Launch& L : s.launches) {
+    const dim3 grid((unsigned)L.count, f->batch);
+    const Work* w = f->work.p + L.off;
+    switch (L.kind) {
+      case sgn::L_ASM:
+        k_assemble<<<grid, kAsmThreads, 0, st>>>(w, f->fronts.p, f->children.p, f->rel.p,
+                                                 f->tile_ptr.p, f->tile_nnz.p, f->tile_loc.p,
+                                                 f->kind_pos.p, d_values, values_stride, eps_x,
+                                                 eps_lambda, f->fstore.p, s.front_doubles);
+        break;
+      case sgn::L_PANEL:
+        k_panel<<<grid, kPanelThreads, 0, st>>>(w, f->fronts.p, f->perm.p, f->fstore.p,
+                                                s.front_doubles, f->wstore.p, s.w_doubles,
+                                                f->status.p);
+        break;
+      case sgn::L_UPDATE:
+        k_update<<<grid, kUpdThreads, 0, st>>>(w, f->fronts.p, f->fstore.p, s.front_doubles,
+                                               f->wstore.p, s.w_doubles);
+        break;
+    }
+  }
+  CUDA_TRY(cudaGetLastError());
+  return SGN_OK;
+}
+
+int sgn_factor_check(sgn_factor f, void* stream, int64_t* pivot_index) {
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<long long> h(f->batch);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), f->status.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (long long v : h)
+    if (v != (long long)INT64_MAX) {
+      if (pivot_index) *pivot_index = v;
+      sgn::last_error() = "zero pivot at unknown " + std::to_string(v);
+      return SGN_SINGULAR;
+    }
+  if (pivot_index) *pivot_index = -1;
+  return SGN_OK;
+}
+
+int sgn_factor_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, void* stream) {
+  return launch_solve(f, d_b, d_x, flags, (cudaStream_t)stream);
+}
+
+void sgn_factor_destroy(sgn_factor f) { delete f; }
+
+int sgn_spmv(sgn_factor f, const double* d_values, int64_t values_stride, const double* d_x,
+             double* d_y, int32_t flags, void* stream) {
+  return launch_spmv(f, d_values, values_stride, d_x, d_y, flags, (cudaStream_t)stream);
+}
+
+int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_stride,
+                      const double* d_rhs, double* d_sol, double tol, int32_t max_iters,
+                      int32_t flags, double* rel_res, int32_t* iters, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = f->n;
+  const int B = f->batch;
+  const size_t N = (size_t)B * std::max<int64_t>(n, 1);
+  int rc;
+  if (!f->bicg_ready) {
+    if ((rc = f->bx.alloc(N)) || (rc = f->br.alloc(N)) || (rc = f->brh.alloc(N)) ||
+        (rc = f->bp.alloc(N)) || (rc = f->bv.alloc(N)) || (rc = f->bs.alloc(N)) ||
+        (rc = f->bt.alloc(N)) || (rc = f->btmp.alloc(N)) || (rc = f->bbest.alloc(N)) ||
+        (rc = f->bb.alloc(N)) || (rc = f->bscr.alloc(N)) ||
+        (rc = f->partial.alloc((size_t)B * kDotBlocks * 2)) || (rc = f->bst.alloc(B)))
+      return rc;
+    f->bicg_ready = true;
+  }
+  const dim3 vg((unsigned)std::min<int64_t>((n + 255) / 256, 1024), B);
+  const dim3 dg(kDotBlocks, B);
+  BiState* S = f->bst.p;
+  auto dot = [&](const double* a, const double* b2, const double* c, const double* d, int step, int it) {
+    k_dot_partial<<<dg, kDotThreads, 0, st>>>(a, b2, c, d, n, f->partial.p);
+    k_dot_final<<<B, 32, 0, st>>>(f->partial.p, S, step, tol, it);
+  };
+  // vectors: bb = b, bx = x, br = r, brh = r_hat, bp = p, bv = v, bs = s, bt = t,
+  //          btmp = b - A x, bscr = A * (.), bbest = best iterate
+  CUDA_TRY(cudaMemcpyAsync(f->bb.p, d_rhs, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  const sgn::Symbolic& sy = f->sym->s;
+  if ((flags & SGN_SOLVE_LEADING) && sy.pair_mode && sy.n_p > 0) {
+    for (int b = 0; b < B; ++b)
+      CUDA_TRY(cudaMemsetAsync(f->bb.p + (size_t)b * n + sy.n_x, 0, sy.n_p * sizeof(double), st));
+  }
+  dot(f->bb.p, f->bb.p, nullptr, nullptr, 0, 0);                                   // bnorm
+  if ((rc = launch_solve(f, f->bb.p, f->bx.p, flags, st))) return rc;              // x0
+  if ((rc = launch_spmv(f, d_values, values_stride, f->bx.p, f->bscr.p, flags, st))) return rc;
+  k_vec<<<vg, 256, 0, st>>>(0, S, n, f->btmp.p, f->bb.p, f->bscr.p, nullptr, nullptr, nullptr);
+  dot(f->btmp.p, f->btmp.p, nullptr, nullptr, 1, 0);                               // res0
+  k_vec<<<vg, 256, 0, st>>>(9, S, n, f->bbest.p, f->bx.p, nullptr, nullptr, nullptr, nullptr);
+  std::vector<BiState> hs(B);
+  auto read_state = [&]() -> int {
+    CUDA_TRY(cudaMemcpyAsync(hs.data(), S, B * sizeof(BiState), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return 0;
+  };
+  if ((rc = read_state())) return rc;
+  bool any = false;
+  for (auto& h : hs) any |= (h.active != 0);
+  if (any && max_iters > 0) {
+    if ((rc = launch_solve(f, f->btmp.p, f->br.p, flags, st))) return rc;          // r = M^-1(b-Ax0)
+    k_vec<<<vg, 256, 0, st>>>(4, S, n, f->brh.p, f->br.p, nullptr, nullptr, nullptr, nullptr);
+    CUDA_TRY(cudaMemsetAsync(f->bp.p, 0, N * sizeof(double), st));
+    CUDA_TRY(cudaMemsetAsync(f->bv.p, 0, N * sizeof(double), st));
+    for (int it = 1; it <= max_iters; ++it) {
+      dot(f->brh.p, f->br.p, nullptr, nullptr, 2, it);                             // rho, beta
+      k_vec<<<vg, 256, 0, st>>>(1, S, n, f->bp.p, f->br.p, f->bv.p, nullptr, nullptr, nullptr);
+      if ((rc = launch_spmv(f, d_values, values_stride, f->bp.p, f->bscr.p, flags, st))) return rc;
+      if ((rc = launch_solve(f, f->bscr.p, f->bv.p, flags, st))) return rc;        // v = M^-1 A p
+      dot(f->brh.p, f->bv.p, nullptr, nullptr, 3, it);                             // alpha
+      k_vec<<<vg, 256, 0, st>>>(2, S, n, f->bs.p, f->br.p, f->bv.p, nullptr, nullptr, nullptr);
+      if ((rc = launch_spmv(f, d_values, values_stride, f->bs.p, f->bscr.p, flags, st))) return rc;
+      if ((rc = launch_solve(f, f->bscr.p, f->bt.p, flags, st))) return rc;        // t = M^-1 A s
+      dot(f->bt.p, f->bt.p, f->bt.p, f->bs.p, 4, it);                              // omega
+      k_vec<<<vg, 256, 0, st>>>(3, S, n, f->bx.p, f->bp.p, f->bs.p, f->bt.p, f->br.p, nullptr);
+      if ((rc = launch_spmv(f, d_values, values_stride, f->bx.p, f->bscr.p, flags, st))) return rc;
+      k_vec<<<vg, 256, 0, st>>>(0, S, n, f->btmp.p, f->bb.p, f->bscr.p, nullptr, nullptr, nullptr);
+      dot(f->btmp.p, f->btmp.p, nullptr, nullptr, 5, it);                          // true residual
+      k_vec<<<vg, 256, 0, st>>>(7, S, n, f->bbest.p, f->bx.p, nullptr, nullptr, nullptr, nullptr);
+      k_clear_reason<<<B, 32, 0, st>>>(S);
+      if ((rc = read_state())) return rc;
+      bool act = false;
+      for (auto& h : hs) act |= (h.active != 0);
+      if (!act) break;
+    }
+  }
+  k_select<<<vg, 256, 0, st>>>(S, n, f->bx.p, f->bbest.p, d_sol);
+  CUDA_TRY(cudaGetLastError());
+  if ((rc = read_state())) return rc;
+  bool fail = false;
+  for (int b = 0; b < B; ++b) {
+    const BiState& h = hs[b];
+    const double res = (h.reason == 1 || h.reason == 4) ? h.res : h.best_res;
+    const int32_t its = h.active ? max_iters : h.iters;
+    if (rel_res) rel_res[b] = res;
+    if (iters) iters[b] = its;
+    if (!(res <= tol)) fail = true;
+  }
+  if (fail) {
+    sgn::last_error() = "BiCGSTAB refinement stalled above tolerance";
+    return SGN_NO_CONVERGENCE;
+  }
+  return SGN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+// Internal data structures shared by the host symbolic analysis (symbolic.cpp) and the
+// device numeric phase (numeric.cu).  Not part of the C ABI.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace sgn {
+
+constexpr int kTile = 32;   // assembly tile, panel width, update tile
+
+// One dense front (supernode) of the multifrontal assembly tree.
+struct Front {
+  int64_t first = 0;      // first elimination position of its pivots
+  int32_t npiv = 0;       // fully-summed (pivot) unknowns
+  int32_t nrow = 0;       // npiv + |struct|
+  int32_t parent = -1;
+  int32_t level = 0;      // height: leaves 0, parent = 1 + max(children)
+  int32_t pivtype = 1;    // 1: 1x1 pivots, 2: 2x2 (x_i, lambda_j) pair pivots
+  int32_t is_root_p = 0;  // the dense p front (skipped by SGN_SOLVE_LEADING)
+  int32_t child_begin = 0, child_end = 0;  // range in Symbolic::children
+  int64_t foff = 0;       // offset of the nrow x nrow column-major front (doubles)
+  int64_t srow_off = 0;   // offset of struct rows (positions) in Symbolic::srows
+  int64_t rel_off = 0;    // offset of rel map (struct -> parent local rows)
+  int64_t uoff = 0;       // offset of the forward-solve update vector (nstruct)
+  int64_t woff = 0;       // offset of the panel W scratch (nrow x 32)
+  int64_t voff = 0;       // offset of the solve front vector (nrow)
+  int64_t tile_base = 0;  // first assembly tile id
+};
+
+// Device-side mirror of Front (POD, 16-byte aligned for vector loads).
+struct DFront {
+  int64_t first;
+  int64_t foff;
+  int64_t srow_off;
+  int64_t rel_off;
+  int64_t uoff;
+  int64_t woff;
+  int64_t voff;
+  int64_t tile_base;
+  int32_t npiv, nrow, parent, pivtype;
+  int32_t child_begin, child_end, is_root_p, level;
+};
+
+struct Work { int32_t f, a, b, c; };   // generic work item
+
+enum LaunchKind : int32_t { L_ASM = 0, L_PANEL = 1, L_UPDATE = 2 };
+struct Launch { int32_t kind; int32_t level; int64_t off; int64_t count; };
+
+struct Symbolic {
+  int64_t n = 0, n_x = 0, n_p = 0, n_c = 0;
+  bool pair_mode = false;
+  std::vector<int64_t> indptr, indices;       // input full CSC pattern
+  std::vector<int64_t> perm, ipos;             // perm[pos] = unknown; ipos[unknown] = pos
+  std::vector<Front> fronts;                   // postorder (children before parents)
+  std::vector<int32_t> children;
+  std::vector<int64_t> srows;                  // struct rows (positions), sorted per front
+  std::vector<int32_t> rel;                    // per front: struct row -> parent local row
+  std::vector<int8_t> kind_pos;                // 0 none, 1 +eps_x, 2 -eps_lambda
+  std::vector<int32_t> front_of_pos;
+  // assembly entry lists per tile
+  std::vector<int64_t> tile_ptr;               // ntiles+1
+  std::vector<int64_t> tile_nnz;               // K nnz index
+  std::vector<int32_t> tile_loc;               // (lr%32)*32 + (lc%32)
+  int64_t ntiles = 0;
+  // schedule
+  int32_t n_levels = 0;
+  std::vector<std::vector<int32_t>> level_fronts;
+  std::vector<Work> work;                      // all work items
+  std::vector<Launch> launches;                // factorization launch schedule
+  // sizes
+  int64_t front_doubles = 0, u_doubles = 0, w_doubles = 0, v_doubles = 0;
+  int64_t nnz_l = 0; double flops = 0; int64_t max_front = 0, max_piv = 0;
+};
+
+std::string& last_error();
+
+// returns 0 ok, 1 singular (pivot_index set), 5 invalid
+int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index);
+
+}  // namespace sgn

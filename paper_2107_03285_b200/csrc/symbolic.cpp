@@ -1,0 +1,746 @@
+// Host symbolic analysis for the multifrontal LDL^T of SGN KKT matrices.
+//
+// Replaces the ordering half of the reference factorization: SuperLU's COLAMD column
+// ordering inside spla.splu (pkg/src/sgnopt/linear_solvers.py:87) together with the
+// structural-singularity checks of SparseFactorization.__init__ (linear_solvers.py:73-85).
+// Runs once per sparsity pattern; deterministic (no hashing of pointers, no threads).
+//
+// KKT mode (n_x > 0): unknown u_x[i] is paired with the multiplier u_l[pi(i)] matched on
+// the pattern of dc/dx (diagonal preferred), giving a 2x2 pivot block
+// [[a+eps, g], [g, -eps]] whose determinant is bounded away from zero for the
+// quasi-definite stabilized matrix.  Pair nodes are ordered by nested dissection of the
+// (compressed) node graph; every parameter unknown is eliminated last in a single dense
+// root front, whose Schur complement is the (SPD) reduced Gauss-Newton Hessian.
+// Generic mode (n_x == 0): 1x1 pivots on every unknown, same nested dissection.
+#include "sgn_internal.h"
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+
+namespace sgn {
+
+std::string& last_error() {
+  static thread_local std::string e;
+  return e;
+}
+
+namespace {
+
+struct Csr {
+  int32_t n = 0;
+  std::vector<int64_t> ptr;
+  std::vector<int32_t> adj;
+};
+
+// --------------------------------------------------------------------------------
+// bipartite matching x_i -> lambda_j on the dc/dx pattern (K rows >= n_x+n_p of column i)
+// --------------------------------------------------------------------------------
+bool match_pairs(const Symbolic& s, std::vector<int64_t>& pi, int64_t* bad) {
+  const int64_t nx = s.n_x, off = s.n_x + s.n_p;
+  pi.assign(nx, -1);
+  std::vector<int64_t> owner(nx, -1);   // lambda j -> x i
+  for (int64_t i = 0; i < nx; ++i) {    // diagonal first
+    for (int64_t k = s.indptr[i]; k < s.indptr[i + 1]; ++k) {
+      if (s.indices[k] == off + i) { pi[i] = i; owner[i] = i; break; }
+    }
+  }
+  struct Frame { int64_t i, k; };
+  std::vector<int64_t> visit(nx, -1), via;
+  std::vector<Frame> st;
+  for (int64_t root = 0; root < nx; ++root) {
+    if (pi[root] >= 0) continue;
+    st.clear();
+    st.push_back({root, s.indptr[root]});
+    visit[root] = root;
+    bool found = false;
+    while (!st.empty() && !found) {
+      const size_t depth = st.size() - 1;
+      Frame& fr = st.back();
+      bool advanced = false;
+      for (; fr.k < s.indptr[fr.i + 1]; ++fr.k) {
+        const int64_t r = s.indices[fr.k];
+        if (r < off) continue;
+        const int64_t j = r - off;
+        if (via.size() <= depth) via.resize(depth + 1);
+        if (owner[j] < 0) {
+          via[depth] = j;
+          for (size_t d = 0; d <= depth; ++d) { pi[st[d].i] = via[d]; owner[via[d]] = st[d].i; }
+          found = true;
+          break;
+        }
+        const int64_t i2 = owner[j];
+        if (visit[i2] == root) continue;
+        visit[i2] = root;
+        via[depth] = j;
+        ++fr.k;
+        st.push_back({i2, s.indptr[i2]});
+        advanced = true;
+        break;
+      }
+      if (!found && !advanced) st.pop_back();
+    }
+    if (!found) { *bad = root; return false; }
+  }
+  return true;
+}
+
+// --------------------------------------------------------------------------------
+// nested dissection on a weighted graph (BFS level structures, George-Liu style)
+// --------------------------------------------------------------------------------
+struct NdFront { std::vector<int32_t> verts; int32_t parent; };
+
+class Dissector {
+ public:
+  Dissector(const Csr& g, const std::vector<int32_t>& w, int64_t leaf)
+      : g_(g), w_(w), leaf_(leaf), mark_(g.n, -1), lev_(g.n, -1) {}
+
+  std::vector<NdFront> run() {
+    std::vector<int32_t> ord(g_.n);
+    std::iota(ord.begin(), ord.end(), 0);
+    ord_.swap(ord);
+    tasks_.push_back({0, (int64_t)ord_.size(), -1});
+    while (!tasks_.empty()) {
+      Task t = tasks_.back();
+      tasks_.pop_back();
+      process(t);
+    }
+    return std::move(fronts_);
+  }
+
+ private:
+  struct Task { int64_t b, e; int32_t parent; };
+  const Csr& g_;
+  const std::vector<int32_t>& w_;
+  int64_t leaf_;
+  std::vector<int32_t> mark_, lev_, ord_;
+  int32_t stamp_ = 0;
+  std::vector<Task> tasks_;
+  std::vector<NdFront> fronts_;
+
+  int32_t make_front(int64_t b, int64_t e, int32_t parent) {
+    NdFront f;
+    f.verts.assign(ord_.begin() + b, ord_.begin() + e);
+    f.parent = parent;
+    fronts_.push_back(std::move(f));
+    return (int32_t)fronts_.size() - 1;
+  }
+
+  // BFS from r restricted to mark_ == stamp_; fills lev_; returns max level; order in q
+  int32_t bfs(int32_t r, std::vector<int32_t>& q) {
+    q.clear();
+    q.push_back(r);
+    lev_[r] = 0;
+    int32_t stampv = stamp_ + 1;  // visited marker: use lev sentinel via vis_
+    vis_stamp_++;
+    if (vis_.size() < (size_t)g_.n) vis_.assign(g_.n, 0);
+    vis_[r] = vis_stamp_;
+    (void)stampv;
+    size_t h = 0;
+    int32_t maxl = 0;
+    while (h < q.size()) {
+      int32_t v = q[h++];
+      for (int64_t k = g_.ptr[v]; k < g_.ptr[v + 1]; ++k) {
+        int32_t u = g_.adj[k];
+        if (mark_[u] != stamp_ || vis_[u] == vis_stamp_) continue;
+        vis_[u] = vis_stamp_;
+        lev_[u] = lev_[v] + 1;
+        maxl = std::max(maxl, lev_[u]);
+        q.push_back(u);
+      }
+    }
+    return maxl;
+  }
+  std::vector<int32_t> vis_;
+  int32_t vis_stamp_ = 0;
+
+  int64_t deg_in(int32_t v) const {
+    int64_t d = 0;
+    for (int64_t k = g_.ptr[v]; k < g_.ptr[v + 1]; ++k) d += (mark_[g_.adj[k]] == stamp_);
+    return d;
+  }
+
+  void process(const Task& t) {
+    int64_t W = 0;
+    ++stamp_;
+    for (int64_t i = t.b; i < t.e; ++i) { mark_[ord_[i]] = stamp_; W += w_[ord_[i]]; }
+    if (t.e - t.b <= 1) { make_front(t.b, t.e, t.parent); return; }
+
+    // connected components of the range
+    std::vector<int32_t> q;
+    std::vector<std::vector<int32_t>> comps;
+    {
+      int64_t seen = 0;
+      vis_stamp_++;
+      if (vis_.size() < (size_t)g_.n) vis_.assign(g_.n, 0);
+      int32_t my = vis_stamp_;
+      for (int64_t i = t.b; i < t.e && seen < t.e - t.b; ++i) {
+        int32_t r = ord_[i];
+        if (vis_[r] == my) continue;
+        std::vector<int32_t> c;
+        c.push_back(r);
+        vis_[r] = my;
+        size_t h = 0;
+        while (h < c.size()) {
+          int32_t v = c[h++];
+          for (int64_t k = g_.ptr[v]; k < g_.ptr[v + 1]; ++k) {
+            int32_t u = g_.adj[k];
+            if (mark_[u] != stamp_ || vis_[u] == my) continue;
+            vis_[u] = my;
+            c.push_back(u);
+          }
+        }
+        seen += (int64_t)c.size();
+        comps.push_back(std::move(c));
+      }
+    }
+    if (comps.size() > 1) {
+      // independent components: each becomes its own subtree under the same parent
+      int64_t pos = t.b;
+      for (auto& c : comps) {
+        const int64_t b = pos;
+        int64_t cw = 0;
+        for (int32_t v : c) { ord_[pos++] = v; cw += w_[v]; }
+        if (cw <= leaf_) make_front(b, pos, t.parent);
+        else tasks_.push_back({b, pos, t.parent});
+      }
+      return;
+    }
+
+    if (W <= leaf_) { make_front(t.b, t.e, t.parent); return; }
+    // single component: pseudo-peripheral root
+    int32_t r = ord_[t.b];
+    {
+      int64_t best = INT64_MAX;
+      for (int64_t i = t.b; i < t.e; ++i) {
+        int64_t d = deg_in(ord_[i]);
+        if (d < best) { best = d; r = ord_[i]; }
+      }
+    }
+    int32_t ecc = bfs(r, q);
+    for (int it = 0; it < 6; ++it) {
+      int32_t cand = -1;
+      int64_t bd = INT64_MAX;
+      for (int32_t v : q)
+        if (lev_[v] == ecc) {
+          int64_t d = deg_in(v);
+          if (d < bd) { bd = d; cand = v; }
+        }
+      std::vector<int32_t> q2;
+      int32_t e2 = bfs(cand, q2);
+      if (e2 > ecc) { ecc = e2; r = cand; q.swap(q2); }
+      else { bfs(r, q); break; }
+    }
+    const int32_t h = ecc;
+    if (h < 2) { make_front(t.b, t.e, t.parent); return; }
+    std::vector<int64_t> lw(h + 1, 0);
+    for (int32_t v : q) lw[lev_[v]] += w_[v];
+    // median level
+    int64_t cum = 0;
+    int32_t s0 = 1;
+    for (int32_t l = 0; l <= h; ++l) {
+      if (cum + lw[l] >= (W + 1) / 2) { s0 = l; break; }
+      cum += lw[l];
+    }
+    s0 = std::max(1, std::min(h - 1, s0));
+    // search nearby levels for a small, balanced separator
+    int32_t best_s = s0;
+    double best_cost = 1e300;
+    {
+      std::vector<int64_t> pre(h + 2, 0);
+      for (int32_t l = 0; l <= h; ++l) pre[l + 1] = pre[l] + lw[l];
+      int32_t span = std::max(2, h / 8);
+      for (int32_t s = std::max(1, s0 - span); s <= std::min(h - 1, s0 + span); ++s) {
+        double wa = (double)pre[s], wb = (double)(W - pre[s + 1]);
+        double mn = std::min(wa, wb);
+        if (mn < 0.2 * W && s != s0) continue;
+        double cost = (double)lw[s] * (1.0 + 2.0 * std::fabs(wa - wb) / (double)W);
+        if (cost < best_cost) { best_cost = cost; best_s = s; }
+      }
+    }
+    const int32_t s = best_s;
+    // refine: separator vertices must touch level s+1
+    std::vector<int32_t> A, B, S;
+    for (int32_t v : q) {
+      int32_t l = lev_[v];
+      if (l < s) A.push_back(v);
+      else if (l > s) B.push_back(v);
+      else {
+        bool touches = false;
+        for (int64_t k = g_.ptr[v]; k < g_.ptr[v + 1] && !touches; ++k) {
+          int32_t u = g_.adj[k];
+          touches = (mark_[u] == stamp_ && lev_[u] == s + 1);
+        }
+        (touches ? S : A).push_back(v);
+      }
+    }
+    int64_t pos = t.b;
+    int64_t a_b = pos; for (int32_t v : A) ord_[pos++] = v; int64_t a_e = pos;
+    int64_t b_b = pos; for (int32_t v : B) ord_[pos++] = v; int64_t b_e = pos;
+    int64_t s_b = pos; for (int32_t v : S) ord_[pos++] = v; int64_t s_e = pos;
+    int32_t f = make_front(s_b, s_e, t.parent);
+    if (b_e > b_b) tasks_.push_back({b_b, b_e, f});
+    if (a_e > a_b) tasks_.push_back({a_b, a_e, f});
+  }
+};
+
+}  // namespace
+
+int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
+  const int64_t n = s.n;
+  *pivot_index = -1;
+  if ((int64_t)s.indptr.size() != n + 1) { last_error() = "indptr size != n+1"; return 5; }
+  const int64_t nnz = s.indptr[n];
+  if ((int64_t)s.indices.size() != nnz) { last_error() = "indices size != nnz"; return 5; }
+  for (int64_t j = 0; j < n; ++j) {
+    if (s.indptr[j + 1] < s.indptr[j]) { last_error() = "indptr not monotone"; return 5; }
+    for (int64_t k = s.indptr[j]; k < s.indptr[j + 1]; ++k) {
+      int64_t r = s.indices[k];
+      if (r < 0 || r >= n) { last_error() = "row index out of range"; return 5; }
+      if (k > s.indptr[j] && s.indices[k - 1] >= r) { last_error() = "rows not sorted/unique"; return 5; }
+    }
+  }
+  // structural symmetry check (the pattern of a symmetric KKT is symmetric)
+  {
+    std::vector<int64_t> cnt(n, 0);
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t k = s.indptr[j]; k < s.indptr[j + 1]; ++k) cnt[s.indices[k]]++;
+    for (int64_t j = 0; j < n; ++j)
+      if (cnt[j] != s.indptr[j + 1] - s.indptr[j]) { last_error() = "pattern is not structurally symmetric"; return 5; }
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t k = s.indptr[j]; k < s.indptr[j + 1]; ++k) {
+        int64_t r = s.indices[k];
+        if (!std::binary_search(s.indices.begin() + s.indptr[r], s.indices.begin() + s.indptr[r + 1], j)) {
+          last_error() = "pattern is not structurally symmetric";
+          return 5;
+        }
+      }
+  }
+  if (leaf_size <= 0) leaf_size = 64;
+  s.pair_mode = (s.n_x > 0);
+  if (s.pair_mode && (s.n_c != s.n_x || 2 * s.n_x + s.n_p != n)) {
+    last_error() = "KKT mode needs n_c == n_x and n == 2*n_x + n_p";
+    return 3;
+  }
+
+  // ---- nodes ----------------------------------------------------------------
+  // node_unk: unknowns of each graph node; p unknowns are not graph nodes in KKT mode
+  std::vector<int64_t> node_of(n, -1);
+  std::vector<std::array<int64_t, 2>> node_unk;
+  std::vector<int32_t> node_w;
+  if (s.pair_mode) {
+    std::vector<int64_t> pi;
+    int64_t bad = -1;
+    if (!match_pairs(s, pi, &bad)) {
+      *pivot_index = bad;
+      last_error() = "structurally singular: no matching multiplier for state " + std::to_string(bad);
+      return 1;
+    }
+    node_unk.resize(s.n_x);
+    for (int64_t i = 0; i < s.n_x; ++i) {
+      int64_t l = s.n_x + s.n_p + pi[i];
+      node_unk[i] = {i, l};
+      node_of[i] = i;
+      node_of[l] = i;
+    }
+    node_w.assign(s.n_x, 2);
+  } else {
+    node_unk.resize(n);
+    for (int64_t i = 0; i < n; ++i) { node_unk[i] = {i, -1}; node_of[i] = i; }
+    node_w.assign(n, 1);
+  }
+  const int64_t N = (int64_t)node_unk.size();
+
+  // ---- node graph -----------------------------------------------------------
+  Csr g;
+  g.n = (int32_t)N;
+  g.ptr.assign(N + 1, 0);
+  {
+    std::vector<int64_t> stampv(N, -1);
+    std::vector<int32_t> tmp;
+    std::vector<int32_t> adj;
+    for (int64_t a = 0; a < N; ++a) {
+      tmp.clear();
+      stampv[a] = a;
+      for (int t = 0; t < 2; ++t) {
+        int64_t u = node_unk[a][t];
+        if (u < 0) continue;
+        for (int64_t k = s.indptr[u]; k < s.indptr[u + 1]; ++k) {
+          int64_t b = node_of[s.indices[k]];
+          if (b < 0 || stampv[b] == a) continue;
+          stampv[b] = a;
+          tmp.push_back((int32_t)b);
+        }
+      }
+      std::sort(tmp.begin(), tmp.end());
+      adj.insert(adj.end(), tmp.begin(), tmp.end());
+      g.ptr[a + 1] = (int64_t)adj.size();
+    }
+    g.adj.swap(adj);
+  }
+
+  // ---- compression of indistinguishable nodes (equal closed neighbourhoods) -----
+  std::vector<int32_t> sv_of(N, -1);
+  std::vector<std::vector<int32_t>> sv_members;
+  {
+    std::vector<uint64_t> key(N);
+    auto mix = [](uint64_t x) { x += 1; x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; return x; };
+    for (int64_t a = 0; a < N; ++a) {
+      uint64_t h = mix((uint64_t)a);     // closed neighbourhood = adj(a) + {a}
+      for (int64_t k = g.ptr[a]; k < g.ptr[a + 1]; ++k) h += mix((uint64_t)g.adj[k]);
+      key[a] = h;
+    }
+    std::vector<int32_t> idx(N);
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) {
+      if (key[x] != key[y]) return key[x] < key[y];
+      return x < y;
+    });
+    auto closed_equal = [&](int32_t a, int32_t b) {
+      // closed nbhd(a) == closed nbhd(b)  <=>  adj(a)+{a} == adj(b)+{b}
+      if (g.ptr[a + 1] - g.ptr[a] != g.ptr[b + 1] - g.ptr[b]) return false;
+      if (node_w[a] != node_w[b]) return false;
+      std::vector<int32_t> ca(g.adj.begin() + g.ptr[a], g.adj.begin() + g.ptr[a + 1]);
+      std::vector<int32_t> cb(g.adj.begin() + g.ptr[b], g.adj.begin() + g.ptr[b + 1]);
+      ca.push_back(a); cb.push_back(b);
+      std::sort(ca.begin(), ca.end()); std::sort(cb.begin(), cb.end());
+      return ca == cb;
+    };
+    for (int64_t i = 0; i < N;) {
+      int64_t j = i;
+      while (j < N && key[idx[j]] == key[idx[i]]) ++j;
+      // group [i, j) by exact equality
+      for (int64_t a = i; a < j; ++a) {
+        int32_t va = idx[a];
+        if (sv_of[va] >= 0) continue;
+        int32_t id = (int32_t)sv_members.size();
+        sv_members.push_back({va});
+        sv_of[va] = id;
+        for (int64_t b = a + 1; b < j; ++b) {
+          int32_t vb = idx[b];
+          if (sv_of[vb] < 0 && closed_equal(va, vb)) { sv_of[vb] = id; sv_members[id].push_back(vb); }
+        }
+      }
+      i = j;
+    }
+    // canonical supervertex numbering: by smallest member
+    std::vector<int32_t> order(sv_members.size());
+    std::iota(order.begin(), order.end(), 0);
+    for (auto& m : sv_members) std::sort(m.begin(), m.end());
+    std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return sv_members[x][0] < sv_members[y][0]; });
+    std::vector<std::vector<int32_t>> sorted(sv_members.size());
+    for (size_t k = 0; k < order.size(); ++k) {
+      sorted[k] = std::move(sv_members[order[k]]);
+      for (int32_t v : sorted[k]) sv_of[v] = (int32_t)k;
+    }
+    sv_members.swap(sorted);
+  }
+  const int64_t NS = (int64_t)sv_members.size();
+  Csr cg;
+  std::vector<int32_t> cw(NS, 0);
+  cg.n = (int32_t)NS;
+  cg.ptr.assign(NS + 1, 0);
+  {
+    std::vector<int64_t> st(NS, -1);
+    std::vector<int32_t> tmp, adj;
+    for (int64_t a = 0; a < NS; ++a) {
+      tmp.clear();
+      st[a] = a;
+      for (int32_t v : sv_members[a]) {
+        cw[a] += node_w[v];
+        for (int64_t k = g.ptr[v]; k < g.ptr[v + 1]; ++k) {
+          int32_t b = sv_of[g.adj[k]];
+          if (st[b] == a) continue;
+          st[b] = a;
+          tmp.push_back(b);
+        }
+      }
+      std::sort(tmp.begin(), tmp.end());
+      adj.insert(adj.end(), tmp.begin(), tmp.end());
+      cg.ptr[a + 1] = (int64_t)adj.size();
+    }
+    cg.adj.swap(adj);
+  }
+
+  // ---- nested dissection -> front tree (top-down creation order) --------------
+  std::vector<NdFront> nd;
+  if (NS > 0) {
+    Dissector d(cg, cw, leaf_size);
+    nd = d.run();
+  }
+  int32_t proot = -1;
+  if (s.pair_mode && s.n_p > 0) {
+    NdFront pf;
+    pf.parent = -1;
+    nd.push_back(pf);
+    proot = (int32_t)nd.size() - 1;
+    for (int32_t f = 0; f < proot; ++f)
+      if (nd[f].parent < 0) nd[f].parent = proot;
+  }
+  const int32_t NF = (int32_t)nd.size();
+
+  // postorder
+  std::vector<std::vector<int32_t>> kids(NF);
+  std::vector<int32_t> roots;
+  for (int32_t f = 0; f < NF; ++f) {
+    if (nd[f].parent >= 0) kids[nd[f].parent].push_back(f);
+    else roots.push_back(f);
+  }
+  std::vector<int32_t> post;
+  post.reserve(NF);
+  {
+    std::vector<std::pair<int32_t, size_t>> st;
+    for (int32_t r : roots) {
+      st.push_back({r, 0});
+      while (!st.empty()) {
+        auto& top = st.back();
+        if (top.second < kids[top.first].size()) {
+          int32_t c = kids[top.first][top.second++];
+          st.push_back({c, 0});
+        } else {
+          post.push_back(top.first);
+          st.pop_back();
+        }
+      }
+    }
+  }
+  std::vector<int32_t> newid(NF);
+  for (int32_t k = 0; k < NF; ++k) newid[post[k]] = k;
+
+  // ---- positions -------------------------------------------------------------
+  s.perm.assign(n, -1);
+  s.ipos.assign(n, -1);
+  s.fronts.assign(NF, Front());
+  s.front_of_pos.assign(n, -1);
+  int64_t pos = 0;
+  for (int32_t k = 0; k < NF; ++k) {
+    const NdFront& src = nd[post[k]];
+    Front& F = s.fronts[k];
+    F.first = pos;
+    F.parent = src.parent >= 0 ? newid[src.parent] : -1;
+    if (post[k] == proot) {
+      F.is_root_p = 1;
+      F.pivtype = 1;
+      for (int64_t u = s.n_x; u < s.n_x + s.n_p; ++u) s.perm[pos++] = u;
+    } else {
+      F.pivtype = s.pair_mode ? 2 : 1;
+      for (int32_t sv : src.verts)
+        for (int32_t v : sv_members[sv])
+          for (int t = 0; t < 2; ++t)
+            if (node_unk[v][t] >= 0) s.perm[pos++] = node_unk[v][t];
+    }
+    F.npiv = (int32_t)(pos - F.first);
+  }
+  if (pos != n) { last_error() = "internal: ordering does not cover all unknowns"; return 5; }
+  for (int64_t q = 0; q < n; ++q) s.ipos[s.perm[q]] = q;
+  for (int32_t k = 0; k < NF; ++k)
+    for (int64_t q = s.fronts[k].first; q < s.fronts[k].first + s.fronts[k].npiv; ++q) s.front_of_pos[q] = k;
+
+  // children lists (in postorder id order)
+  s.children.clear();
+  {
+    std::vector<std::vector<int32_t>> ch(NF);
+    for (int32_t k = 0; k < NF; ++k)
+      if (s.fronts[k].parent >= 0) ch[s.fronts[k].parent].push_back(k);
+    for (int32_t k = 0; k < NF; ++k) {
+      s.fronts[k].child_begin = (int32_t)s.children.size();
+      s.children.insert(s.children.end(), ch[k].begin(), ch[k].end());
+      s.fronts[k].child_end = (int32_t)s.children.size();
+    }
+  }
+
+  // ---- row structures --------------------------------------------------------
+  s.srows.clear();
+  {
+    std::vector<int32_t> mark(n, -1);
+    std::vector<int64_t> tmp;
+    for (int32_t k = 0; k < NF; ++k) {
+      Front& F = s.fronts[k];
+      const int64_t last = F.first + F.npiv - 1;
+      tmp.clear();
+      for (int64_t q = F.first; q <= last; ++q) {
+        int64_t u = s.perm[q];
+        for (int64_t kk = s.indptr[u]; kk < s.indptr[u + 1]; ++kk) {
+          int64_t pv = s.ipos[s.indices[kk]];
+          if (pv > last && mark[pv] != k) { mark[pv] = k; tmp.push_back(pv); }
+        }
+      }
+      for (int32_t ci = F.child_begin; ci < F.child_end; ++ci) {
+        const Front& C = s.fronts[s.children[ci]];
+        int64_t cn = C.nrow - C.npiv;
+        for (int64_t t = 0; t < cn; ++t) {
+          int64_t pv = s.srows[C.srow_off + t];
+          if (pv > last && mark[pv] != k) { mark[pv] = k; tmp.push_back(pv); }
+        }
+      }
+      std::sort(tmp.begin(), tmp.end());
+      F.srow_off = (int64_t)s.srows.size();
+      s.srows.insert(s.srows.end(), tmp.begin(), tmp.end());
+      F.nrow = F.npiv + (int32_t)tmp.size();
+      // every struct row must belong to an ancestor (assembly-tree property)
+      if (!tmp.empty() && F.parent < 0) {
+        last_error() = "internal: root front has a non-empty structure";
+        return 5;
+      }
+    }
+  }
+  // rel maps
+  s.rel.assign(s.srows.size(), 0);
+  for (int32_t k = 0; k < NF; ++k) {
+    const Front& C = s.fronts[k];
+    int64_t cn = C.nrow - C.npiv;
+    if (cn == 0) continue;
+    const Front& P = s.fronts[C.parent];
+    const int64_t plast = P.first + P.npiv - 1;
+    const int64_t* pb = s.srows.data() + P.srow_off;
+    const int64_t pn = P.nrow - P.npiv;
+    for (int64_t t = 0; t < cn; ++t) {
+      int64_t pv = s.srows[C.srow_off + t];
+      int64_t local;
+      if (pv >= P.first && pv <= plast) local = pv - P.first;
+      else {
+        const int64_t* it = std::lower_bound(pb, pb + pn, pv);
+        if (it == pb + pn || *it != pv) { last_error() = "internal: child row missing from parent front"; return 5; }
+        local = P.npiv + (it - pb);
+      }
+      s.rel[C.srow_off + t] = (int32_t)local;
+    }
+  }
+  for (auto& F : s.fronts) F.rel_off = F.srow_off;
+
+  // ---- levels, offsets, stats ------------------------------------------------
+  s.n_levels = 0;
+  for (int32_t k = 0; k < NF; ++k) {
+    Front& F = s.fronts[k];
+    int32_t lv = 0;
+    for (int32_t ci = F.child_begin; ci < F.child_end; ++ci) lv = std::max(lv, s.fronts[s.children[ci]].level + 1);
+    F.level = lv;
+    s.n_levels = std::max(s.n_levels, lv + 1);
+  }
+  s.level_fronts.assign(s.n_levels, {});
+  for (int32_t k = 0; k < NF; ++k) s.level_fronts[s.fronts[k].level].push_back(k);
+
+  s.front_doubles = s.u_doubles = s.w_doubles = s.v_doubles = 0;
+  s.ntiles = 0;
+  s.nnz_l = 0;
+  s.flops = 0;
+  s.max_front = s.max_piv = 0;
+  for (auto& F : s.fronts) {
+    const int64_t nr = F.nrow, ns = F.nrow - F.npiv;
+    F.foff = s.front_doubles; s.front_doubles += nr * nr;
+    F.uoff = s.u_doubles; s.u_doubles += ns;
+    F.woff = s.w_doubles; s.w_doubles += nr * kTile;
+    F.voff = s.v_doubles; s.v_doubles += nr;
+    const int64_t T = (nr + kTile - 1) / kTile;
+    F.tile_base = s.ntiles; s.ntiles += T * (T + 1) / 2;
+    s.nnz_l += (int64_t)F.npiv * (F.npiv + 1) / 2 + (int64_t)F.npiv * ns;
+    for (int64_t j = 0; j < F.npiv; ++j) {
+      double r = (double)(nr - j - 1);
+      s.flops += r * r + 2.0 * r;
+    }
+    s.max_front = std::max<int64_t>(s.max_front, nr);
+    s.max_piv = std::max<int64_t>(s.max_piv, F.npiv);
+  }
+
+  // stabilization kind per position
+  s.kind_pos.assign(n, 0);
+  if (s.pair_mode) {
+    for (int64_t q = 0; q < n; ++q) {
+      int64_t u = s.perm[q];
+      s.kind_pos[q] = (u < s.n_x) ? 1 : (u >= s.n_x + s.n_p ? 2 : 0);
+    }
+  }
+
+  // ---- assembly entry lists per tile (lower triangle in elimination order) -----
+  {
+    std::vector<int64_t> cnt(s.ntiles + 1, 0);
+    std::vector<int64_t> ent_tile;
+    std::vector<int64_t> ent_k;
+    std::vector<int32_t> ent_loc;
+    ent_tile.reserve(nnz / 2 + n);
+    for (int64_t v = 0; v < n; ++v) {
+      const int64_t pv = s.ipos[v];
+      const int32_t f = s.front_of_pos[pv];
+      const Front& F = s.fronts[f];
+      const int64_t lc = pv - F.first;
+      const int64_t last = F.first + F.npiv - 1;
+      const int64_t* sb = s.srows.data() + F.srow_off;
+      const int64_t sn = F.nrow - F.npiv;
+      for (int64_t k = s.indptr[v]; k < s.indptr[v + 1]; ++k) {
+        const int64_t pu = s.ipos[s.indices[k]];
+        if (pu < pv) continue;
+        int64_t lr;
+        if (pu <= last) lr = pu - F.first;
+        else {
+          const int64_t* it = std::lower_bound(sb, sb + sn, pu);
+          if (it == sb + sn || *it != pu) { last_error() = "internal: entry outside front"; return 5; }
+          lr = F.npiv + (it - sb);
+        }
+        const int64_t ti = lr / kTile, tj = lc / kTile;
+        const int64_t tile = F.tile_base + ti * (ti + 1) / 2 + tj;
+        ent_tile.push_back(tile);
+        ent_k.push_back(k);
+        ent_loc.push_back((int32_t)((lr % kTile) * kTile + (lc % kTile)));
+        cnt[tile + 1]++;
+      }
+    }
+    for (int64_t t = 0; t < s.ntiles; ++t) cnt[t + 1] += cnt[t];
+    s.tile_ptr = cnt;
+    s.tile_nnz.assign(ent_tile.size(), 0);
+    s.tile_loc.assign(ent_tile.size(), 0);
+    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    for (size_t e = 0; e < ent_tile.size(); ++e) {
+      int64_t at = fill[ent_tile[e]]++;
+      s.tile_nnz[at] = ent_k[e];
+      s.tile_loc[at] = ent_loc[e];
+    }
+  }
+
+  // ---- factorization launch schedule -----------------------------------------
+  s.work.clear();
+  s.launches.clear();
+  for (int32_t lv = 0; lv < s.n_levels; ++lv) {
+    const auto& fl = s.level_fronts[lv];
+    // assembly tiles
+    int64_t off = (int64_t)s.work.size();
+    for (int32_t f : fl) {
+      const int64_t T = (s.fronts[f].nrow + kTile - 1) / kTile;
+      for (int64_t ti = 0; ti < T; ++ti)
+        for (int64_t tj = 0; tj <= ti; ++tj) s.work.push_back({f, (int32_t)ti, (int32_t)tj, 0});
+    }
+    if ((int64_t)s.work.size() > off) s.launches.push_back({L_ASM, lv, off, (int64_t)s.work.size() - off});
+    int32_t maxp = 0;
+    for (int32_t f : fl) maxp = std::max(maxp, (s.fronts[f].npiv + kTile - 1) / kTile);
+    for (int32_t k = 0; k < maxp; ++k) {
+      off = (int64_t)s.work.size();
+      for (int32_t f : fl) {
+        const Front& F = s.fronts[f];
+        const int32_t j0 = k * kTile;
+        if (j0 >= F.npiv) continue;
+        const int32_t w = std::min(kTile, F.npiv - j0);
+        const int32_t below = F.nrow - j0 - w;
+        const int32_t nt = (below + kTile - 1) / kTile;
+        for (int32_t t = 0; t <= nt; ++t) s.work.push_back({f, k, t, 0});
+      }
+      if ((int64_t)s.work.size() > off) s.launches.push_back({L_PANEL, lv, off, (int64_t)s.work.size() - off});
+      off = (int64_t)s.work.size();
+      for (int32_t f : fl) {
+        const Front& F = s.fronts[f];
+        const int32_t j0 = k * kTile;
+        if (j0 >= F.npiv) continue;
+        const int32_t w = std::min(kTile, F.npiv - j0);
+        const int32_t below = F.nrow - j0 - w;
+        const int32_t T = (below + kTile - 1) / kTile;
+        for (int32_t ti = 0; ti < T; ++ti)
+          for (int32_t tj = 0; tj <= ti; ++tj) s.work.push_back({f, k, ti, tj});
+      }
+      if ((int64_t)s.work.size() > off) s.launches.push_back({L_UPDATE, lv, off, (int64_t)s.work.size() - off});
+    }
+  }
+  return 0;
+}
+
+}  // namespace sgn
