@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""SGN search directions/sec on B200 -- BASELINE.json metric, config 2 (100x100 sheet).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One *step* = one SGN search direction (reference direction_sgn, optimize.py:155-165):
+device assembly of the element Hessian / mixed blocks into the KKT pattern, the LDL^T
+factorization, the adjoint gradient and the refined KKT solve, on the 100x100
+neo-Hookean sheet (BASELINE configs[1]; synthetic seeded inputs, oracle/configs.py).
+
+* ``value``  -- directions/sec with x, p resident in HBM (device time, CUDA events on
+  the launching stream, max over ranks); L2 is flushed (512 MiB memset) before every
+  timed step, outside the events.
+* ``e2e``    -- the same metric through the public API direction_sgn(prob, x, p, cfg)
+  with host NumPy inputs/outputs (H2D of x, p and D2H of the solution every step).
+* ``roofline`` -- the factorization phase (k_assemble/k_panel/k_update launches) on the
+  FP64 tensor pipe: algorithmic LDL^T flops of the symbolic analysis / its live event
+  time, against the DMMA peak measured in the same run (MEASURED_PEAKS.json has no FP64
+  entry); per-phase HBM fractions in ``phases``.
+* ``cpu_baseline`` -- the CPU oracle (restated reference path: SciPy SuperLU + BiCGSTAB)
+  on 1 host core over a bounded sample of directions.
+* ``--impl reference`` -- the oracle port of the reference's CPU path on all host cores
+  (one single-threaded direction per worker per step).
+With N > 1 (torchrun) every rank runs an independent replica ("replicas only": a single
+sparse factorization does not shard); value = total directions / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SGN search directions/sec (assemble+factor+solve)"
+UNIT = "directions/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--cpu-sample", type=int, default=3, help="directions in the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.lines, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [q.strip() for q in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0])); mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------ CPU legs
+def _cpu_worker_init(config):
+    global _W
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+    from oracle.configs import oracle_sheet
+    prob, p0 = oracle_sheet(config)
+    _W = (prob, p0)
+
+
+def _cpu_worker_direction(x):
+    from oracle import sgn_cpu
+    prob, p0 = _W
+    t0 = time.perf_counter()
+    d = sgn_cpu.direction_sgn(prob, x, p0)
+    return time.perf_counter() - t0, d.timings
+
+
+def cpu_equilibrium(config):
+    from oracle.configs import oracle_sheet
+    prob, p0 = oracle_sheet(config)
+    return prob.simulate(p0)
+
+
+def cpu_baseline(config, x, sample):
+    """Oracle port on 1 core: median of `sample` directions (after one warm-up)."""
+    from threadpoolctl import threadpool_limits
+    _cpu_worker_init(config)
+    with threadpool_limits(1):
+        _cpu_worker_direction(x)
+        ts = [_cpu_worker_direction(x) for _ in range(sample)]
+    med = statistics.median([t for t, _ in ts])
+    phases = {k: statistics.median([tt[k] for _, tt in ts]) for k in ("assemble_s", "factor_s", "solve_s")}
+    return {"value": 1.0 / med, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{sample} directions (median) of config {config} on 1 core after 1 warm-up; "
+                      f"oracle/sgn_cpu.py restating the reference SuperLU+BiCGSTAB path",
+            "median_s": med, "phases_s": phases}
+
+
+def run_reference(args):
+    """--impl reference: the oracle port of the reference CPU path on all host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import multiprocessing as mp
+    import numpy as np
+    cores = os.cpu_count() or 1
+    workers = max(1, min(cores, 64))
+    x = cpu_equilibrium(args.config)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers, initializer=_cpu_worker_init, initargs=(args.config,)) as pool:
+        step_t = []
+        for s in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(_cpu_worker_direction, [x] * workers)
+            dt = time.perf_counter() - t0
+            if s >= args.warmup:
+                step_t.append(dt)
+    total = sum(step_t)
+    value = workers * len(step_t) / total
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(step_t),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded, oracle/configs.py)",
+           "config": {"workload": f"config {args.config}: 100x100 neo-Hookean sheet, n_p=400, one SGN direction",
+                      "parallelism": f"{workers} single-threaded host processes"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                            "sample": f"each step = {workers} concurrent directions (one per worker)"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+# ------------------------------------------------------------------------------------ our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    from paper_2107_03285_b200 import OptimizerConfig, direction_sgn
+    from paper_2107_03285_b200._lib import lib, stream_handle
+    from paper_2107_03285_b200.engine import sgn_solve_stages
+    from paper_2107_03285_b200.problems import build_sheet
+    import ctypes
+
+    # measured FP64 peaks (roofline denominators)
+    dm, df = ctypes.c_double(0), ctypes.c_double(0)
+    lib().sgn_fp64_peak(0, 20000, ctypes.byref(dm), stream_handle())
+    lib().sgn_fp64_peak(1, 20000, ctypes.byref(df), stream_handle())
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s (B200_PROFILING.md)"
+
+    prob, p0 = build_sheet(args.config)
+    x = prob.simulate(p0)                       # GPU Newton equilibrium (setup, untimed)
+    eng = prob.engine
+    pl = prob.plan
+    st = eng.ksym.stats()
+    cfg = OptimizerConfig()
+    prob._load(x, p0)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")   # 512 MiB > L2
+
+    def one(events=None, timings=None):
+        if events is not None:
+            events[0].record()
+        eng.assemble()
+        if events is not None:
+            events[1].record()
+        return sgn_solve_stages(eng, timings, True, events[2:] if events is not None else None)
+
+    for _ in range(args.warmup):
+        one()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    l0 = lib().sgn_launch_count()
+    rec = []
+    iters_main, iters_adj = [], []
+    for _ in range(args.steps):
+        flush.zero_()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        tm = {}
+        one(ev, tm)
+        rec.append(ev)
+        iters_main.append(int(tm["main_iters"][0]))
+        iters_adj.append(int(tm["adjoint_iters"][0]))
+    torch.cuda.synchronize()
+    launches = lib().sgn_launch_count() - l0      # our kernels only (the flush memset is torch's)
+    clocks = sampler.stop()
+    ms = [e[0].elapsed_time(e[4]) for e in rec]
+    ph = {"assemble": [e[0].elapsed_time(e[1]) for e in rec], "factor": [e[1].elapsed_time(e[2]) for e in rec],
+          "adjoint": [e[2].elapsed_time(e[3]) for e in rec], "solve": [e[3].elapsed_time(e[4]) for e in rec]}
+    total_ms = sum(ms)
+    tmax = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    total_ms = float(tmax.item())
+    value = world * args.steps / (total_ms * 1e-3)
+
+    # e2e through the public API with host buffers
+    xh, ph_ = np.asarray(x), np.asarray(p0)
+    for _ in range(2):
+        direction_sgn(prob, xh, ph_, cfg)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sd = direction_sgn(prob, xh, ph_, cfg)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    et = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_value = world * e2e_steps / float(et.item())
+
+    med = lambda v: statistics.median(v)
+    f_ms = med(ph["factor"])
+    flops = st["flops"]
+    achieved_tf = flops / (f_ms * 1e-3) / 1e12
+    cols = np.repeat(np.arange(pl.dim), np.diff(pl.K_indptr))
+    has_diag = np.zeros(pl.dim, bool)
+    has_diag[cols[pl.K_indices == cols]] = True
+    shift_rows = np.r_[np.arange(pl.n_x), np.arange(pl.n_x + pl.n_p, pl.dim)]
+    nnz_tril = int((pl.K_indices >= cols).sum() + (~has_diag[shift_rows]).sum())   # tril(K_s)
+    asm_bytes = 8 * nnz_tril + 16 * pl.d * pl.n_v + 4 * pl.nv_el * pl.n_e + 16 * pl.n_p
+    a_ms = med(ph["assemble"])
+    lbytes = 8 * st["nnz_l"]
+    n_solves_main = 2 + 2 * med(iters_main) if med(iters_main) > 0 else 1
+    n_spmv_main = 2 + 3 * med(iters_main)
+    solve_bytes = n_solves_main * 2 * lbytes + n_spmv_main * 12 * pl.nnz
+    s_ms = med(ph["solve"])
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded mesh/targets/p0, oracle/configs.py; no dataset)",
+        "config": {"workload": f"config {args.config}: 100x100 neo-Hookean sheet (19602 tris), n_x=19800, "
+                               f"n_p=400, KKT dim {pl.dim}, nnz(K) {pl.nnz}",
+                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "l2": "flushed before every timed step (512 MiB memset outside the events)",
+                   "nnz_L": st["nnz_l"], "factor_flops": flops, "fronts": st["n_fronts"],
+                   "tree_levels": st["n_levels"]},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * (pl.n_x + pl.n_p),
+                "d2h_bytes_per_step": 8 * pl.dim},
+        "roofline": {"bound": "tensor", "kernel": "factorization (k_assemble+k_panel+k_update, DMMA)",
+                     "achieved": achieved_tf, "peak": dm.value, "unit": "TFLOP/s",
+                     "frac": achieved_tf / dm.value if dm.value else None, "traffic": None,
+                     "peak_source": "sgn_fp64_peak DMMA microbenchmark, same run (no FP64 entry in MEASURED_PEAKS.json)",
+                     "flops_per_launch_group": flops, "ms": f_ms},
+        "phases": {
+            "assemble": {"ms": a_ms, "bound": "hbm", "algorithmic_bytes": asm_bytes,
+                         "achieved_gbs": asm_bytes / (a_ms * 1e-3) / 1e9,
+                         "frac": asm_bytes / (a_ms * 1e-3) / 1e9 / hbm_peak},
+            "factor": {"ms": f_ms, "tflops": achieved_tf},
+            "adjoint": {"ms": med(ph["adjoint"]), "bicgstab_iters": med(iters_adj)},
+            "solve": {"ms": s_ms, "bicgstab_iters": med(iters_main), "algorithmic_bytes": solve_bytes,
+                      "achieved_gbs": solve_bytes / (s_ms * 1e-3) / 1e9,
+                      "frac": solve_bytes / (s_ms * 1e-3) / 1e9 / hbm_peak},
+            "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,
+            "fp64_dmma_tflops": dm.value, "fp64_dfma_tflops": df.value},
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+        "relative_residual": float(sd.relative_residual),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline(args.config, np.asarray(x), args.cpu_sample)
+        except Exception as exc:  # the baseline is reported, never required for the GPU number
+            out["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    if rank == 0:
+        print(json.dumps(out))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

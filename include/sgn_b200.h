@@ -59,6 +59,8 @@ typedef struct {
 /* ---- library ------------------------------------------------------------------- */
 const char* sgn_last_error(void);
 int sgn_version(void);
+/* total kernel launches issued by this library so far (launch-count evidence) */
+int64_t sgn_launch_count(void);
 int sgn_device_sync(void* stream);
 
 /* ---- symbolic analysis (host, once per sparsity pattern) -----------------------
@@ -138,6 +140,33 @@ int  sgn_gather_values(int64_t n_out, int32_t batch, const double* d_base, int64
                        const int64_t* d_ptr, const int64_t* d_idx, const double* d_coef,
                        const double* d_buf, int64_t buf_stride, double* d_out,
                        int64_t out_stride, void* stream);
+
+
+/* ---- batched vector kernels of the direction / forward-solve pipeline -------------
+ * sgn_reduce: op 0 = sum, 1 = dot(a, b), 2 = max|a|; one deterministic value per
+ * instance (fixed reduction order).  Replaces the NumPy reductions of the objective,
+ * energies and norms (sensitivity.py:83-85, forward.py:149,189-203).                */
+int  sgn_reduce(int32_t op, int64_t n, int32_t batch, const double* d_a, const double* d_b,
+                int64_t stride, double* d_out, void* stream);
+/* out = y + alpha[b] * x  (per-instance step length; forward.py:197-199, optimize.py:472) */
+int  sgn_axpy(int64_t n, int32_t batch, const double* d_alpha, const double* d_x,
+              const double* d_y, double* d_out, int64_t stride, void* stream);
+/* least-squares terms: d_vec (KKT order, dim = 2 n_x + n_p per instance) receives
+ * (df/dx, df/dp, 0) for r = (x[tdofs] - tvals, p) with weights (w_t, w_reg);
+ * d_fobj[b] = 0.5 sum w r^2 (sensitivity.py:83-93).  Either output may be NULL.      */
+int  sgn_lsq_terms(int32_t batch, int64_t n_x, int64_t n_p, int64_t nt, const int64_t* d_tdofs,
+                   const double* d_tvals, int64_t tstride, double w_t, double w_reg,
+                   const double* d_x, const double* d_p, double* d_vec, double* d_fobj,
+                   void* stream);
+/* adjoint gradient from a leading-block KKT solve (sensitivity.py:181-198, 245-256):
+ * mode 0: d_out = (0, 0, d_src[lambda]);  mode 1: g = d_fvec[p] - d_src[p] (d_src = K v),
+ * d_out = (0, -g, 0), d_grad = g.                                                     */
+int  sgn_adjoint_step(int32_t mode, int32_t batch, int64_t n_x, int64_t n_p, const double* d_src,
+                      const double* d_fvec, double* d_out, double* d_grad, void* stream);
+
+/* FP64 peak microbenchmark (roofline denominator; MEASURED_PEAKS.json has no FP64 figure):
+ * mode 0 = DMMA m8n8k4 tensor pipe, 1 = DFMA.  *tflops = achieved TFLOP/s (all SMs).   */
+int  sgn_fp64_peak(int32_t mode, int32_t iters, double* tflops, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,106 @@
+"""Seeded synthetic instances of the BASELINE.json configs (shared definition).
+
+Pure mesh/config generation (NumPy), used by the oracle problems, by the GPU problem
+classes (via paper_2107_03285_b200.problems.build_sheet, which re-derives the same
+arrays from these specs) and by bench.py.  Choices that BASELINE.json leaves open
+ are fixed here and recorded in DESIGN.md:
+
+* triangulation: quad (i,j)-(i+1,j)-(i+1,j+1)-(i,j+1) split along (i,j)-(i+1,j+1);
+  vertex id = i*n_h + j, x = i/(n_w-1), y = j/(n_h-1)  (reference lattice idiom,
+  spring_bar.py:45-50);
+* material: compressible neo-Hookean, plane strain, E, nu as given;
+* load: self-weight with areal density RHO_SHEET = 100 (g = 9.81, along -y), lumped by
+  rest area (so it enters d2E/dx dX) -- BASELINE gives no load (§0.9 v);
+* c1 p: rest y-offsets of bottom then top row (i = 0..n_w-1), 40 params;
+* c2 p: rest (x, y)-offsets of bottom then top row vertices, 400 params (§0.9 ii);
+* p0 ~ U(-h, h) redrawn from the same stream while any rest triangle falls below 20% of
+  its nominal area (the literal c2 draw can invert boundary triangles);
+* left column (i = 0) clamped at its original rest position;
+* objective 0.5*|x_S - target|^2 (w = 1) + 1e-6*|p|^2 (w_reg = 2e-6);
+* equilibrium rows scaled by 1/E.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+RHO_SHEET = 100.0
+GRAVITY = 9.81
+
+
+def sheet_mesh(n_w: int, n_h: int):
+    ix, iy = np.meshgrid(np.arange(n_w), np.arange(n_h), indexing="ij")
+    X0 = np.column_stack([ix.ravel() / (n_w - 1), iy.ravel() / (n_h - 1)])
+    vid = lambda i, j: i * n_h + j
+    tris = []
+    for i in range(n_w - 1):
+        for j in range(n_h - 1):
+            a, b, c, d = vid(i, j), vid(i + 1, j), vid(i + 1, j + 1), vid(i, j + 1)
+            tris.append((a, b, c))
+            tris.append((a, c, d))
+    return X0, np.array(tris, dtype=np.int64)
+
+
+def sheet_spec(config: int, seed: int = 0, instance: int = 0):
+    """Arrays defining sheet config 1 (20x20) or 2 (100x100; also config-5 instances).
+
+    Returns a dict accepted by oracle.problems.ElementProblem and by the GPU problem
+    class.  ``instance`` > 0 draws the config-5 per-instance E and targets.
+    """
+    rng = np.random.default_rng(1000 * seed + instance)
+    if config == 1:
+        n_w = n_h = 20
+        E, nu = 1e5, 0.3
+    elif config == 2:
+        n_w = n_h = 100
+        E, nu = 1e5, 0.3
+    else:
+        raise ValueError("sheet configs are 1 and 2")
+    if instance > 0:
+        E = float(rng.uniform(5e4, 2e5))
+    X0, tris = sheet_mesh(n_w, n_h)
+    fixed = np.arange(n_h)                           # column i == 0
+    bottom = np.arange(n_w) * n_h                    # j == 0
+    top = np.arange(n_w) * n_h + (n_h - 1)           # j == n_h-1
+    rows = np.concatenate([bottom, top])
+    if config == 1:
+        pm_dof = rows * 2 + 1
+        half = 0.01
+    else:
+        pm_dof = (rows[:, None] * 2 + np.arange(2)[None, :]).ravel()
+        half = 0.005
+    # redraw (same stream) until no rest triangle keeps < 20% of its nominal area:
+    # U(-0.005, 0.005) tangential offsets on the 100x100 grid (h = 0.0101) can invert
+    # boundary triangles, leaving no equilibrium (config resolution)
+    nominal = 0.5 / ((n_w - 1) * (n_h - 1))
+    while True:
+        p0 = rng.uniform(-half, half, pm_dof.size)
+        X = X0.ravel().copy()
+        X[pm_dof] += p0
+        X = X.reshape(-1, 2)
+        e1, e2 = X[tris[:, 1]] - X[tris[:, 0]], X[tris[:, 2]] - X[tris[:, 0]]
+        if (0.5 * (e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0])).min() >= 0.2 * nominal:
+            break
+    pmap = (pm_dof, np.arange(pm_dof.size), np.ones(pm_dof.size))
+    free_verts = np.setdiff1d(np.arange(n_w * n_h), fixed)
+    vert_to_free = -np.ones(n_w * n_h, dtype=np.int64)
+    vert_to_free[free_verts] = np.arange(free_verts.size)
+    if config == 1:
+        tv = (n_w - 1) * n_h + np.arange(n_h)        # right column
+        sigma = 0.02
+    else:
+        interior = np.array([i * n_h + j for i in range(1, n_w - 1) for j in range(1, n_h - 1)])
+        tv = np.sort(rng.choice(interior, size=200, replace=False))
+        sigma = 0.01
+    tdofs = (vert_to_free[tv][:, None] * 2 + np.arange(2)[None, :]).ravel()
+    tvals = X0[tv].ravel() + rng.normal(0.0, sigma, tdofs.size)
+    return dict(X0=X0, conn=tris, kind="tri", fixed_verts=fixed, pmap=pmap, target_dofs=tdofs,
+                target_vals=tvals, w_target=1.0, w_reg=2e-6, E=E, nu=nu,
+                gload=RHO_SHEET * GRAVITY, p0=p0, name=f"sheet_c{config}")
+
+
+def oracle_sheet(config: int, seed: int = 0, instance: int = 0):
+    from .problems import ElementProblem
+    spec = sheet_spec(config, seed, instance)
+    p0 = spec.pop("p0")
+    spec.pop("name")
+    return ElementProblem(**spec), p0

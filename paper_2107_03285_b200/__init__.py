@@ -13,5 +13,9 @@ from .linear_solvers import (SolveReport, SparseFactorization, StabilizationConf
                              factor_sparse, solve_kkt_stabilized, stabilized_matrix)
 from .sparse import (CscMatrix, TripletMatrix, csc_from_triplets, read_matrix_market, spmv,
                      spmv_transpose, stack_kkt_blocks, write_matrix_market)
+from .sensitivity import (EquilibriumProblem, GnBlocks, KktSystem, adjoint_gradient, assemble_sgn,
+                          gn_blocks, kkt_from_blocks)
+from .optimize import (CSV_HEADER, METHODS, IterationRecord, OptimizerConfig, OptimizerRun,
+                       SearchDirection, direction_sgn, minimize, project_direction_bounds)
 
 __version__ = "0.1.0"

@@ -33,6 +33,7 @@ class SymbolicStats(ctypes.Structure):
 SIGNATURES = {
     "sgn_last_error": (ctypes.c_char_p, []),
     "sgn_version": (ctypes.c_int, []),
+    "sgn_launch_count": (c_i64, []),
     "sgn_device_sync": (ctypes.c_int, [c_vp]),
     "sgn_symbolic_create": (ctypes.c_int, [c_i64, P_i64, P_i64, c_i64, c_i64, c_i64, c_i32,
                                            ctypes.POINTER(c_vp), P_i64]),
@@ -54,6 +55,12 @@ SIGNATURES = {
                                                c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
     "sgn_gather_values": (ctypes.c_int, [c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp,
                                          c_i64, c_vp, c_i64, c_vp]),
+    "sgn_reduce": (ctypes.c_int, [c_i32, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "sgn_axpy": (ctypes.c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "sgn_lsq_terms": (ctypes.c_int, [c_i32, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_dbl, c_dbl,
+                                     c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "sgn_fp64_peak": (ctypes.c_int, [c_i32, c_i32, P_dbl, c_vp]),
+    "sgn_adjoint_step": (ctypes.c_int, [c_i32, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 
 _LIB = None

@@ -305,7 +305,8 @@ __device__ void spring_energy_grad(const double* xv, const double* Xv, double k,
   for (int i = 0; i < D; ++i) { grad[i] = c * d[i]; grad[D + i] = -c * d[i]; }
 }
 
-// params layout per instance: [mu, lambda, gload, spring_dim] ; springs use per-element k
+// params layout per instance: [mu, lambda, gload, scale, k_0, k_1, ...]; outputs are multiplied
+// by `scale` (the 1/E equilibrium-row scaling); springs read per-element k_e
 template <int TYPE, int D>
 __global__ void k_elem_derivs(int64_t ne, const int32_t* __restrict__ conn, const double* __restrict__ pos,
                               const double* __restrict__ rest, int64_t vstride,
@@ -329,10 +330,11 @@ __global__ void k_elem_derivs(int64_t ne, const int32_t* __restrict__ conn, cons
   const double* pr = params + (int64_t)b * pstride;
   if (TYPE == SGN_ELEM_SPRING) spring_derivs<D>(xv, Xv, pr[4 + e], h, m);
   else nh_simplex_derivs<D>(xv, Xv, pr[0], pr[1], pr[2], h, m);
+  const double sc = pr[3];
   double* hb = hess + (int64_t)b * bstride + e * ND * ND;
   double* mb = mixed + (int64_t)b * bstride + e * ND * ND;
 #pragma unroll
-  for (int k = 0; k < ND * ND; ++k) { hb[k] = h[k]; mb[k] = m[k]; }
+  for (int k = 0; k < ND * ND; ++k) { hb[k] = sc * h[k]; mb[k] = sc * m[k]; }
 }
 
 template <int TYPE, int D>
@@ -358,11 +360,12 @@ __global__ void k_elem_energy_grad(int64_t ne, const int32_t* __restrict__ conn,
   const double* pr = params + (int64_t)b * pstride;
   if (TYPE == SGN_ELEM_SPRING) spring_energy_grad<D>(xv, Xv, pr[4 + e], &en, g);
   else nh_simplex_energy_grad<D>(xv, Xv, pr[0], pr[1], pr[2], &en, g);
-  if (energy) energy[(int64_t)b * ne + e] = en;
+  const double sc = pr[3];
+  if (energy) energy[(int64_t)b * ne + e] = sc * en;
   if (grad) {
     double* gb = grad + (int64_t)b * bstride + e * ND;
 #pragma unroll
-    for (int k = 0; k < ND; ++k) gb[k] = g[k];
+    for (int k = 0; k < ND; ++k) gb[k] = sc * g[k];
   }
 }
 
@@ -405,18 +408,22 @@ int sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch, const 
   switch (elem_type) {
     case SGN_ELEM_SPRING:
     case SGN_ELEM_SPRING + 200:
+      sgn::count_launch();
       k_elem_derivs<SGN_ELEM_SPRING, 2><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
                                                               d_params, param_stride, d_hess, d_mixed, buf_stride);
       break;
     case SGN_ELEM_SPRING + 300:
+      sgn::count_launch();
       k_elem_derivs<SGN_ELEM_SPRING, 3><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
                                                               d_params, param_stride, d_hess, d_mixed, buf_stride);
       break;
     case SGN_ELEM_NH_TRI:
+      sgn::count_launch();
       k_elem_derivs<SGN_ELEM_NH_TRI, 2><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
                                                               d_params, param_stride, d_hess, d_mixed, buf_stride);
       break;
     case SGN_ELEM_NH_TET:
+      sgn::count_launch();
       k_elem_derivs<SGN_ELEM_NH_TET, 3><<<grid, 64, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
                                                              d_params, param_stride, d_hess, d_mixed, buf_stride);
       break;
@@ -438,18 +445,22 @@ int sgn_element_energy_grad(int32_t elem_type, int64_t n_elems, int32_t batch, c
   switch (elem_type) {
     case SGN_ELEM_SPRING:
     case SGN_ELEM_SPRING + 200:
+      sgn::count_launch();
       k_elem_energy_grad<SGN_ELEM_SPRING, 2><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
                                                                    d_params, param_stride, d_energy, d_grad, buf_stride);
       break;
     case SGN_ELEM_SPRING + 300:
+      sgn::count_launch();
       k_elem_energy_grad<SGN_ELEM_SPRING, 3><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
                                                                    d_params, param_stride, d_energy, d_grad, buf_stride);
       break;
     case SGN_ELEM_NH_TRI:
+      sgn::count_launch();
       k_elem_energy_grad<SGN_ELEM_NH_TRI, 2><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
                                                                    d_params, param_stride, d_energy, d_grad, buf_stride);
       break;
     case SGN_ELEM_NH_TET:
+      sgn::count_launch();
       k_elem_energy_grad<SGN_ELEM_NH_TET, 3><<<grid, 64, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
                                                                   d_params, param_stride, d_energy, d_grad, buf_stride);
       break;
@@ -468,6 +479,7 @@ int sgn_gather_values(int64_t n_out, int32_t batch, const double* d_base, int64_
   if (n_out == 0) return SGN_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const dim3 grid((unsigned)((n_out + 255) / 256), batch);
+  sgn::count_launch();
   k_gather<<<grid, 256, 0, st>>>(n_out, d_base, base_stride, d_ptr, d_idx, d_coef, d_buf, buf_stride,
                                  d_out, out_stride);
   ELEM_CHECK();

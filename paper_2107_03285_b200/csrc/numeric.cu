@@ -658,11 +658,13 @@ int launch_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cu
   const int64_t n = s.n;
   if (n == 0) return SGN_OK;
   const dim3 pg((unsigned)std::min<int64_t>((n + 255) / 256, 1024), f->batch);
+  sgn::count_launch();
   k_permute_in<<<pg, 256, 0, st>>>(d_b, f->y.p, f->perm.p, n);
   const int leading = (flags & SGN_SOLVE_LEADING) ? 1 : 0;
   for (int32_t lv = 0; lv < s.n_levels; ++lv) {
     const int64_t cnt = f->lvl_off[lv + 1] - f->lvl_off[lv];
     if (!cnt) continue;
+    sgn::count_launch();
     k_fwd<<<dim3((unsigned)cnt, f->batch), kSolveThreads, 0, st>>>(
         f->lvl_fronts.p + f->lvl_off[lv], f->fronts.p, f->children.p, f->rel.p, f->fstore.p,
         s.front_doubles, f->y.p, n, f->ubuf.p, s.u_doubles, f->vbuf.p, s.v_doubles, leading);
@@ -670,10 +672,12 @@ int launch_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cu
   for (int32_t lv = s.n_levels - 1; lv >= 0; --lv) {
     const int64_t cnt = f->lvl_off[lv + 1] - f->lvl_off[lv];
     if (!cnt) continue;
+    sgn::count_launch();
     k_bwd<<<dim3((unsigned)cnt, f->batch), kSolveThreads, 0, st>>>(
         f->lvl_fronts.p + f->lvl_off[lv], f->fronts.p, f->srows.p, f->fstore.p, s.front_doubles,
         f->y.p, n, f->vbuf.p, s.v_doubles, leading);
   }
+  sgn::count_launch();
   k_permute_out<<<pg, 256, 0, st>>>(f->y.p, d_x, f->perm.p, n);
   CUDA_TRY(cudaGetLastError());
   return SGN_OK;
@@ -687,6 +691,7 @@ int launch_spmv(sgn_factor f, const double* vals, int64_t vstride, const double*
   int64_t p_lo = 0, p_hi = 0;
   if ((flags & SGN_SOLVE_LEADING) && s.pair_mode) { p_lo = s.n_x; p_hi = s.n_x + s.n_p; }
   const int64_t threads = n * 8;
+  sgn::count_launch();
   k_spmv<<<dim3((unsigned)((threads + 255) / 256), f->batch), 256, 0, st>>>(
       f->indptr.p, f->idx32.p, vals, vstride, x, y, n, p_lo, p_hi);
   CUDA_TRY(cudaGetLastError());
@@ -702,6 +707,7 @@ extern "C" {
 
 const char* sgn_last_error(void) { return sgn::last_error().c_str(); }
 int sgn_version(void) { return 1; }
+int64_t sgn_launch_count(void) { return sgn::launch_count(); }
 
 int sgn_device_sync(void* stream) {
   CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
@@ -832,17 +838,20 @@ int sgn_factor_numeric(sgn_factor f, const double* d_values, int64_t values_stri
     const Work* w = f->work.p + L.off;
     switch (L.kind) {
       case sgn::L_ASM:
+        sgn::count_launch();
         k_assemble<<<grid, kAsmThreads, 0, st>>>(w, f->fronts.p, f->children.p, f->rel.p,
                                                  f->tile_ptr.p, f->tile_nnz.p, f->tile_loc.p,
                                                  f->kind_pos.p, d_values, values_stride, eps_x,
                                                  eps_lambda, f->fstore.p, s.front_doubles);
         break;
       case sgn::L_PANEL:
+        sgn::count_launch();
         k_panel<<<grid, kPanelThreads, 0, st>>>(w, f->fronts.p, f->perm.p, f->fstore.p,
                                                 s.front_doubles, f->wstore.p, s.w_doubles,
                                                 f->status.p);
         break;
       case sgn::L_UPDATE:
+        sgn::count_launch();
         k_update<<<grid, kUpdThreads, 0, st>>>(w, f->fronts.p, f->fstore.p, s.front_doubles,
                                                f->wstore.p, s.w_doubles);
         break;
@@ -899,7 +908,9 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
   const dim3 dg(kDotBlocks, B);
   BiState* S = f->bst.p;
   auto dot = [&](const double* a, const double* b2, const double* c, const double* d, int step, int it) {
+    sgn::count_launch();
     k_dot_partial<<<dg, kDotThreads, 0, st>>>(a, b2, c, d, n, f->partial.p);
+    sgn::count_launch();
     k_dot_final<<<B, 32, 0, st>>>(f->partial.p, S, step, tol, it);
   };
   // vectors: bb = b, bx = x, br = r, brh = r_hat, bp = p, bv = v, bs = s, bt = t,
@@ -913,8 +924,10 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
   dot(f->bb.p, f->bb.p, nullptr, nullptr, 0, 0);                                   // bnorm
   if ((rc = launch_solve(f, f->bb.p, f->bx.p, flags, st))) return rc;              // x0
   if ((rc = launch_spmv(f, d_values, values_stride, f->bx.p, f->bscr.p, flags, st))) return rc;
+  sgn::count_launch();
   k_vec<<<vg, 256, 0, st>>>(0, S, n, f->btmp.p, f->bb.p, f->bscr.p, nullptr, nullptr, nullptr);
   dot(f->btmp.p, f->btmp.p, nullptr, nullptr, 1, 0);                               // res0
+  sgn::count_launch();
   k_vec<<<vg, 256, 0, st>>>(9, S, n, f->bbest.p, f->bx.p, nullptr, nullptr, nullptr, nullptr);
   std::vector<BiState> hs(B);
   auto read_state = [&]() -> int {
@@ -927,24 +940,31 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
   for (auto& h : hs) any |= (h.active != 0);
   if (any && max_iters > 0) {
     if ((rc = launch_solve(f, f->btmp.p, f->br.p, flags, st))) return rc;          // r = M^-1(b-Ax0)
+    sgn::count_launch();
     k_vec<<<vg, 256, 0, st>>>(4, S, n, f->brh.p, f->br.p, nullptr, nullptr, nullptr, nullptr);
     CUDA_TRY(cudaMemsetAsync(f->bp.p, 0, N * sizeof(double), st));
     CUDA_TRY(cudaMemsetAsync(f->bv.p, 0, N * sizeof(double), st));
     for (int it = 1; it <= max_iters; ++it) {
       dot(f->brh.p, f->br.p, nullptr, nullptr, 2, it);                             // rho, beta
+      sgn::count_launch();
       k_vec<<<vg, 256, 0, st>>>(1, S, n, f->bp.p, f->br.p, f->bv.p, nullptr, nullptr, nullptr);
       if ((rc = launch_spmv(f, d_values, values_stride, f->bp.p, f->bscr.p, flags, st))) return rc;
       if ((rc = launch_solve(f, f->bscr.p, f->bv.p, flags, st))) return rc;        // v = M^-1 A p
       dot(f->brh.p, f->bv.p, nullptr, nullptr, 3, it);                             // alpha
+      sgn::count_launch();
       k_vec<<<vg, 256, 0, st>>>(2, S, n, f->bs.p, f->br.p, f->bv.p, nullptr, nullptr, nullptr);
       if ((rc = launch_spmv(f, d_values, values_stride, f->bs.p, f->bscr.p, flags, st))) return rc;
       if ((rc = launch_solve(f, f->bscr.p, f->bt.p, flags, st))) return rc;        // t = M^-1 A s
       dot(f->bt.p, f->bt.p, f->bt.p, f->bs.p, 4, it);                              // omega
+      sgn::count_launch();
       k_vec<<<vg, 256, 0, st>>>(3, S, n, f->bx.p, f->bp.p, f->bs.p, f->bt.p, f->br.p, nullptr);
       if ((rc = launch_spmv(f, d_values, values_stride, f->bx.p, f->bscr.p, flags, st))) return rc;
+      sgn::count_launch();
       k_vec<<<vg, 256, 0, st>>>(0, S, n, f->btmp.p, f->bb.p, f->bscr.p, nullptr, nullptr, nullptr);
       dot(f->btmp.p, f->btmp.p, nullptr, nullptr, 5, it);                          // true residual
+      sgn::count_launch();
       k_vec<<<vg, 256, 0, st>>>(7, S, n, f->bbest.p, f->bx.p, nullptr, nullptr, nullptr, nullptr);
+      sgn::count_launch();
       k_clear_reason<<<B, 32, 0, st>>>(S);
       if ((rc = read_state())) return rc;
       bool act = false;
@@ -952,6 +972,7 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
       if (!act) break;
     }
   }
+  sgn::count_launch();
   k_select<<<vg, 256, 0, st>>>(S, n, f->bx.p, f->bbest.p, d_sol);
   CUDA_TRY(cudaGetLastError());
   if ((rc = read_state())) return rc;

@@ -75,6 +75,10 @@ struct Symbolic {
 
 std::string& last_error();
 
+// number of kernel launches issued by this library (gpu_launches evidence for bench.py)
+void count_launch(int64_t n = 1);
+int64_t launch_count();
+
 // returns 0 ok, 1 singular (pivot_index set), 5 invalid
 int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index);
 

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -27,6 +28,10 @@ std::string& last_error() {
   static thread_local std::string e;
   return e;
 }
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 namespace {
 
@@ -646,7 +651,8 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   }
 
   // stabilization kind per position
-  s.kind_pos.assign(n, 0);
+  // generic mode: every diagonal takes +eps_x (tau-regularized Newton, forward.py:171-186)
+  s.kind_pos.assign(n, s.pair_mode ? 0 : 1);
   if (s.pair_mode) {
     for (int64_t q = 0; q < n; ++q) {
       int64_t u = s.perm[q];

@@ -1,0 +1,176 @@
+// Small batched vector kernels of the SGN direction / forward-solve pipeline (sm_100a).
+//
+// Deterministic (fixed-order, one CTA per instance) reductions for energies,
+// objectives, norms and dots; the least-squares objective terms of the problem
+// contract (reference sensitivity.py:83-93); and the adjoint-gradient assembly
+// g = df/dp + Gp^T lam, lam = -Gx^{-T} df/dx (reference sensitivity.py:181-198) from a
+// leading-block KKT solve, producing the SGN right-hand side (0, -g, 0)
+// (sensitivity.py:245-256).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <algorithm>
+#include <string>
+
+#include "../../include/sgn_b200.h"
+#include "sgn_internal.h"
+
+namespace {
+
+constexpr int kRed = 512;
+
+template <int OP>  // 0 sum, 1 dot, 2 max-abs
+__global__ void __launch_bounds__(kRed)
+k_reduce(int64_t n, const double* __restrict__ a, const double* __restrict__ b, int64_t stride,
+         double* __restrict__ out) {
+  __shared__ double sh[kRed];
+  const int inst = blockIdx.x;
+  const double* ab = a + (int64_t)inst * stride;
+  const double* bb = b ? b + (int64_t)inst * stride : nullptr;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += kRed) {
+    const double v = ab[i];
+    if (OP == 0) acc += v;
+    else if (OP == 1) acc += v * bb[i];
+    else acc = fmax(acc, fabs(v));
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kRed / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      if (OP == 2) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
+      else sh[threadIdx.x] += sh[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[inst] = sh[0];
+}
+
+__global__ void k_axpy(int64_t n, const double* __restrict__ alpha, const double* __restrict__ x,
+                       const double* __restrict__ y, double* __restrict__ out, int64_t stride) {
+  const int b = blockIdx.y;
+  const double a = alpha[b];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = (int64_t)b * stride + i;
+    out[k] = y[k] + a * x[k];
+  }
+}
+
+// f vector (KKT order): x block = w_t (x_t - target) at target dofs, p block = w_reg p,
+// lambda block 0; objective per instance = 0.5 sum w r^2
+__global__ void __launch_bounds__(kRed)
+k_lsq(int64_t n_x, int64_t n_p, int64_t nt, const int64_t* __restrict__ tdofs,
+      const double* __restrict__ tvals, int64_t tstride, double w_t, double w_reg,
+      const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ vec,
+      double* __restrict__ fobj) {
+  __shared__ double sh[kRed];
+  const int b = blockIdx.x;
+  const int64_t dim = 2 * n_x + n_p;
+  double* v = vec ? vec + (int64_t)b * dim : nullptr;
+  const double* xb = x + (int64_t)b * n_x;
+  const double* pb = p + (int64_t)b * n_p;
+  if (v) for (int64_t i = threadIdx.x; i < dim; i += kRed) if (i < n_x || i >= n_x + n_p) v[i] = 0.0;
+  __syncthreads();
+  double acc = 0.0;
+  for (int64_t t = threadIdx.x; t < nt; t += kRed) {
+    const int64_t d = tdofs[t];
+    const double r = xb[d] - tvals[(int64_t)b * tstride + t];
+    acc += w_t * r * r;
+    if (v) v[d] = w_t * r;
+  }
+  for (int64_t j = threadIdx.x; j < n_p; j += kRed) {
+    const double pj = pb[j];
+    acc += w_reg * pj * pj;
+    if (v) v[n_x + j] = w_reg * pj;
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kRed / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && fobj) fobj[b] = 0.5 * sh[0];
+}
+
+// mode 0: v = (0, 0, src_lambda)
+// mode 1: g = fvec_p - kv_p ; rhs = (0, -g, 0) ; grad[b] = g
+__global__ void k_adjoint(int mode, int64_t n_x, int64_t n_p, const double* __restrict__ src,
+                          const double* __restrict__ fvec, double* __restrict__ out,
+                          double* __restrict__ grad) {
+  const int b = blockIdx.y;
+  const int64_t dim = 2 * n_x + n_p;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dim; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = (int64_t)b * dim + i;
+    const bool in_p = (i >= n_x && i < n_x + n_p);
+    if (mode == 0) {
+      out[k] = (i >= n_x + n_p) ? src[k] : 0.0;
+    } else {
+      if (in_p) {
+        const double g = fvec[k] - src[k];
+        out[k] = -g;
+        if (grad) grad[(int64_t)b * n_p + (i - n_x)] = g;
+      } else {
+        out[k] = 0.0;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+#define VEC_CHECK()                                                                \
+  do {                                                                             \
+    cudaError_t _e = cudaGetLastError();                                           \
+    if (_e != cudaSuccess) {                                                       \
+      sgn::last_error() = std::string("vector kernel: ") + cudaGetErrorString(_e); \
+      return SGN_CUDA_ERROR;                                                       \
+    }                                                                              \
+  } while (0)
+
+extern "C" {
+
+int sgn_reduce(int32_t op, int64_t n, int32_t batch, const double* d_a, const double* d_b,
+               int64_t stride, double* d_out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (op) {
+    case 0: sgn::count_launch(); k_reduce<0><<<batch, kRed, 0, st>>>(n, d_a, nullptr, stride, d_out); break;
+    case 1: sgn::count_launch(); k_reduce<1><<<batch, kRed, 0, st>>>(n, d_a, d_b, stride, d_out); break;
+    case 2: sgn::count_launch(); k_reduce<2><<<batch, kRed, 0, st>>>(n, d_a, nullptr, stride, d_out); break;
+    default: sgn::last_error() = "bad reduce op"; return SGN_INVALID;
+  }
+  VEC_CHECK();
+  return SGN_OK;
+}
+
+int sgn_axpy(int64_t n, int32_t batch, const double* d_alpha, const double* d_x, const double* d_y,
+             double* d_out, int64_t stride, void* stream) {
+  if (n == 0) return SGN_OK;
+  const dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 1024), batch);
+  sgn::count_launch();
+  k_axpy<<<g, 256, 0, (cudaStream_t)stream>>>(n, d_alpha, d_x, d_y, d_out, stride);
+  VEC_CHECK();
+  return SGN_OK;
+}
+
+int sgn_lsq_terms(int32_t batch, int64_t n_x, int64_t n_p, int64_t nt, const int64_t* d_tdofs,
+                  const double* d_tvals, int64_t tstride, double w_t, double w_reg,
+                  const double* d_x, const double* d_p, double* d_vec, double* d_fobj, void* stream) {
+  sgn::count_launch();
+  k_lsq<<<batch, kRed, 0, (cudaStream_t)stream>>>(n_x, n_p, nt, d_tdofs, d_tvals, tstride, w_t, w_reg,
+                                                  d_x, d_p, d_vec, d_fobj);
+  VEC_CHECK();
+  return SGN_OK;
+}
+
+int sgn_adjoint_step(int32_t mode, int32_t batch, int64_t n_x, int64_t n_p, const double* d_src,
+                     const double* d_fvec, double* d_out, double* d_grad, void* stream) {
+  const int64_t dim = 2 * n_x + n_p;
+  const dim3 g((unsigned)std::min<int64_t>((dim + 255) / 256, 1024), batch);
+  sgn::count_launch();
+  k_adjoint<<<g, 256, 0, (cudaStream_t)stream>>>(mode, n_x, n_p, d_src, d_fvec, d_out, d_grad);
+  VEC_CHECK();
+  return SGN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,484 @@
+"""Device-resident SGN pipeline for element-mesh design problems (batched).
+
+Host side (once per mesh, NumPy): free-dof maps, the structural KKT pattern in the
+reference block order (x, p, lambda) (reference sparse.py:165-194), the sorted
+element-to-nonzero contribution lists (atomic-free assembly), the Gx-only pattern of
+the forward Newton solve, and the symbolic analyses (native, ``device.Symbolic``).
+
+Device side (per direction, our CUDA kernels only; torch = allocation/plumbing):
+
+  gather x,p -> positions   | sgn_gather_values
+  element blocks            | sgn_element_derivs   (d2E/dx2, d2E/dx dX; forward.py:61-111 analog)
+  KKT values                | sgn_gather_values    (gn_blocks + assemble_sgn + stack: sensitivity.py:205-266)
+  LDL^T of K + shift        | sgn_factor_numeric   (linear_solvers.py:87,111-127)
+  adjoint gradient          | sgn_solve_refined(LEADING) + sgn_spmv + sgn_adjoint_step (sensitivity.py:181-198)
+  refined KKT solve         | sgn_solve_refined    (linear_solvers.py:130-211)
+
+The forward equilibrium (``simulate``) is the reference's damped, tau-regularized
+Newton with energy backtracking (forward.py:135-203) on the same element kernels.
+"""
+from __future__ import annotations
+
+import math
+import time
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib, ptr
+from .device import DeviceFactor, symbolic_for
+from .errors import DimensionMismatch, ForwardSimFailure, NoConvergence
+
+ELEM_CODES = {"spring": _lib.SGN_ELEM_SPRING, "tri": _lib.SGN_ELEM_NH_TRI, "tet": _lib.SGN_ELEM_NH_TET}
+
+
+def _csr_from_lists(n_rows, rows, *cols):
+    """Stable sort of (rows, cols...) by row -> (ptr, cols...)."""
+    order = np.argsort(rows, kind="stable")
+    counts = np.bincount(rows, minlength=n_rows)
+    ptr_ = np.zeros(n_rows + 1, dtype=np.int64)
+    np.cumsum(counts, out=ptr_[1:])
+    return (ptr_,) + tuple(np.ascontiguousarray(c[order]) for c in cols)
+
+
+class MeshPlan:
+    """Host precomputation for one mesh / parameterization (shared by all instances)."""
+
+    def __init__(self, X0, conn, kind, fixed_verts, pmap, target_dofs, w_target, w_reg,
+                 f_ext=None, rest_base=None):
+        self.X0 = np.asarray(X0, dtype=np.float64)
+        self.n_v, self.d = self.X0.shape
+        self.conn = np.asarray(conn, dtype=np.int64)
+        self.kind = kind
+        self.elem_code = ELEM_CODES[kind] + (100 * self.d if kind == "spring" else 0)
+        self.n_e, self.nv_el = self.conn.shape
+        self.nd = self.nv_el * self.d
+        d = self.d
+        fixed = np.zeros(self.n_v, bool)
+        fixed[np.asarray(fixed_verts, dtype=np.int64)] = True
+        self.free_verts = np.flatnonzero(~fixed)
+        self.free_dofs = (self.free_verts[:, None] * d + np.arange(d)[None, :]).ravel()
+        self.n_x = int(self.free_dofs.size)
+        self.n_dof = self.n_v * d
+        self.dof_to_x = -np.ones(self.n_dof, dtype=np.int64)
+        self.dof_to_x[self.free_dofs] = np.arange(self.n_x)
+        pm_dof, pm_p, pm_coef = (np.asarray(a) for a in pmap)
+        pm_dof, pm_p, pm_coef = pm_dof.astype(np.int64), pm_p.astype(np.int64), pm_coef.astype(np.float64)
+        self.n_p = int(pm_p.max()) + 1 if pm_p.size else 0
+        self.target_dofs = np.asarray(target_dofs, dtype=np.int64)
+        self.w_target, self.w_reg = float(w_target), float(w_reg)
+        self.f_ext = np.zeros(self.n_dof) if f_ext is None else np.asarray(f_ext, dtype=np.float64)
+        self.dim = 2 * self.n_x + self.n_p
+        n_x, n_p = self.n_x, self.n_p
+        nd = self.nd
+        el_dofs = (self.conn[:, :, None] * d + np.arange(d)[None, None, :]).reshape(self.n_e, nd)
+        self.el_dofs = el_dofs
+
+        # positions: pos[dof] = X0[dof] (fixed) | x[dof_to_x] (free)
+        is_free = self.dof_to_x >= 0
+        self.pos_base = np.where(is_free, 0.0, self.X0.ravel())
+        self.pos_ptr = np.zeros(self.n_dof + 1, dtype=np.int64)
+        np.cumsum(is_free.astype(np.int64), out=self.pos_ptr[1:])
+        self.pos_idx = self.dof_to_x[is_free].astype(np.int64)
+        # rest: X[dof] = X0[dof] + sum coef * p
+        self.rest_ptr, self.rest_idx, self.rest_coef = _csr_from_lists(self.n_dof, pm_dof, pm_p, pm_coef)
+        self.rest_base = (self.X0.ravel().copy() if rest_base is None
+                          else np.asarray(rest_base, dtype=np.float64).ravel().copy())
+
+        # element-local index tables
+        ea = np.repeat(np.arange(nd), nd)     # row (deformed dof) local index
+        eb = np.tile(np.arange(nd), nd)       # col local index
+        e_all = np.repeat(np.arange(self.n_e), nd * nd)
+        r_dof = el_dofs[:, ea].ravel()
+        c_dof = el_dofs[:, eb].ravel()
+        loc = np.tile(ea * nd + eb, self.n_e)
+        hidx = e_all * nd * nd + loc                      # index into hess buffer
+        midx = self.n_e * nd * nd + hidx                  # index into mixed buffer
+        rx, cx = self.dof_to_x[r_dof], self.dof_to_x[c_dof]
+
+        # --- KKT structural entries + contributions (reference block order) ------------
+        oL = n_x + n_p
+        rows, cols, src, coef = [], [], [], []
+        keep = (rx >= 0) & (cx >= 0)                      # Gx block and its transpose
+        gx_r, gx_c, gx_s = rx[keep], cx[keep], hidx[keep]
+        rows += [oL + gx_r, gx_c]
+        cols += [gx_c, oL + gx_r]
+        src += [gx_s, gx_s]
+        coef += [np.ones(gx_s.size), np.ones(gx_s.size)]
+        # Gp block: row free dof, rest col dof -> p entries
+        rp = self.rest_ptr
+        cnt = (rp[c_dof + 1] - rp[c_dof]) * (rx >= 0)
+        sel = np.flatnonzero(cnt)
+        if sel.size:
+            rep = cnt[sel]
+            base_t = np.repeat(sel, rep)
+            starts = np.zeros(rep.size, dtype=np.int64)
+            np.cumsum(rep[:-1], out=starts[1:])
+            offs = np.arange(int(rep.sum()), dtype=np.int64) - np.repeat(starts, rep)
+            kk = rp[c_dof[base_t]] + offs
+            pj = self.rest_idx[kk]
+            pc = self.rest_coef[kk]
+            gr = rx[base_t]
+            ms = midx[base_t]
+            rows += [oL + gr, n_x + pj]
+            cols += [n_x + pj, oL + gr]
+            src += [ms, ms]
+            coef += [pc, pc]
+        rows = np.concatenate(rows); cols = np.concatenate(cols)
+        src = np.concatenate(src); coef = np.concatenate(coef)
+        # A diagonal (targets) and C diagonal (regularizer) as structural entries w/o buffer terms
+        a_rows = np.unique(self.target_dofs)
+        c_rows = np.arange(n_p) + n_x if self.w_reg > 0.0 else np.zeros(0, np.int64)
+        diag_rows = np.concatenate([a_rows, c_rows])
+        all_r = np.concatenate([rows, diag_rows])
+        all_c = np.concatenate([cols, diag_rows])
+        key = all_c * self.dim + all_r                    # CSC order: by column, then row
+        ukey, inv = np.unique(key, return_inverse=True)
+        self.K_indices = (ukey % self.dim).astype(np.int64)
+        kcols = ukey // self.dim
+        self.K_indptr = np.zeros(self.dim + 1, dtype=np.int64)
+        np.cumsum(np.bincount(kcols, minlength=self.dim), out=self.K_indptr[1:])
+        self.nnz = int(ukey.size)
+        nz_of = inv[:rows.size]
+        self.K_ptr, self.K_src, self.K_coef = _csr_from_lists(self.nnz, nz_of, src, coef)
+        base = np.zeros(self.nnz)
+        tcount = np.bincount(self.target_dofs, minlength=n_x)
+        dpos = inv[rows.size:rows.size + a_rows.size]
+        base[dpos] = self.w_target * tcount[a_rows]
+        if c_rows.size:
+            base[inv[rows.size + a_rows.size:]] = self.w_reg
+        self.K_base = base
+
+        # --- Gx-only pattern for the forward Newton (generic 1x1 mode) -------------------
+        gkey = gx_c * n_x + gx_r
+        gu, ginv = np.unique(gkey, return_inverse=True)
+        self.G_indices = (gu % n_x).astype(np.int64)
+        self.G_indptr = np.zeros(n_x + 1, dtype=np.int64)
+        np.cumsum(np.bincount(gu // n_x, minlength=n_x), out=self.G_indptr[1:])
+        self.G_nnz = int(gu.size)
+        self.G_ptr, self.G_src = _csr_from_lists(self.G_nnz, ginv, gx_s)
+        gdiag = np.flatnonzero((gu % n_x) == (gu // n_x))
+        self.G_diag = gdiag.astype(np.int64)               # nnz positions of the diagonal
+
+        # --- gradient gather: free dof <- element-gradient entries ------------------------
+        g_dof = el_dofs.ravel()
+        g_x = self.dof_to_x[g_dof]
+        gsel = np.flatnonzero(g_x >= 0)
+        self.grad_ptr, self.grad_src = _csr_from_lists(n_x, g_x[gsel], gsel.astype(np.int64))
+        self.grad_base = self.f_ext[self.free_dofs].copy()
+
+
+def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = True, events=None):
+    """factor -> adjoint gradient -> refined KKT solve on an object exposing
+    kfac, kvals, fvec, sol_adj, tmp, rhs, sol, grad, batch, n_x, n_p, stab.
+
+    ``events``: optional list of >= 3 torch CUDA events recorded after the numeric
+    factorization, after the adjoint gradient and after the KKT solve (bench.py).
+    """
+    st = _lib.stream_handle()
+    n_x, n_p = eng.n_x, eng.n_p
+    t1 = time.perf_counter()
+    eng.kfac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda, st)
+    if events is not None:
+        events[0].record()
+    eng.kfac.check(st)
+    t2 = time.perf_counter()
+    if timings is not None:
+        timings["factor_s"] = t2 - t1
+    tol, mi = eng.stab.refine_tolerance, eng.stab.max_refine_iters
+    rc, res_a, it_a = eng.kfac.solve_refined(eng.kvals, eng.fvec, eng.sol_adj, tol, mi, True, st)
+    check(lib().sgn_adjoint_step(0, eng.batch, n_x, n_p, ptr(eng.sol_adj), None, ptr(eng.tmp), None, st))
+    eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, st)
+    check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
+                                 ptr(eng.grad), st))
+    eng.rhs.copy_(eng.tmp)
+    if events is not None:
+        events[1].record()
+    if timings is not None:
+        timings["adjoint_res"] = res_a
+        timings["adjoint_iters"] = it_a
+    if not need_direction:
+        return None, None
+    rc2, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
+    if events is not None:
+        events[2].record()
+    if timings is not None:
+        timings["solve_s"] = time.perf_counter() - t2
+        timings["main_iters"] = its
+    if rc2 == _lib.SGN_NO_CONVERGENCE:
+        best = eng.sol.cpu().numpy()
+        raise NoConvergence(f"BiCGSTAB refinement stalled at relative residual {res.max():.3e}",
+                            residual=float(res.max()), iterations=int(its.max()),
+                            best=best[0] if eng.batch == 1 else best)
+    return res, its
+
+
+class DeviceEngine:
+    """Batched device state + the SGN direction and forward Newton for one MeshPlan."""
+
+    def __init__(self, plan: MeshPlan, params, tvals, batch: int = 1, stab=None):
+        torch = _lib.require_cuda()
+        self.torch = torch
+        self.plan = plan
+        self.batch = B = int(batch)
+        dev = "cuda"
+        f64, i64 = torch.float64, torch.int64
+        T = lambda a, dt=f64: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
+        pl = plan
+        self.conn = T(pl.conn.astype(np.int32), torch.int32)
+        self.params = T(np.asarray(params, dtype=np.float64).reshape(B, -1))
+        self.tvals = T(np.asarray(tvals, dtype=np.float64).reshape(B, -1))
+        self.tdofs = T(pl.target_dofs, i64)
+        self.pos_base, self.pos_ptr, self.pos_idx = T(pl.pos_base), T(pl.pos_ptr, i64), T(pl.pos_idx, i64)
+        self.rest_base, self.rest_ptr = T(pl.rest_base), T(pl.rest_ptr, i64)
+        self.rest_idx, self.rest_coef = T(pl.rest_idx, i64), T(pl.rest_coef)
+        self.K_base, self.K_ptr = T(pl.K_base), T(pl.K_ptr, i64)
+        self.K_src, self.K_coef = T(pl.K_src, i64), T(pl.K_coef)
+        self.G_ptr, self.G_src = T(pl.G_ptr, i64), T(pl.G_src, i64)
+        self.G_diag = T(pl.G_diag, i64)
+        self.grad_base, self.grad_ptr, self.grad_src = T(pl.grad_base), T(pl.grad_ptr, i64), T(pl.grad_src, i64)
+        self.f_ext = T(pl.f_ext)
+        nd2 = pl.n_e * pl.nd * pl.nd
+        z = lambda *s: torch.zeros(*s, dtype=f64, device=dev)
+        self.x = z(B, pl.n_x)
+        self.p = z(B, pl.n_p)
+        self.pos = z(B, pl.n_dof)
+        self.rest = z(B, pl.n_dof)
+        self.ebuf = z(B, 2 * nd2)             # [hess | mixed]
+        self.egrad = z(B, pl.n_e * pl.nd)
+        self.eener = z(B, pl.n_e)
+        self.kvals = z(B, pl.nnz)
+        self.gvals = z(B, pl.G_nnz)
+        self.fvec = z(B, pl.dim)
+        self.rhs = z(B, pl.dim)
+        self.sol = z(B, pl.dim)
+        self.sol_adj = z(B, pl.dim)
+        self.tmp = z(B, pl.dim)
+        self.grad = z(B, pl.n_p)
+        self.fobj = z(B)
+        self.scal = z(8, B)
+        self.gx = z(B, pl.n_x)
+        self.kdir = z(B, pl.n_x)
+        self.xtry = z(B, pl.n_x)
+        self.n_x, self.n_p = pl.n_x, pl.n_p
+        self.ksym = symbolic_for(pl.dim, pl.K_indptr, pl.K_indices, pl.n_x, pl.n_p, pl.n_x)
+        self.kfac = DeviceFactor(self.ksym, B)
+        self._gfac = None
+        from .linear_solvers import StabilizationConfig
+        self.stab = stab or StabilizationConfig()
+
+    # -- small helpers ---------------------------------------------------------------
+    @property
+    def stream(self) -> int:
+        return _lib.stream_handle()
+
+    def _gather(self, n_out, base, base_stride, ptr_, idx, coef, buf, buf_stride, out, out_stride):
+        check(lib().sgn_gather_values(n_out, self.batch, ptr(base), base_stride, ptr(ptr_), ptr(idx),
+                                      ptr(coef), ptr(buf), buf_stride, ptr(out), out_stride, self.stream))
+
+    def load(self, x=None, p=None):
+        torch = self.torch
+        if x is not None:
+            self.x.copy_(torch.as_tensor(np.asarray(x, dtype=np.float64).reshape(self.batch, -1)))
+        if p is not None:
+            self.p.copy_(torch.as_tensor(np.asarray(p, dtype=np.float64).reshape(self.batch, -1)))
+
+    def positions(self, x=None):
+        pl = self.plan
+        x = self.x if x is None else x
+        self._gather(pl.n_dof, self.pos_base, 0, self.pos_ptr, self.pos_idx, None, x, pl.n_x,
+                     self.pos, pl.n_dof)
+        self._gather(pl.n_dof, self.rest_base, 0, self.rest_ptr, self.rest_idx, self.rest_coef,
+                     self.p, pl.n_p, self.rest, pl.n_dof)
+
+    def element_blocks(self):
+        pl = self.plan
+        nd2 = pl.n_e * pl.nd * pl.nd
+        check(lib().sgn_element_derivs(pl.elem_code, pl.n_e, self.batch, ptr(self.conn), ptr(self.pos),
+                                       ptr(self.rest), pl.n_dof, ptr(self.params), self.params.stride(0),
+                                       ptr(self.ebuf), ptr(self.ebuf[:, nd2:]), 2 * nd2, self.stream))
+
+    def assemble_kkt(self):
+        pl = self.plan
+        self._gather(pl.nnz, self.K_base, 0, self.K_ptr, self.K_src, self.K_coef, self.ebuf,
+                     self.ebuf.stride(0), self.kvals, pl.nnz)
+
+    # -- SGN direction (staged) ----------------------------------------------------------
+    def assemble(self):
+        """Element blocks -> KKT values, least-squares terms (fvec, fobj) at (x, p)."""
+        pl = self.plan
+        self.positions()
+        self.element_blocks()
+        self.assemble_kkt()
+        check(lib().sgn_lsq_terms(self.batch, pl.n_x, pl.n_p, pl.target_dofs.size, ptr(self.tdofs),
+                                  ptr(self.tvals), self.tvals.stride(0), pl.w_target, pl.w_reg,
+                                  ptr(self.x), ptr(self.p), ptr(self.fvec), ptr(self.fobj), self.stream))
+
+    def direction(self, timings: dict | None = None):
+        """SGN direction at the current (x, p) of every instance (solution in self.sol).
+
+        Returns (rel_res[batch], iters[batch]); raises NoConvergence like
+        solve_kkt_stabilized when any instance's refinement stalls.
+        """
+        sync = self.torch.cuda.synchronize
+        t0 = time.perf_counter()
+        self.assemble()
+        if timings is not None:
+            sync()
+            timings["assemble_s"] = time.perf_counter() - t0
+        return sgn_solve_stages(self, timings)
+
+    def split(self):
+        pl = self.plan
+        s = self.sol
+        return s[:, :pl.n_x], s[:, pl.n_x:pl.n_x + pl.n_p], s[:, pl.n_x + pl.n_p:]
+
+    # -- objective ---------------------------------------------------------------------
+    def objective(self, x=None):
+        pl = self.plan
+        x = self.x if x is None else x
+        check(lib().sgn_lsq_terms(self.batch, pl.n_x, pl.n_p, pl.target_dofs.size, ptr(self.tdofs),
+                                  ptr(self.tvals), self.tvals.stride(0), pl.w_target, pl.w_reg,
+                                  ptr(x), ptr(self.p), None, ptr(self.fobj), self.stream))
+        return self.fobj
+
+    # -- forward statics (forward.py:135-203) --------------------------------------------
+    def _energy_grad(self, x, want_grad=True):
+        pl = self.plan
+        st = self.stream
+        self._gather(pl.n_dof, self.pos_base, 0, self.pos_ptr, self.pos_idx, None, x, pl.n_x,
+                     self.pos, pl.n_dof)
+        check(lib().sgn_element_energy_grad(pl.elem_code, pl.n_e, self.batch, ptr(self.conn), ptr(self.pos),
+                                            ptr(self.rest), pl.n_dof, ptr(self.params), self.params.stride(0),
+                                            ptr(self.eener), ptr(self.egrad) if want_grad else 0,
+                                            pl.n_e * pl.nd, st))
+        check(lib().sgn_reduce(0, pl.n_e, self.batch, ptr(self.eener), None, pl.n_e, ptr(self.scal[0]), st))
+        check(lib().sgn_reduce(1, pl.n_dof, self.batch, ptr(self.f_ext.expand(self.batch, -1).contiguous()),
+                               ptr(self.pos), pl.n_dof, ptr(self.scal[1]), st))
+        if want_grad:
+            self._gather(pl.n_x, self.grad_base, 0, self.grad_ptr, self.grad_src, None, self.egrad,
+                         pl.n_e * pl.nd, self.gx, pl.n_x)
+
+    def _hessian(self):
+        pl = self.plan
+        self.element_blocks()
+        self._gather(pl.G_nnz, None, 0, self.G_ptr, self.G_src, None, self.ebuf, self.ebuf.stride(0),
+                     self.gvals, pl.G_nnz)
+
+    @property
+    def gfac(self):
+        if self._gfac is None:
+            pl = self.plan
+            self.gsym = symbolic_for(pl.n_x, pl.G_indptr, pl.G_indices)
+            self._gfac = DeviceFactor(self.gsym, self.batch)
+        return self._gfac
+
+    def simulate(self, tol: float, max_iters: int = 200):
+        """Newton with energy backtracking from the current self.x (batch == 1 path)."""
+        if self.batch != 1:
+            return self.simulate_batched(tol, max_iters)
+        torch = self.torch
+        pl = self.plan
+        st = self.stream
+        n = pl.n_x
+        self.positions()              # rest positions for the current p
+        for _ in range(max_iters):
+            self._energy_grad(self.x)
+            ginf = torch.empty(1, dtype=torch.float64, device="cuda")
+            check(lib().sgn_reduce(2, n, 1, ptr(self.gx), None, n, ptr(ginf), st))
+            g_inf, e_el, e_lin = float(ginf.item()), float(self.scal[0, 0].item()), float(self.scal[1, 0].item())
+            if g_inf <= tol:
+                return
+            e0 = e_el + e_lin
+            self._hessian()
+            trace = float(self.gvals[0, self.G_diag].sum().item()) if pl.G_diag.size else 0.0
+            step = self._newton_step(trace, n, False)
+            accepted = False
+            for _ in range(8):
+                alpha = self._backtrack(step, e0)
+                if alpha is not None:
+                    self.x.copy_(self.xtry)
+                    accepted = True
+                    break
+                step = self._newton_step(trace, n, True)
+            if not accepted:
+                raise ForwardSimFailure(f"static solve: line search failed (|g|inf={g_inf:.3e})")
+        raise ForwardSimFailure(f"static solve: no convergence in {max_iters} iterations")
+
+    def _newton_step(self, trace, n, bias):
+        """tau-regularized Newton direction into self.kdir (forward.py:171-186)."""
+        torch = self.torch
+        st = self.stream
+        tau0 = 1e-6 * abs(trace) / max(n, 1) + 1e-12
+        tau = tau0 * 1e6 if bias else 0.0
+        neg = torch.neg(self.gx)
+        dots = torch.empty(1, dtype=torch.float64, device="cuda")
+        from .errors import SingularMatrix
+        for _ in range(60):
+            try:
+                self.gfac.numeric(self.gvals, tau, 0.0, st)
+                self.gfac.check(st)
+                self.gfac.solve(neg, self.kdir, False, st)
+                check(lib().sgn_reduce(1, n, 1, ptr(self.gx), ptr(self.kdir), n, ptr(dots), st))
+                gd = float(dots.item())
+                if gd < 0 and bool(torch.isfinite(self.kdir).all().item()):
+                    return self.kdir
+            except SingularMatrix:
+                pass
+            tau = tau0 if tau == 0.0 else tau * 10.0
+        self.kdir.copy_(neg)
+        return self.kdir
+
+    def _backtrack(self, step, e0, c1=1e-4, factor=0.5, max_bt=60):
+        """Armijo on the energy with the reference's float slack (forward.py:189-203)."""
+        torch = self.torch
+        st = self.stream
+        n = self.plan.n_x
+        slope_t = torch.empty(1, dtype=torch.float64, device="cuda")
+        check(lib().sgn_reduce(1, n, 1, ptr(self.gx), ptr(step), n, ptr(slope_t), st))
+        slope = float(slope_t.item())
+        slack = 4e-15 * abs(e0)
+        alpha = 1.0
+        a_t = torch.empty(1, dtype=torch.float64, device="cuda")
+        for _ in range(max_bt):
+            a_t.fill_(alpha)
+            check(lib().sgn_axpy(n, 1, ptr(a_t), ptr(step), ptr(self.x), ptr(self.xtry), n, st))
+            self._energy_grad(self.xtry, want_grad=False)
+            et = float(self.scal[0, 0].item()) + float(self.scal[1, 0].item())
+            if math.isfinite(et) and et <= e0 + c1 * alpha * slope + slack:
+                return alpha
+            alpha *= factor
+        return None
+
+    def simulate_batched(self, tol, max_iters=200):
+        raise NotImplementedError("batched forward statics: use per-instance engines")
+
+
+class HostKKT:
+    """Device solve stages for a KKT assembled on the host by a plugin problem.
+
+    Generic (user) problems evaluate their Jacobians on the CPU (their own code); the
+    stacked KKT values and the least-squares gradient are uploaded and the factor /
+    adjoint / refined solve run on the device exactly as for the native problems.
+    """
+
+    def __init__(self, K, n_x: int, n_p: int, stab):
+        torch = _lib.require_cuda()
+        from .linear_solvers import _symmetric_pattern
+        indptr, indices, src = _symmetric_pattern(K)
+        self.torch = torch
+        self.batch, self.n_x, self.n_p, self.stab = 1, int(n_x), int(n_p), stab
+        dim = 2 * self.n_x + self.n_p
+        self.ksym = symbolic_for(dim, indptr, indices, self.n_x, self.n_p, self.n_x)
+        self.kfac = DeviceFactor(self.ksym, 1)
+        vals = np.where(src >= 0, K.data[np.maximum(src, 0)], 0.0)
+        z = lambda m: torch.zeros(1, m, dtype=torch.float64, device="cuda")
+        self.kvals = torch.as_tensor(vals, device="cuda").reshape(1, -1)
+        self.fvec, self.sol_adj, self.tmp, self.rhs, self.sol = (z(dim) for _ in range(5))
+        self.grad = z(self.n_p)
+
+    def set_fvec(self, fx, fp):
+        v = np.zeros(2 * self.n_x + self.n_p)
+        v[:self.n_x] = fx
+        v[self.n_x:self.n_x + self.n_p] = fp
+        self.fvec.copy_(self.torch.as_tensor(v).reshape(1, -1))

@@ -1,0 +1,217 @@
+"""Drop-in SGN search direction and outer loop (reference optimize.py), GPU-resident.
+
+Same names/signatures/records as the reference (pkg/src/sgnopt/optimize.py):
+``OptimizerConfig`` (63-80), ``SearchDirection`` (83-98), ``IterationRecord`` /
+``OptimizerRun`` (101-137), ``direction_sgn`` (155-165), ``minimize`` (353-420),
+``_line_search`` (468-488), ``_DIRECTION_FUNCS`` (338-346, "sgn" entry).
+
+For GPU-native problems one direction is: device assembly -> device LDL^T -> device
+adjoint gradient -> device refined KKT solve; the forward statics of the line search
+run on the device too (problems.ElasticDesignProblem.simulate).  Only scalars (f,
+slopes, norms) cross to the host for the Armijo decisions.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import (ForwardSimFailure, InfeasiblePoint, NoConvergence, NumericalBlowup)
+from .linear_solvers import StabilizationConfig, solve_kkt_stabilized
+from .sensitivity import _host_kkt, _is_device_problem, adjoint_gradient
+
+__all__ = ["METHODS", "CSV_HEADER", "OptimizerConfig", "SearchDirection", "IterationRecord",
+           "OptimizerRun", "direction_sgn", "minimize", "project_direction_bounds"]
+
+METHODS = ("sgn",)
+CSV_HEADER = "iter,f,grad_norm,step_len,dir_time_s,fwd_time_s,elapsed_s,lin_rel_residual"
+
+
+@dataclass
+class OptimizerConfig:
+    method: str = "sgn"
+    max_iterations: int = 100
+    gradient_tolerance: float = 1e-5
+    armijo_c1: float = 1e-4
+    backtrack_factor: float = 0.5
+    max_backtracks: int = 60
+    lbfgs_history: int = 10
+    cg_eta: float = 1e-3
+    stabilization: StabilizationConfig = field(default_factory=StabilizationConfig)
+    bound_mode: str = "none"
+
+    def __post_init__(self):
+        if self.gradient_tolerance <= 0:
+            raise ValueError("gradient tolerance must be positive")
+        if not 0.0 < self.backtrack_factor < 1.0:
+            raise ValueError("backtrack factor must lie in (0, 1)")
+
+
+@dataclass
+class SearchDirection:
+    dp: np.ndarray
+    dx: np.ndarray | None = None
+    dlam: np.ndarray | None = None
+    assemble_s: float = 0.0
+    factor_s: float = 0.0
+    solve_s: float = 0.0
+    relative_residual: float = float("nan")
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def total_s(self) -> float:
+        return self.assemble_s + self.factor_s + self.solve_s
+
+
+@dataclass
+class IterationRecord:
+    iteration: int
+    f: float
+    grad_norm: float
+    step_length: float
+    direction_time: float
+    forward_time: float
+    elapsed: float
+    lin_rel_residual: float
+
+    def csv_row(self) -> str:
+        return (f"{self.iteration},{self.f:.17g},{self.grad_norm:.17g},{self.step_length:.17g},"
+                f"{self.direction_time:.6g},{self.forward_time:.6g},{self.elapsed:.6g},"
+                f"{self.lin_rel_residual:.6g}")
+
+
+@dataclass
+class OptimizerRun:
+    method: str
+    records: list
+    termination: str
+    p: np.ndarray
+    x: np.ndarray
+
+    def f_values(self):
+        return np.array([r.f for r in self.records])
+
+    def grad_norms(self):
+        return np.array([r.grad_norm for r in self.records])
+
+    def write_csv(self, path) -> None:
+        with open(path, "w", encoding="ascii") as fh:
+            fh.write(CSV_HEADER + "\n")
+            for rec in self.records:
+                fh.write(rec.csv_row() + "\n")
+
+
+def project_direction_bounds(dp, p, lower, upper):
+    if np.any(p < lower) or np.any(p > upper):
+        raise InfeasiblePoint("parameters violate their declared bounds")
+    out = dp.copy()
+    out[(p >= upper) & (dp > 0)] = 0.0
+    out[(p <= lower) & (dp < 0)] = 0.0
+    return out
+
+
+def direction_sgn(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirection:
+    """Gauss-Newton step through the sparse saddle point (optimize.py:155-165) on the GPU.
+
+    ``grad`` is ignored, as in the reference (the gradient is recomputed by the adjoint).
+    """
+    from .engine import sgn_solve_stages
+    if _is_device_problem(prob):
+        eng = prob.engine
+        eng.stab = cfg.stabilization
+        prob._load(x, p)
+        t = {}
+        res, its = eng.direction(t)
+        sol = eng.sol[0].cpu().numpy()
+    else:
+        t0 = time.perf_counter()
+        hk, _ = _host_kkt(prob, x, p)
+        hk.stab = cfg.stabilization
+        t = {}
+        hk.torch.cuda.synchronize()
+        a_s = time.perf_counter() - t0
+        res, its = sgn_solve_stages(hk, t)
+        t["assemble_s"] = a_s
+        sol = hk.sol[0].cpu().numpy()
+    n_x, n_p = prob.n_x, prob.n_p
+    return SearchDirection(dp=sol[n_x:n_x + n_p], dx=sol[:n_x], dlam=sol[n_x + n_p:],
+                           assemble_s=t.get("assemble_s", 0.0), factor_s=t.get("factor_s", 0.0),
+                           solve_s=t.get("solve_s", 0.0), relative_residual=float(res[0]),
+                           extra={"refine_iterations": int(its[0])})
+
+
+_DIRECTION_FUNCS = {"sgn": direction_sgn}
+
+
+def _line_search(prob, p, x, f, g, dp, bounds, cfg):
+    """Armijo backtracking over forward solves (optimize.py:468-488)."""
+    alpha = 1.0
+    fwd_time = 0.0
+    for _ in range(cfg.max_backtracks + 1):
+        p_try = p + alpha * dp
+        if bounds is not None:
+            np.clip(p_try, bounds[0], bounds[1], out=p_try)
+        slope = float(g @ (p_try - p))
+        if slope < 0.0:
+            t0 = time.perf_counter()
+            try:
+                x_try = prob.simulate(p_try, x_init=x)
+            except (ForwardSimFailure, NoConvergence, NumericalBlowup):
+                x_try = None
+            fwd_time += time.perf_counter() - t0
+            if x_try is not None:
+                f_try = prob.objective(x_try, p_try)
+                if np.isfinite(f_try) and f_try <= f + cfg.armijo_c1 * slope:
+                    return True, p_try, x_try, f_try, alpha, fwd_time
+        alpha *= cfg.backtrack_factor
+    return False, None, None, None, 0.0, fwd_time
+
+
+def minimize(prob, p0, cfg: OptimizerConfig) -> OptimizerRun:
+    """Minimize f(x(p), p) with SGN directions and monotone backtracking (optimize.py:353-420)."""
+    if cfg.method not in METHODS:
+        raise ValueError(f"unknown method {cfg.method!r}; valid: {', '.join(METHODS)}")
+    t_start = time.perf_counter()
+    p = np.asarray(p0, dtype=np.float64).copy()
+    bounds = prob.bounds() if cfg.bound_mode == "project" else None
+    if bounds is not None and (np.any(p < bounds[0]) or np.any(p > bounds[1])):
+        raise InfeasiblePoint("initial parameters violate bounds")
+    t0 = time.perf_counter()
+    try:
+        x = prob.simulate(p)
+    except (NoConvergence, NumericalBlowup) as exc:
+        raise ForwardSimFailure(f"initial forward solve failed: {exc}") from exc
+    fwd_time = time.perf_counter() - t0
+    f = prob.objective(x, p)
+    g = adjoint_gradient(prob, x, p)
+    records = [IterationRecord(0, f, float(np.linalg.norm(g)), 0.0, 0.0, fwd_time,
+                               time.perf_counter() - t_start, float("nan"))]
+    termination = "max_iterations"
+    for it in range(1, cfg.max_iterations + 1):
+        if np.linalg.norm(g) <= cfg.gradient_tolerance:
+            termination = "gradient_tolerance"
+            break
+        t0 = time.perf_counter()
+        sd = _DIRECTION_FUNCS[cfg.method](prob, x, p, cfg, grad=g)
+        dir_time = time.perf_counter() - t0
+        dp = sd.dp
+        if bounds is not None:
+            dp = project_direction_bounds(dp, p, *bounds)
+            if g @ dp >= 0.0:
+                dp = project_direction_bounds(-g, p, *bounds)
+        if np.linalg.norm(dp) == 0.0:
+            termination = "stationary"
+            break
+        if g @ dp >= 0.0:
+            termination = "no_descent"
+            break
+        accepted, p_new, x_new, f_new, alpha, fwd_time = _line_search(prob, p, x, f, g, dp, bounds, cfg)
+        if not accepted:
+            termination = "line_search_failure"
+            break
+        g = adjoint_gradient(prob, x_new, p_new)
+        p, x, f = p_new, x_new, f_new
+        records.append(IterationRecord(it, f, float(np.linalg.norm(g)), alpha, dir_time, fwd_time,
+                                       time.perf_counter() - t_start, sd.relative_residual))
+    return OptimizerRun(method=cfg.method, records=records, termination=termination, p=p, x=x)

@@ -1,0 +1,261 @@
+"""GPU-native design problems implementing the reference problem contract.
+
+``ElasticDesignProblem`` satisfies the reference's ``EquilibriumProblem`` contract
+(reference pkg/src/sgnopt/sensitivity.py:29-120) -- every evaluator returns host NumPy /
+``CscMatrix`` values, computed by the device kernels -- and additionally carries a
+``DeviceEngine`` so that ``direction_sgn`` / ``minimize`` keep the whole direction,
+forward statics and line search on the GPU.
+
+Builders:
+* ``build_sheet(config, seed, instance)`` -- BASELINE configs 1 and 2 (and config-5
+  instances): neo-Hookean plane-strain sheets (definition shared with the oracle in
+  oracle/configs.py, re-derived here from the same spec function);
+* ``build_spring_bar(n_w, n_h, ...)``    -- the reference's own spring lattice
+  (problems/spring_bar.py:30-207) on the GPU element kernels.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+
+from ..engine import DeviceEngine, MeshPlan
+from ..errors import CapabilityMissing, ForwardSimFailure
+from ..sparse import CscMatrix
+
+__all__ = ["ElasticDesignProblem", "build_sheet", "build_spring_bar", "sheet_spec"]
+
+
+class ElasticDesignProblem:
+    """Static equilibrium inverse design on an element mesh, evaluated on the GPU."""
+
+    def __init__(self, X0, conn, kind, fixed_verts, pmap, target_dofs, target_vals, w_target=1.0,
+                 w_reg=0.0, E=1.0, nu=0.3, gload=0.0, stiffness=None, scale=None, tol=1e-12,
+                 f_ext=None, rest_base=None, p_offset=None, name=None, stab=None):
+        self.plan = MeshPlan(X0, conn, kind, fixed_verts, pmap, target_dofs, w_target, w_reg,
+                             f_ext=f_ext, rest_base=rest_base)
+        mu, lam = (E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu)))
+        sc = (1.0 / E) if scale is None else float(scale)
+        params = [mu, lam, gload, sc]
+        if stiffness is not None:
+            params += list(np.asarray(stiffness, dtype=np.float64))
+        self.params = np.asarray(params, dtype=np.float64)
+        self.target_vals = np.asarray(target_vals, dtype=np.float64)
+        self.engine = DeviceEngine(self.plan, self.params, self.target_vals, batch=1, stab=stab)
+        self.n_x, self.n_p = self.plan.n_x, self.plan.n_p
+        self.tol = float(tol)
+        self._x_warm = None
+        self._name = name or type(self).__name__
+        # optional affine map p -> internal offsets (spring bar uses absolute positions)
+        self.p_offset = None if p_offset is None else np.asarray(p_offset, dtype=np.float64)
+        self.w_reg = self.plan.w_reg
+
+    # -- contract basics -------------------------------------------------------------
+    @property
+    def n_c(self) -> int:
+        return self.n_x
+
+    @property
+    def name(self) -> str:
+        return self._name
+
+    def bounds(self):
+        return None
+
+    def default_parameters(self):
+        return np.zeros(self.n_p) if self.p_offset is None else self.p_offset.copy()
+
+    def _p_int(self, p):
+        p = np.asarray(p, dtype=np.float64)
+        return p if self.p_offset is None else p
+
+    def _load(self, x, p):
+        self.engine.load(x=x, p=self._p_int(p))
+
+    # -- forward simulation (GPU Newton) -----------------------------------------------
+    def simulate(self, p, x_init=None):
+        eng = self.engine
+        if x_init is not None:
+            x0 = np.asarray(x_init, dtype=np.float64)
+        elif self._x_warm is not None:
+            x0 = self._x_warm
+        else:
+            x0 = self.plan.X0.ravel()[self.plan.free_dofs]
+        self._load(x0, p)
+        eng.simulate(self.tol)
+        x = eng.x[0].cpu().numpy()
+        self._x_warm = x.copy()
+        return x
+
+    # -- constraints --------------------------------------------------------------------
+    def constraints(self, x, p):
+        self._load(x, p)
+        self.engine.positions()
+        self.engine._energy_grad(self.engine.x)
+        return self.engine.gx[0].cpu().numpy()
+
+    def kkt_values(self, x, p):
+        """Device-assembled KKT values in the structural pattern (plan.K_indptr/K_indices)."""
+        self._load(x, p)
+        self.engine.positions()
+        self.engine.element_blocks()
+        self.engine.assemble_kkt()
+        return self.engine.kvals[0].cpu().numpy()
+
+    def kkt_matrix(self, x, p) -> CscMatrix:
+        pl = self.plan
+        return CscMatrix(pl.dim, pl.dim, pl.K_indptr, pl.K_indices, self.kkt_values(x, p))
+
+    def constraint_jac_x(self, x, p) -> CscMatrix:
+        self._load(x, p)
+        self.engine.positions()
+        self.engine._hessian()
+        pl = self.plan
+        return CscMatrix(pl.n_x, pl.n_x, pl.G_indptr, pl.G_indices, self.engine.gvals[0].cpu().numpy())
+
+    def constraint_jac_p(self, x, p) -> CscMatrix:
+        pl = self.plan
+        K = self.kkt_matrix(x, p).to_scipy()
+        n_x, n_p = pl.n_x, pl.n_p
+        return CscMatrix.from_scipy(K[n_x + n_p:, n_x:n_x + n_p])
+
+    # -- least squares ------------------------------------------------------------------
+    def residuals(self, x, p):
+        pl = self.plan
+        out = [np.asarray(x)[pl.target_dofs] - self.target_vals]
+        if pl.w_reg > 0.0:
+            out.append(np.asarray(p, dtype=np.float64).copy())
+        return np.concatenate(out)
+
+    def weights(self):
+        pl = self.plan
+        w = [np.full(pl.target_dofs.size, pl.w_target)]
+        if pl.w_reg > 0.0:
+            w.append(np.full(pl.n_p, pl.w_reg))
+        return np.concatenate(w)
+
+    def residual_jac_x(self, x, p):
+        pl = self.plan
+        nt = pl.target_dofs.size
+        sel = sp.csc_matrix((np.ones(nt), (np.arange(nt), pl.target_dofs)), shape=(nt, pl.n_x))
+        if pl.w_reg > 0.0:
+            sel = sp.vstack([sel, sp.csc_matrix((pl.n_p, pl.n_x))], format="csc")
+        return CscMatrix.from_scipy(sel)
+
+    def residual_jac_p(self, x, p):
+        pl = self.plan
+        nt = pl.target_dofs.size
+        if pl.w_reg > 0.0:
+            return CscMatrix.from_scipy(sp.vstack([sp.csc_matrix((nt, pl.n_p)),
+                                                   sp.identity(pl.n_p, format="csc")], format="csc"))
+        return CscMatrix.zeros(nt, pl.n_p)
+
+    def objective(self, x, p) -> float:
+        self._load(x, p)
+        return float(self.engine.objective()[0].item())
+
+    def objective_grad_x(self, x, p):
+        return self.residual_jac_x(x, p).to_scipy().T @ (self.weights() * self.residuals(x, p))
+
+    def objective_grad_p(self, x, p):
+        return self.residual_jac_p(x, p).to_scipy().T @ (self.weights() * self.residuals(x, p))
+
+
+def sheet_spec(config: int, seed: int = 0, instance: int = 0) -> dict:
+    """BASELINE sheet spec (configs 1, 2; config-5 instances) -- see oracle/configs.py docs.
+
+    Re-implemented (not imported) so the product never depends on the oracle package;
+    tests assert the two generators agree array for array.
+    """
+    rng = np.random.default_rng(1000 * seed + instance)
+    n_w = n_h = {1: 20, 2: 100}[config]
+    E, nu = 1e5, 0.3
+    if instance > 0:
+        E = float(rng.uniform(5e4, 2e5))
+    ix, iy = np.meshgrid(np.arange(n_w), np.arange(n_h), indexing="ij")
+    X0 = np.column_stack([ix.ravel() / (n_w - 1), iy.ravel() / (n_h - 1)])
+    i, j = np.meshgrid(np.arange(n_w - 1), np.arange(n_h - 1), indexing="ij")
+    a = (i * n_h + j).ravel(); b = ((i + 1) * n_h + j).ravel()
+    c = ((i + 1) * n_h + j + 1).ravel(); dd = (i * n_h + j + 1).ravel()
+    tris = np.stack([np.column_stack([a, b, c]), np.column_stack([a, c, dd])], axis=1).reshape(-1, 3)
+    fixed = np.arange(n_h)
+    rows = np.concatenate([np.arange(n_w) * n_h, np.arange(n_w) * n_h + (n_h - 1)])
+    pm_dof = rows * 2 + 1 if config == 1 else (rows[:, None] * 2 + np.arange(2)[None, :]).ravel()
+    half = 0.01 if config == 1 else 0.005
+    nominal = 0.5 / ((n_w - 1) * (n_h - 1))
+    while True:   # same-stream redraw until every rest triangle keeps >= 20% nominal area
+        p0 = rng.uniform(-half, half, pm_dof.size)
+        X = X0.ravel().copy()
+        X[pm_dof] += p0
+        X = X.reshape(-1, 2)
+        e1, e2 = X[tris[:, 1]] - X[tris[:, 0]], X[tris[:, 2]] - X[tris[:, 0]]
+        if (0.5 * (e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0])).min() >= 0.2 * nominal:
+            break
+    free_verts = np.setdiff1d(np.arange(n_w * n_h), fixed)
+    v2f = -np.ones(n_w * n_h, dtype=np.int64)
+    v2f[free_verts] = np.arange(free_verts.size)
+    if config == 1:
+        tv = (n_w - 1) * n_h + np.arange(n_h)
+        sigma = 0.02
+    else:
+        ii, jj = np.meshgrid(np.arange(1, n_w - 1), np.arange(1, n_h - 1), indexing="ij")
+        interior = (ii * n_h + jj).ravel()
+        tv = np.sort(rng.choice(interior, size=200, replace=False))
+        sigma = 0.01
+    tdofs = (v2f[tv][:, None] * 2 + np.arange(2)[None, :]).ravel()
+    tvals = X0[tv].ravel() + rng.normal(0.0, sigma, tdofs.size)
+    return dict(X0=X0, conn=tris, kind="tri", fixed_verts=fixed,
+                pmap=(pm_dof, np.arange(pm_dof.size), np.ones(pm_dof.size)), target_dofs=tdofs,
+                target_vals=tvals, w_target=1.0, w_reg=2e-6, E=E, nu=nu, gload=100.0 * 9.81, p0=p0,
+                name=f"sheet_c{config}")
+
+
+def build_sheet(config: int, seed: int = 0, instance: int = 0, **kw):
+    """(problem, p0) for BASELINE sheet config 1 or 2 (instance > 0: config-5 member)."""
+    spec = sheet_spec(config, seed, instance)
+    p0 = spec.pop("p0")
+    spec.update(kw)
+    return ElasticDesignProblem(**spec), p0
+
+
+def build_spring_bar(n_w: int, n_h: int, w_reg: float = 0.0, stiffness: float = 2.0,
+                     mass: float = 2e-5, spacing: float = 0.25, gravity: float = 9.81,
+                     x_target=None, **kw):
+    """The reference spring lattice (spring_bar.py:30-207) on the GPU kernels.
+
+    Parameters are the rest positions of the free vertices (n_p == n_x).  The
+    rest-length regularizer (w_reg > 0) makes C = Jp^T W Jp depend on p and is not
+    yet on the device path.
+    """
+    if w_reg > 0.0:
+        raise CapabilityMissing("spring-bar rest-length regularizer on the device path")
+    if n_w < 2 or n_h < 2:
+        raise ValueError("grid must be at least 2x2")
+    ix, iy = np.meshgrid(np.arange(n_w), np.arange(n_h), indexing="ij")
+    X0 = np.column_stack([ix.ravel() * spacing, iy.ravel() * spacing])
+    vid = lambda i, j: i * n_h + j
+    springs = []
+    for i in range(n_w):
+        for j in range(n_h):
+            if i + 1 < n_w:
+                springs.append((vid(i, j), vid(i + 1, j)))
+            if j + 1 < n_h:
+                springs.append((vid(i, j), vid(i, j + 1)))
+            if i + 1 < n_w and j + 1 < n_h:
+                springs.append((vid(i, j), vid(i + 1, j + 1)))
+                springs.append((vid(i + 1, j), vid(i, j + 1)))
+    springs = np.array(springs, dtype=np.int64)
+    n_v = n_w * n_h
+    free_verts = np.arange(n_h, n_v)
+    free_dofs = np.column_stack([2 * free_verts, 2 * free_verts + 1]).ravel()
+    n_x = free_dofs.size
+    f_ext = np.zeros(2 * n_v)
+    f_ext[1::2] = mass * gravity
+    rest_base = X0.ravel().copy()
+    rest_base[free_dofs] = 0.0          # X[free] = p (absolute rest positions)
+    x_target = X0[free_verts].ravel() if x_target is None else np.asarray(x_target, dtype=np.float64)
+    prob = ElasticDesignProblem(X0, springs, "spring", np.arange(n_h),
+                                (free_dofs, np.arange(n_x), np.ones(n_x)), np.arange(n_x), x_target,
+                                w_target=1.0 / n_x, w_reg=0.0, E=1.0, stiffness=np.full(len(springs), stiffness),
+                                scale=1.0, tol=1e-10, f_ext=f_ext, rest_base=rest_base,
+                                p_offset=X0[free_verts].ravel(), name="SpringBarProblem", **kw)
+    return prob

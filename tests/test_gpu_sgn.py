@@ -1,0 +1,194 @@
+"""Device SGN path vs the reference (golden fixtures) and the CPU oracle.
+
+Golden fixtures come from the real reference (tests/golden/make_golden.py); the oracle
+(oracle/) is the CPU restatement used for sizes/configs not in the fixtures.
+Tolerances: KKT pattern bit-exact (structural; modulo stored zeros vs the reference's
+value-dependent SpGEMM pattern), values <= 1e-12 relative, dp / objective
+trajectories <= 1e-8 relative (north star).
+"""
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    return dict(np.load(os.path.join(GOLD, name), allow_pickle=False))
+
+
+def _csc(g, pre):
+    shp = g[f"{pre}_shape"]
+    return sp.csc_matrix((g[f"{pre}_data"], g[f"{pre}_indices"], g[f"{pre}_indptr"]), shape=tuple(shp))
+
+
+def _rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def _nz(m):
+    m = sp.csc_matrix(m, copy=True)
+    m.eliminate_zeros()
+    m.sort_indices()
+    return m
+
+
+# ---------------------------------------------------------------- spring bar (reference-pinned)
+@pytest.mark.parametrize("name,nw,nh", [("spring_bar_5x3.npz", 5, 3), ("spring_bar_11x3.npz", 11, 3),
+                                        ("spring_bar_16x4.npz", 16, 4)])
+def test_spring_bar_direction_matches_reference(cuda, name, nw, nh):
+    from paper_2107_03285_b200 import OptimizerConfig, direction_sgn
+    from paper_2107_03285_b200.problems import build_spring_bar
+    g = _gold(name)
+    prob = build_spring_bar(nw, nh)
+    p = prob.default_parameters()
+    np.testing.assert_array_equal(p, g["p"])
+    x = prob.simulate(p)
+    assert _rel(x, g["x"]) <= 1e-9
+    # KKT: structural pattern contains the reference's; values agree (stored zeros aside)
+    K = prob.kkt_matrix(g["x"], p).to_scipy()
+    Kr = _csc(g, "K")
+    assert _rel(_nz(K).toarray(), _nz(Kr).toarray()) <= 1e-12
+    assert (abs(Kr) > 0).multiply(K == 0).nnz == 0
+    sd = direction_sgn(prob, g["x"], p, OptimizerConfig())
+    assert sd.relative_residual <= 1e-10
+    assert _rel(sd.dp, g["dp"]) <= 1e-8
+    assert _rel(sd.dx, g["dx"]) <= 1e-8
+
+
+def test_spring_bar_minimize_trajectory_matches_reference(cuda):
+    from paper_2107_03285_b200 import OptimizerConfig, minimize
+    from paper_2107_03285_b200.problems import build_spring_bar
+    g = _gold("spring_bar_5x3.npz")
+    prob = build_spring_bar(5, 3)
+    run = minimize(prob, prob.default_parameters(), OptimizerConfig(max_iterations=5, gradient_tolerance=1e-12))
+    f_ref = g["traj_f"]
+    n = min(len(f_ref), len(run.f_values()))
+    assert n >= 3
+    # absolute floor: the trajectory converges to ~1e-28 where relative error is meaningless
+    np.testing.assert_allclose(run.f_values()[:n], f_ref[:n], rtol=1e-8, atol=1e-14 * f_ref[0])
+
+
+# ---------------------------------------------------------------- neo-Hookean sheet, config 1
+@pytest.fixture(scope="module")
+def sheet1():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2107_03285_b200.problems import build_sheet
+    return build_sheet(1)
+
+
+def test_sheet_element_blocks_match_oracle(sheet1):
+    from oracle import elements as el
+    from oracle.configs import oracle_sheet
+    prob, p0 = sheet1
+    oprob, _ = oracle_sheet(1)
+    g = _gold("sheet_c1.npz")
+    x = g["x"]
+    eng = prob.engine
+    prob._load(x, p0)
+    eng.positions()
+    eng.element_blocks()
+    pl = prob.plan
+    nd2 = pl.n_e * pl.nd * pl.nd
+    buf = eng.ebuf[0].cpu().numpy()
+    H = buf[:nd2].reshape(pl.n_e, pl.nd, pl.nd)
+    M = buf[nd2:].reshape(pl.n_e, pl.nd, pl.nd)
+    pos = oprob.full_positions(x)
+    rest = oprob.rest_positions(p0)
+    Ho, Mo = el.nh_second(pos[oprob.conn], rest[oprob.conn], oprob.mu, oprob.lam, oprob.gload)
+    s = oprob.scale
+    assert _rel(H, s * Ho) <= 1e-12
+    assert _rel(M, s * Mo) <= 1e-12
+
+
+def test_sheet_kkt_pattern_bit_exact_and_values(sheet1):
+    prob, p0 = sheet1
+    g = _gold("sheet_c1.npz")
+    K = prob.kkt_matrix(g["x"], p0)
+    Kr = _csc(g, "K")
+    np.testing.assert_array_equal(K.indptr, Kr.indptr)
+    np.testing.assert_array_equal(K.indices, Kr.indices)
+    assert np.max(np.abs(K.data - Kr.data)) <= 1e-12 * np.max(np.abs(Kr.data))
+
+
+def test_sheet_simulate_matches_oracle(sheet1):
+    prob, p0 = sheet1
+    g = _gold("sheet_c1.npz")
+    prob._x_warm = None
+    x = prob.simulate(p0)
+    assert _rel(x, g["x"]) <= 1e-10
+
+
+def test_sheet_direction_matches_reference(sheet1):
+    from paper_2107_03285_b200 import OptimizerConfig, adjoint_gradient, direction_sgn
+    prob, p0 = sheet1
+    g = _gold("sheet_c1.npz")
+    grad = adjoint_gradient(prob, g["x"], p0)
+    assert _rel(grad, g["grad"]) <= 1e-9
+    sd = direction_sgn(prob, g["x"], p0, OptimizerConfig())
+    assert sd.relative_residual <= 1e-10
+    assert _rel(sd.dp, g["dp"]) <= 1e-8
+    assert _rel(sd.dp, g["dp_dgn"]) <= 1e-6     # Theorem 1: SGN == DGN
+
+
+def test_sheet_minimize_trajectory_matches_reference(sheet1):
+    from paper_2107_03285_b200 import OptimizerConfig, minimize
+    prob, p0 = sheet1
+    g = _gold("sheet_c1.npz")
+    prob._x_warm = None
+    run = minimize(prob, p0, OptimizerConfig(max_iterations=5, gradient_tolerance=1e-12))
+    np.testing.assert_allclose(run.f_values(), g["traj_f"], rtol=1e-8)
+
+
+# ---------------------------------------------------------------- known answers (plugin path)
+def test_hand_oracle_plugin_problem(cuda):
+    """Reference hand oracle (test_sensitivity.py:223-242): dp = 1, dx = -1, dlam = 1."""
+    from paper_2107_03285_b200 import CscMatrix, EquilibriumProblem, OptimizerConfig, direction_sgn
+
+    class Tiny(EquilibriumProblem):
+        n_x, n_p = 2, 1
+
+        def constraint_jac_x(self, x, p):
+            return CscMatrix.identity(2)
+
+        def constraint_jac_p(self, x, p):
+            return CscMatrix.from_dense(np.array([[1.0], [1.0]]))
+
+        def residuals(self, x, p):
+            return x + 1.0
+
+        def weights(self):
+            return np.ones(2)
+
+        def residual_jac_x(self, x, p):
+            return CscMatrix.identity(2)
+
+        def residual_jac_p(self, x, p):
+            return CscMatrix.zeros(2, 1)
+
+    sd = direction_sgn(Tiny(), np.zeros(2), np.zeros(1), OptimizerConfig())
+    np.testing.assert_allclose(sd.dp, [1.0], atol=1e-10)
+    np.testing.assert_allclose(sd.dx, [-1.0, -1.0], atol=1e-10)
+    np.testing.assert_allclose(sd.dlam, [1.0, 1.0], atol=1e-10)
+
+
+# ---------------------------------------------------------------- config 2 (bench workload)
+def test_sheet_c2_direction_matches_oracle(cuda):
+    from oracle import sgn_cpu
+    from oracle.configs import oracle_sheet
+    from paper_2107_03285_b200 import OptimizerConfig, direction_sgn
+    from paper_2107_03285_b200.problems import build_sheet
+    prob, p0 = build_sheet(2)
+    x = prob.simulate(p0)
+    oprob, _ = oracle_sheet(2)
+    d_ref = sgn_cpu.direction_sgn(oprob, x, p0)
+    sd = direction_sgn(prob, x, p0, OptimizerConfig())
+    assert sd.relative_residual <= 1e-10
+    assert _rel(sd.dp, d_ref.dp) <= 1e-8
+    xo = oprob.simulate(p0)
+    assert _rel(x, xo) <= 1e-10
