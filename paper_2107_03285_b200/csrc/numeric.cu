@@ -320,21 +320,113 @@ __device__ __forceinline__ bool pair_skip(int pivtype, int row, int col) {
   return pivtype == 2 && (col & 1) == 0 && row == col + 1;
 }
 
-__global__ void __launch_bounds__(kSolveThreads)
-k_fwd(const int32_t* __restrict__ flist, const DFront* __restrict__ fronts,
-      const int32_t* __restrict__ children, const int32_t* __restrict__ rel,
-      const double* __restrict__ fstore, int64_t fstride, double* __restrict__ y, int64_t n,
-      double* __restrict__ ubuf, int64_t ustride, double* __restrict__ vbuf, int64_t vstride,
-      int leading) {
+// ------------------------------------------------------------------------------------
+// Solve panel Z = [I; L21] L11^{-1} of one front (rows r0..r0+31), built after the front
+// is factored: Z L11 = B with B = e_r (pivot rows) or L21 (struct rows), swept right to
+// left in 32-column blocks; the inter-block products run on DMMA.  With Z the
+// triangular solves are one parallel pass per front (k_fwd / k_bwd below).
+// ------------------------------------------------------------------------------------
+constexpr int kZThreads = 256;
+__global__ void __launch_bounds__(kZThreads)
+k_zpanel(const Work* __restrict__ work, const DFront* __restrict__ fronts,
+         const double* __restrict__ fstore, int64_t fstride, double* __restrict__ zstore,
+         int64_t zstride) {
+  __shared__ double Ts[kTile][kTile + 1];          // final Z block of the step (rows x cols)
+  __shared__ double Ls[kTile][kTile + 1];          // diagonal block of L11
+  const Work wk = work[blockIdx.x];
   const int b = blockIdx.y;
-  const DFront F = fronts[flist[blockIdx.x]];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* yb = y + (int64_t)b * n;
-  if (leading && F.is_root_p) return;
-  double* v = vbuf + (int64_t)b * vstride + F.voff;
-  const double* Fm = fstore + (int64_t)b * fstride + F.foff;
+  const DFront F = fronts[wk.f];
+  const int r0 = wk.a;
+  const int nr = min(kTile, F.nrow - r0);
+  const int npiv = F.npiv;
   const int64_t ld = F.nrow;
-  for (int i = tid; i < F.nrow; i += blockDim.x) v[i] = (i < F.npiv) ? yb[F.first + i] : 0.0;
+  const double* Fm = fstore + (int64_t)b * fstride + F.foff;
+  double* Zm = zstore + (int64_t)b * zstride + F.zoff;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
+  const int cmax = (r0 < npiv) ? min(npiv, r0 + nr) : npiv;
+  const int nb = (cmax + kTile - 1) / kTile;
+  // Z <- B  (identity rows for pivots, L21 rows for the structure)
+  for (int e = tid; e < nr * cmax; e += blockDim.x) {
+    const int i = e % nr, c = e / nr, r = r0 + i;
+    Zm[(int64_t)c * ld + r] = (r < npiv) ? (r == c ? 1.0 : 0.0) : Fm[(int64_t)c * ld + r];
+  }
+  __syncthreads();
+  for (int cbi = nb - 1; cbi >= 0; --cbi) {
+    const int cb = cbi * kTile;
+    const int wb = min(kTile, npiv - cb);
+    for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+      const int i = e & 31, c = e >> 5;
+      Ts[i][c] = (i < nr && c < wb) ? Zm[(int64_t)(cb + c) * ld + r0 + i] : 0.0;
+      const int cp = e & 31;
+      Ls[cp][c] = (cp < wb && c < wb && cp > c && !pair_skip(F.pivtype, cp, c))
+                      ? Fm[(int64_t)(cb + c) * ld + cb + cp] : 0.0;
+    }
+    __syncthreads();
+    if (warp == 0 && lane < nr) {     // z L11blk = t, right to left
+      for (int c = wb - 1; c >= 0; --c) {
+        double z = Ts[lane][c];
+        for (int cp = c + 1; cp < wb; ++cp) z -= Ts[lane][cp] * Ls[cp][c];
+        Ts[lane][c] = z;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+      const int i = e & 31, c = e >> 5;
+      if (i < nr && c < wb) Zm[(int64_t)(cb + c) * ld + r0 + i] = Ts[i][c];
+    }
+    // right-looking update of the remaining column blocks: Z[:, blk] -= Zblk * L11[cb.., blk]
+    for (int blk = warp; blk < cbi; blk += 8) {
+      const int c0 = blk * kTile;
+      double Bf[8][4];   // B fragments: L11[cb + kk + q][c0 + nf*8 + g]
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+        for (int nf = 0; nf < 4; ++nf) {
+          const int kk = ks * 4 + q;
+          Bf[ks][nf] = (kk < wb) ? Fm[(int64_t)(c0 + nf * 8 + g) * ld + cb + kk] : 0.0;
+        }
+      double acc[4][4][2];
+#pragma unroll
+      for (int mf = 0; mf < 4; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+        for (int mf = 0; mf < 4; ++mf) {
+          const double a = Ts[mf * 8 + g][ks * 4 + q];
+#pragma unroll
+          for (int nf = 0; nf < 4; ++nf) dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a, Bf[ks][nf]);
+        }
+      }
+#pragma unroll
+      for (int mf = 0; mf < 4; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = mf * 8 + g, j = nf * 8 + 2 * q + h;
+            if (i < nr) Zm[(int64_t)(c0 + j) * ld + r0 + i] -= acc[mf][nf][h];
+          }
+    }
+    __syncthreads();
+  }
+}
+
+// Forward solve, gather step (one CTA per front): v = [b(pivots); 0] + children updates
+// (extend-add in fixed child order; rel maps are injective within a child).
+__global__ void __launch_bounds__(kSolveThreads)
+k_fwd_gather(const Work* __restrict__ work, const DFront* __restrict__ fronts,
+             const int32_t* __restrict__ children, const int32_t* __restrict__ rel,
+             const double* __restrict__ bperm, int64_t n, const double* __restrict__ ubuf,
+             int64_t ustride, double* __restrict__ vbuf, int64_t vstride, int leading) {
+  const int b = blockIdx.y;
+  const DFront F = fronts[work[blockIdx.x].f];
+  if (leading && F.is_root_p) return;
+  const int tid = threadIdx.x;
+  double* v = vbuf + (int64_t)b * vstride + F.voff;
+  const double* bb = bperm + (int64_t)b * n;
+  for (int i = tid; i < F.nrow; i += blockDim.x) v[i] = (i < F.npiv) ? bb[F.first + i] : 0.0;
   __syncthreads();
   for (int ci = F.child_begin; ci < F.child_end; ++ci) {
     const DFront C = fronts[children[ci]];
@@ -344,85 +436,171 @@ k_fwd(const int32_t* __restrict__ flist, const DFront* __restrict__ fronts,
     for (int t = tid; t < cn; t += blockDim.x) v[rc[t]] += uc[t];
     __syncthreads();
   }
-  for (int jb = 0; jb < F.npiv; jb += 32) {
-    const int wb = min(32, F.npiv - jb);
-    if (warp == 0) {
-      double val = (lane < wb) ? v[jb + lane] : 0.0;
-      for (int c = 0; c < wb; ++c) {
-        const double vc = __shfl_sync(0xffffffffu, val, c);
-        if (lane > c && lane < wb && !pair_skip(F.pivtype, lane, c))
-          val -= Fm[(int64_t)(jb + c) * ld + jb + lane] * vc;
-      }
-      if (lane < wb) v[jb + lane] = val;
-    }
-    __syncthreads();
-    for (int i = jb + wb + tid; i < F.nrow; i += blockDim.x) {
-      double acc = 0.0;
-      for (int c = 0; c < wb; ++c) acc += Fm[(int64_t)(jb + c) * ld + i] * v[jb + c];
-      v[i] -= acc;
-    }
-    __syncthreads();
-  }
-  // D solve, write z to y at pivot positions
-  if (F.pivtype == 2) {
-    for (int j = 2 * tid; j < F.npiv; j += 2 * blockDim.x) {
-      const double a = Fm[(int64_t)j * ld + j], bb = Fm[(int64_t)j * ld + j + 1],
-                   c = Fm[(int64_t)(j + 1) * ld + j + 1];
-      const double det = a * c - bb * bb;
-      const double x0 = v[j], x1 = v[j + 1];
-      yb[F.first + j] = (c * x0 - bb * x1) / det;
-      yb[F.first + j + 1] = (a * x1 - bb * x0) / det;
-    }
-  } else {
-    for (int j = tid; j < F.npiv; j += blockDim.x) yb[F.first + j] = v[j] / Fm[(int64_t)j * ld + j];
-  }
-  double* u = ubuf + (int64_t)b * ustride + F.uoff;
-  for (int i = F.npiv + tid; i < F.nrow; i += blockDim.x) u[i - F.npiv] = v[i];
 }
 
+// last-arriving CTA of a chunk group (ticket); partials are then summed in chunk order
+__device__ __forceinline__ bool group_last(int* ticket, int nch) {
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int old = atomicAdd(ticket, 1);
+    last = (old == nch - 1);
+    if (last) *ticket = 0;     // reset for the next solve
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+// Forward solve, GEMV step on (front, 32-row tile, 64-column chunk):
+//   partial_k = Z[rows, chunk] v[chunk]; the group's last CTA sums the chunks in order:
+//   pivot rows -> z = D^{-1} y1 (zbuf); structure rows -> u = v2 - t (parent update).
 __global__ void __launch_bounds__(kSolveThreads)
-k_bwd(const int32_t* __restrict__ flist, const DFront* __restrict__ fronts,
-      const int64_t* __restrict__ srows, const double* __restrict__ fstore, int64_t fstride,
-      double* __restrict__ y, int64_t n, double* __restrict__ vbuf, int64_t vstride,
-      int leading) {
+k_fwd(const Work* __restrict__ work, const DFront* __restrict__ fronts,
+      const double* __restrict__ fstore, int64_t fstride, const double* __restrict__ zstore,
+      int64_t zstride, const double* __restrict__ vbuf, int64_t vstride,
+      double* __restrict__ zbuf, int64_t n, double* __restrict__ ubuf, int64_t ustride,
+      double* __restrict__ part, int64_t pstride, int* __restrict__ tickets, int64_t n_groups,
+      const int32_t* __restrict__ grp_nchunk, const int64_t* __restrict__ grp_base, int leading) {
+  __shared__ double red[8][33];
   const int b = blockIdx.y;
-  const DFront F = fronts[flist[blockIdx.x]];
+  const Work wk = work[blockIdx.x];
+  const DFront F = fronts[wk.f];
+  if (leading && F.is_root_p) return;
+  const int r0 = wk.a, k = wk.b, g = wk.c;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nr = min(sgn::kFwdRows, F.nrow - r0);
+  const int npiv = F.npiv;
+  const int cend = (r0 < npiv) ? min(npiv, r0 + nr) : npiv;
+  const int c_lo = k * sgn::kFwdCols, c_hi = min(c_lo + sgn::kFwdCols, cend);
+  const double* Zm = zstore + (int64_t)b * zstride + F.zoff;
+  const double* v = vbuf + (int64_t)b * vstride + F.voff;
+  const int64_t ld = F.nrow;
+  __shared__ double vs[sgn::kFwdCols];
+  if (tid < c_hi - c_lo) vs[tid] = v[c_lo + tid];
+  __syncthreads();
+  double a0 = 0.0, a1 = 0.0;
+  if (lane < nr) {
+    const double* zr = Zm + r0 + lane;
+    int c = c_lo + warp;
+    for (; c + 8 < c_hi; c += 16) {
+      a0 += zr[(int64_t)c * ld] * vs[c - c_lo];
+      a1 += zr[(int64_t)(c + 8) * ld] * vs[c + 8 - c_lo];
+    }
+    if (c < c_hi) a0 += zr[(int64_t)c * ld] * vs[c - c_lo];
+  }
+  red[warp][lane] = a0 + a1;
+  __syncthreads();
+  const int nch = grp_nchunk[g];
+  double* pp = part + (int64_t)b * pstride + grp_base[g];
+  if (nch > 1) {
+    if (warp == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += red[w][lane];
+      pp[k * 32 + lane] = t;
+    }
+    if (!group_last(tickets + (int64_t)b * n_groups + g, nch)) return;
+  }
+  if (warp != 0) return;
+  double t = 0.0;
+  if (nch > 1) {
+    for (int kk = 0; kk < nch; ++kk) t += __ldcg(pp + kk * 32 + lane);
+  } else {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+  }
+  const double tp = __shfl_xor_sync(0xffffffffu, t, 1);   // 2x2 pivot partner row
+  if (lane >= nr) return;
+  const int r = r0 + lane;
+  if (r < npiv) {
+    const double* Fm = fstore + (int64_t)b * fstride + F.foff;
+    double* zb = zbuf + (int64_t)b * n;
+    if (F.pivtype == 2) {
+      const int re = r & ~1;
+      const double a = Fm[(int64_t)re * ld + re], bq = Fm[(int64_t)re * ld + re + 1],
+                   c = Fm[(int64_t)(re + 1) * ld + re + 1];
+      const double det = a * c - bq * bq;
+      zb[F.first + r] = ((r & 1) == 0) ? (c * t - bq * tp) / det : (a * t - bq * tp) / det;
+    } else {
+      zb[F.first + r] = t / Fm[(int64_t)r * ld + r];
+    }
+  } else {
+    ubuf[(int64_t)b * ustride + F.uoff + (r - npiv)] = v[r] - t;
+  }
+}
+
+// Backward solve on (front, 32-column tile, 256-row chunk): x1 = Z^T [z1; -x2] as column
+// dots (warp per column, coalesced), chunk partials combined by the group's last CTA.
+__global__ void __launch_bounds__(kSolveThreads)
+k_bwd(const Work* __restrict__ work, const DFront* __restrict__ fronts,
+      const int64_t* __restrict__ srows, const double* __restrict__ zstore, int64_t zstride,
+      const double* __restrict__ zbuf, double* __restrict__ xbuf, int64_t n,
+      double* __restrict__ part, int64_t pstride, int* __restrict__ tickets, int64_t n_groups,
+      const int32_t* __restrict__ grp_nchunk, const int64_t* __restrict__ grp_base, int leading) {
+  __shared__ double colsum[32];
+  const int b = blockIdx.y;
+  const Work wk = work[blockIdx.x];
+  const DFront F = fronts[wk.f];
+  const int c0 = wk.a, rs = wk.b, g = wk.c;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  double* yb = y + (int64_t)b * n;
+  const int ncol = min(sgn::kBwdCols, F.npiv - c0);
+  double* xb = xbuf + (int64_t)b * n;
   if (leading && F.is_root_p) {
-    for (int i = tid; i < F.npiv; i += blockDim.x) yb[F.first + i] = 0.0;
+    if (rs <= c0) for (int j = tid; j < ncol; j += blockDim.x) xb[F.first + c0 + j] = 0.0;
     return;
   }
-  double* v = vbuf + (int64_t)b * vstride + F.voff;
-  const double* Fm = fstore + (int64_t)b * fstride + F.foff;
+  __shared__ double vs[sgn::kBwdRows];
+  const double* zb = zbuf + (int64_t)b * n;
+  const double* Zm = zstore + (int64_t)b * zstride + F.zoff;
   const int64_t ld = F.nrow;
-  for (int i = tid; i < F.nrow; i += blockDim.x)
-    v[i] = (i < F.npiv) ? yb[F.first + i] : yb[srows[F.srow_off + i - F.npiv]];
-  __syncthreads();
-  const int nblk = (F.npiv + 31) / 32;
-  for (int blk = nblk - 1; blk >= 0; --blk) {
-    const int jb = blk * 32, wb = min(32, F.npiv - jb);
-    for (int c = warp; c < wb; c += nwarps) {
-      const double* col = Fm + (int64_t)(jb + c) * ld;
-      double acc = 0.0;
-      for (int i = jb + wb + lane; i < F.nrow; i += 32) acc += col[i] * v[i];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) v[jb + c] -= acc;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      double val = (lane < wb) ? v[jb + lane] : 0.0;
-      for (int c = wb - 1; c >= 0; --c) {
-        const double vc = __shfl_sync(0xffffffffu, val, c);
-        if (lane < c && !pair_skip(F.pivtype, c, lane))
-          val -= Fm[(int64_t)(jb + lane) * ld + jb + c] * vc;
-      }
-      if (lane < wb) v[jb + lane] = val;
-    }
-    __syncthreads();
+  const int64_t* sr = srows + F.srow_off;
+  const int np = F.npiv;
+  const int re = min(rs + sgn::kBwdRows, F.nrow);
+  for (int i = tid; i < re - rs; i += blockDim.x) {
+    const int r = rs + i;
+    vs[i] = (r < np) ? zb[F.first + r] : -xb[sr[r - np]];
   }
-  for (int i = tid; i < F.npiv; i += blockDim.x) yb[F.first + i] = v[i];
+  __syncthreads();
+  // warp w owns columns w, w+8, w+16, w+24 of the tile; all four dots advance together
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const double* col[4];
+  int rbeg[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int j = c0 + warp + 8 * m;
+    col[m] = Zm + (int64_t)j * ld;
+    rbeg[m] = (warp + 8 * m < ncol) ? max(rs, j) : re;   // empty range for missing columns
+  }
+  for (int r = rs + lane; r < re; r += 32) {
+    const double v = vs[r - rs];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (r >= rbeg[m]) acc[m] += col[m][r] * v;
+  }
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    double a = acc[m];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) colsum[warp + 8 * m] = a;
+  }
+  __syncthreads();
+  const int nch = grp_nchunk[g];
+  double* pp = part + (int64_t)b * pstride + grp_base[g];
+  const int k = (rs - (c0 / sgn::kBwdRows) * sgn::kBwdRows) / sgn::kBwdRows;
+  if (nch > 1) {
+    if (tid < 32) pp[k * 32 + tid] = colsum[tid];
+    if (!group_last(tickets + (int64_t)b * n_groups + g, nch)) return;
+    if (tid < ncol) {
+      double t = 0.0;
+      for (int kk = 0; kk < nch; ++kk) t += __ldcg(pp + kk * 32 + tid);
+      xb[F.first + c0 + tid] = t;
+    }
+  } else if (tid < ncol) {
+    xb[F.first + c0 + tid] = colsum[tid];
+  }
 }
 
 __global__ void k_permute_in(const double* __restrict__ x, double* __restrict__ y,
@@ -642,18 +820,37 @@ struct sgn_factor_s {
   DevBuf<int64_t> srows, perm, tile_ptr, tile_nnz, indptr;
   DevBuf<int8_t> kind_pos;
   DevBuf<Work> work;
-  DevBuf<double> fstore, wstore, ubuf, vbuf, y;
+  DevBuf<double> fstore, wstore, ubuf, vbuf, y, zstore, zbuf, xbuf, part;
+  DevBuf<int> tickets;
+  DevBuf<int32_t> grp_nchunk;
+  DevBuf<int64_t> grp_base;
   DevBuf<long long> status;
   std::vector<int64_t> lvl_off;  // level -> offset into lvl_fronts
   // BiCGSTAB workspace
   DevBuf<double> bx, br, brh, bp, bv, bs, bt, btmp, bbest, bb, bscr, partial;
   DevBuf<BiState> bst;
   bool bicg_ready = false;
+  // captured triangular-solve graphs (index = flags)
+  struct SolveGraph {
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t in_node = nullptr, out_node = nullptr;
+    cudaKernelNodeParams in_p{}, out_p{};
+    int64_t kernels = 0;
+  } graphs[2];
+  std::vector<cudaGraph_t> graph_templates;
+  DevBuf<double> gin, gout;   // placeholder endpoints used only while capturing
+  const double* bbuf_in() { if (!gin.p) gin.alloc((size_t)batch * std::max<int64_t>(n, 1)); return gin.p; }
+  double* bbuf_out() { if (!gout.p) gout.alloc((size_t)batch * std::max<int64_t>(n, 1)); return gout.p; }
+  ~sgn_factor_s() {
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (auto g : graph_templates) cudaGraphDestroy(g);
+  }
 };
 
 namespace {
 
-int launch_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st) {
+int launch_solve_raw(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st) {
   const sgn::Symbolic& s = f->sym->s;
   const int64_t n = s.n;
   if (n == 0) return SGN_OK;
@@ -662,24 +859,94 @@ int launch_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cu
   k_permute_in<<<pg, 256, 0, st>>>(d_b, f->y.p, f->perm.p, n);
   const int leading = (flags & SGN_SOLVE_LEADING) ? 1 : 0;
   for (int32_t lv = 0; lv < s.n_levels; ++lv) {
-    const int64_t cnt = f->lvl_off[lv + 1] - f->lvl_off[lv];
-    if (!cnt) continue;
-    sgn::count_launch();
-    k_fwd<<<dim3((unsigned)cnt, f->batch), kSolveThreads, 0, st>>>(
-        f->lvl_fronts.p + f->lvl_off[lv], f->fronts.p, f->children.p, f->rel.p, f->fstore.p,
-        s.front_doubles, f->y.p, n, f->ubuf.p, s.u_doubles, f->vbuf.p, s.v_doubles, leading);
+    if (s.gat_cnt[lv]) {
+      sgn::count_launch();
+      k_fwd_gather<<<dim3((unsigned)s.gat_cnt[lv], f->batch), kSolveThreads, 0, st>>>(
+          f->work.p + s.gat_off[lv], f->fronts.p, f->children.p, f->rel.p, f->y.p, n, f->ubuf.p,
+          s.u_doubles, f->vbuf.p, s.v_doubles, leading);
+    }
+    if (s.fwd_cnt[lv]) {
+      sgn::count_launch();
+      k_fwd<<<dim3((unsigned)s.fwd_cnt[lv], f->batch), kSolveThreads, 0, st>>>(
+          f->work.p + s.fwd_off[lv], f->fronts.p, f->fstore.p, s.front_doubles, f->zstore.p,
+          s.z_doubles, f->vbuf.p, s.v_doubles, f->zbuf.p, n, f->ubuf.p, s.u_doubles, f->part.p,
+          s.part_doubles, f->tickets.p, s.n_groups, f->grp_nchunk.p, f->grp_base.p, leading);
+    }
   }
   for (int32_t lv = s.n_levels - 1; lv >= 0; --lv) {
-    const int64_t cnt = f->lvl_off[lv + 1] - f->lvl_off[lv];
-    if (!cnt) continue;
+    if (!s.bwd_cnt[lv]) continue;
     sgn::count_launch();
-    k_bwd<<<dim3((unsigned)cnt, f->batch), kSolveThreads, 0, st>>>(
-        f->lvl_fronts.p + f->lvl_off[lv], f->fronts.p, f->srows.p, f->fstore.p, s.front_doubles,
-        f->y.p, n, f->vbuf.p, s.v_doubles, leading);
+    k_bwd<<<dim3((unsigned)s.bwd_cnt[lv], f->batch), kSolveThreads, 0, st>>>(
+        f->work.p + s.bwd_off[lv], f->fronts.p, f->srows.p, f->zstore.p, s.z_doubles, f->zbuf.p,
+        f->xbuf.p, n, f->part.p, s.part_doubles, f->tickets.p, s.n_groups, f->grp_nchunk.p,
+        f->grp_base.p, leading);
   }
   sgn::count_launch();
-  k_permute_out<<<pg, 256, 0, st>>>(f->y.p, d_x, f->perm.p, n);
+  k_permute_out<<<pg, 256, 0, st>>>(f->xbuf.p, d_x, f->perm.p, n);
   CUDA_TRY(cudaGetLastError());
+  return SGN_OK;
+}
+
+
+// The solve is a fixed launch sequence per (factor, flags): capture it once as a CUDA
+// graph and replay it, patching only the permute-in / permute-out pointer arguments.
+int launch_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st) {
+  const int64_t n = f->n;
+  if (n == 0) return SGN_OK;
+  auto& G = f->graphs[(flags & SGN_SOLVE_LEADING) ? 1 : 0];
+  if (!G.exec) {
+    const double* cap_in = f->bbuf_in();   // allocate before capturing
+    double* cap_out = f->bbuf_out();
+    if (!cap_in || !cap_out) { sgn::last_error() = "graph placeholder allocation failed"; return SGN_CUDA_ERROR; }
+    CUDA_TRY(cudaDeviceSynchronize());
+    cudaStream_t cs;
+    CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t graph;
+    CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    const int64_t before = sgn::launch_count();
+    int rc = launch_solve_raw(f, cap_in, cap_out, flags, cs);
+    sgn::count_launch(before - sgn::launch_count());   // captured, not launched
+    cudaError_t e = cudaStreamEndCapture(cs, &graph);
+    cudaStreamDestroy(cs);
+    if (rc) return rc;
+    if (e != cudaSuccess) { sgn::last_error() = std::string("capture: ") + cudaGetErrorString(e); return SGN_CUDA_ERROR; }
+    size_t nn = 0;
+    CUDA_TRY(cudaGraphGetNodes(graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CUDA_TRY(cudaGraphGetNodes(graph, nodes.data(), &nn));
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      CUDA_TRY(cudaGraphNodeGetType(nd, &t));
+      if (t != cudaGraphNodeTypeKernel) continue;
+      ++G.kernels;
+      cudaKernelNodeParams p;
+      CUDA_TRY(cudaGraphKernelNodeGetParams(nd, &p));
+      if (p.func == (void*)k_permute_in) { G.in_node = nd; G.in_p = p; }
+      if (p.func == (void*)k_permute_out) { G.out_node = nd; G.out_p = p; }
+    }
+    CUDA_TRY(cudaGraphInstantiate(&G.exec, graph, 0));
+    // the instantiated exec keeps its own copy; node handles stay valid for SetParams
+    G.in_node = G.in_node; G.out_node = G.out_node;
+    f->graph_templates.push_back(graph);
+  }
+  const double* b_arg = d_b;
+  double* y_arg = f->y.p;
+  const int64_t* perm_arg = f->perm.p;
+  int64_t n_arg = n;
+  void* in_args[] = {(void*)&b_arg, (void*)&y_arg, (void*)&perm_arg, (void*)&n_arg};
+  cudaKernelNodeParams pin = G.in_p;
+  pin.kernelParams = in_args;
+  pin.extra = nullptr;
+  CUDA_TRY(cudaGraphExecKernelNodeSetParams(G.exec, G.in_node, &pin));
+  const double* xs_arg = f->xbuf.p;
+  double* x_arg = d_x;
+  void* out_args[] = {(void*)&xs_arg, (void*)&x_arg, (void*)&perm_arg, (void*)&n_arg};
+  cudaKernelNodeParams pout = G.out_p;
+  pout.kernelParams = out_args;
+  pout.extra = nullptr;
+  CUDA_TRY(cudaGraphExecKernelNodeSetParams(G.exec, G.out_node, &pout));
+  CUDA_TRY(cudaGraphLaunch(G.exec, st));
+  sgn::count_launch(G.kernels);
   return SGN_OK;
 }
 
@@ -791,6 +1058,7 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
     DFront& d = df[k];
     d.first = F.first; d.foff = F.foff; d.srow_off = F.srow_off; d.rel_off = F.rel_off;
     d.uoff = F.uoff; d.woff = F.woff; d.voff = F.voff; d.tile_base = F.tile_base;
+    d.zoff = F.zoff; d.pad0 = 0;
     d.npiv = F.npiv; d.nrow = F.nrow; d.parent = F.parent; d.pivtype = F.pivtype;
     d.child_begin = F.child_begin; d.child_end = F.child_end; d.is_root_p = F.is_root_p;
     d.level = F.level;
@@ -817,8 +1085,18 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
       (rc = f->wstore.alloc(B * std::max<int64_t>(s.w_doubles, 1))) ||
       (rc = f->ubuf.alloc(B * std::max<int64_t>(s.u_doubles, 1))) ||
       (rc = f->vbuf.alloc(B * std::max<int64_t>(s.v_doubles, 1))) ||
-      (rc = f->y.alloc(B * std::max<int64_t>(s.n, 1))) || (rc = f->status.alloc(B)))
+      (rc = f->y.alloc(B * std::max<int64_t>(s.n, 1))) || (rc = f->status.alloc(B)) ||
+      (rc = f->zstore.alloc(B * std::max<int64_t>(s.z_doubles, 1))) ||
+      (rc = f->zbuf.alloc(B * std::max<int64_t>(s.n, 1))) ||
+      (rc = f->xbuf.alloc(B * std::max<int64_t>(s.n, 1))))
     return rc;
+  if ((rc = f->part.alloc(B * std::max<int64_t>(s.part_doubles, 1))) ||
+      (rc = f->tickets.alloc(B * std::max<int64_t>(s.n_groups, 1))) ||
+      (rc = f->grp_nchunk.upload(s.grp_nchunk)) || (rc = f->grp_base.upload(s.grp_base)))
+    return rc;
+  CUDA_TRY(cudaMemset(f->tickets.p, 0, f->tickets.n * sizeof(int)));
+  // Z11 = L11^{-1} is lower triangular: the strictly upper part stays zero forever
+  CUDA_TRY(cudaMemset(f->zstore.p, 0, f->zstore.n * sizeof(double)));
   *out = f.release();
   return SGN_OK;
 }
@@ -849,6 +1127,11 @@ int sgn_factor_numeric(sgn_factor f, const double* d_values, int64_t values_stri
         k_panel<<<grid, kPanelThreads, 0, st>>>(w, f->fronts.p, f->perm.p, f->fstore.p,
                                                 s.front_doubles, f->wstore.p, s.w_doubles,
                                                 f->status.p);
+        break;
+      case sgn::L_ZPANEL:
+        sgn::count_launch();
+        k_zpanel<<<grid, kZThreads, 0, st>>>(w, f->fronts.p, f->fstore.p, s.front_doubles,
+                                               f->zstore.p, s.z_doubles);
         break;
       case sgn::L_UPDATE:
         sgn::count_launch();

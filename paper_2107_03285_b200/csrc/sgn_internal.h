@@ -26,6 +26,7 @@ struct Front {
   int64_t woff = 0;       // offset of the panel W scratch (nrow x 32)
   int64_t voff = 0;       // offset of the solve front vector (nrow)
   int64_t tile_base = 0;  // first assembly tile id
+  int64_t zoff = 0;       // offset of the solve panel Z = [I; L21] L11^{-1} (nrow x npiv)
 };
 
 // Device-side mirror of Front (POD, 16-byte aligned for vector loads).
@@ -38,13 +39,19 @@ struct DFront {
   int64_t woff;
   int64_t voff;
   int64_t tile_base;
+  int64_t zoff;
+  int64_t pad0;
   int32_t npiv, nrow, parent, pivtype;
   int32_t child_begin, child_end, is_root_p, level;
 };
 
 struct Work { int32_t f, a, b, c; };   // generic work item
 
-enum LaunchKind : int32_t { L_ASM = 0, L_PANEL = 1, L_UPDATE = 2 };
+enum LaunchKind : int32_t { L_ASM = 0, L_PANEL = 1, L_UPDATE = 2, L_ZPANEL = 3 };
+constexpr int kFwdRows = 32;    // rows per CTA of the forward-solve GEMV
+constexpr int kFwdCols = 64;    // columns (K chunk) per CTA of the forward-solve GEMV
+constexpr int kBwdCols = 32;    // columns per CTA of the backward-solve dots
+constexpr int kBwdRows = 256;   // rows (K chunk) per CTA of the backward-solve dots
 struct Launch { int32_t kind; int32_t level; int64_t off; int64_t count; };
 
 struct Symbolic {
@@ -68,8 +75,15 @@ struct Symbolic {
   std::vector<std::vector<int32_t>> level_fronts;
   std::vector<Work> work;                      // all work items
   std::vector<Launch> launches;                // factorization launch schedule
+  // solve work lists per level (items into `work`): forward (f, row0), backward (f, col0)
+  std::vector<int64_t> fwd_off, fwd_cnt, bwd_off, bwd_cnt, gat_off, gat_cnt;
+  std::vector<int32_t> lvl_max_piv;
+  // chunk-split groups: per (front, tile) group -> number of chunks, partial-sum base
+  std::vector<int32_t> grp_nchunk;
+  std::vector<int64_t> grp_base;
+  int64_t n_groups = 0, part_doubles = 0;
   // sizes
-  int64_t front_doubles = 0, u_doubles = 0, w_doubles = 0, v_doubles = 0;
+  int64_t front_doubles = 0, u_doubles = 0, w_doubles = 0, v_doubles = 0, z_doubles = 0;
   int64_t nnz_l = 0; double flops = 0; int64_t max_front = 0, max_piv = 0;
 };
 

@@ -628,7 +628,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   s.level_fronts.assign(s.n_levels, {});
   for (int32_t k = 0; k < NF; ++k) s.level_fronts[s.fronts[k].level].push_back(k);
 
-  s.front_doubles = s.u_doubles = s.w_doubles = s.v_doubles = 0;
+  s.front_doubles = s.u_doubles = s.w_doubles = s.v_doubles = s.z_doubles = 0;
   s.ntiles = 0;
   s.nnz_l = 0;
   s.flops = 0;
@@ -639,6 +639,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     F.uoff = s.u_doubles; s.u_doubles += ns;
     F.woff = s.w_doubles; s.w_doubles += nr * kTile;
     F.voff = s.v_doubles; s.v_doubles += nr;
+    F.zoff = s.z_doubles; s.z_doubles += nr * F.npiv;
     const int64_t T = (nr + kTile - 1) / kTile;
     F.tile_base = s.ntiles; s.ntiles += T * (T + 1) / 2;
     s.nnz_l += (int64_t)F.npiv * (F.npiv + 1) / 2 + (int64_t)F.npiv * ns;
@@ -745,7 +746,60 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
       }
       if ((int64_t)s.work.size() > off) s.launches.push_back({L_UPDATE, lv, off, (int64_t)s.work.size() - off});
     }
+    // solve panel Z = [I; L21] L11^{-1}: one CTA per 32 rows of every front of the level
+    off = (int64_t)s.work.size();
+    for (int32_t f : fl) {
+      const Front& F = s.fronts[f];
+      if (F.npiv == 0) continue;
+      for (int32_t r0 = 0; r0 < F.nrow; r0 += kTile) s.work.push_back({f, r0, 0, 0});
+    }
+    if ((int64_t)s.work.size() > off) s.launches.push_back({L_ZPANEL, lv, off, (int64_t)s.work.size() - off});
   }
+  // solve work lists: gather (f), forward GEMV (f, row0, chunk, group), backward dots
+  // (f, col0, row chunk, group); each (front, tile) group combines its chunk partials
+  s.fwd_off.assign(s.n_levels, 0); s.fwd_cnt.assign(s.n_levels, 0);
+  s.bwd_off.assign(s.n_levels, 0); s.bwd_cnt.assign(s.n_levels, 0);
+  s.gat_off.assign(s.n_levels, 0); s.gat_cnt.assign(s.n_levels, 0);
+  s.lvl_max_piv.assign(s.n_levels, 0);
+  s.grp_nchunk.clear(); s.grp_base.clear();
+  s.part_doubles = 0;
+  auto new_group = [&](int32_t nch) {
+    s.grp_nchunk.push_back(nch);
+    s.grp_base.push_back(s.part_doubles);
+    s.part_doubles += (int64_t)nch * 32;
+    return (int32_t)s.grp_nchunk.size() - 1;
+  };
+  for (int32_t lv = 0; lv < s.n_levels; ++lv) {
+    s.gat_off[lv] = (int64_t)s.work.size();
+    for (int32_t f : s.level_fronts[lv]) {
+      s.lvl_max_piv[lv] = std::max(s.lvl_max_piv[lv], s.fronts[f].npiv);
+      s.work.push_back({f, 0, 0, 0});
+    }
+    s.gat_cnt[lv] = (int64_t)s.work.size() - s.gat_off[lv];
+    s.fwd_off[lv] = (int64_t)s.work.size();
+    for (int32_t f : s.level_fronts[lv]) {
+      const Front& F = s.fronts[f];
+      for (int32_t r0 = 0; r0 < F.nrow; r0 += kFwdRows) {
+        const int32_t cend = (r0 < F.npiv) ? std::min(F.npiv, r0 + kFwdRows) : F.npiv;
+        const int32_t nch = std::max(1, (cend + kFwdCols - 1) / kFwdCols);
+        const int32_t g = new_group(nch);
+        for (int32_t k = 0; k < nch; ++k) s.work.push_back({f, r0, k, g});
+      }
+    }
+    s.fwd_cnt[lv] = (int64_t)s.work.size() - s.fwd_off[lv];
+    s.bwd_off[lv] = (int64_t)s.work.size();
+    for (int32_t f : s.level_fronts[lv]) {
+      const Front& F = s.fronts[f];
+      for (int32_t c0 = 0; c0 < std::max(F.npiv, 1); c0 += kBwdCols) {
+        const int32_t rs = (c0 / kBwdRows) * kBwdRows;          // first chunk holding rows >= c0
+        const int32_t nch = std::max(1, (F.nrow - rs + kBwdRows - 1) / kBwdRows);
+        const int32_t g = new_group(nch);
+        for (int32_t k = 0; k < nch; ++k) s.work.push_back({f, c0, rs + k * kBwdRows, g});
+      }
+    }
+    s.bwd_cnt[lv] = (int64_t)s.work.size() - s.bwd_off[lv];
+  }
+  s.n_groups = (int64_t)s.grp_nchunk.size();
   return 0;
 }
 
