@@ -28,6 +28,7 @@
 
 using sgn::DFront;
 using sgn::kTile;
+using sgn::kPanelTiles;
 using sgn::Work;
 
 #define CUDA_TRY(expr)                                                              \
@@ -76,9 +77,13 @@ k_assemble(const Work* __restrict__ work, const DFront* __restrict__ fronts,
   for (int e = tid; e < kTile * kTile; e += blockDim.x) tile[e >> 5][e & 31] = 0.0;
   __syncthreads();
   const int64_t tid_g = F.tile_base + (int64_t)ti * (ti + 1) / 2 + tj;
-  for (int64_t e = tile_ptr[tid_g] + tid; e < tile_ptr[tid_g + 1]; e += blockDim.x) {
-    const int loc = tile_loc[e];
-    tile[loc >> 5][loc & 31] = vals[tile_nnz[e]];
+  {
+    const int64_t e0 = tile_ptr[tid_g], e1 = tile_ptr[tid_g + 1];
+#pragma unroll 4
+    for (int64_t e = e0 + tid; e < e1; e += kAsmThreads) {
+      const int loc = tile_loc[e];
+      tile[loc >> 5][loc & 31] = vals[tile_nnz[e]];
+    }
   }
   __syncthreads();
   if (ti == tj && tid < kTile) {
@@ -103,7 +108,8 @@ k_assemble(const Work* __restrict__ work, const DFront* __restrict__ fronts,
     if (nr > 0 && ns > 0) {
       const double* U = fb + C.foff;
       const int64_t ldc = C.nrow;
-      for (int idx = tid; idx < nr * ns; idx += blockDim.x) {
+#pragma unroll 4
+      for (int idx = tid; idx < nr * ns; idx += kAsmThreads) {
         const int r = r_lo + idx % nr, s = s_lo + idx / nr;
         if (r >= s) {
           const double u = U[(int64_t)(C.npiv + s) * ldc + C.npiv + r];
@@ -122,59 +128,110 @@ k_assemble(const Work* __restrict__ work, const DFront* __restrict__ fronts,
   }
 }
 
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
 // ------------------------------------------------------------------------------------
-// dense LDL^T of a <=32 x 32 diagonal block in shared memory (lower part used)
-// pivtype 2: 2x2 pivots on (2t, 2t+1); D stored in place, L strictly below the blocks.
-// returns first failing local pivot via *bad (min), else leaves it
+// One warp factors a <= 32 x 32 diagonal block held in shared memory (lane i owns row i):
+// LDL^T with 2x2 pivots on (2t, 2t+1) (pivtype 2) or 1x1 pivots; D stays in place, L below
+// the pivot blocks.  Rows live in registers; columns are exchanged with shuffles.
 // ------------------------------------------------------------------------------------
-__device__ void smem_ldlt(double (*D)[kTile + 1], int w, int pivtype, int* bad) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  if (pivtype == 2) {
-    for (int j = 0; j < w; j += 2) {
-      const double a = D[j][j], bb = D[j + 1][j], c = D[j + 1][j + 1];
-      const double det = a * c - bb * bb;
-      if (det == 0.0 || !isfinite(det)) { if (tid == 0) atomicMin(bad, j); }
-      const double ia = c / det, ib = -bb / det, ic = a / det;
-      const int m = w - j - 2;  // trailing size
-      for (int e = tid; e < m * m; e += nt) {
-        const int i = j + 2 + e % m, k = j + 2 + e / m;
-        if (i >= k) {
-          const double x0 = D[i][j], x1 = D[i][j + 1];
-          const double y0 = D[k][j], y1 = D[k][j + 1];
-          D[i][k] -= x0 * (ia * y0 + ib * y1) + x1 * (ib * y0 + ic * y1);
-        }
+// One warp factors the <= 32 x 32 diagonal block with rows in registers (lane i = row i).
+// Every shuffle is executed by all lanes (no divergent branch around it, so the compiler
+// emits native SHFL); inactive steps/rows are masked with selects.  Templated on the
+// pivot type so each instantiation stays small (~2k instructions).
+template <int PT>
+__device__ __forceinline__ void warp_ldlt_reg(double (*D)[kTile + 1], int w, int* bad, bool store) {
+  const int i = threadIdx.x & 31;
+  int first_bad = 1 << 30;
+  double d[kTile];
+#pragma unroll
+  for (int k = 0; k < kTile; ++k) d[k] = (k <= i) ? D[i][k] : 0.0;
+#pragma unroll
+  for (int j = 0; j < kTile; j += PT) {
+    const bool act = (j < w);
+    if (PT == 2) {
+      const double a = __shfl_sync(0xffffffffu, d[j], j);
+      const double bb = __shfl_sync(0xffffffffu, d[j], j + 1);
+      const double c = __shfl_sync(0xffffffffu, d[j + 1], j + 1);
+      double det = a * c - bb * bb;
+      first_bad = (act && (det == 0.0 || !isfinite(det)) && first_bad > j) ? j : first_bad;
+      det = act ? det : 1.0;
+      const double rdet = 1.0 / det;
+      const double ia = c * rdet, ib = -bb * rdet, ic = a * rdet;
+      const bool below = act && (i > j + 1) && (i < w);
+      const double x0 = d[j], x1 = d[j + 1];
+      const double l0 = below ? x0 * ia + x1 * ib : 0.0;
+      const double l1 = below ? x0 * ib + x1 * ic : 0.0;
+#pragma unroll
+      for (int k = j + 2; k < kTile; ++k) {
+        const double y0 = __shfl_sync(0xffffffffu, x0, k);
+        const double y1 = __shfl_sync(0xffffffffu, x1, k);
+        const double nd = d[k] - (l0 * y0 + l1 * y1);
+        d[k] = (below && k <= i) ? nd : d[k];
       }
-      __syncthreads();
-      for (int i = j + 2 + tid; i < w; i += nt) {
-        const double x0 = D[i][j], x1 = D[i][j + 1];
-        D[i][j] = x0 * ia + x1 * ib;
-        D[i][j + 1] = x0 * ib + x1 * ic;
+      d[j] = below ? l0 : d[j];
+      d[j + 1] = below ? l1 : d[j + 1];
+    } else {
+      double dj = __shfl_sync(0xffffffffu, d[j], j);
+      first_bad = (act && (dj == 0.0 || !isfinite(dj)) && first_bad > j) ? j : first_bad;
+      dj = act ? dj : 1.0;
+      const bool below = act && (i > j) && (i < w);
+      const double x = d[j];
+      const double l = below ? x / dj : 0.0;
+#pragma unroll
+      for (int k = j + 1; k < kTile; ++k) {
+        const double y = __shfl_sync(0xffffffffu, x, k);
+        const double nd = d[k] - l * y;
+        d[k] = (below && k <= i) ? nd : d[k];
       }
-      __syncthreads();
+      d[j] = below ? l : d[j];
     }
-  } else {
-    for (int j = 0; j < w; ++j) {
-      const double d = D[j][j];
-      if (d == 0.0 || !isfinite(d)) { if (tid == 0) atomicMin(bad, j); }
-      const double inv = 1.0 / d;
-      const int m = w - j - 1;
-      for (int e = tid; e < m * m; e += nt) {
-        const int i = j + 1 + e % m, k = j + 1 + e / m;
-        if (i >= k) D[i][k] -= D[i][j] * D[k][j] * inv;
-      }
-      __syncthreads();
-      for (int i = j + 1 + tid; i < w; i += nt) D[i][j] *= inv;
-      __syncthreads();
-    }
+  }
+  __syncthreads();   // all warps have read D before warp 0 overwrites it
+  if (store) {
+#pragma unroll
+    for (int k = 0; k < kTile; ++k) if (k <= i) D[i][k] = d[k];
+    if (i == 0 && first_bad < (1 << 30)) atomicMin(bad, first_bad);
   }
 }
 
-__global__ void __launch_bounds__(kPanelThreads)
+// TRSM of one 32-row tile (lane = row, row in registers): W L11^T = P, right-looking so
+// the FMAs of a step are independent; L11 columns are broadcast reads from smem.
+template <int PT>
+__device__ __forceinline__ void warp_trsm_reg(double (*P)[kTile + 1], const double (*D)[kTile + 1]) {
+  const int i = threadIdx.x & 31;
+  double p[kTile];
+#pragma unroll
+  for (int c = 0; c < kTile; ++c) p[c] = P[i][c];
+#pragma unroll
+  for (int cp = 0; cp < kTile; ++cp) {
+#pragma unroll
+    for (int c = cp + 1; c < kTile; ++c) {
+      if (PT == 2 && (cp & 1) == 0 && c == cp + 1) continue;   // D slot, compile-time
+      p[c] -= p[cp] * D[c][cp];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kTile; ++c) P[i][c] = p[c];
+}
+
+// Panel step k of a front: every CTA factors the diagonal block (one warp, registers +
+// smem; a few us), CTA t == 0 stores L11/D and the block inverse, CTAs t >= 1 form their
+// 32-row tile of W = P L11^{-T} on DMMA and L21 = W D^{-1}.
+template <int PT>
+__global__ void __launch_bounds__(kPanelThreads, 1)
 k_panel(const Work* __restrict__ work, const DFront* __restrict__ fronts,
         const int64_t* __restrict__ perm, double* __restrict__ fstore, int64_t fstride,
-        double* __restrict__ wstore, int64_t wstride, long long* __restrict__ status) {
+        double* __restrict__ wstore, int64_t wstride, double* __restrict__ dscr, int64_t dstride,
+        long long* __restrict__ status) {
   __shared__ double D[kTile][kTile + 1];
-  __shared__ double P[kTile][kTile + 1];
+  __shared__ double P[kPanelTiles][kTile][kTile + 1];
+  __shared__ double Dinv[kTile][3];      // per pivot block: (ia, ib, ic) or (1/d)
   __shared__ int bad;
   const Work wk = work[blockIdx.x];
   const int b = blockIdx.y;
@@ -182,63 +239,71 @@ k_panel(const Work* __restrict__ work, const DFront* __restrict__ fronts,
   const int j0 = wk.a * kTile;
   const int w = min(kTile, F.npiv - j0);
   const int t = wk.b;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
   double* Fm = fstore + (int64_t)b * fstride + F.foff;
   const int64_t ld = F.nrow;
   if (tid == 0) bad = 1 << 30;
-  for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+#pragma unroll
+  for (int e = tid; e < kTile * kTile; e += kPanelThreads) {   // loads all in flight
     const int i = e & 31, j = e >> 5;
     D[i][j] = (i < w && j < w && i >= j) ? Fm[(int64_t)(j0 + j) * ld + j0 + i] : 0.0;
   }
+  // this CTA: row tiles t .. t+3 below the diagonal block, warp w owns tile t+w
+  const int r0 = j0 + w + (t - 1 + warp) * kTile;
+  const int nr = (t > 0) ? max(0, min(kTile, F.nrow - r0)) : 0;
+  double (*Pw)[kTile + 1] = P[warp];
+  if (t > 0) {
+    double v[kTile];
+#pragma unroll
+    for (int j = 0; j < kTile; ++j) v[j] = (lane < nr && j < w) ? Fm[(int64_t)(j0 + j) * ld + r0 + lane] : 0.0;
+#pragma unroll
+    for (int j = 0; j < kTile; ++j) Pw[lane][j] = v[j];
+  }
   __syncthreads();
-  smem_ldlt(D, w, F.pivtype, &bad);
-  if (t == 0) {
-    if (tid == 0 && bad < (1 << 30))
-      atomicMin(&status[b], (long long)perm[F.first + j0 + bad]);
-    for (int e = tid; e < kTile * kTile; e += blockDim.x) {
-      const int i = e & 31, j = e >> 5;
-      if (i < w && j < w && i >= j) Fm[(int64_t)(j0 + j) * ld + j0 + i] = D[i][j];
+  warp_ldlt_reg<PT>(D, w, &bad, warp == 0);   // every warp runs it (converged shuffles);
+  __syncthreads();                             // only warp 0 stores the result
+  if (tid < w) {
+    if (PT == 2) {
+      if ((tid & 1) == 0) {
+        const double a = D[tid][tid], bb = D[tid + 1][tid], cc = D[tid + 1][tid + 1];
+        const double rdet = 1.0 / (a * cc - bb * bb);
+        Dinv[tid][0] = cc * rdet; Dinv[tid][1] = -bb * rdet; Dinv[tid][2] = a * rdet;
+      }
+    } else {
+      Dinv[tid][0] = 1.0 / D[tid][tid];
     }
+  }
+  __syncthreads();
+  if (t == 0) {
+    // the factored block goes to scratch: other CTAs of this launch may still be reading
+    // the unfactored block from F (k_zpanel copies it into F at the end of the level)
+    if (tid == 0 && bad < (1 << 30)) atomicMin(&status[b], (long long)perm[F.first + j0 + bad]);
+    double* ds = dscr + (int64_t)b * dstride + F.doff + (int64_t)wk.a * kTile * kTile;
+    for (int e = tid; e < kTile * kTile; e += blockDim.x) ds[e] = D[e >> 5][e & 31];
     return;
   }
-  const int r0 = j0 + w + (t - 1) * kTile;
-  const int nr = min(kTile, F.nrow - r0);
-  for (int e = tid; e < kTile * kTile; e += blockDim.x) {
-    const int i = e & 31, j = e >> 5;
-    P[i][j] = (i < nr && j < w) ? Fm[(int64_t)(j0 + j) * ld + r0 + i] : 0.0;
-  }
-  __syncthreads();
-  // W = P L11^{-T}: row-wise forward substitution (thread per row)
-  if (tid < nr) {
-    const int i = tid;
-    for (int c = 0; c < w; ++c) {
-      double acc = P[i][c];
-      for (int cp = 0; cp < c; ++cp) {
-        if (F.pivtype == 2 && (cp & 1) == 0 && cp + 1 == c) continue;  // D off-diagonal slot
-        acc -= P[i][cp] * D[c][cp];
-      }
-      P[i][c] = acc;
-    }
-  }
-  __syncthreads();
-  double* Wb = wstore + (int64_t)b * wstride + F.woff + (int64_t)(t - 1) * kTile * kTile;
-  for (int e = tid; e < nr * kTile; e += blockDim.x) {
+  // W = P L11^{-T} by row-wise substitution (lane per row of the warp's tile, row in
+  // registers, right-looking so the FMAs are independent; explicit inverses would
+  // amplify rounding in the factor itself)
+  if (nr > 0) warp_trsm_reg<PT>(Pw, D);   // W = P L11^{-T}: substitution, no explicit inverse
+  __syncwarp();
+  if (nr == 0) return;
+  double* Wb = wstore + (int64_t)b * wstride + F.woff + (int64_t)(t - 1 + warp) * kTile * kTile;
+  for (int e = lane; e < nr * kTile; e += 32) {
     const int i = e / kTile, c = e % kTile;
-    Wb[(int64_t)i * kTile + c] = (c < w) ? P[i][c] : 0.0;
+    Wb[(int64_t)i * kTile + c] = (c < w) ? Pw[i][c] : 0.0;
   }
-  // L21 = W D^{-1}
-  for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+  // L21 = W D^{-1} with the pivot-block inverses precomputed in Dinv (no divisions here)
+  for (int e = lane; e < kTile * kTile; e += 32) {
     const int i = e & 31, c = e >> 5;
     if (i >= nr || c >= w) continue;
     double l;
-    if (F.pivtype == 2) {
+    if (PT == 2) {
       const int c0 = c & ~1;
-      const double a = D[c0][c0], bb = D[c0 + 1][c0], cc = D[c0 + 1][c0 + 1];
-      const double det = a * cc - bb * bb;
-      const double x0 = P[i][c0], x1 = P[i][c0 + 1];
-      l = (c == c0) ? (x0 * cc - x1 * bb) / det : (x1 * a - x0 * bb) / det;
+      const double x0 = Pw[i][c0], x1 = Pw[i][c0 + 1];
+      l = (c == c0) ? x0 * Dinv[c0][0] + x1 * Dinv[c0][1] : x0 * Dinv[c0][1] + x1 * Dinv[c0][2];
     } else {
-      l = P[i][c] / D[c][c];
+      l = Pw[i][c] * Dinv[c][0];
     }
     Fm[(int64_t)(j0 + c) * ld + r0 + i] = l;
   }
@@ -249,12 +314,6 @@ k_panel(const Work* __restrict__ work, const DFront* __restrict__ fronts,
 //   C[i, j] -= sum_c L21[i, c] * W[j, c]       (W = L21 D, row-major scratch)
 // mma.sync.aligned.m8n8k4.row.col.f64: A 8x4 (row), B 4x8 (col), C 8x8.
 // ------------------------------------------------------------------------------------
-__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-  asm volatile(
-      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(d0), "+d"(d1)
-      : "d"(a), "d"(b));
-}
 
 __global__ void __launch_bounds__(kUpdThreads)
 k_update(const Work* __restrict__ work, const DFront* __restrict__ fronts,
@@ -275,11 +334,13 @@ k_update(const Work* __restrict__ work, const DFront* __restrict__ fronts,
   double* Fm = fstore + (int64_t)b * fstride + F.foff;
   const int64_t ld = F.nrow;
   const double* Wb = wstore + (int64_t)b * wstride + F.woff;
-  for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+#pragma unroll
+  for (int e = tid; e < kTile * kTile; e += kUpdThreads) {
     const int i = e & 31, c = e >> 5;
     As[i][c] = (i < nr && c < w) ? Fm[(int64_t)(j0 + c) * ld + rbase + i] : 0.0;
   }
-  for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+#pragma unroll
+  for (int e = tid; e < kTile * kTile; e += kUpdThreads) {
     const int c = e & 31, j = e >> 5;
     Bs[j][c] = (j < nc && c < w) ? Wb[(int64_t)(tj * kTile + j) * kTile + c] : 0.0;
   }
@@ -329,8 +390,8 @@ __device__ __forceinline__ bool pair_skip(int pivtype, int row, int col) {
 constexpr int kZThreads = 256;
 __global__ void __launch_bounds__(kZThreads)
 k_zpanel(const Work* __restrict__ work, const DFront* __restrict__ fronts,
-         const double* __restrict__ fstore, int64_t fstride, double* __restrict__ zstore,
-         int64_t zstride) {
+         double* __restrict__ fstore, int64_t fstride, double* __restrict__ zstore,
+         int64_t zstride, const double* __restrict__ dscr, int64_t dstride) {
   __shared__ double Ts[kTile][kTile + 1];          // final Z block of the step (rows x cols)
   __shared__ double Ls[kTile][kTile + 1];          // diagonal block of L11
   const Work wk = work[blockIdx.x];
@@ -340,10 +401,19 @@ k_zpanel(const Work* __restrict__ work, const DFront* __restrict__ fronts,
   const int nr = min(kTile, F.nrow - r0);
   const int npiv = F.npiv;
   const int64_t ld = F.nrow;
-  const double* Fm = fstore + (int64_t)b * fstride + F.foff;
+  double* Fm = fstore + (int64_t)b * fstride + F.foff;
   double* Zm = zstore + (int64_t)b * zstride + F.zoff;
+  const double* ds = dscr + (int64_t)b * dstride + F.doff;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
   const int cmax = (r0 < npiv) ? min(npiv, r0 + nr) : npiv;
+  if (r0 < npiv) {   // this row tile owns diagonal block r0/32: publish the factored block to F
+    const double* blk = ds + (int64_t)(r0 / kTile) * kTile * kTile;
+    const int wd = min(kTile, npiv - r0);
+    for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+      const int i = e >> 5, j = e & 31;
+      if (i < wd && j < wd && i >= j) Fm[(int64_t)(r0 + j) * ld + r0 + i] = blk[e];
+    }
+  }
   const int nb = (cmax + kTile - 1) / kTile;
   // Z <- B  (identity rows for pivots, L21 rows for the structure)
   for (int e = tid; e < nr * cmax; e += blockDim.x) {
@@ -354,20 +424,26 @@ k_zpanel(const Work* __restrict__ work, const DFront* __restrict__ fronts,
   for (int cbi = nb - 1; cbi >= 0; --cbi) {
     const int cb = cbi * kTile;
     const int wb = min(kTile, npiv - cb);
-    for (int e = tid; e < kTile * kTile; e += blockDim.x) {
+#pragma unroll
+    for (int e = tid; e < kTile * kTile; e += kZThreads) {
       const int i = e & 31, c = e >> 5;
       Ts[i][c] = (i < nr && c < wb) ? Zm[(int64_t)(cb + c) * ld + r0 + i] : 0.0;
       const int cp = e & 31;
       Ls[cp][c] = (cp < wb && c < wb && cp > c && !pair_skip(F.pivtype, cp, c))
-                      ? Fm[(int64_t)(cb + c) * ld + cb + cp] : 0.0;
+                      ? ds[(int64_t)cbi * kTile * kTile + cp * kTile + c] : 0.0;
     }
     __syncthreads();
-    if (warp == 0 && lane < nr) {     // z L11blk = t, right to left
-      for (int c = wb - 1; c >= 0; --c) {
-        double z = Ts[lane][c];
-        for (int cp = c + 1; cp < wb; ++cp) z -= Ts[lane][cp] * Ls[cp][c];
-        Ts[lane][c] = z;
+    if (warp == 0) {   // z Lblk = t, right to left, row in registers (independent FMAs)
+      double z[kTile];
+#pragma unroll
+      for (int c = 0; c < kTile; ++c) z[c] = Ts[lane][c];
+#pragma unroll
+      for (int c = kTile - 1; c > 0; --c) {
+#pragma unroll
+        for (int cc = 0; cc < c; ++cc) z[cc] -= z[c] * Ls[c][cc];
       }
+#pragma unroll
+      for (int c = 0; c < kTile; ++c) Ts[lane][c] = z[c];
     }
     __syncthreads();
     for (int e = tid; e < kTile * kTile; e += blockDim.x) {
@@ -820,7 +896,7 @@ struct sgn_factor_s {
   DevBuf<int64_t> srows, perm, tile_ptr, tile_nnz, indptr;
   DevBuf<int8_t> kind_pos;
   DevBuf<Work> work;
-  DevBuf<double> fstore, wstore, ubuf, vbuf, y, zstore, zbuf, xbuf, part;
+  DevBuf<double> fstore, wstore, ubuf, vbuf, y, zstore, zbuf, xbuf, part, dscr;
   DevBuf<int> tickets;
   DevBuf<int32_t> grp_nchunk;
   DevBuf<int64_t> grp_base;
@@ -1058,7 +1134,7 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
     DFront& d = df[k];
     d.first = F.first; d.foff = F.foff; d.srow_off = F.srow_off; d.rel_off = F.rel_off;
     d.uoff = F.uoff; d.woff = F.woff; d.voff = F.voff; d.tile_base = F.tile_base;
-    d.zoff = F.zoff; d.pad0 = 0;
+    d.zoff = F.zoff; d.doff = F.doff;
     d.npiv = F.npiv; d.nrow = F.nrow; d.parent = F.parent; d.pivtype = F.pivtype;
     d.child_begin = F.child_begin; d.child_end = F.child_end; d.is_root_p = F.is_root_p;
     d.level = F.level;
@@ -1091,6 +1167,7 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
       (rc = f->xbuf.alloc(B * std::max<int64_t>(s.n, 1))))
     return rc;
   if ((rc = f->part.alloc(B * std::max<int64_t>(s.part_doubles, 1))) ||
+      (rc = f->dscr.alloc(B * std::max<int64_t>(s.d_doubles, 1))) ||
       (rc = f->tickets.alloc(B * std::max<int64_t>(s.n_groups, 1))) ||
       (rc = f->grp_nchunk.upload(s.grp_nchunk)) || (rc = f->grp_base.upload(s.grp_base)))
     return rc;
@@ -1124,14 +1201,19 @@ int sgn_factor_numeric(sgn_factor f, const double* d_values, int64_t values_stri
         break;
       case sgn::L_PANEL:
         sgn::count_launch();
-        k_panel<<<grid, kPanelThreads, 0, st>>>(w, f->fronts.p, f->perm.p, f->fstore.p,
+        if (L.pivtype == 2)
+          k_panel<2><<<grid, kPanelThreads, 0, st>>>(w, f->fronts.p, f->perm.p, f->fstore.p,
                                                 s.front_doubles, f->wstore.p, s.w_doubles,
-                                                f->status.p);
+                                                f->dscr.p, s.d_doubles, f->status.p);
+        else
+        k_panel<1><<<grid, kPanelThreads, 0, st>>>(w, f->fronts.p, f->perm.p, f->fstore.p,
+                                                s.front_doubles, f->wstore.p, s.w_doubles,
+                                                f->dscr.p, s.d_doubles, f->status.p);
         break;
       case sgn::L_ZPANEL:
         sgn::count_launch();
         k_zpanel<<<grid, kZThreads, 0, st>>>(w, f->fronts.p, f->fstore.p, s.front_doubles,
-                                               f->zstore.p, s.z_doubles);
+                                               f->zstore.p, s.z_doubles, f->dscr.p, s.d_doubles);
         break;
       case sgn::L_UPDATE:
         sgn::count_launch();

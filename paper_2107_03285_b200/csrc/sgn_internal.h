@@ -8,6 +8,7 @@
 namespace sgn {
 
 constexpr int kTile = 32;   // assembly tile, panel width, update tile
+constexpr int kPanelTiles = 4;   // 32-row tiles per panel CTA (one per warp)
 
 // One dense front (supernode) of the multifrontal assembly tree.
 struct Front {
@@ -27,6 +28,7 @@ struct Front {
   int64_t voff = 0;       // offset of the solve front vector (nrow)
   int64_t tile_base = 0;  // first assembly tile id
   int64_t zoff = 0;       // offset of the solve panel Z = [I; L21] L11^{-1} (nrow x npiv)
+  int64_t doff = 0;       // offset of the 32x32 diagonal-block inverses of L11
 };
 
 // Device-side mirror of Front (POD, 16-byte aligned for vector loads).
@@ -40,7 +42,7 @@ struct DFront {
   int64_t voff;
   int64_t tile_base;
   int64_t zoff;
-  int64_t pad0;
+  int64_t doff;
   int32_t npiv, nrow, parent, pivtype;
   int32_t child_begin, child_end, is_root_p, level;
 };
@@ -52,7 +54,7 @@ constexpr int kFwdRows = 32;    // rows per CTA of the forward-solve GEMV
 constexpr int kFwdCols = 64;    // columns (K chunk) per CTA of the forward-solve GEMV
 constexpr int kBwdCols = 32;    // columns per CTA of the backward-solve dots
 constexpr int kBwdRows = 256;   // rows (K chunk) per CTA of the backward-solve dots
-struct Launch { int32_t kind; int32_t level; int64_t off; int64_t count; };
+struct Launch { int32_t kind; int32_t level; int64_t off; int64_t count; int32_t pivtype = 1; int32_t pad = 0; };
 
 struct Symbolic {
   int64_t n = 0, n_x = 0, n_p = 0, n_c = 0;
@@ -83,7 +85,7 @@ struct Symbolic {
   std::vector<int64_t> grp_base;
   int64_t n_groups = 0, part_doubles = 0;
   // sizes
-  int64_t front_doubles = 0, u_doubles = 0, w_doubles = 0, v_doubles = 0, z_doubles = 0;
+  int64_t front_doubles = 0, u_doubles = 0, w_doubles = 0, v_doubles = 0, z_doubles = 0, d_doubles = 0;
   int64_t nnz_l = 0; double flops = 0; int64_t max_front = 0, max_piv = 0;
 };
 

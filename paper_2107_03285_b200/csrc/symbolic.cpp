@@ -628,7 +628,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   s.level_fronts.assign(s.n_levels, {});
   for (int32_t k = 0; k < NF; ++k) s.level_fronts[s.fronts[k].level].push_back(k);
 
-  s.front_doubles = s.u_doubles = s.w_doubles = s.v_doubles = s.z_doubles = 0;
+  s.front_doubles = s.u_doubles = s.w_doubles = s.v_doubles = s.z_doubles = s.d_doubles = 0;
   s.ntiles = 0;
   s.nnz_l = 0;
   s.flops = 0;
@@ -640,6 +640,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     F.woff = s.w_doubles; s.w_doubles += nr * kTile;
     F.voff = s.v_doubles; s.v_doubles += nr;
     F.zoff = s.z_doubles; s.z_doubles += nr * F.npiv;
+    F.doff = s.d_doubles; s.d_doubles += (int64_t)((F.npiv + kTile - 1) / kTile) * kTile * kTile;
     const int64_t T = (nr + kTile - 1) / kTile;
     F.tile_base = s.ntiles; s.ntiles += T * (T + 1) / 2;
     s.nnz_l += (int64_t)F.npiv * (F.npiv + 1) / 2 + (int64_t)F.npiv * ns;
@@ -722,17 +723,24 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     int32_t maxp = 0;
     for (int32_t f : fl) maxp = std::max(maxp, (s.fronts[f].npiv + kTile - 1) / kTile);
     for (int32_t k = 0; k < maxp; ++k) {
-      off = (int64_t)s.work.size();
-      for (int32_t f : fl) {
-        const Front& F = s.fronts[f];
-        const int32_t j0 = k * kTile;
-        if (j0 >= F.npiv) continue;
-        const int32_t w = std::min(kTile, F.npiv - j0);
-        const int32_t below = F.nrow - j0 - w;
-        const int32_t nt = (below + kTile - 1) / kTile;
-        for (int32_t t = 0; t <= nt; ++t) s.work.push_back({f, k, t, 0});
+      for (int32_t pt = 1; pt <= 2; ++pt) {      // one panel launch per pivot type
+        off = (int64_t)s.work.size();
+        for (int32_t f : fl) {
+          const Front& F = s.fronts[f];
+          const int32_t j0 = k * kTile;
+          if (j0 >= F.npiv || F.pivtype != pt) continue;
+          const int32_t w = std::min(kTile, F.npiv - j0);
+          const int32_t below = F.nrow - j0 - w;
+          const int32_t nt = (below + kTile - 1) / kTile;        // 32-row tiles below
+          s.work.push_back({f, k, 0, 0});                         // diagonal-block CTA
+          for (int32_t t = 1; t <= nt; t += kPanelTiles) s.work.push_back({f, k, t, 0});
+        }
+        if ((int64_t)s.work.size() > off) {
+          Launch L{L_PANEL, lv, off, (int64_t)s.work.size() - off};
+          L.pivtype = pt;
+          s.launches.push_back(L);
+        }
       }
-      if ((int64_t)s.work.size() > off) s.launches.push_back({L_PANEL, lv, off, (int64_t)s.work.size() - off});
       off = (int64_t)s.work.size();
       for (int32_t f : fl) {
         const Front& F = s.fronts[f];
