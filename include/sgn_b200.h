@@ -91,6 +91,13 @@ void sgn_symbolic_destroy(sgn_symbolic s);
 int  sgn_factor_create(sgn_symbolic s, int32_t batch, sgn_factor* out);
 int  sgn_factor_numeric(sgn_factor f, const double* d_values, int64_t values_stride,
                         double eps_x, double eps_lambda, void* stream);
+/* as sgn_factor_numeric with per-instance shifts (device arrays of length batch; either may
+ * be NULL = 0): the batched tau-regularized Newton of forward.py:171-186 needs one tau per
+ * instance.                                                                           */
+int  sgn_factor_numeric_v(sgn_factor f, const double* d_values, int64_t values_stride,
+                          const double* d_eps_x, const double* d_eps_lambda, void* stream);
+/* synchronizes; pivots[b] = first zero pivot of instance b (original index) or -1 */
+int  sgn_factor_status(sgn_factor f, void* stream, int64_t* pivots);
 /* synchronizes; returns SGN_SINGULAR with the first zero pivot (original index) */
 int  sgn_factor_check(sgn_factor f, void* stream, int64_t* pivot_index);
 /* x = (L D L^T)^{-1} b for every instance (b, x strided by n). Replaces
@@ -151,6 +158,10 @@ int  sgn_reduce(int32_t op, int64_t n, int32_t batch, const double* d_a, const d
 /* out = y + alpha[b] * x  (per-instance step length; forward.py:197-199, optimize.py:472) */
 int  sgn_axpy(int64_t n, int32_t batch, const double* d_alpha, const double* d_x,
               const double* d_y, double* d_out, int64_t stride, void* stream);
+/* dst[b] = src[b] for every instance b with mask[b] != 0 (per-instance acceptance in the
+ * batched Newton / line search, forward.py:197-201, optimize.py:485-486)               */
+int  sgn_masked_copy(int64_t n, int32_t batch, const int32_t* d_mask, const double* d_src,
+                     double* d_dst, int64_t stride, void* stream);
 /* least-squares terms: d_vec (KKT order, dim = 2 n_x + n_p per instance) receives
  * (df/dx, df/dp, 0) for r = (x[tdofs] - tvals, p) with weights (w_t, w_reg);
  * d_fobj[b] = 0.5 sum w r^2 (sensitivity.py:83-93).  Either output may be NULL.      */

@@ -40,6 +40,22 @@ def sheet_mesh(n_w: int, n_h: int):
     return X0, np.array(tris, dtype=np.int64)
 
 
+def _repair_rest(X0, tris, pm_dof, p0, half, rng, n_w, n_h):
+    nominal = 0.5 / ((n_w - 1) * (n_h - 1))
+    vert_of_p = pm_dof // 2
+    while True:
+        X = X0.ravel().copy()
+        X[pm_dof] += p0
+        X = X.reshape(-1, 2)
+        e1, e2 = X[tris[:, 1]] - X[tris[:, 0]], X[tris[:, 2]] - X[tris[:, 0]]
+        bad = (0.5 * (e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0])) < 0.2 * nominal
+        if not bad.any():
+            return p0
+        redo = np.isin(vert_of_p, np.unique(tris[bad]))
+        p0 = p0.copy()
+        p0[redo] = rng.uniform(-half, half, int(redo.sum()))
+
+
 def sheet_spec(config: int, seed: int = 0, instance: int = 0):
     """Arrays defining sheet config 1 (20x20) or 2 (100x100; also config-5 instances).
 
@@ -68,18 +84,11 @@ def sheet_spec(config: int, seed: int = 0, instance: int = 0):
     else:
         pm_dof = (rows[:, None] * 2 + np.arange(2)[None, :]).ravel()
         half = 0.005
-    # redraw (same stream) until no rest triangle keeps < 20% of its nominal area:
-    # U(-0.005, 0.005) tangential offsets on the 100x100 grid (h = 0.0101) can invert
-    # boundary triangles, leaving no equilibrium (config resolution)
-    nominal = 0.5 / ((n_w - 1) * (n_h - 1))
-    while True:
-        p0 = rng.uniform(-half, half, pm_dof.size)
-        X = X0.ravel().copy()
-        X[pm_dof] += p0
-        X = X.reshape(-1, 2)
-        e1, e2 = X[tris[:, 1]] - X[tris[:, 0]], X[tris[:, 2]] - X[tris[:, 0]]
-        if (0.5 * (e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0])).min() >= 0.2 * nominal:
-            break
+    # draw, then redraw (same stream) only the parameters of rest triangles that keep < 20%
+    # of their nominal area: U(-0.005, 0.005) tangential offsets on the 100x100 grid
+    # (h = 0.0101) can invert boundary triangles, leaving no equilibrium
+    p0 = rng.uniform(-half, half, pm_dof.size)
+    p0 = _repair_rest(X0, tris, pm_dof, p0, half, rng, n_w, n_h)
     pmap = (pm_dof, np.arange(pm_dof.size), np.ones(pm_dof.size))
     free_verts = np.setdiff1d(np.arange(n_w * n_h), fixed)
     vert_to_free = -np.ones(n_w * n_h, dtype=np.int64)
@@ -89,12 +98,15 @@ def sheet_spec(config: int, seed: int = 0, instance: int = 0):
         sigma = 0.02
     else:
         interior = np.array([i * n_h + j for i in range(1, n_w - 1) for j in range(1, n_h - 1)])
-        tv = np.sort(rng.choice(interior, size=200, replace=False))
+        if instance == 0:
+            tv = np.sort(rng.choice(interior, size=200, replace=False))
+        else:   # config-5 instances share the target vertex set (one KKT pattern), own offsets
+            tv = sheet_spec(config, seed, 0)["target_verts"]
         sigma = 0.01
     tdofs = (vert_to_free[tv][:, None] * 2 + np.arange(2)[None, :]).ravel()
     tvals = X0[tv].ravel() + rng.normal(0.0, sigma, tdofs.size)
     return dict(X0=X0, conn=tris, kind="tri", fixed_verts=fixed, pmap=pmap, target_dofs=tdofs,
-                target_vals=tvals, w_target=1.0, w_reg=2e-6, E=E, nu=nu,
+                target_vals=tvals, target_verts=tv, w_target=1.0, w_reg=2e-6, E=E, nu=nu,
                 gload=RHO_SHEET * GRAVITY, p0=p0, name=f"sheet_c{config}")
 
 
@@ -103,4 +115,5 @@ def oracle_sheet(config: int, seed: int = 0, instance: int = 0):
     spec = sheet_spec(config, seed, instance)
     p0 = spec.pop("p0")
     spec.pop("name")
+    spec.pop("target_verts")
     return ElementProblem(**spec), p0

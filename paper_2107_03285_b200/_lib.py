@@ -43,7 +43,10 @@ SIGNATURES = {
     "sgn_symbolic_destroy": (None, [c_vp]),
     "sgn_factor_create": (ctypes.c_int, [c_vp, c_i32, ctypes.POINTER(c_vp)]),
     "sgn_factor_numeric": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp]),
+    "sgn_factor_numeric_v": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "sgn_factor_check": (ctypes.c_int, [c_vp, c_vp, P_i64]),
+    "sgn_factor_status": (ctypes.c_int, [c_vp, c_vp, P_i64]),
+    "sgn_masked_copy": (ctypes.c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "sgn_factor_solve": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
     "sgn_factor_destroy": (None, [c_vp]),
     "sgn_spmv": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp]),

@@ -65,6 +65,7 @@ k_assemble(const Work* __restrict__ work, const DFront* __restrict__ fronts,
            const int64_t* __restrict__ tile_ptr, const int64_t* __restrict__ tile_nnz,
            const int32_t* __restrict__ tile_loc, const int8_t* __restrict__ kind_pos,
            const double* __restrict__ values, int64_t vstride, double eps_x, double eps_l,
+           const double* __restrict__ eps_xv, const double* __restrict__ eps_lv,
            double* __restrict__ fstore, int64_t fstride) {
   __shared__ double tile[kTile][kTile + 1];
   const Work w = work[blockIdx.x];
@@ -90,8 +91,8 @@ k_assemble(const Work* __restrict__ work, const DFront* __restrict__ fronts,
     const int r = ti * kTile + tid;
     if (r < F.npiv) {
       const int8_t k = kind_pos[F.first + r];
-      if (k == 1) tile[tid][tid] += eps_x;
-      else if (k == 2) tile[tid][tid] -= eps_l;
+      if (k == 1) tile[tid][tid] += eps_xv ? eps_xv[b] : eps_x;
+      else if (k == 2) tile[tid][tid] -= eps_lv ? eps_lv[b] : eps_l;
     }
   }
   const int i0 = ti * kTile, i1 = min(i0 + kTile, F.nrow);
@@ -1178,8 +1179,23 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
   return SGN_OK;
 }
 
+static int factor_numeric_impl(sgn_factor f, const double* d_values, int64_t values_stride,
+                               double eps_x, double eps_lambda, const double* d_eps_x,
+                               const double* d_eps_l, void* stream);
+
 int sgn_factor_numeric(sgn_factor f, const double* d_values, int64_t values_stride, double eps_x,
                        double eps_lambda, void* stream) {
+  return factor_numeric_impl(f, d_values, values_stride, eps_x, eps_lambda, nullptr, nullptr, stream);
+}
+
+int sgn_factor_numeric_v(sgn_factor f, const double* d_values, int64_t values_stride,
+                         const double* d_eps_x, const double* d_eps_lambda, void* stream) {
+  return factor_numeric_impl(f, d_values, values_stride, 0.0, 0.0, d_eps_x, d_eps_lambda, stream);
+}
+
+static int factor_numeric_impl(sgn_factor f, const double* d_values, int64_t values_stride,
+                               double eps_x, double eps_lambda, const double* d_eps_x,
+                               const double* d_eps_l, void* stream) {
   const sgn::Symbolic& s = f->sym->s;
   cudaStream_t st = (cudaStream_t)stream;
   {
@@ -1197,7 +1213,8 @@ int sgn_factor_numeric(sgn_factor f, const double* d_values, int64_t values_stri
         k_assemble<<<grid, kAsmThreads, 0, st>>>(w, f->fronts.p, f->children.p, f->rel.p,
                                                  f->tile_ptr.p, f->tile_nnz.p, f->tile_loc.p,
                                                  f->kind_pos.p, d_values, values_stride, eps_x,
-                                                 eps_lambda, f->fstore.p, s.front_doubles);
+                                                 eps_lambda, d_eps_x, d_eps_l, f->fstore.p,
+                                                 s.front_doubles);
         break;
       case sgn::L_PANEL:
         sgn::count_launch();
@@ -1238,6 +1255,15 @@ int sgn_factor_check(sgn_factor f, void* stream, int64_t* pivot_index) {
       return SGN_SINGULAR;
     }
   if (pivot_index) *pivot_index = -1;
+  return SGN_OK;
+}
+
+int sgn_factor_status(sgn_factor f, void* stream, int64_t* pivots) {
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<long long> h(f->batch);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), f->status.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int b = 0; b < f->batch; ++b) pivots[b] = (h[b] == (long long)INT64_MAX) ? -1 : (int64_t)h[b];
   return SGN_OK;
 }
 

@@ -117,6 +117,15 @@ __global__ void k_adjoint(int mode, int64_t n_x, int64_t n_p, const double* __re
   }
 }
 
+// dst[b] = src[b] for instances with mask[b] != 0
+__global__ void k_masked_copy(int64_t n, const int32_t* __restrict__ mask, const double* __restrict__ src,
+                              double* __restrict__ dst, int64_t stride) {
+  const int b = blockIdx.y;
+  if (!mask[b]) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[(int64_t)b * stride + i] = src[(int64_t)b * stride + i];
+}
+
 }  // namespace
 
 #define VEC_CHECK()                                                                \
@@ -149,6 +158,16 @@ int sgn_axpy(int64_t n, int32_t batch, const double* d_alpha, const double* d_x,
   const dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 1024), batch);
   sgn::count_launch();
   k_axpy<<<g, 256, 0, (cudaStream_t)stream>>>(n, d_alpha, d_x, d_y, d_out, stride);
+  VEC_CHECK();
+  return SGN_OK;
+}
+
+int sgn_masked_copy(int64_t n, int32_t batch, const int32_t* d_mask, const double* d_src,
+                    double* d_dst, int64_t stride, void* stream) {
+  if (n == 0) return SGN_OK;
+  const dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 1024), batch);
+  sgn::count_launch();
+  k_masked_copy<<<g, 256, 0, (cudaStream_t)stream>>>(n, d_mask, d_src, d_dst, stride);
   VEC_CHECK();
   return SGN_OK;
 }

@@ -104,6 +104,18 @@ class DeviceFactor:
         check(lib().sgn_factor_numeric(self._h, ptr(values), stride, float(eps_x),
                                        float(eps_lambda), stream), what="numeric factorization")
 
+    def numeric_v(self, values, eps_x_dev, eps_lambda_dev=None, stream: int = 0):
+        """Per-instance shifts (device float64 arrays of length batch)."""
+        stride = values.stride(0) if values.dim() == 2 else 0
+        check(lib().sgn_factor_numeric_v(self._h, ptr(values), stride, ptr(eps_x_dev),
+                                         ptr(eps_lambda_dev), stream), what="numeric factorization")
+
+    def status(self, stream: int = 0) -> np.ndarray:
+        """First zero pivot per instance (-1 = none); synchronizes."""
+        out = np.empty(self.batch, dtype=np.int64)
+        check(lib().sgn_factor_status(self._h, stream, out.ctypes.data_as(P_i64)), what="factor status")
+        return out
+
     def check(self, stream: int = 0) -> None:
         piv = ctypes.c_int64(-1)
         rc = lib().sgn_factor_check(self._h, stream, ctypes.byref(piv))

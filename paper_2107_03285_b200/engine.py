@@ -238,6 +238,7 @@ class DeviceEngine:
         self.G_diag = T(pl.G_diag, i64)
         self.grad_base, self.grad_ptr, self.grad_src = T(pl.grad_base), T(pl.grad_ptr, i64), T(pl.grad_src, i64)
         self.f_ext = T(pl.f_ext)
+        self.f_ext_b = self.f_ext.reshape(1, -1).repeat(B, 1).contiguous()
         nd2 = pl.n_e * pl.nd * pl.nd
         z = lambda *s: torch.zeros(*s, dtype=f64, device=dev)
         self.x = z(B, pl.n_x)
@@ -256,7 +257,7 @@ class DeviceEngine:
         self.tmp = z(B, pl.dim)
         self.grad = z(B, pl.n_p)
         self.fobj = z(B)
-        self.scal = z(8, B)
+        self.scal = z(8, B)              # rows: energy, linear energy, trace, |g|inf, ...
         self.gx = z(B, pl.n_x)
         self.kdir = z(B, pl.n_x)
         self.xtry = z(B, pl.n_x)
@@ -353,7 +354,7 @@ class DeviceEngine:
                                             ptr(self.eener), ptr(self.egrad) if want_grad else 0,
                                             pl.n_e * pl.nd, st))
         check(lib().sgn_reduce(0, pl.n_e, self.batch, ptr(self.eener), None, pl.n_e, ptr(self.scal[0]), st))
-        check(lib().sgn_reduce(1, pl.n_dof, self.batch, ptr(self.f_ext.expand(self.batch, -1).contiguous()),
+        check(lib().sgn_reduce(1, pl.n_dof, self.batch, ptr(self.f_ext_b),
                                ptr(self.pos), pl.n_dof, ptr(self.scal[1]), st))
         if want_grad:
             self._gather(pl.n_x, self.grad_base, 0, self.grad_ptr, self.grad_src, None, self.egrad,
@@ -373,85 +374,123 @@ class DeviceEngine:
             self._gfac = DeviceFactor(self.gsym, self.batch)
         return self._gfac
 
-    def simulate(self, tol: float, max_iters: int = 200):
-        """Newton with energy backtracking from the current self.x (batch == 1 path)."""
-        if self.batch != 1:
-            return self.simulate_batched(tol, max_iters)
+    def _trace(self):
+        """Per-instance trace of the Newton Hessian (gathered on the device)."""
+        pl = self.plan
+        if not hasattr(self, "_diag_ptr"):
+            T = lambda a, dt: self.torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device="cuda")
+            self._diag_ptr = T(np.array([0, pl.G_diag.size]), self.torch.int64)
+            self._diag_idx = T(pl.G_diag, self.torch.int64)
+        self._gather(1, None, 0, self._diag_ptr, self._diag_idx, None, self.gvals, pl.G_nnz,
+                     self.scal[2], 1)
+        return self.scal[2].cpu().numpy()
+
+    def _mask(self, m):
+        return self.torch.as_tensor(np.asarray(m, dtype=np.int32), device="cuda")
+
+    def simulate(self, tol: float, max_iters: int = 200, active=None):
+        """Batched damped Newton on the energy from the current x (forward.py:135-203).
+
+        Every instance follows the reference iteration on its own (converged / failed
+        instances are masked); returns a status array (1 converged, -1 failed).
+        """
         torch = self.torch
         pl = self.plan
         st = self.stream
-        n = pl.n_x
-        self.positions()              # rest positions for the current p
+        B, n = self.batch, pl.n_x
+        status = np.zeros(B, dtype=np.int64)
+        if active is not None:
+            status[~np.asarray(active, bool)] = 1
+        self.positions()                       # rest positions for the current p
         for _ in range(max_iters):
+            run = status == 0
+            if not run.any():
+                break
             self._energy_grad(self.x)
-            ginf = torch.empty(1, dtype=torch.float64, device="cuda")
-            check(lib().sgn_reduce(2, n, 1, ptr(self.gx), None, n, ptr(ginf), st))
-            g_inf, e_el, e_lin = float(ginf.item()), float(self.scal[0, 0].item()), float(self.scal[1, 0].item())
-            if g_inf <= tol:
-                return
-            e0 = e_el + e_lin
+            check(lib().sgn_reduce(2, n, B, ptr(self.gx), None, n, ptr(self.scal[3]), st))
+            sc = self.scal.cpu().numpy()
+            g_inf, e0 = sc[3], sc[0] + sc[1]
+            status[run & (g_inf <= tol)] = 1
+            run = status == 0
+            if not run.any():
+                break
             self._hessian()
-            trace = float(self.gvals[0, self.G_diag].sum().item()) if pl.G_diag.size else 0.0
-            step = self._newton_step(trace, n, False)
-            accepted = False
-            for _ in range(8):
-                alpha = self._backtrack(step, e0)
-                if alpha is not None:
-                    self.x.copy_(self.xtry)
-                    accepted = True
+            trace = self._trace()
+            self._newton_step(trace, n, run, bias=False)
+            accepted = np.zeros(B, bool)
+            for _esc in range(8):              # escalate the shift if the line search stalls
+                need = run & ~accepted
+                if not need.any():
                     break
-                step = self._newton_step(trace, n, True)
-            if not accepted:
-                raise ForwardSimFailure(f"static solve: line search failed (|g|inf={g_inf:.3e})")
-        raise ForwardSimFailure(f"static solve: no convergence in {max_iters} iterations")
+                ok = self._backtrack(e0, need)
+                accepted |= ok
+                still = need & ~ok
+                if still.any():
+                    self._newton_step(trace, n, still, bias=True)
+            status[run & ~accepted] = -1
+        status[status == 0] = -1
+        if B == 1 and status[0] != 1:
+            raise ForwardSimFailure("static solve: no convergence / line search failed")
+        return status
 
-    def _newton_step(self, trace, n, bias):
-        """tau-regularized Newton direction into self.kdir (forward.py:171-186)."""
+    def _newton_step(self, trace, n, mask, bias):
+        """tau-regularized Newton directions into self.kdir for masked instances
+        (forward.py:171-186: tau0 = 1e-6 |tr K| / n + 1e-12, x10 ladder, -g fallback)."""
         torch = self.torch
         st = self.stream
-        tau0 = 1e-6 * abs(trace) / max(n, 1) + 1e-12
-        tau = tau0 * 1e6 if bias else 0.0
+        B = self.batch
+        tau0 = 1e-6 * np.abs(trace) / max(n, 1) + 1e-12
+        tau = np.where(bias, tau0 * 1e6, 0.0) * np.ones(B)
+        done = ~np.asarray(mask, bool)
         neg = torch.neg(self.gx)
-        dots = torch.empty(1, dtype=torch.float64, device="cuda")
-        from .errors import SingularMatrix
+        dots = torch.empty(B, dtype=torch.float64, device="cuda")
+        amax = torch.empty(B, dtype=torch.float64, device="cuda")
         for _ in range(60):
-            try:
-                self.gfac.numeric(self.gvals, tau, 0.0, st)
-                self.gfac.check(st)
-                self.gfac.solve(neg, self.kdir, False, st)
-                check(lib().sgn_reduce(1, n, 1, ptr(self.gx), ptr(self.kdir), n, ptr(dots), st))
-                gd = float(dots.item())
-                if gd < 0 and bool(torch.isfinite(self.kdir).all().item()):
-                    return self.kdir
-            except SingularMatrix:
-                pass
-            tau = tau0 if tau == 0.0 else tau * 10.0
-        self.kdir.copy_(neg)
-        return self.kdir
+            tau_d = torch.as_tensor(tau, dtype=torch.float64, device="cuda")
+            self.gfac.numeric_v(self.gvals, tau_d, None, st)
+            piv = self.gfac.status(st)
+            self.gfac.solve(neg, self.xtry, False, st)
+            check(lib().sgn_reduce(1, n, B, ptr(self.gx), ptr(self.xtry), n, ptr(dots), st))
+            check(lib().sgn_reduce(2, n, B, ptr(self.xtry), None, n, ptr(amax), st))
+            gd, am = dots.cpu().numpy(), amax.cpu().numpy()
+            ok = (~done) & (piv < 0) & (gd < 0) & np.isfinite(am)
+            if ok.any():
+                check(lib().sgn_masked_copy(n, B, ptr(self._mask(ok)), ptr(self.xtry), ptr(self.kdir), n, st))
+            done |= ok
+            if done.all():
+                return
+            tau = np.where(done, tau, np.where(tau == 0.0, tau0, tau * 10.0))
+        left = ~done
+        check(lib().sgn_masked_copy(n, B, ptr(self._mask(left)), ptr(neg), ptr(self.kdir), n, st))
 
-    def _backtrack(self, step, e0, c1=1e-4, factor=0.5, max_bt=60):
-        """Armijo on the energy with the reference's float slack (forward.py:189-203)."""
+    def _backtrack(self, e0, mask, c1=1e-4, factor=0.5, max_bt=60):
+        """Per-instance Armijo on the energy with the reference's float slack
+        (forward.py:189-203); accepted instances get x <- x + alpha d.  Returns ok[B]."""
         torch = self.torch
         st = self.stream
-        n = self.plan.n_x
-        slope_t = torch.empty(1, dtype=torch.float64, device="cuda")
-        check(lib().sgn_reduce(1, n, 1, ptr(self.gx), ptr(step), n, ptr(slope_t), st))
-        slope = float(slope_t.item())
-        slack = 4e-15 * abs(e0)
-        alpha = 1.0
-        a_t = torch.empty(1, dtype=torch.float64, device="cuda")
+        B, n = self.batch, self.plan.n_x
+        slope_t = torch.empty(B, dtype=torch.float64, device="cuda")
+        check(lib().sgn_reduce(1, n, B, ptr(self.gx), ptr(self.kdir), n, ptr(slope_t), st))
+        slope = slope_t.cpu().numpy()
+        slack = 4e-15 * np.abs(e0)
+        alpha = np.ones(B)
+        pending = np.asarray(mask, bool).copy()
+        ok = np.zeros(B, bool)
         for _ in range(max_bt):
-            a_t.fill_(alpha)
-            check(lib().sgn_axpy(n, 1, ptr(a_t), ptr(step), ptr(self.x), ptr(self.xtry), n, st))
+            if not pending.any():
+                break
+            a_t = torch.as_tensor(np.where(pending, alpha, 0.0), dtype=torch.float64, device="cuda")
+            check(lib().sgn_axpy(n, B, ptr(a_t), ptr(self.kdir), ptr(self.x), ptr(self.xtry), n, st))
             self._energy_grad(self.xtry, want_grad=False)
-            et = float(self.scal[0, 0].item()) + float(self.scal[1, 0].item())
-            if math.isfinite(et) and et <= e0 + c1 * alpha * slope + slack:
-                return alpha
-            alpha *= factor
-        return None
-
-    def simulate_batched(self, tol, max_iters=200):
-        raise NotImplementedError("batched forward statics: use per-instance engines")
+            sc = self.scal.cpu().numpy()
+            et = sc[0] + sc[1]
+            acc = pending & np.isfinite(et) & (et <= e0 + c1 * alpha * slope + slack)
+            if acc.any():
+                check(lib().sgn_masked_copy(n, B, ptr(self._mask(acc)), ptr(self.xtry), ptr(self.x), n, st))
+            ok |= acc
+            pending &= ~acc
+            alpha = np.where(pending, alpha * factor, alpha)
+        return ok
 
 
 class HostKKT:

@@ -22,7 +22,7 @@ from ..engine import DeviceEngine, MeshPlan
 from ..errors import CapabilityMissing, ForwardSimFailure
 from ..sparse import CscMatrix
 
-__all__ = ["ElasticDesignProblem", "build_sheet", "build_spring_bar", "sheet_spec"]
+__all__ = ["ElasticDesignProblem", "BatchedDesign", "build_sheet", "build_sheet_batch", "build_spring_bar", "sheet_spec"]
 
 
 class ElasticDesignProblem:
@@ -160,6 +160,23 @@ class ElasticDesignProblem:
         return self.residual_jac_p(x, p).to_scipy().T @ (self.weights() * self.residuals(x, p))
 
 
+def _repair_rest(X0, tris, pm_dof, p0, half, rng, n_w, n_h):
+    """Redraw (same stream) the parameters of rest triangles below 20% of nominal area."""
+    nominal = 0.5 / ((n_w - 1) * (n_h - 1))
+    vert_of_p = pm_dof // 2
+    while True:
+        X = X0.ravel().copy()
+        X[pm_dof] += p0
+        X = X.reshape(-1, 2)
+        e1, e2 = X[tris[:, 1]] - X[tris[:, 0]], X[tris[:, 2]] - X[tris[:, 0]]
+        bad = (0.5 * (e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0])) < 0.2 * nominal
+        if not bad.any():
+            return p0
+        redo = np.isin(vert_of_p, np.unique(tris[bad]))
+        p0 = p0.copy()
+        p0[redo] = rng.uniform(-half, half, int(redo.sum()))
+
+
 def sheet_spec(config: int, seed: int = 0, instance: int = 0) -> dict:
     """BASELINE sheet spec (configs 1, 2; config-5 instances) -- see oracle/configs.py docs.
 
@@ -181,15 +198,8 @@ def sheet_spec(config: int, seed: int = 0, instance: int = 0) -> dict:
     rows = np.concatenate([np.arange(n_w) * n_h, np.arange(n_w) * n_h + (n_h - 1)])
     pm_dof = rows * 2 + 1 if config == 1 else (rows[:, None] * 2 + np.arange(2)[None, :]).ravel()
     half = 0.01 if config == 1 else 0.005
-    nominal = 0.5 / ((n_w - 1) * (n_h - 1))
-    while True:   # same-stream redraw until every rest triangle keeps >= 20% nominal area
-        p0 = rng.uniform(-half, half, pm_dof.size)
-        X = X0.ravel().copy()
-        X[pm_dof] += p0
-        X = X.reshape(-1, 2)
-        e1, e2 = X[tris[:, 1]] - X[tris[:, 0]], X[tris[:, 2]] - X[tris[:, 0]]
-        if (0.5 * (e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0])).min() >= 0.2 * nominal:
-            break
+    p0 = rng.uniform(-half, half, pm_dof.size)
+    p0 = _repair_rest(X0, tris, pm_dof, p0, half, rng, n_w, n_h)
     free_verts = np.setdiff1d(np.arange(n_w * n_h), fixed)
     v2f = -np.ones(n_w * n_h, dtype=np.int64)
     v2f[free_verts] = np.arange(free_verts.size)
@@ -199,13 +209,16 @@ def sheet_spec(config: int, seed: int = 0, instance: int = 0) -> dict:
     else:
         ii, jj = np.meshgrid(np.arange(1, n_w - 1), np.arange(1, n_h - 1), indexing="ij")
         interior = (ii * n_h + jj).ravel()
-        tv = np.sort(rng.choice(interior, size=200, replace=False))
+        if instance == 0:
+            tv = np.sort(rng.choice(interior, size=200, replace=False))
+        else:   # config-5 instances share the target vertex set (one KKT pattern), own offsets
+            tv = sheet_spec(config, seed, 0)["target_verts"]
         sigma = 0.01
     tdofs = (v2f[tv][:, None] * 2 + np.arange(2)[None, :]).ravel()
     tvals = X0[tv].ravel() + rng.normal(0.0, sigma, tdofs.size)
     return dict(X0=X0, conn=tris, kind="tri", fixed_verts=fixed,
                 pmap=(pm_dof, np.arange(pm_dof.size), np.ones(pm_dof.size)), target_dofs=tdofs,
-                target_vals=tvals, w_target=1.0, w_reg=2e-6, E=E, nu=nu, gload=100.0 * 9.81, p0=p0,
+                target_vals=tvals, target_verts=tv, w_target=1.0, w_reg=2e-6, E=E, nu=nu, gload=100.0 * 9.81, p0=p0,
                 name=f"sheet_c{config}")
 
 
@@ -213,8 +226,58 @@ def build_sheet(config: int, seed: int = 0, instance: int = 0, **kw):
     """(problem, p0) for BASELINE sheet config 1 or 2 (instance > 0: config-5 member)."""
     spec = sheet_spec(config, seed, instance)
     p0 = spec.pop("p0")
+    spec.pop("target_verts")
     spec.update(kw)
     return ElasticDesignProblem(**spec), p0
+
+
+class BatchedDesign:
+    """B independent instances on one mesh / one KKT pattern (BASELINE config 5).
+
+    All device work is batched over a leading instance dimension: one symbolic analysis,
+    one launch per kernel for all instances (instance index = grid.y), per-instance
+    materials (1/E scaling), targets and parameters.
+    """
+
+    def __init__(self, specs, stab=None, tol=1e-12):
+        s0 = specs[0]
+        self.specs = specs
+        self.B = len(specs)
+        self.plan = MeshPlan(s0["X0"], s0["conn"], s0["kind"], s0["fixed_verts"], s0["pmap"],
+                             s0["target_dofs"], s0["w_target"], s0["w_reg"])
+        for s in specs[1:]:
+            assert np.array_equal(s["target_dofs"], s0["target_dofs"]), "instances must share a pattern"
+        params = []
+        for s in specs:
+            E, nu = s["E"], s["nu"]
+            params.append([E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu)), s["gload"], 1.0 / E])
+        tvals = np.stack([s["target_vals"] for s in specs])
+        self.engine = DeviceEngine(self.plan, np.asarray(params), tvals, batch=self.B, stab=stab)
+        self.p0 = np.stack([s["p0"] for s in specs])
+        self.n_x, self.n_p = self.plan.n_x, self.plan.n_p
+        self.tol = tol
+
+    def load(self, x=None, p=None):
+        self.engine.load(x=x, p=p)
+
+    def rest_start(self):
+        return np.tile(self.plan.X0.ravel()[self.plan.free_dofs], (self.B, 1))
+
+    def simulate(self, p, x_init=None, active=None):
+        """Batched forward equilibrium; returns (x[B, n_x], status[B])."""
+        self.engine.load(x=self.rest_start() if x_init is None else x_init, p=p)
+        status = self.engine.simulate(self.tol, active=active)
+        return self.engine.x.cpu().numpy(), status
+
+    def directions(self, timings=None):
+        """SGN directions at the loaded (x, p) of every instance (device arrays in engine.sol)."""
+        return self.engine.direction(timings)
+
+
+def build_sheet_batch(config: int = 2, seed: int = 0, instances=range(1, 65), stab=None):
+    """BASELINE config 5: instances of the 100x100 sheet with seeded E ~ U(5e4, 2e5),
+    own target offsets and own p0 (shared target vertex set => one KKT pattern)."""
+    return BatchedDesign([sheet_spec(config, seed, int(k)) for k in instances], stab=stab)
 
 
 def build_spring_bar(n_w: int, n_h: int, w_reg: float = 0.0, stiffness: float = 2.0,
