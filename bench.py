@@ -105,12 +105,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ CPU legs
-def _cpu_worker_init(config):
+def _cpu_worker_init(config, targets=None):
     global _W
     from threadpoolctl import threadpool_limits
     threadpool_limits(1)
-    from oracle.configs import oracle_sheet
-    prob, p0 = oracle_sheet(config)
+    if config == 3:
+        from oracle.configs import oracle_beam
+        prob, p0 = oracle_beam(0, targets=targets)
+    else:
+        from oracle.configs import oracle_sheet
+        prob, p0 = oracle_sheet(config)
     _W = (prob, p0)
 
 
@@ -128,10 +132,10 @@ def cpu_equilibrium(config):
     return prob.simulate(p0)
 
 
-def cpu_baseline(config, x, sample):
+def cpu_baseline(config, x, sample, targets=None):
     """Oracle port on 1 core: median of `sample` directions (after one warm-up)."""
     from threadpoolctl import threadpool_limits
-    _cpu_worker_init(config)
+    _cpu_worker_init(config, targets)
     with threadpool_limits(1):
         _cpu_worker_direction(x)
         ts = [_cpu_worker_direction(x) for _ in range(sample)]
@@ -204,8 +208,13 @@ def run_ours(args):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s (B200_PROFILING.md)"
 
-    prob, p0 = build_sheet(args.config)
-    x = prob.simulate(p0)                       # GPU Newton equilibrium (setup, untimed)
+    if args.config == 3:
+        from paper_2107_03285_b200.problems import build_beam
+        prob, p0, _sag = build_beam(0)
+        x = prob._x_warm
+    else:
+        prob, p0 = build_sheet(args.config)
+        x = prob.simulate(p0)                   # GPU Newton equilibrium (setup, untimed)
     eng = prob.engine
     pl = prob.plan
     st = eng.ksym.stats()
@@ -291,8 +300,9 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded mesh/targets/p0, oracle/configs.py; no dataset)",
-        "config": {"workload": f"config {args.config}: 100x100 neo-Hookean sheet (19602 tris), n_x=19800, "
-                               f"n_p=400, KKT dim {pl.dim}, nnz(K) {pl.nnz}",
+        "config": {"workload": {1: "config 1: 20x20 neo-Hookean sheet", 2: "config 2: 100x100 neo-Hookean sheet (19602 tris)",
+                                3: "config 3: 41x11x11 neo-Hookean tet beam (20000 tets)"}[args.config]
+                               + f", n_x={pl.n_x}, n_p={pl.n_p}, KKT dim {pl.dim}, nnz(K) {pl.nnz}",
                    "parallelism": "replicas" if world > 1 else "single GPU",
                    "l2": "flushed before every timed step (512 MiB memset outside the events)",
                    "nnz_L": st["nnz_l"], "factor_flops": flops, "fronts": st["n_fronts"],
@@ -321,7 +331,9 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            out["cpu_baseline"] = cpu_baseline(args.config, np.asarray(x), args.cpu_sample)
+            tgt = np.asarray(x)[pl.target_dofs] if args.config == 3 else None   # sagged tip (config 3)
+            sample = 1 if args.config == 3 else args.cpu_sample
+            out["cpu_baseline"] = cpu_baseline(args.config, np.asarray(x), sample, tgt)
         except Exception as exc:  # the baseline is reported, never required for the GPU number
             out["cpu_baseline"] = {"value": None, "error": repr(exc)}
     if rank == 0:

@@ -405,6 +405,7 @@ int sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch, const 
   if (n_elems == 0) return SGN_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const dim3 grid((unsigned)((n_elems + 127) / 128), batch);
+  const dim3 grid64((unsigned)((n_elems + 63) / 64), batch);   // tets: 64-thread blocks
   switch (elem_type) {
     case SGN_ELEM_SPRING:
     case SGN_ELEM_SPRING + 200:
@@ -424,7 +425,7 @@ int sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch, const 
       break;
     case SGN_ELEM_NH_TET:
       sgn::count_launch();
-      k_elem_derivs<SGN_ELEM_NH_TET, 3><<<grid, 64, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
+      k_elem_derivs<SGN_ELEM_NH_TET, 3><<<grid64, 64, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
                                                              d_params, param_stride, d_hess, d_mixed, buf_stride);
       break;
     default:
@@ -442,6 +443,7 @@ int sgn_element_energy_grad(int32_t elem_type, int64_t n_elems, int32_t batch, c
   if (n_elems == 0) return SGN_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const dim3 grid((unsigned)((n_elems + 127) / 128), batch);
+  const dim3 grid64((unsigned)((n_elems + 63) / 64), batch);   // tets: 64-thread blocks
   switch (elem_type) {
     case SGN_ELEM_SPRING:
     case SGN_ELEM_SPRING + 200:
@@ -461,7 +463,7 @@ int sgn_element_energy_grad(int32_t elem_type, int64_t n_elems, int32_t batch, c
       break;
     case SGN_ELEM_NH_TET:
       sgn::count_launch();
-      k_elem_energy_grad<SGN_ELEM_NH_TET, 3><<<grid, 64, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
+      k_elem_energy_grad<SGN_ELEM_NH_TET, 3><<<grid64, 64, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
                                                                   d_params, param_stride, d_energy, d_grad, buf_stride);
       break;
     default:

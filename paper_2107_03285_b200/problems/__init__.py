@@ -22,7 +22,8 @@ from ..engine import DeviceEngine, MeshPlan
 from ..errors import CapabilityMissing, ForwardSimFailure
 from ..sparse import CscMatrix
 
-__all__ = ["ElasticDesignProblem", "BatchedDesign", "build_sheet", "build_sheet_batch", "build_spring_bar", "sheet_spec"]
+__all__ = ["ElasticDesignProblem", "BatchedDesign", "beam_spec", "build_beam", "build_sheet", "build_sheet_batch",
+           "build_spring_bar", "sheet_spec"]
 
 
 class ElasticDesignProblem:
@@ -322,3 +323,68 @@ def build_spring_bar(n_w: int, n_h: int, w_reg: float = 0.0, stiffness: float = 
                                 scale=1.0, tol=1e-10, f_ext=f_ext, rest_base=rest_base,
                                 p_offset=X0[free_verts].ravel(), name="SpringBarProblem", **kw)
     return prob
+
+
+def beam_spec(seed: int = 0, targets=None) -> dict:
+    """BASELINE config 3 (41x11x11 grid, 5 tets per hex, E = 1e6, nu = 0.45, rho g = 9810,
+    x = 0 face clamped); p = rest normal offsets per (surface vertex, non-clamped face) --
+    1,881 parameters (SURVEY 0.9 iii); C = 2e-6 I (with C = 0 the KKT is singular: rank(H) <= 363
+    < n_p); targets = sagged tip face + N(0.05, 0.01)
+    lift along +y.  Re-implemented from oracle/configs.beam_spec (asserted equal in tests)."""
+    nx, ny, nz = 41, 11, 11
+    lx, ly, lz = 4.0, 1.0, 1.0
+    ii, jj, kk = (a.ravel() for a in np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"))
+    X0 = np.column_stack([ii * lx / (nx - 1), jj * ly / (ny - 1), kk * lz / (nz - 1)])
+    vid = lambda i, j, k: (i * ny + j) * nz + k
+    even = [(0, 4, 2, 1), (6, 2, 4, 7), (5, 4, 1, 7), (3, 2, 7, 1), (4, 2, 1, 7)]
+    odd = [(4, 0, 6, 5), (2, 6, 0, 3), (1, 0, 5, 3), (7, 6, 3, 5), (0, 6, 5, 3)]
+    tets = []
+    for i in range(nx - 1):
+        for j in range(ny - 1):
+            for k in range(nz - 1):
+                c = [vid(i + (a >> 2 & 1), j + (a >> 1 & 1), k + (a & 1)) for a in range(8)]
+                for t in (even if (i + j + k) % 2 == 0 else odd):
+                    tet = [c[a] for a in t]
+                    P = X0[tet]
+                    if np.linalg.det(np.stack([P[1] - P[0], P[2] - P[0], P[3] - P[0]], axis=1)) < 0:
+                        tet[1], tet[2] = tet[2], tet[1]
+                    tets.append(tet)
+    tets = np.array(tets, dtype=np.int64)
+    fixed = np.flatnonzero(ii == 0)
+    faces = [(ii == nx - 1, 0, 1.0), (jj == 0, 1, -1.0), (jj == ny - 1, 1, 1.0),
+             (kk == 0, 2, -1.0), (kk == nz - 1, 2, 1.0)]
+    pm_dof, pm_coef = [], []
+    for v in np.flatnonzero(ii > 0):
+        for mask, axis, sgn in faces:
+            if mask[v]:
+                pm_dof.append(3 * v + axis)
+                pm_coef.append(sgn)
+    free_verts = np.flatnonzero(ii > 0)
+    v2f = -np.ones(X0.shape[0], dtype=np.int64)
+    v2f[free_verts] = np.arange(free_verts.size)
+    tip = np.flatnonzero(ii == nx - 1)
+    tdofs = (v2f[tip][:, None] * 3 + np.arange(3)[None, :]).ravel()
+    rng = np.random.default_rng(3000 + seed)
+    lift = np.zeros((tip.size, 3))
+    lift[:, 1] = rng.normal(0.05, 0.01, tip.size)
+    base = X0[tip].ravel() if targets is None else np.asarray(targets, dtype=np.float64)
+    n_p = len(pm_dof)
+    return dict(X0=X0, conn=tets, kind="tet", fixed_verts=fixed,
+                pmap=(np.array(pm_dof), np.arange(n_p), np.array(pm_coef)), target_dofs=tdofs,
+                target_vals=base + lift.ravel(), w_target=1.0, w_reg=2e-6, E=1e6, nu=0.45,
+                gload=1000.0 * 9.81, p0=np.zeros(n_p), name="beam_c3")
+
+
+def build_beam(seed: int = 0, **kw):
+    """(problem, p0, sag) for config 3: the targets are defined from the device forward
+    solve at p0 = 0 (the sagged tip face), then lifted."""
+    spec = beam_spec(seed)
+    p0 = spec.pop("p0")
+    spec.update(kw)
+    prob = ElasticDesignProblem(**spec)
+    x = prob.simulate(p0)
+    sag = x[prob.plan.target_dofs]
+    lifted = beam_spec(seed, targets=sag)["target_vals"]
+    prob.target_vals = lifted
+    prob.engine.tvals.copy_(prob.engine.torch.as_tensor(lifted).reshape(1, -1))
+    return prob, p0, sag

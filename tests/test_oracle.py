@@ -157,3 +157,29 @@ def test_c2_rest_shape_valid():
     area = 0.5 * (e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0])
     assert area.min() >= 0.2 * 0.5 / 99 ** 2
     assert np.all(np.abs(s["p0"]) <= 0.005)
+
+
+def test_beam_generators_agree_and_mesh_is_conforming():
+    from collections import Counter
+    from oracle.configs import beam_spec
+    from paper_2107_03285_b200.problems import beam_spec as gpu_beam
+    a, b = beam_spec(0), gpu_beam(0)
+    for k, va in a.items():
+        vb = b[k]
+        if isinstance(va, tuple):
+            assert all(np.array_equal(u, v) for u, v in zip(va, vb)), k
+        elif isinstance(va, np.ndarray):
+            assert np.array_equal(va, vb), k
+        else:
+            assert va == vb, k
+    X0, tets = a["X0"], a["conn"]
+    assert tets.shape == (20000, 4) and X0.shape == (4961, 3)
+    P = X0[tets]
+    vol = np.linalg.det(np.stack([P[:, 1] - P[:, 0], P[:, 2] - P[:, 0], P[:, 3] - P[:, 0]], axis=2)) / 6
+    assert vol.min() > 0 and abs(vol.sum() - 4.0) < 1e-12
+    faces = Counter()
+    for t in tets:
+        for f in ((0, 1, 2), (0, 1, 3), (0, 2, 3), (1, 2, 3)):
+            faces[tuple(sorted(t[list(f)]))] += 1
+    assert max(faces.values()) == 2 and sum(v == 1 for v in faces.values()) == 3600
+    assert len(a["p0"]) == 1881 and len(a["target_dofs"]) == 363
