@@ -130,6 +130,8 @@ int  sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_stri
 #define SGN_ELEM_SPRING     1   /* 2-node spring, any dim (forward.py:61-111)        */
 #define SGN_ELEM_NH_TRI     2   /* 3-node neo-Hookean triangle, plane strain         */
 #define SGN_ELEM_NH_TET     3   /* 4-node neo-Hookean tetrahedron                    */
+#define SGN_ELEM_SHELL_MEMBRANE 4 /* 3-node StVK membrane triangle in 3-D (config 4)  */
+#define SGN_ELEM_HINGE      5   /* 4-node dihedral bending hinge (config 4)          */
 int  sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch,
                         const int32_t* d_conn, const double* d_pos, const double* d_rest,
                         int64_t vert_stride, const double* d_params, int64_t param_stride,
@@ -169,9 +171,19 @@ int  sgn_lsq_terms(int32_t batch, int64_t n_x, int64_t n_p, int64_t nt, const in
                    const double* d_tvals, int64_t tstride, double w_t, double w_reg,
                    const double* d_x, const double* d_p, double* d_vec, double* d_fobj,
                    void* stream);
+/* as sgn_lsq_terms with residuals r = x[tdofs] - tvals - R p (config 4: vertical displacement
+ * relative to the p-dependent rest shape): R as CSR over targets (d_rptr/d_ridx/d_rcoef),
+ * R^T as CSR over parameters, d_rscr scratch [batch x nt]; f_p = -R^T w r + w_reg p.     */
+int  sgn_lsq_terms_r(int32_t batch, int64_t n_x, int64_t n_p, int64_t nt, const int64_t* d_tdofs,
+                     const double* d_tvals, int64_t tstride, double w_t, double w_reg,
+                     const double* d_x, const double* d_p, double* d_vec, double* d_fobj,
+                     const int64_t* d_rptr, const int64_t* d_ridx, const double* d_rcoef,
+                     const int64_t* d_rtptr, const int64_t* d_rtidx, const double* d_rtcoef,
+                     double* d_rscr, void* stream);
 /* adjoint gradient from a leading-block KKT solve (sensitivity.py:181-198, 245-256):
  * mode 0: d_out = (0, 0, d_src[lambda]);  mode 1: g = d_fvec[p] - d_src[p] (d_src = K v),
- * d_out = (0, -g, 0), d_grad = g.                                                     */
+ * d_out = (0, -g, 0), d_grad = g;  mode 2: d_out = (0, 0, w) for an n_x-vector w = d_src;
+ * mode 3: d_out (n_x per instance) = x block of d_src.                                                     */
 int  sgn_adjoint_step(int32_t mode, int32_t batch, int64_t n_x, int64_t n_p, const double* d_src,
                       const double* d_fvec, double* d_out, double* d_grad, void* stream);
 

@@ -15,7 +15,7 @@ LIB_PATH = pathlib.Path(__file__).with_name("_sgnb200.so")
 
 SGN_OK, SGN_SINGULAR, SGN_NO_CONVERGENCE, SGN_DIMENSION, SGN_CUDA_ERROR, SGN_INVALID = range(6)
 SGN_SOLVE_LEADING = 1
-SGN_ELEM_SPRING, SGN_ELEM_NH_TRI, SGN_ELEM_NH_TET = 1, 2, 3
+SGN_ELEM_SPRING, SGN_ELEM_NH_TRI, SGN_ELEM_NH_TET, SGN_ELEM_SHELL_MEMBRANE, SGN_ELEM_HINGE = 1, 2, 3, 4, 5
 
 c_i32, c_i64, c_dbl, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 P_i64 = ctypes.POINTER(c_i64)
@@ -63,6 +63,9 @@ SIGNATURES = {
     "sgn_lsq_terms": (ctypes.c_int, [c_i32, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_dbl, c_dbl,
                                      c_vp, c_vp, c_vp, c_vp, c_vp]),
     "sgn_fp64_peak": (ctypes.c_int, [c_i32, c_i32, P_dbl, c_vp]),
+    "sgn_lsq_terms_r": (ctypes.c_int, [c_i32, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_dbl, c_dbl,
+                                       c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                       c_vp, c_vp]),
     "sgn_adjoint_step": (ctypes.c_int, [c_i32, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 

@@ -428,6 +428,10 @@ int sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch, const 
       k_elem_derivs<SGN_ELEM_NH_TET, 3><<<grid64, 64, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
                                                              d_params, param_stride, d_hess, d_mixed, buf_stride);
       break;
+    case SGN_ELEM_SHELL_MEMBRANE:
+    case SGN_ELEM_HINGE:
+      return sgn::launch_shell(true, elem_type, n_elems, batch, d_conn, d_pos, d_rest, vert_stride,
+                               d_params, param_stride, d_hess, d_mixed, buf_stride, stream);
     default:
       sgn::last_error() = "unknown element type";
       return SGN_INVALID;
@@ -466,6 +470,10 @@ int sgn_element_energy_grad(int32_t elem_type, int64_t n_elems, int32_t batch, c
       k_elem_energy_grad<SGN_ELEM_NH_TET, 3><<<grid64, 64, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
                                                                   d_params, param_stride, d_energy, d_grad, buf_stride);
       break;
+    case SGN_ELEM_SHELL_MEMBRANE:
+    case SGN_ELEM_HINGE:
+      return sgn::launch_shell(false, elem_type, n_elems, batch, d_conn, d_pos, d_rest, vert_stride,
+                               d_params, param_stride, d_energy, d_grad, buf_stride, stream);
     default:
       sgn::last_error() = "unknown element type";
       return SGN_INVALID;

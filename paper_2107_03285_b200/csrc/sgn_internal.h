@@ -95,6 +95,10 @@ std::string& last_error();
 void count_launch(int64_t n = 1);
 int64_t launch_count();
 
+int launch_shell(bool derivs, int32_t elem_type, int64_t n_elems, int32_t batch, const int32_t* conn,
+                 const double* pos, const double* rest, int64_t vstride, const double* params,
+                 int64_t pstride, double* out1, double* out2, int64_t bstride, void* stream);
+
 // returns 0 ok, 1 singular (pivot_index set), 5 invalid
 int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index);
 

@@ -57,32 +57,44 @@ __global__ void k_axpy(int64_t n, const double* __restrict__ alpha, const double
   }
 }
 
-// f vector (KKT order): x block = w_t (x_t - target) at target dofs, p block = w_reg p,
-// lambda block 0; objective per instance = 0.5 sum w r^2
+// f vector (KKT order): x block = w_t r at target dofs, p block = -R^T w_t r + w_reg p,
+// lambda block 0, with r = x[tdofs] - tvals - R p (R optional, CSR over targets; R^T is
+// the CSR over parameters); objective per instance = 0.5 sum w r^2 + 0.5 w_reg |p|^2.
 __global__ void __launch_bounds__(kRed)
 k_lsq(int64_t n_x, int64_t n_p, int64_t nt, const int64_t* __restrict__ tdofs,
       const double* __restrict__ tvals, int64_t tstride, double w_t, double w_reg,
       const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ vec,
-      double* __restrict__ fobj) {
+      double* __restrict__ fobj, const int64_t* __restrict__ rptr, const int64_t* __restrict__ ridx,
+      const double* __restrict__ rcoef, const int64_t* __restrict__ rtptr,
+      const int64_t* __restrict__ rtidx, const double* __restrict__ rtcoef,
+      double* __restrict__ rscr) {
   __shared__ double sh[kRed];
   const int b = blockIdx.x;
   const int64_t dim = 2 * n_x + n_p;
   double* v = vec ? vec + (int64_t)b * dim : nullptr;
   const double* xb = x + (int64_t)b * n_x;
   const double* pb = p + (int64_t)b * n_p;
+  double* rs = rscr ? rscr + (int64_t)b * nt : nullptr;
   if (v) for (int64_t i = threadIdx.x; i < dim; i += kRed) if (i < n_x || i >= n_x + n_p) v[i] = 0.0;
   __syncthreads();
   double acc = 0.0;
   for (int64_t t = threadIdx.x; t < nt; t += kRed) {
     const int64_t d = tdofs[t];
-    const double r = xb[d] - tvals[(int64_t)b * tstride + t];
+    double r = xb[d] - tvals[(int64_t)b * tstride + t];
+    if (rptr)
+      for (int64_t k = rptr[t]; k < rptr[t + 1]; ++k) r -= rcoef[k] * pb[ridx[k]];
     acc += w_t * r * r;
     if (v) v[d] = w_t * r;
+    if (rs) rs[t] = w_t * r;
   }
+  __syncthreads();
   for (int64_t j = threadIdx.x; j < n_p; j += kRed) {
     const double pj = pb[j];
     acc += w_reg * pj * pj;
-    if (v) v[n_x + j] = w_reg * pj;
+    double fp = w_reg * pj;
+    if (rtptr)
+      for (int64_t k = rtptr[j]; k < rtptr[j + 1]; ++k) fp -= rtcoef[k] * rs[rtidx[k]];
+    if (v) v[n_x + j] = fp;
   }
   sh[threadIdx.x] = acc;
   __syncthreads();
@@ -95,6 +107,7 @@ k_lsq(int64_t n_x, int64_t n_p, int64_t nt, const int64_t* __restrict__ tdofs,
 
 // mode 0: v = (0, 0, src_lambda)
 // mode 1: g = fvec_p - kv_p ; rhs = (0, -g, 0) ; grad[b] = g
+// mode 2: v = (0, 0, w), w an n_x-vector ; mode 3: out_nx = src[x block]
 __global__ void k_adjoint(int mode, int64_t n_x, int64_t n_p, const double* __restrict__ src,
                           const double* __restrict__ fvec, double* __restrict__ out,
                           double* __restrict__ grad) {
@@ -105,6 +118,10 @@ __global__ void k_adjoint(int mode, int64_t n_x, int64_t n_p, const double* __re
     const bool in_p = (i >= n_x && i < n_x + n_p);
     if (mode == 0) {
       out[k] = (i >= n_x + n_p) ? src[k] : 0.0;
+    } else if (mode == 2) {           // v = (0, 0, w) from an n_x-vector w
+      out[k] = (i >= n_x + n_p) ? src[(int64_t)b * n_x + (i - n_x - n_p)] : 0.0;
+    } else if (mode == 3) {           // out_nx = x block of src (contiguous n_x per instance)
+      if (i < n_x) out[(int64_t)b * n_x + i] = src[k];
     } else {
       if (in_p) {
         const double g = fvec[k] - src[k];
@@ -175,9 +192,20 @@ int sgn_masked_copy(int64_t n, int32_t batch, const int32_t* d_mask, const doubl
 int sgn_lsq_terms(int32_t batch, int64_t n_x, int64_t n_p, int64_t nt, const int64_t* d_tdofs,
                   const double* d_tvals, int64_t tstride, double w_t, double w_reg,
                   const double* d_x, const double* d_p, double* d_vec, double* d_fobj, void* stream) {
+  return sgn_lsq_terms_r(batch, n_x, n_p, nt, d_tdofs, d_tvals, tstride, w_t, w_reg, d_x, d_p, d_vec,
+                         d_fobj, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+int sgn_lsq_terms_r(int32_t batch, int64_t n_x, int64_t n_p, int64_t nt, const int64_t* d_tdofs,
+                    const double* d_tvals, int64_t tstride, double w_t, double w_reg,
+                    const double* d_x, const double* d_p, double* d_vec, double* d_fobj,
+                    const int64_t* d_rptr, const int64_t* d_ridx, const double* d_rcoef,
+                    const int64_t* d_rtptr, const int64_t* d_rtidx, const double* d_rtcoef,
+                    double* d_rscr, void* stream) {
   sgn::count_launch();
   k_lsq<<<batch, kRed, 0, (cudaStream_t)stream>>>(n_x, n_p, nt, d_tdofs, d_tvals, tstride, w_t, w_reg,
-                                                  d_x, d_p, d_vec, d_fobj);
+                                                  d_x, d_p, d_vec, d_fobj, d_rptr, d_ridx, d_rcoef,
+                                                  d_rtptr, d_rtidx, d_rtcoef, d_rscr);
   VEC_CHECK();
   return SGN_OK;
 }

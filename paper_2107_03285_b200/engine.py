@@ -23,13 +23,30 @@ import math
 import time
 
 import numpy as np
+import scipy.sparse as sp
 
 from . import _lib
 from ._lib import check, lib, ptr
 from .device import DeviceFactor, symbolic_for
 from .errors import DimensionMismatch, ForwardSimFailure, NoConvergence
 
-ELEM_CODES = {"spring": _lib.SGN_ELEM_SPRING, "tri": _lib.SGN_ELEM_NH_TRI, "tet": _lib.SGN_ELEM_NH_TET}
+ELEM_CODES = {"spring": _lib.SGN_ELEM_SPRING, "tri": _lib.SGN_ELEM_NH_TRI, "tet": _lib.SGN_ELEM_NH_TET,
+              "membrane": _lib.SGN_ELEM_SHELL_MEMBRANE, "hinge": _lib.SGN_ELEM_HINGE}
+
+
+class ElemGroup:
+    """One element type of a mesh: connectivity + its slices of the block/gradient buffers."""
+
+    def __init__(self, kind, conn, d, hoff, goff):
+        self.kind = kind
+        self.conn = np.asarray(conn, dtype=np.int64)
+        self.n_e, self.nv = self.conn.shape
+        self.nd = self.nv * d
+        self.code = ELEM_CODES[kind] + (100 * d if kind == "spring" else 0)
+        self.hoff = hoff                                   # hess block offset in ebuf
+        self.moff = hoff + self.n_e * self.nd * self.nd    # mixed block offset
+        self.goff = goff                                   # gradient offset in egrad
+        self.size = 2 * self.n_e * self.nd * self.nd
 
 
 def _csr_from_lists(n_rows, rows, *cols):
@@ -45,15 +62,23 @@ class MeshPlan:
     """Host precomputation for one mesh / parameterization (shared by all instances)."""
 
     def __init__(self, X0, conn, kind, fixed_verts, pmap, target_dofs, w_target, w_reg,
-                 f_ext=None, rest_base=None):
+                 f_ext=None, rest_base=None, groups=None, R=None):
         self.X0 = np.asarray(X0, dtype=np.float64)
         self.n_v, self.d = self.X0.shape
-        self.conn = np.asarray(conn, dtype=np.int64)
-        self.kind = kind
-        self.elem_code = ELEM_CODES[kind] + (100 * self.d if kind == "spring" else 0)
-        self.n_e, self.nv_el = self.conn.shape
-        self.nd = self.nv_el * self.d
         d = self.d
+        if groups is None:
+            groups = [(kind, conn)]
+        self.groups = []
+        hoff = goff = 0
+        for gk, gc in groups:
+            g = ElemGroup(gk, gc, d, hoff, goff)
+            self.groups.append(g)
+            hoff += g.size
+            goff += g.n_e * g.nd
+        self.ebuf_size, self.egrad_size = hoff, goff
+        g0 = self.groups[0]
+        self.conn, self.kind, self.elem_code = g0.conn, g0.kind, g0.code     # single-group aliases
+        self.n_e, self.nv_el, self.nd = g0.n_e, g0.nv, g0.nd
         fixed = np.zeros(self.n_v, bool)
         fixed[np.asarray(fixed_verts, dtype=np.int64)] = True
         self.free_verts = np.flatnonzero(~fixed)
@@ -70,9 +95,6 @@ class MeshPlan:
         self.f_ext = np.zeros(self.n_dof) if f_ext is None else np.asarray(f_ext, dtype=np.float64)
         self.dim = 2 * self.n_x + self.n_p
         n_x, n_p = self.n_x, self.n_p
-        nd = self.nd
-        el_dofs = (self.conn[:, :, None] * d + np.arange(d)[None, None, :]).reshape(self.n_e, nd)
-        self.el_dofs = el_dofs
 
         # positions: pos[dof] = X0[dof] (fixed) | x[dof_to_x] (free)
         is_free = self.dof_to_x >= 0
@@ -85,53 +107,75 @@ class MeshPlan:
         self.rest_base = (self.X0.ravel().copy() if rest_base is None
                           else np.asarray(rest_base, dtype=np.float64).ravel().copy())
 
-        # element-local index tables
-        ea = np.repeat(np.arange(nd), nd)     # row (deformed dof) local index
-        eb = np.tile(np.arange(nd), nd)       # col local index
-        e_all = np.repeat(np.arange(self.n_e), nd * nd)
-        r_dof = el_dofs[:, ea].ravel()
-        c_dof = el_dofs[:, eb].ravel()
-        loc = np.tile(ea * nd + eb, self.n_e)
-        hidx = e_all * nd * nd + loc                      # index into hess buffer
-        midx = self.n_e * nd * nd + hidx                  # index into mixed buffer
-        rx, cx = self.dof_to_x[r_dof], self.dof_to_x[c_dof]
-
         # --- KKT structural entries + contributions (reference block order) ------------
         oL = n_x + n_p
         rows, cols, src, coef = [], [], [], []
-        keep = (rx >= 0) & (cx >= 0)                      # Gx block and its transpose
-        gx_r, gx_c, gx_s = rx[keep], cx[keep], hidx[keep]
-        rows += [oL + gx_r, gx_c]
-        cols += [gx_c, oL + gx_r]
-        src += [gx_s, gx_s]
-        coef += [np.ones(gx_s.size), np.ones(gx_s.size)]
-        # Gp block: row free dof, rest col dof -> p entries
+        gx_r_all, gx_c_all, gx_s_all = [], [], []
+        g_rows, g_src = [], []
         rp = self.rest_ptr
-        cnt = (rp[c_dof + 1] - rp[c_dof]) * (rx >= 0)
-        sel = np.flatnonzero(cnt)
-        if sel.size:
-            rep = cnt[sel]
-            base_t = np.repeat(sel, rep)
-            starts = np.zeros(rep.size, dtype=np.int64)
-            np.cumsum(rep[:-1], out=starts[1:])
-            offs = np.arange(int(rep.sum()), dtype=np.int64) - np.repeat(starts, rep)
-            kk = rp[c_dof[base_t]] + offs
-            pj = self.rest_idx[kk]
-            pc = self.rest_coef[kk]
-            gr = rx[base_t]
-            ms = midx[base_t]
-            rows += [oL + gr, n_x + pj]
-            cols += [n_x + pj, oL + gr]
-            src += [ms, ms]
-            coef += [pc, pc]
+        for g in self.groups:
+            nd = g.nd
+            el_dofs = (g.conn[:, :, None] * d + np.arange(d)[None, None, :]).reshape(g.n_e, nd)
+            ea = np.repeat(np.arange(nd), nd)     # row (deformed dof) local index
+            eb = np.tile(np.arange(nd), nd)       # col local index
+            e_all = np.repeat(np.arange(g.n_e), nd * nd)
+            r_dof = el_dofs[:, ea].ravel()
+            c_dof = el_dofs[:, eb].ravel()
+            loc = np.tile(ea * nd + eb, g.n_e)
+            hidx = g.hoff + e_all * nd * nd + loc
+            midx = g.moff + e_all * nd * nd + loc
+            rx, cx = self.dof_to_x[r_dof], self.dof_to_x[c_dof]
+            keep = (rx >= 0) & (cx >= 0)                  # Gx block and its transpose
+            gx_r, gx_c, gx_s = rx[keep], cx[keep], hidx[keep]
+            gx_r_all.append(gx_r); gx_c_all.append(gx_c); gx_s_all.append(gx_s)
+            rows += [oL + gx_r, gx_c]
+            cols += [gx_c, oL + gx_r]
+            src += [gx_s, gx_s]
+            coef += [np.ones(gx_s.size), np.ones(gx_s.size)]
+            # Gp block: row free dof, rest col dof -> p entries
+            cnt = (rp[c_dof + 1] - rp[c_dof]) * (rx >= 0)
+            sel = np.flatnonzero(cnt)
+            if sel.size:
+                rep = cnt[sel]
+                base_t = np.repeat(sel, rep)
+                starts = np.zeros(rep.size, dtype=np.int64)
+                np.cumsum(rep[:-1], out=starts[1:])
+                offs = np.arange(int(rep.sum()), dtype=np.int64) - np.repeat(starts, rep)
+                kk = rp[c_dof[base_t]] + offs
+                pj = self.rest_idx[kk]
+                pc = self.rest_coef[kk]
+                gr = rx[base_t]
+                ms = midx[base_t]
+                rows += [oL + gr, n_x + pj]
+                cols += [n_x + pj, oL + gr]
+                src += [ms, ms]
+                coef += [pc, pc]
+            # gradient gather entries of this group
+            gdof = el_dofs.ravel()
+            gx_ = self.dof_to_x[gdof]
+            gs = np.flatnonzero(gx_ >= 0)
+            g_rows.append(gx_[gs]); g_src.append(g.goff + gs.astype(np.int64))
         rows = np.concatenate(rows); cols = np.concatenate(cols)
         src = np.concatenate(src); coef = np.concatenate(coef)
-        # A diagonal (targets) and C diagonal (regularizer) as structural entries w/o buffer terms
-        a_rows = np.unique(self.target_dofs)
-        c_rows = np.arange(n_p) + n_x if self.w_reg > 0.0 else np.zeros(0, np.int64)
-        diag_rows = np.concatenate([a_rows, c_rows])
-        all_r = np.concatenate([rows, diag_rows])
-        all_c = np.concatenate([cols, diag_rows])
+        gx_r, gx_c, gx_s = np.concatenate(gx_r_all), np.concatenate(gx_c_all), np.concatenate(gx_s_all)
+        # constant Gauss-Newton blocks (sensitivity.py:205-216): A = w on targets, and for a
+        # residual r = x_t - R p: B = -w R^T (p rows, x cols), C = w R^T R + w_reg I
+        nt = self.target_dofs.size
+        crow, ccol, cval = [self.target_dofs], [self.target_dofs], [np.full(nt, self.w_target)]
+        self.R = None
+        if R is not None:
+            Rm = sp.csr_matrix(R)
+            self.R = Rm
+            Rc = Rm.tocoo()
+            bt_x, bt_p, bt_v = self.target_dofs[Rc.row], n_x + Rc.col, -self.w_target * Rc.data
+            crow += [bt_p, bt_x]; ccol += [bt_x, bt_p]; cval += [bt_v, bt_v]
+            CtC = (self.w_target * (Rm.T @ Rm)).tocoo()
+            crow.append(n_x + CtC.row); ccol.append(n_x + CtC.col); cval.append(CtC.data)
+        if self.w_reg > 0.0:
+            crow.append(n_x + np.arange(n_p)); ccol.append(n_x + np.arange(n_p)); cval.append(np.full(n_p, self.w_reg))
+        crow, ccol, cval = np.concatenate(crow), np.concatenate(ccol), np.concatenate(cval)
+        all_r = np.concatenate([rows, crow])
+        all_c = np.concatenate([cols, ccol])
         key = all_c * self.dim + all_r                    # CSC order: by column, then row
         ukey, inv = np.unique(key, return_inverse=True)
         self.K_indices = (ukey % self.dim).astype(np.int64)
@@ -142,12 +186,14 @@ class MeshPlan:
         nz_of = inv[:rows.size]
         self.K_ptr, self.K_src, self.K_coef = _csr_from_lists(self.nnz, nz_of, src, coef)
         base = np.zeros(self.nnz)
-        tcount = np.bincount(self.target_dofs, minlength=n_x)
-        dpos = inv[rows.size:rows.size + a_rows.size]
-        base[dpos] = self.w_target * tcount[a_rows]
-        if c_rows.size:
-            base[inv[rows.size + a_rows.size:]] = self.w_reg
+        np.add.at(base, inv[rows.size:], cval)         # constant entries (sum duplicates)
         self.K_base = base
+        # residual map on the device (CSR over targets and over parameters)
+        if R is not None:
+            Rr = sp.csr_matrix(R); Rr.sort_indices()
+            Rt = sp.csr_matrix(Rr.T); Rt.sort_indices()
+            self.R_ptr, self.R_idx, self.R_val = Rr.indptr.astype(np.int64), Rr.indices.astype(np.int64), Rr.data.copy()
+            self.Rt_ptr, self.Rt_idx, self.Rt_val = Rt.indptr.astype(np.int64), Rt.indices.astype(np.int64), Rt.data.copy()
 
         # --- Gx-only pattern for the forward Newton (generic 1x1 mode) -------------------
         gkey = gx_c * n_x + gx_r
@@ -161,10 +207,7 @@ class MeshPlan:
         self.G_diag = gdiag.astype(np.int64)               # nnz positions of the diagonal
 
         # --- gradient gather: free dof <- element-gradient entries ------------------------
-        g_dof = el_dofs.ravel()
-        g_x = self.dof_to_x[g_dof]
-        gsel = np.flatnonzero(g_x >= 0)
-        self.grad_ptr, self.grad_src = _csr_from_lists(n_x, g_x[gsel], gsel.astype(np.int64))
+        self.grad_ptr, self.grad_src = _csr_from_lists(n_x, np.concatenate(g_rows), np.concatenate(g_src))
         self.grad_base = self.f_ext[self.free_dofs].copy()
 
 
@@ -186,8 +229,14 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
     if timings is not None:
         timings["factor_s"] = t2 - t1
     tol, mi = eng.stab.refine_tolerance, eng.stab.max_refine_iters
-    rc, res_a, it_a = eng.kfac.solve_refined(eng.kvals, eng.fvec, eng.sol_adj, tol, mi, True, st)
-    check(lib().sgn_adjoint_step(0, eng.batch, n_x, n_p, ptr(eng.sol_adj), None, ptr(eng.tmp), None, st))
+    if getattr(eng, "adjoint_gx", False):
+        # lambda = -G_x^{-T} f_x by a direct LDL^T of G_x, as the reference does with its LU
+        # of dc/dx (sensitivity.py:160-191); device problems have symmetric G_x
+        res_a, it_a = eng.adjoint_direct()
+    else:
+        # leading (x, lambda) block of the KKT factor preconditions [[A, G^T], [G, 0]]
+        rc, res_a, it_a = eng.kfac.solve_refined(eng.kvals, eng.fvec, eng.sol_adj, tol, mi, True, st)
+        check(lib().sgn_adjoint_step(0, eng.batch, n_x, n_p, ptr(eng.sol_adj), None, ptr(eng.tmp), None, st))
     eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, st)
     check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
                                  ptr(eng.grad), st))
@@ -225,8 +274,14 @@ class DeviceEngine:
         f64, i64 = torch.float64, torch.int64
         T = lambda a, dt=f64: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
         pl = plan
-        self.conn = T(pl.conn.astype(np.int32), torch.int32)
-        self.params = T(np.asarray(params, dtype=np.float64).reshape(B, -1))
+        self.conns = [T(g.conn.astype(np.int32), torch.int32) for g in pl.groups]
+        self.conn = self.conns[0]
+        plist = params if isinstance(params, (list, tuple)) else [params]
+        self.gparams = [T(np.asarray(pp, dtype=np.float64).reshape(B, -1)) for pp in plist]
+        self.params = self.gparams[0]
+        if pl.R is not None:
+            self.R_ptr, self.R_idx, self.R_val = T(pl.R_ptr, i64), T(pl.R_idx, i64), T(pl.R_val)
+            self.Rt_ptr, self.Rt_idx, self.Rt_val = T(pl.Rt_ptr, i64), T(pl.Rt_idx, i64), T(pl.Rt_val)
         self.tvals = T(np.asarray(tvals, dtype=np.float64).reshape(B, -1))
         self.tdofs = T(pl.target_dofs, i64)
         self.pos_base, self.pos_ptr, self.pos_idx = T(pl.pos_base), T(pl.pos_ptr, i64), T(pl.pos_idx, i64)
@@ -239,15 +294,16 @@ class DeviceEngine:
         self.grad_base, self.grad_ptr, self.grad_src = T(pl.grad_base), T(pl.grad_ptr, i64), T(pl.grad_src, i64)
         self.f_ext = T(pl.f_ext)
         self.f_ext_b = self.f_ext.reshape(1, -1).repeat(B, 1).contiguous()
-        nd2 = pl.n_e * pl.nd * pl.nd
         z = lambda *s: torch.zeros(*s, dtype=f64, device=dev)
         self.x = z(B, pl.n_x)
         self.p = z(B, pl.n_p)
         self.pos = z(B, pl.n_dof)
         self.rest = z(B, pl.n_dof)
-        self.ebuf = z(B, 2 * nd2)             # [hess | mixed]
-        self.egrad = z(B, pl.n_e * pl.nd)
-        self.eener = z(B, pl.n_e)
+        self.ebuf = z(B, pl.ebuf_size)       # per group [hess | mixed]
+        self.egrad = z(B, pl.egrad_size)
+        self.eeners = [z(B, g.n_e) for g in pl.groups]
+        self.eener = self.eeners[0]
+        self.rscr = z(B, max(int(pl.target_dofs.size), 1))
         self.kvals = z(B, pl.nnz)
         self.gvals = z(B, pl.G_nnz)
         self.fvec = z(B, pl.dim)
@@ -257,7 +313,7 @@ class DeviceEngine:
         self.tmp = z(B, pl.dim)
         self.grad = z(B, pl.n_p)
         self.fobj = z(B)
-        self.scal = z(8, B)              # rows: energy, linear energy, trace, |g|inf, ...
+        self.scal = z(8 + len(pl.groups), B)   # rows: energy, linear energy, trace, |g|inf, -, group energies
         self.gx = z(B, pl.n_x)
         self.kdir = z(B, pl.n_x)
         self.xtry = z(B, pl.n_x)
@@ -294,10 +350,10 @@ class DeviceEngine:
 
     def element_blocks(self):
         pl = self.plan
-        nd2 = pl.n_e * pl.nd * pl.nd
-        check(lib().sgn_element_derivs(pl.elem_code, pl.n_e, self.batch, ptr(self.conn), ptr(self.pos),
-                                       ptr(self.rest), pl.n_dof, ptr(self.params), self.params.stride(0),
-                                       ptr(self.ebuf), ptr(self.ebuf[:, nd2:]), 2 * nd2, self.stream))
+        for g, conn, prm in zip(pl.groups, self.conns, self.gparams):
+            check(lib().sgn_element_derivs(g.code, g.n_e, self.batch, ptr(conn), ptr(self.pos), ptr(self.rest),
+                                           pl.n_dof, ptr(prm), prm.stride(0), ptr(self.ebuf[:, g.hoff:]),
+                                           ptr(self.ebuf[:, g.moff:]), pl.ebuf_size, self.stream))
 
     def assemble_kkt(self):
         pl = self.plan
@@ -311,9 +367,7 @@ class DeviceEngine:
         self.positions()
         self.element_blocks()
         self.assemble_kkt()
-        check(lib().sgn_lsq_terms(self.batch, pl.n_x, pl.n_p, pl.target_dofs.size, ptr(self.tdofs),
-                                  ptr(self.tvals), self.tvals.stride(0), pl.w_target, pl.w_reg,
-                                  ptr(self.x), ptr(self.p), ptr(self.fvec), ptr(self.fobj), self.stream))
+        self._lsq(self.x, self.fvec)
 
     def direction(self, timings: dict | None = None):
         """SGN direction at the current (x, p) of every instance (solution in self.sol).
@@ -329,36 +383,72 @@ class DeviceEngine:
             timings["assemble_s"] = time.perf_counter() - t0
         return sgn_solve_stages(self, timings)
 
+    adjoint_gx = True
+
+    def adjoint_direct(self):
+        """w = G_x^{-1} f_x (unshifted LDL^T of the state Jacobian) placed as v = (0, 0, w)
+        in self.tmp; returns (res, iters) placeholders of the refined variant."""
+        pl = self.plan
+        st = self.stream
+        self._gather(pl.G_nnz, None, 0, self.G_ptr, self.G_src, None, self.ebuf, self.ebuf.stride(0),
+                     self.gvals, pl.G_nnz)
+        self.gfac.numeric(self.gvals, 0.0, 0.0, st)
+        self.gfac.check(st)
+        check(lib().sgn_adjoint_step(3, self.batch, pl.n_x, pl.n_p, ptr(self.fvec), None, ptr(self.xtry), None, st))
+        self.gfac.solve(self.xtry, self.kdir, False, st)
+        check(lib().sgn_adjoint_step(2, self.batch, pl.n_x, pl.n_p, ptr(self.kdir), None, ptr(self.tmp), None, st))
+        return np.zeros(self.batch), np.zeros(self.batch, dtype=np.int32)
+
     def split(self):
         pl = self.plan
         s = self.sol
         return s[:, :pl.n_x], s[:, pl.n_x:pl.n_x + pl.n_p], s[:, pl.n_x + pl.n_p:]
 
+    def _lsq(self, x, fvec):
+        """Least-squares terms (sensitivity.py:83-93) incl. the optional residual p-map R."""
+        pl = self.plan
+        if pl.R is None:
+            check(lib().sgn_lsq_terms(self.batch, pl.n_x, pl.n_p, pl.target_dofs.size, ptr(self.tdofs),
+                                      ptr(self.tvals), self.tvals.stride(0), pl.w_target, pl.w_reg,
+                                      ptr(x), ptr(self.p), ptr(fvec), ptr(self.fobj), self.stream))
+        else:
+            check(lib().sgn_lsq_terms_r(self.batch, pl.n_x, pl.n_p, pl.target_dofs.size, ptr(self.tdofs),
+                                        ptr(self.tvals), self.tvals.stride(0), pl.w_target, pl.w_reg,
+                                        ptr(x), ptr(self.p), ptr(fvec), ptr(self.fobj), ptr(self.R_ptr),
+                                        ptr(self.R_idx), ptr(self.R_val), ptr(self.Rt_ptr), ptr(self.Rt_idx),
+                                        ptr(self.Rt_val), ptr(self.rscr), self.stream))
+
     # -- objective ---------------------------------------------------------------------
     def objective(self, x=None):
         pl = self.plan
         x = self.x if x is None else x
-        check(lib().sgn_lsq_terms(self.batch, pl.n_x, pl.n_p, pl.target_dofs.size, ptr(self.tdofs),
-                                  ptr(self.tvals), self.tvals.stride(0), pl.w_target, pl.w_reg,
-                                  ptr(x), ptr(self.p), None, ptr(self.fobj), self.stream))
+        self._lsq(x, None)
         return self.fobj
 
     # -- forward statics (forward.py:135-203) --------------------------------------------
     def _energy_grad(self, x, want_grad=True):
+        """Energies (per group, reduced into scal[5+g]; scal[0] = their sum on read) and the
+        free-dof gradient gx of the current rest shape."""
         pl = self.plan
         st = self.stream
         self._gather(pl.n_dof, self.pos_base, 0, self.pos_ptr, self.pos_idx, None, x, pl.n_x,
                      self.pos, pl.n_dof)
-        check(lib().sgn_element_energy_grad(pl.elem_code, pl.n_e, self.batch, ptr(self.conn), ptr(self.pos),
-                                            ptr(self.rest), pl.n_dof, ptr(self.params), self.params.stride(0),
-                                            ptr(self.eener), ptr(self.egrad) if want_grad else 0,
-                                            pl.n_e * pl.nd, st))
-        check(lib().sgn_reduce(0, pl.n_e, self.batch, ptr(self.eener), None, pl.n_e, ptr(self.scal[0]), st))
-        check(lib().sgn_reduce(1, pl.n_dof, self.batch, ptr(self.f_ext_b),
-                               ptr(self.pos), pl.n_dof, ptr(self.scal[1]), st))
+        for gi, (g, conn, prm, en) in enumerate(zip(pl.groups, self.conns, self.gparams, self.eeners)):
+            check(lib().sgn_element_energy_grad(g.code, g.n_e, self.batch, ptr(conn), ptr(self.pos),
+                                                ptr(self.rest), pl.n_dof, ptr(prm), prm.stride(0), ptr(en),
+                                                ptr(self.egrad[:, g.goff:]) if want_grad else 0,
+                                                pl.egrad_size, st))
+            check(lib().sgn_reduce(0, g.n_e, self.batch, ptr(en), None, g.n_e, ptr(self.scal[5 + gi]), st))
+        check(lib().sgn_reduce(1, pl.n_dof, self.batch, ptr(self.f_ext_b), ptr(self.pos), pl.n_dof,
+                               ptr(self.scal[1]), st))
         if want_grad:
             self._gather(pl.n_x, self.grad_base, 0, self.grad_ptr, self.grad_src, None, self.egrad,
-                         pl.n_e * pl.nd, self.gx, pl.n_x)
+                         pl.egrad_size, self.gx, pl.n_x)
+
+    def _energies(self, sc):
+        """Total energy per instance from a host copy of scal."""
+        ng = len(self.plan.groups)
+        return sc[5:5 + ng].sum(axis=0) + sc[1]
 
     def _hessian(self):
         pl = self.plan
@@ -409,7 +499,7 @@ class DeviceEngine:
             self._energy_grad(self.x)
             check(lib().sgn_reduce(2, n, B, ptr(self.gx), None, n, ptr(self.scal[3]), st))
             sc = self.scal.cpu().numpy()
-            g_inf, e0 = sc[3], sc[0] + sc[1]
+            g_inf, e0 = sc[3], self._energies(sc)
             status[run & (g_inf <= tol)] = 1
             run = status == 0
             if not run.any():
@@ -483,7 +573,7 @@ class DeviceEngine:
             check(lib().sgn_axpy(n, B, ptr(a_t), ptr(self.kdir), ptr(self.x), ptr(self.xtry), n, st))
             self._energy_grad(self.xtry, want_grad=False)
             sc = self.scal.cpu().numpy()
-            et = sc[0] + sc[1]
+            et = self._energies(sc)
             acc = pending & np.isfinite(et) & (et <= e0 + c1 * alpha * slope + slack)
             if acc.any():
                 check(lib().sgn_masked_copy(n, B, ptr(self._mask(acc)), ptr(self.xtry), ptr(self.x), n, st))

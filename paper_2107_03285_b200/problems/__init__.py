@@ -23,7 +23,7 @@ from ..errors import CapabilityMissing, ForwardSimFailure
 from ..sparse import CscMatrix
 
 __all__ = ["ElasticDesignProblem", "BatchedDesign", "beam_spec", "build_beam", "build_sheet", "build_sheet_batch",
-           "build_spring_bar", "sheet_spec"]
+           "build_shell", "build_spring_bar", "sheet_spec", "shell_spec"]
 
 
 class ElasticDesignProblem:
@@ -31,15 +31,20 @@ class ElasticDesignProblem:
 
     def __init__(self, X0, conn, kind, fixed_verts, pmap, target_dofs, target_vals, w_target=1.0,
                  w_reg=0.0, E=1.0, nu=0.3, gload=0.0, stiffness=None, scale=None, tol=1e-12,
-                 f_ext=None, rest_base=None, p_offset=None, name=None, stab=None):
+                 f_ext=None, rest_base=None, p_offset=None, name=None, stab=None, groups=None,
+                 group_params=None, R=None):
         self.plan = MeshPlan(X0, conn, kind, fixed_verts, pmap, target_dofs, w_target, w_reg,
-                             f_ext=f_ext, rest_base=rest_base)
+                             f_ext=f_ext, rest_base=rest_base, groups=groups, R=R)
         mu, lam = (E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu)))
         sc = (1.0 / E) if scale is None else float(scale)
-        params = [mu, lam, gload, sc]
-        if stiffness is not None:
-            params += list(np.asarray(stiffness, dtype=np.float64))
-        self.params = np.asarray(params, dtype=np.float64)
+        if group_params is not None:
+            self.params = [np.asarray(gp, dtype=np.float64) for gp in group_params]
+        else:
+            params = [mu, lam, gload, sc]
+            if stiffness is not None:
+                params += list(np.asarray(stiffness, dtype=np.float64))
+            self.params = np.asarray(params, dtype=np.float64)
+        self.R = None if R is None else sp.csr_matrix(R)
         self.target_vals = np.asarray(target_vals, dtype=np.float64)
         self.engine = DeviceEngine(self.plan, self.params, self.target_vals, batch=1, stab=stab)
         self.n_x, self.n_p = self.plan.n_x, self.plan.n_p
@@ -122,7 +127,10 @@ class ElasticDesignProblem:
     # -- least squares ------------------------------------------------------------------
     def residuals(self, x, p):
         pl = self.plan
-        out = [np.asarray(x)[pl.target_dofs] - self.target_vals]
+        r = np.asarray(x)[pl.target_dofs] - self.target_vals
+        if self.R is not None:
+            r = r - self.R @ np.asarray(p, dtype=np.float64)
+        out = [r]
         if pl.w_reg > 0.0:
             out.append(np.asarray(p, dtype=np.float64).copy())
         return np.concatenate(out)
@@ -145,10 +153,10 @@ class ElasticDesignProblem:
     def residual_jac_p(self, x, p):
         pl = self.plan
         nt = pl.target_dofs.size
+        top = -self.R if self.R is not None else sp.csc_matrix((nt, pl.n_p))
         if pl.w_reg > 0.0:
-            return CscMatrix.from_scipy(sp.vstack([sp.csc_matrix((nt, pl.n_p)),
-                                                   sp.identity(pl.n_p, format="csc")], format="csc"))
-        return CscMatrix.zeros(nt, pl.n_p)
+            return CscMatrix.from_scipy(sp.vstack([top, sp.identity(pl.n_p, format="csc")], format="csc"))
+        return CscMatrix.from_scipy(sp.csc_matrix(top))
 
     def objective(self, x, p) -> float:
         self._load(x, p)
@@ -388,3 +396,70 @@ def build_beam(seed: int = 0, **kw):
     prob.target_vals = lifted
     prob.engine.tvals.copy_(prob.engine.torch.as_tensor(lifted).reshape(1, -1))
     return prob, p0, sag
+
+
+def shell_spec(n: int = 201, nc: int = 100, L: float = 1.0, t: float = 0.05, E: float = 3e10,
+               nu: float = 0.2, rho: float = 2400.0, g: float = 9.81, w_reg: float = 2e-4) -> dict:
+    """BASELINE config 4 (n = 201, nc = 100): triangulated square, StVK membrane + dihedral
+    hinges, four corners pinned, rest heights = bilinear interpolation of an nc x nc control
+    lattice, objective 0.5 |x_z - X_z(p)|^2 + 1e-4 |p|^2.  Re-implemented from
+    oracle/shell.shell_spec (asserted equal in tests)."""
+    ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    X0 = np.column_stack([ii.ravel() * L / (n - 1), jj.ravel() * L / (n - 1), np.zeros(n * n)])
+    i, j = np.meshgrid(np.arange(n - 1), np.arange(n - 1), indexing="ij")
+    a = (i * n + j).ravel(); b = ((i + 1) * n + j).ravel()
+    c = ((i + 1) * n + j + 1).ravel(); d = (i * n + j + 1).ravel()
+    tris = np.stack([np.column_stack([a, b, c]), np.column_stack([a, c, d])], axis=1).reshape(-1, 3)
+    owner, hinges = {}, []
+    for tri in tris.tolist():
+        for k in range(3):
+            u, v, w = tri[k], tri[(k + 1) % 3], tri[(k + 2) % 3]
+            if (v, u) in owner:
+                hinges.append((v, u, owner.pop((v, u)), w))
+            else:
+                owner[(u, v)] = w
+    hinges = np.array(sorted(hinges), dtype=np.int64)
+    corners = np.array([0, n - 1, (n - 1) * n, n * n - 1])
+    h = L / (nc - 1)
+    pm_dof, pm_p, pm_coef = [], [], []
+    for v in range(n * n):
+        x, y = X0[v, 0], X0[v, 1]
+        ca, cb = min(int(np.floor(x / h + 1e-12)), nc - 2), min(int(np.floor(y / h + 1e-12)), nc - 2)
+        s_, tt = x / h - ca, y / h - cb
+        for (da, db, wgt) in ((0, 0, (1 - s_) * (1 - tt)), (1, 0, s_ * (1 - tt)), (0, 1, (1 - s_) * tt), (1, 1, s_ * tt)):
+            if wgt > 1e-14:
+                pm_dof.append(3 * v + 2)
+                pm_p.append((ca + da) * nc + (cb + db))
+                pm_coef.append(wgt)
+    free = np.setdiff1d(np.arange(n * n), corners)
+    v2f = -np.ones(n * n, dtype=np.int64)
+    v2f[free] = np.arange(free.size)
+    tdofs = v2f[free] * 3 + 2
+    alpha, beta = E * nu / (1 - nu ** 2), E / (2 * (1 + nu))
+    kb = E * t ** 3 / (24 * (1 - nu ** 2))
+    return dict(X0=X0, tris=tris, hinges=hinges, fixed_verts=corners,
+                pmap=(np.array(pm_dof), np.array(pm_p), np.array(pm_coef)), target_dofs=tdofs,
+                target_vals=np.zeros(tdofs.size), w_target=1.0, w_reg=w_reg, E=E, t=t, nu=nu,
+                alpha=alpha, beta=beta, kb=kb, rho_g=rho * g, n_p=nc * nc, p0=np.zeros(nc * nc),
+                name=f"shell_{n}x{n}_c{nc}")
+
+
+def build_shell(n: int = 201, nc: int = 100, **kw):
+    """(problem, p0) for config 4 (or a smaller n / nc variant for tests)."""
+    s = shell_spec(n, nc)
+    pm_dof, pm_p, pm_coef = s["pmap"]
+    n_v = s["X0"].shape[0]
+    P = sp.csr_matrix((pm_coef, (pm_dof, pm_p)), shape=(3 * n_v, s["n_p"]))
+    fixed = np.zeros(n_v, bool)
+    fixed[s["fixed_verts"]] = True
+    free_verts = np.flatnonzero(~fixed)
+    free_dofs = (free_verts[:, None] * 3 + np.arange(3)[None, :]).ravel()
+    R = sp.csr_matrix(P[free_dofs][s["target_dofs"]])       # X_z(p) at the target dofs
+    sc = 1.0 / s["E"]
+    membrane = [s["alpha"], s["beta"], s["rho_g"], sc, s["t"]]
+    hinge = [s["kb"], 0.0, 0.0, sc]
+    prob = ElasticDesignProblem(s["X0"], None, None, s["fixed_verts"], s["pmap"], s["target_dofs"],
+                                s["target_vals"], w_target=s["w_target"], w_reg=s["w_reg"],
+                                groups=[("membrane", s["tris"]), ("hinge", s["hinges"])],
+                                group_params=[membrane, hinge], R=R, name=s["name"], **kw)
+    return prob, s["p0"]

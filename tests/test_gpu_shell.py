@@ -1,0 +1,72 @@
+"""BASELINE config 4 machinery (StVK membrane + dihedral hinges + bilinear control lattice)
+on a 21x21 shell with a 10x10 control lattice, device vs the CPU oracle (oracle/shell.py)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def shell():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from oracle.shell import ShellProblem, shell_spec
+    from paper_2107_03285_b200.problems import build_shell
+    prob, p0 = build_shell(21, 10)
+    oprob = ShellProblem(shell_spec(21, 10))
+    rng = np.random.default_rng(5)
+    p = p0 + 1e-3 * rng.standard_normal(p0.size)     # a curved rest shape (non-zero rest angles)
+    return prob, oprob, p
+
+
+def test_shell_element_blocks_match_oracle(shell):
+    from oracle import shell as osh
+    prob, oprob, p = shell
+    x = oprob.simulate(p)
+    prob._load(x, p)
+    prob.engine.positions()
+    prob.engine.element_blocks()
+    buf = prob.engine.ebuf[0].cpu().numpy()
+    pos, rest = oprob.full_positions(x), oprob.rest_positions(p)
+    s = oprob.s
+    for g, (fn, args) in zip(prob.plan.groups, [(osh.membrane_energy, (s["t"], s["alpha"], s["beta"], s["rho_g"])),
+                                                 (osh.hinge_energy, (s["kb"],))]):
+        nd2 = g.n_e * g.nd * g.nd
+        H = buf[g.hoff:g.hoff + nd2].reshape(g.n_e, g.nd, g.nd)
+        M = buf[g.moff:g.moff + nd2].reshape(g.n_e, g.nd, g.nd)
+        _, Ho, Mo = osh.element_derivs(fn, pos[g.conn], rest[g.conn], *args)
+        assert _rel(H, oprob.scale * Ho) <= 1e-11, g.kind
+        assert _rel(M, oprob.scale * Mo) <= 1e-11, g.kind
+
+
+def test_shell_simulate_kkt_and_direction(shell):
+    from oracle import sgn_cpu
+    from paper_2107_03285_b200 import OptimizerConfig, adjoint_gradient, direction_sgn
+    prob, oprob, p = shell
+    x = prob.simulate(p)
+    assert np.abs(oprob.constraints(x, p)).max() <= 1e-12         # device equilibrium, oracle physics
+    K = prob.kkt_matrix(x, p)
+    Kr, rhs_r, g_r = sgn_cpu.assemble_sgn(oprob, x, p)
+    np.testing.assert_array_equal(K.indptr, Kr.indptr)
+    np.testing.assert_array_equal(K.indices, Kr.indices)
+    assert np.max(np.abs(K.data - Kr.data)) <= 1e-12 * np.max(np.abs(Kr.data))
+    g = adjoint_gradient(prob, x, p)
+    assert _rel(g, g_r) <= 1e-9
+    sd = direction_sgn(prob, x, p, OptimizerConfig())
+    assert sd.relative_residual <= 1e-10
+    sol = np.concatenate([sd.dx, sd.dp, sd.dlam])
+    rhs = np.zeros_like(rhs_r)
+    rhs[prob.n_x:prob.n_x + prob.n_p] = -g
+    assert np.linalg.norm(Kr.to_scipy() @ sol - rhs) <= 2e-10 * np.linalg.norm(rhs)
+    ref = sgn_cpu.direction_sgn(oprob, x, p)
+    dgn = sgn_cpu.direction_dgn(oprob, x, p)
+    # the reduced Hessian is ill-conditioned (t^2/12 bending/membrane ratio): require agreement
+    # with the oracle's SGN as tight as the oracle's own SGN-vs-DGN consistency (Theorem 1)
+    self_gap = _rel(ref.dp, dgn.dp)
+    assert _rel(sd.dp, ref.dp) <= max(1e-8, 10.0 * self_gap)
+    assert abs(prob.objective(x, p) - oprob.objective(x, p)) <= 1e-12 * max(1.0, abs(oprob.objective(x, p)))
