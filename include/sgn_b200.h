@@ -106,6 +106,13 @@ int  sgn_factor_check(sgn_factor f, void* stream, int64_t* pivot_index);
 int  sgn_factor_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, void* stream);
 void sgn_factor_destroy(sgn_factor f);
 
+/* Diagnostics (no reference counterpart): the persistent solve's task list and, when the
+ * process ran with SGN_DAG_TRACE=1, the last solve's per-task trace -- 6 words per task
+ * (start, (smid << 48) | signalled, prefetched, ready, combined, end; globaltimer ns,
+ * 0 = phase not reached).  meta: 5 int32 per task
+ * (kind, front, level, a, b); any output pointer may be NULL.                         */
+int  sgn_debug_solve_trace(sgn_factor f, int64_t* out, int64_t cap, int64_t* n_tasks, int32_t* meta);
+
 /* y = K x on the full symmetric CSC pattern (which equals its CSR).  Replaces the
  * scipy SpMV of _relative_residual / _bicgstab_refine (linear_solvers.py:105-108,178-211).
  * flags: SGN_SOLVE_LEADING masks the p block (input and output).                   */

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -694,6 +695,316 @@ __global__ void k_permute_out(const double* __restrict__ y, double* __restrict__
 }
 
 // ------------------------------------------------------------------------------------
+// Persistent dependency-driven triangular solve: ONE launch per solve.  Resident CTAs grab
+// tasks (gather / forward GEMV / backward dots, see symbolic.cpp "persistent solve DAG") in
+// topological order from a global head counter, spin on their (counter, target) waits with
+// gpu-scope acquire loads, run the body and release their counter.  Every value produced
+// inside the launch (v, u, z, x, chunk partials) is read with ld.global.cg (L2), never
+// through a possibly stale L1 line.  The permutation in/out is folded into the gather
+// (b[perm]) and the backward step (x[perm] = ...).
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct SolveArgs {
+  const sgn::Task* tasks; const int32_t* waits; int64_t ntask; int batch;
+  int* head; int* cnt; int n_cnt;
+  const DFront* fronts; const int64_t* srows; const int64_t* gptr; const int32_t* gsrc;
+  const int64_t* perm; const double* fstore; int64_t fstride; const double* zstore; int64_t zstride;
+  double* ubuf; int64_t ustride; double* zbuf; double* xbuf;
+  int64_t n; double* part; int64_t pstride; int* tickets; int64_t n_groups;
+  const int32_t* grp_nchunk; const int64_t* grp_base;
+  const double* b_in; double* x_out; int leading; int nop; int mode;
+  unsigned long long* trace;   // optional, 6 words per task: start, smid|signalled, prefetched, ready, combined, end
+};
+
+// thread 0 spins on the task's (counter, target) pairs; the CTA leaves together
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+
+
+__device__ __forceinline__ void dag_mark(const SolveArgs& A, int64_t idx, int slot) {
+  if (A.trace && threadIdx.x == 0) A.trace[idx * 6 + slot] = gtimer();
+}
+
+__device__ __forceinline__ void dag_wait(const SolveArgs& A, const sgn::Task& T, const int* cnt) {
+  if (threadIdx.x == 0) {
+    for (int w = T.w0; w < T.w1; ++w) {
+      const int* c = cnt + A.waits[2 * w];
+      const int target = A.waits[2 * w + 1];
+      if (A.mode & 1) { while (ld_acquire(c) < target) { } }
+      else { while (ld_acquire(c) < target) __nanosleep(20); }
+    }
+  }
+  __syncthreads();
+}
+
+// last-arriving CTA of a chunk group: one acq_rel ticket atomic (releases this CTA's
+// partial, acquires the others'); the ticket is reset for the next solve
+__device__ __forceinline__ bool dag_group_last(int* ticket, int nch) {
+  __shared__ int last;
+  __syncthreads();                   // the CTA's partial stores precede thread 0's release
+  if (threadIdx.x == 0) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(ticket) : "memory");
+    last = (old == nch - 1);
+    if (last) *ticket = 0;
+  }
+  __syncthreads();
+  return last != 0;
+}
+
+// deterministic sum of nch 32-wide chunk partials: warp w adds chunks w, w+8, ... (loads
+// in flight together), warp 0 then adds the 8 warp sums in order.  Valid in warp 0.
+__device__ __forceinline__ double dag_combine(const double* pp, int nch, double (*red)[33]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double t = 0.0;
+#pragma unroll 4
+  for (int kk = w; kk < nch; kk += 8) t += __ldcg(pp + kk * 32 + lane);
+  red[w][lane] = t;
+  __syncthreads();
+  double s = 0.0;
+  if (w == 0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += red[q][lane];
+  }
+  return s;
+}
+
+// Forward GEMV task (front, 32-row tile, 64-column chunk).  Before waiting it prefetches
+// its Z tile (8 values per thread) and the inverse gather map of the v entries it needs
+// (64 chunk columns + its own struct rows); after the children are done it forms those v
+// entries (b + children updates in child order), multiplies, and the group's last CTA
+// emits z = D^{-1} y1 (pivot rows) or u = v2 - t (struct rows, the parent's update).
+__device__ bool dag_fwd(const SolveArgs& A, const sgn::Task& T, int b, const int* cnt, int64_t idx) {
+  __shared__ double red[8][33];
+  __shared__ double vs[sgn::kFwdCols + sgn::kFwdRows];
+  const DFront F = A.fronts[T.f];
+  const int r0 = T.a, k = T.b, g = T.c;
+  if (A.nop || (A.leading && F.is_root_p)) { dag_wait(A, T, cnt); return k == 0; }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nr = min(sgn::kFwdRows, F.nrow - r0);
+  const int npiv = F.npiv;
+  const int cend = (r0 < npiv) ? min(npiv, r0 + nr) : npiv;
+  const int c_lo = k * sgn::kFwdCols, c_hi = min(c_lo + sgn::kFwdCols, cend);
+  const double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
+  const int64_t ld = F.nrow;
+  double z[8];
+  {
+    const double* zr = Zm + r0 + lane;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int c = c_lo + warp + 8 * m;
+      z[m] = (lane < nr && c < c_hi) ? zr[(int64_t)c * ld] : 0.0;
+    }
+  }
+  int vr = -1;
+  if (tid < sgn::kFwdCols) {
+    if (c_lo + tid < c_hi) vr = c_lo + tid;
+  } else if (tid < sgn::kFwdCols + sgn::kFwdRows) {
+    const int r = r0 + tid - sgn::kFwdCols;
+    if (r < F.nrow && r >= npiv) vr = r;
+  }
+  double base = 0.0;
+  int64_t q0 = 0, q1 = 0;
+  int sq[4] = {0, 0, 0, 0};
+  if (vr >= 0) {
+    base = (vr < npiv) ? A.b_in[(int64_t)b * A.n + A.perm[F.first + vr]] : 0.0;
+    q0 = A.gptr[F.voff + vr];
+    q1 = A.gptr[F.voff + vr + 1];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (q0 + j < q1) sq[j] = A.gsrc[q0 + j];
+  }
+  // pivot rows of this tile: the D block entries the final step needs (static)
+  double da = 1.0, db = 0.0, dc = 1.0;
+  if (warp == 0 && lane < nr && r0 + lane < npiv) {
+    const double* Fm = A.fstore + (int64_t)b * A.fstride + F.foff;
+    const int r = r0 + lane;
+    if (F.pivtype == 2) {
+      const int re = r & ~1;
+      da = Fm[(int64_t)re * ld + re]; db = Fm[(int64_t)re * ld + re + 1]; dc = Fm[(int64_t)(re + 1) * ld + re + 1];
+    } else {
+      da = Fm[(int64_t)r * ld + r];
+    }
+  }
+  dag_mark(A, idx, 2);
+  dag_wait(A, T, cnt);
+  dag_mark(A, idx, 3);
+  if (tid < sgn::kFwdCols + sgn::kFwdRows) {
+    double v = 0.0;
+    if (vr >= 0) {
+      const double* ub = A.ubuf + (int64_t)b * A.ustride;
+      double u[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) u[j] = (q0 + j < q1) ? __ldcg(ub + sq[j]) : 0.0;
+      v = base;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) if (q0 + j < q1) v += u[j];
+      for (int64_t q = q0 + 4; q < q1; ++q) v += __ldcg(ub + A.gsrc[q]);
+    }
+    vs[tid] = v;
+  }
+  __syncthreads();
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) acc += z[m] * vs[warp + 8 * m];
+  red[warp][lane] = acc;
+  __syncthreads();
+  const int nch = A.grp_nchunk[g];
+  double t = 0.0;
+  if (warp == 0) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+  }
+  if (nch > 1) {
+    double* pp = A.part + (int64_t)b * A.pstride + A.grp_base[g];
+    if (warp == 0) pp[k * 32 + lane] = t;
+    if (!dag_group_last(A.tickets + (int64_t)b * A.n_groups + g, nch)) return false;
+    dag_mark(A, idx, 4);
+    t = dag_combine(pp, nch, red);
+  }
+  if (warp == 0) {
+    const double tp = __shfl_xor_sync(0xffffffffu, t, 1);   // 2x2 pivot partner row
+    if (lane < nr) {
+      const int r = r0 + lane;
+      if (r < npiv) {
+        double* zb = A.zbuf + (int64_t)b * A.n;
+        if (F.pivtype == 2) {
+          const double det = da * dc - db * db;
+          zb[F.first + r] = ((r & 1) == 0) ? (dc * t - db * tp) / det : (da * t - db * tp) / det;
+        } else {
+          zb[F.first + r] = t / da;
+        }
+      } else {
+        A.ubuf[(int64_t)b * A.ustride + F.uoff + (r - npiv)] = vs[sgn::kFwdCols + lane] - t;
+      }
+    }
+  }
+  return true;
+}
+
+// Backward task (front, 32-column tile, 128-row chunk): x1 = Z^T [z1; -x2] as column dots.
+// Z (16 values per thread) and the struct-row map are prefetched before the wait.
+__device__ bool dag_bwd(const SolveArgs& A, const sgn::Task& T, int b, const int* cnt, int64_t idx) {
+  __shared__ double colsum[32];
+  __shared__ double vs[sgn::kBwdRows];
+  const DFront F = A.fronts[T.f];
+  const int c0 = T.a, rs = T.b, g = T.c;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ncol = min(sgn::kBwdCols, F.npiv - c0);
+  double* xb = A.xbuf + (int64_t)b * A.n;
+  double* xo = A.x_out + (int64_t)b * A.n;
+  const bool first_chunk = (rs == (c0 / sgn::kBwdRows) * sgn::kBwdRows);
+  if (A.nop) { dag_wait(A, T, cnt); return first_chunk; }
+  if (A.leading && F.is_root_p) {
+    dag_wait(A, T, cnt);
+    if (first_chunk)
+      for (int j = tid; j < ncol; j += blockDim.x) {
+        xb[F.first + c0 + j] = 0.0;
+        xo[A.perm[F.first + c0 + j]] = 0.0;
+      }
+    return first_chunk;
+  }
+  const double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
+  const int64_t ld = F.nrow;
+  const int np = F.npiv;
+  const int re = min(rs + sgn::kBwdRows, F.nrow);
+  double z[4][4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int j = c0 + warp + 8 * m;
+    const bool colok = (warp + 8 * m < ncol);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = rs + lane + 32 * i;
+      z[m][i] = (colok && r < re && r >= j) ? Zm[(int64_t)j * ld + r] : 0.0;
+    }
+  }
+  int64_t srow = -1;
+  if (tid < re - rs && rs + tid >= np) srow = A.srows[F.srow_off + rs + tid - np];
+  dag_mark(A, idx, 2);
+  dag_wait(A, T, cnt);
+  dag_mark(A, idx, 3);
+  if (tid < sgn::kBwdRows) {
+    double v = 0.0;
+    if (tid < re - rs)
+      v = (rs + tid < np) ? __ldcg(A.zbuf + (int64_t)b * A.n + F.first + rs + tid) : -__ldcg(xb + srow);
+    vs[tid] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    double a = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a += z[m][i] * vs[lane + 32 * i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) colsum[warp + 8 * m] = a;
+  }
+  __syncthreads();
+  const int nch = A.grp_nchunk[g];
+  double* pp = A.part + (int64_t)b * A.pstride + A.grp_base[g];
+  const int k = (rs - (c0 / sgn::kBwdRows) * sgn::kBwdRows) / sgn::kBwdRows;
+  double t = 0.0;
+  if (nch > 1) {
+    __shared__ double red[8][33];
+    if (tid < 32) pp[k * 32 + tid] = colsum[tid];
+    if (!dag_group_last(A.tickets + (int64_t)b * A.n_groups + g, nch)) return false;
+    dag_mark(A, idx, 4);
+    t = dag_combine(pp, nch, red);
+  } else if (tid < ncol) {
+    t = colsum[tid];
+  }
+  if (tid < ncol) {
+    xb[F.first + c0 + tid] = t;
+    xo[A.perm[F.first + c0 + tid]] = t;
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(kSolveThreads)
+k_solve_dag(const SolveArgs A) {
+  __shared__ int s_idx;
+  const int64_t total = A.ntask * A.batch;
+  for (;;) {
+    __syncthreads();                               // s_idx of the previous task consumed
+    if (threadIdx.x == 0) s_idx = atomicAdd(A.head, 1);
+    __syncthreads();
+    const int64_t idx = s_idx;
+    if (idx >= total) return;
+    const int64_t ti = idx / A.batch;
+    const int b = (int)(idx - ti * A.batch);
+    const sgn::Task T = A.tasks[ti];
+    int* cnt = A.cnt + (int64_t)b * A.n_cnt;
+    unsigned long long t0 = 0;
+    if (A.trace && threadIdx.x == 0) t0 = gtimer();
+    const bool sig = (T.kind == sgn::T_FWD) ? dag_fwd(A, T, b, cnt, idx) : dag_bwd(A, T, b, cnt, idx);
+    __syncthreads();                               // every thread's writes precede the release
+    if (sig && threadIdx.x == 0) {
+      asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(cnt + T.sig) : "memory");
+    }
+    if (A.trace && threadIdx.x == 0) {
+      unsigned long long* tr = A.trace + idx * 6;
+      tr[0] = t0;
+      tr[5] = gtimer();
+      tr[1] = ((unsigned long long)smid() << 48) | (sig ? 1ull : 0ull);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // SpMV on the symmetric pattern (CSC == CSR), 8 lanes per row
 // ------------------------------------------------------------------------------------
 __global__ void k_spmv(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
@@ -902,6 +1213,12 @@ struct sgn_factor_s {
   DevBuf<int32_t> grp_nchunk;
   DevBuf<int64_t> grp_base;
   DevBuf<long long> status;
+  DevBuf<sgn::Task> stasks;
+  DevBuf<int32_t> swaits, gsrc;
+  DevBuf<int64_t> gptr;
+  DevBuf<int64_t> trace;        // SGN_DAG_TRACE=1: 3 words per solve task (diagnostics)
+  DevBuf<int> scnt;             // [head | batch x n_scnt counters], zeroed before every solve
+  int solve_grid = 0;
   std::vector<int64_t> lvl_off;  // level -> offset into lvl_fronts
   // BiCGSTAB workspace
   DevBuf<double> bx, br, brh, bp, bv, bs, bt, btmp, bbest, bb, bscr, partial;
@@ -965,11 +1282,49 @@ int launch_solve_raw(sgn_factor f, const double* d_b, double* d_x, int32_t flags
 }
 
 
-// The solve is a fixed launch sequence per (factor, flags): capture it once as a CUDA
-// graph and replay it, patching only the permute-in / permute-out pointer arguments.
+// One solve = a counter reset + ONE persistent dependency-driven launch (k_solve_dag).
+int launch_solve_dag(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st) {
+  const sgn::Symbolic& s = f->sym->s;
+  SolveArgs A;
+  A.tasks = f->stasks.p; A.waits = f->swaits.p; A.ntask = (int64_t)s.stasks.size(); A.batch = f->batch;
+  A.head = f->scnt.p; A.cnt = f->scnt.p + 1; A.n_cnt = s.n_scnt;
+  A.fronts = f->fronts.p; A.srows = f->srows.p; A.gptr = f->gptr.p; A.gsrc = f->gsrc.p;
+  A.perm = f->perm.p; A.fstore = f->fstore.p; A.fstride = s.front_doubles;
+  A.zstore = f->zstore.p; A.zstride = s.z_doubles; A.ubuf = f->ubuf.p; A.ustride = s.u_doubles;
+  A.zbuf = f->zbuf.p; A.xbuf = f->xbuf.p; A.n = s.n;
+  A.part = f->part.p; A.pstride = s.part_doubles; A.tickets = f->tickets.p; A.n_groups = s.n_groups;
+  A.grp_nchunk = f->grp_nchunk.p; A.grp_base = f->grp_base.p;
+  A.b_in = d_b; A.x_out = d_x; A.leading = (flags & SGN_SOLVE_LEADING) ? 1 : 0;
+  { const char* e = getenv("SGN_DAG_NOP"); A.nop = (e && *e == '1') ? 1 : 0; }
+  A.trace = nullptr;   // SGN_DAG_TRACE=1: 6 words per task
+  { const char* e = getenv("SGN_DAG_MODE"); A.mode = e ? atoi(e) : 0; }
+  { const char* e = getenv("SGN_DAG_TRACE");
+    if (e && *e == '1') {
+      if (!f->trace.p && f->trace.alloc((size_t)6 * std::max<int64_t>(1, (int64_t)s.stasks.size() * f->batch))) return SGN_CUDA_ERROR;
+      A.trace = (unsigned long long*)f->trace.p;
+      CUDA_TRY(cudaMemsetAsync(f->trace.p, 0, f->trace.n * sizeof(int64_t), st));
+    } }
+  CUDA_TRY(cudaMemsetAsync(f->scnt.p, 0, f->scnt.n * sizeof(int), st));
+  const int64_t total = A.ntask * A.batch;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(f->solve_grid, total));
+  sgn::count_launch();
+  k_solve_dag<<<grid, kSolveThreads, 0, st>>>(A);
+  CUDA_TRY(cudaGetLastError());
+  return SGN_OK;
+}
+
+static bool use_level_solve() {
+  static const int v = [] { const char* e = getenv("SGN_SOLVE_LEVELS"); return (e && *e == '1') ? 1 : 0; }();
+  return v != 0;
+}
+
+// Level-scheduled alternative (SGN_SOLVE_LEVELS=1, kept for A/B timing): a fixed launch
+// sequence per (factor, flags), captured once as a CUDA graph and replayed, patching only
+// the permute-in / permute-out pointer arguments.
 int launch_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st) {
   const int64_t n = f->n;
   if (n == 0) return SGN_OK;
+  if (!use_level_solve()) return launch_solve_dag(f, d_b, d_x, flags, st);
   auto& G = f->graphs[(flags & SGN_SOLVE_LEADING) ? 1 : 0];
   if (!G.exec) {
     const double* cap_in = f->bbuf_in();   // allocate before capturing
@@ -1170,8 +1525,18 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
   if ((rc = f->part.alloc(B * std::max<int64_t>(s.part_doubles, 1))) ||
       (rc = f->dscr.alloc(B * std::max<int64_t>(s.d_doubles, 1))) ||
       (rc = f->tickets.alloc(B * std::max<int64_t>(s.n_groups, 1))) ||
-      (rc = f->grp_nchunk.upload(s.grp_nchunk)) || (rc = f->grp_base.upload(s.grp_base)))
+      (rc = f->grp_nchunk.upload(s.grp_nchunk)) || (rc = f->grp_base.upload(s.grp_base)) ||
+      (rc = f->stasks.upload(s.stasks)) || (rc = f->swaits.upload(s.swaits)) ||
+      (rc = f->gptr.upload(s.gptr)) || (rc = f->gsrc.upload(s.gsrc)) ||
+      (rc = f->scnt.alloc(1 + B * std::max<int64_t>(s.n_scnt, 1))))
     return rc;
+  {
+    int dev = 0, sms = 0, per_sm = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_dag, kSolveThreads, 0));
+    f->solve_grid = std::max(1, sms * std::max(per_sm, 1));
+  }
   CUDA_TRY(cudaMemset(f->tickets.p, 0, f->tickets.n * sizeof(int)));
   // Z11 = L11^{-1} is lower triangular: the strictly upper part stays zero forever
   CUDA_TRY(cudaMemset(f->zstore.p, 0, f->zstore.n * sizeof(double)));
@@ -1264,6 +1629,24 @@ int sgn_factor_status(sgn_factor f, void* stream, int64_t* pivots) {
   CUDA_TRY(cudaMemcpyAsync(h.data(), f->status.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   for (int b = 0; b < f->batch; ++b) pivots[b] = (h[b] == (long long)INT64_MAX) ? -1 : (int64_t)h[b];
+  return SGN_OK;
+}
+
+int sgn_debug_solve_trace(sgn_factor f, int64_t* out, int64_t cap, int64_t* n_tasks, int32_t* meta) {
+  const sgn::Symbolic& s = f->sym->s;
+  const int64_t nt = (int64_t)s.stasks.size() * f->batch;
+  if (n_tasks) *n_tasks = nt;
+  if (meta) {   // per task: kind, front, level, a, b
+    for (size_t t = 0; t < s.stasks.size(); ++t) {
+      const sgn::Task& T = s.stasks[t];
+      meta[5 * t] = T.kind; meta[5 * t + 1] = T.f; meta[5 * t + 2] = s.fronts[T.f].level;
+      meta[5 * t + 3] = T.a; meta[5 * t + 4] = T.b;
+    }
+  }
+  if (out && f->trace.p) {
+    const int64_t m = std::min<int64_t>(cap, 6 * nt);
+    CUDA_TRY(cudaMemcpy(out, f->trace.p, m * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  }
   return SGN_OK;
 }
 

@@ -53,7 +53,13 @@ enum LaunchKind : int32_t { L_ASM = 0, L_PANEL = 1, L_UPDATE = 2, L_ZPANEL = 3 }
 constexpr int kFwdRows = 32;    // rows per CTA of the forward-solve GEMV
 constexpr int kFwdCols = 64;    // columns (K chunk) per CTA of the forward-solve GEMV
 constexpr int kBwdCols = 32;    // columns per CTA of the backward-solve dots
-constexpr int kBwdRows = 256;   // rows (K chunk) per CTA of the backward-solve dots
+constexpr int kBwdRows = 128;   // rows (K chunk) per CTA of the backward-solve dots
+// Persistent dependency-driven (DAG) schedule: a task runs after every (counter, target)
+// wait in waits[w0, w1) is met, then bumps counter `sig` (-1: none).  Tasks are listed in a
+// topological order and grabbed in that order by resident CTAs, so waits always target
+// earlier tasks and the schedule cannot deadlock.
+enum TaskKind : int32_t { T_FWD = 1, T_BWD = 2 };
+struct Task { int32_t kind, f, a, b, c, sig, w0, w1; };
 struct Launch { int32_t kind; int32_t level; int64_t off; int64_t count; int32_t pivtype = 1; int32_t pad = 0; };
 
 struct Symbolic {
@@ -84,6 +90,14 @@ struct Symbolic {
   std::vector<int32_t> grp_nchunk;
   std::vector<int64_t> grp_base;
   int64_t n_groups = 0, part_doubles = 0;
+  // persistent solve schedule: tasks, flat (counter, target) wait pairs, counter count
+  std::vector<Task> stasks;
+  std::vector<int32_t> swaits;
+  int32_t n_scnt = 0;
+  // inverse extend-add map for the solve: front row (voff + r) -> children update slots
+  // (ubuf offsets) in child order: v[r] = b[r] + sum u[gsrc[gptr[voff+r] .. gptr[voff+r+1])]
+  std::vector<int64_t> gptr;
+  std::vector<int32_t> gsrc;
   // sizes
   int64_t front_doubles = 0, u_doubles = 0, w_doubles = 0, v_doubles = 0, z_doubles = 0, d_doubles = 0;
   int64_t nnz_l = 0; double flops = 0; int64_t max_front = 0, max_piv = 0;

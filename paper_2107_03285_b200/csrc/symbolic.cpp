@@ -808,6 +808,67 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     s.bwd_cnt[lv] = (int64_t)s.work.size() - s.bwd_off[lv];
   }
   s.n_groups = (int64_t)s.grp_nchunk.size();
+
+  // ---- persistent solve DAG ------------------------------------------------------------
+  // counters: CF(f) = f (forward row groups done), CB(f) = NF + f (backward groups done).
+  // The extend-add gather of the forward solve is folded into the GEMV tasks through the
+  // inverse map gptr/gsrc, so a front's forward tasks wait directly on its children.
+  {
+    std::vector<int32_t> nfg(NF, 0), nbg(NF, 0);
+    for (int32_t lv = 0; lv < s.n_levels; ++lv) {
+      for (int64_t w = s.fwd_off[lv]; w < s.fwd_off[lv] + s.fwd_cnt[lv]; ++w)
+        if (s.work[w].b == 0) nfg[s.work[w].f]++;
+      for (int64_t w = s.bwd_off[lv]; w < s.bwd_off[lv] + s.bwd_cnt[lv]; ++w)
+        if (s.work[w].b == (s.work[w].a / kBwdRows) * kBwdRows) nbg[s.work[w].f]++;
+    }
+    // inverse gather map
+    {
+      std::vector<int64_t> cnt(s.v_doubles + 1, 0);
+      for (int32_t f = 0; f < NF; ++f) {
+        const Front& F = s.fronts[f];
+        for (int32_t ci = F.child_begin; ci < F.child_end; ++ci) {
+          const Front& C = s.fronts[s.children[ci]];
+          for (int64_t t = 0; t < C.nrow - C.npiv; ++t) cnt[F.voff + s.rel[C.rel_off + t] + 1]++;
+        }
+      }
+      for (int64_t q = 0; q < s.v_doubles; ++q) cnt[q + 1] += cnt[q];
+      s.gptr = cnt;
+      s.gsrc.assign(cnt[s.v_doubles], 0);
+      std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+      for (int32_t f = 0; f < NF; ++f) {
+        const Front& F = s.fronts[f];
+        for (int32_t ci = F.child_begin; ci < F.child_end; ++ci) {   // child order = sum order
+          const Front& C = s.fronts[s.children[ci]];
+          for (int64_t t = 0; t < C.nrow - C.npiv; ++t)
+            s.gsrc[fill[F.voff + s.rel[C.rel_off + t]]++] = (int32_t)(C.uoff + t);
+        }
+      }
+    }
+    s.stasks.clear(); s.swaits.clear();
+    s.n_scnt = 2 * NF;
+    auto add = [&](int32_t kind, const Work& w, int32_t sig, const std::vector<std::pair<int32_t, int32_t>>& ws) {
+      Task t{kind, w.f, w.a, w.b, w.c, sig, (int32_t)(s.swaits.size() / 2), 0};
+      for (auto& p : ws) { s.swaits.push_back(p.first); s.swaits.push_back(p.second); }
+      t.w1 = (int32_t)(s.swaits.size() / 2);
+      s.stasks.push_back(t);
+    };
+    for (int32_t lv = 0; lv < s.n_levels; ++lv) {
+      for (int64_t w = s.fwd_off[lv]; w < s.fwd_off[lv] + s.fwd_cnt[lv]; ++w) {
+        const Front& F = s.fronts[s.work[w].f];
+        std::vector<std::pair<int32_t, int32_t>> ch;
+        for (int32_t ci = F.child_begin; ci < F.child_end; ++ci) ch.push_back({s.children[ci], nfg[s.children[ci]]});
+        add(T_FWD, s.work[w], s.work[w].f, ch);
+      }
+    }
+    for (int32_t lv = s.n_levels - 1; lv >= 0; --lv) {
+      for (int64_t w = s.bwd_off[lv]; w < s.bwd_off[lv] + s.bwd_cnt[lv]; ++w) {
+        const int32_t f = s.work[w].f;
+        const int32_t p = s.fronts[f].parent;
+        if (p >= 0) add(T_BWD, s.work[w], NF + f, {{NF + p, nbg[p]}});
+        else add(T_BWD, s.work[w], NF + f, {{f, nfg[f]}});
+      }
+    }
+  }
   return 0;
 }
 
