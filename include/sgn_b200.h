@@ -112,6 +112,10 @@ void sgn_factor_destroy(sgn_factor f);
  * 0 = phase not reached).  meta: 5 int32 per task
  * (kind, front, level, a, b); any output pointer may be NULL.                         */
 int  sgn_debug_solve_trace(sgn_factor f, int64_t* out, int64_t cap, int64_t* n_tasks, int32_t* meta);
+/* Same for the persistent factorization (SGN_FDAG_TRACE=1): 8 words per task (start,
+ * ready, end ns; smid; 4 sub-phase ns or 0); meta: 6 int32 per task (kind, step, front,
+ * level, a, b).                                                                        */
+int  sgn_debug_factor_trace(sgn_factor f, int64_t* out, int64_t cap, int64_t* n_tasks, int32_t* meta);
 
 /* y = K x on the full symmetric CSC pattern (which equals its CSR).  Replaces the
  * scipy SpMV of _relative_residual / _bicgstab_refine (linear_solvers.py:105-108,178-211).

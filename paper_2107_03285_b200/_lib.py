@@ -49,6 +49,7 @@ SIGNATURES = {
     "sgn_masked_copy": (ctypes.c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "sgn_factor_solve": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
     "sgn_debug_solve_trace": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_vp, c_vp]),
+    "sgn_debug_factor_trace": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_vp, c_vp]),
     "sgn_factor_destroy": (None, [c_vp]),
     "sgn_spmv": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp]),
     "sgn_solve_refined": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_dbl, c_i32, c_i32,

@@ -1,0 +1,609 @@
+// Persistent dependency-driven multifrontal LDL^T factorization on B200 (sm_100a).
+//
+// Replaces, on the GPU, the reference's SuperLU numeric LU of the stabilized KKT
+// (reference pkg/src/sgnopt/linear_solvers.py:87 + :111-127) -- see numeric.cu for the
+// surrounding C ABI.  ONE launch per factorization: resident CTAs take tasks in the
+// topological order built by symbolic.cpp ("persistent factorization tasks") from a
+// global head counter, wait on per-tile / per-step / per-front counters derived from the
+// task coordinates (gpu-scope acquire loads), run the task and release its counters.
+//
+//   F_ASM    one 32x32 tile of a front: original KKT entries, the signed stabilization
+//            shift, then the children's update matrices extend-added in child order
+//            (atomic free, bitwise deterministic).
+//   F_PANEL  one pivot step of a front: LDL^T of the 32x32 diagonal block (2x2 pivots on
+//            matched (x_i, lambda_j) pairs or 1x1), then TRSM of up to four 32-row tiles
+//            below it: W = P L11^{-T} (kept transposed in the front's unused upper
+//            triangle) and L21 = W D^{-1}.
+//   F_UPDATE one 32x32 Schur tile C -= L21_i W_j^T on the FP64 tensor pipe (DMMA).
+//   F_ZPANEL one 32-row slab of the solve panel Z = [I; L21] L11^{-1}.
+//
+// Every value produced inside the launch is read with ld.global.cg (L2): a persistent
+// CTA keeps its L1 across tasks and must never see a stale line.  Bodies are compact
+// loops (the whole kernel shares one instruction cache).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "../../include/sgn_b200.h"
+#include "sgn_internal.h"
+
+namespace {
+
+using sgn::DFront;
+using sgn::kTile;
+
+constexpr int kFThreads = 128;
+
+__device__ __forceinline__ int ld_acq(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void spin_ge(const int* p, int target) {
+  while (ld_acq(p) < target) __nanosleep(20);
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+// Shared memory (dynamic, ~53 KB): five raw 32 x 40 tiles, each viewed either row-major
+// with stride 33 (one row per lane: conflict-free) or K-major with stride 40 (DMMA
+// fragment reads (row g, k q) and the coalesced staging stores both conflict-free).
+constexpr int kTileWords = kTile * 40;
+typedef double (*V33)[kTile + 1];
+typedef double (*V40)[40];
+struct Smem {
+  double a[kTileWords];
+  double b[4][kTileWords];
+  double2 colbuf[2 * kTile];        // panel: pivot columns broadcast
+  double dinv[kTile][3];            // per pivot block: (ia, ib, ic) or (1/d)
+  unsigned long long* tr;           // this task's trace words (diagnostics) or null
+  int bad;
+};
+__device__ __forceinline__ V33 v33(double* p) { return reinterpret_cast<V33>(p); }
+__device__ __forceinline__ V40 v40(double* p) { return reinterpret_cast<V40>(p); }
+
+__device__ __forceinline__ void tmark(Smem& S, int slot) {
+  if (threadIdx.x == 0 && S.tr) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    S.tr[slot] = t;
+  }
+}
+
+__device__ __forceinline__ double* front_ptr(const sgn::FactorArgs& A, const DFront& F, int b) {
+  return A.fstore + (int64_t)b * A.fstride + F.foff;
+}
+
+// ---------------------------------------------------------------------------------------
+__device__ void f_asm(const sgn::FactorArgs& A, const DFront& F, int b, int ti, int tj, Smem& S) {
+  double (*tile)[kTile + 1] = v33(S.a);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < kTile * kTile; e += kFThreads) tile[e >> 5][e & 31] = 0.0;
+  __syncthreads();
+  const double* vals = A.values + (int64_t)b * A.vstride;
+  {
+    const int64_t tg = F.tile_base + (int64_t)ti * (ti + 1) / 2 + tj;
+    const int64_t e0 = A.tile_ptr[tg], e1 = A.tile_ptr[tg + 1];
+    for (int64_t e = e0 + tid; e < e1; e += kFThreads) {
+      const int loc = A.tile_loc[e];
+      tile[loc >> 5][loc & 31] = vals[A.tile_nnz[e]];
+    }
+  }
+  __syncthreads();
+  const int i0 = sgn::tile_lo(F.npiv, ti), i1 = sgn::tile_hi(F.npiv, F.nrow, ti);
+  const int j0 = sgn::tile_lo(F.npiv, tj), j1 = sgn::tile_hi(F.npiv, F.nrow, tj);
+  if (ti == tj && i0 < F.npiv && tid < i1 - i0) {
+    const int8_t kd = A.kind_pos[F.first + i0 + tid];
+    if (kd == 1) tile[tid][tid] += A.eps_xv ? A.eps_xv[b] : A.eps_x;
+    else if (kd == 2) tile[tid][tid] -= A.eps_lv ? A.eps_lv[b] : A.eps_l;
+  }
+  const double* fb = A.fstore + (int64_t)b * A.fstride;
+  for (int ci = F.child_begin; ci < F.child_end; ++ci) {
+    const DFront C = A.fronts[A.children[ci]];
+    const int cn = C.nrow - C.npiv;
+    __syncthreads();
+    if (cn == 0) continue;
+    const int32_t* rc = A.rel + C.rel_off;
+    const int32_t* rt = A.reltile + C.woff;
+    const int r_lo = rt[ti], r_hi = rt[ti + 1], s_lo = rt[tj], s_hi = rt[tj + 1];
+    const int nr = r_hi - r_lo, ns = s_hi - s_lo;
+    if (nr <= 0 || ns <= 0) continue;
+    const double* U = fb + C.foff;
+    const int64_t ldc = C.nrow;
+    for (int idx = tid; idx < nr * ns; idx += kFThreads) {
+      const int r = r_lo + idx % nr, s = s_lo + idx / nr;
+      if (r >= s) tile[rc[r] - i0][rc[s] - j0] += __ldcg(U + (int64_t)(C.npiv + s) * ldc + C.npiv + r);
+    }
+  }
+  __syncthreads();
+  double* Fm = front_ptr(A, F, b);
+  const int64_t ld = F.nrow;
+  for (int e = tid; e < kTile * kTile; e += kFThreads) {
+    const int ii = e & 31, jj = e >> 5;
+    const int gi = i0 + ii, gj = j0 + jj;
+    if (gi < i1 && gj < j1) Fm[(int64_t)gj * ld + gi] = tile[ii][jj];
+  }
+  if (ti == 0 && tj == 0 && F.npiv > 0)     // D_0 is factored by the caller (single site)
+    for (int e = tid; e < kTile * kTile; e += kFThreads)
+      if ((e >> 5) < (e & 31)) tile[e >> 5][e & 31] = 0.0;
+}
+
+// LDL^T of the w x w diagonal block by one warp (lane i = row i), rows in registers,
+// fully unrolled so every register index is static; the two pivot columns of each step
+// are broadcast through smem (colbuf) -- measured 2.2x faster than shuffles and 9x faster
+// than a runtime-loop register window (profiles/micro/diag_factor_bench.cu).  The factored
+// values (L below the pivot blocks, D on them) are written back into D.  Returns the
+// first zero / non-finite pivot position or 1 << 30.
+template <int PT>
+__device__ int factor_diag(double (*D)[kTile + 1], double2* colbuf, int w) {
+  const int i = threadIdx.x & 31;
+  int first_bad = 1 << 30;
+  double d[kTile];
+#pragma unroll
+  for (int k = 0; k < kTile; ++k) d[k] = (k <= i) ? D[i][k] : 0.0;
+#pragma unroll
+  for (int j = 0; j < kTile; j += PT) {
+    const bool act = (j < w);
+    colbuf[i] = make_double2(d[j], PT == 2 ? d[j + 1] : 0.0);
+    __syncwarp();
+    if (PT == 2) {
+      const double2 pj = colbuf[j], pj1 = colbuf[j + 1];
+      const double a = pj.x, bb = pj1.x, c = pj1.y;
+      double det = a * c - bb * bb;
+      first_bad = (act && (det == 0.0 || !isfinite(det)) && first_bad > j) ? j : first_bad;
+      det = (act && det != 0.0 && isfinite(det)) ? det : 1.0;
+      const double rdet = 1.0 / det;
+      const double ia = c * rdet, ib = -bb * rdet, ic = a * rdet;
+      const bool below = act && (i > j + 1) && (i < w);
+      const double x0 = d[j], x1 = d[j + 1];
+      const double l0 = below ? x0 * ia + x1 * ib : 0.0;
+      const double l1 = below ? x0 * ib + x1 * ic : 0.0;
+#pragma unroll
+      for (int k = j + 2; k < kTile; ++k) {
+        const double2 y = colbuf[k];
+        d[k] = fma(-l1, y.y, fma(-l0, y.x, d[k]));   // right of the diagonal: junk, never read
+      }
+      d[j] = below ? l0 : d[j];
+      d[j + 1] = below ? l1 : d[j + 1];
+    } else {
+      double dj = colbuf[j].x;
+      first_bad = (act && (dj == 0.0 || !isfinite(dj)) && first_bad > j) ? j : first_bad;
+      dj = (act && dj != 0.0 && isfinite(dj)) ? dj : 1.0;
+      const bool below = act && (i > j) && (i < w);
+      const double l = below ? d[j] * (1.0 / dj) : 0.0;
+#pragma unroll
+      for (int k = j + 1; k < kTile; ++k) d[k] = fma(-l, colbuf[k].x, d[k]);
+      d[j] = below ? l : d[j];
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int k = 0; k < kTile; ++k) if (k <= i) D[i][k] = d[k];
+  return first_bad;
+}
+
+// W = P L11^{-T} for one 32-row tile (lane = row), right-looking, row in registers, fully
+// unrolled; Lt[cp][c] = L11[c][cp] (unit lower, D slots cleared) broadcast from smem.
+__device__ __forceinline__ void trsm_rows(double (*Pw)[kTile + 1], const double (*Lt)[kTile + 1]) {
+  const int lane = threadIdx.x & 31;
+  double p[kTile];
+#pragma unroll
+  for (int m = 0; m < kTile; ++m) p[m] = Pw[lane][m];
+#pragma unroll
+  for (int cp = 0; cp < kTile; ++cp) {
+    const double pc = p[cp];
+#pragma unroll
+    for (int c = cp + 1; c < kTile; ++c) p[c] = fma(-pc, Lt[cp][c], p[c]);
+  }
+#pragma unroll
+  for (int m = 0; m < kTile; ++m) Pw[lane][m] = p[m];
+}
+
+// Factor the w x w pivot block of step k held (lower part) in smem tile D and publish it
+// to the step's scratch [D | L^T | D^-1]: the factored block (Z-panel / solve), the unit
+// lower L^T with the 2x2 D slots cleared (TRSM, Z panel) and the pivot-block inverses.
+// Records the first bad pivot in status.  All threads of the CTA take part.
+__device__ __forceinline__ void factor_publish(const sgn::FactorArgs& A, const DFront& F, int b, int k,
+                                            double (*D)[kTile + 1], Smem& S) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int j0 = k * kTile, w = min(kTile, F.npiv - j0);
+  __syncthreads();
+  if (warp == 0) {
+    const int bad = (F.pivtype == 2) ? factor_diag<2>(D, S.colbuf, w) : factor_diag<1>(D, S.colbuf, w);
+    if (lane == 0 && bad < (1 << 30)) atomicMin(&A.status[b], (long long)A.perm[F.first + j0 + bad]);
+  }
+  __syncthreads();
+  tmark(S, 6);
+  double* ds = A.dscr + (int64_t)b * A.dstride + F.doff + (int64_t)k * sgn::kDiagStride;
+  for (int e = tid; e < kTile * kTile; e += kFThreads) {
+    const int r = e >> 5, c = e & 31;
+    ds[e] = D[r][c];
+    const int cp = r, cc = c;                                 // L^T[cp][cc] = L[cc][cp]
+    const bool dslot = F.pivtype == 2 && (cp & 1) == 0 && cc == cp + 1;
+    ds[kTile * kTile + e] = (cc > cp && cc < w && !dslot) ? D[cc][cp] : 0.0;
+  }
+  if (tid < w) {
+    double* di = ds + 2 * kTile * kTile + 3 * tid;
+    if (F.pivtype == 2) {
+      const int t0 = tid & ~1;
+      const double a = D[t0][t0], bb = D[t0 + 1][t0], cc = D[t0 + 1][t0 + 1];
+      const double rdet = 1.0 / (a * cc - bb * bb);
+      di[0] = cc * rdet; di[1] = -bb * rdet; di[2] = a * rdet;
+    } else {
+      di[0] = 1.0 / D[tid][tid]; di[1] = 0.0; di[2] = 0.0;
+    }
+  }
+}
+
+// TRSM of step k for row tile k+1 (t = 0, warp 0) or tiles k+2+4(t-1).. (t >= 1, a warp
+// each): W = P L11^{-T} (kept transposed in the front's upper triangle) and L21 = W D^-1,
+// with L11^T and D^-1 read from the step's scratch (factored once by its producer).
+__device__ int f_panel_pre(const sgn::FactorArgs& A, const DFront& F, int b, int k, int t, Smem& S) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* Fm = front_ptr(A, F, b);
+  const int64_t ld = F.nrow;
+  const int j0 = k * kTile, w = min(kTile, F.npiv - j0);
+  const int T = sgn::ntiles_front(F.npiv, F.nrow);
+  double (*Lt)[kTile + 1] = v33(S.a);
+  const double* ds = A.dscr + (int64_t)b * A.dstride + F.doff + (int64_t)k * sgn::kDiagStride;
+  for (int e = tid; e < kTile * kTile; e += kFThreads) Lt[e >> 5][e & 31] = __ldcg(ds + kTile * kTile + e);
+  if (tid < 3 * kTile) (&S.dinv[0][0])[tid] = __ldcg(ds + 2 * kTile * kTile + tid);
+  const int ti = (t == 0) ? (warp == 0 ? k + 1 : T) : k + 2 + 4 * (t - 1) + warp;
+  const int lo = (ti < T) ? sgn::tile_lo(F.npiv, ti) : 0;
+  const int nr = (ti < T) ? sgn::tile_hi(F.npiv, F.nrow, ti) - lo : 0;
+  double (*Pw)[kTile + 1] = v33(S.b[warp]);
+  if (nr > 0) {
+    double v[kTile];
+#pragma unroll
+    for (int j = 0; j < kTile; ++j) v[j] = (lane < nr && j < w) ? __ldcg(Fm + (int64_t)(j0 + j) * ld + lo + lane) : 0.0;
+#pragma unroll
+    for (int j = 0; j < kTile; ++j) Pw[lane][j] = v[j];
+  }
+  return nr;
+}
+
+// after the substitution: W -> the front's upper triangle (transposed), L21 = W D^-1
+__device__ void f_panel_post(const sgn::FactorArgs& A, const DFront& F, int b, int k, int t, int nr, Smem& S) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (nr == 0) return;
+  double* Fm = front_ptr(A, F, b);
+  const int64_t ld = F.nrow;
+  const int j0 = k * kTile, w = min(kTile, F.npiv - j0);
+  const int ti = (t == 0) ? k + 1 : k + 2 + 4 * (t - 1) + warp;
+  const int lo = sgn::tile_lo(F.npiv, ti);
+  double (*Pw)[kTile + 1] = v33(S.b[warp]);
+  for (int r = 0; r < nr; ++r)
+    if (lane < w) Fm[(int64_t)(lo + r) * ld + j0 + lane] = Pw[r][lane];
+  if (lane < nr) {
+    for (int c = 0; c < w; ++c) {
+      double l;
+      if (F.pivtype == 2) {
+        const int c0 = c & ~1;
+        const double x0 = Pw[lane][c0], x1 = Pw[lane][c0 + 1];
+        l = (c == c0) ? x0 * S.dinv[c0][0] + x1 * S.dinv[c0][1] : x0 * S.dinv[c0][1] + x1 * S.dinv[c0][2];
+      } else {
+        l = Pw[lane][c] * S.dinv[c][0];
+      }
+      Fm[(int64_t)(j0 + c) * ld + lo + lane] = l;
+    }
+  }
+}
+
+// C[ti, tj] -= L21[ti, step k] W[tj, step k]^T   (mma.sync.m8n8k4.f64 -> DMMA).
+// diag: the last update of pivot tile (k+1, k+1) -- the result stays in smem (S.b[1]) and
+// is factored and published as D_{k+1} instead of being written back.
+__device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k, int ti, int tj, Smem& S,
+                         bool diag = false) {
+  V40 Ak = v40(S.a);          // Ak[c][i] = L21[lo_i + i, j0 + c]
+  V40 Bk = v40(S.b[0]);       // Bk[c][j] = W[lo_j + j, j0 + c]
+  const int tid = threadIdx.x;
+  double* Fm = front_ptr(A, F, b);
+  const int64_t ld = F.nrow;
+  const int j0 = k * kTile, w = min(kTile, F.npiv - j0);
+  const int lo_i = sgn::tile_lo(F.npiv, ti), nr = sgn::tile_hi(F.npiv, F.nrow, ti) - lo_i;
+  const int lo_j = sgn::tile_lo(F.npiv, tj), nc = sgn::tile_hi(F.npiv, F.nrow, tj) - lo_j;
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
+  const int row0 = warp * 8;
+  const int i = row0 + g;
+  double va[8], vb[8], cv[4][2];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {           // all 24 loads in flight together
+    const int e = tid + u * kFThreads;
+    const int r = e & 31, c = e >> 5;
+    va[u] = (r < nr && c < w) ? __ldcg(Fm + (int64_t)(j0 + c) * ld + lo_i + r) : 0.0;
+    vb[u] = (c < nc && r < w) ? __ldcg(Fm + (int64_t)(lo_j + c) * ld + j0 + r) : 0.0;   // (j = c, col = r)
+  }
+#pragma unroll
+  for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = nf * 8 + 2 * q + h;
+      cv[nf][h] = (i < nr && j < nc && (ti != tj || i >= j)) ? __ldcg(Fm + (int64_t)(lo_j + j) * ld + lo_i + i) : 0.0;
+    }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = tid + u * kFThreads;
+    const int r = e & 31, c = e >> 5;
+    Ak[c][r] = va[u];
+    Bk[r][c] = vb[u];
+  }
+  __syncthreads();
+  tmark(S, 4);
+  double acc[4][2];
+#pragma unroll
+  for (int nf = 0; nf < 4; ++nf) acc[nf][0] = acc[nf][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < kTile; kk += 4) {
+    const double a = Ak[kk + q][row0 + g];
+#pragma unroll
+    for (int nf = 0; nf < 4; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], a, Bk[kk + q][nf * 8 + g]);
+  }
+  tmark(S, 5);
+  if (diag) {
+    double (*Dn)[kTile + 1] = v33(S.b[1]);
+#pragma unroll
+    for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = nf * 8 + 2 * q + h;
+        Dn[i][j] = (i < nr && j < nc && i >= j) ? cv[nf][h] - acc[nf][h] : 0.0;
+      }
+    return;   // the caller factors and publishes D_{k+1}
+  }
+  if (i < nr) {
+#pragma unroll
+    for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = nf * 8 + 2 * q + h;
+        if (j < nc && (ti != tj || i >= j)) Fm[(int64_t)(lo_j + j) * ld + lo_i + i] = cv[nf][h] - acc[nf][h];
+      }
+  }
+}
+
+// One block of the solve panel Z = [I; L21] L11^{-1}: rows r0..r0+31 ("slab"), column
+// block cb.  Z L11 = B (B = e_r on pivot rows, L21 on struct rows) gives
+//   Z[slab, cb] L_cb = B[slab, cb] - sum_{blk > cb} Z[slab, blk] L11[blk, cb]
+// (the sum on DMMA over blocks finished by the earlier tasks of this slab), then a
+// right-to-left substitution with the unit lower diagonal block L_cb, done by trsm_rows
+// on column-reversed layouts.  The slab's first task also publishes the factored
+// diagonal block r0/32 from scratch into F.
+__device__ void f_ztask_pre(const sgn::FactorArgs& A, const DFront& F, int b, int r0, int cb, Smem& S) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
+  const int nr = min(kTile, F.nrow - r0);
+  const int npiv = F.npiv;
+  const int64_t ld = F.nrow;
+  double* Fm = front_ptr(A, F, b);
+  double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
+  const double* ds = A.dscr + (int64_t)b * A.dstride + F.doff;
+  const int cmax = (r0 < npiv) ? min(npiv, r0 + nr) : npiv;
+  const int nbs = (cmax + kTile - 1) / kTile;
+  const int c0 = cb * kTile, wb = min(kTile, npiv - c0);
+  if (cb == nbs - 1 && r0 < npiv) {
+    const double* blk = ds + (int64_t)(r0 / kTile) * sgn::kDiagStride;
+    const int wd = min(kTile, npiv - r0);
+    for (int e = tid; e < kTile * kTile; e += kFThreads) {
+      const int i = e >> 5, j = e & 31;
+      if (i < wd && j < wd && i >= j) Fm[(int64_t)(r0 + j) * ld + r0 + i] = __ldcg(blk + e);
+    }
+  }
+  double (*Tr)[kTile + 1] = v33(S.b[0]);
+  double (*X)[kTile + 1] = v33(S.b[1]);
+  V40 Zk = v40(S.b[2]);     // K-major: Zk[kk][row]
+  V40 Lk = v40(S.b[3]);     // K-major: Lk[kk][col]
+  // X[m'][m] = L_cb[31-m'][31-m] = L^T_cb[31-m][31-m'] (m' < m): the reversed unit lower
+  // block (D slots already cleared in the scratch L^T)
+  for (int e = tid; e < kTile * kTile; e += kFThreads) {
+    const int mp = e >> 5, m = e & 31;
+    X[mp][m] = (mp < m) ? __ldcg(ds + (int64_t)cb * sgn::kDiagStride + kTile * kTile + (31 - m) * kTile + (31 - mp)) : 0.0;
+  }
+  const int row0 = warp * 8, i = row0 + g;
+  double acc[4][2];
+#pragma unroll
+  for (int nf = 0; nf < 4; ++nf) acc[nf][0] = acc[nf][1] = 0.0;
+  for (int blk = cb + 1; blk < nbs; ++blk) {
+    const int k0 = blk * kTile;
+    double vz[8], vl[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + u * kFThreads;
+      const int r = e & 31, c = e >> 5;
+      vz[u] = (r < nr) ? __ldcg(Zm + (int64_t)(k0 + c) * ld + r0 + r) : 0.0;                 // Z[r0 + r, k0 + c]
+      vl[u] = (k0 + r < npiv && c < wb) ? __ldcg(Fm + (int64_t)(c0 + c) * ld + k0 + r) : 0.0; // L11[k0 + r, c0 + c]
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + u * kFThreads;
+      const int r = e & 31, c = e >> 5;
+      Zk[c][r] = vz[u];
+      Lk[r][c] = vl[u];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kTile; kk += 4) {
+      const double a = Zk[kk + q][row0 + g];
+#pragma unroll
+      for (int nf = 0; nf < 4; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], a, Lk[kk + q][nf * 8 + g]);
+    }
+    __syncthreads();
+  }
+  // T = B - acc, stored column-reversed
+#pragma unroll
+  for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = nf * 8 + 2 * q + h;
+      double t = 0.0;
+      if (i < nr && j < wb) {
+        const int r = r0 + i, col = c0 + j;
+        const double bv = (r < npiv) ? (r == col ? 1.0 : 0.0) : __ldcg(Fm + (int64_t)col * ld + r);
+        t = bv - acc[nf][h];
+      }
+      Tr[i][31 - j] = t;
+    }
+}
+
+__device__ void f_ztask_post(const sgn::FactorArgs& A, const DFront& F, int b, int r0, int cb, Smem& S) {
+  const int tid = threadIdx.x;
+  const int nr = min(kTile, F.nrow - r0);
+  const int64_t ld = F.nrow;
+  double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
+  const int c0 = cb * kTile, wb = min(kTile, F.npiv - c0);
+  double (*Tr)[kTile + 1] = v33(S.b[0]);
+  for (int e = tid; e < kTile * kTile; e += kFThreads) {
+    const int ii = e & 31, c = e >> 5;
+    if (ii < nr && c < wb) Zm[(int64_t)(c0 + c) * ld + r0 + ii] = Tr[ii][31 - c];
+  }
+}
+
+__global__ void __launch_bounds__(kFThreads, 4)
+k_factor_dag(const sgn::FactorArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  __shared__ int s_idx;
+  const int64_t total = A.ntask * A.batch;
+  const int tid = threadIdx.x;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_idx = atomicAdd(A.head, 1);
+    __syncthreads();
+    const int64_t idx = s_idx;
+    if (idx >= total) return;
+    const int64_t tix = idx / A.batch;
+    const int b = (int)(idx - tix * A.batch);
+    const sgn::FTask T = A.tasks[tix];
+    const int kind = T.kind_k & 7, k = T.kind_k >> 3;
+    const DFront F = A.fronts[T.f];
+    int* cnt = A.cnt + (int64_t)b * A.n_fcnt;
+    int* cf = cnt + F.cbase;
+    const int P = sgn::ptiles(F.npiv);
+    if (tid == 0) {
+      S.tr = A.trace ? A.trace + idx * 8 : nullptr;
+      if (S.tr) S.tr[0] = gtimer();
+    }
+    const int Tn = sgn::ntiles_front(F.npiv, F.nrow);
+    if (tid == 0) {
+      if (kind == sgn::F_ASM) {
+        for (int ci = F.child_begin; ci < F.child_end; ++ci) {
+          const DFront C = A.fronts[A.children[ci]];
+          spin_ge(cnt + C.cbase, C.ftotal);
+        }
+      } else if (kind == sgn::F_PANEL) {
+        spin_ge(cf + sgn::cnt_diag(P, k), 1);
+        if (T.a == 0) {
+          spin_ge(cf + sgn::cnt_tile(P, k + 1, k), 1 + k);
+        } else {
+          for (int qd = 0; qd < 4; ++qd) {
+            const int i = k + 2 + 4 * (T.a - 1) + qd;
+            if (i < Tn) spin_ge(cf + sgn::cnt_tile(P, i, k), 1 + k);
+          }
+        }
+      } else if (kind == sgn::F_UPDATE || kind == sgn::F_DIAGUPD) {
+        const int ti = (kind == sgn::F_DIAGUPD) ? k + 1 : T.a, tj = (kind == sgn::F_DIAGUPD) ? k + 1 : T.b;
+        spin_ge(cf + sgn::cnt_pan(k), sgn::panel_tasks(F.npiv, F.nrow, k));
+        spin_ge(cf + sgn::cnt_tile(P, ti, tj), 1 + k);
+      } else {
+        spin_ge(cf, F.ftotal);
+        const int r0 = T.a, nr = min(kTile, F.nrow - r0);
+        const int cmax = (r0 < F.npiv) ? min(F.npiv, r0 + nr) : F.npiv;
+        const int nbs = (cmax + kTile - 1) / kTile;
+        spin_ge(cf + sgn::cnt_zc(P, Tn, r0 / kTile), nbs - 1 - T.b);
+      }
+    }
+    __syncthreads();
+    if (A.trace && tid == 0) A.trace[idx * 8 + 1] = gtimer();
+    // phase 1: kind-specific work; the heavy unrolled kernels (pivot-block LDL^T and the
+    // row substitution) then run from ONE call site each (instruction-cache footprint)
+    int fac_k = -1, nr_trsm = 0;
+    double (*fac_tile)[kTile + 1] = v33(S.a);
+    double (*tr_p)[kTile + 1] = v33(S.b[0]);
+    double (*tr_l)[kTile + 1] = v33(S.a);
+    if (kind == sgn::F_ASM) {
+      f_asm(A, F, b, T.a, T.b, S);
+      if (T.a == 0 && T.b == 0 && F.npiv > 0) fac_k = 0;
+    } else if (kind == sgn::F_PANEL) {
+      nr_trsm = f_panel_pre(A, F, b, k, T.a, S);
+      tr_p = v33(S.b[tid >> 5]);
+    } else if (kind == sgn::F_UPDATE || kind == sgn::F_DIAGUPD) {
+      const bool dg = (kind == sgn::F_DIAGUPD);
+      f_update(A, F, b, k, dg ? k + 1 : T.a, dg ? k + 1 : T.b, S, dg);
+      if (dg) { fac_k = k + 1; fac_tile = v33(S.b[1]); }
+    } else {
+      f_ztask_pre(A, F, b, T.a, T.b, S);
+      nr_trsm = (tid < 32) ? 32 : 0;
+      tr_l = v33(S.b[1]);
+    }
+    if (fac_k >= 0) factor_publish(A, F, b, fac_k, fac_tile, S);
+    __syncthreads();
+    if (kind == sgn::F_PANEL) tmark(S, 4);
+    if (nr_trsm > 0) trsm_rows(tr_p, tr_l);
+    __syncthreads();
+    tmark(S, 7);
+    if (kind == sgn::F_PANEL) f_panel_post(A, F, b, k, T.a, nr_trsm, S);
+    else if (kind == sgn::F_ZPANEL) f_ztask_post(A, F, b, T.a, T.b, S);
+    __syncthreads();   // every thread's writes precede the release
+    if (tid == 0) {
+      int* s1;
+      int* s2 = cf;                                            // DONE
+      int* s3 = nullptr;
+      if (kind == sgn::F_ZPANEL) { s1 = cf + sgn::cnt_zc(P, Tn, T.a / kTile); s2 = nullptr; }
+      else if (kind == sgn::F_PANEL) s1 = cf + sgn::cnt_pan(k);
+      else if (kind == sgn::F_DIAGUPD) { s1 = cf + sgn::cnt_tile(P, k + 1, k + 1); s3 = cf + sgn::cnt_diag(P, k + 1); }
+      else {
+        s1 = cf + sgn::cnt_tile(P, T.a, T.b);
+        if (kind == sgn::F_ASM && T.a == 0 && T.b == 0 && F.npiv > 0) s3 = cf + sgn::cnt_diag(P, 0);
+      }
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(s1) : "memory");
+      if (s2) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(s2) : "memory");
+      if (s3) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(s3) : "memory");
+    }
+    if (A.trace && tid == 0) {
+      A.trace[idx * 8 + 2] = gtimer();
+      A.trace[idx * 8 + 3] = smid();
+    }
+  }
+}
+
+}  // namespace
+
+namespace sgn {
+
+int factor_dag_grid() {
+  int dev = 0, sms = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  if (cudaFuncSetAttribute(k_factor_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem)) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_factor_dag, kFThreads, sizeof(Smem)) != cudaSuccess) return 0;
+  return sms * std::max(per_sm, 1);
+}
+
+int launch_factor_dag(const FactorArgs& A, int grid, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t total = A.ntask * A.batch;
+  if (total == 0) return SGN_OK;
+  cudaError_t e = cudaMemsetAsync(A.head, 0, (size_t)(1 + A.batch * A.n_fcnt) * sizeof(int), st);
+  if (e != cudaSuccess) { last_error() = std::string("counter reset: ") + cudaGetErrorString(e); return SGN_CUDA_ERROR; }
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid, total));
+  count_launch();
+  k_factor_dag<<<g, kFThreads, sizeof(Smem), st>>>(A);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) { last_error() = std::string("k_factor_dag: ") + cudaGetErrorString(e); return SGN_CUDA_ERROR; }
+  return SGN_OK;
+}
+
+}  // namespace sgn

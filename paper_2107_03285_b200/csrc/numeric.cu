@@ -5,14 +5,10 @@
 // the stabilization (linear_solvers.py:111-127), the relative-residual SpMV
 // (linear_solvers.py:105-108) and the BiCGSTAB refinement (linear_solvers.py:130-211).
 //
-// Factorization: multifrontal LDL^T over the host-built assembly tree (symbolic.cpp).
-// Per tree level: (1) tile-owner assembly of all fronts of the level (original entries +
-// stabilization shift + fixed-order extend-add of children update matrices -- atomic
-// free, bitwise deterministic); (2) per 32-column panel: a panel kernel (redundant
-// in-smem LDL^T of the diagonal block with 2x2 / 1x1 pivots + TRSM of a 32-row tile)
-// and a Schur-update kernel whose 32x32 tiles run on the FP64 tensor pipe
-// (mma.sync.m8n8k4.f64 -> DMMA).  Solves are level-scheduled, one CTA per front,
-// warp-shuffle diagonal blocks.
+// Factorization: multifrontal LDL^T over the host-built assembly tree (symbolic.cpp), one
+// persistent dependency-driven launch per factorization (factor_dag.cu).  Triangular
+// solves: one persistent dependency-driven launch per solve (k_solve_dag below) over the
+// solve panels Z = [I; L21] L11^{-1} built by the factorization.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -30,7 +26,6 @@
 using sgn::DFront;
 using sgn::kTile;
 using sgn::kPanelTiles;
-using sgn::Work;
 
 #define CUDA_TRY(expr)                                                              \
   do {                                                                              \
@@ -43,656 +38,7 @@ using sgn::Work;
 
 namespace {
 
-constexpr int kAsmThreads = 256;
-constexpr int kPanelThreads = 128;
-constexpr int kUpdThreads = 128;
 constexpr int kSolveThreads = 256;
-
-// ------------------------------------------------------------------------------------
-// assembly: one CTA owns one 32x32 lower tile of one front
-// ------------------------------------------------------------------------------------
-__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int v) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (a[mid] < v) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-__global__ void __launch_bounds__(kAsmThreads)
-k_assemble(const Work* __restrict__ work, const DFront* __restrict__ fronts,
-           const int32_t* __restrict__ children, const int32_t* __restrict__ rel,
-           const int64_t* __restrict__ tile_ptr, const int64_t* __restrict__ tile_nnz,
-           const int32_t* __restrict__ tile_loc, const int8_t* __restrict__ kind_pos,
-           const double* __restrict__ values, int64_t vstride, double eps_x, double eps_l,
-           const double* __restrict__ eps_xv, const double* __restrict__ eps_lv,
-           double* __restrict__ fstore, int64_t fstride) {
-  __shared__ double tile[kTile][kTile + 1];
-  const Work w = work[blockIdx.x];
-  const int b = blockIdx.y;
-  const DFront F = fronts[w.f];
-  const int ti = w.a, tj = w.b;
-  const int tid = threadIdx.x;
-  double* fb = fstore + (int64_t)b * fstride;
-  const double* vals = values + (int64_t)b * vstride;
-  for (int e = tid; e < kTile * kTile; e += blockDim.x) tile[e >> 5][e & 31] = 0.0;
-  __syncthreads();
-  const int64_t tid_g = F.tile_base + (int64_t)ti * (ti + 1) / 2 + tj;
-  {
-    const int64_t e0 = tile_ptr[tid_g], e1 = tile_ptr[tid_g + 1];
-#pragma unroll 4
-    for (int64_t e = e0 + tid; e < e1; e += kAsmThreads) {
-      const int loc = tile_loc[e];
-      tile[loc >> 5][loc & 31] = vals[tile_nnz[e]];
-    }
-  }
-  __syncthreads();
-  if (ti == tj && tid < kTile) {
-    const int r = ti * kTile + tid;
-    if (r < F.npiv) {
-      const int8_t k = kind_pos[F.first + r];
-      if (k == 1) tile[tid][tid] += eps_xv ? eps_xv[b] : eps_x;
-      else if (k == 2) tile[tid][tid] -= eps_lv ? eps_lv[b] : eps_l;
-    }
-  }
-  const int i0 = ti * kTile, i1 = min(i0 + kTile, F.nrow);
-  const int j0 = tj * kTile, j1 = min(j0 + kTile, F.nrow);
-  for (int ci = F.child_begin; ci < F.child_end; ++ci) {
-    const DFront C = fronts[children[ci]];
-    const int cn = C.nrow - C.npiv;
-    if (cn == 0) continue;
-    const int32_t* rc = rel + C.rel_off;
-    const int r_lo = lower_bound_i32(rc, cn, i0), r_hi = lower_bound_i32(rc, cn, i1);
-    const int s_lo = lower_bound_i32(rc, cn, j0), s_hi = lower_bound_i32(rc, cn, j1);
-    const int nr = r_hi - r_lo, ns = s_hi - s_lo;
-    __syncthreads();
-    if (nr > 0 && ns > 0) {
-      const double* U = fb + C.foff;
-      const int64_t ldc = C.nrow;
-#pragma unroll 4
-      for (int idx = tid; idx < nr * ns; idx += kAsmThreads) {
-        const int r = r_lo + idx % nr, s = s_lo + idx / nr;
-        if (r >= s) {
-          const double u = U[(int64_t)(C.npiv + s) * ldc + C.npiv + r];
-          tile[rc[r] - i0][rc[s] - j0] += u;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  double* Fm = fb + F.foff;
-  const int64_t ld = F.nrow;
-  for (int e = tid; e < kTile * kTile; e += blockDim.x) {
-    const int ii = e & 31, jj = e >> 5;
-    const int gi = i0 + ii, gj = j0 + jj;
-    if (gi < i1 && gj < j1) Fm[(int64_t)gj * ld + gi] = tile[ii][jj];
-  }
-}
-
-__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-  asm volatile(
-      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(d0), "+d"(d1)
-      : "d"(a), "d"(b));
-}
-
-// ------------------------------------------------------------------------------------
-// One warp factors a <= 32 x 32 diagonal block held in shared memory (lane i owns row i):
-// LDL^T with 2x2 pivots on (2t, 2t+1) (pivtype 2) or 1x1 pivots; D stays in place, L below
-// the pivot blocks.  Rows live in registers; columns are exchanged with shuffles.
-// ------------------------------------------------------------------------------------
-// One warp factors the <= 32 x 32 diagonal block with rows in registers (lane i = row i).
-// Every shuffle is executed by all lanes (no divergent branch around it, so the compiler
-// emits native SHFL); inactive steps/rows are masked with selects.  Templated on the
-// pivot type so each instantiation stays small (~2k instructions).
-template <int PT>
-__device__ __forceinline__ void warp_ldlt_reg(double (*D)[kTile + 1], int w, int* bad, bool store) {
-  const int i = threadIdx.x & 31;
-  int first_bad = 1 << 30;
-  double d[kTile];
-#pragma unroll
-  for (int k = 0; k < kTile; ++k) d[k] = (k <= i) ? D[i][k] : 0.0;
-#pragma unroll
-  for (int j = 0; j < kTile; j += PT) {
-    const bool act = (j < w);
-    if (PT == 2) {
-      const double a = __shfl_sync(0xffffffffu, d[j], j);
-      const double bb = __shfl_sync(0xffffffffu, d[j], j + 1);
-      const double c = __shfl_sync(0xffffffffu, d[j + 1], j + 1);
-      double det = a * c - bb * bb;
-      first_bad = (act && (det == 0.0 || !isfinite(det)) && first_bad > j) ? j : first_bad;
-      det = act ? det : 1.0;
-      const double rdet = 1.0 / det;
-      const double ia = c * rdet, ib = -bb * rdet, ic = a * rdet;
-      const bool below = act && (i > j + 1) && (i < w);
-      const double x0 = d[j], x1 = d[j + 1];
-      const double l0 = below ? x0 * ia + x1 * ib : 0.0;
-      const double l1 = below ? x0 * ib + x1 * ic : 0.0;
-#pragma unroll
-      for (int k = j + 2; k < kTile; ++k) {
-        const double y0 = __shfl_sync(0xffffffffu, x0, k);
-        const double y1 = __shfl_sync(0xffffffffu, x1, k);
-        const double nd = d[k] - (l0 * y0 + l1 * y1);
-        d[k] = (below && k <= i) ? nd : d[k];
-      }
-      d[j] = below ? l0 : d[j];
-      d[j + 1] = below ? l1 : d[j + 1];
-    } else {
-      double dj = __shfl_sync(0xffffffffu, d[j], j);
-      first_bad = (act && (dj == 0.0 || !isfinite(dj)) && first_bad > j) ? j : first_bad;
-      dj = act ? dj : 1.0;
-      const bool below = act && (i > j) && (i < w);
-      const double x = d[j];
-      const double l = below ? x / dj : 0.0;
-#pragma unroll
-      for (int k = j + 1; k < kTile; ++k) {
-        const double y = __shfl_sync(0xffffffffu, x, k);
-        const double nd = d[k] - l * y;
-        d[k] = (below && k <= i) ? nd : d[k];
-      }
-      d[j] = below ? l : d[j];
-    }
-  }
-  __syncthreads();   // all warps have read D before warp 0 overwrites it
-  if (store) {
-#pragma unroll
-    for (int k = 0; k < kTile; ++k) if (k <= i) D[i][k] = d[k];
-    if (i == 0 && first_bad < (1 << 30)) atomicMin(bad, first_bad);
-  }
-}
-
-// TRSM of one 32-row tile (lane = row, row in registers): W L11^T = P, right-looking so
-// the FMAs of a step are independent; L11 columns are broadcast reads from smem.
-template <int PT>
-__device__ __forceinline__ void warp_trsm_reg(double (*P)[kTile + 1], const double (*D)[kTile + 1]) {
-  const int i = threadIdx.x & 31;
-  double p[kTile];
-#pragma unroll
-  for (int c = 0; c < kTile; ++c) p[c] = P[i][c];
-#pragma unroll
-  for (int cp = 0; cp < kTile; ++cp) {
-#pragma unroll
-    for (int c = cp + 1; c < kTile; ++c) {
-      if (PT == 2 && (cp & 1) == 0 && c == cp + 1) continue;   // D slot, compile-time
-      p[c] -= p[cp] * D[c][cp];
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < kTile; ++c) P[i][c] = p[c];
-}
-
-// Panel step k of a front: every CTA factors the diagonal block (one warp, registers +
-// smem; a few us), CTA t == 0 stores L11/D and the block inverse, CTAs t >= 1 form their
-// 32-row tile of W = P L11^{-T} on DMMA and L21 = W D^{-1}.
-template <int PT>
-__global__ void __launch_bounds__(kPanelThreads, 1)
-k_panel(const Work* __restrict__ work, const DFront* __restrict__ fronts,
-        const int64_t* __restrict__ perm, double* __restrict__ fstore, int64_t fstride,
-        double* __restrict__ wstore, int64_t wstride, double* __restrict__ dscr, int64_t dstride,
-        long long* __restrict__ status) {
-  __shared__ double D[kTile][kTile + 1];
-  __shared__ double P[kPanelTiles][kTile][kTile + 1];
-  __shared__ double Dinv[kTile][3];      // per pivot block: (ia, ib, ic) or (1/d)
-  __shared__ int bad;
-  const Work wk = work[blockIdx.x];
-  const int b = blockIdx.y;
-  const DFront F = fronts[wk.f];
-  const int j0 = wk.a * kTile;
-  const int w = min(kTile, F.npiv - j0);
-  const int t = wk.b;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
-  double* Fm = fstore + (int64_t)b * fstride + F.foff;
-  const int64_t ld = F.nrow;
-  if (tid == 0) bad = 1 << 30;
-#pragma unroll
-  for (int e = tid; e < kTile * kTile; e += kPanelThreads) {   // loads all in flight
-    const int i = e & 31, j = e >> 5;
-    D[i][j] = (i < w && j < w && i >= j) ? Fm[(int64_t)(j0 + j) * ld + j0 + i] : 0.0;
-  }
-  // this CTA: row tiles t .. t+3 below the diagonal block, warp w owns tile t+w
-  const int r0 = j0 + w + (t - 1 + warp) * kTile;
-  const int nr = (t > 0) ? max(0, min(kTile, F.nrow - r0)) : 0;
-  double (*Pw)[kTile + 1] = P[warp];
-  if (t > 0) {
-    double v[kTile];
-#pragma unroll
-    for (int j = 0; j < kTile; ++j) v[j] = (lane < nr && j < w) ? Fm[(int64_t)(j0 + j) * ld + r0 + lane] : 0.0;
-#pragma unroll
-    for (int j = 0; j < kTile; ++j) Pw[lane][j] = v[j];
-  }
-  __syncthreads();
-  warp_ldlt_reg<PT>(D, w, &bad, warp == 0);   // every warp runs it (converged shuffles);
-  __syncthreads();                             // only warp 0 stores the result
-  if (tid < w) {
-    if (PT == 2) {
-      if ((tid & 1) == 0) {
-        const double a = D[tid][tid], bb = D[tid + 1][tid], cc = D[tid + 1][tid + 1];
-        const double rdet = 1.0 / (a * cc - bb * bb);
-        Dinv[tid][0] = cc * rdet; Dinv[tid][1] = -bb * rdet; Dinv[tid][2] = a * rdet;
-      }
-    } else {
-      Dinv[tid][0] = 1.0 / D[tid][tid];
-    }
-  }
-  __syncthreads();
-  if (t == 0) {
-    // the factored block goes to scratch: other CTAs of this launch may still be reading
-    // the unfactored block from F (k_zpanel copies it into F at the end of the level)
-    if (tid == 0 && bad < (1 << 30)) atomicMin(&status[b], (long long)perm[F.first + j0 + bad]);
-    double* ds = dscr + (int64_t)b * dstride + F.doff + (int64_t)wk.a * kTile * kTile;
-    for (int e = tid; e < kTile * kTile; e += blockDim.x) ds[e] = D[e >> 5][e & 31];
-    return;
-  }
-  // W = P L11^{-T} by row-wise substitution (lane per row of the warp's tile, row in
-  // registers, right-looking so the FMAs are independent; explicit inverses would
-  // amplify rounding in the factor itself)
-  if (nr > 0) warp_trsm_reg<PT>(Pw, D);   // W = P L11^{-T}: substitution, no explicit inverse
-  __syncwarp();
-  if (nr == 0) return;
-  double* Wb = wstore + (int64_t)b * wstride + F.woff + (int64_t)(t - 1 + warp) * kTile * kTile;
-  for (int e = lane; e < nr * kTile; e += 32) {
-    const int i = e / kTile, c = e % kTile;
-    Wb[(int64_t)i * kTile + c] = (c < w) ? Pw[i][c] : 0.0;
-  }
-  // L21 = W D^{-1} with the pivot-block inverses precomputed in Dinv (no divisions here)
-  for (int e = lane; e < kTile * kTile; e += 32) {
-    const int i = e & 31, c = e >> 5;
-    if (i >= nr || c >= w) continue;
-    double l;
-    if (PT == 2) {
-      const int c0 = c & ~1;
-      const double x0 = Pw[i][c0], x1 = Pw[i][c0 + 1];
-      l = (c == c0) ? x0 * Dinv[c0][0] + x1 * Dinv[c0][1] : x0 * Dinv[c0][1] + x1 * Dinv[c0][2];
-    } else {
-      l = Pw[i][c] * Dinv[c][0];
-    }
-    Fm[(int64_t)(j0 + c) * ld + r0 + i] = l;
-  }
-}
-
-// ------------------------------------------------------------------------------------
-// Schur update of one 32x32 lower tile of the trailing matrix on the FP64 tensor pipe:
-//   C[i, j] -= sum_c L21[i, c] * W[j, c]       (W = L21 D, row-major scratch)
-// mma.sync.aligned.m8n8k4.row.col.f64: A 8x4 (row), B 4x8 (col), C 8x8.
-// ------------------------------------------------------------------------------------
-
-__global__ void __launch_bounds__(kUpdThreads)
-k_update(const Work* __restrict__ work, const DFront* __restrict__ fronts,
-         double* __restrict__ fstore, int64_t fstride, const double* __restrict__ wstore,
-         int64_t wstride) {
-  __shared__ double As[kTile][kTile + 1];
-  __shared__ double Bs[kTile][kTile + 1];
-  const Work wk = work[blockIdx.x];
-  const int b = blockIdx.y;
-  const DFront F = fronts[wk.f];
-  const int j0 = wk.a * kTile;
-  const int w = min(kTile, F.npiv - j0);
-  const int o = j0 + w;
-  const int ti = wk.b, tj = wk.c;
-  const int rbase = o + ti * kTile, cbase = o + tj * kTile;
-  const int nr = min(kTile, F.nrow - rbase), nc = min(kTile, F.nrow - cbase);
-  const int tid = threadIdx.x;
-  double* Fm = fstore + (int64_t)b * fstride + F.foff;
-  const int64_t ld = F.nrow;
-  const double* Wb = wstore + (int64_t)b * wstride + F.woff;
-#pragma unroll
-  for (int e = tid; e < kTile * kTile; e += kUpdThreads) {
-    const int i = e & 31, c = e >> 5;
-    As[i][c] = (i < nr && c < w) ? Fm[(int64_t)(j0 + c) * ld + rbase + i] : 0.0;
-  }
-#pragma unroll
-  for (int e = tid; e < kTile * kTile; e += kUpdThreads) {
-    const int c = e & 31, j = e >> 5;
-    Bs[j][c] = (j < nc && c < w) ? Wb[(int64_t)(tj * kTile + j) * kTile + c] : 0.0;
-  }
-  __syncthreads();
-  const int warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, q = lane & 3;
-  const int row0 = warp * 8;
-  double acc[4][2];
-#pragma unroll
-  for (int nf = 0; nf < 4; ++nf) acc[nf][0] = acc[nf][1] = 0.0;
-#pragma unroll
-  for (int kk = 0; kk < kTile; kk += 4) {
-    const double a = As[row0 + g][kk + q];
-#pragma unroll
-    for (int nf = 0; nf < 4; ++nf) {
-      const double bv = Bs[nf * 8 + g][kk + q];
-      dmma_8x8x4(acc[nf][0], acc[nf][1], a, bv);
-    }
-  }
-  const int i = row0 + g;
-  if (i < nr) {
-#pragma unroll
-    for (int nf = 0; nf < 4; ++nf) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = nf * 8 + 2 * q + h;
-        if (j < nc && (ti != tj || i >= j)) Fm[(int64_t)(cbase + j) * ld + rbase + i] -= acc[nf][h];
-      }
-    }
-  }
-}
-
-// ------------------------------------------------------------------------------------
-// level-scheduled multifrontal solves (one CTA per front)
-// ------------------------------------------------------------------------------------
-__device__ __forceinline__ bool pair_skip(int pivtype, int row, int col) {
-  // in 2x2-pivot fronts L(2t+1, 2t) is structurally zero (slot holds D)
-  return pivtype == 2 && (col & 1) == 0 && row == col + 1;
-}
-
-// ------------------------------------------------------------------------------------
-// Solve panel Z = [I; L21] L11^{-1} of one front (rows r0..r0+31), built after the front
-// is factored: Z L11 = B with B = e_r (pivot rows) or L21 (struct rows), swept right to
-// left in 32-column blocks; the inter-block products run on DMMA.  With Z the
-// triangular solves are one parallel pass per front (k_fwd / k_bwd below).
-// ------------------------------------------------------------------------------------
-constexpr int kZThreads = 256;
-__global__ void __launch_bounds__(kZThreads)
-k_zpanel(const Work* __restrict__ work, const DFront* __restrict__ fronts,
-         double* __restrict__ fstore, int64_t fstride, double* __restrict__ zstore,
-         int64_t zstride, const double* __restrict__ dscr, int64_t dstride) {
-  __shared__ double Ts[kTile][kTile + 1];          // final Z block of the step (rows x cols)
-  __shared__ double Ls[kTile][kTile + 1];          // diagonal block of L11
-  const Work wk = work[blockIdx.x];
-  const int b = blockIdx.y;
-  const DFront F = fronts[wk.f];
-  const int r0 = wk.a;
-  const int nr = min(kTile, F.nrow - r0);
-  const int npiv = F.npiv;
-  const int64_t ld = F.nrow;
-  double* Fm = fstore + (int64_t)b * fstride + F.foff;
-  double* Zm = zstore + (int64_t)b * zstride + F.zoff;
-  const double* ds = dscr + (int64_t)b * dstride + F.doff;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
-  const int cmax = (r0 < npiv) ? min(npiv, r0 + nr) : npiv;
-  if (r0 < npiv) {   // this row tile owns diagonal block r0/32: publish the factored block to F
-    const double* blk = ds + (int64_t)(r0 / kTile) * kTile * kTile;
-    const int wd = min(kTile, npiv - r0);
-    for (int e = tid; e < kTile * kTile; e += blockDim.x) {
-      const int i = e >> 5, j = e & 31;
-      if (i < wd && j < wd && i >= j) Fm[(int64_t)(r0 + j) * ld + r0 + i] = blk[e];
-    }
-  }
-  const int nb = (cmax + kTile - 1) / kTile;
-  // Z <- B  (identity rows for pivots, L21 rows for the structure)
-  for (int e = tid; e < nr * cmax; e += blockDim.x) {
-    const int i = e % nr, c = e / nr, r = r0 + i;
-    Zm[(int64_t)c * ld + r] = (r < npiv) ? (r == c ? 1.0 : 0.0) : Fm[(int64_t)c * ld + r];
-  }
-  __syncthreads();
-  for (int cbi = nb - 1; cbi >= 0; --cbi) {
-    const int cb = cbi * kTile;
-    const int wb = min(kTile, npiv - cb);
-#pragma unroll
-    for (int e = tid; e < kTile * kTile; e += kZThreads) {
-      const int i = e & 31, c = e >> 5;
-      Ts[i][c] = (i < nr && c < wb) ? Zm[(int64_t)(cb + c) * ld + r0 + i] : 0.0;
-      const int cp = e & 31;
-      Ls[cp][c] = (cp < wb && c < wb && cp > c && !pair_skip(F.pivtype, cp, c))
-                      ? ds[(int64_t)cbi * kTile * kTile + cp * kTile + c] : 0.0;
-    }
-    __syncthreads();
-    if (warp == 0) {   // z Lblk = t, right to left, row in registers (independent FMAs)
-      double z[kTile];
-#pragma unroll
-      for (int c = 0; c < kTile; ++c) z[c] = Ts[lane][c];
-#pragma unroll
-      for (int c = kTile - 1; c > 0; --c) {
-#pragma unroll
-        for (int cc = 0; cc < c; ++cc) z[cc] -= z[c] * Ls[c][cc];
-      }
-#pragma unroll
-      for (int c = 0; c < kTile; ++c) Ts[lane][c] = z[c];
-    }
-    __syncthreads();
-    for (int e = tid; e < kTile * kTile; e += blockDim.x) {
-      const int i = e & 31, c = e >> 5;
-      if (i < nr && c < wb) Zm[(int64_t)(cb + c) * ld + r0 + i] = Ts[i][c];
-    }
-    // right-looking update of the remaining column blocks: Z[:, blk] -= Zblk * L11[cb.., blk]
-    for (int blk = warp; blk < cbi; blk += 8) {
-      const int c0 = blk * kTile;
-      double Bf[8][4];   // B fragments: L11[cb + kk + q][c0 + nf*8 + g]
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-        for (int nf = 0; nf < 4; ++nf) {
-          const int kk = ks * 4 + q;
-          Bf[ks][nf] = (kk < wb) ? Fm[(int64_t)(c0 + nf * 8 + g) * ld + cb + kk] : 0.0;
-        }
-      double acc[4][4][2];
-#pragma unroll
-      for (int mf = 0; mf < 4; ++mf)
-#pragma unroll
-        for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-#pragma unroll
-        for (int mf = 0; mf < 4; ++mf) {
-          const double a = Ts[mf * 8 + g][ks * 4 + q];
-#pragma unroll
-          for (int nf = 0; nf < 4; ++nf) dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], a, Bf[ks][nf]);
-        }
-      }
-#pragma unroll
-      for (int mf = 0; mf < 4; ++mf)
-#pragma unroll
-        for (int nf = 0; nf < 4; ++nf)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int i = mf * 8 + g, j = nf * 8 + 2 * q + h;
-            if (i < nr) Zm[(int64_t)(c0 + j) * ld + r0 + i] -= acc[mf][nf][h];
-          }
-    }
-    __syncthreads();
-  }
-}
-
-// Forward solve, gather step (one CTA per front): v = [b(pivots); 0] + children updates
-// (extend-add in fixed child order; rel maps are injective within a child).
-__global__ void __launch_bounds__(kSolveThreads)
-k_fwd_gather(const Work* __restrict__ work, const DFront* __restrict__ fronts,
-             const int32_t* __restrict__ children, const int32_t* __restrict__ rel,
-             const double* __restrict__ bperm, int64_t n, const double* __restrict__ ubuf,
-             int64_t ustride, double* __restrict__ vbuf, int64_t vstride, int leading) {
-  const int b = blockIdx.y;
-  const DFront F = fronts[work[blockIdx.x].f];
-  if (leading && F.is_root_p) return;
-  const int tid = threadIdx.x;
-  double* v = vbuf + (int64_t)b * vstride + F.voff;
-  const double* bb = bperm + (int64_t)b * n;
-  for (int i = tid; i < F.nrow; i += blockDim.x) v[i] = (i < F.npiv) ? bb[F.first + i] : 0.0;
-  __syncthreads();
-  for (int ci = F.child_begin; ci < F.child_end; ++ci) {
-    const DFront C = fronts[children[ci]];
-    const int cn = C.nrow - C.npiv;
-    const double* uc = ubuf + (int64_t)b * ustride + C.uoff;
-    const int32_t* rc = rel + C.rel_off;
-    for (int t = tid; t < cn; t += blockDim.x) v[rc[t]] += uc[t];
-    __syncthreads();
-  }
-}
-
-// last-arriving CTA of a chunk group (ticket); partials are then summed in chunk order
-__device__ __forceinline__ bool group_last(int* ticket, int nch) {
-  __shared__ int last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int old = atomicAdd(ticket, 1);
-    last = (old == nch - 1);
-    if (last) *ticket = 0;     // reset for the next solve
-  }
-  __syncthreads();
-  if (last) __threadfence();
-  return last;
-}
-
-// Forward solve, GEMV step on (front, 32-row tile, 64-column chunk):
-//   partial_k = Z[rows, chunk] v[chunk]; the group's last CTA sums the chunks in order:
-//   pivot rows -> z = D^{-1} y1 (zbuf); structure rows -> u = v2 - t (parent update).
-__global__ void __launch_bounds__(kSolveThreads)
-k_fwd(const Work* __restrict__ work, const DFront* __restrict__ fronts,
-      const double* __restrict__ fstore, int64_t fstride, const double* __restrict__ zstore,
-      int64_t zstride, const double* __restrict__ vbuf, int64_t vstride,
-      double* __restrict__ zbuf, int64_t n, double* __restrict__ ubuf, int64_t ustride,
-      double* __restrict__ part, int64_t pstride, int* __restrict__ tickets, int64_t n_groups,
-      const int32_t* __restrict__ grp_nchunk, const int64_t* __restrict__ grp_base, int leading) {
-  __shared__ double red[8][33];
-  const int b = blockIdx.y;
-  const Work wk = work[blockIdx.x];
-  const DFront F = fronts[wk.f];
-  if (leading && F.is_root_p) return;
-  const int r0 = wk.a, k = wk.b, g = wk.c;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nr = min(sgn::kFwdRows, F.nrow - r0);
-  const int npiv = F.npiv;
-  const int cend = (r0 < npiv) ? min(npiv, r0 + nr) : npiv;
-  const int c_lo = k * sgn::kFwdCols, c_hi = min(c_lo + sgn::kFwdCols, cend);
-  const double* Zm = zstore + (int64_t)b * zstride + F.zoff;
-  const double* v = vbuf + (int64_t)b * vstride + F.voff;
-  const int64_t ld = F.nrow;
-  __shared__ double vs[sgn::kFwdCols];
-  if (tid < c_hi - c_lo) vs[tid] = v[c_lo + tid];
-  __syncthreads();
-  double a0 = 0.0, a1 = 0.0;
-  if (lane < nr) {
-    const double* zr = Zm + r0 + lane;
-    int c = c_lo + warp;
-    for (; c + 8 < c_hi; c += 16) {
-      a0 += zr[(int64_t)c * ld] * vs[c - c_lo];
-      a1 += zr[(int64_t)(c + 8) * ld] * vs[c + 8 - c_lo];
-    }
-    if (c < c_hi) a0 += zr[(int64_t)c * ld] * vs[c - c_lo];
-  }
-  red[warp][lane] = a0 + a1;
-  __syncthreads();
-  const int nch = grp_nchunk[g];
-  double* pp = part + (int64_t)b * pstride + grp_base[g];
-  if (nch > 1) {
-    if (warp == 0) {
-      double t = 0.0;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) t += red[w][lane];
-      pp[k * 32 + lane] = t;
-    }
-    if (!group_last(tickets + (int64_t)b * n_groups + g, nch)) return;
-  }
-  if (warp != 0) return;
-  double t = 0.0;
-  if (nch > 1) {
-    for (int kk = 0; kk < nch; ++kk) t += __ldcg(pp + kk * 32 + lane);
-  } else {
-#pragma unroll
-    for (int w = 0; w < 8; ++w) t += red[w][lane];
-  }
-  const double tp = __shfl_xor_sync(0xffffffffu, t, 1);   // 2x2 pivot partner row
-  if (lane >= nr) return;
-  const int r = r0 + lane;
-  if (r < npiv) {
-    const double* Fm = fstore + (int64_t)b * fstride + F.foff;
-    double* zb = zbuf + (int64_t)b * n;
-    if (F.pivtype == 2) {
-      const int re = r & ~1;
-      const double a = Fm[(int64_t)re * ld + re], bq = Fm[(int64_t)re * ld + re + 1],
-                   c = Fm[(int64_t)(re + 1) * ld + re + 1];
-      const double det = a * c - bq * bq;
-      zb[F.first + r] = ((r & 1) == 0) ? (c * t - bq * tp) / det : (a * t - bq * tp) / det;
-    } else {
-      zb[F.first + r] = t / Fm[(int64_t)r * ld + r];
-    }
-  } else {
-    ubuf[(int64_t)b * ustride + F.uoff + (r - npiv)] = v[r] - t;
-  }
-}
-
-// Backward solve on (front, 32-column tile, 256-row chunk): x1 = Z^T [z1; -x2] as column
-// dots (warp per column, coalesced), chunk partials combined by the group's last CTA.
-__global__ void __launch_bounds__(kSolveThreads)
-k_bwd(const Work* __restrict__ work, const DFront* __restrict__ fronts,
-      const int64_t* __restrict__ srows, const double* __restrict__ zstore, int64_t zstride,
-      const double* __restrict__ zbuf, double* __restrict__ xbuf, int64_t n,
-      double* __restrict__ part, int64_t pstride, int* __restrict__ tickets, int64_t n_groups,
-      const int32_t* __restrict__ grp_nchunk, const int64_t* __restrict__ grp_base, int leading) {
-  __shared__ double colsum[32];
-  const int b = blockIdx.y;
-  const Work wk = work[blockIdx.x];
-  const DFront F = fronts[wk.f];
-  const int c0 = wk.a, rs = wk.b, g = wk.c;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int ncol = min(sgn::kBwdCols, F.npiv - c0);
-  double* xb = xbuf + (int64_t)b * n;
-  if (leading && F.is_root_p) {
-    if (rs <= c0) for (int j = tid; j < ncol; j += blockDim.x) xb[F.first + c0 + j] = 0.0;
-    return;
-  }
-  __shared__ double vs[sgn::kBwdRows];
-  const double* zb = zbuf + (int64_t)b * n;
-  const double* Zm = zstore + (int64_t)b * zstride + F.zoff;
-  const int64_t ld = F.nrow;
-  const int64_t* sr = srows + F.srow_off;
-  const int np = F.npiv;
-  const int re = min(rs + sgn::kBwdRows, F.nrow);
-  for (int i = tid; i < re - rs; i += blockDim.x) {
-    const int r = rs + i;
-    vs[i] = (r < np) ? zb[F.first + r] : -xb[sr[r - np]];
-  }
-  __syncthreads();
-  // warp w owns columns w, w+8, w+16, w+24 of the tile; all four dots advance together
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  const double* col[4];
-  int rbeg[4];
-#pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    const int j = c0 + warp + 8 * m;
-    col[m] = Zm + (int64_t)j * ld;
-    rbeg[m] = (warp + 8 * m < ncol) ? max(rs, j) : re;   // empty range for missing columns
-  }
-  for (int r = rs + lane; r < re; r += 32) {
-    const double v = vs[r - rs];
-#pragma unroll
-    for (int m = 0; m < 4; ++m)
-      if (r >= rbeg[m]) acc[m] += col[m][r] * v;
-  }
-#pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    double a = acc[m];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) colsum[warp + 8 * m] = a;
-  }
-  __syncthreads();
-  const int nch = grp_nchunk[g];
-  double* pp = part + (int64_t)b * pstride + grp_base[g];
-  const int k = (rs - (c0 / sgn::kBwdRows) * sgn::kBwdRows) / sgn::kBwdRows;
-  if (nch > 1) {
-    if (tid < 32) pp[k * 32 + tid] = colsum[tid];
-    if (!group_last(tickets + (int64_t)b * n_groups + g, nch)) return;
-    if (tid < ncol) {
-      double t = 0.0;
-      for (int kk = 0; kk < nch; ++kk) t += __ldcg(pp + kk * 32 + tid);
-      xb[F.first + c0 + tid] = t;
-    }
-  } else if (tid < ncol) {
-    xb[F.first + c0 + tid] = colsum[tid];
-  }
-}
-
-__global__ void k_permute_in(const double* __restrict__ x, double* __restrict__ y,
-                             const int64_t* __restrict__ perm, int64_t n) {
-  const int b = blockIdx.y;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
-    y[(int64_t)b * n + q] = x[(int64_t)b * n + perm[q]];
-}
-__global__ void k_permute_out(const double* __restrict__ y, double* __restrict__ x,
-                              const int64_t* __restrict__ perm, int64_t n) {
-  const int b = blockIdx.y;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
-    x[(int64_t)b * n + perm[q]] = y[(int64_t)b * n + q];
-}
 
 // ------------------------------------------------------------------------------------
 // Persistent dependency-driven triangular solve: ONE launch per solve.  Resident CTAs grab
@@ -1204,83 +550,31 @@ struct sgn_factor_s {
   int32_t batch = 1;
   int64_t n = 0;
   DevBuf<DFront> fronts;
-  DevBuf<int32_t> children, rel, tile_loc, lvl_fronts, idx32;
+  DevBuf<int32_t> children, rel, reltile, tile_loc, idx32;
   DevBuf<int64_t> srows, perm, tile_ptr, tile_nnz, indptr;
   DevBuf<int8_t> kind_pos;
-  DevBuf<Work> work;
-  DevBuf<double> fstore, wstore, ubuf, vbuf, y, zstore, zbuf, xbuf, part, dscr;
+  DevBuf<double> fstore, ubuf, zstore, zbuf, xbuf, part, dscr;
   DevBuf<int> tickets;
   DevBuf<int32_t> grp_nchunk;
   DevBuf<int64_t> grp_base;
-  DevBuf<long long> status;
+  DevBuf<long long> status, status_init;
+  DevBuf<sgn::FTask> ftasks;
+  DevBuf<int64_t> ftrace;       // SGN_FDAG_TRACE=1: 4 words per factor task (diagnostics)
+  DevBuf<int> fcnt;             // [head | batch x n_fcnt counters] of the persistent factorization
+  int factor_grid = 0;
   DevBuf<sgn::Task> stasks;
   DevBuf<int32_t> swaits, gsrc;
   DevBuf<int64_t> gptr;
   DevBuf<int64_t> trace;        // SGN_DAG_TRACE=1: 3 words per solve task (diagnostics)
   DevBuf<int> scnt;             // [head | batch x n_scnt counters], zeroed before every solve
   int solve_grid = 0;
-  std::vector<int64_t> lvl_off;  // level -> offset into lvl_fronts
   // BiCGSTAB workspace
   DevBuf<double> bx, br, brh, bp, bv, bs, bt, btmp, bbest, bb, bscr, partial;
   DevBuf<BiState> bst;
   bool bicg_ready = false;
-  // captured triangular-solve graphs (index = flags)
-  struct SolveGraph {
-    cudaGraphExec_t exec = nullptr;
-    cudaGraphNode_t in_node = nullptr, out_node = nullptr;
-    cudaKernelNodeParams in_p{}, out_p{};
-    int64_t kernels = 0;
-  } graphs[2];
-  std::vector<cudaGraph_t> graph_templates;
-  DevBuf<double> gin, gout;   // placeholder endpoints used only while capturing
-  const double* bbuf_in() { if (!gin.p) gin.alloc((size_t)batch * std::max<int64_t>(n, 1)); return gin.p; }
-  double* bbuf_out() { if (!gout.p) gout.alloc((size_t)batch * std::max<int64_t>(n, 1)); return gout.p; }
-  ~sgn_factor_s() {
-    for (auto& g : graphs)
-      if (g.exec) cudaGraphExecDestroy(g.exec);
-    for (auto g : graph_templates) cudaGraphDestroy(g);
-  }
 };
 
 namespace {
-
-int launch_solve_raw(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st) {
-  const sgn::Symbolic& s = f->sym->s;
-  const int64_t n = s.n;
-  if (n == 0) return SGN_OK;
-  const dim3 pg((unsigned)std::min<int64_t>((n + 255) / 256, 1024), f->batch);
-  sgn::count_launch();
-  k_permute_in<<<pg, 256, 0, st>>>(d_b, f->y.p, f->perm.p, n);
-  const int leading = (flags & SGN_SOLVE_LEADING) ? 1 : 0;
-  for (int32_t lv = 0; lv < s.n_levels; ++lv) {
-    if (s.gat_cnt[lv]) {
-      sgn::count_launch();
-      k_fwd_gather<<<dim3((unsigned)s.gat_cnt[lv], f->batch), kSolveThreads, 0, st>>>(
-          f->work.p + s.gat_off[lv], f->fronts.p, f->children.p, f->rel.p, f->y.p, n, f->ubuf.p,
-          s.u_doubles, f->vbuf.p, s.v_doubles, leading);
-    }
-    if (s.fwd_cnt[lv]) {
-      sgn::count_launch();
-      k_fwd<<<dim3((unsigned)s.fwd_cnt[lv], f->batch), kSolveThreads, 0, st>>>(
-          f->work.p + s.fwd_off[lv], f->fronts.p, f->fstore.p, s.front_doubles, f->zstore.p,
-          s.z_doubles, f->vbuf.p, s.v_doubles, f->zbuf.p, n, f->ubuf.p, s.u_doubles, f->part.p,
-          s.part_doubles, f->tickets.p, s.n_groups, f->grp_nchunk.p, f->grp_base.p, leading);
-    }
-  }
-  for (int32_t lv = s.n_levels - 1; lv >= 0; --lv) {
-    if (!s.bwd_cnt[lv]) continue;
-    sgn::count_launch();
-    k_bwd<<<dim3((unsigned)s.bwd_cnt[lv], f->batch), kSolveThreads, 0, st>>>(
-        f->work.p + s.bwd_off[lv], f->fronts.p, f->srows.p, f->zstore.p, s.z_doubles, f->zbuf.p,
-        f->xbuf.p, n, f->part.p, s.part_doubles, f->tickets.p, s.n_groups, f->grp_nchunk.p,
-        f->grp_base.p, leading);
-  }
-  sgn::count_launch();
-  k_permute_out<<<pg, 256, 0, st>>>(f->xbuf.p, d_x, f->perm.p, n);
-  CUDA_TRY(cudaGetLastError());
-  return SGN_OK;
-}
-
 
 // One solve = a counter reset + ONE persistent dependency-driven launch (k_solve_dag).
 int launch_solve_dag(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st) {
@@ -1313,73 +607,9 @@ int launch_solve_dag(sgn_factor f, const double* d_b, double* d_x, int32_t flags
   return SGN_OK;
 }
 
-static bool use_level_solve() {
-  static const int v = [] { const char* e = getenv("SGN_SOLVE_LEVELS"); return (e && *e == '1') ? 1 : 0; }();
-  return v != 0;
-}
-
-// Level-scheduled alternative (SGN_SOLVE_LEVELS=1, kept for A/B timing): a fixed launch
-// sequence per (factor, flags), captured once as a CUDA graph and replayed, patching only
-// the permute-in / permute-out pointer arguments.
 int launch_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st) {
-  const int64_t n = f->n;
-  if (n == 0) return SGN_OK;
-  if (!use_level_solve()) return launch_solve_dag(f, d_b, d_x, flags, st);
-  auto& G = f->graphs[(flags & SGN_SOLVE_LEADING) ? 1 : 0];
-  if (!G.exec) {
-    const double* cap_in = f->bbuf_in();   // allocate before capturing
-    double* cap_out = f->bbuf_out();
-    if (!cap_in || !cap_out) { sgn::last_error() = "graph placeholder allocation failed"; return SGN_CUDA_ERROR; }
-    CUDA_TRY(cudaDeviceSynchronize());
-    cudaStream_t cs;
-    CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    cudaGraph_t graph;
-    CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    const int64_t before = sgn::launch_count();
-    int rc = launch_solve_raw(f, cap_in, cap_out, flags, cs);
-    sgn::count_launch(before - sgn::launch_count());   // captured, not launched
-    cudaError_t e = cudaStreamEndCapture(cs, &graph);
-    cudaStreamDestroy(cs);
-    if (rc) return rc;
-    if (e != cudaSuccess) { sgn::last_error() = std::string("capture: ") + cudaGetErrorString(e); return SGN_CUDA_ERROR; }
-    size_t nn = 0;
-    CUDA_TRY(cudaGraphGetNodes(graph, nullptr, &nn));
-    std::vector<cudaGraphNode_t> nodes(nn);
-    CUDA_TRY(cudaGraphGetNodes(graph, nodes.data(), &nn));
-    for (auto nd : nodes) {
-      cudaGraphNodeType t;
-      CUDA_TRY(cudaGraphNodeGetType(nd, &t));
-      if (t != cudaGraphNodeTypeKernel) continue;
-      ++G.kernels;
-      cudaKernelNodeParams p;
-      CUDA_TRY(cudaGraphKernelNodeGetParams(nd, &p));
-      if (p.func == (void*)k_permute_in) { G.in_node = nd; G.in_p = p; }
-      if (p.func == (void*)k_permute_out) { G.out_node = nd; G.out_p = p; }
-    }
-    CUDA_TRY(cudaGraphInstantiate(&G.exec, graph, 0));
-    // the instantiated exec keeps its own copy; node handles stay valid for SetParams
-    G.in_node = G.in_node; G.out_node = G.out_node;
-    f->graph_templates.push_back(graph);
-  }
-  const double* b_arg = d_b;
-  double* y_arg = f->y.p;
-  const int64_t* perm_arg = f->perm.p;
-  int64_t n_arg = n;
-  void* in_args[] = {(void*)&b_arg, (void*)&y_arg, (void*)&perm_arg, (void*)&n_arg};
-  cudaKernelNodeParams pin = G.in_p;
-  pin.kernelParams = in_args;
-  pin.extra = nullptr;
-  CUDA_TRY(cudaGraphExecKernelNodeSetParams(G.exec, G.in_node, &pin));
-  const double* xs_arg = f->xbuf.p;
-  double* x_arg = d_x;
-  void* out_args[] = {(void*)&xs_arg, (void*)&x_arg, (void*)&perm_arg, (void*)&n_arg};
-  cudaKernelNodeParams pout = G.out_p;
-  pout.kernelParams = out_args;
-  pout.extra = nullptr;
-  CUDA_TRY(cudaGraphExecKernelNodeSetParams(G.exec, G.out_node, &pout));
-  CUDA_TRY(cudaGraphLaunch(G.exec, st));
-  sgn::count_launch(G.kernels);
-  return SGN_OK;
+  if (f->n == 0) return SGN_OK;
+  return launch_solve_dag(f, d_b, d_x, flags, st);
 }
 
 int launch_spmv(sgn_factor f, const double* vals, int64_t vstride, const double* x, double* y,
@@ -1494,30 +724,21 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
     d.npiv = F.npiv; d.nrow = F.nrow; d.parent = F.parent; d.pivtype = F.pivtype;
     d.child_begin = F.child_begin; d.child_end = F.child_end; d.is_root_p = F.is_root_p;
     d.level = F.level;
+    d.cbase = F.cbase; d.ftotal = F.ftotal; d.pad = 0;
   }
-  std::vector<int32_t> lf;
-  f->lvl_off.assign(s.n_levels + 1, 0);
-  for (int32_t lv = 0; lv < s.n_levels; ++lv) {
-    f->lvl_off[lv] = (int64_t)lf.size();
-    lf.insert(lf.end(), s.level_fronts[lv].begin(), s.level_fronts[lv].end());
-  }
-  f->lvl_off[s.n_levels] = (int64_t)lf.size();
   std::vector<int32_t> idx32(s.indices.begin(), s.indices.end());
   int rc = 0;
   if ((rc = f->fronts.upload(df)) || (rc = f->children.upload(s.children)) ||
-      (rc = f->rel.upload(s.rel)) || (rc = f->tile_loc.upload(s.tile_loc)) ||
-      (rc = f->lvl_fronts.upload(lf)) || (rc = f->idx32.upload(idx32)) ||
+      (rc = f->rel.upload(s.rel)) || (rc = f->reltile.upload(s.reltile)) || (rc = f->tile_loc.upload(s.tile_loc)) ||
+      (rc = f->idx32.upload(idx32)) ||
       (rc = f->srows.upload(s.srows)) || (rc = f->perm.upload(s.perm)) ||
       (rc = f->tile_ptr.upload(s.tile_ptr)) || (rc = f->tile_nnz.upload(s.tile_nnz)) ||
-      (rc = f->indptr.upload(s.indptr)) || (rc = f->kind_pos.upload(s.kind_pos)) ||
-      (rc = f->work.upload(s.work)))
+      (rc = f->indptr.upload(s.indptr)) || (rc = f->kind_pos.upload(s.kind_pos)))
     return rc;
   const size_t B = (size_t)batch;
   if ((rc = f->fstore.alloc(B * std::max<int64_t>(s.front_doubles, 1))) ||
-      (rc = f->wstore.alloc(B * std::max<int64_t>(s.w_doubles, 1))) ||
       (rc = f->ubuf.alloc(B * std::max<int64_t>(s.u_doubles, 1))) ||
-      (rc = f->vbuf.alloc(B * std::max<int64_t>(s.v_doubles, 1))) ||
-      (rc = f->y.alloc(B * std::max<int64_t>(s.n, 1))) || (rc = f->status.alloc(B)) ||
+      (rc = f->status.alloc(B)) ||
       (rc = f->zstore.alloc(B * std::max<int64_t>(s.z_doubles, 1))) ||
       (rc = f->zbuf.alloc(B * std::max<int64_t>(s.n, 1))) ||
       (rc = f->xbuf.alloc(B * std::max<int64_t>(s.n, 1))))
@@ -1527,6 +748,9 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
       (rc = f->tickets.alloc(B * std::max<int64_t>(s.n_groups, 1))) ||
       (rc = f->grp_nchunk.upload(s.grp_nchunk)) || (rc = f->grp_base.upload(s.grp_base)) ||
       (rc = f->stasks.upload(s.stasks)) || (rc = f->swaits.upload(s.swaits)) ||
+      (rc = f->ftasks.upload(s.ftasks)) ||
+      (rc = f->fcnt.alloc(1 + B * std::max<int64_t>(s.n_fcnt, 1))) ||
+      (rc = f->status_init.upload(std::vector<long long>(B, (long long)INT64_MAX))) ||
       (rc = f->gptr.upload(s.gptr)) || (rc = f->gsrc.upload(s.gsrc)) ||
       (rc = f->scnt.alloc(1 + B * std::max<int64_t>(s.n_scnt, 1))))
     return rc;
@@ -1536,6 +760,8 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_dag, kSolveThreads, 0));
     f->solve_grid = std::max(1, sms * std::max(per_sm, 1));
+    f->factor_grid = sgn::factor_dag_grid();
+    if (f->factor_grid <= 0) { sgn::last_error() = "factor occupancy query failed"; return SGN_CUDA_ERROR; }
   }
   CUDA_TRY(cudaMemset(f->tickets.p, 0, f->tickets.n * sizeof(int)));
   // Z11 = L11^{-1} is lower triangular: the strictly upper part stays zero forever
@@ -1563,49 +789,26 @@ static int factor_numeric_impl(sgn_factor f, const double* d_values, int64_t val
                                const double* d_eps_l, void* stream) {
   const sgn::Symbolic& s = f->sym->s;
   cudaStream_t st = (cudaStream_t)stream;
-  {
-    std::vector<long long> init(f->batch, (long long)INT64_MAX);
-    CUDA_TRY(cudaMemcpyAsync(f->status.p, init.data(), init.size() * sizeof(long long),
-                             cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaStreamSynchronize(st));  // keep `init` alive until the copy is done
-  }
-  for (const sgn::Launch& L : s.launches) {
-    const dim3 grid((unsigned)L.count, f->batch);
-    const Work* w = f->work.p + L.off;
-    switch (L.kind) {
-      case sgn::L_ASM:
-        sgn::count_launch();
-        k_assemble<<<grid, kAsmThreads, 0, st>>>(w, f->fronts.p, f->children.p, f->rel.p,
-                                                 f->tile_ptr.p, f->tile_nnz.p, f->tile_loc.p,
-                                                 f->kind_pos.p, d_values, values_stride, eps_x,
-                                                 eps_lambda, d_eps_x, d_eps_l, f->fstore.p,
-                                                 s.front_doubles);
-        break;
-      case sgn::L_PANEL:
-        sgn::count_launch();
-        if (L.pivtype == 2)
-          k_panel<2><<<grid, kPanelThreads, 0, st>>>(w, f->fronts.p, f->perm.p, f->fstore.p,
-                                                s.front_doubles, f->wstore.p, s.w_doubles,
-                                                f->dscr.p, s.d_doubles, f->status.p);
-        else
-        k_panel<1><<<grid, kPanelThreads, 0, st>>>(w, f->fronts.p, f->perm.p, f->fstore.p,
-                                                s.front_doubles, f->wstore.p, s.w_doubles,
-                                                f->dscr.p, s.d_doubles, f->status.p);
-        break;
-      case sgn::L_ZPANEL:
-        sgn::count_launch();
-        k_zpanel<<<grid, kZThreads, 0, st>>>(w, f->fronts.p, f->fstore.p, s.front_doubles,
-                                               f->zstore.p, s.z_doubles, f->dscr.p, s.d_doubles);
-        break;
-      case sgn::L_UPDATE:
-        sgn::count_launch();
-        k_update<<<grid, kUpdThreads, 0, st>>>(w, f->fronts.p, f->fstore.p, s.front_doubles,
-                                               f->wstore.p, s.w_doubles);
-        break;
-    }
-  }
-  CUDA_TRY(cudaGetLastError());
-  return SGN_OK;
+  CUDA_TRY(cudaMemcpyAsync(f->status.p, f->status_init.p, f->batch * sizeof(long long),
+                           cudaMemcpyDeviceToDevice, st));
+  sgn::FactorArgs A;
+  A.tasks = f->ftasks.p; A.ntask = (int64_t)s.ftasks.size(); A.batch = f->batch;
+  A.head = f->fcnt.p; A.cnt = f->fcnt.p + 1; A.n_fcnt = s.n_fcnt;
+  A.fronts = f->fronts.p; A.children = f->children.p; A.rel = f->rel.p; A.reltile = f->reltile.p;
+  A.tile_ptr = f->tile_ptr.p; A.tile_nnz = f->tile_nnz.p; A.tile_loc = f->tile_loc.p;
+  A.kind_pos = f->kind_pos.p; A.values = d_values; A.vstride = values_stride;
+  A.eps_x = eps_x; A.eps_l = eps_lambda; A.eps_xv = d_eps_x; A.eps_lv = d_eps_l;
+  A.perm = f->perm.p; A.fstore = f->fstore.p; A.fstride = s.front_doubles;
+  A.zstore = f->zstore.p; A.zstride = s.z_doubles; A.dscr = f->dscr.p; A.dstride = s.d_doubles;
+  A.status = f->status.p;
+  A.trace = nullptr;
+  { const char* e = getenv("SGN_FDAG_TRACE");
+    if (e && *e == '1') {
+      if (!f->ftrace.p && f->ftrace.alloc((size_t)8 * std::max<int64_t>(1, A.ntask * f->batch))) return SGN_CUDA_ERROR;
+      A.trace = (unsigned long long*)f->ftrace.p;
+      CUDA_TRY(cudaMemsetAsync(f->ftrace.p, 0, f->ftrace.n * sizeof(int64_t), st));
+    } }
+  return sgn::launch_factor_dag(A, f->factor_grid, st);
 }
 
 int sgn_factor_check(sgn_factor f, void* stream, int64_t* pivot_index) {
@@ -1646,6 +849,24 @@ int sgn_debug_solve_trace(sgn_factor f, int64_t* out, int64_t cap, int64_t* n_ta
   if (out && f->trace.p) {
     const int64_t m = std::min<int64_t>(cap, 6 * nt);
     CUDA_TRY(cudaMemcpy(out, f->trace.p, m * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  }
+  return SGN_OK;
+}
+
+int sgn_debug_factor_trace(sgn_factor f, int64_t* out, int64_t cap, int64_t* n_tasks, int32_t* meta) {
+  const sgn::Symbolic& s = f->sym->s;
+  const int64_t nt = (int64_t)s.ftasks.size() * f->batch;
+  if (n_tasks) *n_tasks = nt;
+  if (meta) {   // per task: kind, step, front, level, a, b
+    for (size_t t = 0; t < s.ftasks.size(); ++t) {
+      const sgn::FTask& T = s.ftasks[t];
+      meta[6 * t] = T.kind_k & 7; meta[6 * t + 1] = T.kind_k >> 3; meta[6 * t + 2] = T.f;
+      meta[6 * t + 3] = s.fronts[T.f].level; meta[6 * t + 4] = T.a; meta[6 * t + 5] = T.b;
+    }
+  }
+  if (out && f->ftrace.p) {
+    const int64_t m = std::min<int64_t>(cap, 8 * nt);
+    CUDA_TRY(cudaMemcpy(out, f->ftrace.p, m * sizeof(int64_t), cudaMemcpyDeviceToHost));
   }
   return SGN_OK;
 }

@@ -5,6 +5,12 @@
 #include <string>
 #include <vector>
 
+#ifdef __CUDACC__
+#define SGN_HD __host__ __device__ __forceinline__
+#else
+#define SGN_HD inline
+#endif
+
 namespace sgn {
 
 constexpr int kTile = 32;   // assembly tile, panel width, update tile
@@ -24,11 +30,13 @@ struct Front {
   int64_t srow_off = 0;   // offset of struct rows (positions) in Symbolic::srows
   int64_t rel_off = 0;    // offset of rel map (struct -> parent local rows)
   int64_t uoff = 0;       // offset of the forward-solve update vector (nstruct)
-  int64_t woff = 0;       // offset of the panel W scratch (nrow x 32)
+  int64_t woff = 0;       // offset of its rel ranges per parent tile (Symbolic::reltile)
   int64_t voff = 0;       // offset of the solve front vector (nrow)
   int64_t tile_base = 0;  // first assembly tile id
   int64_t zoff = 0;       // offset of the solve panel Z = [I; L21] L11^{-1} (nrow x npiv)
-  int64_t doff = 0;       // offset of the 32x32 diagonal-block inverses of L11
+  int64_t doff = 0;       // offset of the factored 32x32 diagonal blocks (scratch)
+  int64_t cbase = 0;      // first dependency counter of the front (persistent factorization)
+  int32_t ftotal = 0;     // assembly + panel + update tasks of the front
 };
 
 // Device-side mirror of Front (POD, 16-byte aligned for vector loads).
@@ -45,7 +53,49 @@ struct DFront {
   int64_t doff;
   int32_t npiv, nrow, parent, pivtype;
   int32_t child_begin, child_end, is_root_p, level;
+  int64_t cbase;
+  int32_t ftotal, pad;
 };
+
+// Split tile grid of a front: pivot tiles a < P cover rows [32a, min(32a+32, npiv)), the
+// contribution tiles a >= P cover [npiv + 32(a-P), ...).  Pivot step k is tile k, so every
+// Schur-update step touches whole tiles and per-tile dependency counters are exact.
+SGN_HD int ptiles(int npiv) { return (npiv + 31) / 32; }
+SGN_HD int ntiles_front(int npiv, int nrow) { return ptiles(npiv) + (nrow - npiv + 31) / 32; }
+SGN_HD int tile_lo(int npiv, int a) {
+  const int P = ptiles(npiv);
+  return a < P ? 32 * a : npiv + 32 * (a - P);
+}
+SGN_HD int tile_hi(int npiv, int nrow, int a) {
+  const int P = ptiles(npiv);
+  return a < P ? (32 * a + 32 < npiv ? 32 * a + 32 : npiv) : (npiv + 32 * (a - P) + 32 < nrow ? npiv + 32 * (a - P) + 32 : nrow);
+}
+SGN_HD int tile_of_row(int npiv, int r) { return r < npiv ? r / 32 : ptiles(npiv) + (r - npiv) / 32; }
+
+// Persistent factorization task (16 bytes).  kind_k = kind | (k << 3); waits and signals
+// are derived from the coordinates on the device (no stored wait lists).  Per pivot step
+// k of a front the diagonal block D_k is factored ONCE (by the assembly task of tile
+// (0,0) for k = 0, else by F_DIAGUPD(k-1)) and published to scratch as [D | L^T | D^-1]:
+//   F_ASM     (f, a=ti, b=tj): waits DONE(child) == ftotal(child) for every child
+//   F_PANEL   (f, k, a=t)    : TRSM of row tiles {k+1} (t = 0) or k+2+4(t-1).. (t >= 1);
+//                              waits DIAG(f, k), TILE(f, i, k) == 1 + k for its rows
+//   F_UPDATE  (f, k, a=ti, b=tj): waits PAN(f, k) == TRSM tasks of step k, TILE(f,ti,tj) == 1+k
+//   F_DIAGUPD (f, k)         : last update of tile (k+1, k+1) + LDL^T of D_{k+1}; waits as
+//                              F_UPDATE(k, k+1, k+1); signals DIAG(f, k+1)
+//   F_ZPANEL  (f, a=r0, b=cb): waits DONE(f) == ftotal(f), ZC(f, r0/32) == blocks right of cb
+// counters of front f at cbase: DONE, PAN(k), DIAG(k) (k < P), TILE(ti*(ti+1)/2 + tj), ZC(slab)
+enum FKind : int32_t { F_ASM = 0, F_PANEL = 1, F_UPDATE = 2, F_ZPANEL = 3, F_DIAGUPD = 4 };
+struct FTask { int32_t kind_k, f, a, b; };
+constexpr int kDiagStride = 2 * kTile * kTile + 3 * kTile;   // scratch per step: D, L^T, D^-1
+SGN_HD int panel_tasks(int npiv, int nrow, int k) {   // TRSM tasks of step k
+  const int T = ntiles_front(npiv, nrow);
+  const int rest = T - k - 2;
+  return (k + 1 < T ? 1 : 0) + (rest > 0 ? (rest + 3) / 4 : 0);
+}
+SGN_HD int cnt_pan(int k) { return 1 + k; }
+SGN_HD int cnt_diag(int P, int k) { return 1 + P + k; }
+SGN_HD int cnt_tile(int P, int ti, int tj) { return 1 + 2 * P + ti * (ti + 1) / 2 + tj; }
+SGN_HD int cnt_zc(int P, int T, int slab) { return 1 + 2 * P + T * (T + 1) / 2 + slab; }
 
 struct Work { int32_t f, a, b, c; };   // generic work item
 
@@ -71,6 +121,7 @@ struct Symbolic {
   std::vector<int32_t> children;
   std::vector<int64_t> srows;                  // struct rows (positions), sorted per front
   std::vector<int32_t> rel;                    // per front: struct row -> parent local row
+  std::vector<int32_t> reltile;                // per front: first rel index >= each parent tile (T_parent + 1)
   std::vector<int8_t> kind_pos;                // 0 none, 1 +eps_x, 2 -eps_lambda
   std::vector<int32_t> front_of_pos;
   // assembly entry lists per tile
@@ -98,10 +149,28 @@ struct Symbolic {
   // (ubuf offsets) in child order: v[r] = b[r] + sum u[gsrc[gptr[voff+r] .. gptr[voff+r+1])]
   std::vector<int64_t> gptr;
   std::vector<int32_t> gsrc;
+  // persistent factorization: tasks in topological order + counters per instance
+  std::vector<FTask> ftasks;
+  int64_t n_fcnt = 0;
   // sizes
   int64_t front_doubles = 0, u_doubles = 0, w_doubles = 0, v_doubles = 0, z_doubles = 0, d_doubles = 0;
   int64_t nnz_l = 0; double flops = 0; int64_t max_front = 0, max_piv = 0;
 };
+
+// arguments of the persistent factorization launch (factor_dag.cu); head is followed by
+// batch x n_fcnt dependency counters, all zeroed before every factorization
+struct FactorArgs {
+  const FTask* tasks; int64_t ntask; int32_t batch;
+  int* head; int* cnt; int64_t n_fcnt;
+  const DFront* fronts; const int32_t* children; const int32_t* rel; const int32_t* reltile;
+  const int64_t* tile_ptr; const int64_t* tile_nnz; const int32_t* tile_loc; const int8_t* kind_pos;
+  const double* values; int64_t vstride; double eps_x, eps_l; const double* eps_xv; const double* eps_lv;
+  const int64_t* perm; double* fstore; int64_t fstride; double* zstore; int64_t zstride;
+  double* dscr; int64_t dstride; long long* status;
+  unsigned long long* trace;   // optional (SGN_FDAG_TRACE=1): 4 words per task
+};
+int factor_dag_grid();
+int launch_factor_dag(const FactorArgs& A, int grid, void* stream);
 
 std::string& last_error();
 

@@ -637,11 +637,10 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     const int64_t nr = F.nrow, ns = F.nrow - F.npiv;
     F.foff = s.front_doubles; s.front_doubles += nr * nr;
     F.uoff = s.u_doubles; s.u_doubles += ns;
-    F.woff = s.w_doubles; s.w_doubles += nr * kTile;
     F.voff = s.v_doubles; s.v_doubles += nr;
     F.zoff = s.z_doubles; s.z_doubles += nr * F.npiv;
-    F.doff = s.d_doubles; s.d_doubles += (int64_t)((F.npiv + kTile - 1) / kTile) * kTile * kTile;
-    const int64_t T = (nr + kTile - 1) / kTile;
+    F.doff = s.d_doubles; s.d_doubles += (int64_t)((F.npiv + kTile - 1) / kTile) * kDiagStride;
+    const int64_t T = ntiles_front(F.npiv, F.nrow);
     F.tile_base = s.ntiles; s.ntiles += T * (T + 1) / 2;
     s.nnz_l += (int64_t)F.npiv * (F.npiv + 1) / 2 + (int64_t)F.npiv * ns;
     for (int64_t j = 0; j < F.npiv; ++j) {
@@ -687,11 +686,11 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
           if (it == sb + sn || *it != pu) { last_error() = "internal: entry outside front"; return 5; }
           lr = F.npiv + (it - sb);
         }
-        const int64_t ti = lr / kTile, tj = lc / kTile;
+        const int64_t ti = tile_of_row(F.npiv, (int)lr), tj = tile_of_row(F.npiv, (int)lc);
         const int64_t tile = F.tile_base + ti * (ti + 1) / 2 + tj;
         ent_tile.push_back(tile);
         ent_k.push_back(k);
-        ent_loc.push_back((int32_t)((lr % kTile) * kTile + (lc % kTile)));
+        ent_loc.push_back((int32_t)((lr - tile_lo(F.npiv, (int)ti)) * kTile + (lc - tile_lo(F.npiv, (int)tj))));
         cnt[tile + 1]++;
       }
     }
@@ -707,62 +706,102 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     }
   }
 
-  // ---- factorization launch schedule -----------------------------------------
+  // child rel ranges per parent tile: rows of child c landing in parent tile a are
+  // rel[reltile[c.woff + a] .. reltile[c.woff + a + 1])  (rel is increasing)
+  s.reltile.clear();
+  for (auto& C : s.fronts) {
+    C.woff = (int64_t)s.reltile.size();
+    if (C.parent < 0) continue;
+    const Front& P = s.fronts[C.parent];
+    const int32_t TP = ntiles_front(P.npiv, P.nrow);
+    const int32_t* rc = s.rel.data() + C.rel_off;
+    const int32_t cn = C.nrow - C.npiv;
+    for (int32_t a = 0; a <= TP; ++a) {
+      const int32_t lo = (a < TP) ? tile_lo(P.npiv, a) : P.nrow;
+      s.reltile.push_back((int32_t)(std::lower_bound(rc, rc + cn, lo) - rc));
+    }
+  }
+  s.w_doubles = 0;
+
+  // ---- persistent factorization tasks (topological order) -----------------------------
+  // per level: assembly tiles of its fronts; per pivot step k: panel tasks, then Schur
+  // updates with the look-ahead column (tj == k+1) first so the next panel can start
+  // while the rest of the trailing matrix is updated; finally the solve panels Z.
   s.work.clear();
   s.launches.clear();
-  for (int32_t lv = 0; lv < s.n_levels; ++lv) {
-    const auto& fl = s.level_fronts[lv];
-    // assembly tiles
-    int64_t off = (int64_t)s.work.size();
-    for (int32_t f : fl) {
-      const int64_t T = (s.fronts[f].nrow + kTile - 1) / kTile;
-      for (int64_t ti = 0; ti < T; ++ti)
-        for (int64_t tj = 0; tj <= ti; ++tj) s.work.push_back({f, (int32_t)ti, (int32_t)tj, 0});
+  s.ftasks.clear();
+  s.n_fcnt = 0;
+  for (auto& F : s.fronts) {
+    const int64_t P = ptiles(F.npiv), T = ntiles_front(F.npiv, F.nrow);
+    F.cbase = s.n_fcnt;
+    s.n_fcnt += 1 + 2 * P + T * (T + 1) / 2 + (F.nrow + kTile - 1) / kTile;
+    int64_t tot = T * (T + 1) / 2;                        // assembly tiles
+    for (int64_t k = 0; k < P; ++k) {
+      tot += panel_tasks(F.npiv, F.nrow, (int)k);
+      const int64_t m = T - k - 1;                        // trailing tiles per side
+      tot += m * (m + 1) / 2;                             // updates (+ the DIAGUPD one)
     }
-    if ((int64_t)s.work.size() > off) s.launches.push_back({L_ASM, lv, off, (int64_t)s.work.size() - off});
-    int32_t maxp = 0;
-    for (int32_t f : fl) maxp = std::max(maxp, (s.fronts[f].npiv + kTile - 1) / kTile);
-    for (int32_t k = 0; k < maxp; ++k) {
-      for (int32_t pt = 1; pt <= 2; ++pt) {      // one panel launch per pivot type
-        off = (int64_t)s.work.size();
-        for (int32_t f : fl) {
-          const Front& F = s.fronts[f];
-          const int32_t j0 = k * kTile;
-          if (j0 >= F.npiv || F.pivtype != pt) continue;
-          const int32_t w = std::min(kTile, F.npiv - j0);
-          const int32_t below = F.nrow - j0 - w;
-          const int32_t nt = (below + kTile - 1) / kTile;        // 32-row tiles below
-          s.work.push_back({f, k, 0, 0});                         // diagonal-block CTA
-          for (int32_t t = 1; t <= nt; t += kPanelTiles) s.work.push_back({f, k, t, 0});
-        }
-        if ((int64_t)s.work.size() > off) {
-          Launch L{L_PANEL, lv, off, (int64_t)s.work.size() - off};
-          L.pivtype = pt;
-          s.launches.push_back(L);
-        }
-      }
-      off = (int64_t)s.work.size();
-      for (int32_t f : fl) {
-        const Front& F = s.fronts[f];
-        const int32_t j0 = k * kTile;
-        if (j0 >= F.npiv) continue;
-        const int32_t w = std::min(kTile, F.npiv - j0);
-        const int32_t below = F.nrow - j0 - w;
-        const int32_t T = (below + kTile - 1) / kTile;
-        for (int32_t ti = 0; ti < T; ++ti)
-          for (int32_t tj = 0; tj <= ti; ++tj) s.work.push_back({f, k, ti, tj});
-      }
-      if ((int64_t)s.work.size() > off) s.launches.push_back({L_UPDATE, lv, off, (int64_t)s.work.size() - off});
-    }
-    // solve panel Z = [I; L21] L11^{-1}: one CTA per 32 rows of every front of the level
-    off = (int64_t)s.work.size();
+    if (tot > INT32_MAX) { last_error() = "front too large for the task schedule"; return 5; }
+    F.ftotal = (int32_t)tot;
+  }
+  auto ft = [&](int32_t kind, int32_t k, int32_t f, int32_t a, int32_t b) {
+    s.ftasks.push_back(FTask{kind | (k << 3), f, a, b});
+  };
+  // Z blocks (slab r0, column block cb), right to left within a slab
+  auto add_ztasks = [&](const std::vector<int32_t>& fl) {
     for (int32_t f : fl) {
       const Front& F = s.fronts[f];
       if (F.npiv == 0) continue;
-      for (int32_t r0 = 0; r0 < F.nrow; r0 += kTile) s.work.push_back({f, r0, 0, 0});
+      const int32_t nb = (F.npiv + kTile - 1) / kTile;
+      for (int32_t cb = nb - 1; cb >= 0; --cb)
+        for (int32_t r0 = 0; r0 < F.nrow; r0 += kTile) {
+          const int32_t nr = std::min(kTile, F.nrow - r0);
+          const int32_t cmax = (r0 < F.npiv) ? std::min(F.npiv, r0 + nr) : F.npiv;
+          if (cb < (cmax + kTile - 1) / kTile) ft(F_ZPANEL, 0, f, r0, cb);
+        }
     }
-    if ((int64_t)s.work.size() > off) s.launches.push_back({L_ZPANEL, lv, off, (int64_t)s.work.size() - off});
+  };
+  for (int32_t lv = 0; lv < s.n_levels; ++lv) {
+    const auto& fl = s.level_fronts[lv];
+    for (int32_t f : fl) {
+      const int32_t T = ntiles_front(s.fronts[f].npiv, s.fronts[f].nrow);
+      for (int32_t ti = 0; ti < T; ++ti)
+        for (int32_t tj = 0; tj <= ti; ++tj) ft(F_ASM, 0, f, ti, tj);
+    }
+    int32_t maxp = 0;
+    for (int32_t f : fl) maxp = std::max(maxp, ptiles(s.fronts[f].npiv));
+    for (int32_t k = 0; k < maxp; ++k) {
+      for (int32_t f : fl) {
+        const Front& F = s.fronts[f];
+        if (k >= ptiles(F.npiv)) continue;
+        const int32_t np = panel_tasks(F.npiv, F.nrow, k);
+        for (int32_t t = 0; t < np; ++t) ft(F_PANEL, k, f, t, 0);
+      }
+      for (int32_t f : fl) {                                 // next diagonal block
+        const Front& F = s.fronts[f];
+        if (k + 1 < ptiles(F.npiv)) ft(F_DIAGUPD, k, f, 0, 0);
+      }
+      for (int32_t f : fl) {                                 // look-ahead column first
+        const Front& F = s.fronts[f];
+        if (k >= ptiles(F.npiv)) continue;
+        const int32_t T = ntiles_front(F.npiv, F.nrow);
+        const bool diag_next = k + 1 < ptiles(F.npiv);
+        if (k + 1 < T)
+          for (int32_t ti = k + 1; ti < T; ++ti)
+            if (!(diag_next && ti == k + 1)) ft(F_UPDATE, k, f, ti, k + 1);
+      }
+      for (int32_t f : fl) {
+        const Front& F = s.fronts[f];
+        if (k >= ptiles(F.npiv)) continue;
+        const int32_t T = ntiles_front(F.npiv, F.nrow);
+        for (int32_t tj = k + 2; tj < T; ++tj)
+          for (int32_t ti = tj; ti < T; ++ti) ft(F_UPDATE, k, f, ti, tj);
+      }
+    }
   }
+  // solve-panel blocks last (bottom levels first): they fill the CTAs left idle by the
+  // top levels' dependency chain instead of delaying the levels above
+  for (int32_t lv = 0; lv < s.n_levels; ++lv) add_ztasks(s.level_fronts[lv]);
   // solve work lists: gather (f), forward GEMV (f, row0, chunk, group), backward dots
   // (f, col0, row chunk, group); each (front, tile) group combines its chunk partials
   s.fwd_off.assign(s.n_levels, 0); s.fwd_cnt.assign(s.n_levels, 0);

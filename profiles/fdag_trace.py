@@ -1,0 +1,72 @@
+"""Trace one persistent factorization (SGN_FDAG_TRACE=1) and summarise it.
+
+  python profiles/fdag_trace.py [--config 2]
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+KIND = {0: "asm", 1: "panel", 2: "update", 3: "zpanel"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--out", default="gpurun_out/fdag_trace.npz")
+    a = ap.parse_args()
+    os.environ["SGN_FDAG_TRACE"] = "1"
+    import torch
+    from paper_2107_03285_b200._lib import lib
+    from paper_2107_03285_b200.problems import build_sheet
+    prob, p0 = build_sheet(a.config)
+    x = prob.simulate(p0)
+    prob._load(x, p0)
+    eng = prob.engine
+    eng.direction()
+    fac = eng.kfac
+    for _ in range(3):
+        fac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda)
+    torch.cuda.synchronize()
+    nt = ctypes.c_int64()
+    lib().sgn_debug_factor_trace(fac._h, None, 0, ctypes.byref(nt), None)
+    meta = np.zeros(6 * nt.value, np.int32)
+    tr = np.zeros(8 * nt.value, np.int64)
+    lib().sgn_debug_factor_trace(fac._h, tr.ctypes.data_as(ctypes.c_void_p), tr.size, None,
+                                 meta.ctypes.data_as(ctypes.c_void_p))
+    tr = tr.reshape(-1, 8)
+    meta = meta.reshape(-1, 6)
+    base = tr[:, 0].min()
+    T = (tr[:, :3].astype(np.float64) - base) / 1e3
+    M = np.where(tr[:, 4:8] > 0, (tr[:, 4:8].astype(np.float64) - base) / 1e3, np.nan)
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    np.savez(a.out, T=T, M=M, sm=tr[:, 3], meta=meta)
+    kind, step, front, lvl = meta[:, 0], meta[:, 1], meta[:, 2], meta[:, 3]
+    print("span us %.1f tasks %d" % (T[:, 2].max(), len(T)))
+    for k in range(4):
+        m = kind == k
+        if m.any():
+            print(f"{KIND[k]:7s} n={m.sum():6d} busy_med={np.median(T[m, 2] - T[m, 1]):6.2f} "
+                  f"wait_med={np.median(T[m, 1] - T[m, 0]):6.2f} busy_sum_us={np.sum(T[m, 2] - T[m, 1]):9.1f}")
+    print("per level: first ready / last end (us)")
+    for L in sorted(set(lvl.tolist())):
+        m = lvl == L
+        print(f"L{L:2d} n={m.sum():6d} ready={T[m, 1].min():8.1f} end={T[m, 2].max():8.1f} "
+              f"panels={np.sum(m & (kind == 1)):5d} steps={step[m].max() + 1:3d}")
+    # critical chain of the top front: per step, panel end and look-ahead update end
+    top = front[np.argmax(lvl)]
+    m = front == top
+    print("top front", top, "steps")
+    for s in range(step[m & (kind == 1)].max() + 1):
+        pm = m & (kind == 1) & (step == s)
+        um = m & (kind == 2) & (step == s)
+        print(f"  k={s:3d} panel ready {T[pm, 1].min():8.1f} end {T[pm, 2].max():8.1f} busy {np.max(T[pm, 2] - T[pm, 1]):5.2f}"
+              + (f" | upd end {T[um, 2].max():8.1f} busy_med {np.median(T[um, 2] - T[um, 1]):5.2f}" if um.any() else ""))
+
+
+if __name__ == "__main__":
+    main()
