@@ -259,13 +259,12 @@ __device__ int f_panel_pre(const sgn::FactorArgs& A, const DFront& F, int b, int
   const int j0 = k * kTile, w = min(kTile, F.npiv - j0);
   const int T = sgn::ntiles_front(F.npiv, F.nrow);
   double (*Lt)[kTile + 1] = v33(S.a);
-  const double* ds = A.dscr + (int64_t)b * A.dstride + F.doff + (int64_t)k * sgn::kDiagStride;
-  for (int e = tid; e < kTile * kTile; e += kFThreads) Lt[e >> 5][e & 31] = __ldcg(ds + kTile * kTile + e);
-  if (tid < 3 * kTile) (&S.dinv[0][0])[tid] = __ldcg(ds + 2 * kTile * kTile + tid);
   const int ti = (t == 0) ? (warp == 0 ? k + 1 : T) : k + 2 + 4 * (t - 1) + warp;
   const int lo = (ti < T) ? sgn::tile_lo(F.npiv, ti) : 0;
   const int nr = (ti < T) ? sgn::tile_hi(F.npiv, F.nrow, ti) - lo : 0;
   double (*Pw)[kTile + 1] = v33(S.b[warp]);
+  // the row tiles are final (waited by the caller): load them while D_k may still be in
+  // production, then wait for D_k and read its published L^T / D^-1
   if (nr > 0) {
     double v[kTile];
 #pragma unroll
@@ -273,6 +272,14 @@ __device__ int f_panel_pre(const sgn::FactorArgs& A, const DFront& F, int b, int
 #pragma unroll
     for (int j = 0; j < kTile; ++j) Pw[lane][j] = v[j];
   }
+  if (tid == 0) {
+    const int P = sgn::ptiles(F.npiv);
+    spin_ge(A.cnt + (int64_t)b * A.n_fcnt + F.cbase + sgn::cnt_diag(P, k), 1);
+  }
+  __syncthreads();
+  const double* ds = A.dscr + (int64_t)b * A.dstride + F.doff + (int64_t)k * sgn::kDiagStride;
+  for (int e = tid; e < kTile * kTile; e += kFThreads) Lt[e >> 5][e & 31] = __ldcg(ds + kTile * kTile + e);
+  if (tid < 3 * kTile) (&S.dinv[0][0])[tid] = __ldcg(ds + 2 * kTile * kTile + tid);
   return nr;
 }
 
@@ -320,13 +327,8 @@ __device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k
   const int row0 = warp * 8;
   const int i = row0 + g;
   double va[8], vb[8], cv[4][2];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {           // all 24 loads in flight together
-    const int e = tid + u * kFThreads;
-    const int r = e & 31, c = e >> 5;
-    va[u] = (r < nr && c < w) ? __ldcg(Fm + (int64_t)(j0 + c) * ld + lo_i + r) : 0.0;
-    vb[u] = (c < nc && r < w) ? __ldcg(Fm + (int64_t)(lo_j + c) * ld + j0 + r) : 0.0;   // (j = c, col = r)
-  }
+  // C is final up to step k-1 (waited by the caller): prefetch it while step k's panels
+  // may still be running, then wait for them and load L21 / W
 #pragma unroll
   for (int nf = 0; nf < 4; ++nf)
 #pragma unroll
@@ -334,6 +336,16 @@ __device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k
       const int j = nf * 8 + 2 * q + h;
       cv[nf][h] = (i < nr && j < nc && (ti != tj || i >= j)) ? __ldcg(Fm + (int64_t)(lo_j + j) * ld + lo_i + i) : 0.0;
     }
+  if (tid == 0)
+    spin_ge(A.cnt + (int64_t)b * A.n_fcnt + F.cbase + sgn::cnt_pan(k), sgn::panel_tasks(F.npiv, F.nrow, k));
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {           // 16 operand loads in flight together
+    const int e = tid + u * kFThreads;
+    const int r = e & 31, c = e >> 5;
+    va[u] = (r < nr && c < w) ? __ldcg(Fm + (int64_t)(j0 + c) * ld + lo_i + r) : 0.0;
+    vb[u] = (c < nc && r < w) ? __ldcg(Fm + (int64_t)(lo_j + c) * ld + j0 + r) : 0.0;   // (j = c, col = r)
+  }
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     const int e = tid + u * kFThreads;
@@ -502,8 +514,7 @@ k_factor_dag(const sgn::FactorArgs A) {
           const DFront C = A.fronts[A.children[ci]];
           spin_ge(cnt + C.cbase, C.ftotal);
         }
-      } else if (kind == sgn::F_PANEL) {
-        spin_ge(cf + sgn::cnt_diag(P, k), 1);
+      } else if (kind == sgn::F_PANEL) {          // DIAG(k) is awaited inside (after P loads)
         if (T.a == 0) {
           spin_ge(cf + sgn::cnt_tile(P, k + 1, k), 1 + k);
         } else {
@@ -512,9 +523,8 @@ k_factor_dag(const sgn::FactorArgs A) {
             if (i < Tn) spin_ge(cf + sgn::cnt_tile(P, i, k), 1 + k);
           }
         }
-      } else if (kind == sgn::F_UPDATE || kind == sgn::F_DIAGUPD) {
+      } else if (kind == sgn::F_UPDATE || kind == sgn::F_DIAGUPD) {   // PAN(k) awaited inside
         const int ti = (kind == sgn::F_DIAGUPD) ? k + 1 : T.a, tj = (kind == sgn::F_DIAGUPD) ? k + 1 : T.b;
-        spin_ge(cf + sgn::cnt_pan(k), sgn::panel_tasks(F.npiv, F.nrow, k));
         spin_ge(cf + sgn::cnt_tile(P, ti, tj), 1 + k);
       } else {
         spin_ge(cf, F.ftotal);

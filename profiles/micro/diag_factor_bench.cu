@@ -2,6 +2,7 @@
 // (variants of factor_diag in paper_2107_03285_b200/csrc/factor_dag.cu).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o diag_bench diag_factor_bench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 constexpr int kTile = 32;
@@ -250,7 +251,7 @@ __device__ int fd_unrolled_smem(double (*D)[kTile + 1], double2* colbuf, int w) 
 }
 
 template <int V, int PT>
-__global__ void kbench(const double* in, double* out, long long* cyc, int reps) {
+__global__ void kbench(const double* in, double* out, long long* cyc, int reps, int wr) {
   __shared__ double D[kTile][kTile + 1];
   __shared__ double2 colbuf[2 * kTile];
   const int i = threadIdx.x;
@@ -264,8 +265,8 @@ __global__ void kbench(const double* in, double* out, long long* cyc, int reps) 
     else if (V == 1) bad += fd_window<PT, true>(D, colbuf, kTile);
     else if (V == 2) bad += fd_smem<PT>(D, kTile);
     else if (V == 3) bad += fd_unrolled<PT>(D, kTile);
-    else if (V == 4) bad += fd_window_pad<PT>(D, colbuf, kTile);
-    else bad += fd_unrolled_smem<PT>(D, colbuf, kTile);
+    else if (V == 4) bad += fd_window_pad<PT>(D, colbuf, wr);
+    else bad += fd_unrolled_smem<PT>(D, colbuf, wr);
     __syncwarp();
     const long long t1 = clock64();
     total += t1 - t0;
@@ -274,7 +275,8 @@ __global__ void kbench(const double* in, double* out, long long* cyc, int reps) 
   if (i == 0) { cyc[0] = total / reps; cyc[1] = bad; }
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const int wr = argc > 1 ? atoi(argv[1]) : 32;
   double h[kTile * kTile];
   for (int i = 0; i < kTile; ++i)
     for (int k = 0; k < kTile; ++k) {
@@ -293,19 +295,19 @@ int main() {
       double o[kTile * kTile];
       for (int rep = 0; rep < 2; ++rep) {
         if (pt == 1) {
-          if (v == 0) kbench<0, 1><<<1, 32>>>(din, dout, dc, 20);
-          if (v == 1) kbench<1, 1><<<1, 32>>>(din, dout, dc, 20);
-          if (v == 2) kbench<2, 1><<<1, 32>>>(din, dout, dc, 20);
-          if (v == 3) kbench<3, 1><<<1, 32>>>(din, dout, dc, 20);
-          if (v == 4) kbench<4, 1><<<1, 32>>>(din, dout, dc, 20);
-          if (v == 5) kbench<5, 1><<<1, 32>>>(din, dout, dc, 20);
+          if (v == 0) kbench<0, 1><<<1, 32>>>(din, dout, dc, 20, wr);
+          if (v == 1) kbench<1, 1><<<1, 32>>>(din, dout, dc, 20, wr);
+          if (v == 2) kbench<2, 1><<<1, 32>>>(din, dout, dc, 20, wr);
+          if (v == 3) kbench<3, 1><<<1, 32>>>(din, dout, dc, 20, wr);
+          if (v == 4) kbench<4, 1><<<1, 32>>>(din, dout, dc, 20, wr);
+          if (v == 5) kbench<5, 1><<<1, 32>>>(din, dout, dc, 20, wr);
         } else {
-          if (v == 0) kbench<0, 2><<<1, 32>>>(din, dout, dc, 20);
-          if (v == 1) kbench<1, 2><<<1, 32>>>(din, dout, dc, 20);
-          if (v == 2) kbench<2, 2><<<1, 32>>>(din, dout, dc, 20);
-          if (v == 3) kbench<3, 2><<<1, 32>>>(din, dout, dc, 20);
-          if (v == 4) kbench<4, 2><<<1, 32>>>(din, dout, dc, 20);
-          if (v == 5) kbench<5, 2><<<1, 32>>>(din, dout, dc, 20);
+          if (v == 0) kbench<0, 2><<<1, 32>>>(din, dout, dc, 20, wr);
+          if (v == 1) kbench<1, 2><<<1, 32>>>(din, dout, dc, 20, wr);
+          if (v == 2) kbench<2, 2><<<1, 32>>>(din, dout, dc, 20, wr);
+          if (v == 3) kbench<3, 2><<<1, 32>>>(din, dout, dc, 20, wr);
+          if (v == 4) kbench<4, 2><<<1, 32>>>(din, dout, dc, 20, wr);
+          if (v == 5) kbench<5, 2><<<1, 32>>>(din, dout, dc, 20, wr);
         }
         cudaDeviceSynchronize();
       }
