@@ -64,6 +64,7 @@ struct SolveArgs {
   int64_t n; double* part; int64_t pstride; int* tickets; int64_t n_groups;
   const int32_t* grp_nchunk; const int64_t* grp_base;
   const double* b_in; double* x_out; int leading; int nop; int mode;
+  const int* gate;             // optional: skip the whole solve when *gate == 0
   unsigned long long* trace;   // optional, 6 words per task: start, smid|signalled, prefetched, ready, combined, end
 };
 
@@ -323,6 +324,7 @@ __device__ bool dag_bwd(const SolveArgs& A, const sgn::Task& T, int b, const int
 __global__ void __launch_bounds__(kSolveThreads)
 k_solve_dag(const SolveArgs A) {
   __shared__ int s_idx;
+  if (A.gate && *A.gate == 0) return;
   const int64_t total = A.ntask * A.batch;
   for (;;) {
     __syncthreads();                               // s_idx of the previous task consumed
@@ -356,7 +358,8 @@ k_solve_dag(const SolveArgs A) {
 __global__ void k_spmv(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                        const double* __restrict__ vals, int64_t vstride,
                        const double* __restrict__ x, double* __restrict__ y, int64_t n,
-                       int64_t p_lo, int64_t p_hi) {
+                       int64_t p_lo, int64_t p_hi, const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;        // refinement finished for every instance
   const int b = blockIdx.y;
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
   const int sub = threadIdx.x & 7;
@@ -382,55 +385,20 @@ __global__ void k_spmv(const int64_t* __restrict__ ptr, const int32_t* __restric
 constexpr int kDotBlocks = 64;
 constexpr int kDotThreads = 256;
 
-// up to 2 dot products in one pass: out[b*2+0] = a.b, out[b*2+1] = c.d (if c)
-__global__ void __launch_bounds__(kDotThreads)
-k_dot_partial(const double* __restrict__ a, const double* __restrict__ bvec,
-              const double* __restrict__ c, const double* __restrict__ d, int64_t n,
-              double* __restrict__ partial) {
-  __shared__ double s0[kDotThreads], s1[kDotThreads];
-  const int b = blockIdx.y;
-  const double* ab = a + (int64_t)b * n;
-  const double* bb = bvec + (int64_t)b * n;
-  double acc0 = 0.0, acc1 = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    acc0 += ab[i] * bb[i];
-    if (c) acc1 += c[(int64_t)b * n + i] * d[(int64_t)b * n + i];
-  }
-  s0[threadIdx.x] = acc0;
-  s1[threadIdx.x] = acc1;
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) { s0[threadIdx.x] += s0[threadIdx.x + s]; s1[threadIdx.x] += s1[threadIdx.x + s]; }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    partial[((int64_t)b * kDotBlocks + blockIdx.x) * 2 + 0] = s0[0];
-    partial[((int64_t)b * kDotBlocks + blockIdx.x) * 2 + 1] = s1[0];
-  }
-}
-
 struct BiState {
   double rho, alpha, omega, bnorm, best_res, res, dot0, dot1;
-  int32_t active, iters, reason, pad;
+  int32_t active, iters, reason, cur;   // cur: current iteration (device-side loop counter)
 };
 
-// reduce partials and run one scalar step of BiCGSTAB per instance.
-// step: 0 = bnorm, 1 = initial residual (res0), 2 = rho, 3 = alpha, 4 = omega, 5 = residual
-__global__ void k_dot_final(const double* __restrict__ partial, BiState* __restrict__ st,
-                            int step, double tol, int32_t it) {
-  const int b = blockIdx.x;
-  if (threadIdx.x != 0) return;
-  double s0 = 0.0, s1 = 0.0;
-  for (int k = 0; k < kDotBlocks; ++k) {
-    s0 += partial[((int64_t)b * kDotBlocks + k) * 2 + 0];
-    s1 += partial[((int64_t)b * kDotBlocks + k) * 2 + 1];
-  }
-  BiState& S = st[b];
+// One scalar step of BiCGSTAB per instance from the reduced dots s0 (= a.b) and s1 (= c.d).
+// step: 0 = bnorm, 1 = initial residual (res0), 2 = rho/beta (starts iteration cur+1),
+//       3 = alpha, 4 = omega, 5 = true residual of the iterate
+__device__ void bicg_scalar(BiState& S, int step, double s0, double s1, double tol) {
   S.dot0 = s0;
   S.dot1 = s1;
   if (step == 0) {
     S.bnorm = sqrt(s0);
-    S.iters = 0; S.reason = 0; S.active = 1;
+    S.iters = 0; S.reason = 0; S.active = 1; S.cur = 0;
     S.rho = S.alpha = S.omega = 1.0;
     if (S.bnorm == 0.0) { S.active = 0; S.res = 0.0; S.best_res = 0.0; S.reason = 4; }
     return;
@@ -441,23 +409,83 @@ __global__ void k_dot_final(const double* __restrict__ partial, BiState* __restr
     S.best_res = S.res;
     if (S.res <= tol) { S.active = 0; S.reason = 1; }
   } else if (step == 2) {
+    S.cur += 1;
+    if (S.reason == 10) S.reason = 0;      // the previous iterate's best-copy is done
     const double rho_new = s0;
-    if (rho_new == 0.0 || S.omega == 0.0) { S.active = 0; S.reason = 2; S.iters = it - 1; return; }
+    if (rho_new == 0.0 || S.omega == 0.0) { S.active = 0; S.reason = 2; S.iters = S.cur - 1; return; }
     const double beta = (rho_new / S.rho) * (S.alpha / S.omega);
     S.rho = rho_new;
     S.dot1 = beta;
   } else if (step == 3) {
-    if (s0 == 0.0) { S.active = 0; S.reason = 2; S.iters = it - 1; return; }
+    if (s0 == 0.0) { S.active = 0; S.reason = 2; S.iters = S.cur - 1; return; }
     S.alpha = S.rho / s0;
   } else if (step == 4) {
-    // s0 = t.t, s1 = t.s
-    S.omega = (s0 > 0.0) ? s1 / s0 : 0.0;
+    S.omega = (s0 > 0.0) ? s1 / s0 : 0.0;          // s0 = t.t, s1 = t.s
   } else if (step == 5) {
     S.res = sqrt(s0) / S.bnorm;
-    S.iters = it;
+    S.iters = S.cur;
     if (S.res < S.best_res) { S.best_res = S.res; S.reason = 10; /* copy best */ }
     if (S.res <= tol) { S.active = 0; S.reason = 1; }
   }
+}
+
+// Dots + scalar step in ONE launch: every block reduces its slice (fixed tree), the last
+// block of the instance (ticket) adds the block partials in block order and runs the
+// scalar step.  mode 0: s0 = a.b, s1 = c.d (c optional); mode 1 (residual): r = a - b,
+// s0 = r.r, and r is stored to `out` when given.
+__global__ void __launch_bounds__(kDotThreads)
+k_dotF(int mode, const double* __restrict__ a, const double* __restrict__ bvec,
+       const double* __restrict__ c, const double* __restrict__ d, double* __restrict__ out,
+       int64_t n, double* __restrict__ partial, int* __restrict__ tickets,
+       BiState* __restrict__ st, int step, double tol) {
+  __shared__ double s0[kDotThreads], s1[kDotThreads];
+  __shared__ int last;
+  const int b = blockIdx.y;
+  const int64_t base = (int64_t)b * n;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (mode == 1) {
+      const double r = a[base + i] - bvec[base + i];
+      if (out) out[base + i] = r;
+      acc0 += r * r;
+    } else {
+      acc0 += a[base + i] * bvec[base + i];
+      if (c) acc1 += c[base + i] * d[base + i];
+    }
+  }
+  s0[threadIdx.x] = acc0;
+  s1[threadIdx.x] = acc1;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) { s0[threadIdx.x] += s0[threadIdx.x + k]; s1[threadIdx.x] += s1[threadIdx.x + k]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partial[((int64_t)b * kDotBlocks + blockIdx.x) * 2 + 0] = s0[0];
+    partial[((int64_t)b * kDotBlocks + blockIdx.x) * 2 + 1] = s1[0];
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(tickets + b) : "memory");
+    last = (old == (int)gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  tickets[b] = 0;
+  double t0 = 0.0, t1 = 0.0;
+  for (int k = 0; k < (int)gridDim.x; ++k) {
+    t0 += __ldcg(partial + ((int64_t)b * kDotBlocks + k) * 2 + 0);
+    t1 += __ldcg(partial + ((int64_t)b * kDotBlocks + k) * 2 + 1);
+  }
+  bicg_scalar(st[b], step, t0, t1, tol);
+}
+
+// loop control: gate = any instance still iterating; sets the graph's WHILE condition
+__global__ void k_cond(const BiState* __restrict__ st, int B, int max_iters, int* __restrict__ gate,
+                       cudaGraphConditionalHandle h, int set_handle) {
+  if (threadIdx.x != 0) return;
+  int any = 0;
+  for (int b = 0; b < B; ++b) any |= (st[b].active != 0 && st[b].cur < max_iters);
+  *gate = any;
+  if (set_handle) cudaGraphSetConditional(h, any ? 1u : 0u);
 }
 
 // vector kernels (each masked by the instance's active flag)
@@ -499,10 +527,6 @@ __global__ void k_vec(int mode, const BiState* __restrict__ st, int64_t n,
   }
 }
 
-__global__ void k_clear_reason(BiState* st) {
-  const int b = blockIdx.x;
-  if (threadIdx.x == 0 && st[b].reason == 10) st[b].reason = 0;
-}
 
 // final select: out = (converged at last iterate) ? x : best
 __global__ void k_select(const BiState* __restrict__ st, int64_t n, const double* __restrict__ x,
@@ -571,13 +595,27 @@ struct sgn_factor_s {
   // BiCGSTAB workspace
   DevBuf<double> bx, br, brh, bp, bv, bs, bt, btmp, bbest, bb, bscr, partial;
   DevBuf<BiState> bst;
+  DevBuf<int> gate, dtick;
   bool bicg_ready = false;
+  // refinement graphs: prologue + WHILE(any instance iterating){ one BiCGSTAB iteration }
+  struct BicgGraph {
+    const double* vals = nullptr; int64_t vstride = 0; int32_t flags = 0; double tol = 0; int32_t max_iters = 0;
+    cudaGraph_t graph = nullptr; cudaGraphExec_t exec = nullptr; int64_t k_pro = 0, k_body = 0;
+  };
+  std::vector<BicgGraph> bgraphs;
+  ~sgn_factor_s() {
+    for (auto& g : bgraphs) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      if (g.graph) cudaGraphDestroy(g.graph);
+    }
+  }
 };
 
 namespace {
 
 // One solve = a counter reset + ONE persistent dependency-driven launch (k_solve_dag).
-int launch_solve_dag(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st) {
+int launch_solve_dag(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st,
+                     const int* gate = nullptr) {
   const sgn::Symbolic& s = f->sym->s;
   SolveArgs A;
   A.tasks = f->stasks.p; A.waits = f->swaits.p; A.ntask = (int64_t)s.stasks.size(); A.batch = f->batch;
@@ -589,6 +627,7 @@ int launch_solve_dag(sgn_factor f, const double* d_b, double* d_x, int32_t flags
   A.part = f->part.p; A.pstride = s.part_doubles; A.tickets = f->tickets.p; A.n_groups = s.n_groups;
   A.grp_nchunk = f->grp_nchunk.p; A.grp_base = f->grp_base.p;
   A.b_in = d_b; A.x_out = d_x; A.leading = (flags & SGN_SOLVE_LEADING) ? 1 : 0;
+  A.gate = gate;
   { const char* e = getenv("SGN_DAG_NOP"); A.nop = (e && *e == '1') ? 1 : 0; }
   A.trace = nullptr;   // SGN_DAG_TRACE=1: 6 words per task
   { const char* e = getenv("SGN_DAG_MODE"); A.mode = e ? atoi(e) : 0; }
@@ -607,13 +646,14 @@ int launch_solve_dag(sgn_factor f, const double* d_b, double* d_x, int32_t flags
   return SGN_OK;
 }
 
-int launch_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st) {
+int launch_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, cudaStream_t st,
+                 const int* gate = nullptr) {
   if (f->n == 0) return SGN_OK;
-  return launch_solve_dag(f, d_b, d_x, flags, st);
+  return launch_solve_dag(f, d_b, d_x, flags, st, gate);
 }
 
 int launch_spmv(sgn_factor f, const double* vals, int64_t vstride, const double* x, double* y,
-                int32_t flags, cudaStream_t st) {
+                int32_t flags, cudaStream_t st, const int* gate = nullptr) {
   const sgn::Symbolic& s = f->sym->s;
   const int64_t n = s.n;
   if (n == 0) return SGN_OK;
@@ -622,7 +662,7 @@ int launch_spmv(sgn_factor f, const double* vals, int64_t vstride, const double*
   const int64_t threads = n * 8;
   sgn::count_launch();
   k_spmv<<<dim3((unsigned)((threads + 255) / 256), f->batch), 256, 0, st>>>(
-      f->indptr.p, f->idx32.p, vals, vstride, x, y, n, p_lo, p_hi);
+      f->indptr.p, f->idx32.p, vals, vstride, x, y, n, p_lo, p_hi, gate);
   CUDA_TRY(cudaGetLastError());
   return SGN_OK;
 }
@@ -882,6 +922,107 @@ int sgn_spmv(sgn_factor f, const double* d_values, int64_t values_stride, const 
   return launch_spmv(f, d_values, values_stride, d_x, d_y, flags, (cudaStream_t)stream);
 }
 
+// Left-preconditioned restart-free BiCGSTAB on the UNSHIFTED K with the stabilized factor
+// as preconditioner (reference linear_solvers.py:130-211: x0 = M^-1 b; stop on the true
+// residual; best iterate kept).  The whole iteration runs device-side: a CUDA graph with a
+// WHILE conditional node whose body is one iteration; k_cond sets the condition from the
+// per-instance state, and the gated solves / SpMVs of a finished refinement return at once.
+// One host synchronisation per call.
+static int build_bicg_graph(sgn_factor f, sgn_factor_s::BicgGraph& G) {
+  const int64_t n = f->n;
+  const int B = f->batch;
+  const size_t N = (size_t)B * std::max<int64_t>(n, 1);
+  const dim3 vg((unsigned)std::min<int64_t>((n + 255) / 256, 1024), B);
+  const dim3 dg(kDotBlocks, B);
+  BiState* S = f->bst.p;
+  const double tol = G.tol;
+  const int32_t flags = G.flags;
+  const int* gate = f->gate.p;
+  cudaStream_t cs;
+  CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  CUDA_TRY(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+  const int64_t before = sgn::launch_count();
+  auto dotF = [&](int mode, const double* a, const double* b2, const double* c, const double* d, double* out, int step) {
+    sgn::count_launch();
+    k_dotF<<<dg, kDotThreads, 0, cs>>>(mode, a, b2, c, d, out, n, f->partial.p, f->dtick.p, S, step, tol);
+  };
+  auto vec = [&](int mode, double* o, const double* x, const double* y, const double* z, double* o2) {
+    sgn::count_launch();
+    k_vec<<<vg, 256, 0, cs>>>(mode, S, n, o, x, y, z, o2, nullptr);
+  };
+  int rc = SGN_OK;
+  // ---- prologue: x0 = M^-1 b, res0, r = M^-1 (b - A x0), r_hat = r, p = v = 0
+  CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  dotF(0, f->bb.p, f->bb.p, nullptr, nullptr, nullptr, 0);                              // bnorm
+  if (!rc) rc = launch_solve(f, f->bb.p, f->bx.p, flags, cs);                           // x0
+  if (!rc) rc = launch_spmv(f, G.vals, G.vstride, f->bx.p, f->bscr.p, flags, cs);
+  dotF(1, f->bb.p, f->bscr.p, nullptr, nullptr, f->btmp.p, 1);                          // res0
+  vec(9, f->bbest.p, f->bx.p, nullptr, nullptr, nullptr);
+  sgn::count_launch();
+  k_cond<<<1, 32, 0, cs>>>(S, B, G.max_iters, f->gate.p, h, 1);
+  if (!rc) rc = launch_solve(f, f->btmp.p, f->br.p, flags, cs, gate);                   // r
+  vec(4, f->brh.p, f->br.p, nullptr, nullptr, nullptr);
+  cudaMemsetAsync(f->bp.p, 0, N * sizeof(double), cs);
+  cudaMemsetAsync(f->bv.p, 0, N * sizeof(double), cs);
+  cudaStreamCaptureStatus cst;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaError_t e = cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &ndeps);
+  std::vector<cudaGraphNode_t> leaf(deps, deps + (e == cudaSuccess ? ndeps : 0));
+  cudaGraph_t gout;
+  cudaError_t e2 = cudaStreamEndCapture(cs, &gout);
+  G.k_pro = sgn::launch_count() - before;
+  if (rc || e != cudaSuccess || e2 != cudaSuccess) {
+    cudaStreamDestroy(cs);
+    cudaGraphDestroy(g);
+    if (!rc) { sgn::last_error() = std::string("refinement graph prologue: ") + cudaGetErrorString(e != cudaSuccess ? e : e2); rc = SGN_CUDA_ERROR; }
+    sgn::count_launch(before - sgn::launch_count());
+    return rc;
+  }
+  // ---- WHILE node
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cnode;
+  CUDA_TRY(cudaGraphAddNode(&cnode, g, leaf.data(), leaf.size(), &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  const int64_t before_body = sgn::launch_count();
+  CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  dotF(0, f->brh.p, f->br.p, nullptr, nullptr, nullptr, 2);                             // rho, beta
+  vec(1, f->bp.p, f->br.p, f->bv.p, nullptr, nullptr);                                  // p
+  if (!rc) rc = launch_spmv(f, G.vals, G.vstride, f->bp.p, f->bscr.p, flags, cs, gate);
+  if (!rc) rc = launch_solve(f, f->bscr.p, f->bv.p, flags, cs, gate);                   // v = M^-1 A p
+  dotF(0, f->brh.p, f->bv.p, nullptr, nullptr, nullptr, 3);                             // alpha
+  vec(2, f->bs.p, f->br.p, f->bv.p, nullptr, nullptr);                                  // s
+  if (!rc) rc = launch_spmv(f, G.vals, G.vstride, f->bs.p, f->bscr.p, flags, cs, gate);
+  if (!rc) rc = launch_solve(f, f->bscr.p, f->bt.p, flags, cs, gate);                   // t = M^-1 A s
+  dotF(0, f->bt.p, f->bt.p, f->bt.p, f->bs.p, nullptr, 4);                              // omega
+  vec(3, f->bx.p, f->bp.p, f->bs.p, f->bt.p, f->br.p);                                  // x, r
+  if (!rc) rc = launch_spmv(f, G.vals, G.vstride, f->bx.p, f->bscr.p, flags, cs, gate);
+  dotF(1, f->bb.p, f->bscr.p, nullptr, nullptr, nullptr, 5);                            // true residual
+  vec(7, f->bbest.p, f->bx.p, nullptr, nullptr, nullptr);                               // best copy
+  sgn::count_launch();
+  k_cond<<<1, 32, 0, cs>>>(S, B, G.max_iters, f->gate.p, h, 1);
+  cudaGraph_t bout;
+  e = cudaStreamEndCapture(cs, &bout);
+  G.k_body = sgn::launch_count() - before_body;
+  sgn::count_launch(before - sgn::launch_count());   // captured, not launched
+  cudaStreamDestroy(cs);
+  if (rc || e != cudaSuccess) {
+    cudaGraphDestroy(g);
+    if (!rc) { sgn::last_error() = std::string("refinement graph body: ") + cudaGetErrorString(e); rc = SGN_CUDA_ERROR; }
+    return rc;
+  }
+  CUDA_TRY(cudaGraphInstantiate(&G.exec, g, 0));
+  G.graph = g;
+  return SGN_OK;
+}
+
 int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_stride,
                       const double* d_rhs, double* d_sol, double tol, int32_t max_iters,
                       int32_t flags, double* rel_res, int32_t* iters, void* stream) {
@@ -895,82 +1036,41 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
         (rc = f->bp.alloc(N)) || (rc = f->bv.alloc(N)) || (rc = f->bs.alloc(N)) ||
         (rc = f->bt.alloc(N)) || (rc = f->btmp.alloc(N)) || (rc = f->bbest.alloc(N)) ||
         (rc = f->bb.alloc(N)) || (rc = f->bscr.alloc(N)) ||
-        (rc = f->partial.alloc((size_t)B * kDotBlocks * 2)) || (rc = f->bst.alloc(B)))
+        (rc = f->partial.alloc((size_t)B * kDotBlocks * 2)) || (rc = f->bst.alloc(B)) ||
+        (rc = f->gate.alloc(1)) || (rc = f->dtick.alloc(B)))
       return rc;
+    CUDA_TRY(cudaMemset(f->dtick.p, 0, B * sizeof(int)));
     f->bicg_ready = true;
   }
-  const dim3 vg((unsigned)std::min<int64_t>((n + 255) / 256, 1024), B);
-  const dim3 dg(kDotBlocks, B);
-  BiState* S = f->bst.p;
-  auto dot = [&](const double* a, const double* b2, const double* c, const double* d, int step, int it) {
-    sgn::count_launch();
-    k_dot_partial<<<dg, kDotThreads, 0, st>>>(a, b2, c, d, n, f->partial.p);
-    sgn::count_launch();
-    k_dot_final<<<B, 32, 0, st>>>(f->partial.p, S, step, tol, it);
-  };
-  // vectors: bb = b, bx = x, br = r, brh = r_hat, bp = p, bv = v, bs = s, bt = t,
-  //          btmp = b - A x, bscr = A * (.), bbest = best iterate
+  sgn_factor_s::BicgGraph* G = nullptr;
+  for (auto& g : f->bgraphs)
+    if (g.vals == d_values && g.vstride == values_stride && g.flags == flags && g.tol == tol && g.max_iters == max_iters) G = &g;
+  if (!G) {
+    CUDA_TRY(cudaStreamSynchronize(st));
+    sgn_factor_s::BicgGraph ng;
+    ng.vals = d_values; ng.vstride = values_stride; ng.flags = flags; ng.tol = tol; ng.max_iters = max_iters;
+    if ((rc = build_bicg_graph(f, ng))) return rc;
+    f->bgraphs.push_back(ng);
+    G = &f->bgraphs.back();
+  }
+  // call-specific endpoints stay outside the graph: b in, the selected solution out
   CUDA_TRY(cudaMemcpyAsync(f->bb.p, d_rhs, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
   const sgn::Symbolic& sy = f->sym->s;
   if ((flags & SGN_SOLVE_LEADING) && sy.pair_mode && sy.n_p > 0) {
     for (int b = 0; b < B; ++b)
       CUDA_TRY(cudaMemsetAsync(f->bb.p + (size_t)b * n + sy.n_x, 0, sy.n_p * sizeof(double), st));
   }
-  dot(f->bb.p, f->bb.p, nullptr, nullptr, 0, 0);                                   // bnorm
-  if ((rc = launch_solve(f, f->bb.p, f->bx.p, flags, st))) return rc;              // x0
-  if ((rc = launch_spmv(f, d_values, values_stride, f->bx.p, f->bscr.p, flags, st))) return rc;
+  CUDA_TRY(cudaGraphLaunch(G->exec, st));
+  const dim3 vg((unsigned)std::min<int64_t>((n + 255) / 256, 1024), B);
   sgn::count_launch();
-  k_vec<<<vg, 256, 0, st>>>(0, S, n, f->btmp.p, f->bb.p, f->bscr.p, nullptr, nullptr, nullptr);
-  dot(f->btmp.p, f->btmp.p, nullptr, nullptr, 1, 0);                               // res0
-  sgn::count_launch();
-  k_vec<<<vg, 256, 0, st>>>(9, S, n, f->bbest.p, f->bx.p, nullptr, nullptr, nullptr, nullptr);
-  std::vector<BiState> hs(B);
-  auto read_state = [&]() -> int {
-    CUDA_TRY(cudaMemcpyAsync(hs.data(), S, B * sizeof(BiState), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    return 0;
-  };
-  if ((rc = read_state())) return rc;
-  bool any = false;
-  for (auto& h : hs) any |= (h.active != 0);
-  if (any && max_iters > 0) {
-    if ((rc = launch_solve(f, f->btmp.p, f->br.p, flags, st))) return rc;          // r = M^-1(b-Ax0)
-    sgn::count_launch();
-    k_vec<<<vg, 256, 0, st>>>(4, S, n, f->brh.p, f->br.p, nullptr, nullptr, nullptr, nullptr);
-    CUDA_TRY(cudaMemsetAsync(f->bp.p, 0, N * sizeof(double), st));
-    CUDA_TRY(cudaMemsetAsync(f->bv.p, 0, N * sizeof(double), st));
-    for (int it = 1; it <= max_iters; ++it) {
-      dot(f->brh.p, f->br.p, nullptr, nullptr, 2, it);                             // rho, beta
-      sgn::count_launch();
-      k_vec<<<vg, 256, 0, st>>>(1, S, n, f->bp.p, f->br.p, f->bv.p, nullptr, nullptr, nullptr);
-      if ((rc = launch_spmv(f, d_values, values_stride, f->bp.p, f->bscr.p, flags, st))) return rc;
-      if ((rc = launch_solve(f, f->bscr.p, f->bv.p, flags, st))) return rc;        // v = M^-1 A p
-      dot(f->brh.p, f->bv.p, nullptr, nullptr, 3, it);                             // alpha
-      sgn::count_launch();
-      k_vec<<<vg, 256, 0, st>>>(2, S, n, f->bs.p, f->br.p, f->bv.p, nullptr, nullptr, nullptr);
-      if ((rc = launch_spmv(f, d_values, values_stride, f->bs.p, f->bscr.p, flags, st))) return rc;
-      if ((rc = launch_solve(f, f->bscr.p, f->bt.p, flags, st))) return rc;        // t = M^-1 A s
-      dot(f->bt.p, f->bt.p, f->bt.p, f->bs.p, 4, it);                              // omega
-      sgn::count_launch();
-      k_vec<<<vg, 256, 0, st>>>(3, S, n, f->bx.p, f->bp.p, f->bs.p, f->bt.p, f->br.p, nullptr);
-      if ((rc = launch_spmv(f, d_values, values_stride, f->bx.p, f->bscr.p, flags, st))) return rc;
-      sgn::count_launch();
-      k_vec<<<vg, 256, 0, st>>>(0, S, n, f->btmp.p, f->bb.p, f->bscr.p, nullptr, nullptr, nullptr);
-      dot(f->btmp.p, f->btmp.p, nullptr, nullptr, 5, it);                          // true residual
-      sgn::count_launch();
-      k_vec<<<vg, 256, 0, st>>>(7, S, n, f->bbest.p, f->bx.p, nullptr, nullptr, nullptr, nullptr);
-      sgn::count_launch();
-      k_clear_reason<<<B, 32, 0, st>>>(S);
-      if ((rc = read_state())) return rc;
-      bool act = false;
-      for (auto& h : hs) act |= (h.active != 0);
-      if (!act) break;
-    }
-  }
-  sgn::count_launch();
-  k_select<<<vg, 256, 0, st>>>(S, n, f->bx.p, f->bbest.p, d_sol);
+  k_select<<<vg, 256, 0, st>>>(f->bst.p, n, f->bx.p, f->bbest.p, d_sol);
   CUDA_TRY(cudaGetLastError());
-  if ((rc = read_state())) return rc;
+  std::vector<BiState> hs(B);
+  CUDA_TRY(cudaMemcpyAsync(hs.data(), f->bst.p, B * sizeof(BiState), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  int32_t max_cur = 0;
+  for (auto& h : hs) max_cur = std::max(max_cur, h.cur);
+  sgn::count_launch(G->k_pro + G->k_body * (int64_t)max_cur);
   bool fail = false;
   for (int b = 0; b < B; ++b) {
     const BiState& h = hs[b];
