@@ -314,9 +314,11 @@ def run_ours(args):
                    "tree_levels": st["n_levels"]},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * (pl.n_x + pl.n_p),
                 "d2h_bytes_per_step": 8 * pl.dim},
-        "roofline": {"bound": "tensor", "kernel": "factorization (k_assemble+k_panel+k_update, DMMA)",
+        "roofline": {"bound": "tensor", "kernel": "k_factor_dag (persistent multifrontal LDL^T, DMMA Schur tiles)",
                      "achieved": achieved_tf, "peak": dm.value, "unit": "TFLOP/s",
-                     "frac": achieved_tf / dm.value if dm.value else None, "traffic": None,
+                     "frac": achieved_tf / dm.value if dm.value else None,
+                     "traffic": ncu_traffic(args.config).get("dram_bytes"),
+                     "traffic_source": ncu_traffic(args.config).get("source"),
                      "peak_source": "sgn_fp64_peak DMMA microbenchmark, same run (no FP64 entry in MEASURED_PEAKS.json)",
                      "flops_per_launch_group": flops, "ms": f_ms},
         "phases": {
@@ -350,6 +352,16 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def ncu_traffic(config):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one k_factor_dag launch from the committed
+    ncu --set full capture summary (profiles/ncu_traffic.json), or {} when none was taken."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh).get(str(config), {})
+    except (OSError, ValueError):
+        return {}
 
 
 def run_batch(args):

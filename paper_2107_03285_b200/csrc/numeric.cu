@@ -928,7 +928,10 @@ int sgn_spmv(sgn_factor f, const double* d_values, int64_t values_stride, const 
 // WHILE conditional node whose body is one iteration; k_cond sets the condition from the
 // per-instance state, and the gated solves / SpMVs of a finished refinement return at once.
 // One host synchronisation per call.
-static int build_bicg_graph(sgn_factor f, sgn_factor_s::BicgGraph& G) {
+// Issue the refinement prologue (phase 0) or one iteration (phase 1) on stream cs; the
+// graph path captures these, the host-driven path (SGN_BICG_GRAPH=0) launches them.
+static int issue_bicg(sgn_factor f, const sgn_factor_s::BicgGraph& G, int phase, cudaStream_t cs,
+                      cudaGraphConditionalHandle h, int set_handle) {
   const int64_t n = f->n;
   const int B = f->batch;
   const size_t N = (size_t)B * std::max<int64_t>(n, 1);
@@ -938,13 +941,6 @@ static int build_bicg_graph(sgn_factor f, sgn_factor_s::BicgGraph& G) {
   const double tol = G.tol;
   const int32_t flags = G.flags;
   const int* gate = f->gate.p;
-  cudaStream_t cs;
-  CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  cudaGraph_t g;
-  CUDA_TRY(cudaGraphCreate(&g, 0));
-  cudaGraphConditionalHandle h;
-  CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
-  const int64_t before = sgn::launch_count();
   auto dotF = [&](int mode, const double* a, const double* b2, const double* c, const double* d, double* out, int step) {
     sgn::count_launch();
     k_dotF<<<dg, kDotThreads, 0, cs>>>(mode, a, b2, c, d, out, n, f->partial.p, f->dtick.p, S, step, tol);
@@ -954,19 +950,48 @@ static int build_bicg_graph(sgn_factor f, sgn_factor_s::BicgGraph& G) {
     k_vec<<<vg, 256, 0, cs>>>(mode, S, n, o, x, y, z, o2, nullptr);
   };
   int rc = SGN_OK;
-  // ---- prologue: x0 = M^-1 b, res0, r = M^-1 (b - A x0), r_hat = r, p = v = 0
+  if (phase == 0) {   // x0 = M^-1 b, res0, r = M^-1 (b - A x0), r_hat = r, p = v = 0
+    dotF(0, f->bb.p, f->bb.p, nullptr, nullptr, nullptr, 0);                            // bnorm
+    if (!rc) rc = launch_solve(f, f->bb.p, f->bx.p, flags, cs);                         // x0
+    if (!rc) rc = launch_spmv(f, G.vals, G.vstride, f->bx.p, f->bscr.p, flags, cs);
+    dotF(1, f->bb.p, f->bscr.p, nullptr, nullptr, f->btmp.p, 1);                        // res0
+    vec(9, f->bbest.p, f->bx.p, nullptr, nullptr, nullptr);
+    sgn::count_launch();
+    k_cond<<<1, 32, 0, cs>>>(S, B, G.max_iters, f->gate.p, h, set_handle);
+    if (!rc) rc = launch_solve(f, f->btmp.p, f->br.p, flags, cs, gate);                 // r
+    vec(4, f->brh.p, f->br.p, nullptr, nullptr, nullptr);
+    cudaMemsetAsync(f->bp.p, 0, N * sizeof(double), cs);
+    cudaMemsetAsync(f->bv.p, 0, N * sizeof(double), cs);
+  } else {
+    dotF(0, f->brh.p, f->br.p, nullptr, nullptr, nullptr, 2);                           // rho, beta
+    vec(1, f->bp.p, f->br.p, f->bv.p, nullptr, nullptr);                                // p
+    if (!rc) rc = launch_spmv(f, G.vals, G.vstride, f->bp.p, f->bscr.p, flags, cs, gate);
+    if (!rc) rc = launch_solve(f, f->bscr.p, f->bv.p, flags, cs, gate);                 // v = M^-1 A p
+    dotF(0, f->brh.p, f->bv.p, nullptr, nullptr, nullptr, 3);                           // alpha
+    vec(2, f->bs.p, f->br.p, f->bv.p, nullptr, nullptr);                                // s
+    if (!rc) rc = launch_spmv(f, G.vals, G.vstride, f->bs.p, f->bscr.p, flags, cs, gate);
+    if (!rc) rc = launch_solve(f, f->bscr.p, f->bt.p, flags, cs, gate);                 // t = M^-1 A s
+    dotF(0, f->bt.p, f->bt.p, f->bt.p, f->bs.p, nullptr, 4);                            // omega
+    vec(3, f->bx.p, f->bp.p, f->bs.p, f->bt.p, f->br.p);                                // x, r
+    if (!rc) rc = launch_spmv(f, G.vals, G.vstride, f->bx.p, f->bscr.p, flags, cs, gate);
+    dotF(1, f->bb.p, f->bscr.p, nullptr, nullptr, nullptr, 5);                          // true residual
+    vec(7, f->bbest.p, f->bx.p, nullptr, nullptr, nullptr);                             // best copy
+    sgn::count_launch();
+    k_cond<<<1, 32, 0, cs>>>(S, B, G.max_iters, f->gate.p, h, set_handle);
+  }
+  return rc;
+}
+
+static int build_bicg_graph(sgn_factor f, sgn_factor_s::BicgGraph& G) {
+  cudaStream_t cs;
+  CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  CUDA_TRY(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+  const int64_t before = sgn::launch_count();
   CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  dotF(0, f->bb.p, f->bb.p, nullptr, nullptr, nullptr, 0);                              // bnorm
-  if (!rc) rc = launch_solve(f, f->bb.p, f->bx.p, flags, cs);                           // x0
-  if (!rc) rc = launch_spmv(f, G.vals, G.vstride, f->bx.p, f->bscr.p, flags, cs);
-  dotF(1, f->bb.p, f->bscr.p, nullptr, nullptr, f->btmp.p, 1);                          // res0
-  vec(9, f->bbest.p, f->bx.p, nullptr, nullptr, nullptr);
-  sgn::count_launch();
-  k_cond<<<1, 32, 0, cs>>>(S, B, G.max_iters, f->gate.p, h, 1);
-  if (!rc) rc = launch_solve(f, f->btmp.p, f->br.p, flags, cs, gate);                   // r
-  vec(4, f->brh.p, f->br.p, nullptr, nullptr, nullptr);
-  cudaMemsetAsync(f->bp.p, 0, N * sizeof(double), cs);
-  cudaMemsetAsync(f->bv.p, 0, N * sizeof(double), cs);
+  int rc = issue_bicg(f, G, 0, cs, h, 1);
   cudaStreamCaptureStatus cst;
   const cudaGraphNode_t* deps = nullptr;
   size_t ndeps = 0;
@@ -978,11 +1003,10 @@ static int build_bicg_graph(sgn_factor f, sgn_factor_s::BicgGraph& G) {
   if (rc || e != cudaSuccess || e2 != cudaSuccess) {
     cudaStreamDestroy(cs);
     cudaGraphDestroy(g);
-    if (!rc) { sgn::last_error() = std::string("refinement graph prologue: ") + cudaGetErrorString(e != cudaSuccess ? e : e2); rc = SGN_CUDA_ERROR; }
     sgn::count_launch(before - sgn::launch_count());
+    if (!rc) { sgn::last_error() = std::string("refinement graph prologue: ") + cudaGetErrorString(e != cudaSuccess ? e : e2); rc = SGN_CUDA_ERROR; }
     return rc;
   }
-  // ---- WHILE node
   cudaGraphNodeParams cp = {};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = h;
@@ -993,21 +1017,7 @@ static int build_bicg_graph(sgn_factor f, sgn_factor_s::BicgGraph& G) {
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   const int64_t before_body = sgn::launch_count();
   CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  dotF(0, f->brh.p, f->br.p, nullptr, nullptr, nullptr, 2);                             // rho, beta
-  vec(1, f->bp.p, f->br.p, f->bv.p, nullptr, nullptr);                                  // p
-  if (!rc) rc = launch_spmv(f, G.vals, G.vstride, f->bp.p, f->bscr.p, flags, cs, gate);
-  if (!rc) rc = launch_solve(f, f->bscr.p, f->bv.p, flags, cs, gate);                   // v = M^-1 A p
-  dotF(0, f->brh.p, f->bv.p, nullptr, nullptr, nullptr, 3);                             // alpha
-  vec(2, f->bs.p, f->br.p, f->bv.p, nullptr, nullptr);                                  // s
-  if (!rc) rc = launch_spmv(f, G.vals, G.vstride, f->bs.p, f->bscr.p, flags, cs, gate);
-  if (!rc) rc = launch_solve(f, f->bscr.p, f->bt.p, flags, cs, gate);                   // t = M^-1 A s
-  dotF(0, f->bt.p, f->bt.p, f->bt.p, f->bs.p, nullptr, 4);                              // omega
-  vec(3, f->bx.p, f->bp.p, f->bs.p, f->bt.p, f->br.p);                                  // x, r
-  if (!rc) rc = launch_spmv(f, G.vals, G.vstride, f->bx.p, f->bscr.p, flags, cs, gate);
-  dotF(1, f->bb.p, f->bscr.p, nullptr, nullptr, nullptr, 5);                            // true residual
-  vec(7, f->bbest.p, f->bx.p, nullptr, nullptr, nullptr);                               // best copy
-  sgn::count_launch();
-  k_cond<<<1, 32, 0, cs>>>(S, B, G.max_iters, f->gate.p, h, 1);
+  rc = issue_bicg(f, G, 1, cs, h, 1);
   cudaGraph_t bout;
   e = cudaStreamEndCapture(cs, &bout);
   G.k_body = sgn::launch_count() - before_body;
@@ -1021,6 +1031,11 @@ static int build_bicg_graph(sgn_factor f, sgn_factor_s::BicgGraph& G) {
   CUDA_TRY(cudaGraphInstantiate(&G.exec, g, 0));
   G.graph = g;
   return SGN_OK;
+}
+
+static bool bicg_use_graph() {
+  static const int v = [] { const char* e = getenv("SGN_BICG_GRAPH"); return (e && *e == '0') ? 0 : 1; }();
+  return v != 0;
 }
 
 int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_stride,
@@ -1043,9 +1058,13 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
     f->bicg_ready = true;
   }
   sgn_factor_s::BicgGraph* G = nullptr;
+  sgn_factor_s::BicgGraph hostG;   // host-driven loop (SGN_BICG_GRAPH=0, e.g. for complete ncu launch lists)
+  hostG.vals = d_values; hostG.vstride = values_stride; hostG.flags = flags; hostG.tol = tol; hostG.max_iters = max_iters;
+  const bool use_graph = bicg_use_graph();
   for (auto& g : f->bgraphs)
     if (g.vals == d_values && g.vstride == values_stride && g.flags == flags && g.tol == tol && g.max_iters == max_iters) G = &g;
-  if (!G) {
+  if (!use_graph) G = &hostG;
+  else if (!G) {
     CUDA_TRY(cudaStreamSynchronize(st));
     sgn_factor_s::BicgGraph ng;
     ng.vals = d_values; ng.vstride = values_stride; ng.flags = flags; ng.tol = tol; ng.max_iters = max_iters;
@@ -1060,7 +1079,19 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
     for (int b = 0; b < B; ++b)
       CUDA_TRY(cudaMemsetAsync(f->bb.p + (size_t)b * n + sy.n_x, 0, sy.n_p * sizeof(double), st));
   }
-  CUDA_TRY(cudaGraphLaunch(G->exec, st));
+  if (use_graph) {
+    CUDA_TRY(cudaGraphLaunch(G->exec, st));
+  } else {
+    cudaGraphConditionalHandle none = 0;
+    if ((rc = issue_bicg(f, *G, 0, st, none, 0))) return rc;
+    for (int it = 0; it < max_iters; ++it) {
+      int any = 0;
+      CUDA_TRY(cudaMemcpyAsync(&any, f->gate.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      if (!any) break;
+      if ((rc = issue_bicg(f, *G, 1, st, none, 0))) return rc;
+    }
+  }
   const dim3 vg((unsigned)std::min<int64_t>((n + 255) / 256, 1024), B);
   sgn::count_launch();
   k_select<<<vg, 256, 0, st>>>(f->bst.p, n, f->bx.p, f->bbest.p, d_sol);
@@ -1068,9 +1099,11 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
   std::vector<BiState> hs(B);
   CUDA_TRY(cudaMemcpyAsync(hs.data(), f->bst.p, B * sizeof(BiState), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  int32_t max_cur = 0;
-  for (auto& h : hs) max_cur = std::max(max_cur, h.cur);
-  sgn::count_launch(G->k_pro + G->k_body * (int64_t)max_cur);
+  if (use_graph) {
+    int32_t max_cur = 0;
+    for (auto& h : hs) max_cur = std::max(max_cur, h.cur);
+    sgn::count_launch(G->k_pro + G->k_body * (int64_t)max_cur);
+  }
   bool fail = false;
   for (int b = 0; b < B; ++b) {
     const BiState& h = hs[b];

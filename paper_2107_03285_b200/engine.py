@@ -469,10 +469,14 @@ class DeviceEngine:
         pl = self.plan
         if not hasattr(self, "_diag_ptr"):
             T = lambda a, dt: self.torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device="cuda")
-            self._diag_ptr = T(np.array([0, pl.G_diag.size]), self.torch.int64)
+            self._diag_ptr = T(np.arange(pl.G_diag.size + 1), self.torch.int64)
             self._diag_idx = T(pl.G_diag, self.torch.int64)
-        self._gather(1, None, 0, self._diag_ptr, self._diag_idx, None, self.gvals, pl.G_nnz,
-                     self.scal[2], 1)
+            self._diag_buf = self.torch.empty((self.batch, pl.G_diag.size), dtype=self.torch.float64, device="cuda")
+        n = int(pl.G_diag.size)
+        self._gather(n, None, 0, self._diag_ptr, self._diag_idx, None, self.gvals, pl.G_nnz,
+                     self._diag_buf, n)                         # one thread per diagonal entry
+        check(lib().sgn_reduce(0, n, self.batch, ptr(self._diag_buf), None, n, ptr(self.scal[2]),
+                               _lib.stream_handle()))           # fixed-tree sum
         return self.scal[2].cpu().numpy()
 
     def _mask(self, m):
