@@ -587,6 +587,29 @@ class DeviceEngine:
         return ok
 
 
+def kkt_inverse_p(eng, rhs_p, factor: bool):
+    """Solve the stabilized-then-refined SGN KKT system with right-hand side (0, rhs_p, 0)
+    on the device (the initial inverse Hessian of L-BFGS-SGN, optimize.py:446-450).
+
+    factor=True (re)factors the KKT values first (assembled by the caller).  Returns the
+    host solution and (rel_res, iters) of instance 0.
+    """
+    st = _lib.stream_handle()
+    n_x, n_p = eng.n_x, eng.n_p
+    if factor:
+        eng.kfac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda, st)
+        eng.kfac.check(st)
+    eng.rhs.zero_()
+    eng.rhs[0, n_x:n_x + n_p].copy_(eng.torch.from_numpy(np.ascontiguousarray(rhs_p, dtype=np.float64)))
+    rc, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, eng.stab.refine_tolerance,
+                                          eng.stab.max_refine_iters, False, st)
+    sol = eng.sol[0].cpu().numpy()
+    if rc == _lib.SGN_NO_CONVERGENCE:
+        raise NoConvergence(f"BiCGSTAB refinement stalled at relative residual {res.max():.3e}",
+                            residual=float(res.max()), iterations=int(its.max()), best=sol)
+    return sol, float(res[0]), int(its[0])
+
+
 class HostKKT:
     """Device solve stages for a KKT assembled on the host by a plugin problem.
 

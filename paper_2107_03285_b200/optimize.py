@@ -24,7 +24,7 @@ from .sensitivity import _host_kkt, _is_device_problem, adjoint_gradient
 __all__ = ["METHODS", "CSV_HEADER", "OptimizerConfig", "SearchDirection", "IterationRecord",
            "OptimizerRun", "direction_sgn", "minimize", "project_direction_bounds"]
 
-METHODS = ("sgn",)
+METHODS = ("sgn", "lbfgs", "lbfgs_sgn")
 CSV_HEADER = "iter,f,grad_norm,step_len,dir_time_s,fwd_time_s,elapsed_s,lin_rel_residual"
 
 
@@ -144,6 +144,86 @@ def direction_sgn(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirectio
 _DIRECTION_FUNCS = {"sgn": direction_sgn}
 
 
+def direction_lbfgs(history, grad: np.ndarray, apply_h0=None) -> np.ndarray:
+    """L-BFGS two-loop recursion, returning -H grad (reference optimize.py:310-335).
+
+    ``history``: (s, y, rho) triples, oldest first; ``apply_h0`` maps a vector through the
+    initial inverse Hessian (default gamma I, gamma = s.y / y.y of the newest pair, 1 when
+    the history is empty).  n_p-length host vectors: the expensive part of L-BFGS-SGN is
+    ``apply_h0`` (a device KKT solve).
+    """
+    q = np.asarray(grad, dtype=np.float64).copy()
+    alphas = []
+    for s, y, rho in reversed(history):
+        a = rho * (s @ q)
+        alphas.append(a)
+        q -= a * y
+    if apply_h0 is None:
+        gamma = 1.0
+        if history:
+            s, y, _ = history[-1]
+            gamma = (s @ y) / (y @ y)
+        r = gamma * q
+    else:
+        r = apply_h0(q)
+    for (s, y, rho), a in zip(history, reversed(alphas)):
+        b = rho * (y @ r)
+        r += s * (a - b)
+    return -r
+
+
+def _direction_lbfgs_sgn(prob, x, p, cfg: OptimizerConfig, g, history) -> SearchDirection:
+    """Two-loop recursion whose initial inverse Hessian is the sparse Gauss-Newton solve
+    (reference optimize.py:433-457): H0^{-1} q = -(dp slot of K^{-1} (0, -q, 0)).  The KKT is
+    assembled and factored once per direction on the device; an empty history reproduces
+    ``direction_sgn`` bitwise (reference checks.py:213-226)."""
+    from .engine import kkt_inverse_p
+    t0 = time.perf_counter()
+    if _is_device_problem(prob):
+        eng = prob.engine
+        eng.stab = cfg.stabilization
+        prob._load(x, p)
+        eng.assemble()
+    else:
+        eng, _ = _host_kkt(prob, x, p)
+        eng.stab = cfg.stabilization
+    eng.torch.cuda.synchronize()
+    assemble_s = time.perf_counter() - t0
+    reports = []
+    n_x, n_p = prob.n_x, prob.n_p
+
+    def apply_h0(q):
+        t1 = time.perf_counter()
+        sol, res, its = kkt_inverse_p(eng, -np.asarray(q, dtype=np.float64), factor=not reports)
+        reports.append((res, its, time.perf_counter() - t1))
+        return -sol[n_x:n_x + n_p]
+
+    dp = direction_lbfgs(history, g, apply_h0)
+    res, its, solve_s = reports[-1]
+    return SearchDirection(dp=dp, assemble_s=assemble_s, solve_s=solve_s, relative_residual=res,
+                           extra={"refine_iterations": its})
+
+
+def _compute_direction(prob, x, p, cfg: OptimizerConfig, g, history) -> SearchDirection:
+    """Method dispatch of the outer loop (reference optimize.py:423-430)."""
+    if cfg.method == "lbfgs":
+        t0 = time.perf_counter()
+        dp = direction_lbfgs(history, g)
+        return SearchDirection(dp=dp, assemble_s=time.perf_counter() - t0)
+    if cfg.method == "lbfgs_sgn":
+        return _direction_lbfgs_sgn(prob, x, p, cfg, g, history)
+    return _DIRECTION_FUNCS[cfg.method](prob, x, p, cfg, grad=g)
+
+
+def _push_history(history, s, y, cap):
+    """Curvature-guarded history update (reference optimize.py:460-465)."""
+    sy = float(s @ y)
+    if sy > 1e-12 * np.linalg.norm(s) * np.linalg.norm(y):
+        history.append((s, y, 1.0 / sy))
+        if len(history) > cap:
+            history.pop(0)
+
+
 def _line_search(prob, p, x, f, g, dp, bounds, cfg):
     """Armijo backtracking over forward solves (optimize.py:468-488)."""
     alpha = 1.0
@@ -187,13 +267,14 @@ def minimize(prob, p0, cfg: OptimizerConfig) -> OptimizerRun:
     g = adjoint_gradient(prob, x, p)
     records = [IterationRecord(0, f, float(np.linalg.norm(g)), 0.0, 0.0, fwd_time,
                                time.perf_counter() - t_start, float("nan"))]
+    history = []
     termination = "max_iterations"
     for it in range(1, cfg.max_iterations + 1):
         if np.linalg.norm(g) <= cfg.gradient_tolerance:
             termination = "gradient_tolerance"
             break
         t0 = time.perf_counter()
-        sd = _DIRECTION_FUNCS[cfg.method](prob, x, p, cfg, grad=g)
+        sd = _compute_direction(prob, x, p, cfg, g, history)
         dir_time = time.perf_counter() - t0
         dp = sd.dp
         if bounds is not None:
@@ -210,8 +291,10 @@ def minimize(prob, p0, cfg: OptimizerConfig) -> OptimizerRun:
         if not accepted:
             termination = "line_search_failure"
             break
-        g = adjoint_gradient(prob, x_new, p_new)
-        p, x, f = p_new, x_new, f_new
+        g_new = adjoint_gradient(prob, x_new, p_new)
+        if cfg.method in ("lbfgs", "lbfgs_sgn"):
+            _push_history(history, p_new - p, g_new - g, cfg.lbfgs_history)
+        p, x, f, g = p_new, x_new, f_new, g_new
         records.append(IterationRecord(it, f, float(np.linalg.norm(g)), alpha, dir_time, fwd_time,
                                        time.perf_counter() - t_start, sd.relative_residual))
     return OptimizerRun(method=cfg.method, records=records, termination=termination, p=p, x=x)

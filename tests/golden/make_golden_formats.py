@@ -1,0 +1,61 @@
+"""Golden on-disk formats written by the REAL reference (run in the build container).
+
+    python tests/golden/make_golden_formats.py
+
+* ref_kkt_spring_bar_5x3/kkt.mtx + stats.json -- the reference's cmd_kkt_dump output for the
+  spring bar 5x3 (cli.py:284-305; write_matrix_market, sparse.py:192-199)
+* ref_convergence_sgn_5x3.csv -- OptimizerRun.write_csv of a 4-iteration reference minimize
+  ('sgn') on the same problem (optimize.py:60,112-137)
+* ref_lbfgs_11x3.npz -- f / |g| / p trajectories of the reference minimize with 'lbfgs_sgn'
+  (optimize.py:433-457) and 'lbfgs' on the spring bar 11x3, 6 iterations
+The GPU path must emit the same schemas.
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+from make_golden import import_reference  # noqa: E402
+
+
+def main():
+    import_reference()
+    from sgnopt.optimize import OptimizerConfig, minimize
+    from sgnopt.linear_solvers import factor_sparse
+    from sgnopt.problems import build_spring_bar
+    from sgnopt.sensitivity import assemble_sgn, gn_blocks
+    from sgnopt.sparse import write_matrix_market
+    prob = build_spring_bar(5, 3)
+    p = prob.default_parameters()
+    x = prob.simulate(p)
+    kkt = assemble_sgn(prob, x, p, gn_blocks(prob, x, p))
+    out = os.path.join(HERE, "ref_kkt_spring_bar_5x3")
+    os.makedirs(out, exist_ok=True)
+    write_matrix_market(kkt.matrix, os.path.join(out, "kkt.mtx"))
+    stats = {"problem": "spring_bar", "dimension": kkt.matrix.rows, "n_x": kkt.n_x, "n_p": kkt.n_p,
+             "nnz": kkt.matrix.nnz, "factor_fill_nnz": factor_sparse(kkt.matrix).fill_nnz}
+    with open(os.path.join(out, "stats.json"), "w", encoding="utf-8") as fh:
+        json.dump(stats, fh, indent=2)
+    prob = build_spring_bar(5, 3)
+    run = minimize(prob, prob.default_parameters(),
+                   OptimizerConfig(method="sgn", max_iterations=4, gradient_tolerance=1e-12))
+    run.write_csv(os.path.join(HERE, "ref_convergence_sgn_5x3.csv"))
+    # SGN-initialised L-BFGS and plain L-BFGS trajectories
+    import numpy as np
+    traj = {}
+    for method in ("lbfgs_sgn", "lbfgs"):
+        prob = build_spring_bar(11, 3)
+        run = minimize(prob, prob.default_parameters(),
+                       OptimizerConfig(method=method, max_iterations=6, gradient_tolerance=1e-12))
+        traj[f"{method}_f"] = run.f_values()
+        traj[f"{method}_g"] = run.grad_norms()
+        traj[f"{method}_p"] = run.p
+    np.savez(os.path.join(HERE, "ref_lbfgs_11x3.npz"), **traj)
+    print("wrote", out, "ref_convergence_sgn_5x3.csv and ref_lbfgs_11x3.npz")
+
+
+if __name__ == "__main__":
+    main()
