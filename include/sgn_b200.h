@@ -116,6 +116,13 @@ int  sgn_debug_solve_trace(sgn_factor f, int64_t* out, int64_t cap, int64_t* n_t
  * ready, end ns; smid; 4 sub-phase ns or 0); meta: 6 int32 per task (kind, step, front,
  * level, a, b).                                                                        */
 int  sgn_debug_factor_trace(sgn_factor f, int64_t* out, int64_t cap, int64_t* n_tasks, int32_t* meta);
+/* Diagnostics: copy one internal buffer of a factor to the host (which: 0 fronts store,
+ * 1 solve panels, 2 pivot-block scratch, 3 front table, 4 factor tasks, 5 solve tasks,
+ * 6/7 gather map, 8 permutation, 9 tickets, 10 struct rows, 11 rel tile ranges).     */
+int  sgn_debug_factor_buffer(sgn_factor f, int32_t which, void* out, int64_t cap_bytes, int64_t* size_bytes);
+/* Diagnostics: fill the fronts, solve panels, pivot scratch and solve scratch with `value`
+ * (tests use NaN to prove no kernel reads memory it has not written).                   */
+int  sgn_debug_poison(sgn_factor f, double value);
 
 /* y = K x on the full symmetric CSC pattern (which equals its CSR).  Replaces the
  * scipy SpMV of _relative_residual / _bicgstab_refine (linear_solvers.py:105-108,178-211).

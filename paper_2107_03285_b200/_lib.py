@@ -50,6 +50,8 @@ SIGNATURES = {
     "sgn_factor_solve": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
     "sgn_debug_solve_trace": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_vp, c_vp]),
     "sgn_debug_factor_trace": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_vp, c_vp]),
+    "sgn_debug_factor_buffer": (ctypes.c_int, [c_vp, c_i32, c_vp, ctypes.c_int64, c_vp]),
+    "sgn_debug_poison": (ctypes.c_int, [c_vp, c_dbl]),
     "sgn_factor_destroy": (None, [c_vp]),
     "sgn_spmv": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp]),
     "sgn_solve_refined": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_dbl, c_i32, c_i32,

@@ -434,7 +434,9 @@ __device__ void f_ztask_pre(const sgn::FactorArgs& A, const DFront& F, int b, in
     for (int u = 0; u < 8; ++u) {
       const int e = tid + u * kFThreads;
       const int r = e & 31, c = e >> 5;
-      vz[u] = (r < nr) ? __ldcg(Zm + (int64_t)(k0 + c) * ld + r0 + r) : 0.0;                 // Z[r0 + r, k0 + c]
+      // Z[r0 + r, k0 + c]: mask the columns past npiv too -- they lie outside this front's Z
+      // storage, and 0 (L11 padding) x NaN (whatever is there) would poison the block
+      vz[u] = (r < nr && k0 + c < npiv) ? __ldcg(Zm + (int64_t)(k0 + c) * ld + r0 + r) : 0.0;
       vl[u] = (k0 + r < npiv && c < wb) ? __ldcg(Fm + (int64_t)(c0 + c) * ld + k0 + r) : 0.0; // L11[k0 + r, c0 + c]
     }
 #pragma unroll

@@ -806,6 +806,10 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
   CUDA_TRY(cudaMemset(f->tickets.p, 0, f->tickets.n * sizeof(int)));
   // Z11 = L11^{-1} is lower triangular: the strictly upper part stays zero forever
   CUDA_TRY(cudaMemset(f->zstore.p, 0, f->zstore.n * sizeof(double)));
+  // cudaMemset runs on the legacy default stream and may still be in flight; callers may
+  // use the factor from non-blocking streams (torch side streams) that are NOT ordered
+  // after it, so the zeroed tickets / Z storage must be complete before returning.
+  CUDA_TRY(cudaDeviceSynchronize());
   *out = f.release();
   return SGN_OK;
 }
@@ -907,6 +911,45 @@ int sgn_debug_factor_trace(sgn_factor f, int64_t* out, int64_t cap, int64_t* n_t
   if (out && f->ftrace.p) {
     const int64_t m = std::min<int64_t>(cap, 8 * nt);
     CUDA_TRY(cudaMemcpy(out, f->ftrace.p, m * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  }
+  return SGN_OK;
+}
+
+// fill every buffer a factorization / solve must write before reading with `value`
+__global__ void k_fill(double* p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+int sgn_debug_poison(sgn_factor f, double value) {
+  DevBuf<double>* bufs[] = {&f->fstore, &f->zstore, &f->dscr, &f->ubuf, &f->zbuf, &f->xbuf, &f->part};
+  for (auto* b : bufs)
+    if (b->p && b->n) k_fill<<<1024, 256>>>(b->p, (int64_t)b->n, value);
+  CUDA_TRY(cudaDeviceSynchronize());
+  return SGN_OK;
+}
+
+int sgn_debug_factor_buffer(sgn_factor f, int32_t which, void* out, int64_t cap_bytes, int64_t* size_bytes) {
+  const void* src = nullptr;
+  size_t bytes = 0;
+  switch (which) {
+    case 0: src = f->fstore.p; bytes = f->fstore.n * sizeof(double); break;
+    case 1: src = f->zstore.p; bytes = f->zstore.n * sizeof(double); break;
+    case 2: src = f->dscr.p; bytes = f->dscr.n * sizeof(double); break;
+    case 3: src = f->fronts.p; bytes = f->fronts.n * sizeof(DFront); break;
+    case 4: src = f->ftasks.p; bytes = f->ftasks.n * sizeof(sgn::FTask); break;
+    case 5: src = f->stasks.p; bytes = f->stasks.n * sizeof(sgn::Task); break;
+    case 6: src = f->gptr.p; bytes = f->gptr.n * sizeof(int64_t); break;
+    case 7: src = f->gsrc.p; bytes = f->gsrc.n * sizeof(int32_t); break;
+    case 8: src = f->perm.p; bytes = f->perm.n * sizeof(int64_t); break;
+    case 9: src = f->tickets.p; bytes = f->tickets.n * sizeof(int); break;
+    case 10: src = f->srows.p; bytes = f->srows.n * sizeof(int64_t); break;
+    case 11: src = f->reltile.p; bytes = f->reltile.n * sizeof(int32_t); break;
+    default: sgn::last_error() = "unknown buffer"; return SGN_INVALID;
+  }
+  if (size_bytes) *size_bytes = (int64_t)bytes;
+  if (out && src) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(out, src, std::min<size_t>(bytes, (size_t)cap_bytes), cudaMemcpyDeviceToHost));
   }
   return SGN_OK;
 }
@@ -1054,7 +1097,7 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
         (rc = f->partial.alloc((size_t)B * kDotBlocks * 2)) || (rc = f->bst.alloc(B)) ||
         (rc = f->gate.alloc(1)) || (rc = f->dtick.alloc(B)))
       return rc;
-    CUDA_TRY(cudaMemset(f->dtick.p, 0, B * sizeof(int)));
+    CUDA_TRY(cudaMemsetAsync(f->dtick.p, 0, B * sizeof(int), st));   // ordered on the caller's stream
     f->bicg_ready = true;
   }
   sgn_factor_s::BicgGraph* G = nullptr;

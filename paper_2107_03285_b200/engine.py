@@ -20,6 +20,7 @@ Newton with energy backtracking (forward.py:135-203) on the same element kernels
 from __future__ import annotations
 
 import math
+import os
 import time
 
 import numpy as np
@@ -211,6 +212,23 @@ class MeshPlan:
         self.grad_base = self.f_ext[self.free_dofs].copy()
 
 
+_SIDE_STREAM = os.environ.get("SGN_SIDE_STREAM", "1") != "0"
+_DEBUG_NAN = os.environ.get("SGN_DEBUG_NAN", "0") == "1"
+
+
+def _nan_probe(eng, where):
+    """Diagnostics only (SGN_DEBUG_NAN=1): report the first non-finite device buffer."""
+    if not _DEBUG_NAN:
+        return
+    eng.torch.cuda.synchronize()
+    for name in ("kvals", "fvec", "gvals", "tmp", "rhs", "grad", "sol", "x", "p"):
+        t = getattr(eng, name, None)
+        if t is not None and not bool(eng.torch.isfinite(t).all()):
+            import sys
+            print(f"[nan-probe] {where}: {name} non-finite ({int((~eng.torch.isfinite(t)).sum())} entries)",
+                  file=sys.stderr, flush=True)
+
+
 def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = True, events=None):
     """factor -> adjoint gradient -> refined KKT solve on an object exposing
     kfac, kvals, fvec, sol_adj, tmp, rhs, sol, grad, batch, n_x, n_p, stab.
@@ -220,40 +238,89 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
     """
     st = _lib.stream_handle()
     n_x, n_p = eng.n_x, eng.n_p
-    t1 = time.perf_counter()
-    eng.kfac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda, st)
-    if events is not None:
-        events[0].record()
-    eng.kfac.check(st)
-    t2 = time.perf_counter()
-    if timings is not None:
-        timings["factor_s"] = t2 - t1
     tol, mi = eng.stab.refine_tolerance, eng.stab.max_refine_iters
-    if getattr(eng, "adjoint_gx", False):
-        # lambda = -G_x^{-T} f_x by a direct LDL^T of G_x, as the reference does with its LU
-        # of dc/dx (sensitivity.py:160-191); device problems have symmetric G_x
-        res_a, it_a = eng.adjoint_direct()
+    torch = eng.torch
+    cur = torch.cuda.current_stream()
+    t1 = time.perf_counter()
+    if getattr(eng, "adjoint_gx", False) and _SIDE_STREAM:
+        # The adjoint (G_x factor + solve, reference sensitivity.py:160-198) does not depend
+        # on the KKT factor: it runs on a side stream.  The KKT factorization's persistent
+        # CTAs retire once its task list is taken, so the G_x launch fills the SMs its
+        # dependency-chain tail leaves idle.  Zero-pivot checks of both factors follow the
+        # refined solve (still before any convergence error, as in the reference).
+        if not hasattr(eng, "_side_stream"):
+            eng._side_stream = torch.cuda.Stream()
+        side = eng._side_stream
+        ev_asm, ev_adj = torch.cuda.Event(), torch.cuda.Event()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev_asm.record(cur)
+        f0.record(cur)
+        eng.kfac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda, st)
+        f1.record(cur)
+        if events is not None:
+            events[0].record()
+        side.wait_event(ev_asm)
+        with torch.cuda.stream(side):
+            sst = _lib.stream_handle()
+            res_a, it_a = eng.adjoint_direct(check_pivots=False)
+            eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, sst)
+            check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
+                                         ptr(eng.grad), sst))
+            eng.rhs.copy_(eng.tmp)
+            ev_adj.record(side)
+        cur.wait_event(ev_adj)
+        if events is not None:
+            events[1].record()
+        if timings is not None:
+            timings["adjoint_res"] = res_a
+            timings["adjoint_iters"] = it_a
+        if not need_direction:
+            eng.kfac.check(st)
+            eng.gfac.check(st)
+            return None, None
+        rc2, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
+        if events is not None:
+            events[2].record()
+        eng.kfac.check(st)
+        eng.gfac.check(st)
+        if timings is not None:
+            timings["factor_s"] = f0.elapsed_time(f1) * 1e-3
+            timings["solve_s"] = time.perf_counter() - t1 - timings["factor_s"]
+            timings["main_iters"] = its
     else:
-        # leading (x, lambda) block of the KKT factor preconditions [[A, G^T], [G, 0]]
-        rc, res_a, it_a = eng.kfac.solve_refined(eng.kvals, eng.fvec, eng.sol_adj, tol, mi, True, st)
-        check(lib().sgn_adjoint_step(0, eng.batch, n_x, n_p, ptr(eng.sol_adj), None, ptr(eng.tmp), None, st))
-    eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, st)
-    check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
-                                 ptr(eng.grad), st))
-    eng.rhs.copy_(eng.tmp)
-    if events is not None:
-        events[1].record()
-    if timings is not None:
-        timings["adjoint_res"] = res_a
-        timings["adjoint_iters"] = it_a
-    if not need_direction:
-        return None, None
-    rc2, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
-    if events is not None:
-        events[2].record()
-    if timings is not None:
-        timings["solve_s"] = time.perf_counter() - t2
-        timings["main_iters"] = its
+        _nan_probe(eng, "before factor")
+        eng.kfac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda, st)
+        if events is not None:
+            events[0].record()
+        eng.kfac.check(st)
+        t2 = time.perf_counter()
+        if timings is not None:
+            timings["factor_s"] = t2 - t1
+        if getattr(eng, "adjoint_gx", False):
+            res_a, it_a = eng.adjoint_direct()
+        else:
+            # leading (x, lambda) block of the KKT factor preconditions [[A, G^T], [G, 0]]
+            rc, res_a, it_a = eng.kfac.solve_refined(eng.kvals, eng.fvec, eng.sol_adj, tol, mi, True, st)
+            check(lib().sgn_adjoint_step(0, eng.batch, n_x, n_p, ptr(eng.sol_adj), None, ptr(eng.tmp), None, st))
+        eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, st)
+        check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
+                                     ptr(eng.grad), st))
+        eng.rhs.copy_(eng.tmp)
+        if events is not None:
+            events[1].record()
+        if timings is not None:
+            timings["adjoint_res"] = res_a
+            timings["adjoint_iters"] = it_a
+        _nan_probe(eng, "after adjoint")
+        if not need_direction:
+            return None, None
+        rc2, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
+        _nan_probe(eng, f"after refine rc={rc2}")
+        if events is not None:
+            events[2].record()
+        if timings is not None:
+            timings["solve_s"] = time.perf_counter() - t2
+            timings["main_iters"] = its
     if rc2 == _lib.SGN_NO_CONVERGENCE:
         best = eng.sol.cpu().numpy()
         raise NoConvergence(f"BiCGSTAB refinement stalled at relative residual {res.max():.3e}",
@@ -385,15 +452,17 @@ class DeviceEngine:
 
     adjoint_gx = True
 
-    def adjoint_direct(self):
+    def adjoint_direct(self, check_pivots: bool = True):
         """w = G_x^{-1} f_x (unshifted LDL^T of the state Jacobian) placed as v = (0, 0, w)
-        in self.tmp; returns (res, iters) placeholders of the refined variant."""
+        in self.tmp; returns (res, iters) placeholders of the refined variant.  With
+        check_pivots=False the caller checks the factor's status later (no host sync here)."""
         pl = self.plan
         st = self.stream
         self._gather(pl.G_nnz, None, 0, self.G_ptr, self.G_src, None, self.ebuf, self.ebuf.stride(0),
                      self.gvals, pl.G_nnz)
         self.gfac.numeric(self.gvals, 0.0, 0.0, st)
-        self.gfac.check(st)
+        if check_pivots:
+            self.gfac.check(st)
         check(lib().sgn_adjoint_step(3, self.batch, pl.n_x, pl.n_p, ptr(self.fvec), None, ptr(self.xtry), None, st))
         self.gfac.solve(self.xtry, self.kdir, False, st)
         check(lib().sgn_adjoint_step(2, self.batch, pl.n_x, pl.n_p, ptr(self.kdir), None, ptr(self.tmp), None, st))
