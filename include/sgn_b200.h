@@ -106,6 +106,33 @@ int  sgn_factor_check(sgn_factor f, void* stream, int64_t* pivot_index);
 int  sgn_factor_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, void* stream);
 void sgn_factor_destroy(sgn_factor f);
 
+/* X[:, j] = (L D L^T)^{-1} B[:, j] for nrhs right-hand sides against ONE factor (batch 1),
+ * column j at B + j*n.  Replaces the n_p back-substitutions of sensitivity_matrix
+ * (reference sensitivity.py:167-178: factor.solve(dcdp dense)).                           */
+int  sgn_factor_solve_multi(sgn_factor f, const double* d_B, double* d_X, int32_t nrhs, void* stream);
+
+/* Smallest 1x1 pivot D_rr of a generic-mode factor (batch instance 0) and its unknown:
+ * the positive-definiteness test of the dense Gauss-Newton factorization (reference
+ * linear_solvers.py:214-240, cho_factor -> NotPositiveDefinite(pivot_index)).        */
+int  sgn_factor_min_pivot(sgn_factor f, double* min_pivot, int64_t* position, void* stream);
+
+/* ---- dense Gauss-Newton (DGN) building blocks, SURVEY 8(f) 2 -------------------------
+ * Blocks of the stacked KKT [[A, B^T, G_x^T], [B, C, G_p^T], [G_x, G_p, 0]] are read from
+ * its full CSC (int64 indptr / indices, symmetric so CSC == CSR).
+ * sgn_csc_block_dense: out (column-major nr x nc) = K[r0:r0+nr, c0:c0+nc]  (dcdp.to_dense,
+ *   blocks.C.to_dense; sensitivity.py:177, 240).
+ * sgn_csc_spmm: Y[j][r] = sum_c K[r0+r, c0+c] X[j][c] (A @ sens, B @ sens; sensitivity.py:239-240).
+ * sgn_gemm_tn: C (column-major n x n) = X Y^T for row-major X, Y (n x K): sens^T (A sens), DMMA.
+ * sgn_gn_hessian: H = sym(STAS + BS + BS^T + C) (dense_gn_hessian, sensitivity.py:232-242). */
+int  sgn_csc_block_dense(int64_t n_cols_total, const int64_t* d_ptr, const int64_t* d_idx, const double* d_val,
+                         int64_t r0, int64_t nr, int64_t c0, int64_t nc, double* d_out, void* stream);
+int  sgn_csc_spmm(const int64_t* d_ptr, const int64_t* d_idx, const double* d_val, int64_t r0, int64_t nr,
+                  int64_t c0, int64_t ncol, const double* d_X, int64_t ldx, double* d_Y, int64_t ldy,
+                  int64_t m, void* stream);
+int  sgn_gemm_tn(const double* d_X, const double* d_Y, int64_t n, int64_t K, double* d_C, void* stream);
+int  sgn_gn_hessian(const double* d_stas, const double* d_bs, const double* d_c, int64_t n, double* d_H,
+                    void* stream);
+
 /* Diagnostics (no reference counterpart): the persistent solve's task list and, when the
  * process ran with SGN_DAG_TRACE=1, the last solve's per-task trace -- 6 words per task
  * (start, (smid << 48) | signalled, prefetched, ready, combined, end; globaltimer ns,

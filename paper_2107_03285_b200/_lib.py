@@ -48,6 +48,13 @@ SIGNATURES = {
     "sgn_factor_status": (ctypes.c_int, [c_vp, c_vp, P_i64]),
     "sgn_masked_copy": (ctypes.c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "sgn_factor_solve": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "sgn_factor_solve_multi": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "sgn_factor_min_pivot": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "sgn_csc_block_dense": (ctypes.c_int, [c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "sgn_csc_spmm": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
+                                    c_i64, c_vp]),
+    "sgn_gemm_tn": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp]),
+    "sgn_gn_hessian": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "sgn_debug_solve_trace": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_vp, c_vp]),
     "sgn_debug_factor_trace": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int64, c_vp, c_vp]),
     "sgn_debug_factor_buffer": (ctypes.c_int, [c_vp, c_i32, c_vp, ctypes.c_int64, c_vp]),

@@ -589,6 +589,10 @@ struct sgn_factor_s {
   DevBuf<sgn::Task> stasks;
   DevBuf<int32_t> swaits, gsrc;
   DevBuf<int64_t> gptr;
+  // multi-RHS solves (one factor, nrhs right-hand sides): per-RHS solve scratch
+  DevBuf<double> mubuf, mzbuf, mxbuf, mpart;
+  DevBuf<int> mtickets, mscnt;
+  int32_t mcap = 0;
   DevBuf<int64_t> trace;        // SGN_DAG_TRACE=1: 3 words per solve task (diagnostics)
   DevBuf<int> scnt;             // [head | batch x n_scnt counters], zeroed before every solve
   int solve_grid = 0;
@@ -638,6 +642,41 @@ int launch_solve_dag(sgn_factor f, const double* d_b, double* d_x, int32_t flags
       CUDA_TRY(cudaMemsetAsync(f->trace.p, 0, f->trace.n * sizeof(int64_t), st));
     } }
   CUDA_TRY(cudaMemsetAsync(f->scnt.p, 0, f->scnt.n * sizeof(int), st));
+  const int64_t total = A.ntask * A.batch;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(f->solve_grid, total));
+  sgn::count_launch();
+  k_solve_dag<<<grid, kSolveThreads, 0, st>>>(A);
+  CUDA_TRY(cudaGetLastError());
+  return SGN_OK;
+}
+
+// nrhs right-hand sides against ONE factor (batch 1): the persistent solve runs with the
+// right-hand sides as its batch dimension, fronts / Z shared (stride 0), scratch per RHS.
+int launch_solve_multi(sgn_factor f, const double* d_B, double* d_X, int32_t nrhs, cudaStream_t st) {
+  const sgn::Symbolic& s = f->sym->s;
+  if (s.n == 0 || nrhs <= 0) return SGN_OK;
+  int rc;
+  if (nrhs > f->mcap) {
+    const size_t R = (size_t)nrhs;
+    if ((rc = f->mubuf.alloc(R * std::max<int64_t>(s.u_doubles, 1))) || (rc = f->mzbuf.alloc(R * s.n)) ||
+        (rc = f->mxbuf.alloc(R * s.n)) || (rc = f->mpart.alloc(R * std::max<int64_t>(s.part_doubles, 1))) ||
+        (rc = f->mtickets.alloc(R * std::max<int64_t>(s.n_groups, 1))) ||
+        (rc = f->mscnt.alloc(1 + R * std::max<int64_t>(s.n_scnt, 1))))
+      return rc;
+    CUDA_TRY(cudaMemsetAsync(f->mtickets.p, 0, f->mtickets.n * sizeof(int), st));
+    f->mcap = nrhs;
+  }
+  SolveArgs A;
+  A.tasks = f->stasks.p; A.waits = f->swaits.p; A.ntask = (int64_t)s.stasks.size(); A.batch = nrhs;
+  A.head = f->mscnt.p; A.cnt = f->mscnt.p + 1; A.n_cnt = s.n_scnt;
+  A.fronts = f->fronts.p; A.srows = f->srows.p; A.gptr = f->gptr.p; A.gsrc = f->gsrc.p;
+  A.perm = f->perm.p; A.fstore = f->fstore.p; A.fstride = 0;
+  A.zstore = f->zstore.p; A.zstride = 0; A.ubuf = f->mubuf.p; A.ustride = s.u_doubles;
+  A.zbuf = f->mzbuf.p; A.xbuf = f->mxbuf.p; A.n = s.n;
+  A.part = f->mpart.p; A.pstride = s.part_doubles; A.tickets = f->mtickets.p; A.n_groups = s.n_groups;
+  A.grp_nchunk = f->grp_nchunk.p; A.grp_base = f->grp_base.p;
+  A.b_in = d_B; A.x_out = d_X; A.leading = 0; A.gate = nullptr; A.nop = 0; A.trace = nullptr; A.mode = 0;
+  CUDA_TRY(cudaMemsetAsync(f->mscnt.p, 0, (1 + (size_t)nrhs * std::max<int64_t>(s.n_scnt, 1)) * sizeof(int), st));
   const int64_t total = A.ntask * A.batch;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(f->solve_grid, total));
   sgn::count_launch();
@@ -952,6 +991,17 @@ int sgn_debug_factor_buffer(sgn_factor f, int32_t which, void* out, int64_t cap_
     CUDA_TRY(cudaMemcpy(out, src, std::min<size_t>(bytes, (size_t)cap_bytes), cudaMemcpyDeviceToHost));
   }
   return SGN_OK;
+}
+
+int sgn_factor_min_pivot(sgn_factor f, double* min_pivot, int64_t* position, void* stream) {
+  const sgn::Symbolic& s = f->sym->s;
+  if (s.pair_mode) { sgn::last_error() = "min pivot is defined for 1x1-pivot (generic) factors"; return SGN_INVALID; }
+  return sgn::min_pivot(f->fronts.p, (int32_t)s.fronts.size(), f->fstore.p, min_pivot, position, stream);
+}
+
+int sgn_factor_solve_multi(sgn_factor f, const double* d_B, double* d_X, int32_t nrhs, void* stream) {
+  if (f->batch != 1) { sgn::last_error() = "multi-RHS solves need a batch-1 factor"; return SGN_INVALID; }
+  return launch_solve_multi(f, d_B, d_X, nrhs, (cudaStream_t)stream);
 }
 
 int sgn_factor_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, void* stream) {

@@ -170,6 +170,8 @@ struct FactorArgs {
   unsigned long long* trace;   // optional (SGN_FDAG_TRACE=1): 4 words per task
 };
 int factor_dag_grid();
+int min_pivot(const DFront* d_fronts, int32_t n_fronts, const double* d_fstore, double* out_min,
+              int64_t* out_pos, void* stream);
 int launch_factor_dag(const FactorArgs& A, int grid, void* stream);
 
 std::string& last_error();

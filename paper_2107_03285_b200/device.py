@@ -125,6 +125,10 @@ class DeviceFactor:
         flags = _lib.SGN_SOLVE_LEADING if leading else 0
         check(lib().sgn_factor_solve(self._h, ptr(b), ptr(x), flags, stream), what="solve")
 
+    def solve_multi(self, B, X, stream: int = 0) -> None:
+        """X[j] = A^{-1} B[j] for the rows j of a (nrhs, n) float64 CUDA tensor (batch-1 factor)."""
+        check(lib().sgn_factor_solve_multi(self._h, ptr(B), ptr(X), int(B.shape[0]), stream), what="multi solve")
+
     def spmv(self, values, x, y, leading: bool = False, stream: int = 0) -> None:
         stride = values.stride(0) if values.dim() == 2 else 0
         flags = _lib.SGN_SOLVE_LEADING if leading else 0

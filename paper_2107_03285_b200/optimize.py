@@ -17,14 +17,15 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import (ForwardSimFailure, InfeasiblePoint, NoConvergence, NumericalBlowup)
+from .errors import (CapabilityMissing, ForwardSimFailure, InfeasiblePoint, NoConvergence, NotPositiveDefinite,
+                     NumericalBlowup)
 from .linear_solvers import StabilizationConfig, solve_kkt_stabilized
 from .sensitivity import _host_kkt, _is_device_problem, adjoint_gradient
 
 __all__ = ["METHODS", "CSV_HEADER", "OptimizerConfig", "SearchDirection", "IterationRecord",
            "OptimizerRun", "direction_sgn", "minimize", "project_direction_bounds"]
 
-METHODS = ("sgn", "lbfgs", "lbfgs_sgn")
+METHODS = ("sgn", "dgn", "lbfgs", "lbfgs_sgn")
 CSV_HEADER = "iter,f,grad_norm,step_len,dir_time_s,fwd_time_s,elapsed_s,lin_rel_residual"
 
 
@@ -141,7 +142,97 @@ def direction_sgn(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirectio
                            extra={"refine_iterations": int(its[0])})
 
 
-_DIRECTION_FUNCS = {"sgn": direction_sgn}
+def direction_dgn(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirection:
+    """Gauss-Newton step through the dense reduced Hessian (reference optimize.py:168-198),
+    on the device for device problems:
+
+    * S = -G_x^{-1} G_p: the unshifted G_x factor + one multi-RHS solve with the n_p
+      columns of G_p (sensitivity.py:167-178);
+    * H = S^T A S + B S + (B S)^T + C, symmetrised (sensitivity.py:232-242): sparse-times-
+      dense products from the KKT CSC, S^T (A S) on a DMMA GEMM;
+    * dp = -H^{-1} g by the multifrontal LDL^T on the dense pattern; a non-positive pivot
+      raises NotPositiveDefinite(pivot_index) like cho_factor (linear_solvers.py:214-240).
+
+    The sensitivity-matrix time and the dense factorization time are reported separately
+    (``extra``) as in the reference.
+    """
+    if not _is_device_problem(prob):
+        raise CapabilityMissing("direction_dgn on the device needs a device problem "
+                                "(problems.ElasticDesignProblem)")
+    import ctypes
+    from . import _lib
+    from ._lib import check, lib, ptr
+    from .device import DeviceFactor, symbolic_for
+    eng = prob.engine
+    if eng.batch != 1:
+        raise CapabilityMissing("direction_dgn: one instance per engine")
+    pl = prob.plan
+    torch = eng.torch
+    st = _lib.stream_handle()
+    n_x, n_p, dim = pl.n_x, pl.n_p, pl.dim
+    sync = torch.cuda.synchronize
+    prob._load(x, p)
+    eng.assemble()
+    sync()
+    t0 = time.perf_counter()
+    # S = -G_x^{-1} G_p
+    eng._gather(pl.G_nnz, None, 0, eng.G_ptr, eng.G_src, None, eng.ebuf, eng.ebuf.stride(0), eng.gvals, pl.G_nnz)
+    eng.gfac.numeric(eng.gvals, 0.0, 0.0, st)
+    eng.gfac.check(st)
+    if not hasattr(eng, "_dgn"):
+        T = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.int64, device="cuda")
+        E = lambda *shape: torch.empty(shape, dtype=torch.float64, device="cuda")
+        dsym = symbolic_for(n_p, np.arange(0, n_p * n_p + 1, n_p, dtype=np.int64),
+                            np.tile(np.arange(n_p, dtype=np.int64), n_p))
+        eng._dgn = dict(kp=T(pl.K_indptr), ki=T(pl.K_indices), GP=E(n_p, n_x), S=E(n_p, n_x), AS=E(n_p, n_x),
+                        STAS=E(n_p, n_p), BS=E(n_p, n_p), C=E(n_p, n_p), H=E(1, n_p * n_p), rhs=E(1, n_p),
+                        dp=E(1, n_p), dsym=dsym, dfac=DeviceFactor(dsym, 1))
+    d = eng._dgn
+    kv = eng.kvals[0]
+    check(lib().sgn_csc_block_dense(dim, ptr(d["kp"]), ptr(d["ki"]), ptr(kv), n_x + n_p, n_x, n_x, n_p,
+                                    ptr(d["GP"]), st))                      # G_p, column j = RHS j
+    eng.gfac.solve_multi(d["GP"], d["S"], st)
+    d["S"].neg_()
+    sync()
+    t_sens = time.perf_counter() - t0
+    # H = S^T A S + B S + (B S)^T + C
+    t1 = time.perf_counter()
+    check(lib().sgn_csc_spmm(ptr(d["kp"]), ptr(d["ki"]), ptr(kv), 0, n_x, 0, n_x, ptr(d["S"]), n_x,
+                             ptr(d["AS"]), n_x, n_p, st))
+    check(lib().sgn_gemm_tn(ptr(d["S"]), ptr(d["AS"]), n_p, n_x, ptr(d["STAS"]), st))
+    check(lib().sgn_csc_spmm(ptr(d["kp"]), ptr(d["ki"]), ptr(kv), n_x, n_p, 0, n_x, ptr(d["S"]), n_x,
+                             ptr(d["BS"]), n_p, n_p, st))
+    check(lib().sgn_csc_block_dense(dim, ptr(d["kp"]), ptr(d["ki"]), ptr(kv), n_x, n_p, n_x, n_p,
+                                    ptr(d["C"]), st))
+    check(lib().sgn_gn_hessian(ptr(d["STAS"]), ptr(d["BS"]), ptr(d["C"]), n_p, ptr(d["H"]), st))
+    if grad is None:
+        grad = adjoint_gradient(prob, x, p)
+    grad = np.asarray(grad, dtype=np.float64)
+    sync()
+    assemble_s = time.perf_counter() - t1 + t_sens
+    # dense factorization + positivity
+    t2 = time.perf_counter()
+    d["dfac"].numeric(d["H"], 0.0, 0.0, st)
+    d["dfac"].check(st)
+    mn, pos = ctypes.c_double(), ctypes.c_int64()
+    check(lib().sgn_factor_min_pivot(d["dfac"]._h, ctypes.byref(mn), ctypes.byref(pos), st))
+    if not mn.value > 0.0:
+        raise NotPositiveDefinite(f"dense Gauss-Newton Hessian is not positive definite "
+                                  f"(pivot {pos.value}: {mn.value:.3e})", pivot_index=int(pos.value))
+    factor_s = time.perf_counter() - t2
+    t3 = time.perf_counter()
+    d["rhs"][0].copy_(torch.from_numpy(-grad))
+    d["dfac"].solve(d["rhs"], d["dp"], False, st)
+    dp = d["dp"][0].cpu().numpy()
+    solve_s = time.perf_counter() - t3
+    h = d["H"][0].cpu().numpy().reshape(n_p, n_p)
+    gnorm = np.linalg.norm(grad)
+    res = float(np.linalg.norm(h @ dp + grad) / gnorm) if gnorm > 0 else 0.0
+    return SearchDirection(dp=dp, assemble_s=assemble_s, factor_s=factor_s, solve_s=solve_s,
+                           relative_residual=res, extra={"sens_matrix_s": t_sens, "dense_factor_s": factor_s})
+
+
+_DIRECTION_FUNCS = {"sgn": direction_sgn, "dgn": direction_dgn}
 
 
 def direction_lbfgs(history, grad: np.ndarray, apply_h0=None) -> np.ndarray:
