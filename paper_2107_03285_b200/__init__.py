@@ -16,7 +16,7 @@ from .sparse import (CscMatrix, TripletMatrix, csc_from_triplets, read_matrix_ma
 from .sensitivity import (EquilibriumProblem, GnBlocks, KktSystem, adjoint_gradient, assemble_sgn,
                           gn_blocks, kkt_from_blocks)
 from .optimize import (CSV_HEADER, METHODS, IterationRecord, OptimizerConfig, OptimizerRun,
-                       SearchDirection, direction_dgn, direction_lbfgs, direction_sgn, minimize,
+                       SearchDirection, direction_cg_gn, direction_dgn, direction_lbfgs, direction_sgn, minimize,
                        project_direction_bounds)
 
 __version__ = "0.1.0"

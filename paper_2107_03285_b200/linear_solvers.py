@@ -23,7 +23,7 @@ import scipy.sparse as sp
 
 from . import _lib
 from .device import DeviceFactor, symbolic_for
-from .errors import (CapabilityMissing, DimensionMismatch, NoConvergence, SingularMatrix)
+from .errors import (CapabilityMissing, DimensionMismatch, NegativeCurvature, NoConvergence, SingularMatrix)
 from .sparse import CscMatrix
 
 __all__ = ["SolveReport", "StabilizationConfig", "SparseFactorization", "factor_sparse",
@@ -207,3 +207,90 @@ def solve_kkt_stabilized(k, rhs, cfg: StabilizationConfig | None = None):
             f"BiCGSTAB refinement stalled at relative residual {res[0]:.3e} after {its[0]} iterations",
             residual=float(res[0]), iterations=int(its[0]), best=x)
     return x, report
+
+
+class DeviceReducedOperator:
+    """Matrix-free reduced Gauss-Newton Hessian y -> S^T A S y + B S y + S^T B^T y + C y,
+    S = -G_x^{-1} G_p (reference linear_solvers.py:243-268), applied on the device: the
+    KKT blocks A, B, C, G_p are read from the engine's KKT CSC (sgn_csc_spmm) and the two
+    solves per application use the engine's unshifted G_x factor (symmetric G_x)."""
+
+    def __init__(self, eng, plan):
+        from ._lib import check, lib, ptr
+        self._check, self._lib, self._ptr = check, lib, ptr
+        torch = eng.torch
+        self.eng, self.torch = eng, torch
+        self.n_x, self.n_p = plan.n_x, plan.n_p
+        T = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.int64, device="cuda")
+        if not hasattr(eng, "_kpat"):
+            eng._kpat = (T(plan.K_indptr), T(plan.K_indices))
+        self.kp, self.ki = eng._kpat
+        E = lambda n: torch.empty(n, dtype=torch.float64, device="cuda")
+        self.y, self.gy, self.t, self.u, self.u2, self.w = E(self.n_p), E(self.n_x), E(self.n_x), E(self.n_x), E(self.n_x), E(self.n_x)
+        self.r1, self.r2, self.r3 = E(self.n_p), E(self.n_p), E(self.n_p)
+        self.applications = 0
+
+    def _spmm(self, r0, nr, c0, nc, x, y, st):
+        self._check(self._lib().sgn_csc_spmm(self._ptr(self.kp), self._ptr(self.ki), self._ptr(self.eng.kvals[0]),
+                                             r0, nr, c0, nc, self._ptr(x), nc, self._ptr(y), nr, 1, st))
+
+    def apply(self, yv: np.ndarray) -> np.ndarray:
+        self.applications += 1
+        st = _lib.stream_handle()
+        n_x, n_p = self.n_x, self.n_p
+        lam0, p0 = n_x + n_p, n_x
+        self.y.copy_(self.torch.from_numpy(np.ascontiguousarray(yv, dtype=np.float64)))
+        self._spmm(lam0, n_x, p0, n_p, self.y, self.gy, st)                   # G_p y
+        self.eng.gfac.solve(self.gy.view(1, -1), self.t.view(1, -1), False, st)
+        self.t.neg_()                                                           # t = S y
+        self._spmm(0, n_x, 0, n_x, self.t, self.u, st)                         # A t
+        self._spmm(0, n_x, p0, n_p, self.y, self.u2, st)                       # B^T y
+        self.u.add_(self.u2)
+        self.eng.gfac.solve(self.u.view(1, -1), self.w.view(1, -1), False, st)   # G_x^{-T} u
+        self._spmm(p0, n_p, lam0, n_x, self.w, self.r1, st)                    # G_p^T w
+        self._spmm(p0, n_p, 0, n_x, self.t, self.r2, st)                       # B t
+        self._spmm(p0, n_p, p0, n_p, self.y, self.r3, st)                      # C y
+        self.r2.sub_(self.r1).add_(self.r3)
+        return self.r2.cpu().numpy()
+
+
+def cg_reduced(op, rhs: np.ndarray, eta: float = 1e-3, max_iters: int | None = None):
+    """CG on the reduced operator to relative residual eta (reference linear_solvers.py:271-323):
+    raises NegativeCurvature (last iterate) on non-positive curvature and NoConvergence past
+    the cap (default 10 n_p); the recursive residual is confirmed by a true one."""
+    rhs = np.asarray(rhs, dtype=np.float64)
+    if rhs.shape != (op.n_p,):
+        raise DimensionMismatch(f"rhs has length {rhs.size}, expected {op.n_p}")
+    if max_iters is None:
+        max_iters = 10 * op.n_p
+    t0 = time.perf_counter()
+    bnorm = float(np.linalg.norm(rhs))
+    x = np.zeros_like(rhs)
+    if bnorm == 0.0:
+        return x, SolveReport(0.0, 0, 0.0, time.perf_counter() - t0)
+    r = rhs.copy()
+    pdir = r.copy()
+    rs = float(r @ r)
+    it = 0
+    while it < max_iters:
+        it += 1
+        hp = op.apply(pdir)
+        php = float(pdir @ hp)
+        if php <= 0.0:
+            raise NegativeCurvature(f"non-positive curvature {php:.3e} at CG iteration {it}",
+                                    best=x, iterations=it)
+        step = rs / php
+        x += step * pdir
+        r -= step * hp
+        if np.linalg.norm(r) <= eta * bnorm:
+            true_r = rhs - op.apply(x)
+            true_norm = float(np.linalg.norm(true_r))
+            if true_norm <= eta * bnorm:
+                return x, SolveReport(true_norm / bnorm, it, 0.0, time.perf_counter() - t0)
+            r = true_r
+        rs_new = float(r @ r)
+        pdir = r + (rs_new / rs) * pdir
+        rs = rs_new
+    res = float(np.linalg.norm(rhs - op.apply(x)) / bnorm)
+    raise NoConvergence(f"CG exceeded {max_iters} iterations (relative residual {res:.3e})",
+                        residual=res, iterations=it, best=x)

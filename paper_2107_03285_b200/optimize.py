@@ -25,7 +25,7 @@ from .sensitivity import _host_kkt, _is_device_problem, adjoint_gradient
 __all__ = ["METHODS", "CSV_HEADER", "OptimizerConfig", "SearchDirection", "IterationRecord",
            "OptimizerRun", "direction_sgn", "minimize", "project_direction_bounds"]
 
-METHODS = ("sgn", "dgn", "lbfgs", "lbfgs_sgn")
+METHODS = ("sgn", "dgn", "cg_gn", "lbfgs", "lbfgs_sgn")
 CSV_HEADER = "iter,f,grad_norm,step_len,dir_time_s,fwd_time_s,elapsed_s,lin_rel_residual"
 
 
@@ -232,7 +232,45 @@ def direction_dgn(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirectio
                            relative_residual=res, extra={"sens_matrix_s": t_sens, "dense_factor_s": factor_s})
 
 
-_DIRECTION_FUNCS = {"sgn": direction_sgn, "dgn": direction_dgn}
+def direction_cg_gn(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirection:
+    """Matrix-free CG on the reduced Gauss-Newton operator (reference optimize.py:212-232),
+    operator applications on the device (two G_x solves each).  Negative curvature falls
+    back to CG's last iterate, or steepest descent if CG has not moved, as in the reference."""
+    from .linear_solvers import DeviceReducedOperator, cg_reduced
+    from .errors import NegativeCurvature
+    if not _is_device_problem(prob):
+        raise CapabilityMissing("direction_cg_gn on the device needs a device problem")
+    eng = prob.engine
+    if eng.batch != 1:
+        raise CapabilityMissing("direction_cg_gn: one instance per engine")
+    pl = prob.plan
+    t0 = time.perf_counter()
+    if grad is None:
+        grad = adjoint_gradient(prob, x, p)
+    prob._load(x, p)
+    eng.assemble()
+    st = _lib_stream()
+    eng._gather(pl.G_nnz, None, 0, eng.G_ptr, eng.G_src, None, eng.ebuf, eng.ebuf.stride(0), eng.gvals, pl.G_nnz)
+    eng.gfac.numeric(eng.gvals, 0.0, 0.0, st)
+    eng.gfac.check(st)
+    op = DeviceReducedOperator(eng, pl)
+    assemble_s = time.perf_counter() - t0
+    try:
+        dp, rep = cg_reduced(op, -np.asarray(grad, dtype=np.float64), eta=cfg.cg_eta)
+        return SearchDirection(dp=dp, assemble_s=assemble_s, solve_s=rep.solve_time,
+                               relative_residual=rep.relative_residual,
+                               extra={"cg_iterations": rep.refine_iterations, "operator_applications": op.applications})
+    except NegativeCurvature as exc:
+        dp = exc.best if exc.best is not None and np.linalg.norm(exc.best) > 0 else -np.asarray(grad)
+        return SearchDirection(dp=dp, assemble_s=assemble_s)
+
+
+def _lib_stream() -> int:
+    from . import _lib
+    return _lib.stream_handle()
+
+
+_DIRECTION_FUNCS = {"sgn": direction_sgn, "dgn": direction_dgn, "cg_gn": direction_cg_gn}
 
 
 def direction_lbfgs(history, grad: np.ndarray, apply_h0=None) -> np.ndarray:

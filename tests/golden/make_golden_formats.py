@@ -8,6 +8,8 @@
   ('sgn') on the same problem (optimize.py:60,112-137)
 * ref_lbfgs_11x3.npz -- f / |g| / p trajectories of the reference minimize with 'lbfgs_sgn'
   (optimize.py:433-457) and 'lbfgs' on the spring bar 11x3, 6 iterations
+* ref_cg_gn.npz -- direction_cg_gn (optimize.py:212-232) on the spring bars 5x3 / 11x3 at
+  cg_eta 1e-3 and 1e-10
 The GPU path must emit the same schemas.
 """
 from __future__ import annotations
@@ -54,6 +56,21 @@ def main():
         traj[f"{method}_g"] = run.grad_norms()
         traj[f"{method}_p"] = run.p
     np.savez(os.path.join(HERE, "ref_lbfgs_11x3.npz"), **traj)
+    # matrix-free CG on the reduced Gauss-Newton operator (optimize.py:212-232)
+    from sgnopt.optimize import direction_cg_gn
+    from sgnopt.sensitivity import adjoint_gradient
+    cg = {}
+    for nw, nh in ((5, 3), (11, 3)):
+        prob = build_spring_bar(nw, nh)
+        p = prob.default_parameters()
+        x = prob.simulate(p)
+        g = adjoint_gradient(prob, x, p)
+        for eta in (1e-3, 1e-10):
+            sd = direction_cg_gn(prob, x, p, OptimizerConfig(cg_eta=eta), grad=g)
+            cg[f"dp_{nw}x{nh}_{eta:g}"] = sd.dp
+            cg[f"res_{nw}x{nh}_{eta:g}"] = sd.relative_residual
+        cg[f"x_{nw}x{nh}"], cg[f"p_{nw}x{nh}"], cg[f"g_{nw}x{nh}"] = x, p, g
+    np.savez(os.path.join(HERE, "ref_cg_gn.npz"), **cg)
     print("wrote", out, "ref_convergence_sgn_5x3.csv and ref_lbfgs_11x3.npz")
 
 

@@ -54,3 +54,21 @@ def test_dgn_minimize_trajectory(cuda):
     n = min(len(run.f_values()), len(g["traj_f"]))
     # SGN and DGN take the same steps (Theorem 1): the reference SGN trajectory is the target
     np.testing.assert_allclose(run.f_values()[:n], g["traj_f"][:n], rtol=1e-7, atol=1e-14 * g["traj_f"][0])
+
+
+@pytest.mark.parametrize("nw,nh", [(5, 3), (11, 3)])
+def test_cg_gn_matches_reference(cuda, nw, nh):
+    """Matrix-free CG on the reduced GN operator (reference optimize.py:212-232) with device
+    operator applications: at cg_eta 1e-10 it reproduces the reference dp; at the default
+    1e-3 both stop at the same tolerance (same iterates up to rounding)."""
+    from paper_2107_03285_b200 import OptimizerConfig, direction_cg_gn
+    from paper_2107_03285_b200.problems import build_spring_bar
+    g = dict(np.load(os.path.join(GOLD, "ref_cg_gn.npz")))
+    prob = build_spring_bar(nw, nh)
+    x, p, grad = g[f"x_{nw}x{nh}"], g[f"p_{nw}x{nh}"], g[f"g_{nw}x{nh}"]
+    tight = direction_cg_gn(prob, x, p, OptimizerConfig(cg_eta=1e-10), grad=grad)
+    assert tight.relative_residual <= 1e-10
+    assert _rel(tight.dp, g[f"dp_{nw}x{nh}_1e-10"]) <= 1e-8
+    loose = direction_cg_gn(prob, x, p, OptimizerConfig(), grad=grad)
+    assert loose.relative_residual <= 1e-3
+    assert _rel(loose.dp, g[f"dp_{nw}x{nh}_0.001"]) <= 1e-6
