@@ -14,9 +14,10 @@ from .linear_solvers import (SolveReport, SparseFactorization, StabilizationConf
 from .sparse import (CscMatrix, TripletMatrix, csc_from_triplets, read_matrix_market, spmv,
                      spmv_transpose, stack_kkt_blocks, write_matrix_market)
 from .sensitivity import (EquilibriumProblem, GnBlocks, KktSystem, adjoint_gradient, assemble_sgn,
-                          gn_blocks, kkt_from_blocks)
+                          gn_blocks, kkt_from_blocks, solve_block_gn)
 from .optimize import (CSV_HEADER, METHODS, IterationRecord, OptimizerConfig, OptimizerRun,
-                       SearchDirection, direction_cg_gn, direction_dgn, direction_lbfgs, direction_sgn, minimize,
+                       SearchDirection, direction_bgn, direction_cg_gn, direction_dgn, direction_gd, direction_lbfgs,
+                       direction_sgn, minimize,
                        project_direction_bounds)
 
 __version__ = "0.1.0"

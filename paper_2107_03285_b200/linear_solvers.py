@@ -4,7 +4,8 @@ Mirrors the reference's solver surface (reference pkg/src/sgnopt/linear_solvers.
 
 * ``SolveReport`` / ``StabilizationConfig``            (linear_solvers.py:31-58)
 * ``SparseFactorization`` / ``factor_sparse``          (linear_solvers.py:61-102)
-  -> multifrontal LDL^T on the device (symmetric input; 1x1 pivots in generic mode)
+  -> multifrontal LDL^T on the device (symmetric input; 1x1 pivots in generic mode);
+     unsymmetric square input through its symmetric saddle form [[0, M^T], [M, 0]]
 * ``stabilized_matrix``                                 (linear_solvers.py:111-127)
 * ``solve_kkt_stabilized``                              (linear_solvers.py:130-175)
   -> factor K + diag(+eps_x, 0, -eps_lambda) with (x_i, lambda_i) 2x2 pivots, then
@@ -129,33 +130,98 @@ class _DeviceSystem:
         return out.reshape(b.shape)
 
 
-class SparseFactorization:
-    """Device LDL^T of a square symmetric sparse matrix (replaces linear_solvers.py:61-97).
+def _is_symmetric(m: CscMatrix) -> bool:
+    """Numerically symmetric to 1e-14 relative (pattern union allowed)."""
+    a = m.to_scipy()
+    d = (a - a.T).tocsc()
+    d.eliminate_zeros()
+    if d.nnz == 0:
+        return True
+    return bool(np.max(np.abs(d.data)) <= 1e-14 * max(np.max(np.abs(a.data)) if a.nnz else 0.0, 1e-300))
 
-    ``fill_nnz`` counts the equivalent LU entries with the unit diagonal excluded
-    (2 * strictly-lower(L) + n), so a factored identity reports exactly n as in the
-    reference's SuperLU accounting.
+
+def _augmented(m: CscMatrix) -> CscMatrix:
+    """[[0, M^T], [M, 0]]: the symmetric saddle form of a square unsymmetric M."""
+    a = m.to_scipy().tocsc()
+    return CscMatrix.from_scipy(sp.bmat([[None, a.T], [a, None]], format="csc"))
+
+
+class SparseFactorization:
+    """Sparse factorization of a square matrix on the device (replaces linear_solvers.py:61-97).
+
+    Symmetric input: multifrontal LDL^T (1x1 pivots).  ``fill_nnz`` counts the equivalent LU
+    entries with the unit diagonal excluded (2 * strictly-lower(L) + n), so a factored
+    identity reports exactly n as in the reference's SuperLU accounting.
+
+    Unsymmetric input (the reference hands it to SuperLU; here dc/dp in the block solve,
+    sensitivity.py:284): the device factors the symmetric saddle form [[0, M^T], [M, 0]]
+    with the KKT solver's 2x2 pivots on a structural matching of M (no shift), and each
+    solve is refined by BiCGSTAB against the exact saddle matrix to ``refine_tolerance``.
+    M x = b is the (0, b) right-hand side (x = first half), M^T x = b is (b, 0) (x = second
+    half).  ``fill_nnz`` is then nnz of the saddle factor's L minus n.
     """
 
-    __slots__ = ("n", "fill_nnz", "_sys")
+    __slots__ = ("n", "fill_nnz", "_sys", "_unsym", "refine_tolerance", "max_refine_iters", "last_report")
 
-    def __init__(self, m: CscMatrix):
+    def __init__(self, m: CscMatrix, refine_tolerance: float = 1e-12, max_refine_iters: int = 50):
         _structural_checks(m)
-        self._sys = _DeviceSystem(m)
-        self._sys.factorize()
         self.n = m.rows
-        self.fill_nnz = int(2 * self._sys.sym.stats()["nnz_l"] - self.n)
+        self._unsym = not _is_symmetric(m)
+        self.refine_tolerance = float(refine_tolerance)
+        self.max_refine_iters = int(max_refine_iters)
+        self.last_report = None
+        if self._unsym:
+            self._sys = _DeviceSystem(_augmented(m), self.n, 0, self.n)
+            self._sys.factorize()
+            self.fill_nnz = int(self._sys.sym.stats()["nnz_l"] - self.n)
+        else:
+            self._sys = _DeviceSystem(m)
+            self._sys.factorize()
+            self.fill_nnz = int(2 * self._sys.sym.stats()["nnz_l"] - self.n)
 
     def solve(self, b, transpose: bool = False) -> np.ndarray:
-        """x = A^{-1} b (``transpose`` is a no-op for the symmetric factor; sensitivity.py:191)."""
+        """x = A^{-1} b, or A^{-T} b with ``transpose`` (a no-op for a symmetric factor;
+        sensitivity.py:191)."""
         b = np.asarray(b, dtype=np.float64)
         if b.shape[0] != self.n:
             raise DimensionMismatch(f"rhs has {b.shape[0]} rows, expected {self.n}")
-        return self._sys.solve_host(b)
+        if not self._unsym:
+            return self._sys.solve_host(b)
+        return self._solve_saddle(b, transpose)
+
+    def _solve_saddle(self, b: np.ndarray, transpose: bool) -> np.ndarray:
+        torch = self._sys.torch
+        n = self.n
+        cols = b.reshape(n, -1)
+        out = np.empty_like(cols)
+        stream = _lib.stream_handle()
+        worst, iters = 0.0, 0
+        for j in range(cols.shape[1]):
+            rhs = np.zeros(2 * n)
+            if transpose:
+                rhs[:n] = cols[:, j]
+            else:
+                rhs[n:] = cols[:, j]
+            if not np.any(rhs):
+                out[:, j] = 0.0
+                continue
+            d_rhs = torch.from_numpy(rhs).to("cuda")
+            d_sol = torch.empty_like(d_rhs)
+            rc, res, its = self._sys.factor.solve_refined(self._sys.values, d_rhs, d_sol, self.refine_tolerance,
+                                                          self.max_refine_iters, False, stream)
+            sol = d_sol.cpu().numpy()
+            if rc == _lib.SGN_NO_CONVERGENCE:
+                raise NoConvergence(f"unsymmetric solve stalled at relative residual {res[0]:.3e} after "
+                                    f"{its[0]} iterations", residual=float(res[0]), iterations=int(its[0]),
+                                    best=sol[n:] if transpose else sol[:n])
+            out[:, j] = sol[n:] if transpose else sol[:n]
+            worst, iters = max(worst, float(res[0])), iters + int(its[0])
+        self.last_report = SolveReport(worst, iters)
+        return out.reshape(b.shape)
 
 
 def factor_sparse(m: CscMatrix) -> SparseFactorization:
-    """Factor a square symmetric sparse matrix on the device (linear_solvers.py:100-102)."""
+    """Factor a square sparse matrix on the device (linear_solvers.py:100-102)."""
     return SparseFactorization(m)
 
 

@@ -20,12 +20,12 @@ import numpy as np
 from .errors import (CapabilityMissing, ForwardSimFailure, InfeasiblePoint, NoConvergence, NotPositiveDefinite,
                      NumericalBlowup)
 from .linear_solvers import StabilizationConfig, solve_kkt_stabilized
-from .sensitivity import _host_kkt, _is_device_problem, adjoint_gradient
+from .sensitivity import _host_kkt, _is_device_problem, adjoint_gradient, gn_blocks
 
 __all__ = ["METHODS", "CSV_HEADER", "OptimizerConfig", "SearchDirection", "IterationRecord",
            "OptimizerRun", "direction_sgn", "minimize", "project_direction_bounds"]
 
-METHODS = ("sgn", "dgn", "cg_gn", "lbfgs", "lbfgs_sgn")
+METHODS = ("sgn", "dgn", "bgn", "cg_gn", "gd", "lbfgs", "lbfgs_sgn")
 CSV_HEADER = "iter,f,grad_norm,step_len,dir_time_s,fwd_time_s,elapsed_s,lin_rel_residual"
 
 
@@ -265,12 +265,34 @@ def direction_cg_gn(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirect
         return SearchDirection(dp=dp, assemble_s=assemble_s)
 
 
+def direction_bgn(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirection:
+    """Block-substitution Gauss-Newton step (reference optimize.py:201-209): needs B = C = 0
+    and a square dc/dp; both factorizations and solves on the device (``solve_block_gn``)."""
+    from .sensitivity import solve_block_gn
+    t0 = time.perf_counter()
+    blocks = gn_blocks(prob, x, p)
+    assemble_s = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    dp = solve_block_gn(prob, x, p, blocks.A)
+    return SearchDirection(dp=dp, assemble_s=assemble_s, solve_s=time.perf_counter() - t1)
+
+
+def direction_gd(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirection:
+    """Steepest descent in parameter space (reference optimize.py:235-240); the gradient
+    is the device adjoint solve."""
+    t0 = time.perf_counter()
+    if grad is None:
+        grad = adjoint_gradient(prob, x, p)
+    return SearchDirection(dp=-np.asarray(grad, dtype=np.float64), assemble_s=time.perf_counter() - t0)
+
+
 def _lib_stream() -> int:
     from . import _lib
     return _lib.stream_handle()
 
 
-_DIRECTION_FUNCS = {"sgn": direction_sgn, "dgn": direction_dgn, "cg_gn": direction_cg_gn}
+_DIRECTION_FUNCS = {"sgn": direction_sgn, "dgn": direction_dgn, "bgn": direction_bgn, "cg_gn": direction_cg_gn,
+                    "gd": direction_gd}
 
 
 def direction_lbfgs(history, grad: np.ndarray, apply_h0=None) -> np.ndarray:

@@ -24,7 +24,7 @@ from .errors import CapabilityMissing
 from .sparse import CscMatrix, stack_kkt_blocks
 
 __all__ = ["EquilibriumProblem", "GnBlocks", "KktSystem", "gn_blocks", "kkt_from_blocks",
-           "assemble_sgn", "adjoint_gradient"]
+           "assemble_sgn", "adjoint_gradient", "solve_block_gn"]
 
 
 class EquilibriumProblem:
@@ -167,3 +167,17 @@ def assemble_sgn(prob, x, p, blocks: GnBlocks | None = None) -> KktSystem:
         return KktSystem(K, rhs, n_x, n_p, n_x)
     blocks = blocks or gn_blocks(prob, x, p)
     return kkt_from_blocks(blocks, prob.constraint_jac_x(x, p), prob.constraint_jac_p(x, p), g)
+
+
+def solve_block_gn(prob, x, p, A: CscMatrix) -> np.ndarray:
+    """Block-substitution Gauss-Newton step for B = C = 0 (sensitivity.py:269-284):
+    dp = (dc/dp)^{-1} (dc/dx) A^{-1} (df/dx)^T -- two device factorizations (A symmetric
+    LDL^T; the square unsymmetric dc/dp through its saddle form, ``SparseFactorization``)."""
+    from .errors import NonSquareParamJacobian
+    from .linear_solvers import factor_sparse
+    if prob.n_p != prob.n_c:
+        raise NonSquareParamJacobian(f"block solve needs n_p == n_c, got n_p={prob.n_p}, n_c={prob.n_c}")
+    dy = factor_sparse(A).solve(prob.objective_grad_x(x, p))
+    rhs = prob.constraint_jac_x(x, p).to_scipy() @ dy
+    return factor_sparse(prob.constraint_jac_p(x, p)).solve(rhs)
+

@@ -10,6 +10,9 @@
   (optimize.py:433-457) and 'lbfgs' on the spring bar 11x3, 6 iterations
 * ref_cg_gn.npz -- direction_cg_gn (optimize.py:212-232) on the spring bars 5x3 / 11x3 at
   cg_eta 1e-3 and 1e-10
+* ref_bgn.npz -- direction_bgn / direction_sgn on the spring bars 6x3 / 11x3 (w_reg 0), the
+  reference's unsymmetric factor_sparse(dc/dp) solves (plain and transposed), and a
+  4-iteration 'bgn' minimize trajectory
 The GPU path must emit the same schemas.
 """
 from __future__ import annotations
@@ -71,6 +74,32 @@ def main():
             cg[f"res_{nw}x{nh}_{eta:g}"] = sd.relative_residual
         cg[f"x_{nw}x{nh}"], cg[f"p_{nw}x{nh}"], cg[f"g_{nw}x{nh}"] = x, p, g
     np.savez(os.path.join(HERE, "ref_cg_gn.npz"), **cg)
+    # block-substitution GN (optimize.py:201-209, sensitivity.py:269-284) and the unsymmetric
+    # sparse solve it needs (SuperLU in the reference, linear_solvers.py:61-97)
+    from sgnopt.optimize import direction_bgn, direction_sgn
+    bgn = {}
+    for nw, nh in ((6, 3), (11, 3)):
+        prob = build_spring_bar(nw, nh, w_reg=0.0)
+        p = prob.default_parameters()
+        x = prob.simulate(p)
+        k = f"{nw}x{nh}"
+        bgn[f"x_{k}"], bgn[f"p_{k}"] = x, p
+        bgn[f"dp_bgn_{k}"] = direction_bgn(prob, x, p, OptimizerConfig()).dp
+        bgn[f"dp_sgn_{k}"] = direction_sgn(prob, x, p, OptimizerConfig()).dp
+        gp = prob.constraint_jac_p(x, p)
+        rhs = np.random.default_rng(7).standard_normal(gp.rows)
+        fac = factor_sparse(gp)
+        bgn[f"gp_indptr_{k}"], bgn[f"gp_indices_{k}"], bgn[f"gp_data_{k}"] = gp.indptr, gp.indices, gp.data
+        bgn[f"gp_rhs_{k}"] = rhs
+        bgn[f"gp_sol_{k}"] = fac.solve(rhs)
+        bgn[f"gp_solT_{k}"] = fac.solve(rhs, transpose=True)
+        bgn[f"gp_fill_{k}"] = fac.fill_nnz
+    prob = build_spring_bar(6, 3, w_reg=0.0)
+    run = minimize(prob, prob.default_parameters(),
+                   OptimizerConfig(method="bgn", max_iterations=4, gradient_tolerance=1e-12))
+    bgn["traj_bgn_f"] = run.f_values()
+    bgn["traj_bgn_g"] = run.grad_norms()
+    np.savez(os.path.join(HERE, "ref_bgn.npz"), **bgn)
     print("wrote", out, "ref_convergence_sgn_5x3.csv and ref_lbfgs_11x3.npz")
 
 
