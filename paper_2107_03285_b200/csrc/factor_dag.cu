@@ -387,100 +387,93 @@ __device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k
   }
 }
 
-// One block of the solve panel Z = [I; L21] L11^{-1}: rows r0..r0+31 ("slab"), column
-// block cb.  Z L11 = B (B = e_r on pivot rows, L21 on struct rows) gives
-//   Z[slab, cb] L_cb = B[slab, cb] - sum_{blk > cb} Z[slab, blk] L11[blk, cb]
-// (the sum on DMMA over blocks finished by the earlier tasks of this slab), then a
-// right-to-left substitution with the unit lower diagonal block L_cb, done by trsm_rows
-// on column-reversed layouts.  The slab's first task also publishes the factored
-// diagonal block r0/32 from scratch into F.
-__device__ void f_ztask_pre(const sgn::FactorArgs& A, const DFront& F, int b, int r0, int cb, Smem& S) {
+// One block Z(t, cb) of the solve panel Z = [I; L21] L11^{-1} (L11 unit lower, the 2x2
+// pivot slots belong to D), t a tile of the split grid, cb a pivot column block:
+//   pivot tile t < P:   Z(t, cb) = L(t,t)^{-1} (delta_{t,cb} I - sum_{j=cb}^{t-1} L(t,j) Z(j,cb))
+//   struct tile t >= P: Z(t, cb) = sum_{j=cb}^{P-1} L(t,j) Z(j,cb)
+// Pivot rows go top-down, so block (t, cb) needs only D_t and the tiles above it in its
+// column block: the panel of a front's pivot tile t is built while steps > t are still
+// being factored, and the last one is one task after the front's last pivot step.  The
+// sum is on DMMA; the left solve with L(t,t) is trsm_rows on the transposed block
+// against the published L^T of step t.  Block (t, t) also publishes the factored diagonal
+// block from scratch into F.  Returns the transposed block in S.b[0] (Pw[col][row]).
+__device__ void f_ztask_pre(const sgn::FactorArgs& A, const DFront& F, int b, int t, int cb, Smem& S) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
-  const int nr = min(kTile, F.nrow - r0);
-  const int npiv = F.npiv;
+  const int npiv = F.npiv, P = sgn::ptiles(npiv);
+  const int lo = sgn::tile_lo(npiv, t), nr = sgn::tile_hi(npiv, F.nrow, t) - lo;
+  const bool piv = t < P;
   const int64_t ld = F.nrow;
   double* Fm = front_ptr(A, F, b);
-  double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
+  const double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
   const double* ds = A.dscr + (int64_t)b * A.dstride + F.doff;
-  const int cmax = (r0 < npiv) ? min(npiv, r0 + nr) : npiv;
-  const int nbs = (cmax + kTile - 1) / kTile;
   const int c0 = cb * kTile, wb = min(kTile, npiv - c0);
-  if (cb == nbs - 1 && r0 < npiv) {
-    const double* blk = ds + (int64_t)(r0 / kTile) * sgn::kDiagStride;
-    const int wd = min(kTile, npiv - r0);
+  if (piv && cb == t) {
+    const double* blk = ds + (int64_t)t * sgn::kDiagStride;
     for (int e = tid; e < kTile * kTile; e += kFThreads) {
       const int i = e >> 5, j = e & 31;
-      if (i < wd && j < wd && i >= j) Fm[(int64_t)(r0 + j) * ld + r0 + i] = __ldcg(blk + e);
+      if (i < nr && j < nr && i >= j) Fm[(int64_t)(lo + j) * ld + lo + i] = __ldcg(blk + e);
     }
   }
-  double (*Tr)[kTile + 1] = v33(S.b[0]);
-  double (*X)[kTile + 1] = v33(S.b[1]);
-  V40 Zk = v40(S.b[2]);     // K-major: Zk[kk][row]
-  V40 Lk = v40(S.b[3]);     // K-major: Lk[kk][col]
-  // X[m'][m] = L_cb[31-m'][31-m] = L^T_cb[31-m][31-m'] (m' < m): the reversed unit lower
-  // block (D slots already cleared in the scratch L^T)
-  for (int e = tid; e < kTile * kTile; e += kFThreads) {
-    const int mp = e >> 5, m = e & 31;
-    X[mp][m] = (mp < m) ? __ldcg(ds + (int64_t)cb * sgn::kDiagStride + kTile * kTile + (31 - m) * kTile + (31 - mp)) : 0.0;
+  double (*Pw)[kTile + 1] = v33(S.b[0]);
+  V40 Lk = v40(S.b[2]);     // K-major: Lk[kk][row] = L(lo + row, k0 + kk)
+  V40 Zk = v40(S.b[3]);     // K-major: Zk[kk][col] = Z(k0 + kk, c0 + col)
+  if (piv) {                // L^T of step t for the left solve
+    double (*Lt)[kTile + 1] = v33(S.b[1]);
+    const double* lt = ds + (int64_t)t * sgn::kDiagStride + kTile * kTile;
+    for (int e = tid; e < kTile * kTile; e += kFThreads) Lt[e >> 5][e & 31] = __ldcg(lt + e);
   }
   const int row0 = warp * 8, i = row0 + g;
   double acc[4][2];
 #pragma unroll
   for (int nf = 0; nf < 4; ++nf) acc[nf][0] = acc[nf][1] = 0.0;
-  for (int blk = cb + 1; blk < nbs; ++blk) {
-    const int k0 = blk * kTile;
-    double vz[8], vl[8];
+  const int jend = piv ? t : P;
+  for (int j = cb; j < jend; ++j) {
+    const int k0 = j * kTile, kw = min(kTile, npiv - k0);
+    double vl[8], vz[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = tid + u * kFThreads;
       const int r = e & 31, c = e >> 5;
-      // Z[r0 + r, k0 + c]: mask the columns past npiv too -- they lie outside this front's Z
-      // storage, and 0 (L11 padding) x NaN (whatever is there) would poison the block
-      vz[u] = (r < nr && k0 + c < npiv) ? __ldcg(Zm + (int64_t)(k0 + c) * ld + r0 + r) : 0.0;
-      vl[u] = (k0 + r < npiv && c < wb) ? __ldcg(Fm + (int64_t)(c0 + c) * ld + k0 + r) : 0.0; // L11[k0 + r, c0 + c]
+      vl[u] = (r < nr && c < kw) ? __ldcg(Fm + (int64_t)(k0 + c) * ld + lo + r) : 0.0;  // L(lo + r, k0 + c)
+      vz[u] = (r < kw && c < wb) ? __ldcg(Zm + (int64_t)(c0 + c) * ld + k0 + r) : 0.0;  // Z(k0 + r, c0 + c)
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = tid + u * kFThreads;
       const int r = e & 31, c = e >> 5;
-      Zk[c][r] = vz[u];
-      Lk[r][c] = vl[u];
+      Lk[c][r] = vl[u];
+      Zk[r][c] = vz[u];
     }
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < kTile; kk += 4) {
-      const double a = Zk[kk + q][row0 + g];
+      const double a = Lk[kk + q][row0 + g];
 #pragma unroll
-      for (int nf = 0; nf < 4; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], a, Lk[kk + q][nf * 8 + g]);
+      for (int nf = 0; nf < 4; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], a, Zk[kk + q][nf * 8 + g]);
     }
     __syncthreads();
   }
-  // T = B - acc, stored column-reversed
 #pragma unroll
   for (int nf = 0; nf < 4; ++nf)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int j = nf * 8 + 2 * q + h;
-      double t = 0.0;
-      if (i < nr && j < wb) {
-        const int r = r0 + i, col = c0 + j;
-        const double bv = (r < npiv) ? (r == col ? 1.0 : 0.0) : __ldcg(Fm + (int64_t)col * ld + r);
-        t = bv - acc[nf][h];
-      }
-      Tr[i][31 - j] = t;
+      double v = 0.0;
+      if (i < nr && j < wb) v = piv ? (((cb == t && i == j) ? 1.0 : 0.0) - acc[nf][h]) : acc[nf][h];
+      Pw[j][i] = v;
     }
 }
 
-__device__ void f_ztask_post(const sgn::FactorArgs& A, const DFront& F, int b, int r0, int cb, Smem& S) {
+__device__ void f_ztask_post(const sgn::FactorArgs& A, const DFront& F, int b, int t, int cb, Smem& S) {
   const int tid = threadIdx.x;
-  const int nr = min(kTile, F.nrow - r0);
+  const int lo = sgn::tile_lo(F.npiv, t), nr = sgn::tile_hi(F.npiv, F.nrow, t) - lo;
   const int64_t ld = F.nrow;
   double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
   const int c0 = cb * kTile, wb = min(kTile, F.npiv - c0);
-  double (*Tr)[kTile + 1] = v33(S.b[0]);
+  double (*Pw)[kTile + 1] = v33(S.b[0]);
   for (int e = tid; e < kTile * kTile; e += kFThreads) {
     const int ii = e & 31, c = e >> 5;
-    if (ii < nr && c < wb) Zm[(int64_t)(c0 + c) * ld + r0 + ii] = Tr[ii][31 - c];
+    if (ii < nr && c < wb) Zm[(int64_t)(c0 + c) * ld + lo + ii] = Pw[c][ii];
   }
 }
 
@@ -528,12 +521,14 @@ k_factor_dag(const sgn::FactorArgs A) {
       } else if (kind == sgn::F_UPDATE || kind == sgn::F_DIAGUPD) {   // PAN(k) awaited inside
         const int ti = (kind == sgn::F_DIAGUPD) ? k + 1 : T.a, tj = (kind == sgn::F_DIAGUPD) ? k + 1 : T.b;
         spin_ge(cf + sgn::cnt_tile(P, ti, tj), 1 + k);
-      } else {
-        spin_ge(cf, F.ftotal);
-        const int r0 = T.a, nr = min(kTile, F.nrow - r0);
-        const int cmax = (r0 < F.npiv) ? min(F.npiv, r0 + nr) : F.npiv;
-        const int nbs = (cmax + kTile - 1) / kTile;
-        spin_ge(cf + sgn::cnt_zc(P, Tn, r0 / kTile), nbs - 1 - T.b);
+      } else {                                    // Z(t, cb): see f_ztask_pre
+        if (T.a < P) {
+          spin_ge(cf + sgn::cnt_diag(P, T.a), 1);
+          if (T.a > T.b) spin_ge(cf + sgn::cnt_zc(P, Tn, T.b), T.a - T.b);
+        } else {
+          spin_ge(cf, F.ftotal);
+          spin_ge(cf + sgn::cnt_zc(P, Tn, T.b), P - T.b);
+        }
       }
     }
     __syncthreads();
@@ -556,7 +551,7 @@ k_factor_dag(const sgn::FactorArgs A) {
       if (dg) { fac_k = k + 1; fac_tile = v33(S.b[1]); }
     } else {
       f_ztask_pre(A, F, b, T.a, T.b, S);
-      nr_trsm = (tid < 32) ? 32 : 0;
+      nr_trsm = (T.a < P && tid < 32) ? 32 : 0;
       tr_l = v33(S.b[1]);
     }
     if (fac_k >= 0) factor_publish(A, F, b, fac_k, fac_tile, S);
@@ -572,7 +567,7 @@ k_factor_dag(const sgn::FactorArgs A) {
       int* s1;
       int* s2 = cf;                                            // DONE
       int* s3 = nullptr;
-      if (kind == sgn::F_ZPANEL) { s1 = cf + sgn::cnt_zc(P, Tn, T.a / kTile); s2 = nullptr; }
+      if (kind == sgn::F_ZPANEL) { s1 = (T.a < P) ? cf + sgn::cnt_zc(P, Tn, T.b) : nullptr; s2 = nullptr; }
       else if (kind == sgn::F_PANEL) s1 = cf + sgn::cnt_pan(k);
       else if (kind == sgn::F_DIAGUPD) { s1 = cf + sgn::cnt_tile(P, k + 1, k + 1); s3 = cf + sgn::cnt_diag(P, k + 1); }
       else {
@@ -580,7 +575,7 @@ k_factor_dag(const sgn::FactorArgs A) {
         if (kind == sgn::F_ASM && T.a == 0 && T.b == 0 && F.npiv > 0) s3 = cf + sgn::cnt_diag(P, 0);
       }
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(s1) : "memory");
+      if (s1) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(s1) : "memory");
       if (s2) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(s2) : "memory");
       if (s3) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(s3) : "memory");
     }

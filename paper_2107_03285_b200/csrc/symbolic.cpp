@@ -19,6 +19,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -747,19 +748,36 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   auto ft = [&](int32_t kind, int32_t k, int32_t f, int32_t a, int32_t b) {
     s.ftasks.push_back(FTask{kind | (k << 3), f, a, b});
   };
-  // Z blocks (slab r0, column block cb), right to left within a slab
-  auto add_ztasks = [&](const std::vector<int32_t>& fl) {
-    for (int32_t f : fl) {
+  // Z blocks Z(t, cb) (f_ztask_pre): pivot tiles top-down, then the struct tiles.  Fronts
+  // with at least kZInlineSteps pivot steps (the dependency-chain-bound upper fronts) get
+  // their pivot-tile blocks right after pivot step t, so the panel is built while the
+  // front is still being factored; all other blocks go to a queue (bottom levels first).
+  constexpr int32_t kZInlineSteps = 8;
+  std::vector<FTask> zq;
+  std::vector<int32_t> zq_level;
+  auto z_inline = [&](const Front& F) { return ptiles(F.npiv) >= kZInlineSteps; };
+  for (int32_t lv = 0; lv < s.n_levels; ++lv)
+    for (int32_t f : s.level_fronts[lv]) {
       const Front& F = s.fronts[f];
       if (F.npiv == 0) continue;
-      const int32_t nb = (F.npiv + kTile - 1) / kTile;
-      for (int32_t cb = nb - 1; cb >= 0; --cb)
-        for (int32_t r0 = 0; r0 < F.nrow; r0 += kTile) {
-          const int32_t nr = std::min(kTile, F.nrow - r0);
-          const int32_t cmax = (r0 < F.npiv) ? std::min(F.npiv, r0 + nr) : F.npiv;
-          if (cb < (cmax + kTile - 1) / kTile) ft(F_ZPANEL, 0, f, r0, cb);
+      const int32_t P = ptiles(F.npiv), T = ntiles_front(F.npiv, F.nrow);
+      for (int32_t t = z_inline(F) ? P : 0; t < T; ++t)
+        for (int32_t cb = 0; cb < std::min(t + 1, P); ++cb) {
+          zq.push_back(FTask{F_ZPANEL, f, t, cb});
+          zq_level.push_back(lv);
         }
     }
+  // Queued blocks are interleaved into the upper levels' schedule: after every pivot step
+  // of level lv, up to zquota blocks of fronts at levels <= lv - 2 (finished by the time
+  // the grab reaches them, so they never hold a CTA waiting).  They fill the CTAs the
+  // dependency chain of the upper fronts leaves idle; the rest go last.
+  // SGN_ZQUOTA overrides the per-step quota (0 = all queued blocks last).
+  size_t zhead = 0;
+  int64_t zquota = 256;
+  if (const char* e = std::getenv("SGN_ZQUOTA")) zquota = std::atoll(e);
+  auto emit_z = [&](int32_t lv) {
+    for (int64_t q = 0; q < zquota && zhead < zq.size() && zq_level[zhead] <= lv - 2; ++q)
+      s.ftasks.push_back(zq[zhead++]);
   };
   for (int32_t lv = 0; lv < s.n_levels; ++lv) {
     const auto& fl = s.level_fronts[lv];
@@ -797,11 +815,15 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
         for (int32_t tj = k + 2; tj < T; ++tj)
           for (int32_t ti = tj; ti < T; ++ti) ft(F_UPDATE, k, f, ti, tj);
       }
+      for (int32_t f : fl) {                                 // inline Z row of pivot tile k
+        const Front& F = s.fronts[f];
+        if (k < ptiles(F.npiv) && z_inline(F))
+          for (int32_t cb = 0; cb <= k; ++cb) ft(F_ZPANEL, 0, f, k, cb);
+      }
+      emit_z(lv);
     }
   }
-  // solve-panel blocks last (bottom levels first): they fill the CTAs left idle by the
-  // top levels' dependency chain instead of delaying the levels above
-  for (int32_t lv = 0; lv < s.n_levels; ++lv) add_ztasks(s.level_fronts[lv]);
+  while (zhead < zq.size()) s.ftasks.push_back(zq[zhead++]);
   // solve work lists: gather (f), forward GEMV (f, row0, chunk, group), backward dots
   // (f, col0, row chunk, group); each (front, tile) group combines its chunk partials
   s.fwd_off.assign(s.n_levels, 0); s.fwd_cnt.assign(s.n_levels, 0);

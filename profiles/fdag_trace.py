@@ -11,7 +11,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-KIND = {0: "asm", 1: "panel", 2: "update", 3: "zpanel"}
+KIND = {0: "asm", 1: "panel", 2: "update", 3: "zpanel", 4: "diagupd"}
 
 
 def main():
@@ -47,16 +47,18 @@ def main():
     np.savez(a.out, T=T, M=M, sm=tr[:, 3], meta=meta)
     kind, step, front, lvl = meta[:, 0], meta[:, 1], meta[:, 2], meta[:, 3]
     print("span us %.1f tasks %d" % (T[:, 2].max(), len(T)))
-    for k in range(4):
+    for k in range(5):
         m = kind == k
         if m.any():
             print(f"{KIND[k]:7s} n={m.sum():6d} busy_med={np.median(T[m, 2] - T[m, 1]):6.2f} "
                   f"wait_med={np.median(T[m, 1] - T[m, 0]):6.2f} busy_sum_us={np.sum(T[m, 2] - T[m, 1]):9.1f}")
     print("per level: first ready / last end (us)")
     for L in sorted(set(lvl.tolist())):
-        m = lvl == L
+        m = (lvl == L) & (kind != 3)
+        z = (lvl == L) & (kind == 3)
         print(f"L{L:2d} n={m.sum():6d} ready={T[m, 1].min():8.1f} end={T[m, 2].max():8.1f} "
-              f"panels={np.sum(m & (kind == 1)):5d} steps={step[m].max() + 1:3d}")
+              f"panels={np.sum(m & (kind == 1)):5d} steps={step[m].max() + 1:3d}"
+              + (f" | z n={z.sum():5d} {T[z, 1].min():8.1f}-{T[z, 2].max():8.1f}" if z.any() else ""))
     # critical chain of the top front: per step, panel end and look-ahead update end
     top = front[np.argmax(lvl)]
     m = front == top
