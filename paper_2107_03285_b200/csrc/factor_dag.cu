@@ -590,13 +590,19 @@ k_factor_dag(const sgn::FactorArgs A) {
 
 namespace sgn {
 
-int factor_dag_grid() {
-  int dev = 0, sms = 0, per_sm = 0;
+int factor_dag_grid(int ctas_per_sm) {
+  static int cached_dev = -1, sms = 0, occ = 0;     // one device per process
+  int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
-  if (cudaFuncSetAttribute(k_factor_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem)) != cudaSuccess) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_factor_dag, kFThreads, sizeof(Smem)) != cudaSuccess) return 0;
-  return sms * std::max(per_sm, 1);
+  if (dev != cached_dev) {
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    if (cudaFuncSetAttribute(k_factor_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem)) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_factor_dag, kFThreads, sizeof(Smem)) != cudaSuccess) return 0;
+    cached_dev = dev;
+  }
+  int per_sm = std::max(occ, 1);
+  if (ctas_per_sm > 0) per_sm = std::min(per_sm, ctas_per_sm);
+  return sms * per_sm;
 }
 
 int launch_factor_dag(const FactorArgs& A, int grid, void* stream) {

@@ -999,6 +999,14 @@ int sgn_factor_min_pivot(sgn_factor f, double* min_pivot, int64_t* position, voi
   return sgn::min_pivot(f->fronts.p, (int32_t)s.fronts.size(), f->fstore.p, min_pivot, position, stream);
 }
 
+int sgn_factor_set_ctas_per_sm(sgn_factor f, int32_t ctas_per_sm) {
+  if (!f || ctas_per_sm < 0) { sgn::last_error() = "set_ctas_per_sm: invalid argument"; return SGN_INVALID; }
+  const int g = sgn::factor_dag_grid(ctas_per_sm);
+  if (g <= 0) { sgn::last_error() = "set_ctas_per_sm: no CUDA device"; return SGN_CUDA_ERROR; }
+  f->factor_grid = g;
+  return SGN_OK;
+}
+
 int sgn_factor_solve_multi(sgn_factor f, const double* d_B, double* d_X, int32_t nrhs, void* stream) {
   if (f->batch != 1) { sgn::last_error() = "multi-RHS solves need a batch-1 factor"; return SGN_INVALID; }
   return launch_solve_multi(f, d_B, d_X, nrhs, (cudaStream_t)stream);

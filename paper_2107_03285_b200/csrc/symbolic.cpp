@@ -522,6 +522,8 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   s.fronts.assign(NF, Front());
   s.front_of_pos.assign(n, -1);
   int64_t pos = 0;
+  bool generic_pairs = true;
+  if (const char* e = std::getenv("SGN_GENERIC_PAIRS")) generic_pairs = std::atoi(e) != 0;
   for (int32_t k = 0; k < NF; ++k) {
     const NdFront& src = nd[post[k]];
     Front& F = s.fronts[k];
@@ -529,7 +531,10 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     F.parent = src.parent >= 0 ? newid[src.parent] : -1;
     if (post[k] == proot) {
       F.is_root_p = 1;
-      F.pivtype = 1;
+      // the p block's Schur complement is the (regularized) reduced Gauss-Newton Hessian:
+      // 2x2 pivots on consecutive p unknowns halve the serial pivot chain of the root's
+      // diagonal blocks (an even count keeps every pair inside one 32-column tile)
+      F.pivtype = (s.pair_mode && s.n_p % 2 == 0) ? 2 : 1;
       for (int64_t u = s.n_x; u < s.n_x + s.n_p; ++u) s.perm[pos++] = u;
     } else {
       F.pivtype = s.pair_mode ? 2 : 1;
@@ -539,6 +544,11 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
             if (node_unk[v][t] >= 0) s.perm[pos++] = node_unk[v][t];
     }
     F.npiv = (int32_t)(pos - F.first);
+    // generic mode: consecutive unknowns of an even-sized front are pivoted as 2x2 blocks
+    // (half the serial chain of the diagonal-block LDL^T).  A 2x2 principal block of an
+    // SPD matrix is SPD, and a block is singular only if the 1x1 pair would be too
+    // (d2 = det / a); SGN_GENERIC_PAIRS=0 keeps 1x1 pivots.
+    if (!s.pair_mode && generic_pairs && F.npiv % 2 == 0) F.pivtype = 2;
   }
   if (pos != n) { last_error() = "internal: ordering does not cover all unknowns"; return 5; }
   for (int64_t q = 0; q < n; ++q) s.ipos[s.perm[q]] = q;

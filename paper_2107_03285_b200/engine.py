@@ -213,6 +213,8 @@ class MeshPlan:
 
 
 _SIDE_STREAM = os.environ.get("SGN_SIDE_STREAM", "1") != "0"
+_KKT_CTAS = int(os.environ.get("SGN_KKT_CTAS", "3"))
+_GX_CTAS = int(os.environ.get("SGN_GX_CTAS", "1"))
 _DEBUG_NAN = os.environ.get("SGN_DEBUG_NAN", "0") == "1"
 
 
@@ -250,6 +252,11 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
         # refined solve (still before any convergence error, as in the reference).
         if not hasattr(eng, "_side_stream"):
             eng._side_stream = torch.cuda.Stream()
+        # split the persistent CTA slots: 4 per SM fit; the KKT factor takes _KKT_CTAS of
+        # them and the G_x factor the rest, so both run from the start instead of G_x
+        # waiting for the KKT grid to retire (the G_x factor keeps the full grid elsewhere)
+        eng.kfac.set_ctas_per_sm(_KKT_CTAS)
+        eng.gfac.set_ctas_per_sm(_GX_CTAS)
         side = eng._side_stream
         ev_asm, ev_adj = torch.cuda.Event(), torch.cuda.Event()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -269,6 +276,7 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
             eng.rhs.copy_(eng.tmp)
             ev_adj.record(side)
         cur.wait_event(ev_adj)
+        eng.gfac.set_ctas_per_sm(0)
         if events is not None:
             events[1].record()
         if timings is not None:

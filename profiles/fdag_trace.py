@@ -18,6 +18,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--out", default="gpurun_out/fdag_trace.npz")
+    ap.add_argument("--which", default="kkt", choices=("kkt", "gx"), help="KKT or G_x (adjoint) factor")
     a = ap.parse_args()
     os.environ["SGN_FDAG_TRACE"] = "1"
     import torch
@@ -28,9 +29,12 @@ def main():
     prob._load(x, p0)
     eng = prob.engine
     eng.direction()
-    fac = eng.kfac
+    fac = eng.kfac if a.which == "kkt" else eng.gfac
     for _ in range(3):
-        fac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda)
+        if a.which == "kkt":
+            fac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda)
+        else:
+            fac.numeric(eng.gvals, 0.0, 0.0)
     torch.cuda.synchronize()
     nt = ctypes.c_int64()
     lib().sgn_debug_factor_trace(fac._h, None, 0, ctypes.byref(nt), None)
