@@ -321,7 +321,181 @@ __device__ bool dag_bwd(const SolveArgs& A, const sgn::Task& T, int b, const int
   return true;
 }
 
-__global__ void __launch_bounds__(kSolveThreads)
+// Forward task of a whole small front (npiv <= 64, nrow <= kFatRows; symbolic.cpp
+// "fat" work items): dag_fwd's 32-row tiles, up to 8 of them, in one CTA, so a bottom-level
+// front is one task (no extra waves, no chunk groups).  Z is held 4 tiles at a time (the
+// first 4 prefetched before the wait); per row tile the sums are dag_fwd's.
+__device__ bool dag_fwd_fat(const SolveArgs& A, const sgn::Task& T, int b, const int* cnt, int64_t idx) {
+  constexpr int RT = 4, NT = sgn::kFatRows / 32, NV = sgn::kFwdCols + sgn::kFatRows;
+  __shared__ double redf[NT][8][33];
+  __shared__ double vsf[NV];
+  const DFront F = A.fronts[T.f];
+  if (A.nop || (A.leading && F.is_root_p)) { dag_wait(A, T, cnt); return true; }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int npiv = F.npiv, nrow = F.nrow;
+  const int ntile = (nrow + 31) / 32;
+  const double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
+  const int64_t ld = nrow;
+  double z[RT][8];
+  auto load_z = [&](int t0) {
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      const int r = 32 * (t0 + t) + lane;
+      const int climit = (r < npiv) ? min(npiv, 32 * (t0 + t) + 32) : npiv;   // Z(t, cb), cb <= t
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int c = warp + 8 * m;
+        z[t][m] = (r < nrow && c < climit) ? Zm[(int64_t)c * ld + r] : 0.0;
+      }
+    }
+  };
+  load_z(0);
+  // v entries: e < kFwdCols -> pivot column e; e >= kFwdCols -> struct row npiv + e - kFwdCols
+  auto v_row = [&](int e) { return e < sgn::kFwdCols ? (e < npiv ? e : -1)
+                                                      : (npiv + e - sgn::kFwdCols < nrow ? npiv + e - sgn::kFwdCols : -1); };
+  const int vr = v_row(tid);
+  double base = 0.0;
+  int64_t q0 = 0, q1 = 0;
+  int sq[4] = {0, 0, 0, 0};
+  if (vr >= 0) {
+    base = (vr < npiv) ? A.b_in[(int64_t)b * A.n + A.perm[F.first + vr]] : 0.0;
+    q0 = A.gptr[F.voff + vr];
+    q1 = A.gptr[F.voff + vr + 1];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (q0 + j < q1) sq[j] = A.gsrc[q0 + j];
+  }
+  double da = 1.0, db = 0.0, dc = 1.0;            // D entries of row 32 warp + lane
+  {
+    const int r = 32 * warp + lane;
+    if (warp < NT && r < npiv) {
+      const double* Fm = A.fstore + (int64_t)b * A.fstride + F.foff;
+      if (F.pivtype == 2) {
+        const int re = r & ~1;
+        da = Fm[(int64_t)re * ld + re]; db = Fm[(int64_t)re * ld + re + 1]; dc = Fm[(int64_t)(re + 1) * ld + re + 1];
+      } else {
+        da = Fm[(int64_t)r * ld + r];
+      }
+    }
+  }
+  dag_mark(A, idx, 2);
+  dag_wait(A, T, cnt);
+  dag_mark(A, idx, 3);
+  const double* ub = A.ubuf + (int64_t)b * A.ustride;
+  {
+    double v = 0.0;
+    if (vr >= 0) {
+      double u[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) u[j] = (q0 + j < q1) ? __ldcg(ub + sq[j]) : 0.0;
+      v = base;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) if (q0 + j < q1) v += u[j];
+      for (int64_t q = q0 + 4; q < q1; ++q) v += __ldcg(ub + A.gsrc[q]);
+    }
+    vsf[tid] = v;
+  }
+  for (int e = tid + kSolveThreads; e < NV; e += kSolveThreads) {   // struct rows past 192
+    const int r2 = v_row(e);
+    double v = 0.0;
+    if (r2 >= 0)
+      for (int64_t q = A.gptr[F.voff + r2]; q < A.gptr[F.voff + r2 + 1]; ++q) v += __ldcg(ub + A.gsrc[q]);
+    vsf[e] = v;
+  }
+  __syncthreads();
+  for (int t0 = 0; t0 < ntile; t0 += RT) {
+    if (t0 > 0) load_z(t0);
+#pragma unroll
+    for (int t = 0; t < RT; ++t) {
+      if (t0 + t < NT) {
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) acc += z[t][m] * vsf[warp + 8 * m];
+        redf[t0 + t][warp][lane] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp < ntile) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += redf[warp][w][lane];
+    const double tp = __shfl_xor_sync(0xffffffffu, t, 1);   // 2x2 pivot partner row
+    const int r = 32 * warp + lane;
+    if (r < npiv) {
+      double* zb = A.zbuf + (int64_t)b * A.n;
+      if (F.pivtype == 2) {
+        const double det = da * dc - db * db;
+        zb[F.first + r] = ((r & 1) == 0) ? (dc * t - db * tp) / det : (da * t - db * tp) / det;
+      } else {
+        zb[F.first + r] = t / da;
+      }
+    } else if (r < nrow) {
+      A.ubuf[(int64_t)b * A.ustride + F.uoff + (r - npiv)] = vsf[sgn::kFwdCols + (r - npiv)] - t;
+    }
+  }
+  return true;
+}
+
+// Backward task of a whole small front: x1 = Z^T [z1; -x2] over all its rows
+// (<= kFatRowsBwd, prefetched before the wait) and pivot columns (<= 64) in one CTA.
+__device__ bool dag_bwd_fat(const SolveArgs& A, const sgn::Task& T, int b, const int* cnt, int64_t idx) {
+  constexpr int RT = sgn::kFatRowsBwd / 32;
+  __shared__ double vsb[sgn::kFatRowsBwd];
+  const DFront F = A.fronts[T.f];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int np = F.npiv, nrow = F.nrow;
+  double* xb = A.xbuf + (int64_t)b * A.n;
+  double* xo = A.x_out + (int64_t)b * A.n;
+  if (A.nop) { dag_wait(A, T, cnt); return true; }
+  if (A.leading && F.is_root_p) {
+    dag_wait(A, T, cnt);
+    for (int j = tid; j < np; j += blockDim.x) {
+      xb[F.first + j] = 0.0;
+      xo[A.perm[F.first + j]] = 0.0;
+    }
+    return true;
+  }
+  const double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
+  const int64_t ld = nrow;
+  double z[8][RT];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const int j = warp + 8 * m;
+#pragma unroll
+    for (int i = 0; i < RT; ++i) {
+      const int r = lane + 32 * i;
+      z[m][i] = (j < np && r < nrow && r >= j) ? Zm[(int64_t)j * ld + r] : 0.0;
+    }
+  }
+  int64_t srow = -1;
+  if (tid < nrow && tid >= np) srow = A.srows[F.srow_off + tid - np];
+  dag_mark(A, idx, 2);
+  dag_wait(A, T, cnt);
+  dag_mark(A, idx, 3);
+  if (tid < sgn::kFatRowsBwd) {
+    double v = 0.0;
+    if (tid < nrow) v = (tid < np) ? __ldcg(A.zbuf + (int64_t)b * A.n + F.first + tid) : -__ldcg(xb + srow);
+    vsb[tid] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    double a = 0.0;
+#pragma unroll
+    for (int i = 0; i < RT; ++i) a += z[m][i] * vsb[lane + 32 * i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    const int j = warp + 8 * m;
+    if (lane == 0 && j < np) {
+      xb[F.first + j] = a;
+      xo[A.perm[F.first + j]] = a;
+    }
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(kSolveThreads, 3)
 k_solve_dag(const SolveArgs A) {
   __shared__ int s_idx;
   if (A.gate && *A.gate == 0) return;
@@ -338,7 +512,11 @@ k_solve_dag(const SolveArgs A) {
     int* cnt = A.cnt + (int64_t)b * A.n_cnt;
     unsigned long long t0 = 0;
     if (A.trace && threadIdx.x == 0) t0 = gtimer();
-    const bool sig = (T.kind == sgn::T_FWD) ? dag_fwd(A, T, b, cnt, idx) : dag_bwd(A, T, b, cnt, idx);
+    bool sig;
+    if (T.kind == sgn::T_FWD) sig = dag_fwd(A, T, b, cnt, idx);
+    else if (T.kind == sgn::T_BWD) sig = dag_bwd(A, T, b, cnt, idx);
+    else if (T.kind == sgn::T_FWD_FAT) sig = dag_fwd_fat(A, T, b, cnt, idx);
+    else sig = dag_bwd_fat(A, T, b, cnt, idx);
     __syncthreads();                               // every thread's writes precede the release
     if (sig && threadIdx.x == 0) {
       asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(cnt + T.sig) : "memory");

@@ -106,11 +106,14 @@ constexpr int kFwdRows = 32;    // rows per CTA of the forward-solve GEMV
 constexpr int kFwdCols = 64;    // columns (K chunk) per CTA of the forward-solve GEMV
 constexpr int kBwdCols = 32;    // columns per CTA of the backward-solve dots
 constexpr int kBwdRows = 128;   // rows (K chunk) per CTA of the backward-solve dots
+constexpr int kFatRows = 256;     // rows of a one-task ("fat") forward front solve
+constexpr int kFatRowsBwd = 128;  // rows of a one-task backward front solve (Z prefetched whole)
 // Persistent dependency-driven (DAG) schedule: a task runs after every (counter, target)
 // wait in waits[w0, w1) is met, then bumps counter `sig` (-1: none).  Tasks are listed in a
 // topological order and grabbed in that order by resident CTAs, so waits always target
 // earlier tasks and the schedule cannot deadlock.
-enum TaskKind : int32_t { T_FWD = 1, T_BWD = 2 };
+// T_FWD_FAT / T_BWD_FAT: the whole forward / backward step of a small front in one task
+enum TaskKind : int32_t { T_FWD = 1, T_BWD = 2, T_FWD_FAT = 3, T_BWD_FAT = 4 };
 struct Task { int32_t kind, f, a, b, c, sig, w0, w1; };
 struct Launch { int32_t kind; int32_t level; int64_t off; int64_t count; int32_t pivtype = 1; int32_t pad = 0; };
 

@@ -842,6 +842,13 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   s.lvl_max_piv.assign(s.n_levels, 0);
   s.grp_nchunk.clear(); s.grp_base.clear();
   s.part_doubles = 0;
+  // small fronts (the bottom levels) solve as one task each (T_FWD_FAT / T_BWD_FAT);
+  // SGN_FAT_SOLVE=0 keeps the tiled tasks
+  bool fat_solve = true;
+  if (const char* e = std::getenv("SGN_FAT_SOLVE")) fat_solve = std::atoi(e) != 0;
+  auto fat_front = [&](const Front& F, int32_t rows) {
+    return fat_solve && F.npiv >= 1 && F.npiv <= kFwdCols && F.nrow <= rows;
+  };
   auto new_group = [&](int32_t nch) {
     s.grp_nchunk.push_back(nch);
     s.grp_base.push_back(s.part_doubles);
@@ -858,6 +865,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     s.fwd_off[lv] = (int64_t)s.work.size();
     for (int32_t f : s.level_fronts[lv]) {
       const Front& F = s.fronts[f];
+      if (fat_front(F, kFatRows)) { s.work.push_back({f, -1, 0, new_group(1)}); continue; }
       for (int32_t r0 = 0; r0 < F.nrow; r0 += kFwdRows) {
         const int32_t cend = (r0 < F.npiv) ? std::min(F.npiv, r0 + kFwdRows) : F.npiv;
         const int32_t nch = std::max(1, (cend + kFwdCols - 1) / kFwdCols);
@@ -869,6 +877,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     s.bwd_off[lv] = (int64_t)s.work.size();
     for (int32_t f : s.level_fronts[lv]) {
       const Front& F = s.fronts[f];
+      if (fat_front(F, kFatRowsBwd)) { s.work.push_back({f, -1, 0, new_group(1)}); continue; }
       for (int32_t c0 = 0; c0 < std::max(F.npiv, 1); c0 += kBwdCols) {
         const int32_t rs = (c0 / kBwdRows) * kBwdRows;          // first chunk holding rows >= c0
         const int32_t nch = std::max(1, (F.nrow - rs + kBwdRows - 1) / kBwdRows);
@@ -928,15 +937,16 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
         const Front& F = s.fronts[s.work[w].f];
         std::vector<std::pair<int32_t, int32_t>> ch;
         for (int32_t ci = F.child_begin; ci < F.child_end; ++ci) ch.push_back({s.children[ci], nfg[s.children[ci]]});
-        add(T_FWD, s.work[w], s.work[w].f, ch);
+        add(s.work[w].a < 0 ? T_FWD_FAT : T_FWD, s.work[w], s.work[w].f, ch);
       }
     }
     for (int32_t lv = s.n_levels - 1; lv >= 0; --lv) {
       for (int64_t w = s.bwd_off[lv]; w < s.bwd_off[lv] + s.bwd_cnt[lv]; ++w) {
         const int32_t f = s.work[w].f;
         const int32_t p = s.fronts[f].parent;
-        if (p >= 0) add(T_BWD, s.work[w], NF + f, {{NF + p, nbg[p]}});
-        else add(T_BWD, s.work[w], NF + f, {{f, nfg[f]}});
+        const int32_t kind = s.work[w].a < 0 ? T_BWD_FAT : T_BWD;
+        if (p >= 0) add(kind, s.work[w], NF + f, {{NF + p, nbg[p]}});
+        else add(kind, s.work[w], NF + f, {{f, nfg[f]}});
       }
     }
   }

@@ -54,11 +54,12 @@ def main():
     print("phase medians (us): pre = start->prefetched, wait = ->ready, comb = ready->combined (group last), fin = ->end")
     rows = []
     md = lambda v: np.nanmedian(v) if np.any(~np.isnan(v)) else float("nan")
-    for k, name in [(1, "fwd"), (2, "bwd")]:
-        for L in sorted(set(lvl[kind == k].tolist())):
-            m = (kind == k) & (lvl == L)
+    for ks, name in [((1, 3), "fwd"), ((2, 4), "bwd")]:
+        km = np.isin(kind, ks)
+        for L in sorted(set(lvl[km].tolist())):
+            m = km & (lvl == L)
             t = T[m]
-            rows.append(f"{name} L{L:2d} n={m.sum():5d} start={np.nanmin(t[:, 0]):7.2f} "
+            rows.append(f"{name} L{L:2d} n={m.sum():5d} fat={np.sum(m & (kind > 2)):4d} start={np.nanmin(t[:, 0]):7.2f} "
                         f"ready_last={np.nanmax(t[:, 2]):7.2f} end_last={np.nanmax(t[:, 4]):7.2f} "
                         f"pre={md(t[:, 1] - t[:, 0]):5.2f} wait={md(t[:, 2] - t[:, 1]):6.2f} "
                         f"comb={md(t[:, 3] - t[:, 2]):5.2f} fin={md(t[:, 4] - t[:, 3]):5.2f} "
