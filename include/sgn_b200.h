@@ -106,11 +106,12 @@ int  sgn_factor_check(sgn_factor f, void* stream, int64_t* pivot_index);
 int  sgn_factor_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, void* stream);
 void sgn_factor_destroy(sgn_factor f);
 
-/* Persistent CTAs per SM of this factor's numeric factorization (0 = the occupancy
- * limit, 4).  Two factorizations issued on concurrent streams -- the KKT factor and the
- * adjoint's G_x factor of one direction (sensitivity.py:194-198 next to
- * linear_solvers.py:130-175) -- split the SMs' CTA slots instead of queueing.           */
-int  sgn_factor_set_ctas_per_sm(sgn_factor f, int32_t ctas_per_sm);
+/* Persistent grid (CTAs) of this factor's numeric factorization; ctas <= 0 restores the
+ * default (every SM at the occupancy limit); *grid (may be NULL) = the grid in effect.
+ * Two factorizations issued on concurrent streams -- the KKT factor and the adjoint's G_x
+ * factor of one direction (sensitivity.py:194-198 next to linear_solvers.py:130-175) --
+ * split the SMs' CTA slots instead of queueing.                                        */
+int  sgn_factor_set_grid(sgn_factor f, int32_t ctas, int32_t* grid);
 
 /* X[:, j] = (L D L^T)^{-1} B[:, j] for nrhs right-hand sides against ONE factor (batch 1),
  * column j at B + j*n.  Replaces the n_p back-substitutions of sensitivity_matrix

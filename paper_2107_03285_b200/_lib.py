@@ -49,7 +49,7 @@ SIGNATURES = {
     "sgn_masked_copy": (ctypes.c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "sgn_factor_solve": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
     "sgn_factor_solve_multi": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
-    "sgn_factor_set_ctas_per_sm": (ctypes.c_int, [c_vp, c_i32]),
+    "sgn_factor_set_grid": (ctypes.c_int, [c_vp, c_i32, ctypes.POINTER(ctypes.c_int32)]),
     "sgn_factor_min_pivot": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "sgn_csc_block_dense": (ctypes.c_int, [c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp]),
     "sgn_csc_spmm": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,

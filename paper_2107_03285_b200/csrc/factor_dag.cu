@@ -590,7 +590,7 @@ k_factor_dag(const sgn::FactorArgs A) {
 
 namespace sgn {
 
-int factor_dag_grid(int ctas_per_sm) {
+int factor_dag_grid() {
   static int cached_dev = -1, sms = 0, occ = 0;     // one device per process
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
@@ -601,7 +601,6 @@ int factor_dag_grid(int ctas_per_sm) {
     cached_dev = dev;
   }
   int per_sm = std::max(occ, 1);
-  if (ctas_per_sm > 0) per_sm = std::min(per_sm, ctas_per_sm);
   return sms * per_sm;
 }
 

@@ -1177,11 +1177,12 @@ int sgn_factor_min_pivot(sgn_factor f, double* min_pivot, int64_t* position, voi
   return sgn::min_pivot(f->fronts.p, (int32_t)s.fronts.size(), f->fstore.p, min_pivot, position, stream);
 }
 
-int sgn_factor_set_ctas_per_sm(sgn_factor f, int32_t ctas_per_sm) {
-  if (!f || ctas_per_sm < 0) { sgn::last_error() = "set_ctas_per_sm: invalid argument"; return SGN_INVALID; }
-  const int g = sgn::factor_dag_grid(ctas_per_sm);
-  if (g <= 0) { sgn::last_error() = "set_ctas_per_sm: no CUDA device"; return SGN_CUDA_ERROR; }
-  f->factor_grid = g;
+int sgn_factor_set_grid(sgn_factor f, int32_t ctas, int32_t* grid) {
+  if (!f) { sgn::last_error() = "set_grid: invalid argument"; return SGN_INVALID; }
+  const int full = sgn::factor_dag_grid();
+  if (full <= 0) { sgn::last_error() = "set_grid: no CUDA device"; return SGN_CUDA_ERROR; }
+  f->factor_grid = (ctas > 0) ? std::min(ctas, full) : full;
+  if (grid) *grid = f->factor_grid;
   return SGN_OK;
 }
 

@@ -174,7 +174,7 @@ struct FactorArgs {
   double* dscr; int64_t dstride; long long* status;
   unsigned long long* trace;   // optional (SGN_FDAG_TRACE=1): 4 words per task
 };
-int factor_dag_grid(int ctas_per_sm = 0);   // persistent CTAs (0 = occupancy limit per SM)
+int factor_dag_grid();   // persistent CTAs: SMs x occupancy limit
 int min_pivot(const DFront* d_fronts, int32_t n_fronts, const double* d_fstore, double* out_min,
               int64_t* out_pos, void* stream);
 int launch_factor_dag(const FactorArgs& A, int grid, void* stream);

@@ -125,9 +125,12 @@ class DeviceFactor:
         flags = _lib.SGN_SOLVE_LEADING if leading else 0
         check(lib().sgn_factor_solve(self._h, ptr(b), ptr(x), flags, stream), what="solve")
 
-    def set_ctas_per_sm(self, n: int) -> None:
-        """Cap the persistent factorization grid at n CTAs per SM (0 = occupancy limit)."""
-        check(lib().sgn_factor_set_ctas_per_sm(self._h, int(n)), what="factor grid")
+    def set_grid(self, ctas: int) -> int:
+        """Persistent factorization grid of ``ctas`` CTAs (<= 0: the occupancy limit, all
+        SMs); returns the grid in effect."""
+        out = ctypes.c_int32()
+        check(lib().sgn_factor_set_grid(self._h, int(ctas), ctypes.byref(out)), what="factor grid")
+        return out.value
 
     def solve_multi(self, B, X, stream: int = 0) -> None:
         """X[j] = A^{-1} B[j] for the rows j of a (nrhs, n) float64 CUDA tensor (batch-1 factor)."""

@@ -213,8 +213,17 @@ class MeshPlan:
 
 
 _SIDE_STREAM = os.environ.get("SGN_SIDE_STREAM", "1") != "0"
-_KKT_CTAS = int(os.environ.get("SGN_KKT_CTAS", "3"))
-_GX_CTAS = int(os.environ.get("SGN_GX_CTAS", "1"))
+_GX_CTAS = int(os.environ.get("SGN_GX_CTAS", "0"))     # 0: 3/16 of the grid
+
+
+def _gx_share(eng, full: int) -> int:
+    """CTAs of the concurrent G_x factorization.  The G_x factor is dependency-chain bound
+    like the KKT one, so its share is not its flop share (0.11 on config 2, where 74 of 592
+    CTAs made it finish 0.6 ms after the KKT factor): 3/16 of the grid (111 of 592) was the
+    best of 37..222 on config 2 (profiles/scripts/ctas.sh)."""
+    if _GX_CTAS > 0:
+        return min(_GX_CTAS, full - 1)
+    return max(1, (3 * full) // 16)
 _DEBUG_NAN = os.environ.get("SGN_DEBUG_NAN", "0") == "1"
 
 
@@ -252,11 +261,13 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
         # refined solve (still before any convergence error, as in the reference).
         if not hasattr(eng, "_side_stream"):
             eng._side_stream = torch.cuda.Stream()
-        # split the persistent CTA slots: 4 per SM fit; the KKT factor takes _KKT_CTAS of
-        # them and the G_x factor the rest, so both run from the start instead of G_x
-        # waiting for the KKT grid to retire (the G_x factor keeps the full grid elsewhere)
-        eng.kfac.set_ctas_per_sm(_KKT_CTAS)
-        eng.gfac.set_ctas_per_sm(_GX_CTAS)
+        # split the persistent CTA slots (SMs x 4): the G_x factor takes _GX_CTAS of them
+        # and the KKT factor the rest, so both run from the start instead of G_x waiting
+        # for the KKT grid to retire (the G_x factor keeps the full grid elsewhere)
+        full = eng.kfac.set_grid(0)
+        gx = _gx_share(eng, full)
+        eng.gfac.set_grid(gx)
+        eng.kfac.set_grid(full - gx)
         side = eng._side_stream
         ev_asm, ev_adj = torch.cuda.Event(), torch.cuda.Event()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -276,7 +287,7 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
             eng.rhs.copy_(eng.tmp)
             ev_adj.record(side)
         cur.wait_event(ev_adj)
-        eng.gfac.set_ctas_per_sm(0)
+        eng.gfac.set_grid(0)
         if events is not None:
             events[1].record()
         if timings is not None:
