@@ -313,56 +313,71 @@ __device__ void f_panel_post(const sgn::FactorArgs& A, const DFront& F, int b, i
 // C[ti, tj] -= L21[ti, step k] W[tj, step k]^T   (mma.sync.m8n8k4.f64 -> DMMA).
 // diag: the last update of pivot tile (k+1, k+1) -- the result stays in smem (S.b[1]) and
 // is factored and published as D_{k+1} instead of being written back.
-__device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k, int ti, int tj, Smem& S,
+__device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k0, int k, int ti, int tj, Smem& S,
                          bool diag = false) {
   V40 Ak = v40(S.a);          // Ak[c][i] = L21[lo_i + i, j0 + c]
   V40 Bk = v40(S.b[0]);       // Bk[c][j] = W[lo_j + j, j0 + c]
   const int tid = threadIdx.x;
   double* Fm = front_ptr(A, F, b);
   const int64_t ld = F.nrow;
-  const int j0 = k * kTile, w = min(kTile, F.npiv - j0);
   const int lo_i = sgn::tile_lo(F.npiv, ti), nr = sgn::tile_hi(F.npiv, F.nrow, ti) - lo_i;
   const int lo_j = sgn::tile_lo(F.npiv, tj), nc = sgn::tile_hi(F.npiv, F.nrow, tj) - lo_j;
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
   const int row0 = warp * 8;
   const int i = row0 + g;
-  double va[8], vb[8], cv[4][2];
-  // C is final up to step k-1 (waited by the caller): prefetch it while step k's panels
-  // may still be running, then wait for them and load L21 / W
+  double va[8], vb[8];
+  V40 Cs = v40(S.b[2]);       // Cs[j][i] = C(lo_i + i, lo_j + j): staged, not held in registers
+  // C is final up to step k0-1 (waited by the caller): load it while step k's panels may
+  // still be running, then wait for them and stream the L21 / W tiles of steps k0..k
+  {
+    double cv[8];
 #pragma unroll
-  for (int nf = 0; nf < 4; ++nf)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int j = nf * 8 + 2 * q + h;
-      cv[nf][h] = (i < nr && j < nc && (ti != tj || i >= j)) ? __ldcg(Fm + (int64_t)(lo_j + j) * ld + lo_i + i) : 0.0;
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + u * kFThreads;
+      const int r = e & 31, c = e >> 5;
+      cv[u] = (r < nr && c < nc && (ti != tj || r >= c)) ? __ldcg(Fm + (int64_t)(lo_j + c) * ld + lo_i + r) : 0.0;
     }
-  if (tid == 0)
-    spin_ge(A.cnt + (int64_t)b * A.n_fcnt + F.cbase + sgn::cnt_pan(k), sgn::panel_tasks(F.npiv, F.nrow, k));
-  __syncthreads();
+    if (tid == 0)
+      spin_ge(A.cnt + (int64_t)b * A.n_fcnt + F.cbase + sgn::cnt_pan(k), sgn::panel_tasks(F.npiv, F.nrow, k));
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {           // 16 operand loads in flight together
-    const int e = tid + u * kFThreads;
-    const int r = e & 31, c = e >> 5;
-    va[u] = (r < nr && c < w) ? __ldcg(Fm + (int64_t)(j0 + c) * ld + lo_i + r) : 0.0;
-    vb[u] = (c < nc && r < w) ? __ldcg(Fm + (int64_t)(lo_j + c) * ld + j0 + r) : 0.0;   // (j = c, col = r)
-  }
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int e = tid + u * kFThreads;
-    const int r = e & 31, c = e >> 5;
-    Ak[c][r] = va[u];
-    Bk[r][c] = vb[u];
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + u * kFThreads;
+      Cs[e >> 5][e & 31] = cv[u];
+    }
   }
   __syncthreads();
-  tmark(S, 4);
+#define SGN_LOAD_STEP(S_)                                                                          \
+  do {                                                                                             \
+    const int j0_ = (S_) * kTile, w_ = min(kTile, F.npiv - j0_);                                   \
+    _Pragma("unroll") for (int u = 0; u < 8; ++u) {                                                \
+      const int e = tid + u * kFThreads;                                                           \
+      const int r = e & 31, c = e >> 5;                                                            \
+      va[u] = (r < nr && c < w_) ? __ldcg(Fm + (int64_t)(j0_ + c) * ld + lo_i + r) : 0.0;          \
+      vb[u] = (c < nc && r < w_) ? __ldcg(Fm + (int64_t)(lo_j + c) * ld + j0_ + r) : 0.0;          \
+    }                                                                                              \
+  } while (0)
+  SGN_LOAD_STEP(k0);   // 16 operand loads in flight together
   double acc[4][2];
 #pragma unroll
   for (int nf = 0; nf < 4; ++nf) acc[nf][0] = acc[nf][1] = 0.0;
+  for (int s = k0; s <= k; ++s) {
 #pragma unroll
-  for (int kk = 0; kk < kTile; kk += 4) {
-    const double a = Ak[kk + q][row0 + g];
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + u * kFThreads;
+      const int r = e & 31, c = e >> 5;
+      Ak[c][r] = va[u];
+      Bk[r][c] = vb[u];
+    }
+    __syncthreads();
+    if (s < k) SGN_LOAD_STEP(s + 1);      // next step's operands in flight during the DMMAs
+    tmark(S, 4);
 #pragma unroll
-    for (int nf = 0; nf < 4; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], a, Bk[kk + q][nf * 8 + g]);
+    for (int kk = 0; kk < kTile; kk += 4) {
+      const double a = Ak[kk + q][row0 + g];
+#pragma unroll
+      for (int nf = 0; nf < 4; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], a, Bk[kk + q][nf * 8 + g]);
+    }
+    __syncthreads();
   }
   tmark(S, 5);
   if (diag) {
@@ -372,7 +387,7 @@ __device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int j = nf * 8 + 2 * q + h;
-        Dn[i][j] = (i < nr && j < nc && i >= j) ? cv[nf][h] - acc[nf][h] : 0.0;
+        Dn[i][j] = (i < nr && j < nc && i >= j) ? Cs[j][i] - acc[nf][h] : 0.0;
       }
     return;   // the caller factors and publishes D_{k+1}
   }
@@ -382,7 +397,7 @@ __device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int j = nf * 8 + 2 * q + h;
-        if (j < nc && (ti != tj || i >= j)) Fm[(int64_t)(lo_j + j) * ld + lo_i + i] = cv[nf][h] - acc[nf][h];
+        if (j < nc && (ti != tj || i >= j)) Fm[(int64_t)(lo_j + j) * ld + lo_i + i] = Cs[j][i] - acc[nf][h];
       }
   }
 }
@@ -503,6 +518,8 @@ k_factor_dag(const sgn::FactorArgs A) {
       if (S.tr) S.tr[0] = gtimer();
     }
     const int Tn = sgn::ntiles_front(F.npiv, F.nrow);
+    // F_UPDATE: b = tj | (ns << 16) applies steps k-ns+1 .. k (ns = 0 or 1: step k alone)
+    const int tjb = T.b & 0xffff, ns = (kind == sgn::F_UPDATE) ? max(1, T.b >> 16) : 1;
     if (tid == 0) {
       if (kind == sgn::F_ASM) {
         for (int ci = F.child_begin; ci < F.child_end; ++ci) {
@@ -519,8 +536,8 @@ k_factor_dag(const sgn::FactorArgs A) {
           }
         }
       } else if (kind == sgn::F_UPDATE || kind == sgn::F_DIAGUPD) {   // PAN(k) awaited inside
-        const int ti = (kind == sgn::F_DIAGUPD) ? k + 1 : T.a, tj = (kind == sgn::F_DIAGUPD) ? k + 1 : T.b;
-        spin_ge(cf + sgn::cnt_tile(P, ti, tj), 1 + k);
+        const int ti = (kind == sgn::F_DIAGUPD) ? k + 1 : T.a, tj = (kind == sgn::F_DIAGUPD) ? k + 1 : tjb;
+        spin_ge(cf + sgn::cnt_tile(P, ti, tj), 2 + k - ns);
       } else {                                    // Z(t, cb): see f_ztask_pre
         if (T.a < P) {
           spin_ge(cf + sgn::cnt_diag(P, T.a), 1);
@@ -547,7 +564,7 @@ k_factor_dag(const sgn::FactorArgs A) {
       tr_p = v33(S.b[tid >> 5]);
     } else if (kind == sgn::F_UPDATE || kind == sgn::F_DIAGUPD) {
       const bool dg = (kind == sgn::F_DIAGUPD);
-      f_update(A, F, b, k, dg ? k + 1 : T.a, dg ? k + 1 : T.b, S, dg);
+      f_update(A, F, b, k - ns + 1, k, dg ? k + 1 : T.a, dg ? k + 1 : tjb, S, dg);
       if (dg) { fac_k = k + 1; fac_tile = v33(S.b[1]); }
     } else {
       f_ztask_pre(A, F, b, T.a, T.b, S);
@@ -571,11 +588,11 @@ k_factor_dag(const sgn::FactorArgs A) {
       else if (kind == sgn::F_PANEL) s1 = cf + sgn::cnt_pan(k);
       else if (kind == sgn::F_DIAGUPD) { s1 = cf + sgn::cnt_tile(P, k + 1, k + 1); s3 = cf + sgn::cnt_diag(P, k + 1); }
       else {
-        s1 = cf + sgn::cnt_tile(P, T.a, T.b);
+        s1 = cf + sgn::cnt_tile(P, T.a, tjb);
         if (kind == sgn::F_ASM && T.a == 0 && T.b == 0 && F.npiv > 0) s3 = cf + sgn::cnt_diag(P, 0);
       }
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      if (s1) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(s1) : "memory");
+      if (s1) asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(s1), "r"(ns) : "memory");   // TILE += steps applied
       if (s2) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(s2) : "memory");
       if (s3) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(s3) : "memory");
     }

@@ -746,17 +746,19 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     const int64_t P = ptiles(F.npiv), T = ntiles_front(F.npiv, F.nrow);
     F.cbase = s.n_fcnt;
     s.n_fcnt += 1 + 2 * P + T * (T + 1) / 2 + (F.nrow + kTile - 1) / kTile;
-    int64_t tot = T * (T + 1) / 2;                        // assembly tiles
-    for (int64_t k = 0; k < P; ++k) {
-      tot += panel_tasks(F.npiv, F.nrow, (int)k);
-      const int64_t m = T - k - 1;                        // trailing tiles per side
-      tot += m * (m + 1) / 2;                             // updates (+ the DIAGUPD one)
-    }
-    if (tot > INT32_MAX) { last_error() = "front too large for the task schedule"; return 5; }
-    F.ftotal = (int32_t)tot;
+    if (T >= (1 << 16)) { last_error() = "front too large for the task schedule"; return 5; }
+    F.ftotal = 0;                                         // counted as the tasks are emitted
   }
+  // Schur updates off the look-ahead column are applied in groups of up to kUpdGroup
+  // consecutive pivot steps by one task (the C tile is read and written once per group;
+  // the step tiles stream through shared memory): F_UPDATE b = tj | (ns << 16).
+  // SGN_UPD_GROUP overrides (1 = one task per step).
+  int32_t kUpdGroup = 8;
+  if (const char* e = std::getenv("SGN_UPD_GROUP")) kUpdGroup = std::max(1, std::atoi(e));
+  std::vector<int64_t> fcount(s.fronts.size(), 0);
   auto ft = [&](int32_t kind, int32_t k, int32_t f, int32_t a, int32_t b) {
     s.ftasks.push_back(FTask{kind | (k << 3), f, a, b});
+    if (kind != F_ZPANEL) ++fcount[f];                    // every other kind signals DONE
   };
   // Z blocks Z(t, cb) (f_ztask_pre): pivot tiles top-down, then the struct tiles.  Fronts
   // with at least kZInlineSteps pivot steps (the dependency-chain-bound upper fronts) get
@@ -822,8 +824,18 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
         const Front& F = s.fronts[f];
         if (k >= ptiles(F.npiv)) continue;
         const int32_t T = ntiles_front(F.npiv, F.nrow);
-        for (int32_t tj = k + 2; tj < T; ++tj)
-          for (int32_t ti = tj; ti < T; ++ti) ft(F_UPDATE, k, f, ti, tj);
+        const int32_t P = ptiles(F.npiv);
+        // column tj: step tj-1 is the look-ahead update, step tj-2 stays a single-step
+        // task (it sits one chain step from the pivot block tj), steps <= tj-3 are grouped
+        for (int32_t tj = k + 2; tj < T; ++tj) {
+          int32_t ns = 1;
+          if (k <= tj - 3) {
+            const int32_t kmax = std::min(tj - 3, P - 1);
+            if ((k + 1) % kUpdGroup != 0 && k != kmax) continue;
+            ns = k - (k / kUpdGroup) * kUpdGroup + 1;
+          }
+          for (int32_t ti = tj; ti < T; ++ti) ft(F_UPDATE, k, f, ti, tj | (ns << 16));
+        }
       }
       for (int32_t f : fl) {                                 // inline Z row of pivot tile k
         const Front& F = s.fronts[f];
@@ -834,6 +846,10 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     }
   }
   while (zhead < zq.size()) s.ftasks.push_back(zq[zhead++]);
+  for (size_t f = 0; f < s.fronts.size(); ++f) {
+    if (fcount[f] > INT32_MAX) { last_error() = "front too large for the task schedule"; return 5; }
+    s.fronts[f].ftotal = (int32_t)fcount[f];
+  }
   // solve work lists: gather (f), forward GEMV (f, row0, chunk, group), backward dots
   // (f, col0, row chunk, group); each (front, tile) group combines its chunk partials
   s.fwd_off.assign(s.n_levels, 0); s.fwd_cnt.assign(s.n_levels, 0);

@@ -19,12 +19,18 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--out", default="gpurun_out/fdag_trace.npz")
     ap.add_argument("--which", default="kkt", choices=("kkt", "gx"), help="KKT or G_x (adjoint) factor")
+    ap.add_argument("--summary", action="store_true", help="per-kind totals only")
     a = ap.parse_args()
     os.environ["SGN_FDAG_TRACE"] = "1"
     import torch
     from paper_2107_03285_b200._lib import lib
-    from paper_2107_03285_b200.problems import build_sheet
-    prob, p0 = build_sheet(a.config)
+    from paper_2107_03285_b200.problems import build_beam, build_sheet, build_shell
+    if a.config == 3:
+        prob, p0, _ = build_beam(0)
+    elif a.config == 4:
+        prob, p0 = build_shell(201, 100)
+    else:
+        prob, p0 = build_sheet(a.config)
     x = prob.simulate(p0)
     prob._load(x, p0)
     eng = prob.engine
@@ -56,6 +62,8 @@ def main():
         if m.any():
             print(f"{KIND[k]:7s} n={m.sum():6d} busy_med={np.median(T[m, 2] - T[m, 1]):6.2f} "
                   f"wait_med={np.median(T[m, 1] - T[m, 0]):6.2f} busy_sum_us={np.sum(T[m, 2] - T[m, 1]):9.1f}")
+    if a.summary:
+        return
     print("per level: first ready / last end (us)")
     for L in sorted(set(lvl.tolist())):
         m = (lvl == L) & (kind != 3)
