@@ -182,6 +182,18 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------------ our arm
+def assembly_bytes(pl):
+    """Algorithmic assembly bytes per instance: 8 nnz(tril K_s) + 16 d n_v +
+    4 k n_e + 16 n_p."""
+    import numpy as np
+    cols = np.repeat(np.arange(pl.dim), np.diff(pl.K_indptr))
+    has_diag = np.zeros(pl.dim, bool)
+    has_diag[cols[pl.K_indices == cols]] = True
+    shift_rows = np.r_[np.arange(pl.n_x), np.arange(pl.n_x + pl.n_p, pl.dim)]
+    nnz_tril = int((pl.K_indices >= cols).sum() + (~has_diag[shift_rows]).sum())   # tril(K_s)
+    return 8 * nnz_tril + 16 * pl.d * pl.n_v + 4 * pl.nv_el * pl.n_e + 16 * pl.n_p
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -287,12 +299,7 @@ def run_ours(args):
     f_ms = med(ph["factor"])
     flops = st["flops"]
     achieved_tf = flops / (f_ms * 1e-3) / 1e12
-    cols = np.repeat(np.arange(pl.dim), np.diff(pl.K_indptr))
-    has_diag = np.zeros(pl.dim, bool)
-    has_diag[cols[pl.K_indices == cols]] = True
-    shift_rows = np.r_[np.arange(pl.n_x), np.arange(pl.n_x + pl.n_p, pl.dim)]
-    nnz_tril = int((pl.K_indices >= cols).sum() + (~has_diag[shift_rows]).sum())   # tril(K_s)
-    asm_bytes = 8 * nnz_tril + 16 * pl.d * pl.n_v + 4 * pl.nv_el * pl.n_e + 16 * pl.n_p
+    asm_bytes = assembly_bytes(pl)
     a_ms = med(ph["assemble"])
     lbytes = 8 * st["nnz_l"]
     n_solves_main = 2 + 2 * med(iters_main) if med(iters_main) > 0 else 1
@@ -396,16 +403,18 @@ def run_batch(args):
     sampler = ClockSampler(local)
     sampler.start()
     l0 = lib().sgn_launch_count()
-    ms = []
+    ms, ams = [], []
     for _ in range(args.steps):
         flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, ea, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record()
         eng.assemble()
+        ea.record()
         sgn_solve_stages(eng, None)
         e1.record()
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
+        ams.append(e0.elapsed_time(ea))
     launches = lib().sgn_launch_count() - l0
     clocks = sampler.stop()
     tmax = torch.tensor([sum(ms)], dtype=torch.float64, device="cuda")
@@ -425,6 +434,12 @@ def run_batch(args):
     et = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    a_ms = statistics.median(ams)
+    a_bytes = len(rows) * assembly_bytes(bd.plan)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s (B200_PROFILING.md)"
     # the single collective: gather every instance's dp on every rank
     tg = time.perf_counter()
     if dist is not None:
@@ -444,6 +459,11 @@ def run_batch(args):
                    "h2d_bytes_per_step": 8 * len(rows) * (bd.n_x + bd.n_p),
                    "d2h_bytes_per_step": 8 * len(rows) * bd.n_p},
            "gather": {"ms": gather_ms, "bytes": int(full.nbytes), "rows": int(full.shape[0])},
+           "phases": {"assemble": {"ms": a_ms, "bound": "hbm", "algorithmic_bytes": a_bytes,
+                                   "achieved_gbs": a_bytes / (a_ms * 1e-3) / 1e9,
+                                   "frac": a_bytes / (a_ms * 1e-3) / 1e9 / hbm_peak,
+                                   "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,
+                                   "note": f"{len(rows)} instances per launch; median over steps"}},
            "clocks": clocks, "gpu_launches": int(launches)}
     if rank == 0:
         print(json.dumps(out))

@@ -178,7 +178,9 @@ int  sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_stri
  * Replaces the NumPy element kernels + COO->CSC of constraint_jac_x / constraint_jac_p
  * (spring analog: forward.py:61-111, spring_bar.py:144-156).  Per element, writes the
  * element Hessian d2E/dx2 and mixed derivative d2E/dx dX (rest coordinates) in
- * row-major (nd x nd) blocks, nd = nodes_per_elem * dim.                           */
+ * row-major (nd x nd) blocks, nd = nodes_per_elem * dim.  d_mixed == NULL: Hessians
+ * only (forward Newton).  d_mslot (neo-Hookean simplices, optional): compact mixed
+ * slot per element (-1: not in the p-map support, skipped); NULL: one per element. */
 #define SGN_ELEM_SPRING     1   /* 2-node spring, any dim (forward.py:61-111)        */
 #define SGN_ELEM_NH_TRI     2   /* 3-node neo-Hookean triangle, plane strain         */
 #define SGN_ELEM_NH_TET     3   /* 4-node neo-Hookean tetrahedron                    */
@@ -187,7 +189,8 @@ int  sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_stri
 int  sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch,
                         const int32_t* d_conn, const double* d_pos, const double* d_rest,
                         int64_t vert_stride, const double* d_params, int64_t param_stride,
-                        double* d_hess, double* d_mixed, int64_t buf_stride, void* stream);
+                        double* d_hess, double* d_mixed, const int32_t* d_mslot,
+                        int64_t buf_stride, void* stream);
 /* element energies / gradients for the forward solve and line search
  * (spring_energy/spring_gradient analog, forward.py:34-48) */
 int  sgn_element_energy_grad(int32_t elem_type, int64_t n_elems, int32_t batch,
@@ -195,6 +198,30 @@ int  sgn_element_energy_grad(int32_t elem_type, int64_t n_elems, int32_t batch,
                              int64_t vert_stride, const double* d_params, int64_t param_stride,
                              double* d_energy, double* d_grad, int64_t buf_stride, void* stream);
 
+/* mixed blocks d2E/dx dX of the listed neo-Hookean simplices (the p-map support) into
+ * compact slots: block t <- element d_elems[t] (constraint_jac_p's element terms).     */
+int  sgn_element_mixed(int32_t elem_type, int64_t n_list, int32_t batch, const int32_t* d_elems,
+                       const int32_t* d_conn, const double* d_pos, const double* d_rest,
+                       int64_t vert_stride, const double* d_params, int64_t param_stride,
+                       double* d_mixed, int64_t buf_stride, void* stream);
+/* Fused vertex-centric assembly of the G_x entries of a single-group neo-Hookean mesh
+ * (replaces constraint_jac_x's element triplets + COO->CSC for those entries,
+ * spring analog forward.py:51-78, sensitivity.py:245-256 for the KKT placement): one
+ * task per vertex, its incident elements' Hessian columns staged in shared memory, each
+ * output the fixed-order sum of its element entries written to K (both symmetric copies)
+ * and/or G_x.  Plan arrays from the host (engine.VertexPlan); group = lanes per vertex
+ * (>= max incident elements: 6/8/16 for triangles, 16/32 for tetrahedra).              */
+int  sgn_vertex_assemble(int32_t elem_type, int32_t n_task, int32_t group, int32_t batch,
+                         const int32_t* d_inc_ptr, const int32_t* d_inc_ea, const int32_t* d_out_ptr,
+                         const int32_t* d_out_dst, const int32_t* d_con_ptr, const int32_t* d_con_idx,
+                         const int32_t* d_conn, const double* d_pos, const double* d_rest,
+                         int64_t vert_stride, const double* d_params, int64_t param_stride,
+                         double* d_kvals, int64_t kstride, double* d_gvals, int64_t gstride, void* stream);
+/* out[dst[k]] = base[k] + sum coef * buf[idx]: the gather restricted to a list of outputs
+ * (the KKT entries the vertex assembly does not produce: constants and G_p).          */
+int  sgn_gather_to(int64_t n_out, int32_t batch, const int64_t* d_dst, const double* d_base,
+                   const int64_t* d_ptr, const int64_t* d_idx, const double* d_coef, const double* d_buf,
+                   int64_t buf_stride, double* d_out, int64_t out_stride, void* stream);
 /* out[k] = base[k] + sum_{t in ptr[k]..ptr[k+1]} coef[t] * buf[idx[t]]  (atomic-free,
  * fixed-order segmented sum into a precomputed CSC pattern; per instance strided).  */
 int  sgn_gather_values(int64_t n_out, int32_t batch, const double* d_base, int64_t base_stride,

@@ -65,11 +65,18 @@ SIGNATURES = {
     "sgn_solve_refined": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_dbl, c_i32, c_i32,
                                          P_dbl, P_i32, c_vp]),
     "sgn_element_derivs": (ctypes.c_int, [c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp,
-                                          c_i64, c_vp, c_vp, c_i64, c_vp]),
+                                          c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "sgn_element_energy_grad": (ctypes.c_int, [c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_i64,
                                                c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
     "sgn_gather_values": (ctypes.c_int, [c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp,
                                          c_i64, c_vp, c_i64, c_vp]),
+    "sgn_vertex_assemble": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                           c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                                           c_vp]),
+    "sgn_element_mixed": (ctypes.c_int, [c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
+                                         c_i64, c_vp]),
+    "sgn_gather_to": (ctypes.c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64,
+                                     c_vp]),
     "sgn_reduce": (ctypes.c_int, [c_i32, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "sgn_axpy": (ctypes.c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "sgn_lsq_terms": (ctypes.c_int, [c_i32, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_dbl, c_dbl,

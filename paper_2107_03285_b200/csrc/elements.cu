@@ -150,10 +150,48 @@ __device__ __forceinline__ void distribute(const Mat<D>& H, double* out, int str
 template <int D>
 __device__ __forceinline__ double factorial_inv() { return D == 2 ? 0.5 : (1.0 / 6.0); }
 
-// neo-Hookean simplex: derivs
+// Hessian columns (a, 0..D-1) of one neo-Hookean simplex, out[i * ND + r] = d2E/dx_r dx_(a,i)
+// (unscaled); the same arithmetic as the column loop of nh_simplex_derivs below.
 template <int D>
-__device__ void nh_simplex_derivs(const double* xv, const double* Xv, double mu, double lam,
-                                  double gload, double* hess, double* mixed) {
+__device__ __forceinline__ void nh_hess_vertex_cols(const double* xv, const double* Xv, double mu, double lam,
+                                                    int a, double sc, double* out) {
+  constexpr int ND = (D + 1) * D;
+  Mat<D> Ds, Dm;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      Ds.a[i][c] = xv[(c + 1) * D + i] - xv[i];
+      Dm.a[i][c] = Xv[(c + 1) * D + i] - Xv[i];
+    }
+  const Mat<D> B = inverse(Dm);
+  const double A = det(Dm) * factorial_inv<D>();
+  NhState<D> s;
+  s.F = mul(Ds, B);
+  const double J = det(s.F);
+  s.lnJ = log(J);
+  s.FiT = transpose(inverse(s.F));
+  const Mat<D> BT = transpose(B);
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const Mat<D> dF = mul(edge_dir<D>(a, i), B);
+    Mat<D> dH = mul(nh_dP(s, dF, mu, lam), BT);
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c) dH.a[r][c] *= A;
+    double col[ND];
+    distribute(dH, col, 1);
+#pragma unroll
+    for (int r = 0; r < ND; ++r) out[i * ND + r] = sc * col[r];
+  }
+}
+
+// neo-Hookean simplex: derivs
+template <int D, int LD = (D + 1) * D>
+__device__ __forceinline__ void nh_simplex_derivs(const double* xv, const double* Xv, double mu, double lam,
+                                                  double gload, double* hess, double* mixed,
+                                                  bool want_mixed = true) {
   constexpr int NV = D + 1, ND = NV * D;
   Mat<D> Ds, Dm;
 #pragma unroll
@@ -173,7 +211,9 @@ __device__ void nh_simplex_derivs(const double* xv, const double* Xv, double mu,
   const Mat<D> P = nh_P(s, mu, lam);
   const Mat<D> BT = transpose(B);
   const Mat<D> PBT = mul(P, BT);
-  // hessian columns: perturb deformed dof (a, i)
+  // hessian columns: perturb deformed dof (a, i); triangles unroll fully (static staging
+  // indices), tets keep the vertex loop (their staging is shared memory: dynamic is fine)
+#pragma unroll (D == 2 ? NV : 1)
   for (int a = 0; a < NV; ++a)
 #pragma unroll
     for (int i = 0; i < D; ++i) {
@@ -186,7 +226,9 @@ __device__ void nh_simplex_derivs(const double* xv, const double* Xv, double mu,
         for (int c = 0; c < D; ++c) dH.a[r][c] *= A;
       distribute(dH, hess + col, ND);
     }
+  if (!want_mixed) return;
   // mixed columns: perturb rest dof (a, i)
+#pragma unroll (D == 2 ? NV : 1)
   for (int a = 0; a < NV; ++a)
 #pragma unroll
     for (int i = 0; i < D; ++i) {
@@ -369,6 +411,171 @@ __global__ void k_elem_energy_grad(int64_t ne, const int32_t* __restrict__ conn,
   }
 }
 
+// Neo-Hookean simplices (assembly throughput path): one thread per element, all columns
+// unrolled, blocks staged in shared memory (element stride ND*ND+1 doubles: odd, so the
+// per-thread staging stores are bank-conflict free), then copied out by the whole CTA as
+// one contiguous, coalesced run of [hess | mixed] rows per block (the per-thread stores of
+// the register/local-memory variant touched one sector per element and entry).
+template <int D, int EPB>
+__global__ void __launch_bounds__(EPB)
+k_nh_derivs(int64_t ne, const int32_t* __restrict__ conn, const double* __restrict__ pos,
+            const double* __restrict__ rest, int64_t vstride, const double* __restrict__ params,
+            int64_t pstride, double* __restrict__ hess, double* __restrict__ mixed,
+            const int32_t* __restrict__ mslot, const int32_t* __restrict__ elist, int64_t bstride) {
+  constexpr int NV = D + 1, ND = NV * D, NN = ND * ND, SS = NN + 1;
+  extern __shared__ double stage[];             // [EPB][SS] hess, then [EPB][SS] mixed
+  const int b = blockIdx.y;
+  const int64_t e0 = (int64_t)blockIdx.x * EPB;
+  // elist (mixed-only mode): entry t is element elist[t], its mixed block goes to slot t
+  const int64_t e = (elist && e0 + threadIdx.x < ne) ? (int64_t)__ldg(elist + e0 + threadIdx.x) : e0 + threadIdx.x;
+  const double* pr = params + (int64_t)b * pstride;
+  const double sc = pr[3];
+  const bool in_range = e0 + threadIdx.x < ne;
+  const bool want_mixed = in_range && mixed && (elist || !mslot || mslot[e] >= 0);
+  if (in_range && (hess || want_mixed)) {
+    double xv[ND], Xv[ND];
+    const double* pb = pos + (int64_t)b * vstride;
+    const double* rb = rest + (int64_t)b * vstride;
+    int32_t vv[NV];
+#pragma unroll
+    for (int a = 0; a < NV; ++a) vv[a] = __ldg(conn + e * NV + a);
+#pragma unroll
+    for (int a = 0; a < NV; ++a)
+#pragma unroll
+      for (int i = 0; i < D; ++i) { xv[a * D + i] = pb[(int64_t)vv[a] * D + i]; Xv[a * D + i] = rb[(int64_t)vv[a] * D + i]; }
+    double* hs = stage + threadIdx.x * SS;
+    double* ms = stage + (EPB + threadIdx.x) * SS;
+    nh_simplex_derivs<D>(xv, Xv, pr[0], pr[1], pr[2], hs, ms, want_mixed);
+#pragma unroll
+    for (int k = 0; k < NN; ++k) hs[k] *= sc;
+    if (want_mixed)
+#pragma unroll
+      for (int k = 0; k < NN; ++k) ms[k] *= sc;
+  }
+  __syncthreads();
+  const int nel = (int)(ne - e0 < EPB ? ne - e0 : EPB);
+  const int64_t nloc = (int64_t)nel * NN;
+  if (hess) {
+    double* hb = hess + (int64_t)b * bstride + e0 * NN;
+    for (int64_t f = threadIdx.x; f < nloc; f += EPB) {
+      const int j = (int)(f / NN), k = (int)(f - (int64_t)j * NN);
+      hb[f] = stage[j * SS + k];
+    }
+  }
+  if (!mixed) return;
+  // compact slots are increasing in e, so the block's support elements are one contiguous run
+  double* mb = mixed + (int64_t)b * bstride;
+  for (int64_t f = threadIdx.x; f < nloc; f += EPB) {
+    const int j = (int)(f / NN), k = (int)(f - (int64_t)j * NN);
+    const int64_t slot = (mslot && !elist) ? (int64_t)__ldg(mslot + e0 + j) : e0 + j;
+    if (slot >= 0) mb[slot * NN + k] = stage[(EPB + j) * SS + k];
+  }
+}
+
+template <int D, int EPB>
+int launch_nh_derivs(int64_t ne, int32_t batch, const int32_t* conn, const double* pos, const double* rest,
+                     int64_t vstride, const double* params, int64_t pstride, double* hess, double* mixed,
+                     const int32_t* mslot, const int32_t* elist, int64_t bstride, cudaStream_t st) {
+  constexpr int ND = (D + 1) * D;
+  const size_t smem = 2 * EPB * (ND * ND + 1) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_nh_derivs<D, EPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return SGN_CUDA_ERROR;
+    attr = true;
+  }
+  const dim3 grid((unsigned)((ne + EPB - 1) / EPB), batch);
+  k_nh_derivs<D, EPB><<<grid, EPB, smem, st>>>(ne, conn, pos, rest, vstride, params, pstride, hess, mixed, mslot,
+                                                elist, bstride);
+  return SGN_OK;
+}
+
+// Fused vertex-centric G_x assembly (engine.VertexPlan): a group of GS lanes per vertex
+// task; lane s computes the Hessian columns of the task vertex in its incident element s
+// (ascending element order) into shared memory; then each output -- column dof (v, i),
+// row dof r -- is the fixed-order sum of its staged element entries, written to
+// K[lambda_r, x_c], K[x_c, lambda_r] (kv) and G_x[r, c] (gv; either may be NULL).
+template <int GS>
+constexpr int vertex_gpb() { return GS == 6 ? 16 : 128 / GS; }   // groups per block
+
+template <int D, int GS>
+__global__ void __launch_bounds__(vertex_gpb<GS>() * GS)
+k_vertex_assemble(int32_t ntask, const int32_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc_ea,
+                  const int32_t* __restrict__ out_ptr, const int32_t* __restrict__ out_dst,
+                  const int32_t* __restrict__ con_ptr, const int32_t* __restrict__ con_idx,
+                  const int32_t* __restrict__ conn, const double* __restrict__ pos,
+                  const double* __restrict__ rest, int64_t vstride, const double* __restrict__ params,
+                  int64_t pstride, double* __restrict__ kv, int64_t kstride, double* __restrict__ gv,
+                  int64_t gstride) {
+  constexpr int NV = D + 1, ND = NV * D, SLOT = D * ND, GPB = vertex_gpb<GS>();
+  __shared__ double sm[GPB][GS * SLOT];
+  const int grp = threadIdx.x / GS, lane = threadIdx.x % GS;
+  const int64_t task = (int64_t)blockIdx.x * GPB + grp;
+  const int b = blockIdx.y;
+  const double* pr = params + (int64_t)b * pstride;
+  if (task < ntask) {
+    const int i0 = __ldg(inc_ptr + task), n = __ldg(inc_ptr + task + 1) - i0;
+    if (lane < n) {
+      const int ea = __ldg(inc_ea + i0 + lane);
+      const int64_t e = ea >> 2;
+      const int a = ea & 3;
+      const double* pb = pos + (int64_t)b * vstride;
+      const double* rb = rest + (int64_t)b * vstride;
+      double xv[ND], Xv[ND];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const int64_t v = __ldg(conn + e * NV + q);
+#pragma unroll
+        for (int i = 0; i < D; ++i) { xv[q * D + i] = pb[v * D + i]; Xv[q * D + i] = rb[v * D + i]; }
+      }
+      nh_hess_vertex_cols<D>(xv, Xv, pr[0], pr[1], a, pr[3], &sm[grp][lane * SLOT]);
+    }
+  }
+  __syncthreads();
+  if (task >= ntask) return;
+  const int o0 = __ldg(out_ptr + task), o1 = __ldg(out_ptr + task + 1);
+  double* kb = kv ? kv + (int64_t)b * kstride : nullptr;
+  double* gb = gv ? gv + (int64_t)b * gstride : nullptr;
+  for (int o = o0 + lane; o < o1; o += GS) {
+    double v = 0.0;
+    const int t1 = __ldg(con_ptr + o + 1);
+    for (int t = __ldg(con_ptr + o); t < t1; ++t) v += sm[grp][__ldg(con_idx + t)];
+    if (kb) {
+      kb[__ldg(out_dst + 3 * o)] = v;
+      kb[__ldg(out_dst + 3 * o + 1)] = v;
+    }
+    if (gb) gb[__ldg(out_dst + 3 * o + 2)] = v;
+  }
+}
+
+template <int D, int GS>
+void launch_vertex(int32_t ntask, int32_t batch, const int32_t* inc_ptr, const int32_t* inc_ea,
+                   const int32_t* out_ptr, const int32_t* out_dst, const int32_t* con_ptr,
+                   const int32_t* con_idx, const int32_t* conn, const double* pos, const double* rest,
+                   int64_t vstride, const double* params, int64_t pstride, double* kv, int64_t kstride,
+                   double* gv, int64_t gstride, cudaStream_t st) {
+  constexpr int GPB = vertex_gpb<GS>();
+  const dim3 grid((unsigned)((ntask + GPB - 1) / GPB), batch);
+  k_vertex_assemble<D, GS><<<grid, GPB * GS, 0, st>>>(ntask, inc_ptr, inc_ea, out_ptr, out_dst, con_ptr, con_idx,
+                                                  conn, pos, rest, vstride, params, pstride, kv, kstride, gv,
+                                                  gstride);
+}
+
+// out[dst[k]] = base[k] + sum coef * buf[idx]  (the gather restricted to a list of outputs)
+__global__ void k_gather_to(int64_t n_out, const int64_t* __restrict__ dst, const double* __restrict__ base,
+                            const int64_t* __restrict__ ptr, const int64_t* __restrict__ idx,
+                            const double* __restrict__ coef, const double* __restrict__ buf,
+                            int64_t buf_stride, double* __restrict__ out, int64_t out_stride) {
+  const int b = blockIdx.y;
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n_out) return;
+  const double* bb = buf + (int64_t)b * buf_stride;
+  double s = base ? base[k] : 0.0;
+  const int64_t e = ptr[k + 1];
+  for (int64_t t = ptr[k]; t < e; ++t) s += (coef ? coef[t] : 1.0) * bb[idx[t]];
+  out[(int64_t)b * out_stride + dst[k]] = s;
+}
+
 __global__ void k_gather(int64_t n_out, const double* __restrict__ base, int64_t base_stride,
                          const int64_t* __restrict__ ptr, const int64_t* __restrict__ idx,
                          const double* __restrict__ coef, const double* __restrict__ buf,
@@ -401,7 +608,17 @@ extern "C" {
 int sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch, const int32_t* d_conn,
                        const double* d_pos, const double* d_rest, int64_t vert_stride,
                        const double* d_params, int64_t param_stride, double* d_hess,
-                       double* d_mixed, int64_t buf_stride, void* stream) {
+                       double* d_mixed, const int32_t* d_mslot, int64_t buf_stride, void* stream) {
+  if (d_mslot && elem_type != SGN_ELEM_NH_TRI && elem_type != SGN_ELEM_NH_TET) {
+    sgn::last_error() = "mixed slots are supported for neo-Hookean simplices only";
+    return SGN_INVALID;
+  }
+  // non-simplex kinds always write every mixed block; a NULL d_mixed goes to scratch-free
+  // Hessian-only paths for simplices, and is rejected for the others
+  if ((!d_mixed || !d_hess) && elem_type != SGN_ELEM_NH_TRI && elem_type != SGN_ELEM_NH_TET) {
+    sgn::last_error() = "Hessian-only evaluation is supported for neo-Hookean simplices only";
+    return SGN_INVALID;
+  }
   if (n_elems == 0) return SGN_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const dim3 grid((unsigned)((n_elems + 127) / 128), batch);
@@ -420,13 +637,19 @@ int sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch, const 
       break;
     case SGN_ELEM_NH_TRI:
       sgn::count_launch();
-      k_elem_derivs<SGN_ELEM_NH_TRI, 2><<<grid, 128, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
-                                                              d_params, param_stride, d_hess, d_mixed, buf_stride);
+      if (launch_nh_derivs<2, 64>(n_elems, batch, d_conn, d_pos, d_rest, vert_stride, d_params, param_stride,
+                                  d_hess, d_mixed, d_mslot, nullptr, buf_stride, st) != SGN_OK) {
+        sgn::last_error() = "k_nh_derivs<2>: smem attribute";
+        return SGN_CUDA_ERROR;
+      }
       break;
     case SGN_ELEM_NH_TET:
       sgn::count_launch();
-      k_elem_derivs<SGN_ELEM_NH_TET, 3><<<grid64, 64, 0, st>>>(n_elems, d_conn, d_pos, d_rest, vert_stride,
-                                                             d_params, param_stride, d_hess, d_mixed, buf_stride);
+      if (launch_nh_derivs<3, 32>(n_elems, batch, d_conn, d_pos, d_rest, vert_stride, d_params, param_stride,
+                                  d_hess, d_mixed, d_mslot, nullptr, buf_stride, st) != SGN_OK) {
+        sgn::last_error() = "k_nh_derivs<3>: smem attribute";
+        return SGN_CUDA_ERROR;
+      }
       break;
     case SGN_ELEM_SHELL_MEMBRANE:
     case SGN_ELEM_HINGE:
@@ -478,6 +701,67 @@ int sgn_element_energy_grad(int32_t elem_type, int64_t n_elems, int32_t batch, c
       sgn::last_error() = "unknown element type";
       return SGN_INVALID;
   }
+  ELEM_CHECK();
+  return SGN_OK;
+}
+
+int sgn_element_mixed(int32_t elem_type, int64_t n_list, int32_t batch, const int32_t* d_elems,
+                      const int32_t* d_conn, const double* d_pos, const double* d_rest, int64_t vert_stride,
+                      const double* d_params, int64_t param_stride, double* d_mixed, int64_t buf_stride,
+                      void* stream) {
+  if (n_list == 0) return SGN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (elem_type == SGN_ELEM_NH_TRI)
+    rc = launch_nh_derivs<2, 64>(n_list, batch, d_conn, d_pos, d_rest, vert_stride, d_params, param_stride,
+                                 nullptr, d_mixed, nullptr, d_elems, buf_stride, st);
+  else if (elem_type == SGN_ELEM_NH_TET)
+    rc = launch_nh_derivs<3, 32>(n_list, batch, d_conn, d_pos, d_rest, vert_stride, d_params, param_stride,
+                                 nullptr, d_mixed, nullptr, d_elems, buf_stride, st);
+  else {
+    sgn::last_error() = "sgn_element_mixed: neo-Hookean simplices only";
+    return SGN_INVALID;
+  }
+  if (rc != SGN_OK) { sgn::last_error() = "k_nh_derivs: smem attribute"; return rc; }
+  sgn::count_launch();
+  ELEM_CHECK();
+  return SGN_OK;
+}
+
+int sgn_vertex_assemble(int32_t elem_type, int32_t n_task, int32_t group, int32_t batch,
+                        const int32_t* d_inc_ptr, const int32_t* d_inc_ea, const int32_t* d_out_ptr,
+                        const int32_t* d_out_dst, const int32_t* d_con_ptr, const int32_t* d_con_idx,
+                        const int32_t* d_conn, const double* d_pos, const double* d_rest, int64_t vert_stride,
+                        const double* d_params, int64_t param_stride, double* d_kvals, int64_t kstride,
+                        double* d_gvals, int64_t gstride, void* stream) {
+  if (n_task == 0) return SGN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+#define VA_ARGS n_task, batch, d_inc_ptr, d_inc_ea, d_out_ptr, d_out_dst, d_con_ptr, d_con_idx, d_conn, d_pos, \
+                d_rest, vert_stride, d_params, param_stride, d_kvals, kstride, d_gvals, gstride, st
+  if (elem_type == SGN_ELEM_NH_TRI && group <= 6) launch_vertex<2, 6>(VA_ARGS);
+  else if (elem_type == SGN_ELEM_NH_TRI && group <= 8) launch_vertex<2, 8>(VA_ARGS);
+  else if (elem_type == SGN_ELEM_NH_TRI && group <= 16) launch_vertex<2, 16>(VA_ARGS);
+  else if (elem_type == SGN_ELEM_NH_TET && group <= 16) launch_vertex<3, 16>(VA_ARGS);
+  else if (elem_type == SGN_ELEM_NH_TET && group <= 32) launch_vertex<3, 32>(VA_ARGS);
+  else {
+    sgn::last_error() = "vertex assembly: unsupported element type / incidence";
+    return SGN_INVALID;
+  }
+#undef VA_ARGS
+  sgn::count_launch();
+  ELEM_CHECK();
+  return SGN_OK;
+}
+
+int sgn_gather_to(int64_t n_out, int32_t batch, const int64_t* d_dst, const double* d_base,
+                  const int64_t* d_ptr, const int64_t* d_idx, const double* d_coef, const double* d_buf,
+                  int64_t buf_stride, double* d_out, int64_t out_stride, void* stream) {
+  if (n_out == 0) return SGN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const dim3 grid((unsigned)((n_out + 255) / 256), batch);
+  sgn::count_launch();
+  k_gather_to<<<grid, 256, 0, st>>>(n_out, d_dst, d_base, d_ptr, d_idx, d_coef, d_buf, buf_stride, d_out,
+                                    out_stride);
   ELEM_CHECK();
   return SGN_OK;
 }

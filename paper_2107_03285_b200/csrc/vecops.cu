@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdint>
 #include <algorithm>
+#include <mutex>
 #include <string>
 
 #include "../../include/sgn_b200.h"
@@ -60,25 +61,35 @@ __global__ void k_axpy(int64_t n, const double* __restrict__ alpha, const double
 // f vector (KKT order): x block = w_t r at target dofs, p block = -R^T w_t r + w_reg p,
 // lambda block 0, with r = x[tdofs] - tvals - R p (R optional, CSR over targets; R^T is
 // the CSR over parameters); objective per instance = 0.5 sum w r^2 + 0.5 w_reg |p|^2.
-__global__ void __launch_bounds__(kRed)
-k_lsq(int64_t n_x, int64_t n_p, int64_t nt, const int64_t* __restrict__ tdofs,
-      const double* __restrict__ tvals, int64_t tstride, double w_t, double w_reg,
-      const double* __restrict__ x, const double* __restrict__ p, double* __restrict__ vec,
-      double* __restrict__ fobj, const int64_t* __restrict__ rptr, const int64_t* __restrict__ ridx,
-      const double* __restrict__ rcoef, const int64_t* __restrict__ rtptr,
-      const int64_t* __restrict__ rtidx, const double* __restrict__ rtcoef,
-      double* __restrict__ rscr) {
-  __shared__ double sh[kRed];
-  const int b = blockIdx.x;
+// Two grid-stride kernels (targets, then parameters: the R^T rows read the target
+// residuals) on up to kLsqBlocks CTAs per instance; block partials are summed by the last
+// CTA of the second kernel in block order (fixed tree: deterministic for any batch size).
+constexpr int kLsqThreads = 256, kLsqBlocks = 64;
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = kLsqThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  return sh[0];
+}
+
+__global__ void __launch_bounds__(kLsqThreads)
+k_lsq_targets(int64_t n_x, int64_t n_p, int64_t nt, const int64_t* __restrict__ tdofs,
+              const double* __restrict__ tvals, int64_t tstride, double w_t, const double* __restrict__ x,
+              const double* __restrict__ p, double* __restrict__ vec, const int64_t* __restrict__ rptr,
+              const int64_t* __restrict__ ridx, const double* __restrict__ rcoef, double* __restrict__ rscr,
+              double* __restrict__ part) {
+  __shared__ double sh[kLsqThreads];
+  const int b = blockIdx.y;
   const int64_t dim = 2 * n_x + n_p;
   double* v = vec ? vec + (int64_t)b * dim : nullptr;
   const double* xb = x + (int64_t)b * n_x;
   const double* pb = p + (int64_t)b * n_p;
   double* rs = rscr ? rscr + (int64_t)b * nt : nullptr;
-  if (v) for (int64_t i = threadIdx.x; i < dim; i += kRed) if (i < n_x || i >= n_x + n_p) v[i] = 0.0;
-  __syncthreads();
   double acc = 0.0;
-  for (int64_t t = threadIdx.x; t < nt; t += kRed) {
+  for (int64_t t = blockIdx.x * (int64_t)kLsqThreads + threadIdx.x; t < nt; t += (int64_t)gridDim.x * kLsqThreads) {
     const int64_t d = tdofs[t];
     double r = xb[d] - tvals[(int64_t)b * tstride + t];
     if (rptr)
@@ -87,8 +98,24 @@ k_lsq(int64_t n_x, int64_t n_p, int64_t nt, const int64_t* __restrict__ tdofs,
     if (v) v[d] = w_t * r;
     if (rs) rs[t] = w_t * r;
   }
-  __syncthreads();
-  for (int64_t j = threadIdx.x; j < n_p; j += kRed) {
+  const double tot = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[((int64_t)b * 2 * kLsqBlocks) + blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kLsqThreads)
+k_lsq_params(int64_t n_x, int64_t n_p, int64_t nt, int nbt, double w_reg, const double* __restrict__ p,
+             double* __restrict__ vec, double* __restrict__ fobj, const int64_t* __restrict__ rtptr,
+             const int64_t* __restrict__ rtidx, const double* __restrict__ rtcoef,
+             const double* __restrict__ rscr, double* __restrict__ part, int* __restrict__ tickets) {
+  __shared__ double sh[kLsqThreads];
+  __shared__ int last;
+  const int b = blockIdx.y;
+  const int64_t dim = 2 * n_x + n_p;
+  double* v = vec ? vec + (int64_t)b * dim : nullptr;
+  const double* pb = p + (int64_t)b * n_p;
+  const double* rs = rscr ? rscr + (int64_t)b * nt : nullptr;
+  double acc = 0.0;
+  for (int64_t j = blockIdx.x * (int64_t)kLsqThreads + threadIdx.x; j < n_p; j += (int64_t)gridDim.x * kLsqThreads) {
     const double pj = pb[j];
     acc += w_reg * pj * pj;
     double fp = w_reg * pj;
@@ -96,13 +123,21 @@ k_lsq(int64_t n_x, int64_t n_p, int64_t nt, const int64_t* __restrict__ tdofs,
       for (int64_t k = rtptr[j]; k < rtptr[j + 1]; ++k) fp -= rtcoef[k] * rs[rtidx[k]];
     if (v) v[n_x + j] = fp;
   }
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  for (int s = kRed / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-    __syncthreads();
+  const double tot = block_sum(acc, sh);
+  double* pp = part + (int64_t)b * 2 * kLsqBlocks;
+  if (threadIdx.x == 0) {
+    pp[kLsqBlocks + blockIdx.x] = tot;
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(tickets + b) : "memory");
+    last = (old == (int)gridDim.x - 1);
   }
-  if (threadIdx.x == 0 && fobj) fobj[b] = 0.5 * sh[0];
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  tickets[b] = 0;
+  double t = 0.0;
+  for (int k = 0; k < nbt; ++k) t += __ldcg(pp + k);
+  for (int k = 0; k < (int)gridDim.x; ++k) t += __ldcg(pp + kLsqBlocks + k);
+  if (fobj) fobj[b] = 0.5 * t;
 }
 
 // mode 0: v = (0, 0, src_lambda)
@@ -202,10 +237,41 @@ int sgn_lsq_terms_r(int32_t batch, int64_t n_x, int64_t n_p, int64_t nt, const i
                     const int64_t* d_rptr, const int64_t* d_ridx, const double* d_rcoef,
                     const int64_t* d_rtptr, const int64_t* d_rtidx, const double* d_rtcoef,
                     double* d_rscr, void* stream) {
-  sgn::count_launch();
-  k_lsq<<<batch, kRed, 0, (cudaStream_t)stream>>>(n_x, n_p, nt, d_tdofs, d_tvals, tstride, w_t, w_reg,
-                                                  d_x, d_p, d_vec, d_fobj, d_rptr, d_ridx, d_rcoef,
-                                                  d_rtptr, d_rtidx, d_rtcoef, d_rscr);
+  // per-process scratch: block partials + self-resetting tickets (stream-ordered use; one
+  // host thread per context, as for every entry point of this library)
+  static std::mutex mu;
+  static double* part = nullptr;
+  static int* tick = nullptr;
+  static int32_t cap = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (batch > cap) {
+      cudaDeviceSynchronize();
+      if (part) cudaFree(part);
+      if (tick) cudaFree(tick);
+      part = nullptr; tick = nullptr; cap = 0;
+      if (cudaMalloc(&part, (size_t)batch * 2 * kLsqBlocks * sizeof(double)) != cudaSuccess ||
+          cudaMalloc(&tick, (size_t)batch * sizeof(int)) != cudaSuccess ||
+          cudaMemset(tick, 0, (size_t)batch * sizeof(int)) != cudaSuccess) {
+        sgn::last_error() = "lsq scratch allocation failed";
+        return SGN_CUDA_ERROR;
+      }
+      cap = batch;
+    }
+  }
+  const int64_t dim = 2 * n_x + n_p;
+  if (d_vec && cudaMemsetAsync(d_vec, 0, (size_t)batch * dim * sizeof(double), st) != cudaSuccess) {
+    sgn::last_error() = "lsq: vector reset failed";
+    return SGN_CUDA_ERROR;
+  }
+  const int nbt = (int)std::max<int64_t>(1, std::min<int64_t>(kLsqBlocks, (nt + kLsqThreads - 1) / kLsqThreads));
+  const int nbp = (int)std::max<int64_t>(1, std::min<int64_t>(kLsqBlocks, (n_p + kLsqThreads - 1) / kLsqThreads));
+  sgn::count_launch(2);
+  k_lsq_targets<<<dim3(nbt, batch), kLsqThreads, 0, st>>>(n_x, n_p, nt, d_tdofs, d_tvals, tstride, w_t, d_x, d_p,
+                                                         d_vec, d_rptr, d_ridx, d_rcoef, d_rscr, part);
+  k_lsq_params<<<dim3(nbp, batch), kLsqThreads, 0, st>>>(n_x, n_p, nt, nbt, w_reg, d_p, d_vec, d_fobj, d_rtptr,
+                                                        d_rtidx, d_rtcoef, d_rscr, part, tick);
   VEC_CHECK();
   return SGN_OK;
 }

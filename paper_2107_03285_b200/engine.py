@@ -38,16 +38,30 @@ ELEM_CODES = {"spring": _lib.SGN_ELEM_SPRING, "tri": _lib.SGN_ELEM_NH_TRI, "tet"
 class ElemGroup:
     """One element type of a mesh: connectivity + its slices of the block/gradient buffers."""
 
-    def __init__(self, kind, conn, d, hoff, goff):
+    def __init__(self, kind, conn, d, hoff, goff, rest_dof_used=None):
         self.kind = kind
         self.conn = np.asarray(conn, dtype=np.int64)
         self.n_e, self.nv = self.conn.shape
         self.nd = self.nv * d
         self.code = ELEM_CODES[kind] + (100 * d if kind == "spring" else 0)
+        # mixed blocks d2E/dx dX are needed only for elements with a rest dof in the p-map
+        # support (neo-Hookean simplices: compact slots; other kinds keep one per element)
+        self.mslot = None
+        self.n_m = self.n_e
+        if rest_dof_used is not None and kind in ("tri", "tet"):
+            el_dofs = (self.conn[:, :, None] * d + np.arange(d)[None, None, :]).reshape(self.n_e, self.nd)
+            sup = rest_dof_used[el_dofs].any(axis=1)
+            self.mslot = np.where(sup, np.cumsum(sup) - 1, -1).astype(np.int32)
+            self.n_m = int(sup.sum())
+            self.melems = np.flatnonzero(sup).astype(np.int32)      # support elements, slot order
         self.hoff = hoff                                   # hess block offset in ebuf
-        self.moff = hoff + self.n_e * self.nd * self.nd    # mixed block offset
+        self.moff = hoff + self.n_e * self.nd * self.nd    # mixed block offset (compact slots)
         self.goff = goff                                   # gradient offset in egrad
-        self.size = 2 * self.n_e * self.nd * self.nd
+        self.size = (self.n_e + self.n_m) * self.nd * self.nd
+
+    def mixed_index(self, e):
+        """ebuf offset (relative to moff, in blocks) of element e's mixed block (-1: none)."""
+        return np.asarray(e) if self.mslot is None else self.mslot[e].astype(np.int64)
 
 
 def _csr_from_lists(n_rows, rows, *cols):
@@ -71,8 +85,10 @@ class MeshPlan:
             groups = [(kind, conn)]
         self.groups = []
         hoff = goff = 0
+        rest_used = np.zeros(self.n_v * d, bool)
+        rest_used[np.asarray(pmap[0], dtype=np.int64)] = True
         for gk, gc in groups:
-            g = ElemGroup(gk, gc, d, hoff, goff)
+            g = ElemGroup(gk, gc, d, hoff, goff, rest_used)
             self.groups.append(g)
             hoff += g.size
             goff += g.n_e * g.nd
@@ -124,7 +140,7 @@ class MeshPlan:
             c_dof = el_dofs[:, eb].ravel()
             loc = np.tile(ea * nd + eb, g.n_e)
             hidx = g.hoff + e_all * nd * nd + loc
-            midx = g.moff + e_all * nd * nd + loc
+            midx = g.moff + g.mixed_index(e_all) * nd * nd + loc    # valid where the p-map reads it
             rx, cx = self.dof_to_x[r_dof], self.dof_to_x[c_dof]
             keep = (rx >= 0) & (cx >= 0)                  # Gx block and its transpose
             gx_r, gx_c, gx_s = rx[keep], cx[keep], hidx[keep]
@@ -210,6 +226,105 @@ class MeshPlan:
         # --- gradient gather: free dof <- element-gradient entries ------------------------
         self.grad_ptr, self.grad_src = _csr_from_lists(n_x, np.concatenate(g_rows), np.concatenate(g_src))
         self.grad_base = self.f_ext[self.free_dofs].copy()
+
+
+class VertexPlan:
+    """Fused vertex-centric assembly of the G_x entries (neo-Hookean simplices, one group).
+
+    One task per vertex with a free dof; its incident elements (ascending) each compute
+    the element-Hessian columns of that vertex's dofs into shared memory, and each output
+    (column dof (v, i), row dof r) is the fixed-order sum of its element entries, written
+    to K[lambda_r, x_(v,i)], to K[x_r, lambda_(v,i)] (= G_x[(v,i), r], by the symmetry of
+    the element Hessians: both copies are one contiguous run of column (v,i)'s nonzeros, so
+    every store is coalesced) and to G_x[r, (v,i)].  It is the sum, in the same element
+    order, of the staged path (element blocks -> sorted element->nonzero lists, `k_gather`),
+    without the element-block round trip through HBM; K comes out exactly symmetric.  The remaining KKT entries (constants and the G_p block) keep the gather,
+    restricted to their own nonzeros (`rest_*`)."""
+
+    def __init__(self, pl: "MeshPlan"):
+        g = pl.groups[0]
+        d, nd, nv = pl.d, g.nd, g.nv
+        el_dofs = (g.conn[:, :, None] * d + np.arange(d)[None, None, :]).reshape(g.n_e, nd)
+        free_v = (pl.dof_to_x.reshape(pl.n_v, d) >= 0).any(axis=1)
+        e_p = np.repeat(np.arange(g.n_e), nv)
+        a_p = np.tile(np.arange(nv), g.n_e)
+        v_p = g.conn.ravel()
+        keep = free_v[v_p]
+        e_p, a_p, v_p = e_p[keep], a_p[keep], v_p[keep]
+        o = np.lexsort((e_p, v_p))
+        e_p, a_p, v_p = e_p[o], a_p[o], v_p[o]
+        tv, t_start, t_cnt = np.unique(v_p, return_index=True, return_counts=True)
+        self.n_task = int(tv.size)
+        self.max_inc = int(t_cnt.max())
+        self.inc_ptr = np.r_[t_start, v_p.size].astype(np.int32)
+        self.inc_ea = (e_p * 4 + a_p).astype(np.int32)
+        t_p = np.repeat(np.arange(self.n_task), t_cnt)
+        s_p = np.arange(v_p.size) - np.repeat(t_start, t_cnt)
+        # contributions: (pair, column axis i, element row r)
+        P, I, R = np.meshgrid(np.arange(v_p.size), np.arange(d), np.arange(nd), indexing="ij")
+        P, I, R = P.ravel(), I.ravel(), R.ravel()
+        c_dof = v_p[P] * d + I
+        r_dof = el_dofs[e_p[P], R]
+        cx, rx = pl.dof_to_x[c_dof], pl.dof_to_x[r_dof]
+        ok = (cx >= 0) & (rx >= 0)
+        P, I, R, cx, rx = P[ok], I[ok], R[ok], cx[ok], rx[ok]
+        smem = s_p[P] * (d * nd) + I * nd + R
+        tt = t_p[P]
+        o = np.lexsort((e_p[P], rx, cx, tt))          # output (task, col, row), then element order
+        tt, cx, rx, smem = tt[o], cx[o], rx[o], smem[o]
+        okey = (tt.astype(np.int64) * pl.n_x + cx) * pl.n_x + rx
+        first = np.r_[True, okey[1:] != okey[:-1]]
+        oidx = np.flatnonzero(first)
+        self.n_out = int(oidx.size)
+        self.con_ptr = np.r_[oidx, okey.size].astype(np.int32)
+        self.con_idx = smem.astype(np.int32)
+        ot, ocx, orx = tt[oidx], cx[oidx], rx[oidx]
+        self.out_ptr = np.searchsorted(ot, np.arange(self.n_task + 1)).astype(np.int32)
+        # destinations: K (lambda_r, x_c), K (x_c, lambda_r), G (r, c)
+        oL = pl.n_x + pl.n_p
+        kcol = np.repeat(np.arange(pl.dim, dtype=np.int64), np.diff(pl.K_indptr))
+        kkey = kcol * pl.dim + pl.K_indices
+        k1 = ocx * pl.dim + (oL + orx)
+        k2 = (oL + ocx) * pl.dim + orx        # K[x_r, lambda_c] = G_x[c, r]: symmetric copy, same column run
+        n1, n2 = np.searchsorted(kkey, k1), np.searchsorted(kkey, k2)
+        assert (kkey[n1] == k1).all() and (kkey[n2] == k2).all()
+        gcol = np.repeat(np.arange(pl.n_x, dtype=np.int64), np.diff(pl.G_indptr))
+        gkey = gcol * pl.n_x + pl.G_indices
+        k3 = ocx * pl.n_x + orx
+        n3 = np.searchsorted(gkey, k3)
+        assert (gkey[n3] == k3).all()
+        assert pl.nnz < 2 ** 31 and pl.G_nnz < 2 ** 31
+        self.out_dst = np.stack([n1, n2, n3], axis=1).astype(np.int32).ravel()
+        # every fused K entry is a pure G_x entry: no constant, only element-Hessian terms
+        fused = np.zeros(pl.nnz, bool)
+        fused[n1] = True
+        fused[n2] = True
+        assert fused.sum() == 2 * self.n_out
+        cnt = np.diff(pl.K_ptr)
+        fsrc = pl.K_src[np.repeat(fused, cnt)]
+        assert (pl.K_base[fused] == 0.0).all() and (fsrc < g.moff).all()
+        ncon = np.diff(self.con_ptr)
+        assert (cnt[n1] == ncon).all() and (cnt[n2] == ncon).all()   # same terms as the staged lists
+        # the complement (constants, G_p): restricted gather lists
+        rest = np.flatnonzero(~fused)
+        rc = cnt[rest]
+        self.rest_dst = rest.astype(np.int64)
+        self.rest_ptr = np.r_[0, np.cumsum(rc)].astype(np.int64)
+        sel = np.repeat(pl.K_ptr[rest], rc) + (np.arange(int(rc.sum())) - np.repeat(self.rest_ptr[:-1], rc))
+        self.rest_src = pl.K_src[sel].astype(np.int64)
+        self.rest_coef = pl.K_coef[sel].astype(np.float64)
+        self.rest_base = pl.K_base[rest].copy()
+        self.needs_mixed = bool(self.rest_src.size)
+
+
+def vertex_plan(pl: "MeshPlan"):
+    """VertexPlan for single-group neo-Hookean meshes (max 32 elements per vertex), else None."""
+    if os.environ.get("SGN_FUSED_ASSEMBLY", "1") == "0":
+        return None
+    if len(pl.groups) != 1 or pl.groups[0].kind not in ("tri", "tet"):
+        return None
+    vp = VertexPlan(pl)
+    return vp if vp.max_inc <= 32 else None
 
 
 _SIDE_STREAM = os.environ.get("SGN_SIDE_STREAM", "1") != "0"
@@ -404,6 +519,18 @@ class DeviceEngine:
         self.kdir = z(B, pl.n_x)
         self.xtry = z(B, pl.n_x)
         self.n_x, self.n_p = pl.n_x, pl.n_p
+        self.vplan = vertex_plan(pl)
+        if self.vplan is not None:
+            vp, i32 = self.vplan, torch.int32
+            self.v_inc_ptr, self.v_inc_ea = T(vp.inc_ptr, i32), T(vp.inc_ea, i32)
+            self.v_out_ptr, self.v_out_dst = T(vp.out_ptr, i32), T(vp.out_dst, i32)
+            self.v_con_ptr, self.v_con_idx = T(vp.con_ptr, i32), T(vp.con_idx, i32)
+            self.r_dst, self.r_base = T(vp.rest_dst, i64), T(vp.rest_base)
+            self.r_ptr, self.r_src, self.r_coef = T(vp.rest_ptr, i64), T(vp.rest_src, i64), T(vp.rest_coef)
+            self.v_group = next(gs for gs in ((6, 8, 16, 32) if pl.groups[0].kind == "tri" else (16, 32))
+                                if vp.max_inc <= gs)
+            self.v_melems = T(pl.groups[0].melems, i32)
+        self._gx_ready = False
         self.ksym = symbolic_for(pl.dim, pl.K_indptr, pl.K_indices, pl.n_x, pl.n_p, pl.n_x)
         self.kfac = DeviceFactor(self.ksym, B)
         self._gfac = None
@@ -429,29 +556,78 @@ class DeviceEngine:
     def positions(self, x=None):
         pl = self.plan
         x = self.x if x is None else x
+        self._gx_ready = False
         self._gather(pl.n_dof, self.pos_base, 0, self.pos_ptr, self.pos_idx, None, x, pl.n_x,
                      self.pos, pl.n_dof)
         self._gather(pl.n_dof, self.rest_base, 0, self.rest_ptr, self.rest_idx, self.rest_coef,
                      self.p, pl.n_p, self.rest, pl.n_dof)
 
-    def element_blocks(self):
+    def element_blocks(self, mixed: bool = True, hess: bool = True):
+        """Element Hessians (and, with mixed=True, the rest-shape mixed blocks of the
+        p-map support) into ebuf; the forward Newton needs the Hessians only, the fused
+        KKT assembly the mixed blocks only."""
         pl = self.plan
-        for g, conn, prm in zip(pl.groups, self.conns, self.gparams):
+        if not hasattr(self, "_mslots"):
+            self._mslots = [None if g.mslot is None else
+                            self.torch.as_tensor(g.mslot, dtype=self.torch.int32, device="cuda") for g in pl.groups]
+        for g, conn, prm, ms in zip(pl.groups, self.conns, self.gparams, self._mslots):
             check(lib().sgn_element_derivs(g.code, g.n_e, self.batch, ptr(conn), ptr(self.pos), ptr(self.rest),
-                                           pl.n_dof, ptr(prm), prm.stride(0), ptr(self.ebuf[:, g.hoff:]),
-                                           ptr(self.ebuf[:, g.moff:]), pl.ebuf_size, self.stream))
+                                           pl.n_dof, ptr(prm), prm.stride(0),
+                                           ptr(self.ebuf[:, g.hoff:]) if (hess or g.mslot is None) else None,
+                                           ptr(self.ebuf[:, g.moff:]) if (mixed or g.mslot is None) else None,
+                                           ptr(ms) if ms is not None else None, pl.ebuf_size, self.stream))
+
+    def _vertex(self, kv, gv):
+        pl, vp = self.plan, self.vplan
+        g = pl.groups[0]
+        check(lib().sgn_vertex_assemble(g.code, vp.n_task, self.v_group, self.batch, ptr(self.v_inc_ptr),
+                                        ptr(self.v_inc_ea), ptr(self.v_out_ptr), ptr(self.v_out_dst),
+                                        ptr(self.v_con_ptr), ptr(self.v_con_idx), ptr(self.conns[0]),
+                                        ptr(self.pos), ptr(self.rest), pl.n_dof, ptr(self.gparams[0]),
+                                        self.gparams[0].stride(0), ptr(kv), pl.nnz if kv is not None else 0,
+                                        ptr(gv), pl.G_nnz if gv is not None else 0, self.stream))
 
     def assemble_kkt(self):
+        """KKT values (and G_x, for the adjoint) from the current positions.  Fused path
+        (single-group neo-Hookean meshes): G_x entries by the vertex kernel, mixed blocks of
+        the p-map support, then the remaining entries by the restricted gather.  Otherwise
+        the staged path: element blocks -> gather."""
         pl = self.plan
+        if self.vplan is not None:
+            self._vertex(self.kvals, self.gvals)
+            if self.vplan.needs_mixed:
+                g = pl.groups[0]
+                check(lib().sgn_element_mixed(g.code, g.n_m, self.batch, ptr(self.v_melems), ptr(self.conns[0]),
+                                              ptr(self.pos), ptr(self.rest), pl.n_dof, ptr(self.gparams[0]),
+                                              self.gparams[0].stride(0), ptr(self.ebuf[:, g.moff:]),
+                                              pl.ebuf_size, self.stream))
+            check(lib().sgn_gather_to(self.r_dst.numel(), self.batch, ptr(self.r_dst), ptr(self.r_base),
+                                      ptr(self.r_ptr), ptr(self.r_src), ptr(self.r_coef), ptr(self.ebuf),
+                                      self.ebuf.stride(0), ptr(self.kvals), pl.nnz, self.stream))
+            self._gx_ready = True
+            return
+        self.element_blocks()
         self._gather(pl.nnz, self.K_base, 0, self.K_ptr, self.K_src, self.K_coef, self.ebuf,
                      self.ebuf.stride(0), self.kvals, pl.nnz)
+
+    def gx_values(self, force: bool = False):
+        """G_x = dc/dx values (generic pattern) at the current positions into self.gvals."""
+        if self._gx_ready and not force:
+            return
+        pl = self.plan
+        if self.vplan is not None:
+            self._vertex(None, self.gvals)
+        else:
+            self.element_blocks(mixed=False)
+            self._gather(pl.G_nnz, None, 0, self.G_ptr, self.G_src, None, self.ebuf, self.ebuf.stride(0),
+                         self.gvals, pl.G_nnz)
+        self._gx_ready = True
 
     # -- SGN direction (staged) ----------------------------------------------------------
     def assemble(self):
         """Element blocks -> KKT values, least-squares terms (fvec, fobj) at (x, p)."""
         pl = self.plan
         self.positions()
-        self.element_blocks()
         self.assemble_kkt()
         self._lsq(self.x, self.fvec)
 
@@ -477,8 +653,7 @@ class DeviceEngine:
         check_pivots=False the caller checks the factor's status later (no host sync here)."""
         pl = self.plan
         st = self.stream
-        self._gather(pl.G_nnz, None, 0, self.G_ptr, self.G_src, None, self.ebuf, self.ebuf.stride(0),
-                     self.gvals, pl.G_nnz)
+        self.gx_values()
         self.gfac.numeric(self.gvals, 0.0, 0.0, st)
         if check_pivots:
             self.gfac.check(st)
@@ -519,6 +694,7 @@ class DeviceEngine:
         free-dof gradient gx of the current rest shape."""
         pl = self.plan
         st = self.stream
+        self._gx_ready = False
         self._gather(pl.n_dof, self.pos_base, 0, self.pos_ptr, self.pos_idx, None, x, pl.n_x,
                      self.pos, pl.n_dof)
         for gi, (g, conn, prm, en) in enumerate(zip(pl.groups, self.conns, self.gparams, self.eeners)):
@@ -539,10 +715,7 @@ class DeviceEngine:
         return sc[5:5 + ng].sum(axis=0) + sc[1]
 
     def _hessian(self):
-        pl = self.plan
-        self.element_blocks()
-        self._gather(pl.G_nnz, None, 0, self.G_ptr, self.G_src, None, self.ebuf, self.ebuf.stride(0),
-                     self.gvals, pl.G_nnz)
+        self.gx_values(force=True)
 
     @property
     def gfac(self):

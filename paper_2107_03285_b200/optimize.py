@@ -176,7 +176,7 @@ def direction_dgn(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirectio
     sync()
     t0 = time.perf_counter()
     # S = -G_x^{-1} G_p
-    eng._gather(pl.G_nnz, None, 0, eng.G_ptr, eng.G_src, None, eng.ebuf, eng.ebuf.stride(0), eng.gvals, pl.G_nnz)
+    eng.gx_values()
     eng.gfac.numeric(eng.gvals, 0.0, 0.0, st)
     eng.gfac.check(st)
     if not hasattr(eng, "_dgn"):
@@ -250,7 +250,7 @@ def direction_cg_gn(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirect
     prob._load(x, p)
     eng.assemble()
     st = _lib_stream()
-    eng._gather(pl.G_nnz, None, 0, eng.G_ptr, eng.G_src, None, eng.ebuf, eng.ebuf.stride(0), eng.gvals, pl.G_nnz)
+    eng.gx_values()
     eng.gfac.numeric(eng.gvals, 0.0, 0.0, st)
     eng.gfac.check(st)
     op = DeviceReducedOperator(eng, pl)

@@ -103,7 +103,6 @@ class ElasticDesignProblem:
         """Device-assembled KKT values in the structural pattern (plan.K_indptr/K_indices)."""
         self._load(x, p)
         self.engine.positions()
-        self.engine.element_blocks()
         self.engine.assemble_kkt()
         return self.engine.kvals[0].cpu().numpy()
 

@@ -15,7 +15,7 @@ for D, code in ((2, 2), (3, 3)):
     params = torch.as_tensor([mu, lam, g, 1.0], dtype=torch.float64, device="cuda")
     nd = nv * D
     h = torch.zeros(nd * nd, dtype=torch.float64, device="cuda"); m = torch.zeros_like(h)
-    rc = lib().sgn_element_derivs(code, 1, 1, ptr(conn), ptr(pos), ptr(rest), nv * D, ptr(params), 4, ptr(h), ptr(m), nd * nd, 0)
+    rc = lib().sgn_element_derivs(code, 1, 1, ptr(conn), ptr(pos), ptr(rest), nv * D, ptr(params), 4, ptr(h), ptr(m), None, nd * nd, 0)
     torch.cuda.synchronize()
     hg, mg = h.cpu().numpy().reshape(nd, nd), m.cpu().numpy().reshape(nd, nd)
     print(D, rc, "H err", np.abs(hg - H[0]).max(), "M err", np.abs(mg - M[0]).max())

@@ -30,9 +30,11 @@ def test_tet_element_blocks_match_oracle(beam):
     pl = prob.plan
     nd2 = pl.n_e * pl.nd * pl.nd
     buf = prob.engine.ebuf[0].cpu().numpy()
-    sel = np.arange(0, pl.n_e, 97)
+    g0 = pl.groups[0]
+    sup = np.flatnonzero(g0.mslot >= 0)            # surface tets: mixed blocks in compact slots
+    sel = sup[::29]
     H = buf[:nd2].reshape(pl.n_e, pl.nd, pl.nd)[sel]
-    M = buf[nd2:].reshape(pl.n_e, pl.nd, pl.nd)[sel]
+    M = buf[nd2:nd2 + sup.size * pl.nd * pl.nd].reshape(sup.size, pl.nd, pl.nd)[g0.mslot[sel]]
     pos, rest = oprob.full_positions(x), oprob.rest_positions(p0)
     Ho, Mo = el.nh_second(pos[oprob.conn[sel]], rest[oprob.conn[sel]], oprob.mu, oprob.lam, oprob.gload)
     assert _rel(H, oprob.scale * Ho) <= 1e-12

@@ -96,14 +96,23 @@ def test_sheet_element_blocks_match_oracle(sheet1):
     pl = prob.plan
     nd2 = pl.n_e * pl.nd * pl.nd
     buf = eng.ebuf[0].cpu().numpy()
+    g0 = pl.groups[0]
+    sup = np.flatnonzero(g0.mslot >= 0)            # mixed blocks: p-map support, compact slots
+    assert sup.size == g0.n_m and 0 < sup.size < pl.n_e
     H = buf[:nd2].reshape(pl.n_e, pl.nd, pl.nd)
-    M = buf[nd2:].reshape(pl.n_e, pl.nd, pl.nd)
+    M = buf[nd2:nd2 + sup.size * pl.nd * pl.nd].reshape(sup.size, pl.nd, pl.nd)
     pos = oprob.full_positions(x)
     rest = oprob.rest_positions(p0)
     Ho, Mo = el.nh_second(pos[oprob.conn], rest[oprob.conn], oprob.mu, oprob.lam, oprob.gload)
     s = oprob.scale
     assert _rel(H, s * Ho) <= 1e-12
-    assert _rel(M, s * Mo) <= 1e-12
+    assert _rel(M, s * Mo[sup]) <= 1e-12
+    # every element outside the support has a zero mixed block in the oracle's G_p terms
+    out = np.setdiff1d(np.arange(pl.n_e), sup)
+    rest_used = np.zeros(pl.n_v * pl.d, bool)
+    rest_used[pl.rest_ptr[1:] > pl.rest_ptr[:-1]] = True
+    el_dofs = (pl.conn[:, :, None] * pl.d + np.arange(pl.d)).reshape(pl.n_e, -1)
+    assert not rest_used[el_dofs[out]].any()
 
 
 def test_sheet_kkt_pattern_bit_exact_and_values(sheet1):
