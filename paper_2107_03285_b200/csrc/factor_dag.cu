@@ -337,8 +337,11 @@ __device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k
       const int r = e & 31, c = e >> 5;
       cv[u] = (r < nr && c < nc && (ti != tj || r >= c)) ? __ldcg(Fm + (int64_t)(lo_j + c) * ld + lo_i + r) : 0.0;
     }
-    if (tid == 0)
-      spin_ge(A.cnt + (int64_t)b * A.n_fcnt + F.cbase + sgn::cnt_pan(k), sgn::panel_tasks(F.npiv, F.nrow, k));
+    if (tid == 0) {
+      // the diagonal update reads row tile k+1 only: its TRSM task (t = 0) is enough
+      if (diag) spin_ge(A.cnt + (int64_t)b * A.n_fcnt + F.cbase + sgn::cnt_pan0(F.npiv, F.nrow, k), 1);
+      else spin_ge(A.cnt + (int64_t)b * A.n_fcnt + F.cbase + sgn::cnt_pan(k), sgn::panel_tasks(F.npiv, F.nrow, k));
+    }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = tid + u * kFThreads;
@@ -585,7 +588,10 @@ k_factor_dag(const sgn::FactorArgs A) {
       int* s2 = cf;                                            // DONE
       int* s3 = nullptr;
       if (kind == sgn::F_ZPANEL) { s1 = (T.a < P) ? cf + sgn::cnt_zc(P, Tn, T.b) : nullptr; s2 = nullptr; }
-      else if (kind == sgn::F_PANEL) s1 = cf + sgn::cnt_pan(k);
+      else if (kind == sgn::F_PANEL) {
+        s1 = cf + sgn::cnt_pan(k);
+        if (T.a == 0) s3 = cf + sgn::cnt_pan0(F.npiv, F.nrow, k);
+      }
       else if (kind == sgn::F_DIAGUPD) { s1 = cf + sgn::cnt_tile(P, k + 1, k + 1); s3 = cf + sgn::cnt_diag(P, k + 1); }
       else {
         s1 = cf + sgn::cnt_tile(P, T.a, tjb);

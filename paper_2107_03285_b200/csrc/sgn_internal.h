@@ -85,7 +85,8 @@ SGN_HD int tile_of_row(int npiv, int r) { return r < npiv ? r / 32 : ptiles(npiv
 //   F_ZPANEL  (f, a=t, b=cb)  : solve-panel block Z(t, cb).  Pivot tile t < P waits DIAG(f, t)
 //                              and ZC(f, cb) == t - cb (the blocks above it), signals ZC(f, cb);
 //                              struct tile t >= P waits DONE(f) == ftotal(f), ZC(f, cb) == P - cb
-// counters of front f at cbase: DONE, PAN(k), DIAG(k) (k < P), TILE(ti*(ti+1)/2 + tj), ZC(cb)
+// counters of front f at cbase: DONE, PAN(k), DIAG(k) (k < P), TILE(ti*(ti+1)/2 + tj), ZC(cb),
+// PAN0(k) (k < P)
 enum FKind : int32_t { F_ASM = 0, F_PANEL = 1, F_UPDATE = 2, F_ZPANEL = 3, F_DIAGUPD = 4 };
 struct FTask { int32_t kind_k, f, a, b; };
 constexpr int kDiagStride = 2 * kTile * kTile + 3 * kTile;   // scratch per step: D, L^T, D^-1
@@ -98,6 +99,11 @@ SGN_HD int cnt_pan(int k) { return 1 + k; }
 SGN_HD int cnt_diag(int P, int k) { return 1 + P + k; }
 SGN_HD int cnt_tile(int P, int ti, int tj) { return 1 + 2 * P + ti * (ti + 1) / 2 + tj; }
 SGN_HD int cnt_zc(int P, int T, int slab) { return 1 + 2 * P + T * (T + 1) / 2 + slab; }
+// PAN0(k): the TRSM task of row tile k+1 (t = 0) of step k -- all the diagonal update reads
+SGN_HD int cnt_pan0(int npiv, int nrow, int k) {
+  const int P = ptiles(npiv), T = ntiles_front(npiv, nrow);
+  return 1 + 2 * P + T * (T + 1) / 2 + (nrow + 31) / 32 + k;
+}
 
 struct Work { int32_t f, a, b, c; };   // generic work item
 

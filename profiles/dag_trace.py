@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--out", default="gpurun_out/dag_trace.npz")
     a = ap.parse_args()
     os.environ["SGN_DAG_TRACE"] = "1"
+    os.environ["SGN_BICG_GRAPH"] = "0"      # trace buffers are allocated lazily (not under capture)
     import torch
     from paper_2107_03285_b200._lib import lib
     from paper_2107_03285_b200.problems import build_sheet
