@@ -424,37 +424,55 @@ __device__ void f_ztask_pre(const sgn::FactorArgs& A, const DFront& F, int b, in
   double* Fm = front_ptr(A, F, b);
   const double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
   const double* ds = A.dscr + (int64_t)b * A.dstride + F.doff;
+  int* cf = A.cnt + (int64_t)b * A.n_fcnt + F.cbase;
+  const int Tn = sgn::ntiles_front(npiv, F.nrow);
   const int c0 = cb * kTile, wb = min(kTile, npiv - c0);
-  if (piv && cb == t) {
-    const double* blk = ds + (int64_t)t * sgn::kDiagStride;
-    for (int e = tid; e < kTile * kTile; e += kFThreads) {
-      const int i = e >> 5, j = e & 31;
-      if (i < nr && j < nr && i >= j) Fm[(int64_t)(lo + j) * ld + lo + i] = __ldcg(blk + e);
-    }
-  }
   double (*Pw)[kTile + 1] = v33(S.b[0]);
   V40 Lk = v40(S.b[2]);     // K-major: Lk[kk][row] = L(lo + row, k0 + kk)
   V40 Zk = v40(S.b[3]);     // K-major: Zk[kk][col] = Z(k0 + kk, c0 + col)
-  if (piv) {                // L^T of step t for the left solve
-    double (*Lt)[kTile + 1] = v33(S.b[1]);
-    const double* lt = ds + (int64_t)t * sgn::kDiagStride + kTile * kTile;
-    for (int e = tid; e < kTile * kTile; e += kFThreads) Lt[e >> 5][e & 31] = __ldcg(lt + e);
-  }
   const int row0 = warp * 8, i = row0 + g;
   double acc[4][2];
 #pragma unroll
   for (int nf = 0; nf < 4; ++nf) acc[nf][0] = acc[nf][1] = 0.0;
+  // L(t, j) is final up front (pivot tiles: DIAG(t) implies every panel of steps < t that
+  // wrote row tile t; struct tiles: the last step's panels, PAN(P-1), imply all earlier
+  // ones).  The Z(j, cb) terms are consumed as they become final (progressive waits on
+  // ZC(cb) instead of one up-front wait for the whole column above t): the column chain
+  // Z(t-1, cb) -> Z(t, cb) then costs one term, not the whole sum.
+  __shared__ int s_ready;
   const int jend = piv ? t : P;
-  for (int j = cb; j < jend; ++j) {
-    const int k0 = j * kTile, kw = min(kTile, npiv - k0);
-    double vl[8], vz[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = tid + u * kFThreads;
-      const int r = e & 31, c = e >> 5;
-      vl[u] = (r < nr && c < kw) ? __ldcg(Fm + (int64_t)(k0 + c) * ld + lo + r) : 0.0;  // L(lo + r, k0 + c)
-      vz[u] = (r < kw && c < wb) ? __ldcg(Zm + (int64_t)(c0 + c) * ld + k0 + r) : 0.0;  // Z(k0 + r, c0 + c)
+  int ready = cb;
+  if (tid == 0) {
+    if (piv) spin_ge(cf + sgn::cnt_diag(P, t), 1);
+    else spin_ge(cf + sgn::cnt_pan(P - 1), sgn::panel_tasks(npiv, F.nrow, P - 1));
+  }
+  __syncthreads();
+  double vl[8], vz[8];
+#define SGN_Z_LOAD(J_)                                                                              \
+  do {                                                                                              \
+    const int k0_ = (J_) * kTile, kw_ = min(kTile, npiv - k0_);                                     \
+    _Pragma("unroll") for (int u = 0; u < 8; ++u) {                                                 \
+      const int e = tid + u * kFThreads;                                                            \
+      const int r = e & 31, c = e >> 5;                                                             \
+      vl[u] = (r < nr && c < kw_) ? __ldcg(Fm + (int64_t)(k0_ + c) * ld + lo + r) : 0.0;            \
+      vz[u] = (r < kw_ && c < wb) ? __ldcg(Zm + (int64_t)(c0 + c) * ld + k0_ + r) : 0.0;            \
+    }                                                                                               \
+  } while (0)
+  auto wait_term = [&](int j) {
+    if (j < ready) return;
+    if (tid == 0) {
+      int zc;
+      while ((zc = ld_acq(cf + sgn::cnt_zc(P, Tn, cb))) < j - cb + 1) __nanosleep(20);
+      s_ready = cb + zc;
     }
+    __syncthreads();
+    ready = s_ready;
+  };
+  if (cb < jend) {
+    wait_term(cb);
+    SGN_Z_LOAD(cb);
+  }
+  for (int j = cb; j < jend; ++j) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = tid + u * kFThreads;
@@ -463,6 +481,10 @@ __device__ void f_ztask_pre(const sgn::FactorArgs& A, const DFront& F, int b, in
       Zk[r][c] = vz[u];
     }
     __syncthreads();
+    if (j + 1 < jend) {                   // next term's tiles in flight during the DMMAs
+      wait_term(j + 1);
+      SGN_Z_LOAD(j + 1);
+    }
 #pragma unroll
     for (int kk = 0; kk < kTile; kk += 4) {
       const double a = Lk[kk + q][row0 + g];
@@ -470,6 +492,19 @@ __device__ void f_ztask_pre(const sgn::FactorArgs& A, const DFront& F, int b, in
       for (int nf = 0; nf < 4; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], a, Zk[kk + q][nf * 8 + g]);
     }
     __syncthreads();
+  }
+#undef SGN_Z_LOAD
+  if (piv) {                // the left solve: D_t / L^T of step t (DIAG(t) waited above)
+    if (cb == t) {          // block (t, t) also publishes the factored diagonal block into F
+      const double* blk = ds + (int64_t)t * sgn::kDiagStride;
+      for (int e = tid; e < kTile * kTile; e += kFThreads) {
+        const int ii = e >> 5, jj = e & 31;
+        if (ii < nr && jj < nr && ii >= jj) Fm[(int64_t)(lo + jj) * ld + lo + ii] = __ldcg(blk + e);
+      }
+    }
+    double (*Lt)[kTile + 1] = v33(S.b[1]);
+    const double* lt = ds + (int64_t)t * sgn::kDiagStride + kTile * kTile;
+    for (int e = tid; e < kTile * kTile; e += kFThreads) Lt[e >> 5][e & 31] = __ldcg(lt + e);
   }
 #pragma unroll
   for (int nf = 0; nf < 4; ++nf)
@@ -541,15 +576,7 @@ k_factor_dag(const sgn::FactorArgs A) {
       } else if (kind == sgn::F_UPDATE || kind == sgn::F_DIAGUPD) {   // PAN(k) awaited inside
         const int ti = (kind == sgn::F_DIAGUPD) ? k + 1 : T.a, tj = (kind == sgn::F_DIAGUPD) ? k + 1 : tjb;
         spin_ge(cf + sgn::cnt_tile(P, ti, tj), 2 + k - ns);
-      } else {                                    // Z(t, cb): see f_ztask_pre
-        if (T.a < P) {
-          spin_ge(cf + sgn::cnt_diag(P, T.a), 1);
-          if (T.a > T.b) spin_ge(cf + sgn::cnt_zc(P, Tn, T.b), T.a - T.b);
-        } else {
-          spin_ge(cf, F.ftotal);
-          spin_ge(cf + sgn::cnt_zc(P, Tn, T.b), P - T.b);
-        }
-      }
+      }                                           // Z(t, cb): progressive waits in f_ztask_pre
     }
     __syncthreads();
     if (A.trace && tid == 0) A.trace[idx * 8 + 1] = gtimer();

@@ -82,9 +82,10 @@ SGN_HD int tile_of_row(int npiv, int r) { return r < npiv ? r / 32 : ptiles(npiv
 //   F_UPDATE  (f, k, a=ti, b=tj): waits PAN(f, k) == TRSM tasks of step k, TILE(f,ti,tj) == 1+k
 //   F_DIAGUPD (f, k)         : last update of tile (k+1, k+1) + LDL^T of D_{k+1}; waits as
 //                              F_UPDATE(k, k+1, k+1); signals DIAG(f, k+1)
-//   F_ZPANEL  (f, a=t, b=cb)  : solve-panel block Z(t, cb).  Pivot tile t < P waits DIAG(f, t)
-//                              and ZC(f, cb) == t - cb (the blocks above it), signals ZC(f, cb);
-//                              struct tile t >= P waits DONE(f) == ftotal(f), ZC(f, cb) == P - cb
+//   F_ZPANEL  (f, a=t, b=cb)  : solve-panel block Z(t, cb) = sum_j L(t, j) Z(j, cb) (+ left solve
+//                              with L(t, t) for pivot tiles).  Waits DIAG(f, t) (pivot tiles) or
+//                              PAN(f, P-1) (struct tiles), then progressively, per term j,
+//                              ZC(f, cb) > j - cb; pivot tiles signal ZC(f, cb)
 // counters of front f at cbase: DONE, PAN(k), DIAG(k) (k < P), TILE(ti*(ti+1)/2 + tj), ZC(cb),
 // PAN0(k) (k < P)
 enum FKind : int32_t { F_ASM = 0, F_PANEL = 1, F_UPDATE = 2, F_ZPANEL = 3, F_DIAGUPD = 4 };

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--out", default="gpurun_out/fdag_trace.npz")
     ap.add_argument("--which", default="kkt", choices=("kkt", "gx"), help="KKT or G_x (adjoint) factor")
     ap.add_argument("--summary", action="store_true", help="per-kind totals only")
+    ap.add_argument("--ctas", type=int, default=592, help="persistent CTAs (timeline normalisation)")
     a = ap.parse_args()
     os.environ["SGN_FDAG_TRACE"] = "1"
     import torch
@@ -61,7 +62,24 @@ def main():
         m = kind == k
         if m.any():
             print(f"{KIND[k]:7s} n={m.sum():6d} busy_med={np.median(T[m, 2] - T[m, 1]):6.2f} "
-                  f"wait_med={np.median(T[m, 1] - T[m, 0]):6.2f} busy_sum_us={np.sum(T[m, 2] - T[m, 1]):9.1f}")
+                  f"wait_med={np.median(T[m, 1] - T[m, 0]):6.2f} busy_sum_us={np.sum(T[m, 2] - T[m, 1]):9.1f} "
+                  f"wait_sum_us={np.sum(T[m, 1] - T[m, 0]):9.1f}")
+    # CTA occupancy over time: busy / waiting / idle (between tasks) fractions per 5% of the span
+    span = T[:, 2].max()
+    sm = a_sm = None
+    nb = 20
+    edges = np.linspace(0, span, nb + 1)
+    def frac(t0, t1):
+        out = np.zeros(nb)
+        for i in range(nb):
+            lo, hi = edges[i], edges[i + 1]
+            out[i] = np.clip(np.minimum(t1, hi) - np.maximum(t0, lo), 0, None).sum()
+        return out
+    nct = len(set(zip(tr_sm.tolist()))) if False else None
+    busy, wait = frac(T[:, 1], T[:, 2]), frac(T[:, 0], T[:, 1])
+    cap = (edges[1] - edges[0]) * a.ctas
+    print("timeline (per 5% of span): busy% / wait%")
+    print(" ".join(f"{100 * b / cap:3.0f}/{100 * w / cap:2.0f}" for b, w in zip(busy, wait)))
     if a.summary:
         return
     print("per level: first ready / last end (us)")
