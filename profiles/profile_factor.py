@@ -12,9 +12,16 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     a = ap.parse_args()
     import torch
-    from paper_2107_03285_b200.problems import build_sheet
-    prob, p0 = build_sheet(a.config)
-    x = prob.simulate(p0)
+    from paper_2107_03285_b200.problems import build_beam, build_sheet, build_shell
+    if a.config == 3:
+        prob, p0, _ = build_beam(0)
+        x = prob._x_warm
+    elif a.config == 4:
+        prob, p0 = build_shell(201, 100)
+        x = prob.simulate(p0)
+    else:
+        prob, p0 = build_sheet(a.config)
+        x = prob.simulate(p0)
     prob._load(x, p0)
     eng = prob.engine
     eng.direction()
