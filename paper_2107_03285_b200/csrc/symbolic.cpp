@@ -325,7 +325,10 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
         }
       }
   }
-  if (leaf_size <= 0) leaf_size = 64;
+  if (leaf_size <= 0) {
+    leaf_size = 64;
+    if (const char* e = std::getenv("SGN_LEAF_SIZE")) leaf_size = std::max<int64_t>(4, std::atoll(e));
+  }
   s.pair_mode = (s.n_x > 0);
   if (s.pair_mode && (s.n_c != s.n_x || 2 * s.n_x + s.n_p != n)) {
     last_error() = "KKT mode needs n_c == n_x and n == 2*n_x + n_p";

@@ -238,8 +238,9 @@ class VertexPlan:
     the element Hessians: both copies are one contiguous run of column (v,i)'s nonzeros, so
     every store is coalesced) and to G_x[r, (v,i)].  It is the sum, in the same element
     order, of the staged path (element blocks -> sorted element->nonzero lists, `k_gather`),
-    without the element-block round trip through HBM; K comes out exactly symmetric.  The remaining KKT entries (constants and the G_p block) keep the gather,
-    restricted to their own nonzeros (`rest_*`)."""
+    without the element-block round trip through HBM.  The remaining KKT entries
+    (constants and the G_p block) keep the gather, restricted to their own nonzeros
+    (`rest_*`)."""
 
     def __init__(self, pl: "MeshPlan"):
         g = pl.groups[0]

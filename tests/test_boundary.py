@@ -106,3 +106,62 @@ def test_c2_plan_and_symbolic_sizes():
     sy = Symbolic(pl.dim, pl.K_indptr, pl.K_indices, pl.n_x, pl.n_p, pl.n_x)
     st = sy.stats()
     assert st["n"] == 40000 and st["max_piv"] == 400
+
+
+@pytest.mark.parametrize("which", ["c1", "c3"])
+def test_vertex_plan_covers_the_staged_lists(which):
+    """The fused vertex-centric assembly plan sums, for every G_x entry of K (both copies)
+    and of G_x, exactly the element-Hessian terms of the staged element->nonzero lists, in
+    the same element order; the rest of K (constants, G_p) goes to the restricted gather."""
+    from paper_2107_03285_b200.engine import MeshPlan, vertex_plan
+    from paper_2107_03285_b200.problems import beam_spec, sheet_spec
+    s = sheet_spec(1) if which == "c1" else beam_spec(0)
+    pl = MeshPlan(s["X0"], s["conn"], s["kind"], s["fixed_verts"], s["pmap"], s["target_dofs"],
+                  s.get("w_target", 1.0), s.get("w_reg", 0.0), f_ext=s.get("f_ext"),
+                  rest_base=s.get("rest_base"), R=s.get("R"))
+    vp = vertex_plan(pl)
+    assert vp is not None and vp.max_inc <= 32
+    g = pl.groups[0]
+    d, nd = pl.d, g.nd
+    dst = vp.out_dst.reshape(-1, 3)
+    # every K nonzero is produced exactly once: fused (two copies per output) or restricted
+    owner = np.zeros(pl.nnz, np.int64)
+    np.add.at(owner, dst[:, 0], 1)
+    np.add.at(owner, dst[:, 1], 1)
+    np.add.at(owner, vp.rest_dst, 1)
+    assert (owner == 1).all()
+    assert np.array_equal(np.sort(dst[:, 2]), np.arange(pl.G_nnz))     # G_x: each entry once
+    # per output: the staged list of its K[lambda_r, x_c] entry, decoded to (element, row, col)
+    inc_e, inc_a = vp.inc_ea >> 2, vp.inc_ea & 3
+    task_of_out = np.repeat(np.arange(vp.n_task), np.diff(vp.out_ptr))
+    rng = np.random.default_rng(0)
+    for o in rng.choice(vp.n_out, size=min(300, vp.n_out), replace=False):
+        t = task_of_out[o]
+        cons = vp.con_idx[vp.con_ptr[o]:vp.con_ptr[o + 1]]
+        slot, i, r = cons // (d * nd), (cons // nd) % d, cons % nd
+        elems = inc_e[vp.inc_ptr[t] + slot]
+        a = inc_a[vp.inc_ptr[t] + slot]
+        got = [(int(e), int(rr), int(aa * d + ii)) for e, rr, aa, ii in zip(elems, r, a, i)]
+        k = dst[o, 0]
+        src = pl.K_src[pl.K_ptr[k]:pl.K_ptr[k + 1]] - g.hoff
+        want = [(int(x // (nd * nd)), int((x % (nd * nd)) // nd), int(x % nd)) for x in src]
+        assert got == want                      # same terms, same (ascending element) order
+        assert np.all(pl.K_coef[pl.K_ptr[k]:pl.K_ptr[k + 1]] == 1.0) and pl.K_base[k] == 0.0
+
+
+def test_mixed_slots_cover_the_pmap_support():
+    from paper_2107_03285_b200.engine import MeshPlan
+    from paper_2107_03285_b200.problems import sheet_spec
+    s = sheet_spec(2)
+    pl = MeshPlan(s["X0"], s["conn"], "tri", s["fixed_verts"], s["pmap"], s["target_dofs"], 1.0, 2e-6)
+    g = pl.groups[0]
+    used = np.zeros(pl.n_v * pl.d, bool)
+    used[np.asarray(s["pmap"][0])] = True
+    el_dofs = (g.conn[:, :, None] * pl.d + np.arange(pl.d)).reshape(g.n_e, -1)
+    sup = used[el_dofs].any(axis=1)
+    assert np.array_equal(g.mslot >= 0, sup) and np.array_equal(g.melems, np.flatnonzero(sup))
+    assert np.array_equal(g.mslot[g.melems], np.arange(g.n_m))
+    # every G_p contribution reads a mixed slot of the support
+    nd2 = g.nd * g.nd
+    msrc = pl.K_src[pl.K_src >= g.moff] - g.moff
+    assert (msrc // nd2 < g.n_m).all()

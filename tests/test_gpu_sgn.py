@@ -201,3 +201,34 @@ def test_sheet_c2_direction_matches_oracle(cuda):
     assert _rel(sd.dp, d_ref.dp) <= 1e-8
     xo = oprob.simulate(p0)
     assert _rel(x, xo) <= 1e-10
+
+
+@pytest.mark.parametrize("which", ["sheet", "beam"])
+def test_fused_vertex_assembly_matches_staged_path(cuda, which):
+    """Fused vertex-centric assembly (product path) vs the staged element-block + gather
+    path: same terms in the same order, so K and G_x agree to rounding of the symmetric
+    copy (column (v, i) of the element Hessians in place of its row)."""
+    from paper_2107_03285_b200.problems import build_beam, build_sheet
+    if which == "sheet":
+        prob, p0 = build_sheet(1)
+        x = prob.simulate(p0)
+    else:
+        prob, p0, _ = build_beam(0)
+        x = prob._x_warm
+    eng, pl = prob.engine, prob.plan
+    assert eng.vplan is not None
+    prob._load(x, p0)
+    eng.positions()
+    eng.assemble_kkt()
+    kf, gf = eng.kvals[0].cpu().numpy().copy(), eng.gvals[0].cpu().numpy().copy()
+    vp, eng.vplan = eng.vplan, None
+    try:
+        eng.positions()
+        eng.assemble_kkt()
+        eng.gx_values(force=True)
+        ks, gs = eng.kvals[0].cpu().numpy(), eng.gvals[0].cpu().numpy()
+    finally:
+        eng.vplan = vp
+    assert _rel(kf, ks) <= 1e-14 and _rel(gf, gs) <= 1e-14
+    K = sp.csc_matrix((kf, pl.K_indices, pl.K_indptr), shape=(pl.dim, pl.dim))
+    assert abs(K - K.T).max() <= 1e-14 * abs(K).max()
