@@ -26,6 +26,20 @@ def main():
     import torch
     from paper_2107_03285_b200._lib import lib
     from paper_2107_03285_b200.problems import build_beam, build_sheet, build_shell
+    if a.config == 5:
+        from paper_2107_03285_b200.problems import build_sheet_batch
+        bd = build_sheet_batch(2, 0, instances=range(1, 65))
+        X, _ = bd.simulate(bd.p0)
+        bd.load(X, bd.p0)
+        eng = bd.engine
+        eng.assemble()
+        from paper_2107_03285_b200.engine import sgn_solve_stages
+        sgn_solve_stages(eng, None)
+        fac = eng.kfac
+        for _ in range(2):
+            fac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda)
+        torch.cuda.synchronize()
+        return summarize(a, fac)
     if a.config == 3:
         prob, p0, _ = build_beam(0)
     elif a.config == 4:
@@ -43,6 +57,11 @@ def main():
         else:
             fac.numeric(eng.gvals, 0.0, 0.0)
     torch.cuda.synchronize()
+    return summarize(a, fac)
+
+
+def summarize(a, fac):
+    from paper_2107_03285_b200._lib import lib
     nt = ctypes.c_int64()
     lib().sgn_debug_factor_trace(fac._h, None, 0, ctypes.byref(nt), None)
     meta = np.zeros(6 * nt.value, np.int32)
@@ -51,6 +70,9 @@ def main():
                                  meta.ctypes.data_as(ctypes.c_void_p))
     tr = tr.reshape(-1, 8)
     meta = meta.reshape(-1, 6)
+    B = int(getattr(fac, "batch", 1))
+    if B > 1:                       # trace rows are task-major, instance-minor
+        meta = np.repeat(meta[:len(meta) // B], B, axis=0)
     base = tr[:, 0].min()
     T = (tr[:, :3].astype(np.float64) - base) / 1e3
     M = np.where(tr[:, 4:8] > 0, (tr[:, 4:8].astype(np.float64) - base) / 1e3, np.nan)
