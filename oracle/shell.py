@@ -235,9 +235,10 @@ def shell_spec(n: int = 201, nc: int = 100, L: float = 1.0, t: float = 0.05, E: 
 class ShellProblem:
     """Oracle shell problem (membrane + hinge groups; residual r = x_z - X_z(p)).
 
-    Contract = reference sensitivity.py:29-120; equilibrium rows scaled by 1/E."""
+    Contract = reference sensitivity.py:29-120; equilibrium rows scaled by the inverse
+    geometric mean of the membrane and lowest bending stiffness."""
 
-    def __init__(self, spec, tol=1e-12):
+    def __init__(self, spec, tol=None):
         self.s = spec
         self.X0 = spec["X0"]
         self.n_v = self.X0.shape[0]
@@ -254,8 +255,13 @@ class ShellProblem:
         self.tdofs = spec["target_dofs"]
         # residual p-map R: r = x[tdofs] - X(p)[free dof of tdofs]
         self.R = sp.csr_matrix(self.P[self.free_dofs][self.tdofs])
-        self.scale = 1.0 / spec["E"]
-        self.tol = tol
+        # equilibrium rows scaled by the inverse geometric mean of the membrane and lowest
+        # bending stiffness (as paper_2107_03285_b200.problems.shell_scale, which says why)
+        n = int(round(np.sqrt(self.n_v)))
+        h = 1.0 / (n - 1)
+        D = spec["E"] * spec["t"] ** 3 / (12.0 * (1.0 - spec["nu"] ** 2))
+        self.scale = 1.0 / np.sqrt(spec["E"] * spec["t"] * D * np.pi ** 4 * h * h)
+        self.tol = tol if tol is not None else 1e-4 * self.scale * spec["rho_g"] * spec["t"] * h * h
         self.groups = [("membrane", spec["tris"]), ("hinge", spec["hinges"])]
         self._x_warm = None
 

@@ -495,6 +495,170 @@ __device__ bool dag_bwd_fat(const SolveArgs& A, const sgn::Task& T, int b, const
   return true;
 }
 
+// ---- no-Z root front (Front::noz): blocked substitution with L11 read from the front -----
+// The factored diagonal blocks sit in the front (D on the diagonal / 2x2 slots, unit L
+// strictly below, factor_dag.cu:factor_publish); L_ji below them.  Row tile j is one task.
+// Forward: y_j = L_jj^{-1} (v_j - sum_{i<j} L_ji y_i), z_j = D_j^{-1} y_j, with v_j the
+// right-hand side + children's updates (as dag_fwd) and y kept in the root's x slots; the
+// terms are consumed as the front's forward counter CF(f) says y_i is final.
+// Backward: x_j = L_jj^{-T} (z_j - sum_{i>j} L_ij^T x_i), progressive over CB(f).
+__device__ __forceinline__ bool dslot(int pivtype, int r, int c) {   // D's off-diagonal of a 2x2 pivot
+  return pivtype == 2 && (r & 1) && c == r - 1;
+}
+
+__device__ bool dag_root_fwd(const SolveArgs& A, const sgn::Task& T, int b, const int* cnt, int64_t idx) {
+  __shared__ double part[8][33];
+  __shared__ double Ls[32][33];
+  __shared__ int s_ready;
+  const DFront F = A.fronts[T.f];
+  const int j = -T.a - 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r0 = 32 * j, w = min(32, F.npiv - r0);
+  if (A.nop || (A.leading && F.is_root_p)) { dag_wait(A, T, cnt); return true; }
+  const double* Fm = A.fstore + (int64_t)b * A.fstride + F.foff;
+  const int64_t ld = F.nrow;
+  double* yb = A.xbuf + (int64_t)b * A.n + F.first;
+  double base = 0.0;
+  int64_t q0 = 0, q1 = 0;
+  if (warp == 0 && lane < w) {
+    base = A.b_in[(int64_t)b * A.n + A.perm[F.first + r0 + lane]];
+    q0 = A.gptr[F.voff + r0 + lane];
+    q1 = A.gptr[F.voff + r0 + lane + 1];
+  }
+  // the diagonal block (final: the factorization is complete before any solve)
+  for (int e = tid; e < 1024; e += kSolveThreads) {
+    const int r = e & 31, c = e >> 5;
+    Ls[r][c] = (r < w && c < w && c <= r) ? Fm[(int64_t)(r0 + c) * ld + r0 + r] : 0.0;
+  }
+  dag_wait(A, T, cnt);                                  // children's forward done
+  const int* cf = cnt + T.sig;                          // CF(f): this front's tiles, in order
+  double acc = 0.0;                                     // row r0 + lane, columns 4 warp + m of tile i
+  int ready = 0;
+  for (int i = 0; i < j; ++i) {
+    if (i >= ready) {
+      if (tid == 0) {
+        int c;
+        while ((c = ld_acquire(cf)) < i + 1) __nanosleep(20);
+        s_ready = c;
+      }
+      __syncthreads();
+      ready = s_ready;
+    }
+    const int c0 = 32 * i + 4 * warp;
+    double l[4], y[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      l[m] = (lane < w) ? __ldcg(Fm + (int64_t)(c0 + m) * ld + r0 + lane) : 0.0;
+      y[m] = __ldcg(yb + c0 + m);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) acc = fma(l[m], y[m], acc);
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp != 0) return true;
+  double v = 0.0;
+  if (lane < w) {
+    const double* ub = A.ubuf + (int64_t)b * A.ustride;
+    v = base;
+    for (int64_t q = q0; q < q1; ++q) v += __ldcg(ub + A.gsrc[q]);
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += part[k][lane];
+    v -= s;
+  }
+  // unit lower substitution inside the diagonal block (lane = row), D slots excluded
+  double y = v;
+  for (int c = 0; c < w; ++c) {
+    const double yc = __shfl_sync(0xffffffffu, y, c);
+    if (lane > c && !dslot(F.pivtype, lane, c)) y = fma(-Ls[lane][c], yc, y);
+  }
+  const double yp = __shfl_xor_sync(0xffffffffu, y, 1);   // 2x2 pivot partner
+  if (lane < w) {
+    yb[r0 + lane] = y;
+    double z;
+    if (F.pivtype == 2) {
+      const int re = lane & ~1;
+      const double da = Ls[re][re], db = Ls[re + 1][re], dc = Ls[re + 1][re + 1];
+      const double det = da * dc - db * db;
+      z = ((lane & 1) == 0) ? (dc * y - db * yp) / det : (da * y - db * yp) / det;
+    } else {
+      z = y / Ls[lane][lane];
+    }
+    A.zbuf[(int64_t)b * A.n + F.first + r0 + lane] = z;
+  }
+  return true;
+}
+
+__device__ bool dag_root_bwd(const SolveArgs& A, const sgn::Task& T, int b, const int* cnt, int64_t idx) {
+  __shared__ double Ls[32][33];
+  __shared__ double colsum[8][33];
+  __shared__ int s_ready;
+  const DFront F = A.fronts[T.f];
+  const int j = -T.a - 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r0 = 32 * j, w = min(32, F.npiv - r0);
+  const int P = (F.npiv + 31) / 32;
+  double* xb = A.xbuf + (int64_t)b * A.n + F.first;
+  double* xo = A.x_out + (int64_t)b * A.n;
+  if (A.nop) { dag_wait(A, T, cnt); return true; }
+  if (A.leading && F.is_root_p) {
+    dag_wait(A, T, cnt);
+    if (tid < w) { xb[r0 + tid] = 0.0; xo[A.perm[F.first + r0 + tid]] = 0.0; }
+    return true;
+  }
+  const double* Fm = A.fstore + (int64_t)b * A.fstride + F.foff;
+  const int64_t ld = F.nrow;
+  for (int e = tid; e < 1024; e += kSolveThreads) {
+    const int r = e & 31, c = e >> 5;
+    Ls[r][c] = (r < w && c < w && c <= r) ? Fm[(int64_t)(r0 + c) * ld + r0 + r] : 0.0;
+  }
+  dag_wait(A, T, cnt);                                  // the front's forward done
+  const int* cbk = cnt + T.sig;                         // CB(f): tiles P-1, P-2, ... done
+  // acc[m]: column r0 + 4 warp + m, partial over rows 32 i + lane
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int ready = P;                                        // x_i final for i >= ready
+  for (int i = P - 1; i > j; --i) {
+    if (i < ready) {
+      if (tid == 0) {
+        int c;
+        while ((c = ld_acquire(cbk)) < P - i) __nanosleep(20);
+        s_ready = P - c;
+      }
+      __syncthreads();
+      ready = s_ready;
+    }
+    const int ri = 32 * i + lane;
+    const double xi = (ri < F.npiv) ? __ldcg(xb + ri) : 0.0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int c = 4 * warp + m;
+      const double l = (ri < F.npiv && c < w) ? __ldcg(Fm + (int64_t)(r0 + c) * ld + ri) : 0.0;
+      acc[m] = fma(l, xi, acc[m]);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    double a = acc[m];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) colsum[0][4 * warp + m] = a;
+  }
+  __syncthreads();
+  if (warp != 0) return true;
+  double x = (lane < w) ? __ldcg(A.zbuf + (int64_t)b * A.n + F.first + r0 + lane) - colsum[0][lane] : 0.0;
+  // unit upper (L_jj^T) back substitution, lane = column c: x_c -= L[r][c] x_r for r > c
+  for (int r = w - 1; r > 0; --r) {
+    const double xr = __shfl_sync(0xffffffffu, x, r);
+    if (lane < r && !dslot(F.pivtype, r, lane)) x = fma(-Ls[r][lane], xr, x);
+  }
+  if (lane < w) {
+    xb[r0 + lane] = x;
+    xo[A.perm[F.first + r0 + lane]] = x;
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(kSolveThreads, 3)
 k_solve_dag(const SolveArgs A) {
   __shared__ int s_idx;
@@ -516,7 +680,9 @@ k_solve_dag(const SolveArgs A) {
     if (T.kind == sgn::T_FWD) sig = dag_fwd(A, T, b, cnt, idx);
     else if (T.kind == sgn::T_BWD) sig = dag_bwd(A, T, b, cnt, idx);
     else if (T.kind == sgn::T_FWD_FAT) sig = dag_fwd_fat(A, T, b, cnt, idx);
-    else sig = dag_bwd_fat(A, T, b, cnt, idx);
+    else if (T.kind == sgn::T_BWD_FAT) sig = dag_bwd_fat(A, T, b, cnt, idx);
+    else if (T.kind == sgn::T_RFWD) sig = dag_root_fwd(A, T, b, cnt, idx);
+    else sig = dag_root_bwd(A, T, b, cnt, idx);
     __syncthreads();                               // every thread's writes precede the release
     if (sig && threadIdx.x == 0) {
       asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(cnt + T.sig) : "memory");
@@ -981,7 +1147,7 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
     d.npiv = F.npiv; d.nrow = F.nrow; d.parent = F.parent; d.pivtype = F.pivtype;
     d.child_begin = F.child_begin; d.child_end = F.child_end; d.is_root_p = F.is_root_p;
     d.level = F.level;
-    d.cbase = F.cbase; d.ftotal = F.ftotal; d.pad = 0;
+    d.cbase = F.cbase; d.ftotal = F.ftotal; d.flags = F.noz ? 1 : 0;
   }
   std::vector<int32_t> idx32(s.indices.begin(), s.indices.end());
   int rc = 0;

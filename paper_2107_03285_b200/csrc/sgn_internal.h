@@ -37,6 +37,7 @@ struct Front {
   int64_t doff = 0;       // offset of the factored 32x32 diagonal blocks (scratch)
   int64_t cbase = 0;      // first dependency counter of the front (persistent factorization)
   int32_t ftotal = 0;     // assembly + panel + update tasks of the front
+  int32_t noz = 0;        // no solve panel: the root p-front of a large n_p (blocked substitution)
 };
 
 // Device-side mirror of Front (POD, 16-byte aligned for vector loads).
@@ -54,7 +55,7 @@ struct DFront {
   int32_t npiv, nrow, parent, pivtype;
   int32_t child_begin, child_end, is_root_p, level;
   int64_t cbase;
-  int32_t ftotal, pad;
+  int32_t ftotal, flags;  // flags bit 0: noz (Front::noz)
 };
 
 // Split tile grid of a front: pivot tiles a < P cover rows [32a, min(32a+32, npiv)), the
@@ -120,7 +121,9 @@ constexpr int kFatRowsBwd = 128;  // rows of a one-task backward front solve (Z 
 // topological order and grabbed in that order by resident CTAs, so waits always target
 // earlier tasks and the schedule cannot deadlock.
 // T_FWD_FAT / T_BWD_FAT: the whole forward / backward step of a small front in one task
-enum TaskKind : int32_t { T_FWD = 1, T_BWD = 2, T_FWD_FAT = 3, T_BWD_FAT = 4 };
+// T_RFWD / T_RBWD: row tile j of a no-Z root front (work item a = -2 - j), blocked
+// substitution with L11 read from the front, progressive over the front's own counter
+enum TaskKind : int32_t { T_FWD = 1, T_BWD = 2, T_FWD_FAT = 3, T_BWD_FAT = 4, T_RFWD = 5, T_RBWD = 6 };
 struct Task { int32_t kind, f, a, b, c, sig, w0, w1; };
 struct Launch { int32_t kind; int32_t level; int64_t off; int64_t count; int32_t pivtype = 1; int32_t pad = 0; };
 

@@ -647,12 +647,19 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   s.nnz_l = 0;
   s.flops = 0;
   s.max_front = s.max_piv = 0;
+  // The root p-front of a large n_p (>= kNoZTiles pivot tiles, no contribution rows) gets no
+  // solve panel: forming L11^{-1} costs npiv^3/3 flops (as much as its factorization) and a
+  // column-serial tail, to speed up a handful of solves.  Its solves are blocked
+  // substitutions instead (T_RFWD / T_RBWD).  SGN_NOZ_TILES overrides (0: always Z).
+  int64_t kNoZTiles = 0;     // off by default: pays only when few solves follow a factorization
+  if (const char* e = std::getenv("SGN_NOZ_TILES")) kNoZTiles = std::atoll(e);
   for (auto& F : s.fronts) {
     const int64_t nr = F.nrow, ns = F.nrow - F.npiv;
+    F.noz = (kNoZTiles > 0 && F.is_root_p && ns == 0 && ptiles(F.npiv) >= kNoZTiles) ? 1 : 0;
     F.foff = s.front_doubles; s.front_doubles += nr * nr;
     F.uoff = s.u_doubles; s.u_doubles += ns;
     F.voff = s.v_doubles; s.v_doubles += nr;
-    F.zoff = s.z_doubles; s.z_doubles += nr * F.npiv;
+    F.zoff = s.z_doubles; s.z_doubles += F.noz ? 0 : nr * F.npiv;
     F.doff = s.d_doubles; s.d_doubles += (int64_t)((F.npiv + kTile - 1) / kTile) * kDiagStride;
     const int64_t T = ntiles_front(F.npiv, F.nrow);
     F.tile_base = s.ntiles; s.ntiles += T * (T + 1) / 2;
@@ -774,7 +781,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   for (int32_t lv = 0; lv < s.n_levels; ++lv)
     for (int32_t f : s.level_fronts[lv]) {
       const Front& F = s.fronts[f];
-      if (F.npiv == 0) continue;
+      if (F.npiv == 0 || F.noz) continue;
       const int32_t P = ptiles(F.npiv), T = ntiles_front(F.npiv, F.nrow);
       for (int32_t t = z_inline(F) ? P : 0; t < T; ++t)
         for (int32_t cb = 0; cb < std::min(t + 1, P); ++cb) {
@@ -842,7 +849,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
       }
       for (int32_t f : fl) {                                 // inline Z row of pivot tile k
         const Front& F = s.fronts[f];
-        if (k < ptiles(F.npiv) && z_inline(F))
+        if (k < ptiles(F.npiv) && z_inline(F) && !F.noz)
           for (int32_t cb = 0; cb <= k; ++cb) ft(F_ZPANEL, 0, f, k, cb);
       }
       emit_z(lv);
@@ -884,6 +891,10 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     s.fwd_off[lv] = (int64_t)s.work.size();
     for (int32_t f : s.level_fronts[lv]) {
       const Front& F = s.fronts[f];
+      if (F.noz) {                                        // blocked substitution, tile by tile
+        for (int32_t j = 0; j < ptiles(F.npiv); ++j) s.work.push_back({f, -2 - j, 0, new_group(1)});
+        continue;
+      }
       if (fat_front(F, kFatRows)) { s.work.push_back({f, -1, 0, new_group(1)}); continue; }
       for (int32_t r0 = 0; r0 < F.nrow; r0 += kFwdRows) {
         const int32_t cend = (r0 < F.npiv) ? std::min(F.npiv, r0 + kFwdRows) : F.npiv;
@@ -896,6 +907,10 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     s.bwd_off[lv] = (int64_t)s.work.size();
     for (int32_t f : s.level_fronts[lv]) {
       const Front& F = s.fronts[f];
+      if (F.noz) {                                        // last tile first
+        for (int32_t j = ptiles(F.npiv) - 1; j >= 0; --j) s.work.push_back({f, -2 - j, 0, new_group(1)});
+        continue;
+      }
       if (fat_front(F, kFatRowsBwd)) { s.work.push_back({f, -1, 0, new_group(1)}); continue; }
       for (int32_t c0 = 0; c0 < std::max(F.npiv, 1); c0 += kBwdCols) {
         const int32_t rs = (c0 / kBwdRows) * kBwdRows;          // first chunk holding rows >= c0
@@ -918,7 +933,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
       for (int64_t w = s.fwd_off[lv]; w < s.fwd_off[lv] + s.fwd_cnt[lv]; ++w)
         if (s.work[w].b == 0) nfg[s.work[w].f]++;
       for (int64_t w = s.bwd_off[lv]; w < s.bwd_off[lv] + s.bwd_cnt[lv]; ++w)
-        if (s.work[w].b == (s.work[w].a / kBwdRows) * kBwdRows) nbg[s.work[w].f]++;
+        if (s.work[w].a <= -2 || s.work[w].b == (s.work[w].a / kBwdRows) * kBwdRows) nbg[s.work[w].f]++;
     }
     // inverse gather map
     {
@@ -956,14 +971,14 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
         const Front& F = s.fronts[s.work[w].f];
         std::vector<std::pair<int32_t, int32_t>> ch;
         for (int32_t ci = F.child_begin; ci < F.child_end; ++ci) ch.push_back({s.children[ci], nfg[s.children[ci]]});
-        add(s.work[w].a < 0 ? T_FWD_FAT : T_FWD, s.work[w], s.work[w].f, ch);
+        add(s.work[w].a <= -2 ? T_RFWD : (s.work[w].a < 0 ? T_FWD_FAT : T_FWD), s.work[w], s.work[w].f, ch);
       }
     }
     for (int32_t lv = s.n_levels - 1; lv >= 0; --lv) {
       for (int64_t w = s.bwd_off[lv]; w < s.bwd_off[lv] + s.bwd_cnt[lv]; ++w) {
         const int32_t f = s.work[w].f;
         const int32_t p = s.fronts[f].parent;
-        const int32_t kind = s.work[w].a < 0 ? T_BWD_FAT : T_BWD;
+        const int32_t kind = s.work[w].a <= -2 ? T_RBWD : (s.work[w].a < 0 ? T_BWD_FAT : T_BWD);
         if (p >= 0) add(kind, s.work[w], NF + f, {{NF + p, nbg[p]}});
         else add(kind, s.work[w], NF + f, {{f, nfg[f]}});
       }

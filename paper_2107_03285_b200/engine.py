@@ -341,6 +341,7 @@ def _gx_share(eng, full: int) -> int:
         return min(_GX_CTAS, full - 1)
     return max(1, (3 * full) // 16)
 _DEBUG_NAN = os.environ.get("SGN_DEBUG_NAN", "0") == "1"
+_DEBUG_NEWTON = os.environ.get("SGN_DEBUG_NEWTON", "0") == "1"
 
 
 def _nan_probe(eng, where):
@@ -766,6 +767,8 @@ class DeviceEngine:
             check(lib().sgn_reduce(2, n, B, ptr(self.gx), None, n, ptr(self.scal[3]), st))
             sc = self.scal.cpu().numpy()
             g_inf, e0 = sc[3], self._energies(sc)
+            if _DEBUG_NEWTON:
+                print(f"[newton] |g|inf {g_inf[:4]} E {e0[:4]} tol {tol:.3e}", flush=True)
             status[run & (g_inf <= tol)] = 1
             run = status == 0
             if not run.any():

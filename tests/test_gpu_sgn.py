@@ -232,3 +232,32 @@ def test_fused_vertex_assembly_matches_staged_path(cuda, which):
     assert _rel(kf, ks) <= 1e-14 and _rel(gf, gs) <= 1e-14
     K = sp.csc_matrix((kf, pl.K_indices, pl.K_indptr), shape=(pl.dim, pl.dim))
     assert abs(K - K.T).max() <= 1e-14 * abs(K).max()
+
+
+def test_no_solve_panel_root_front_matches_oracle(cuda):
+    """Root p-front without a solve panel (SGN_NOZ_TILES: blocked substitution over L11 in
+    the solve, T_RFWD / T_RBWD) on config 1 and 2: same direction as the oracle.  Run in a
+    subprocess: the option is read when the symbolic analysis is built."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+from oracle import sgn_cpu
+from oracle.configs import oracle_sheet
+from paper_2107_03285_b200 import OptimizerConfig, direction_sgn
+from paper_2107_03285_b200.problems import build_sheet
+for c in (1, 2):
+    prob, p0 = build_sheet(c)
+    x = prob.simulate(p0)
+    sd = direction_sgn(prob, x, p0, OptimizerConfig())
+    oprob, _ = oracle_sheet(c)
+    ref = sgn_cpu.direction_sgn(oprob, x, p0)
+    err = np.linalg.norm(sd.dp - ref.dp) / np.linalg.norm(ref.dp)
+    assert sd.relative_residual <= 1e-10 and err <= 1e-8, (c, err, sd.relative_residual)
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SGN_NOZ_TILES="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
