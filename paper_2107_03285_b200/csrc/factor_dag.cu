@@ -236,14 +236,6 @@ __device__ __forceinline__ void factor_publish(const sgn::FactorArgs& A, const D
     const bool dslot = F.pivtype == 2 && (cp & 1) == 0 && cc == cp + 1;
     ds[kTile * kTile + e] = (cc > cp && cc < w && !dslot) ? D[cc][cp] : 0.0;
   }
-  if (F.flags & 1) {          // no solve panel: the factored diagonal block goes to the front here
-    double* Fm = front_ptr(A, F, b);
-    const int64_t ld = F.nrow;
-    for (int e = tid; e < kTile * kTile; e += kFThreads) {
-      const int r = e & 31, c = e >> 5;
-      if (r < w && c < w && c <= r) Fm[(int64_t)(j0 + c) * ld + j0 + r] = D[r][c];
-    }
-  }
   if (tid < w) {
     double* di = ds + 2 * kTile * kTile + 3 * tid;
     if (F.pivtype == 2) {

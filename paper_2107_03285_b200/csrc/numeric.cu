@@ -64,6 +64,7 @@ struct SolveArgs {
   int64_t n; double* part; int64_t pstride; int* tickets; int64_t n_groups;
   const int32_t* grp_nchunk; const int64_t* grp_base;
   const double* b_in; double* x_out; int leading; int nop; int mode;
+  const double* dscr; int64_t dstride;   // factored pivot blocks [D | L^T | D^-1] per step
   const int* gate;             // optional: skip the whole solve when *gate == 0
   unsigned long long* trace;   // optional, 6 words per task: start, smid|signalled, prefetched, ready, combined, end
 };
@@ -325,9 +326,14 @@ __device__ bool dag_bwd(const SolveArgs& A, const sgn::Task& T, int b, const int
 // "fat" work items): dag_fwd's 32-row tiles, up to 8 of them, in one CTA, so a bottom-level
 // front is one task (no extra waves, no chunk groups).  Z is held 4 tiles at a time (the
 // first 4 prefetched before the wait); per row tile the sums are dag_fwd's.
+// per-CTA scratch of the fat forward task, reused by the root substitution tasks (only one
+// task runs at a time in a CTA; function-scope __shared__ arrays of the inlined task bodies
+// would be allocated side by side and the solve kernel's smem limits its L1)
+__shared__ double g_fat_red[sgn::kFatRows / 32][8][33];
+
 __device__ bool dag_fwd_fat(const SolveArgs& A, const sgn::Task& T, int b, const int* cnt, int64_t idx) {
   constexpr int RT = 4, NT = sgn::kFatRows / 32, NV = sgn::kFwdCols + sgn::kFatRows;
-  __shared__ double redf[NT][8][33];
+  double (*redf)[8][33] = g_fat_red;
   __shared__ double vsf[NV];
   const DFront F = A.fronts[T.f];
   if (A.nop || (A.leading && F.is_root_p)) { dag_wait(A, T, cnt); return true; }
@@ -496,8 +502,9 @@ __device__ bool dag_bwd_fat(const SolveArgs& A, const sgn::Task& T, int b, const
 }
 
 // ---- no-Z root front (Front::noz): blocked substitution with L11 read from the front -----
-// The factored diagonal blocks sit in the front (D on the diagonal / 2x2 slots, unit L
-// strictly below, factor_dag.cu:factor_publish); L_ji below them.  Row tile j is one task.
+// The factored diagonal blocks come from the factorization's published pivot-block scratch
+// (D on the diagonal / 2x2 slots, unit L strictly below, factor_dag.cu:factor_publish);
+// L_ji below them from the front.  Row tile j is one task.
 // Forward: y_j = L_jj^{-1} (v_j - sum_{i<j} L_ji y_i), z_j = D_j^{-1} y_j, with v_j the
 // right-hand side + children's updates (as dag_fwd) and y kept in the root's x slots; the
 // terms are consumed as the front's forward counter CF(f) says y_i is final.
@@ -506,10 +513,15 @@ __device__ __forceinline__ bool dslot(int pivtype, int r, int c) {   // D's off-
   return pivtype == 2 && (r & 1) && c == r - 1;
 }
 
+static_assert(sgn::kFatRows / 32 >= 5, "root substitution scratch lives in g_fat_red");
+__shared__ int g_root_ready;
+#define g_root_ls (reinterpret_cast<double(*)[33]>(&g_fat_red[0][0][0]))   // 32 x 33
+#define g_root_red (g_fat_red[4])                                           // 8 x 33
+
 __device__ bool dag_root_fwd(const SolveArgs& A, const sgn::Task& T, int b, const int* cnt, int64_t idx) {
-  __shared__ double part[8][33];
-  __shared__ double Ls[32][33];
-  __shared__ int s_ready;
+  double (*part)[33] = g_root_red;
+  double (*Ls)[33] = g_root_ls;
+  int& s_ready = g_root_ready;
   const DFront F = A.fronts[T.f];
   const int j = -T.a - 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -525,10 +537,11 @@ __device__ bool dag_root_fwd(const SolveArgs& A, const sgn::Task& T, int b, cons
     q0 = A.gptr[F.voff + r0 + lane];
     q1 = A.gptr[F.voff + r0 + lane + 1];
   }
-  // the diagonal block (final: the factorization is complete before any solve)
+  // the factored diagonal block, row-major in the step's published scratch [D | L^T | D^-1]
+  const double* dsj = A.dscr + (int64_t)b * A.dstride + F.doff + (int64_t)j * sgn::kDiagStride;
   for (int e = tid; e < 1024; e += kSolveThreads) {
-    const int r = e & 31, c = e >> 5;
-    Ls[r][c] = (r < w && c < w && c <= r) ? Fm[(int64_t)(r0 + c) * ld + r0 + r] : 0.0;
+    const int r = e >> 5, c = e & 31;
+    Ls[r][c] = (r < w && c < w && c <= r) ? dsj[e] : 0.0;
   }
   dag_wait(A, T, cnt);                                  // children's forward done
   const int* cf = cnt + T.sig;                          // CF(f): this front's tiles, in order
@@ -591,9 +604,9 @@ __device__ bool dag_root_fwd(const SolveArgs& A, const sgn::Task& T, int b, cons
 }
 
 __device__ bool dag_root_bwd(const SolveArgs& A, const sgn::Task& T, int b, const int* cnt, int64_t idx) {
-  __shared__ double Ls[32][33];
-  __shared__ double colsum[8][33];
-  __shared__ int s_ready;
+  double (*Ls)[33] = g_root_ls;
+  double (*colsum)[33] = g_root_red;
+  int& s_ready = g_root_ready;
   const DFront F = A.fronts[T.f];
   const int j = -T.a - 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -609,9 +622,10 @@ __device__ bool dag_root_bwd(const SolveArgs& A, const sgn::Task& T, int b, cons
   }
   const double* Fm = A.fstore + (int64_t)b * A.fstride + F.foff;
   const int64_t ld = F.nrow;
+  const double* dsj = A.dscr + (int64_t)b * A.dstride + F.doff + (int64_t)j * sgn::kDiagStride;
   for (int e = tid; e < 1024; e += kSolveThreads) {
-    const int r = e & 31, c = e >> 5;
-    Ls[r][c] = (r < w && c < w && c <= r) ? Fm[(int64_t)(r0 + c) * ld + r0 + r] : 0.0;
+    const int r = e >> 5, c = e & 31;
+    Ls[r][c] = (r < w && c < w && c <= r) ? dsj[e] : 0.0;
   }
   dag_wait(A, T, cnt);                                  // the front's forward done
   const int* cbk = cnt + T.sig;                         // CB(f): tiles P-1, P-2, ... done
@@ -971,6 +985,7 @@ int launch_solve_dag(sgn_factor f, const double* d_b, double* d_x, int32_t flags
   A.fronts = f->fronts.p; A.srows = f->srows.p; A.gptr = f->gptr.p; A.gsrc = f->gsrc.p;
   A.perm = f->perm.p; A.fstore = f->fstore.p; A.fstride = s.front_doubles;
   A.zstore = f->zstore.p; A.zstride = s.z_doubles; A.ubuf = f->ubuf.p; A.ustride = s.u_doubles;
+  A.dscr = f->dscr.p; A.dstride = s.d_doubles;
   A.zbuf = f->zbuf.p; A.xbuf = f->xbuf.p; A.n = s.n;
   A.part = f->part.p; A.pstride = s.part_doubles; A.tickets = f->tickets.p; A.n_groups = s.n_groups;
   A.grp_nchunk = f->grp_nchunk.p; A.grp_base = f->grp_base.p;
@@ -1016,6 +1031,7 @@ int launch_solve_multi(sgn_factor f, const double* d_B, double* d_X, int32_t nrh
   A.fronts = f->fronts.p; A.srows = f->srows.p; A.gptr = f->gptr.p; A.gsrc = f->gsrc.p;
   A.perm = f->perm.p; A.fstore = f->fstore.p; A.fstride = 0;
   A.zstore = f->zstore.p; A.zstride = 0; A.ubuf = f->mubuf.p; A.ustride = s.u_doubles;
+  A.dscr = f->dscr.p; A.dstride = 0;
   A.zbuf = f->mzbuf.p; A.xbuf = f->mxbuf.p; A.n = s.n;
   A.part = f->mpart.p; A.pstride = s.part_doubles; A.tickets = f->mtickets.p; A.n_groups = s.n_groups;
   A.grp_nchunk = f->grp_nchunk.p; A.grp_base = f->grp_base.p;
