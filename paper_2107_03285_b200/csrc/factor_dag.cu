@@ -534,12 +534,20 @@ __global__ void __launch_bounds__(kFThreads, 4)
 k_factor_dag(const sgn::FactorArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
-  __shared__ int s_idx;
+  __shared__ int s_idx, s_base, s_left;
   const int64_t total = A.ntask * A.batch;
   const int tid = threadIdx.x;
+  // batched factorizations take runs of A.run consecutive instances of one task per grab
+  // (one atomic and one look at the task list per run); the run is processed in order, so
+  // the earliest unfinished task is still always running (deadlock freedom unchanged)
+  if (tid == 0) s_left = 0;
   for (;;) {
     __syncthreads();
-    if (tid == 0) s_idx = atomicAdd(A.head, 1);
+    if (tid == 0) {
+      if (s_left == 0) { s_base = atomicAdd(A.head, A.run); s_left = A.run; }
+      s_idx = s_base + (A.run - s_left);
+      --s_left;
+    }
     __syncthreads();
     const int64_t idx = s_idx;
     if (idx >= total) return;
@@ -660,7 +668,7 @@ int launch_factor_dag(const FactorArgs& A, int grid, void* stream) {
   if (total == 0) return SGN_OK;
   cudaError_t e = cudaMemsetAsync(A.head, 0, (size_t)(1 + A.batch * A.n_fcnt) * sizeof(int), st);
   if (e != cudaSuccess) { last_error() = std::string("counter reset: ") + cudaGetErrorString(e); return SGN_CUDA_ERROR; }
-  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid, total));
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid, (total + A.run - 1) / A.run));
   count_launch();
   k_factor_dag<<<g, kFThreads, sizeof(Smem), st>>>(A);
   e = cudaGetLastError();

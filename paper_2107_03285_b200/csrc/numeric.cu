@@ -1244,6 +1244,12 @@ static int factor_numeric_impl(sgn_factor f, const double* d_values, int64_t val
   A.perm = f->perm.p; A.fstore = f->fstore.p; A.fstride = s.front_doubles;
   A.zstore = f->zstore.p; A.zstride = s.z_doubles; A.dscr = f->dscr.p; A.dstride = s.d_doubles;
   A.status = f->status.p;
+  // runs of instances per grab for batched factorizations (SGN_FRUN overrides)
+  A.run = (f->batch >= 8 && f->batch % 4 == 0) ? 4 : 1;
+  if (const char* e = getenv("SGN_FRUN")) {
+    const int r = atoi(e);
+    if (r >= 1 && f->batch % r == 0) A.run = r;
+  }
   A.trace = nullptr;
   { const char* e = getenv("SGN_FDAG_TRACE");
     if (e && *e == '1') {

@@ -183,6 +183,7 @@ struct FactorArgs {
   const int64_t* perm; double* fstore; int64_t fstride; double* zstore; int64_t zstride;
   double* dscr; int64_t dstride; long long* status;
   unsigned long long* trace;   // optional (SGN_FDAG_TRACE=1): 4 words per task
+  int32_t run;                 // instances per grab (divides batch; 1 for a single instance)
 };
 int factor_dag_grid();   // persistent CTAs: SMs x occupancy limit
 int min_pivot(const DFront* d_fronts, int32_t n_fronts, const double* d_fstore, double* out_min,

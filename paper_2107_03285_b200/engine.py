@@ -339,6 +339,8 @@ def _gx_share(eng, full: int) -> int:
     best of 37..222 on config 2 (profiles/scripts/ctas.sh)."""
     if _GX_CTAS > 0:
         return min(_GX_CTAS, full - 1)
+    if eng.batch > 1:      # batched instances are throughput-bound: 1/4 (config 5 sweep, 111..222 CTAs)
+        return max(1, full // 4)
     return max(1, (3 * full) // 16)
 _DEBUG_NAN = os.environ.get("SGN_DEBUG_NAN", "0") == "1"
 _DEBUG_NEWTON = os.environ.get("SGN_DEBUG_NEWTON", "0") == "1"
