@@ -39,6 +39,7 @@ using sgn::kPanelTiles;
 namespace {
 
 constexpr int kSolveThreads = 256;
+constexpr int kWideBatch = 8;      // batches from this size solve with k_solve_dag<4>
 
 // ------------------------------------------------------------------------------------
 // Persistent dependency-driven triangular solve: ONE launch per solve.  Resident CTAs grab
@@ -673,8 +674,16 @@ __device__ bool dag_root_bwd(const SolveArgs& A, const sgn::Task& T, int b, cons
   return true;
 }
 
-__global__ void __launch_bounds__(kSolveThreads, 3)
-k_solve_dag(const SolveArgs A) {
+// One body, two register budgets: 3 CTAs/SM (80 registers) for a single instance, whose
+// solve is a dependency chain; 4 CTAs/SM (64 registers, more spills) for batches, whose
+// solve is bound by the Z traffic in flight (config 5 batched solve 4.1 -> 3.6 ms, while a
+// config-2 solve would go 110 -> 121 us).
+__device__ __forceinline__ void solve_dag_body(const SolveArgs& A);
+
+template <int MINB>
+__global__ void __launch_bounds__(kSolveThreads, MINB) k_solve_dag(const SolveArgs A) { solve_dag_body(A); }
+
+__device__ __forceinline__ void solve_dag_body(const SolveArgs& A) {
   __shared__ int s_idx;
   if (A.gate && *A.gate == 0) return;
   const int64_t total = A.ntask * A.batch;
@@ -953,7 +962,7 @@ struct sgn_factor_s {
   int32_t mcap = 0;
   DevBuf<int64_t> trace;        // SGN_DAG_TRACE=1: 3 words per solve task (diagnostics)
   DevBuf<int> scnt;             // [head | batch x n_scnt counters], zeroed before every solve
-  int solve_grid = 0;
+  int solve_grid = 0, solve_grid4 = 0;
   // BiCGSTAB workspace
   DevBuf<double> bx, br, brh, bp, bv, bs, bt, btmp, bbest, bb, bscr, partial;
   DevBuf<BiState> bst;
@@ -1002,9 +1011,11 @@ int launch_solve_dag(sgn_factor f, const double* d_b, double* d_x, int32_t flags
     } }
   CUDA_TRY(cudaMemsetAsync(f->scnt.p, 0, f->scnt.n * sizeof(int), st));
   const int64_t total = A.ntask * A.batch;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(f->solve_grid, total));
+  const bool wide = A.batch >= kWideBatch;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(wide ? f->solve_grid4 : f->solve_grid, total));
   sgn::count_launch();
-  k_solve_dag<<<grid, kSolveThreads, 0, st>>>(A);
+  if (wide) k_solve_dag<4><<<grid, kSolveThreads, 0, st>>>(A);
+  else k_solve_dag<3><<<grid, kSolveThreads, 0, st>>>(A);
   CUDA_TRY(cudaGetLastError());
   return SGN_OK;
 }
@@ -1038,9 +1049,11 @@ int launch_solve_multi(sgn_factor f, const double* d_B, double* d_X, int32_t nrh
   A.b_in = d_B; A.x_out = d_X; A.leading = 0; A.gate = nullptr; A.nop = 0; A.trace = nullptr; A.mode = 0;
   CUDA_TRY(cudaMemsetAsync(f->mscnt.p, 0, (1 + (size_t)nrhs * std::max<int64_t>(s.n_scnt, 1)) * sizeof(int), st));
   const int64_t total = A.ntask * A.batch;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(f->solve_grid, total));
+  const bool wide = nrhs >= kWideBatch;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(wide ? f->solve_grid4 : f->solve_grid, total));
   sgn::count_launch();
-  k_solve_dag<<<grid, kSolveThreads, 0, st>>>(A);
+  if (wide) k_solve_dag<4><<<grid, kSolveThreads, 0, st>>>(A);
+  else k_solve_dag<3><<<grid, kSolveThreads, 0, st>>>(A);
   CUDA_TRY(cudaGetLastError());
   return SGN_OK;
 }
@@ -1197,8 +1210,10 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
     int dev = 0, sms = 0, per_sm = 0;
     CUDA_TRY(cudaGetDevice(&dev));
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_dag, kSolveThreads, 0));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_dag<3>, kSolveThreads, 0));
     f->solve_grid = std::max(1, sms * std::max(per_sm, 1));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_dag<4>, kSolveThreads, 0));
+    f->solve_grid4 = std::max(1, sms * std::max(per_sm, 1));
     f->factor_grid = sgn::factor_dag_grid();
     if (f->factor_grid <= 0) { sgn::last_error() = "factor occupancy query failed"; return SGN_CUDA_ERROR; }
   }
