@@ -534,26 +534,38 @@ __global__ void __launch_bounds__(kFThreads, 4)
 k_factor_dag(const sgn::FactorArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
-  __shared__ int s_idx, s_base, s_left;
+  __shared__ int s_idx, s_base, s_left, s_sub, s_subend, s_cur;
   const int64_t total = A.ntask * A.batch;
   const int tid = threadIdx.x;
   // batched factorizations take runs of A.run consecutive instances of one task per grab
   // (one atomic and one look at the task list per run); the run is processed in order, so
-  // the earliest unfinished task is still always running (deadlock freedom unchanged)
-  if (tid == 0) s_left = 0;
+  // the earliest unfinished task is still always running (deadlock freedom unchanged).
+  // An F_FAT task (a whole small front) runs its sub-tasks fat[a .. b) back to back under
+  // the same index before the next grab.
+  if (tid == 0) { s_left = 0; s_sub = 0; s_subend = 0; }
   for (;;) {
     __syncthreads();
     if (tid == 0) {
-      if (s_left == 0) { s_base = atomicAdd(A.head, A.run); s_left = A.run; }
-      s_idx = s_base + (A.run - s_left);
-      --s_left;
+      if (s_sub < s_subend) {
+        s_cur = s_sub++;
+      } else {
+        if (s_left == 0) { s_base = atomicAdd(A.head, A.run); s_left = A.run; }
+        s_idx = s_base + (A.run - s_left);
+        --s_left;
+        s_cur = -1;
+      }
     }
     __syncthreads();
     const int64_t idx = s_idx;
     if (idx >= total) return;
     const int64_t tix = idx / A.batch;
     const int b = (int)(idx - tix * A.batch);
-    const sgn::FTask T = A.tasks[tix];
+    sgn::FTask T = (s_cur >= 0) ? A.fat[s_cur] : A.tasks[tix];
+    if ((T.kind_k & 7) == sgn::F_FAT) {
+      __syncthreads();                                        // s_cur read by every thread
+      if (tid == 0) { s_sub = T.a + 1; s_subend = T.b; }
+      T = A.fat[T.a];
+    }
     const int kind = T.kind_k & 7, k = T.kind_k >> 3;
     const DFront F = A.fronts[T.f];
     int* cnt = A.cnt + (int64_t)b * A.n_fcnt;

@@ -949,7 +949,7 @@ struct sgn_factor_s {
   DevBuf<int32_t> grp_nchunk;
   DevBuf<int64_t> grp_base;
   DevBuf<long long> status, status_init;
-  DevBuf<sgn::FTask> ftasks;
+  DevBuf<sgn::FTask> ftasks, fat;
   DevBuf<int64_t> ftrace;       // SGN_FDAG_TRACE=1: 4 words per factor task (diagnostics)
   DevBuf<int> fcnt;             // [head | batch x n_fcnt counters] of the persistent factorization
   int factor_grid = 0;
@@ -1200,7 +1200,7 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
       (rc = f->tickets.alloc(B * std::max<int64_t>(s.n_groups, 1))) ||
       (rc = f->grp_nchunk.upload(s.grp_nchunk)) || (rc = f->grp_base.upload(s.grp_base)) ||
       (rc = f->stasks.upload(s.stasks)) || (rc = f->swaits.upload(s.swaits)) ||
-      (rc = f->ftasks.upload(s.ftasks)) ||
+      (rc = f->ftasks.upload(s.ftasks)) || (rc = f->fat.upload(s.fat)) ||
       (rc = f->fcnt.alloc(1 + B * std::max<int64_t>(s.n_fcnt, 1))) ||
       (rc = f->status_init.upload(std::vector<long long>(B, (long long)INT64_MAX))) ||
       (rc = f->gptr.upload(s.gptr)) || (rc = f->gsrc.upload(s.gsrc)) ||
@@ -1250,7 +1250,7 @@ static int factor_numeric_impl(sgn_factor f, const double* d_values, int64_t val
   CUDA_TRY(cudaMemcpyAsync(f->status.p, f->status_init.p, f->batch * sizeof(long long),
                            cudaMemcpyDeviceToDevice, st));
   sgn::FactorArgs A;
-  A.tasks = f->ftasks.p; A.ntask = (int64_t)s.ftasks.size(); A.batch = f->batch;
+  A.tasks = f->ftasks.p; A.ntask = (int64_t)s.ftasks.size(); A.batch = f->batch; A.fat = f->fat.p;
   A.head = f->fcnt.p; A.cnt = f->fcnt.p + 1; A.n_fcnt = s.n_fcnt;
   A.fronts = f->fronts.p; A.children = f->children.p; A.rel = f->rel.p; A.reltile = f->reltile.p;
   A.tile_ptr = f->tile_ptr.p; A.tile_nnz = f->tile_nnz.p; A.tile_loc = f->tile_loc.p;

@@ -89,7 +89,10 @@ SGN_HD int tile_of_row(int npiv, int r) { return r < npiv ? r / 32 : ptiles(npiv
 //                              ZC(f, cb) > j - cb; pivot tiles signal ZC(f, cb)
 // counters of front f at cbase: DONE, PAN(k), DIAG(k) (k < P), TILE(ti*(ti+1)/2 + tj), ZC(cb),
 // PAN0(k) (k < P)
-enum FKind : int32_t { F_ASM = 0, F_PANEL = 1, F_UPDATE = 2, F_ZPANEL = 3, F_DIAGUPD = 4 };
+//   F_FAT     (f, a, b)      : a whole small front in one CTA: runs fat[a .. b) (its tasks in the
+//                              order above, then its Z blocks) back to back; the sub-tasks signal
+//                              their own counters, so the waits between them pass at once
+enum FKind : int32_t { F_ASM = 0, F_PANEL = 1, F_UPDATE = 2, F_ZPANEL = 3, F_DIAGUPD = 4, F_FAT = 5 };
 struct FTask { int32_t kind_k, f, a, b; };
 constexpr int kDiagStride = 2 * kTile * kTile + 3 * kTile;   // scratch per step: D, L^T, D^-1
 SGN_HD int panel_tasks(int npiv, int nrow, int k) {   // TRSM tasks of step k
@@ -166,6 +169,7 @@ struct Symbolic {
   std::vector<int32_t> gsrc;
   // persistent factorization: tasks in topological order + counters per instance
   std::vector<FTask> ftasks;
+  std::vector<FTask> fat;                      // sub-tasks of the F_FAT fronts
   int64_t n_fcnt = 0;
   // sizes
   int64_t front_doubles = 0, u_doubles = 0, w_doubles = 0, v_doubles = 0, z_doubles = 0, d_doubles = 0;
@@ -175,7 +179,7 @@ struct Symbolic {
 // arguments of the persistent factorization launch (factor_dag.cu); head is followed by
 // batch x n_fcnt dependency counters, all zeroed before every factorization
 struct FactorArgs {
-  const FTask* tasks; int64_t ntask; int32_t batch;
+  const FTask* tasks; int64_t ntask; int32_t batch; const FTask* fat;
   int* head; int* cnt; int64_t n_fcnt;
   const DFront* fronts; const int32_t* children; const int32_t* rel; const int32_t* reltile;
   const int64_t* tile_ptr; const int64_t* tile_nnz; const int32_t* tile_loc; const int8_t* kind_pos;
