@@ -335,13 +335,14 @@ _GX_CTAS = int(os.environ.get("SGN_GX_CTAS", "0"))     # 0: 3/16 of the grid
 def _gx_share(eng, full: int) -> int:
     """CTAs of the concurrent G_x factorization.  The G_x factor is dependency-chain bound
     like the KKT one, so its share is not its flop share (0.11 on config 2, where 74 of 592
-    CTAs made it finish 0.6 ms after the KKT factor): 3/16 of the grid (111 of 592) was the
-    best of 37..222 on config 2 (profiles/scripts/ctas.sh)."""
+    CTAs made it finish 0.6 ms after the KKT factor): 7/32 of the grid (129 of 592) was the
+    best of 92..166 on config 2 after the round-1 factorization changes (3/16 before;
+    profiles/scripts/ctas.sh)."""
     if _GX_CTAS > 0:
         return min(_GX_CTAS, full - 1)
     if eng.batch > 1:      # batched instances are throughput-bound: 1/4 (config 5 sweep, 111..222 CTAs)
         return max(1, full // 4)
-    return max(1, (3 * full) // 16)
+    return max(1, (7 * full) // 32)
 _DEBUG_NAN = os.environ.get("SGN_DEBUG_NAN", "0") == "1"
 _DEBUG_NEWTON = os.environ.get("SGN_DEBUG_NEWTON", "0") == "1"
 
