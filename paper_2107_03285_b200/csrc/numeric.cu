@@ -805,9 +805,10 @@ k_dotF(int mode, const double* __restrict__ a, const double* __restrict__ bvec,
        const double* __restrict__ c, const double* __restrict__ d, double* __restrict__ out,
        int64_t n, double* __restrict__ partial, int* __restrict__ tickets,
        BiState* __restrict__ st, int step, double tol) {
-  __shared__ double s0[kDotThreads], s1[kDotThreads];
+  __shared__ double s0[kDotThreads / 32], s1[kDotThreads / 32];
   __shared__ int last;
   const int b = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t base = (int64_t)b * n;
   double acc0 = 0.0, acc1 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -820,28 +821,45 @@ k_dotF(int mode, const double* __restrict__ a, const double* __restrict__ bvec,
       if (c) acc1 += c[base + i] * d[base + i];
     }
   }
-  s0[threadIdx.x] = acc0;
-  s1[threadIdx.x] = acc1;
-  __syncthreads();
-  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
-    if (threadIdx.x < k) { s0[threadIdx.x] += s0[threadIdx.x + k]; s1[threadIdx.x] += s1[threadIdx.x + k]; }
-    __syncthreads();
+  // fixed shuffle trees (warp, then the 8 warp sums): deterministic, two barriers
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
+    acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
   }
-  if (threadIdx.x == 0) {
-    partial[((int64_t)b * kDotBlocks + blockIdx.x) * 2 + 0] = s0[0];
-    partial[((int64_t)b * kDotBlocks + blockIdx.x) * 2 + 1] = s1[0];
-    int old;
-    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(tickets + b) : "memory");
-    last = (old == (int)gridDim.x - 1);
+  if (lane == 0) { s0[warp] = acc0; s1[warp] = acc1; }
+  __syncthreads();
+  if (warp == 0) {
+    double v0 = lane < kDotThreads / 32 ? s0[lane] : 0.0, v1 = lane < kDotThreads / 32 ? s1[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+      v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    }
+    if (lane == 0) {
+      partial[((int64_t)b * kDotBlocks + blockIdx.x) * 2 + 0] = v0;
+      partial[((int64_t)b * kDotBlocks + blockIdx.x) * 2 + 1] = v1;
+      int old;
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(tickets + b) : "memory");
+      last = (old == (int)gridDim.x - 1);
+    }
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  tickets[b] = 0;
+  if (!last || warp != 0) return;
+  // the last block: warp 0 loads the block partials (all in flight) and sums them in a
+  // fixed shuffle tree, then lane 0 runs the scalar step
   double t0 = 0.0, t1 = 0.0;
-  for (int k = 0; k < (int)gridDim.x; ++k) {
+  for (int k = lane; k < (int)gridDim.x; k += 32) {
     t0 += __ldcg(partial + ((int64_t)b * kDotBlocks + k) * 2 + 0);
     t1 += __ldcg(partial + ((int64_t)b * kDotBlocks + k) * 2 + 1);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+    t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+  }
+  if (lane != 0) return;
+  tickets[b] = 0;
   bicg_scalar(st[b], step, t0, t1, tol);
 }
 
