@@ -40,6 +40,10 @@ namespace {
 
 constexpr int kSolveThreads = 256;
 constexpr int kWideBatch = 8;      // batches from this size solve with k_solve_dag<4>
+// single instances whose solve panels hold this many doubles also solve with k_solve_dag<4>
+// (measured: config 3, 25 M nnz(L): solve 6.77 -> 5.85 ms; config 4: 218 -> 175 ms;
+// config 2, 6 M: 1.65 -> 1.80 ms, so it stays on the 3-CTA/SM chain kernel)
+constexpr int64_t kWideZ = 12000000;
 
 // ------------------------------------------------------------------------------------
 // Persistent dependency-driven triangular solve: ONE launch per solve.  Resident CTAs grab
@@ -981,6 +985,7 @@ struct sgn_factor_s {
   DevBuf<int64_t> trace;        // SGN_DAG_TRACE=1: 3 words per solve task (diagnostics)
   DevBuf<int> scnt;             // [head | batch x n_scnt counters], zeroed before every solve
   int solve_grid = 0, solve_grid4 = 0;
+  bool solve_wide = false;      // 4-CTA/SM solve kernel for a single instance too (large fronts)
   // BiCGSTAB workspace
   DevBuf<double> bx, br, brh, bp, bv, bs, bt, btmp, bbest, bb, bscr, partial;
   DevBuf<BiState> bst;
@@ -1029,7 +1034,7 @@ int launch_solve_dag(sgn_factor f, const double* d_b, double* d_x, int32_t flags
     } }
   CUDA_TRY(cudaMemsetAsync(f->scnt.p, 0, f->scnt.n * sizeof(int), st));
   const int64_t total = A.ntask * A.batch;
-  const bool wide = A.batch >= kWideBatch;
+  const bool wide = A.batch >= kWideBatch || f->solve_wide;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(wide ? f->solve_grid4 : f->solve_grid, total));
   sgn::count_launch();
   if (wide) k_solve_dag<4><<<grid, kSolveThreads, 0, st>>>(A);
@@ -1232,6 +1237,10 @@ int sgn_factor_create(sgn_symbolic h, int32_t batch, sgn_factor* out) {
     f->solve_grid = std::max(1, sms * std::max(per_sm, 1));
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_dag<4>, kSolveThreads, 0));
     f->solve_grid4 = std::max(1, sms * std::max(per_sm, 1));
+    // solves dominated by Z traffic rather than by the dependency chain: many/large fronts
+    // (SGN_SOLVE_WIDE=0/1 overrides)
+    f->solve_wide = s.z_doubles >= kWideZ;
+    if (const char* e = getenv("SGN_SOLVE_WIDE")) f->solve_wide = atoi(e) != 0;
     f->factor_grid = sgn::factor_dag_grid();
     if (f->factor_grid <= 0) { sgn::last_error() = "factor occupancy query failed"; return SGN_CUDA_ERROR; }
   }
