@@ -335,14 +335,21 @@ _GX_CTAS = int(os.environ.get("SGN_GX_CTAS", "0"))     # 0: 3/16 of the grid
 def _gx_share(eng, full: int) -> int:
     """CTAs of the concurrent G_x factorization.  The G_x factor is dependency-chain bound
     like the KKT one, so its share is not its flop share (0.11 on config 2, where 74 of 592
-    CTAs made it finish 0.6 ms after the KKT factor): 7/32 of the grid (129 of 592) was the
-    best of 92..166 on config 2 after the round-1 factorization changes (3/16 before;
-    profiles/scripts/ctas.sh)."""
+    CTAs made it finish 0.6 ms after the KKT factor)."""
     if _GX_CTAS > 0:
         return min(_GX_CTAS, full - 1)
     if eng.batch > 1:      # batched instances are throughput-bound: 1/4 (config 5 sweep, 111..222 CTAs)
         return max(1, full // 4)
-    return max(1, (7 * full) // 32)
+    # single instance: proportional to the G_x factor's share of the flops, 1.85 x
+    # flops(G_x) / flops(KKT), within [1/16, 1/4] of the grid.  Sweeps (SGN_GX_CTAS):
+    # config 2 (ratio 0.119) best at 129 of 592, config 3 (0.066) at 74, config 4 (~0.03)
+    # at 37 (factor 208 -> 174 ms against the fixed 7/32)
+    if not hasattr(eng, "_gx_frac"):
+        fk = float(eng.ksym.stats()["flops"])
+        eng.gfac                                   # builds gsym
+        fg = float(eng.gsym.stats()["flops"])
+        eng._gx_frac = min(0.25, max(1.0 / 16.0, 1.85 * fg / max(fk, 1.0)))
+    return max(1, int(round(eng._gx_frac * full)))
 _DEBUG_NAN = os.environ.get("SGN_DEBUG_NAN", "0") == "1"
 _DEBUG_NEWTON = os.environ.get("SGN_DEBUG_NEWTON", "0") == "1"
 
