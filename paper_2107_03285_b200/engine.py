@@ -329,6 +329,7 @@ def vertex_plan(pl: "MeshPlan"):
 
 
 _SIDE_STREAM = os.environ.get("SGN_SIDE_STREAM", "1") != "0"
+_DIR_GRAPH = os.environ.get("SGN_DIRECTION_GRAPH", "1") != "0"
 _GX_CTAS = int(os.environ.get("SGN_GX_CTAS", "0"))     # 0: 3/16 of the grid
 
 
@@ -367,7 +368,48 @@ def _nan_probe(eng, where):
                   file=sys.stderr, flush=True)
 
 
-def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = True, events=None):
+def _factor_adjoint(eng, st, cur, f0=None, f1=None, events=None):
+    """KKT factor on `cur` || adjoint gradient and the SGN right-hand side on a side stream,
+    joined back into `cur`; no host synchronization (so it can be graph-captured)."""
+    torch = eng.torch
+    n_x, n_p = eng.n_x, eng.n_p
+    if not hasattr(eng, "_side_stream"):
+        eng._side_stream = torch.cuda.Stream()
+    # split the persistent CTA slots (SMs x 4): the G_x factor takes _GX_CTAS of them
+    # and the KKT factor the rest, so both run from the start instead of G_x waiting
+    # for the KKT grid to retire (the G_x factor keeps the full grid elsewhere)
+    full = eng.kfac.set_grid(0)
+    gx = _gx_share(eng, full)
+    eng.gfac.set_grid(gx)
+    eng.kfac.set_grid(full - gx)
+    side = eng._side_stream
+    ev_asm, ev_adj = torch.cuda.Event(), torch.cuda.Event()
+    ev_asm.record(cur)
+    if f0 is not None:
+        f0.record(cur)
+    eng.kfac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda, st)
+    if f1 is not None:
+        f1.record(cur)
+    if events is not None:
+        events[0].record()
+    side.wait_event(ev_asm)
+    with torch.cuda.stream(side):
+        sst = _lib.stream_handle()
+        res_a, it_a = eng.adjoint_direct(check_pivots=False)
+        eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, sst)
+        check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
+                                     ptr(eng.grad), sst))
+        eng.rhs.copy_(eng.tmp)
+        ev_adj.record(side)
+    cur.wait_event(ev_adj)
+    eng.gfac.set_grid(0)
+    if events is not None:
+        events[1].record()
+    return res_a, it_a
+
+
+def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = True, events=None,
+                     pre_done: bool = False):
     """factor -> adjoint gradient -> refined KKT solve on an object exposing
     kfac, kvals, fvec, sol_adj, tmp, rhs, sol, grad, batch, n_x, n_p, stab.
 
@@ -386,37 +428,11 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
         # CTAs retire once its task list is taken, so the G_x launch fills the SMs its
         # dependency-chain tail leaves idle.  Zero-pivot checks of both factors follow the
         # refined solve (still before any convergence error, as in the reference).
-        if not hasattr(eng, "_side_stream"):
-            eng._side_stream = torch.cuda.Stream()
-        # split the persistent CTA slots (SMs x 4): the G_x factor takes _GX_CTAS of them
-        # and the KKT factor the rest, so both run from the start instead of G_x waiting
-        # for the KKT grid to retire (the G_x factor keeps the full grid elsewhere)
-        full = eng.kfac.set_grid(0)
-        gx = _gx_share(eng, full)
-        eng.gfac.set_grid(gx)
-        eng.kfac.set_grid(full - gx)
-        side = eng._side_stream
-        ev_asm, ev_adj = torch.cuda.Event(), torch.cuda.Event()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev_asm.record(cur)
-        f0.record(cur)
-        eng.kfac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda, st)
-        f1.record(cur)
-        if events is not None:
-            events[0].record()
-        side.wait_event(ev_asm)
-        with torch.cuda.stream(side):
-            sst = _lib.stream_handle()
-            res_a, it_a = eng.adjoint_direct(check_pivots=False)
-            eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, sst)
-            check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
-                                         ptr(eng.grad), sst))
-            eng.rhs.copy_(eng.tmp)
-            ev_adj.record(side)
-        cur.wait_event(ev_adj)
-        eng.gfac.set_grid(0)
-        if events is not None:
-            events[1].record()
+        if pre_done:                  # assembly / factor / adjoint already replayed from a graph
+            res_a, it_a = np.zeros(eng.batch), np.zeros(eng.batch, dtype=np.int32)
+        else:
+            res_a, it_a = _factor_adjoint(eng, st, cur, f0, f1, events)
         if timings is not None:
             timings["adjoint_res"] = res_a
             timings["adjoint_iters"] = it_a
@@ -424,14 +440,20 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
             eng.kfac.check(st)
             eng.gfac.check(st)
             return None, None
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(cur)
         rc2, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
+        s1.record(cur)
         if events is not None:
             events[2].record()
         eng.kfac.check(st)
         eng.gfac.check(st)
-        if timings is not None:
-            timings["factor_s"] = f0.elapsed_time(f1) * 1e-3
-            timings["solve_s"] = time.perf_counter() - t1 - timings["factor_s"]
+        if timings is not None:         # device events: no host sync between the phases
+            s1.synchronize()
+            if not pre_done:
+                timings["factor_s"] = f0.elapsed_time(f1) * 1e-3
+            timings["solve_s"] = s0.elapsed_time(s1) * 1e-3
             timings["main_iters"] = its
     else:
         _nan_probe(eng, "before factor")
@@ -649,13 +671,61 @@ class DeviceEngine:
         Returns (rel_res[batch], iters[batch]); raises NoConvergence like
         solve_kkt_stabilized when any instance's refinement stalls.
         """
-        sync = self.torch.cuda.synchronize
-        t0 = time.perf_counter()
-        self.assemble()
-        if timings is not None:
-            sync()
-            timings["assemble_s"] = time.perf_counter() - t0
-        return sgn_solve_stages(self, timings)
+        torch = self.torch
+        graphs = self._direction_graphs()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        if graphs is not None:
+            # assembly, then KKT factor || adjoint + right-hand side: two graph launches
+            # instead of ~30 kernel / memset launches issued from Python
+            graphs[0].replay()
+            e1.record()
+            graphs[1].replay()
+            e2.record()
+        else:
+            self.assemble()
+            e1.record()
+        try:
+            return sgn_solve_stages(self, timings, pre_done=graphs is not None)
+        finally:
+            if timings is not None:       # device events, read after the refinement's sync
+                e1.synchronize()
+                timings["assemble_s"] = e0.elapsed_time(e1) * 1e-3
+                if graphs is not None:
+                    e2.synchronize()
+                    timings["factor_s"] = e1.elapsed_time(e2) * 1e-3
+
+    def _direction_graphs(self):
+        """(assembly graph, factor || adjoint graph), captured once per stabilization shift;
+        None when disabled (SGN_DIRECTION_GRAPH=0), without the side stream, or when the
+        capture fails (the eager path then stays in use)."""
+        if not (_DIR_GRAPH and _SIDE_STREAM and getattr(self, "adjoint_gx", False)):
+            return None
+        key = (float(self.stab.eps_x), float(self.stab.eps_lambda))
+        cached = getattr(self, "_dgraphs", None)
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        if cached is not None and cached[1] is None:          # capture failed before
+            return None
+        torch = self.torch
+        try:
+            # warm-up off the graph: lazily created factors, scratch buffers, kernel attributes
+            self.assemble()
+            _factor_adjoint(self, _lib.stream_handle(), torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g1):
+                self.assemble()
+            with torch.cuda.graph(g2):
+                _factor_adjoint(self, _lib.stream_handle(), torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            self._dgraphs = (key, (g1, g2))
+        except Exception as exc:                              # noqa: BLE001 -- fall back to eager
+            import sys
+            print(f"[sgn] direction graph capture failed, eager path: {exc!r}", file=sys.stderr)
+            torch.cuda.synchronize()
+            self._dgraphs = (key, None)
+        return self._dgraphs[1]
 
     adjoint_gx = True
 
