@@ -147,6 +147,12 @@ def cpu_baseline(config, x, sample, targets=None):
             "median_s": med, "phases_s": phases}
 
 
+WORKLOADS = {1: "config 1: 20x20 neo-Hookean sheet (722 tris), n_p=40",
+             2: "config 2: 100x100 neo-Hookean sheet (19602 tris), n_p=400",
+             3: "config 3: 41x11x11 neo-Hookean tet beam (20000 tets)",
+             4: "config 4: 201x201 discrete shell (80000 StVK triangles + 119600 hinges), n_p=10000"}
+
+
 def run_reference(args):
     """--impl reference: the oracle port of the reference CPU path on all host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -172,7 +178,7 @@ def run_reference(args):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(step_t),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded, oracle/configs.py)",
-           "config": {"workload": f"config {args.config}: 100x100 neo-Hookean sheet, n_p=400, one SGN direction",
+           "config": {"workload": WORKLOADS.get(args.config, f"config {args.config}"),
                       "parallelism": f"{workers} single-threaded host processes"},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
                             "sample": f"each step = {workers} concurrent directions (one per worker)"},
@@ -328,10 +334,8 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded mesh/targets/p0, oracle/configs.py; no dataset)",
-        "config": {"workload": {1: "config 1: 20x20 neo-Hookean sheet", 2: "config 2: 100x100 neo-Hookean sheet (19602 tris)",
-                                3: "config 3: 41x11x11 neo-Hookean tet beam (20000 tets)",
-                                4: "config 4: 201x201 discrete shell (80000 StVK triangles + 119600 hinges)"}[args.config]
-                               + f", n_x={pl.n_x}, n_p={pl.n_p}, KKT dim {pl.dim}, nnz(K) {pl.nnz}",
+        "config": {"workload": WORKLOADS[args.config],
+                   "sizes": f"n_x={pl.n_x}, n_p={pl.n_p}, KKT dim {pl.dim}, nnz(K) {pl.nnz}",
                    "parallelism": "replicas" if world > 1 else "single GPU",
                    "l2": "flushed before every timed step (512 MiB memset outside the events)",
                    "nnz_L": st["nnz_l"], "factor_flops": flops, "fronts": st["n_fronts"],
