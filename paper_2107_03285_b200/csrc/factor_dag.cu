@@ -338,9 +338,10 @@ __device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k
       cv[u] = (r < nr && c < nc && (ti != tj || r >= c)) ? __ldcg(Fm + (int64_t)(lo_j + c) * ld + lo_i + r) : 0.0;
     }
     if (tid == 0) {
-      // the diagonal update reads row tile k+1 only: its TRSM task (t = 0) is enough
-      if (diag) spin_ge(A.cnt + (int64_t)b * A.n_fcnt + F.cbase + sgn::cnt_pan0(F.npiv, F.nrow, k), 1);
-      else spin_ge(A.cnt + (int64_t)b * A.n_fcnt + F.cbase + sgn::cnt_pan(k), sgn::panel_tasks(F.npiv, F.nrow, k));
+      // the TRSM tasks of step k that wrote row tiles ti and tj (the diagonal update: k+1)
+      const int* cfb = A.cnt + (int64_t)b * A.n_fcnt + F.cbase;
+      spin_ge(cfb + sgn::cnt_pant(F.npiv, F.nrow, k, sgn::pan_task_of(k, ti)), 1);
+      if (tj != ti) spin_ge(cfb + sgn::cnt_pant(F.npiv, F.nrow, k, sgn::pan_task_of(k, tj)), 1);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -637,7 +638,7 @@ k_factor_dag(const sgn::FactorArgs A) {
       if (kind == sgn::F_ZPANEL) { s1 = (T.a < P) ? cf + sgn::cnt_zc(P, Tn, T.b) : nullptr; s2 = nullptr; }
       else if (kind == sgn::F_PANEL) {
         s1 = cf + sgn::cnt_pan(k);
-        if (T.a == 0) s3 = cf + sgn::cnt_pan0(F.npiv, F.nrow, k);
+        s3 = cf + sgn::cnt_pant(F.npiv, F.nrow, k, T.a);
       }
       else if (kind == sgn::F_DIAGUPD) { s1 = cf + sgn::cnt_tile(P, k + 1, k + 1); s3 = cf + sgn::cnt_diag(P, k + 1); }
       else {

@@ -88,7 +88,7 @@ SGN_HD int tile_of_row(int npiv, int r) { return r < npiv ? r / 32 : ptiles(npiv
 //                              PAN(f, P-1) (struct tiles), then progressively, per term j,
 //                              ZC(f, cb) > j - cb; pivot tiles signal ZC(f, cb)
 // counters of front f at cbase: DONE, PAN(k), DIAG(k) (k < P), TILE(ti*(ti+1)/2 + tj), ZC(cb),
-// PAN0(k) (k < P)
+// PANT(k, t) (k < P, t < T)
 //   F_FAT     (f, a, b)      : a whole small front in one CTA: runs fat[a .. b) (its tasks in the
 //                              order above, then its Z blocks) back to back; the sub-tasks signal
 //                              their own counters, so the waits between them pass at once
@@ -104,11 +104,16 @@ SGN_HD int cnt_pan(int k) { return 1 + k; }
 SGN_HD int cnt_diag(int P, int k) { return 1 + P + k; }
 SGN_HD int cnt_tile(int P, int ti, int tj) { return 1 + 2 * P + ti * (ti + 1) / 2 + tj; }
 SGN_HD int cnt_zc(int P, int T, int slab) { return 1 + 2 * P + T * (T + 1) / 2 + slab; }
-// PAN0(k): the TRSM task of row tile k+1 (t = 0) of step k -- all the diagonal update reads
-SGN_HD int cnt_pan0(int npiv, int nrow, int k) {
+// PANT(k, t): TRSM task t of step k (t = 0: row tile k+1; t >= 1: row tiles k+2+4(t-1)..).
+// A Schur update of step k waits for the tasks of its two row tiles only (earlier steps of
+// those rows are implied: each TRSM waited for its rows' updates of the previous step).
+SGN_HD int cnt_pant(int npiv, int nrow, int k, int t) {
   const int P = ptiles(npiv), T = ntiles_front(npiv, nrow);
-  return 1 + 2 * P + T * (T + 1) / 2 + (nrow + 31) / 32 + k;
+  return 1 + 2 * P + T * (T + 1) / 2 + (nrow + 31) / 32 + k * T + t;
 }
+SGN_HD int pan_task_of(int k, int tile) { return tile == k + 1 ? 0 : 1 + (tile - k - 2) / 4; }
+// PAN0(k): the TRSM task of row tile k+1 (t = 0) of step k -- all the diagonal update reads
+SGN_HD int cnt_pan0(int npiv, int nrow, int k) { return cnt_pant(npiv, nrow, k, 0); }
 
 struct Work { int32_t f, a, b, c; };   // generic work item
 

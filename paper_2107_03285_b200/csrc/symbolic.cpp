@@ -755,7 +755,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   for (auto& F : s.fronts) {
     const int64_t P = ptiles(F.npiv), T = ntiles_front(F.npiv, F.nrow);
     F.cbase = s.n_fcnt;
-    s.n_fcnt += 1 + 2 * P + T * (T + 1) / 2 + (F.nrow + kTile - 1) / kTile + P;   // ... ZC, PAN0
+    s.n_fcnt += 1 + 2 * P + T * (T + 1) / 2 + (F.nrow + kTile - 1) / kTile + P * T;   // ... ZC, PANT
     if (T >= (1 << 16)) { last_error() = "front too large for the task schedule"; return 5; }
     F.ftotal = 0;                                         // counted as the tasks are emitted
   }
