@@ -599,6 +599,16 @@ class DeviceEngine:
             self.p.copy_(self._pin_p, non_blocking=True)
         self._pin_ev.record()
 
+    def solution_host(self, b: int = 0) -> np.ndarray:
+        """Instance b's KKT solution on the host: device -> pinned buffer (asynchronous copy,
+        one stream sync) -> a fresh numpy array the caller owns."""
+        torch = self.torch
+        if not hasattr(self, "_pin_sol"):
+            self._pin_sol = torch.empty(tuple(self.sol.shape[1:]), dtype=torch.float64, pin_memory=True)
+        self._pin_sol.copy_(self.sol[b], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self._pin_sol.numpy().copy()
+
     def positions(self, x=None):
         pl = self.plan
         x = self.x if x is None else x

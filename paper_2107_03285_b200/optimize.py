@@ -124,7 +124,7 @@ def direction_sgn(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirectio
         prob._load(x, p)
         t = {}
         res, its = eng.direction(t)
-        sol = eng.sol[0].cpu().numpy()
+        sol = eng.solution_host(0)
     else:
         t0 = time.perf_counter()
         hk, _ = _host_kkt(prob, x, p)
