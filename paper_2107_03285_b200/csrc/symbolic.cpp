@@ -793,7 +793,8 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   // with at least kZInlineSteps pivot steps (the dependency-chain-bound upper fronts) get
   // their pivot-tile blocks right after pivot step t, so the panel is built while the
   // front is still being factored; all other blocks go to a queue (bottom levels first).
-  constexpr int32_t kZInlineSteps = 8;
+  int32_t kZInlineSteps = 8;
+  if (const char* e = std::getenv("SGN_ZINLINE")) kZInlineSteps = std::max(1, std::atoi(e));
   std::vector<FTask> zq;
   std::vector<int32_t> zq_level;
   auto z_inline = [&](const Front& F) { return ptiles(F.npiv) >= kZInlineSteps; };
