@@ -53,7 +53,7 @@ typedef struct {
     int64_t max_piv;       /* largest pivot block of a front              */
     int64_t launches;      /* kernel launches of one numeric factorization */
     double  flops;         /* LDL^T flops of one numeric factorization    */
-    int64_t pair_mode;     /* 1 = (x_i, lambda_pi(i)) 2x2 pivots + p-root  */
+    int64_t pair_mode;     /* 1 = (x_i, lambda_pi(i)) 2x2 pivots; 2 = also p pairs in the dissection */
 } sgn_symbolic_stats;
 
 /* ---- library ------------------------------------------------------------------- */
@@ -74,6 +74,32 @@ int sgn_device_sync(void* stream);
 int sgn_symbolic_create(int64_t n, const int64_t* indptr, const int64_t* indices,
                         int64_t n_x, int64_t n_p, int64_t n_c, int32_t leaf_size,
                         sgn_symbolic* out, int64_t* pivot_index);
+
+/* Options of the symbolic analysis and of the task schedules it builds (all former
+ * SGN_* environment knobs).  sgn_symbolic_options_default() fills the defaults; a zero
+ * field of a default-filled struct is meaningful (e.g. noz_tiles = 0: off).            */
+typedef struct {
+    int32_t leaf_size;     /* max unknowns in a leaf front (default 64)                      */
+    int32_t p_order;       /* KKT mode: 0 = p unknowns eliminated last in one dense root
+                              front (needed when C = d2f/dp2 may be singular); 1 = p unknowns
+                              join the nested dissection as consecutive 2x2 pairs (the caller
+                              asserts C > 0: the stabilized KKT is then quasi-definite, and a
+                              p pair's Schur block stays positive definite); an odd last p is
+                              eliminated last on its own.  (default 0)                        */
+    int32_t upd_group;     /* pivot steps per grouped Schur-update task (default 8)          */
+    int32_t zinline;       /* fronts with >= zinline pivot tiles build Z inline (default 8)  */
+    int32_t zquota;        /* queued Z blocks interleaved per pivot step (default 256)       */
+    int32_t noz_tiles;     /* root p-front of >= noz_tiles tiles gets no Z (default 0: off)  */
+    int32_t fat_tiles;     /* fronts of <= fat_tiles tiles factor as one task (default 0)    */
+    int32_t fat_solve;     /* small fronts solve as one task (default 1)                     */
+    int32_t generic_pairs; /* generic mode: 2x2 pivots on consecutive unknowns (default 1)   */
+    int32_t reserved[7];
+} sgn_symbolic_options;
+void sgn_symbolic_options_default(sgn_symbolic_options* o);
+/* as sgn_symbolic_create, with options (NULL = defaults) */
+int sgn_symbolic_create_ex(int64_t n, const int64_t* indptr, const int64_t* indices,
+                           int64_t n_x, int64_t n_p, int64_t n_c, const sgn_symbolic_options* opts,
+                           sgn_symbolic* out, int64_t* pivot_index);
 int  sgn_symbolic_get_stats(sgn_symbolic s, sgn_symbolic_stats* out);
 /* perm[k] = original unknown eliminated at position k */
 int  sgn_symbolic_get_perm(sgn_symbolic s, int64_t* perm);
@@ -243,22 +269,24 @@ int  sgn_axpy(int64_t n, int32_t batch, const double* d_alpha, const double* d_x
  * batched Newton / line search, forward.py:197-201, optimize.py:485-486)               */
 int  sgn_masked_copy(int64_t n, int32_t batch, const int32_t* d_mask, const double* d_src,
                      double* d_dst, int64_t stride, void* stream);
-/* least-squares terms: d_vec (KKT order, dim = 2 n_x + n_p per instance) receives
- * (df/dx, df/dp, 0) for r = (x[tdofs] - tvals, p) with weights (w_t, w_reg);
- * d_fobj[b] = 0.5 sum w r^2 (sensitivity.py:83-93).  Either output may be NULL.      */
-int  sgn_lsq_terms(int32_t batch, int64_t n_x, int64_t n_p, int64_t nt, const int64_t* d_tdofs,
-                   const double* d_tvals, int64_t tstride, double w_t, double w_reg,
-                   const double* d_x, const double* d_p, double* d_vec, double* d_fobj,
-                   void* stream);
-/* as sgn_lsq_terms with residuals r = x[tdofs] - tvals - R p (config 4: vertical displacement
- * relative to the p-dependent rest shape): R as CSR over targets (d_rptr/d_ridx/d_rcoef),
- * R^T as CSR over parameters, d_rscr scratch [batch x nt]; f_p = -R^T w r + w_reg p.     */
-int  sgn_lsq_terms_r(int32_t batch, int64_t n_x, int64_t n_p, int64_t nt, const int64_t* d_tdofs,
-                     const double* d_tvals, int64_t tstride, double w_t, double w_reg,
-                     const double* d_x, const double* d_p, double* d_vec, double* d_fobj,
-                     const int64_t* d_rptr, const int64_t* d_ridx, const double* d_rcoef,
-                     const int64_t* d_rtptr, const int64_t* d_rtidx, const double* d_rtcoef,
-                     double* d_rscr, void* stream);
+/* least-squares terms (sensitivity.py:83-93): d_vec (KKT order, dim = 2 n_x + n_p per
+ * instance) receives (df/dx, df/dp, 0) for r = (sigma x[tdofs] - tvals - R p, p) with weights
+ * (w_t, w_reg): f_x = sigma w_t r at the targets, f_p = -R^T w_t r + w_reg p; d_fobj[b] =
+ * 0.5 sum w r^2.  Either output may be NULL.  sigma = x_scale (1 for a position state; the
+ * shell's displacement state).  R (optional) is the CSR over targets
+ * (rptr/ridx/rcoef) with its transpose over parameters (rtptr/...) and needs rscr
+ * [batch x n_t].  part [batch x 128 doubles] and tickets [batch ints, zeroed once] are the
+ * caller's scratch (one set per concurrently used engine; the tickets reset themselves).  */
+typedef struct {
+    int64_t n_x, n_p, n_t;
+    const int64_t* tdofs; const double* tvals; int64_t tstride;
+    double w_t, w_reg, x_scale;
+    const int64_t* rptr; const int64_t* ridx; const double* rcoef;
+    const int64_t* rtptr; const int64_t* rtidx; const double* rtcoef;
+    double* rscr; double* part; int32_t* tickets;
+} sgn_lsq_args;
+int  sgn_lsq_eval(int32_t batch, const sgn_lsq_args* args, const double* d_x, const double* d_p,
+                  double* d_vec, double* d_fobj, void* stream);
 /* adjoint gradient from a leading-block KKT solve (sensitivity.py:181-198, 245-256):
  * mode 0: d_out = (0, 0, d_src[lambda]);  mode 1: g = d_fvec[p] - d_src[p] (d_src = K v),
  * d_out = (0, -g, 0), d_grad = g;  mode 2: d_out = (0, 0, w) for an n_x-vector w = d_src;

@@ -232,11 +232,18 @@ def shell_spec(n: int = 201, nc: int = 100, L: float = 1.0, t: float = 0.05, E: 
                 name=f"shell_{n}x{n}_c{nc}")
 
 
-class ShellProblem:
-    """Oracle shell problem (membrane + hinge groups; residual r = x_z - X_z(p)).
+SHELL_DISP_SCALE = 1e-3      # state = displacement from X(p) in millimetres (as the product)
 
-    Contract = reference sensitivity.py:29-120; equilibrium rows scaled by the inverse
-    geometric mean of the membrane and lowest bending stiffness."""
+
+class ShellProblem:
+    """Oracle shell problem (membrane + hinge groups).
+
+    Contract = reference sensitivity.py:29-120.  State x = displacement of the free dofs from
+    the p-dependent rest shape, in millimetres: pos = X(p) + sigma x (sigma = 1e-3; fixed
+    corners stay at X0).  Residual r = sigma x_z (the vertical displacement in metres) and
+    p (regularizer); constraints c = s dE/dpos on the free dofs, with s the inverse geometric
+    mean of the membrane and lowest bending stiffness; dc/dx = s sigma H_ff and dc/dp =
+    s (H_f,free P_free + M P) (M = d2E/dpos dX).  DESIGN.md section 6 says why this state."""
 
     def __init__(self, spec, tol=None):
         self.s = spec
@@ -252,11 +259,9 @@ class ShellProblem:
         self.dof_to_x[self.free_dofs] = np.arange(self.n_x)
         pm_dof, pm_p, pm_coef = spec["pmap"]
         self.P = sp.csr_matrix((pm_coef, (pm_dof, pm_p)), shape=(self.n_v * 3, self.n_p))
+        self.Pf = sp.csr_matrix(self.P[self.free_dofs])          # free rest dofs <- p
         self.tdofs = spec["target_dofs"]
-        # residual p-map R: r = x[tdofs] - X(p)[free dof of tdofs]
-        self.R = sp.csr_matrix(self.P[self.free_dofs][self.tdofs])
-        # equilibrium rows scaled by the inverse geometric mean of the membrane and lowest
-        # bending stiffness (as paper_2107_03285_b200.problems.shell_scale, which says why)
+        self.sigma = SHELL_DISP_SCALE
         n = int(round(np.sqrt(self.n_v)))
         h = 1.0 / (n - 1)
         D = spec["E"] * spec["t"] ** 3 / (12.0 * (1.0 - spec["nu"] ** 2))
@@ -275,9 +280,9 @@ class ShellProblem:
     def rest_positions(self, p):
         return (self.X0.ravel() + self.P @ np.asarray(p, dtype=np.float64)).reshape(-1, 3)
 
-    def full_positions(self, x):
+    def full_positions(self, x, p):
         pos = self.X0.ravel().copy()
-        pos[self.free_dofs] = x
+        pos[self.free_dofs] = self.rest_positions(p).ravel()[self.free_dofs] + self.sigma * np.asarray(x)
         return pos.reshape(-1, 3)
 
     def _energy_args(self, kind):
@@ -320,28 +325,31 @@ class ShellProblem:
         return out
 
     def simulate(self, p, x_init=None):
+        """Static equilibrium in the displacement state (forward.py:135-168 with the energy
+        s E(X(p) + sigma x): gradient sigma c, Hessian sigma dc/dx; the stopping test on c is
+        the problem's tolerance, as on the device)."""
         rest = self.rest_positions(p)
-        s = self.scale
+        s, sg = self.scale, self.sigma
 
         def energy(xf):
-            return s * self._energy_full(self.full_positions(xf), rest)
+            return s * self._energy_full(self.full_positions(xf, p), rest)
 
         def gradient(xf):
-            return s * self._grad_full(self.full_positions(xf), rest)[self.free_dofs]
+            return sg * s * self._grad_full(self.full_positions(xf, p), rest)[self.free_dofs]
 
         def hessian(xf):
-            return s * self.constraint_jac_x_raw(self.full_positions(xf), rest)
+            return sg * sg * s * self._hess_ff(self.full_positions(xf, p), rest)
 
         start = x_init if x_init is not None else (self._x_warm if self._x_warm is not None
-                                                   else self.X0.ravel()[self.free_dofs])
-        x = solve_static(energy, gradient, hessian, np.asarray(start, dtype=np.float64), self.tol)
+                                                   else np.zeros(self.n_x))
+        x = solve_static(energy, gradient, hessian, np.asarray(start, dtype=np.float64), sg * self.tol)
         self._x_warm = x.copy()
         return x
 
     def constraints(self, x, p):
-        return self.scale * self._grad_full(self.full_positions(x), self.rest_positions(p))[self.free_dofs]
+        return self.scale * self._grad_full(self.full_positions(x, p), self.rest_positions(p))[self.free_dofs]
 
-    def constraint_jac_x_raw(self, pos, rest):
+    def _hess_ff(self, pos, rest):
         rows, cols, vals = [], [], []
         for dofs, H, _ in self._blocks(pos, rest):
             nd = dofs.shape[1]
@@ -354,34 +362,40 @@ class ShellProblem:
                               (self.n_x, self.n_x)).to_scipy()
 
     def constraint_jac_x(self, x, p):
-        return Csc(self.scale * self.constraint_jac_x_raw(self.full_positions(x), self.rest_positions(p)))
+        return Csc(self.scale * self.sigma * self._hess_ff(self.full_positions(x, p), self.rest_positions(p)))
 
     def constraint_jac_p(self, x, p):
+        """s (H_f,free P_free + M P): element by element, one COO build (no SpGEMM, so the
+        pattern is structural)."""
         rows, cols, vals = [], [], []
-        Pc = self.P
-        for dofs, _, M in self._blocks(self.full_positions(x), self.rest_positions(p)):
+        Pc, Pf_ = self.P, self.Pf
+        for dofs, H, M in self._blocks(self.full_positions(x, p), self.rest_positions(p)):
             ne, nd = dofs.shape
-            for bb in range(nd):
-                rx = self.dof_to_x[dofs[:, bb]]
-                for cc in range(nd):
-                    cd = dofs[:, cc]
-                    st, en = Pc.indptr[cd], Pc.indptr[cd + 1]
-                    cnt = (en - st) * (rx >= 0)
-                    if not cnt.any():
-                        continue
-                    sel = np.flatnonzero(cnt)
-                    rep = cnt[sel]
-                    e_idx = np.repeat(sel, rep)
-                    offs = np.arange(rep.sum()) - np.repeat(np.cumsum(rep) - rep, rep)
-                    kk = st[e_idx] + offs
-                    rows.append(rx[e_idx]); cols.append(Pc.indices[kk]); vals.append(M[e_idx, bb, cc] * Pc.data[kk])
+            # element-local (row a, col b) pairs with a free row; each col dof b expands over
+            # its p-map entries: coefficient * (M[a, b] + H[a, b] if b is a free dof)
+            a_loc = np.repeat(np.arange(nd), nd)
+            b_loc = np.tile(np.arange(nd), nd)
+            rdof = dofs[:, a_loc].ravel()
+            cdof = dofs[:, b_loc].ravel()
+            e_id = np.repeat(np.arange(ne), nd * nd)
+            rx = self.dof_to_x[rdof]
+            cnt = (Pc.indptr[cdof + 1] - Pc.indptr[cdof]) * (rx >= 0)
+            sel = np.flatnonzero(cnt)
+            rep_ = cnt[sel]
+            t = np.repeat(sel, rep_)
+            offs = np.arange(rep_.sum()) - np.repeat(np.cumsum(rep_) - rep_, rep_)
+            kk = Pc.indptr[cdof[t]] + offs
+            loc = (a_loc * nd + b_loc)[t % (nd * nd)]
+            m = M.reshape(ne, -1)[e_id[t], loc]
+            hv = H.reshape(ne, -1)[e_id[t], loc] * (self.dof_to_x[cdof[t]] >= 0)
+            rows.append(rx[t]); cols.append(Pc.indices[kk]); vals.append(Pc.data[kk] * (m + hv))
         return csc_structural(np.concatenate(rows), np.concatenate(cols), self.scale * np.concatenate(vals),
                               (self.n_x, self.n_p))
 
-    # least squares: r = [x_t - X_t(p) - target ; p]
+    # least squares: r = [sigma x_t - target ; p]
     def residuals(self, x, p):
         p = np.asarray(p, dtype=np.float64)
-        r = np.asarray(x)[self.tdofs] - self.R @ p - self.s["target_vals"]
+        r = self.sigma * np.asarray(x)[self.tdofs] - self.s["target_vals"]
         return np.concatenate([r, p]) if self.s["w_reg"] > 0 else r
 
     def weights(self):
@@ -392,13 +406,13 @@ class ShellProblem:
 
     def residual_jac_x(self, x, p):
         nt = self.tdofs.size
-        J = sp.csc_matrix((np.ones(nt), (np.arange(nt), self.tdofs)), shape=(nt, self.n_x))
+        J = sp.csc_matrix((np.full(nt, self.sigma), (np.arange(nt), self.tdofs)), shape=(nt, self.n_x))
         if self.s["w_reg"] > 0:
             J = sp.vstack([J, sp.csc_matrix((self.n_p, self.n_x))], format="csc")
         return Csc(J)
 
     def residual_jac_p(self, x, p):
-        J = -self.R
+        J = sp.csc_matrix((self.tdofs.size, self.n_p))
         if self.s["w_reg"] > 0:
             J = sp.vstack([J, sp.identity(self.n_p)], format="csc")
         return Csc(J)

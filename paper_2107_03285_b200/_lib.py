@@ -29,6 +29,21 @@ class SymbolicStats(ctypes.Structure):
                 ("launches", c_i64), ("flops", c_dbl), ("pair_mode", c_i64)]
 
 
+class SymbolicOptions(ctypes.Structure):
+    """sgn_symbolic_options (include/sgn_b200.h)."""
+    _fields_ = [("leaf_size", c_i32), ("p_order", c_i32), ("upd_group", c_i32), ("zinline", c_i32),
+                ("zquota", c_i32), ("noz_tiles", c_i32), ("fat_tiles", c_i32), ("fat_solve", c_i32),
+                ("generic_pairs", c_i32), ("reserved", c_i32 * 7)]
+
+
+class LsqArgs(ctypes.Structure):
+    """sgn_lsq_args (include/sgn_b200.h)."""
+    _fields_ = [("n_x", c_i64), ("n_p", c_i64), ("n_t", c_i64), ("tdofs", c_vp), ("tvals", c_vp),
+                ("tstride", c_i64), ("w_t", c_dbl), ("w_reg", c_dbl), ("x_scale", c_dbl),
+                ("rptr", c_vp), ("ridx", c_vp), ("rcoef", c_vp), ("rtptr", c_vp), ("rtidx", c_vp),
+                ("rtcoef", c_vp), ("rscr", c_vp), ("part", c_vp), ("tickets", c_vp)]
+
+
 # name -> (restype, argtypes); every symbol include/sgn_b200.h declares
 SIGNATURES = {
     "sgn_last_error": (ctypes.c_char_p, []),
@@ -37,6 +52,9 @@ SIGNATURES = {
     "sgn_device_sync": (ctypes.c_int, [c_vp]),
     "sgn_symbolic_create": (ctypes.c_int, [c_i64, P_i64, P_i64, c_i64, c_i64, c_i64, c_i32,
                                            ctypes.POINTER(c_vp), P_i64]),
+    "sgn_symbolic_options_default": (None, [ctypes.POINTER(SymbolicOptions)]),
+    "sgn_symbolic_create_ex": (ctypes.c_int, [c_i64, P_i64, P_i64, c_i64, c_i64, c_i64,
+                                              ctypes.POINTER(SymbolicOptions), ctypes.POINTER(c_vp), P_i64]),
     "sgn_symbolic_get_stats": (ctypes.c_int, [c_vp, ctypes.POINTER(SymbolicStats)]),
     "sgn_symbolic_get_perm": (ctypes.c_int, [c_vp, P_i64]),
     "sgn_symbolic_get_fronts": (ctypes.c_int, [c_vp, P_i64, P_i64, P_i64, P_i64, P_i64, P_i64]),
@@ -79,12 +97,8 @@ SIGNATURES = {
                                      c_vp]),
     "sgn_reduce": (ctypes.c_int, [c_i32, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "sgn_axpy": (ctypes.c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
-    "sgn_lsq_terms": (ctypes.c_int, [c_i32, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_dbl, c_dbl,
-                                     c_vp, c_vp, c_vp, c_vp, c_vp]),
     "sgn_fp64_peak": (ctypes.c_int, [c_i32, c_i32, P_dbl, c_vp]),
-    "sgn_lsq_terms_r": (ctypes.c_int, [c_i32, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_dbl, c_dbl,
-                                       c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                       c_vp, c_vp]),
+    "sgn_lsq_eval": (ctypes.c_int, [c_i32, ctypes.c_void_p, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "sgn_adjoint_step": (ctypes.c_int, [c_i32, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 

@@ -1118,10 +1118,35 @@ int sgn_device_sync(void* stream) {
   return SGN_OK;
 }
 
+void sgn_symbolic_options_default(sgn_symbolic_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  const sgn::SymOptions d;
+  o->leaf_size = d.leaf_size; o->p_order = d.p_order; o->upd_group = d.upd_group;
+  o->zinline = d.zinline; o->zquota = d.zquota; o->noz_tiles = d.noz_tiles;
+  o->fat_tiles = d.fat_tiles; o->fat_solve = d.fat_solve; o->generic_pairs = d.generic_pairs;
+}
+
 int sgn_symbolic_create(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t n_x,
                         int64_t n_p, int64_t n_c, int32_t leaf_size, sgn_symbolic* out,
                         int64_t* pivot_index) {
+  sgn_symbolic_options o;
+  sgn_symbolic_options_default(&o);
+  if (leaf_size > 0) o.leaf_size = leaf_size;
+  return sgn_symbolic_create_ex(n, indptr, indices, n_x, n_p, n_c, &o, out, pivot_index);
+}
+
+int sgn_symbolic_create_ex(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t n_x,
+                           int64_t n_p, int64_t n_c, const sgn_symbolic_options* opts,
+                           sgn_symbolic* out, int64_t* pivot_index) {
   try {
+    sgn::SymOptions so;
+    if (opts) {
+      so.leaf_size = opts->leaf_size; so.p_order = opts->p_order; so.upd_group = opts->upd_group;
+      so.zinline = opts->zinline; so.zquota = opts->zquota; so.noz_tiles = opts->noz_tiles;
+      so.fat_tiles = opts->fat_tiles; so.fat_solve = opts->fat_solve;
+      so.generic_pairs = opts->generic_pairs;
+    }
     if (!out || !indptr || n < 0) { sgn::last_error() = "bad arguments"; return SGN_INVALID; }
     auto h = std::make_unique<sgn_symbolic_s>();
     h->s.n = n; h->s.n_x = n_x; h->s.n_p = n_p; h->s.n_c = n_c;
@@ -1129,7 +1154,7 @@ int sgn_symbolic_create(int64_t n, const int64_t* indptr, const int64_t* indices
     const int64_t nnz = h->s.indptr[n];
     h->s.indices.assign(indices, indices + nnz);
     int64_t piv = -1;
-    int rc = sgn::build_symbolic(h->s, leaf_size, &piv);
+    int rc = sgn::build_symbolic(h->s, so, &piv);
     if (pivot_index) *pivot_index = piv;
     if (rc) return rc;
     *out = h.release();
@@ -1151,7 +1176,7 @@ int sgn_symbolic_get_stats(sgn_symbolic h, sgn_symbolic_stats* o) {
   o->max_piv = s.max_piv;
   o->launches = (int64_t)s.launches.size();
   o->flops = s.flops;
-  o->pair_mode = s.pair_mode ? 1 : 0;
+  o->pair_mode = s.pair_mode ? 1 + s.p_order : 0;
   return SGN_OK;
 }
 
@@ -1421,7 +1446,16 @@ int sgn_factor_solve_multi(sgn_factor f, const double* d_B, double* d_X, int32_t
   return launch_solve_multi(f, d_B, d_X, nrhs, (cudaStream_t)stream);
 }
 
+static int leading_ok(sgn_factor f, int32_t flags) {
+  if ((flags & SGN_SOLVE_LEADING) && f->sym->s.p_order) {
+    sgn::last_error() = "SGN_SOLVE_LEADING needs p unknowns eliminated last (p_order 0)";
+    return SGN_INVALID;
+  }
+  return SGN_OK;
+}
+
 int sgn_factor_solve(sgn_factor f, const double* d_b, double* d_x, int32_t flags, void* stream) {
+  if (int rc = leading_ok(f, flags)) return rc;
   return launch_solve(f, d_b, d_x, flags, (cudaStream_t)stream);
 }
 
@@ -1551,6 +1585,7 @@ static bool bicg_use_graph() {
 int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_stride,
                       const double* d_rhs, double* d_sol, double tol, int32_t max_iters,
                       int32_t flags, double* rel_res, int32_t* iters, void* stream) {
+  if (int rc = leading_ok(f, flags)) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = f->n;
   const int B = f->batch;

@@ -135,9 +135,23 @@ enum TaskKind : int32_t { T_FWD = 1, T_BWD = 2, T_FWD_FAT = 3, T_BWD_FAT = 4, T_
 struct Task { int32_t kind, f, a, b, c, sig, w0, w1; };
 struct Launch { int32_t kind; int32_t level; int64_t off; int64_t count; int32_t pivtype = 1; int32_t pad = 0; };
 
+// Options of the symbolic analysis and its schedules (mirror of sgn_symbolic_options).
+struct SymOptions {
+  int32_t leaf_size = 64;     // max unknowns in a leaf front
+  int32_t p_order = 0;        // 0: p unknowns last (dense root front); 1: p pairs in the dissection
+  int32_t upd_group = 8;      // pivot steps per grouped Schur-update task
+  int32_t zinline = 8;        // fronts with >= zinline pivot tiles build Z inline
+  int32_t zquota = 256;       // queued Z blocks interleaved per pivot step
+  int32_t noz_tiles = 0;      // root p-front of >= noz_tiles tiles gets no Z (0: off)
+  int32_t fat_tiles = 0;      // fronts of <= fat_tiles tiles factor as one task (0: off)
+  int32_t fat_solve = 1;      // small fronts solve as one task
+  int32_t generic_pairs = 1;  // generic mode: 2x2 pivots on consecutive unknowns
+};
+
 struct Symbolic {
   int64_t n = 0, n_x = 0, n_p = 0, n_c = 0;
   bool pair_mode = false;
+  int32_t p_order = 0;                         // SymOptions::p_order in effect
   std::vector<int64_t> indptr, indices;       // input full CSC pattern
   std::vector<int64_t> perm, ipos;             // perm[pos] = unknown; ipos[unknown] = pos
   std::vector<Front> fronts;                   // postorder (children before parents)
@@ -210,6 +224,6 @@ int launch_shell(bool derivs, int32_t elem_type, int64_t n_elems, int32_t batch,
                  int64_t pstride, double* out1, double* out2, int64_t bstride, void* stream);
 
 // returns 0 ok, 1 singular (pivot_index set), 5 invalid
-int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index);
+int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index);
 
 }  // namespace sgn

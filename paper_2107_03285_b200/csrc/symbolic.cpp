@@ -295,7 +295,7 @@ class Dissector {
 
 }  // namespace
 
-int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
+int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
   const int64_t n = s.n;
   *pivot_index = -1;
   if ((int64_t)s.indptr.size() != n + 1) { last_error() = "indptr size != n+1"; return 5; }
@@ -325,18 +325,21 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
         }
       }
   }
-  if (leaf_size <= 0) {
-    leaf_size = 64;
-    if (const char* e = std::getenv("SGN_LEAF_SIZE")) leaf_size = std::max<int64_t>(4, std::atoll(e));
-  }
+  const int64_t leaf_size = opt.leaf_size > 0 ? std::max<int64_t>(4, opt.leaf_size) : 64;
   s.pair_mode = (s.n_x > 0);
+  s.p_order = (s.pair_mode && opt.p_order == 1) ? 1 : 0;
   if (s.pair_mode && (s.n_c != s.n_x || 2 * s.n_x + s.n_p != n)) {
     last_error() = "KKT mode needs n_c == n_x and n == 2*n_x + n_p";
     return 3;
   }
 
   // ---- nodes ----------------------------------------------------------------
-  // node_unk: unknowns of each graph node; p unknowns are not graph nodes in KKT mode
+  // node_unk: unknowns of each graph node.  p unknowns are not graph nodes in KKT mode
+  // with p_order 0 (all eliminated last, in the root front); with p_order 1 the pairs
+  // (p_2k, p_2k+1) are nodes of weight 2 (2x2 pivots: the p block's Schur complement is
+  // positive definite when C > 0), and an odd last p alone is eliminated last.
+  const int64_t n_p_nodes = s.p_order ? s.n_p / 2 : 0;
+  const int64_t n_root_p = s.pair_mode ? s.n_p - 2 * n_p_nodes : 0;
   std::vector<int64_t> node_of(n, -1);
   std::vector<std::array<int64_t, 2>> node_unk;
   std::vector<int32_t> node_w;
@@ -356,6 +359,12 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
       node_of[l] = i;
     }
     node_w.assign(s.n_x, 2);
+    for (int64_t k = 0; k < n_p_nodes; ++k) {
+      const int64_t a = s.n_x + 2 * k;
+      node_of[a] = node_of[a + 1] = (int64_t)node_unk.size();
+      node_unk.push_back({a, a + 1});
+      node_w.push_back(2);
+    }
   } else {
     node_unk.resize(n);
     for (int64_t i = 0; i < n; ++i) { node_unk[i] = {i, -1}; node_of[i] = i; }
@@ -481,7 +490,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
     nd = d.run();
   }
   int32_t proot = -1;
-  if (s.pair_mode && s.n_p > 0) {
+  if (s.pair_mode && n_root_p > 0) {
     NdFront pf;
     pf.parent = -1;
     nd.push_back(pf);
@@ -525,8 +534,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   s.fronts.assign(NF, Front());
   s.front_of_pos.assign(n, -1);
   int64_t pos = 0;
-  bool generic_pairs = true;
-  if (const char* e = std::getenv("SGN_GENERIC_PAIRS")) generic_pairs = std::atoi(e) != 0;
+  const bool generic_pairs = opt.generic_pairs != 0;
   for (int32_t k = 0; k < NF; ++k) {
     const NdFront& src = nd[post[k]];
     Front& F = s.fronts[k];
@@ -537,14 +545,19 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
       // the p block's Schur complement is the (regularized) reduced Gauss-Newton Hessian:
       // 2x2 pivots on consecutive p unknowns halve the serial pivot chain of the root's
       // diagonal blocks (an even count keeps every pair inside one 32-column tile)
-      F.pivtype = (s.pair_mode && s.n_p % 2 == 0) ? 2 : 1;
-      for (int64_t u = s.n_x; u < s.n_x + s.n_p; ++u) s.perm[pos++] = u;
+      F.pivtype = (s.pair_mode && n_root_p % 2 == 0) ? 2 : 1;
+      for (int64_t u = s.n_x + s.n_p - n_root_p; u < s.n_x + s.n_p; ++u) s.perm[pos++] = u;
     } else {
       F.pivtype = s.pair_mode ? 2 : 1;
-      for (int32_t sv : src.verts)
-        for (int32_t v : sv_members[sv])
-          for (int t = 0; t < 2; ++t)
-            if (node_unk[v][t] >= 0) s.perm[pos++] = node_unk[v][t];
+      // (x, lambda) pair nodes first, then p pairs: a p pair pivots on the Schur complement
+      // of the front's states (the positive definite reduced Hessian block)
+      for (int pass = 0; pass < (s.p_order ? 2 : 1); ++pass)
+        for (int32_t sv : src.verts)
+          for (int32_t v : sv_members[sv]) {
+            if (s.p_order && ((v >= s.n_x) != (pass == 1))) continue;
+            for (int t = 0; t < 2; ++t)
+              if (node_unk[v][t] >= 0) s.perm[pos++] = node_unk[v][t];
+          }
     }
     F.npiv = (int32_t)(pos - F.first);
     // generic mode: consecutive unknowns of an even-sized front are pivoted as 2x2 blocks
@@ -651,8 +664,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   // solve panel: forming L11^{-1} costs npiv^3/3 flops (as much as its factorization) and a
   // column-serial tail, to speed up a handful of solves.  Its solves are blocked
   // substitutions instead (T_RFWD / T_RBWD).  SGN_NOZ_TILES overrides (0: always Z).
-  int64_t kNoZTiles = 0;     // off by default: pays only when few solves follow a factorization
-  if (const char* e = std::getenv("SGN_NOZ_TILES")) kNoZTiles = std::atoll(e);
+  const int64_t kNoZTiles = opt.noz_tiles;   // 0 (default): off; pays only when few solves follow
   for (auto& F : s.fronts) {
     const int64_t nr = F.nrow, ns = F.nrow - F.npiv;
     F.noz = (kNoZTiles > 0 && F.is_root_p && ns == 0 && ptiles(F.npiv) >= kNoZTiles) ? 1 : 0;
@@ -763,14 +775,12 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   // consecutive pivot steps by one task (the C tile is read and written once per group;
   // the step tiles stream through shared memory): F_UPDATE b = tj | (ns << 16).
   // SGN_UPD_GROUP overrides (1 = one task per step).
-  int32_t kUpdGroup = 8;
-  if (const char* e = std::getenv("SGN_UPD_GROUP")) kUpdGroup = std::max(1, std::atoi(e));
+  const int32_t kUpdGroup = std::max(1, opt.upd_group);
   std::vector<int64_t> fcount(s.fronts.size(), 0);
   // Small fronts (<= kFatTiles tiles: the bottom levels) run as ONE task (F_FAT): their
   // tasks and Z blocks back to back in one CTA, without a grab, wait and counter hop per
   // tile.  SGN_FAT_TILES overrides (0: off).
-  int32_t kFatTiles = 0;     // off by default (measured: c2 span 1.53 -> 1.64 ms, c5 -1.7 %)
-  if (const char* e = std::getenv("SGN_FAT_TILES")) kFatTiles = std::atoi(e);
+  const int32_t kFatTiles = opt.fat_tiles;   // 0 (default): off (measured: c2 span 1.53 -> 1.64 ms, c5 -1.7 %)
   const int32_t NFr = (int32_t)s.fronts.size();
   std::vector<char> is_fat(NFr, 0);
   std::vector<int64_t> fat_slot(NFr, -1);
@@ -793,8 +803,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   // with at least kZInlineSteps pivot steps (the dependency-chain-bound upper fronts) get
   // their pivot-tile blocks right after pivot step t, so the panel is built while the
   // front is still being factored; all other blocks go to a queue (bottom levels first).
-  int32_t kZInlineSteps = 8;
-  if (const char* e = std::getenv("SGN_ZINLINE")) kZInlineSteps = std::max(1, std::atoi(e));
+  const int32_t kZInlineSteps = std::max(1, opt.zinline);
   std::vector<FTask> zq;
   std::vector<int32_t> zq_level;
   auto z_inline = [&](const Front& F) { return ptiles(F.npiv) >= kZInlineSteps; };
@@ -815,8 +824,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   // dependency chain of the upper fronts leaves idle; the rest go last.
   // SGN_ZQUOTA overrides the per-step quota (0 = all queued blocks last).
   size_t zhead = 0;
-  int64_t zquota = 256;
-  if (const char* e = std::getenv("SGN_ZQUOTA")) zquota = std::atoll(e);
+  const int64_t zquota = std::max(0, opt.zquota);
   auto emit_z = [&](int32_t lv) {
     for (int64_t q = 0; q < zquota && zhead < zq.size() && zq_level[zhead] <= lv - 2; ++q)
       s.ftasks.push_back(zq[zhead++]);
@@ -901,8 +909,7 @@ int build_symbolic(Symbolic& s, int64_t leaf_size, int64_t* pivot_index) {
   s.part_doubles = 0;
   // small fronts (the bottom levels) solve as one task each (T_FWD_FAT / T_BWD_FAT);
   // SGN_FAT_SOLVE=0 keeps the tiled tasks
-  bool fat_solve = true;
-  if (const char* e = std::getenv("SGN_FAT_SOLVE")) fat_solve = std::atoi(e) != 0;
+  const bool fat_solve = opt.fat_solve != 0;
   auto fat_front = [&](const Front& F, int32_t rows) {
     return fat_solve && F.npiv >= 1 && F.npiv <= kFwdCols && F.nrow <= rows;
   };

@@ -58,8 +58,8 @@ __global__ void k_axpy(int64_t n, const double* __restrict__ alpha, const double
   }
 }
 
-// f vector (KKT order): x block = w_t r at target dofs, p block = -R^T w_t r + w_reg p,
-// lambda block 0, with r = x[tdofs] - tvals - R p (R optional, CSR over targets; R^T is
+// f vector (KKT order): x block = sigma w_t r at target dofs, p block = -R^T w_t r + w_reg p,
+// lambda block 0, with r = sigma x[tdofs] - tvals - R p (R optional, CSR over targets; R^T is
 // the CSR over parameters); objective per instance = 0.5 sum w r^2 + 0.5 w_reg |p|^2.
 // Two grid-stride kernels (targets, then parameters: the R^T rows read the target
 // residuals) on up to kLsqBlocks CTAs per instance; block partials are summed by the last
@@ -77,7 +77,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 
 __global__ void __launch_bounds__(kLsqThreads)
 k_lsq_targets(int64_t n_x, int64_t n_p, int64_t nt, const int64_t* __restrict__ tdofs,
-              const double* __restrict__ tvals, int64_t tstride, double w_t, const double* __restrict__ x,
+              const double* __restrict__ tvals, int64_t tstride, double w_t, double xs, const double* __restrict__ x,
               const double* __restrict__ p, double* __restrict__ vec, const int64_t* __restrict__ rptr,
               const int64_t* __restrict__ ridx, const double* __restrict__ rcoef, double* __restrict__ rscr,
               double* __restrict__ part) {
@@ -91,11 +91,11 @@ k_lsq_targets(int64_t n_x, int64_t n_p, int64_t nt, const int64_t* __restrict__ 
   double acc = 0.0;
   for (int64_t t = blockIdx.x * (int64_t)kLsqThreads + threadIdx.x; t < nt; t += (int64_t)gridDim.x * kLsqThreads) {
     const int64_t d = tdofs[t];
-    double r = xb[d] - tvals[(int64_t)b * tstride + t];
+    double r = xs * xb[d] - tvals[(int64_t)b * tstride + t];
     if (rptr)
       for (int64_t k = rptr[t]; k < rptr[t + 1]; ++k) r -= rcoef[k] * pb[ridx[k]];
     acc += w_t * r * r;
-    if (v) v[d] = w_t * r;
+    if (v) v[d] = xs * w_t * r;
     if (rs) rs[t] = w_t * r;
   }
   const double tot = block_sum(acc, sh);
@@ -224,42 +224,12 @@ int sgn_masked_copy(int64_t n, int32_t batch, const int32_t* d_mask, const doubl
   return SGN_OK;
 }
 
-int sgn_lsq_terms(int32_t batch, int64_t n_x, int64_t n_p, int64_t nt, const int64_t* d_tdofs,
-                  const double* d_tvals, int64_t tstride, double w_t, double w_reg,
-                  const double* d_x, const double* d_p, double* d_vec, double* d_fobj, void* stream) {
-  return sgn_lsq_terms_r(batch, n_x, n_p, nt, d_tdofs, d_tvals, tstride, w_t, w_reg, d_x, d_p, d_vec,
-                         d_fobj, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
-}
-
-int sgn_lsq_terms_r(int32_t batch, int64_t n_x, int64_t n_p, int64_t nt, const int64_t* d_tdofs,
-                    const double* d_tvals, int64_t tstride, double w_t, double w_reg,
-                    const double* d_x, const double* d_p, double* d_vec, double* d_fobj,
-                    const int64_t* d_rptr, const int64_t* d_ridx, const double* d_rcoef,
-                    const int64_t* d_rtptr, const int64_t* d_rtidx, const double* d_rtcoef,
-                    double* d_rscr, void* stream) {
-  // per-process scratch: block partials + self-resetting tickets (stream-ordered use; one
-  // host thread per context, as for every entry point of this library)
-  static std::mutex mu;
-  static double* part = nullptr;
-  static int* tick = nullptr;
-  static int32_t cap = 0;
+int sgn_lsq_eval(int32_t batch, const sgn_lsq_args* a, const double* d_x, const double* d_p,
+                 double* d_vec, double* d_fobj, void* stream) {
+  if (!a || !a->part || !a->tickets || batch < 1) { sgn::last_error() = "lsq: bad arguments"; return SGN_INVALID; }
+  if (a->rptr && !a->rscr) { sgn::last_error() = "lsq: a residual p-map needs rscr"; return SGN_INVALID; }
   cudaStream_t st = (cudaStream_t)stream;
-  {
-    std::lock_guard<std::mutex> g(mu);
-    if (batch > cap) {
-      cudaDeviceSynchronize();
-      if (part) cudaFree(part);
-      if (tick) cudaFree(tick);
-      part = nullptr; tick = nullptr; cap = 0;
-      if (cudaMalloc(&part, (size_t)batch * 2 * kLsqBlocks * sizeof(double)) != cudaSuccess ||
-          cudaMalloc(&tick, (size_t)batch * sizeof(int)) != cudaSuccess ||
-          cudaMemset(tick, 0, (size_t)batch * sizeof(int)) != cudaSuccess) {
-        sgn::last_error() = "lsq scratch allocation failed";
-        return SGN_CUDA_ERROR;
-      }
-      cap = batch;
-    }
-  }
+  const int64_t n_x = a->n_x, n_p = a->n_p, nt = a->n_t;
   const int64_t dim = 2 * n_x + n_p;
   if (d_vec && cudaMemsetAsync(d_vec, 0, (size_t)batch * dim * sizeof(double), st) != cudaSuccess) {
     sgn::last_error() = "lsq: vector reset failed";
@@ -268,10 +238,11 @@ int sgn_lsq_terms_r(int32_t batch, int64_t n_x, int64_t n_p, int64_t nt, const i
   const int nbt = (int)std::max<int64_t>(1, std::min<int64_t>(kLsqBlocks, (nt + kLsqThreads - 1) / kLsqThreads));
   const int nbp = (int)std::max<int64_t>(1, std::min<int64_t>(kLsqBlocks, (n_p + kLsqThreads - 1) / kLsqThreads));
   sgn::count_launch(2);
-  k_lsq_targets<<<dim3(nbt, batch), kLsqThreads, 0, st>>>(n_x, n_p, nt, d_tdofs, d_tvals, tstride, w_t, d_x, d_p,
-                                                         d_vec, d_rptr, d_ridx, d_rcoef, d_rscr, part);
-  k_lsq_params<<<dim3(nbp, batch), kLsqThreads, 0, st>>>(n_x, n_p, nt, nbt, w_reg, d_p, d_vec, d_fobj, d_rtptr,
-                                                        d_rtidx, d_rtcoef, d_rscr, part, tick);
+  k_lsq_targets<<<dim3(nbt, batch), kLsqThreads, 0, st>>>(n_x, n_p, nt, a->tdofs, a->tvals, a->tstride, a->w_t,
+                                                         a->x_scale, d_x, d_p, d_vec, a->rptr, a->ridx, a->rcoef,
+                                                         a->rscr, a->part);
+  k_lsq_params<<<dim3(nbp, batch), kLsqThreads, 0, st>>>(n_x, n_p, nt, nbt, a->w_reg, d_p, d_vec, d_fobj, a->rtptr,
+                                                        a->rtidx, a->rtcoef, a->rscr, a->part, a->tickets);
   VEC_CHECK();
   return SGN_OK;
 }

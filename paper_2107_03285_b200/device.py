@@ -22,19 +22,42 @@ def _i64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.int64)
 
 
+# option fields of sgn_symbolic_options and the SGN_* variables that override them (for
+# profiling sweeps only; the product path passes options explicitly)
+_OPTION_ENV = {"leaf_size": "SGN_LEAF_SIZE", "upd_group": "SGN_UPD_GROUP", "zinline": "SGN_ZINLINE",
+               "zquota": "SGN_ZQUOTA", "noz_tiles": "SGN_NOZ_TILES", "fat_tiles": "SGN_FAT_TILES",
+               "fat_solve": "SGN_FAT_SOLVE", "generic_pairs": "SGN_GENERIC_PAIRS", "p_order": "SGN_P_ORDER"}
+
+
+def symbolic_options(**kw) -> "_lib.SymbolicOptions":
+    """Defaults (sgn_symbolic_options_default), then SGN_* environment overrides
+    (experiments), then the keyword arguments."""
+    import os
+    o = _lib.SymbolicOptions()
+    lib().sgn_symbolic_options_default(ctypes.byref(o))
+    for f, env in _OPTION_ENV.items():
+        if os.environ.get(env):
+            setattr(o, f, int(os.environ[env]))
+    for f, v in kw.items():
+        if v is not None:
+            setattr(o, f, int(v))
+    return o
+
+
 class Symbolic:
-    """Ordering + assembly tree + maps for one pattern (sgn_symbolic_create)."""
+    """Ordering + assembly tree + maps for one pattern (sgn_symbolic_create_ex)."""
 
     def __init__(self, n: int, indptr, indices, n_x: int = 0, n_p: int = 0, n_c: int = 0,
-                 leaf_size: int = 0):
+                 leaf_size: int = 0, **options):
         self.n, self.n_x, self.n_p, self.n_c = int(n), int(n_x), int(n_p), int(n_c)
         self.indptr = _i64(indptr)
         self.indices = _i64(indices)
         h = ctypes.c_void_p()
         piv = ctypes.c_int64(-1)
-        rc = lib().sgn_symbolic_create(
+        self.options = symbolic_options(leaf_size=leaf_size or None, **options)
+        rc = lib().sgn_symbolic_create_ex(
             self.n, self.indptr.ctypes.data_as(P_i64), self.indices.ctypes.data_as(P_i64),
-            self.n_x, self.n_p, self.n_c, int(leaf_size), ctypes.byref(h), ctypes.byref(piv))
+            self.n_x, self.n_p, self.n_c, ctypes.byref(self.options), ctypes.byref(h), ctypes.byref(piv))
         check(rc, piv.value, "symbolic analysis")
         self._h = h
 
@@ -72,14 +95,15 @@ class Symbolic:
             self._h = None
 
 
-def symbolic_for(n: int, indptr, indices, n_x: int = 0, n_p: int = 0, n_c: int = 0) -> Symbolic:
+def symbolic_for(n: int, indptr, indices, n_x: int = 0, n_p: int = 0, n_c: int = 0, **options) -> Symbolic:
     """Cached symbolic analysis (the pattern is analysed once, SURVEY §8(b) sgn_symbolic)."""
     indptr, indices = _i64(indptr), _i64(indices)
+    o = symbolic_options(**options)
     key = (int(n), int(n_x), int(n_p), int(n_c), indptr.tobytes().__hash__(),
-           indices.tobytes().__hash__(), int(indices.size))
+           indices.tobytes().__hash__(), int(indices.size), bytes(o))
     sym = _CACHE.get(key)
     if sym is None:
-        sym = Symbolic(n, indptr, indices, n_x, n_p, n_c)
+        sym = Symbolic(n, indptr, indices, n_x, n_p, n_c, **options)
         _CACHE[key] = sym
         while len(_CACHE) > _CACHE_MAX:
             _CACHE.popitem(last=False)

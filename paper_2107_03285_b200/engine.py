@@ -19,6 +19,7 @@ Newton with energy backtracking (forward.py:135-203) on the same element kernels
 """
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 import time
@@ -77,7 +78,14 @@ class MeshPlan:
     """Host precomputation for one mesh / parameterization (shared by all instances)."""
 
     def __init__(self, X0, conn, kind, fixed_verts, pmap, target_dofs, w_target, w_reg,
-                 f_ext=None, rest_base=None, groups=None, R=None):
+                 f_ext=None, rest_base=None, groups=None, R=None, disp_scale=None):
+        """disp_scale = sigma selects the displacement state: x = (pos - X(p)) / sigma on the free
+        dofs (fixed dofs stay at X0).  Then G_x = sigma * dc/dpos, the G_p block gains the
+        element-Hessian terms of the free dofs the p-map moves (dc/dp at fixed x), and the
+        least-squares residual of a target is sigma * x.  Without it x = positions."""
+        self.disp_scale = None if disp_scale is None else float(disp_scale)
+        if self.disp_scale is not None and R is not None:
+            raise ValueError("the displacement state has no residual p-map")
         self.X0 = np.asarray(X0, dtype=np.float64)
         self.n_v, self.d = self.X0.shape
         d = self.d
@@ -121,6 +129,13 @@ class MeshPlan:
         self.pos_idx = self.dof_to_x[is_free].astype(np.int64)
         # rest: X[dof] = X0[dof] + sum coef * p
         self.rest_ptr, self.rest_idx, self.rest_coef = _csr_from_lists(self.n_dof, pm_dof, pm_p, pm_coef)
+        if self.disp_scale is not None:
+            # displacement state: pos = restpos + sigma x, restpos = X(p) on free dofs, X0 on fixed
+            self.pos_coef = np.full(self.pos_idx.size, self.disp_scale)
+            fr = is_free[pm_dof]
+            self.restpos_ptr, self.restpos_idx, self.restpos_coef = _csr_from_lists(
+                self.n_dof, pm_dof[fr], pm_p[fr], pm_coef[fr])
+        sig = 1.0 if self.disp_scale is None else self.disp_scale
         self.rest_base = (self.X0.ravel().copy() if rest_base is None
                           else np.asarray(rest_base, dtype=np.float64).ravel().copy())
 
@@ -148,7 +163,7 @@ class MeshPlan:
             rows += [oL + gx_r, gx_c]
             cols += [gx_c, oL + gx_r]
             src += [gx_s, gx_s]
-            coef += [np.ones(gx_s.size), np.ones(gx_s.size)]
+            coef += [np.full(gx_s.size, sig), np.full(gx_s.size, sig)]
             # Gp block: row free dof, rest col dof -> p entries
             cnt = (rp[c_dof + 1] - rp[c_dof]) * (rx >= 0)
             sel = np.flatnonzero(cnt)
@@ -167,6 +182,15 @@ class MeshPlan:
                 cols += [n_x + pj, oL + gr]
                 src += [ms, ms]
                 coef += [pc, pc]
+                if self.disp_scale is not None:
+                    # dc/dp at fixed displacement: the free dofs the p-map moves carry
+                    # their element-Hessian column (H P_free), next to the mixed block (M P)
+                    fcol = cx[base_t] >= 0
+                    hs = hidx[base_t][fcol]
+                    rows += [oL + gr[fcol], n_x + pj[fcol]]
+                    cols += [n_x + pj[fcol], oL + gr[fcol]]
+                    src += [hs, hs]
+                    coef += [pc[fcol], pc[fcol]]
             # gradient gather entries of this group
             gdof = el_dofs.ravel()
             gx_ = self.dof_to_x[gdof]
@@ -178,7 +202,7 @@ class MeshPlan:
         # constant Gauss-Newton blocks (sensitivity.py:205-216): A = w on targets, and for a
         # residual r = x_t - R p: B = -w R^T (p rows, x cols), C = w R^T R + w_reg I
         nt = self.target_dofs.size
-        crow, ccol, cval = [self.target_dofs], [self.target_dofs], [np.full(nt, self.w_target)]
+        crow, ccol, cval = [self.target_dofs], [self.target_dofs], [np.full(nt, self.w_target * sig * sig)]
         self.R = None
         if R is not None:
             Rm = sp.csr_matrix(R)
@@ -220,6 +244,7 @@ class MeshPlan:
         np.cumsum(np.bincount(gu // n_x, minlength=n_x), out=self.G_indptr[1:])
         self.G_nnz = int(gu.size)
         self.G_ptr, self.G_src = _csr_from_lists(self.G_nnz, ginv, gx_s)
+        self.G_coef = None if self.disp_scale is None else np.full(self.G_src.size, self.disp_scale)
         gdiag = np.flatnonzero((gu % n_x) == (gu // n_x))
         self.G_diag = gdiag.astype(np.int64)               # nnz positions of the diagonal
 
@@ -520,11 +545,18 @@ class DeviceEngine:
         self.tvals = T(np.asarray(tvals, dtype=np.float64).reshape(B, -1))
         self.tdofs = T(pl.target_dofs, i64)
         self.pos_base, self.pos_ptr, self.pos_idx = T(pl.pos_base), T(pl.pos_ptr, i64), T(pl.pos_idx, i64)
+        self.disp_scale = pl.disp_scale
+        if pl.disp_scale is not None:
+            self.pos_coef = T(pl.pos_coef)
+            self.restpos_ptr, self.restpos_idx = T(pl.restpos_ptr, i64), T(pl.restpos_idx, i64)
+            self.restpos_coef = T(pl.restpos_coef)
+            self.X0_flat = T(pl.X0.ravel())
         self.rest_base, self.rest_ptr = T(pl.rest_base), T(pl.rest_ptr, i64)
         self.rest_idx, self.rest_coef = T(pl.rest_idx, i64), T(pl.rest_coef)
         self.K_base, self.K_ptr = T(pl.K_base), T(pl.K_ptr, i64)
         self.K_src, self.K_coef = T(pl.K_src, i64), T(pl.K_coef)
         self.G_ptr, self.G_src = T(pl.G_ptr, i64), T(pl.G_src, i64)
+        self.G_coef = None if pl.G_coef is None else T(pl.G_coef)
         self.G_diag = T(pl.G_diag, i64)
         self.grad_base, self.grad_ptr, self.grad_src = T(pl.grad_base), T(pl.grad_ptr, i64), T(pl.grad_src, i64)
         self.f_ext = T(pl.f_ext)
@@ -534,6 +566,7 @@ class DeviceEngine:
         self.p = z(B, pl.n_p)
         self.pos = z(B, pl.n_dof)
         self.rest = z(B, pl.n_dof)
+        self.restpos = z(B, pl.n_dof) if pl.disp_scale is not None else None
         self.ebuf = z(B, pl.ebuf_size)       # per group [hess | mixed]
         self.egrad = z(B, pl.egrad_size)
         self.eeners = [z(B, g.n_e) for g in pl.groups]
@@ -565,7 +598,10 @@ class DeviceEngine:
                                 if vp.max_inc <= gs)
             self.v_melems = T(pl.groups[0].melems, i32)
         self._gx_ready = False
-        self.ksym = symbolic_for(pl.dim, pl.K_indptr, pl.K_indices, pl.n_x, pl.n_p, pl.n_x)
+        # C = w R^T R + w_reg I > 0 when w_reg > 0: the stabilized KKT is quasi-definite and the
+        # p unknowns can join the nested dissection (p_order 1); otherwise they stay last
+        self.ksym = symbolic_for(pl.dim, pl.K_indptr, pl.K_indices, pl.n_x, pl.n_p, pl.n_x,
+                                 p_order=1 if pl.w_reg > 0.0 else 0)
         self.kfac = DeviceFactor(self.ksym, B)
         self._gfac = None
         from .linear_solvers import StabilizationConfig
@@ -609,14 +645,26 @@ class DeviceEngine:
         torch.cuda.current_stream().synchronize()
         return self._pin_sol.numpy().copy()
 
+    def _deformed(self, x):
+        """pos = X0 (fixed) | x (free): position state; pos = restpos + sigma x: displacement state."""
+        pl = self.plan
+        if pl.disp_scale is None:
+            self._gather(pl.n_dof, self.pos_base, 0, self.pos_ptr, self.pos_idx, None, x, pl.n_x,
+                         self.pos, pl.n_dof)
+        else:
+            self._gather(pl.n_dof, self.restpos, pl.n_dof, self.pos_ptr, self.pos_idx, self.pos_coef, x,
+                         pl.n_x, self.pos, pl.n_dof)
+
     def positions(self, x=None):
         pl = self.plan
         x = self.x if x is None else x
         self._gx_ready = False
-        self._gather(pl.n_dof, self.pos_base, 0, self.pos_ptr, self.pos_idx, None, x, pl.n_x,
-                     self.pos, pl.n_dof)
         self._gather(pl.n_dof, self.rest_base, 0, self.rest_ptr, self.rest_idx, self.rest_coef,
                      self.p, pl.n_p, self.rest, pl.n_dof)
+        if pl.disp_scale is not None:
+            self._gather(pl.n_dof, self.X0_flat, 0, self.restpos_ptr, self.restpos_idx, self.restpos_coef,
+                         self.p, pl.n_p, self.restpos, pl.n_dof)
+        self._deformed(x)
 
     def element_blocks(self, mixed: bool = True, hess: bool = True):
         """Element Hessians (and, with mixed=True, the rest-shape mixed blocks of the
@@ -675,7 +723,7 @@ class DeviceEngine:
             self._vertex(None, self.gvals)
         else:
             self.element_blocks(mixed=False)
-            self._gather(pl.G_nnz, None, 0, self.G_ptr, self.G_src, None, self.ebuf, self.ebuf.stride(0),
+            self._gather(pl.G_nnz, None, 0, self.G_ptr, self.G_src, self.G_coef, self.ebuf, self.ebuf.stride(0),
                          self.gvals, pl.G_nnz)
         self._gx_ready = True
 
@@ -772,18 +820,26 @@ class DeviceEngine:
         return s[:, :pl.n_x], s[:, pl.n_x:pl.n_x + pl.n_p], s[:, pl.n_x + pl.n_p:]
 
     def _lsq(self, x, fvec):
-        """Least-squares terms (sensitivity.py:83-93) incl. the optional residual p-map R."""
+        """Least-squares terms (sensitivity.py:83-93) incl. the optional residual p-map R and
+        the displacement state's scale; the block partials and tickets are this engine's own."""
         pl = self.plan
-        if pl.R is None:
-            check(lib().sgn_lsq_terms(self.batch, pl.n_x, pl.n_p, pl.target_dofs.size, ptr(self.tdofs),
-                                      ptr(self.tvals), self.tvals.stride(0), pl.w_target, pl.w_reg,
-                                      ptr(x), ptr(self.p), ptr(fvec), ptr(self.fobj), self.stream))
-        else:
-            check(lib().sgn_lsq_terms_r(self.batch, pl.n_x, pl.n_p, pl.target_dofs.size, ptr(self.tdofs),
-                                        ptr(self.tvals), self.tvals.stride(0), pl.w_target, pl.w_reg,
-                                        ptr(x), ptr(self.p), ptr(fvec), ptr(self.fobj), ptr(self.R_ptr),
-                                        ptr(self.R_idx), ptr(self.R_val), ptr(self.Rt_ptr), ptr(self.Rt_idx),
-                                        ptr(self.Rt_val), ptr(self.rscr), self.stream))
+        if not hasattr(self, "_lsq_args"):
+            torch = self.torch
+            self._lsq_part = torch.zeros(self.batch, 128, dtype=torch.float64, device="cuda")
+            self._lsq_tick = torch.zeros(self.batch, dtype=torch.int32, device="cuda")
+            a = _lib.LsqArgs()
+            a.n_x, a.n_p, a.n_t = pl.n_x, pl.n_p, int(pl.target_dofs.size)
+            a.tdofs, a.tvals, a.tstride = ptr(self.tdofs), ptr(self.tvals), self.tvals.stride(0)
+            a.w_t, a.w_reg = pl.w_target, pl.w_reg
+            a.x_scale = 1.0 if pl.disp_scale is None else pl.disp_scale
+            if pl.R is not None:
+                a.rptr, a.ridx, a.rcoef = ptr(self.R_ptr), ptr(self.R_idx), ptr(self.R_val)
+                a.rtptr, a.rtidx, a.rtcoef = ptr(self.Rt_ptr), ptr(self.Rt_idx), ptr(self.Rt_val)
+                a.rscr = ptr(self.rscr)
+            a.part, a.tickets = ptr(self._lsq_part), ptr(self._lsq_tick)
+            self._lsq_args = a
+        check(lib().sgn_lsq_eval(self.batch, ctypes.byref(self._lsq_args), ptr(x), ptr(self.p), ptr(fvec),
+                                 ptr(self.fobj), self.stream))
 
     # -- objective ---------------------------------------------------------------------
     def objective(self, x=None):
@@ -799,8 +855,7 @@ class DeviceEngine:
         pl = self.plan
         st = self.stream
         self._gx_ready = False
-        self._gather(pl.n_dof, self.pos_base, 0, self.pos_ptr, self.pos_idx, None, x, pl.n_x,
-                     self.pos, pl.n_dof)
+        self._deformed(x)
         for gi, (g, conn, prm, en) in enumerate(zip(pl.groups, self.conns, self.gparams, self.eeners)):
             check(lib().sgn_element_energy_grad(g.code, g.n_e, self.batch, ptr(conn), ptr(self.pos),
                                                 ptr(self.rest), pl.n_dof, ptr(prm), prm.stride(0), ptr(en),
@@ -933,6 +988,8 @@ class DeviceEngine:
         slope_t = torch.empty(B, dtype=torch.float64, device="cuda")
         check(lib().sgn_reduce(1, n, B, ptr(self.gx), ptr(self.kdir), n, ptr(slope_t), st))
         slope = slope_t.cpu().numpy()
+        if self.plan.disp_scale is not None:       # dE/dalpha = c . (sigma d) in the displacement state
+            slope = slope * self.plan.disp_scale
         slack = 4e-15 * np.abs(e0)
         alpha = np.ones(B)
         pending = np.asarray(mask, bool).copy()

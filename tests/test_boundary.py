@@ -61,6 +61,28 @@ def test_symbolic_kkt_tree_reproduces_factorization(shape):
     assert err <= 1e-13
 
 
+@pytest.mark.parametrize("shape", [(6, 5, 2, 7, 1e-2), (12, 10, 2, 9, 1e-3), (20, 17, 2, 30, 1e-3),
+                                   (20, 17, 2, 31, 1e-3)])
+def test_symbolic_p_pairs_in_dissection(shape):
+    """p_order 1 (C > 0): p pairs are dissection nodes (an odd last p is eliminated last),
+    the tree reproduces the factorization, and the ordering is deterministic."""
+    from paper_2107_03285_b200.device import Symbolic
+    K, n_x, n_p, _ = kkt_system(*shape)
+    s = Symbolic(K.shape[0], K.indptr, K.indices, n_x, n_p, n_x, leaf_size=16, p_order=1)
+    s2 = Symbolic(K.shape[0], K.indptr, K.indices, n_x, n_p, n_x, leaf_size=16, p_order=1)
+    assert s.stats()["pair_mode"] == 2
+    perm = s.perm()
+    assert np.array_equal(perm, s2.perm())
+    assert np.array_equal(np.sort(perm), np.arange(K.shape[0]))
+    if n_p % 2:
+        assert perm[-1] == n_x + n_p - 1
+    pos = np.argsort(perm)
+    for k in range(n_p // 2):                         # each p pair stays adjacent, in order
+        assert pos[n_x + 2 * k + 1] == pos[n_x + 2 * k] + 1
+    _, _, _, err, _ = emulate(K, s, 1e-6, 1e-6)
+    assert err <= 1e-12          # small C pivots (1e-3) eliminated early: modest growth
+
+
 def test_symbolic_generic_mode_and_determinism():
     from paper_2107_03285_b200.device import Symbolic
     g = grid_laplacian(15, 13, 2)

@@ -183,3 +183,34 @@ def test_beam_generators_agree_and_mesh_is_conforming():
             faces[tuple(sorted(t[list(f)]))] += 1
     assert max(faces.values()) == 2 and sum(v == 1 for v in faces.values()) == 3600
     assert len(a["p0"]) == 1881 and len(a["target_dofs"]) == 363
+
+
+def test_shell_displacement_state_jacobians_fd_and_theorem1():
+    """Config-4 oracle (displacement state in mm): dc/dx and dc/dp against central
+    differences of the constraints, and SGN = DGN (Theorem 1, checks.py:71-128)."""
+    from oracle import sgn_cpu
+    from oracle.shell import ShellProblem, shell_spec
+    spec = shell_spec(9, 5)
+    prob = ShellProblem(spec)
+    rng = np.random.default_rng(1)
+    p = 2e-3 * rng.standard_normal(prob.n_p)
+    x = prob.simulate(p)
+    assert np.abs(prob.constraints(x, p)).max() <= prob.tol
+    Gx = prob.constraint_jac_x(x, p).to_scipy()
+    Gp = prob.constraint_jac_p(x, p).to_scipy()
+    for _ in range(3):
+        v = rng.standard_normal(prob.n_x)
+        h = 1e-4
+        fd = (prob.constraints(x + h * v, p) - prob.constraints(x - h * v, p)) / (2 * h)
+        assert _rel(Gx @ v, fd) <= 1e-7
+        v = rng.standard_normal(prob.n_p)
+        h = 1e-7
+        fd = (prob.constraints(x, p + h * v) - prob.constraints(x, p - h * v)) / (2 * h)
+        assert _rel(Gp @ v, fd) <= 1e-6
+    # this coarse bumpy shell's reduced Hessian amplifies the refinement's residual into dp
+    # (3e-7 at the default 1e-10 tolerance); the reference's own knob, a tighter
+    # refine_tolerance, gives Theorem 1 to 2e-10
+    d_sgn = sgn_cpu.direction_sgn(prob, x, p, sgn_cpu.Stab(refine_tolerance=1e-12))
+    d_dgn = sgn_cpu.direction_dgn(prob, x, p)
+    assert d_sgn.res <= 1e-12
+    assert _rel(d_sgn.dp, d_dgn.dp) <= 1e-8
