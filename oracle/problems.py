@@ -176,32 +176,23 @@ class ElementProblem(_LsqMixin):
         return Csc(m.to_scipy() * self.scale)
 
     def constraint_jac_p(self, x, p):
+        """dc/dp = sum_e M_e P_e by one triplet build over every (element, row a, col b, p-map
+        entry of col b) -- vectorised, the pattern structural (no SpGEMM)."""
         _, M = self._second(self.full_positions(x), self.rest_positions(p))
         ne, nd, _ = M.shape
-        rows, cols, vals = [], [], []
         Pc = self.P.tocsr()
-        for b in range(nd):
-            rdof = self.el_dofs[:, b]
-            rx = self.dof_to_x[rdof]
-            for c in range(nd):
-                cdof = self.el_dofs[:, c]
-                # expand rest dof -> parameters
-                starts, ends = Pc.indptr[cdof], Pc.indptr[cdof + 1]
-                cnt = ends - starts
-                if not cnt.any():
-                    continue
-                e_idx = np.repeat(np.arange(ne), cnt)
-                k_idx = np.concatenate([np.arange(s_, e_) for s_, e_ in zip(starts, ends)]) if cnt.sum() else np.zeros(0, int)
-                pr = rx[e_idx]
-                keep = pr >= 0
-                rows.append(pr[keep])
-                cols.append(Pc.indices[k_idx][keep])
-                vals.append((M[e_idx, b, c] * Pc.data[k_idx])[keep])
-        if rows:
-            r, c, v = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
-        else:
-            r = c = np.zeros(0, int); v = np.zeros(0)
-        return csc_structural(r, c, self.scale * v, (self.n_x, self.n_p))
+        a_loc = np.repeat(np.arange(nd), nd)
+        b_loc = np.tile(np.arange(nd), nd)
+        rx = self.dof_to_x[self.el_dofs[:, a_loc].ravel()]
+        cdof = self.el_dofs[:, b_loc].ravel()
+        cnt = (Pc.indptr[cdof + 1] - Pc.indptr[cdof]) * (rx >= 0)
+        sel = np.flatnonzero(cnt)
+        rep = cnt[sel]
+        t = np.repeat(sel, rep)
+        offs = np.arange(int(rep.sum())) - np.repeat(np.cumsum(rep) - rep, rep)
+        kk = Pc.indptr[cdof[t]] + offs
+        v = M.reshape(ne, nd * nd)[t // (nd * nd), t % (nd * nd)] * Pc.data[kk]
+        return csc_structural(rx[t], Pc.indices[kk], self.scale * v, (self.n_x, self.n_p))
 
     # -- least squares (spring_bar.py:159-184 idiom) -----------------------------------------
     def residuals(self, x, p):
