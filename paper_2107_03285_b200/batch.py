@@ -36,3 +36,180 @@ def gather_instances(local: np.ndarray, n_total: int, world: int, rank: int, dev
         k = len(partition(n_total, world, r))
         rows.append(outs[r].cpu().numpy()[:k])
     return np.concatenate(rows, axis=0)
+
+
+class BatchRun:
+    """Per-instance outcome of ``minimize_batched`` (the batched analogue of the reference's
+    OptimizerRun, optimize.py:101-137): f / gradient-norm / step-length trajectories
+    ([B, max_iterations + 1], NaN after an instance terminated), termination strings, the
+    final parameters and the number of SGN directions each instance actually used."""
+
+    def __init__(self, f, grad_norm, alpha, rel_res, termination, p, directions, timings):
+        self.f, self.grad_norm, self.alpha, self.rel_res = f, grad_norm, alpha, rel_res
+        self.termination, self.p, self.directions, self.timings = termination, p, directions, timings
+
+    def trajectory(self, b: int) -> np.ndarray:
+        f = self.f[b]
+        return f[np.isfinite(f)]
+
+    def pack(self) -> np.ndarray:
+        """One float64 row per instance for the end-of-run gather: [f(it+1) | |g|(it+1) |
+        alpha(it+1) | directions | termination code]."""
+        codes = np.array([TERMINATIONS.index(t) for t in self.termination], dtype=np.float64)
+        return np.concatenate([self.f, self.grad_norm, self.alpha, self.directions[:, None].astype(np.float64),
+                               codes[:, None]], axis=1)
+
+    @staticmethod
+    def unpack_row(row: np.ndarray, iters: int) -> dict:
+        n = iters + 1
+        return dict(f=row[:n], grad_norm=row[n:2 * n], alpha=row[2 * n:3 * n], directions=int(row[3 * n]),
+                    termination=TERMINATIONS[int(row[3 * n + 1])])
+
+
+TERMINATIONS = ("max_iterations", "gradient_tolerance", "stationary", "no_descent", "line_search_failure",
+                "forward_failure")
+
+
+def minimize_batched(bd, p0, cfg, max_iterations: int | None = None) -> BatchRun:
+    """SGN outer loops of B independent instances on one device batch.
+
+    Each instance follows the reference minimize (optimize.py:353-420) with its own Armijo
+    backtracking (_line_search, optimize.py:468-488) and its own termination; the
+    instances share every launch: one batched SGN direction per iteration, the pending
+    trial points of all instances' line searches forward-solved as ONE masked batched Newton
+    (engine.simulate(active=...)), one batched adjoint gradient after the accepted steps.
+    p, x, g, dp stay on the device; only per-instance scalars (f, slopes, norms: B doubles)
+    reach the host for the Armijo and termination decisions.  Instances never read one
+    another's data, so an instance's trajectory is bitwise the same in any batch.
+    """
+    import time
+    from . import _lib
+    from ._lib import check, lib, ptr
+    from .engine import adjoint_gradient_stage
+    from .errors import ForwardSimFailure, NoConvergence
+    eng = bd.engine
+    torch = eng.torch
+    B, n_x, n_p = bd.B, bd.n_x, bd.n_p
+    iters = cfg.max_iterations if max_iterations is None else int(max_iterations)
+    eng.stab = cfg.stabilization
+    st = _lib.stream_handle()
+    dev = dict(dtype=torch.float64, device="cuda")
+    p_cur = torch.empty(B, n_p, **dev)
+    x_cur = torch.empty(B, n_x, **dev)
+    g = torch.empty(B, n_p, **dev)
+    dp = torch.empty(B, n_p, **dev)
+    step = torch.empty(B, n_p, **dev)
+    red = torch.empty(B, **dev)
+    neg1 = torch.full((B,), -1.0, **dev)
+
+    def dot(a, b):
+        check(lib().sgn_reduce(1, a.shape[1], B, ptr(a), ptr(b), a.shape[1], ptr(red), st))
+        return red.cpu().numpy().copy()
+
+    def mask(m):
+        return torch.as_tensor(np.asarray(m, dtype=np.int32), device="cuda")
+
+    def gradient_into(sel):
+        """g[sel] <- adjoint gradient at (eng.x, eng.p) (batched; other rows untouched)."""
+        eng.assemble()
+        adjoint_gradient_stage(eng)
+        check(lib().sgn_masked_copy(n_p, B, ptr(mask(sel)), ptr(eng.grad), ptr(g), n_p, st))
+
+    t0 = time.perf_counter()
+    timings = dict(direction_s=0.0, line_search_s=0.0, gradient_s=0.0)
+    term = ["max_iterations"] * B
+    active = np.ones(B, bool)
+    # initial forward solve (minimize: optimize.py:364-368), from the rest shape
+    eng.load(x=bd.rest_start(), p=np.asarray(p0, dtype=np.float64).reshape(B, n_p))
+    status = eng.simulate(bd.tol)
+    for b in np.flatnonzero(status != 1):
+        term[b] = "forward_failure"
+    active &= status == 1
+    p_cur.copy_(eng.p)
+    x_cur.copy_(eng.x)
+    f = eng.objective().cpu().numpy().copy()
+    gradient_into(np.ones(B, bool))
+    F = np.full((B, iters + 1), np.nan)
+    GN = np.full((B, iters + 1), np.nan)
+    AL = np.full((B, iters + 1), np.nan)
+    RR = np.full((B, iters + 1), np.nan)
+    ndir = np.zeros(B, dtype=np.int64)
+    gn = np.sqrt(dot(g, g))
+    F[:, 0], GN[:, 0], AL[:, 0] = f, gn, 0.0
+    for it in range(1, iters + 1):
+        done = active & (gn <= cfg.gradient_tolerance)
+        for b in np.flatnonzero(done):
+            term[b] = "gradient_tolerance"
+        active &= ~done
+        if not active.any():
+            break
+        # one batched SGN direction at every instance's (x, p)
+        td = time.perf_counter()
+        eng.x.copy_(x_cur)
+        eng.p.copy_(p_cur)
+        try:
+            res, _ = eng.direction()
+        except NoConvergence as exc:       # the reference raises too; every row keeps its best
+            res = np.full(B, float(exc.residual))
+        dp.copy_(eng.sol[:, n_x:n_x + n_p])
+        ndir += active
+        timings["direction_s"] += time.perf_counter() - td
+        dpn, gdp = dot(dp, dp), dot(g, dp)
+        for b in np.flatnonzero(active & (dpn == 0.0)):
+            term[b] = "stationary"
+        active &= dpn != 0.0
+        for b in np.flatnonzero(active & (gdp >= 0.0)):
+            term[b] = "no_descent"
+        active &= gdp < 0.0
+        if not active.any():
+            break
+        # per-instance Armijo backtracking; all pending trial points in one masked batch
+        tl = time.perf_counter()
+        alpha = np.ones(B)
+        pending = active.copy()
+        acc_alpha = np.zeros(B)
+        for _ in range(cfg.max_backtracks + 1):
+            if not pending.any():
+                break
+            a_d = torch.as_tensor(alpha, **dev)
+            check(lib().sgn_axpy(n_p, B, ptr(a_d), ptr(dp), ptr(p_cur), ptr(eng.p), n_p, st))   # p_try
+            check(lib().sgn_axpy(n_p, B, ptr(neg1), ptr(p_cur), ptr(eng.p), ptr(step), n_p, st))
+            slope = dot(g, step)                                     # g . (p_try - p)
+            run = pending & (slope < 0.0)
+            if run.any():
+                eng.x.copy_(x_cur)                                   # warm start x_init = x
+                try:
+                    stat = eng.simulate(bd.tol, active=run)
+                except ForwardSimFailure:                            # B == 1 raises instead
+                    stat = np.full(B, -1)
+                ok = run & (stat == 1)
+                ft = eng.objective().cpu().numpy()
+                acc = ok & np.isfinite(ft) & (ft <= f + cfg.armijo_c1 * slope)
+                if acc.any():
+                    m = mask(acc)
+                    check(lib().sgn_masked_copy(n_p, B, ptr(m), ptr(eng.p), ptr(p_cur), n_p, st))
+                    check(lib().sgn_masked_copy(n_x, B, ptr(m), ptr(eng.x), ptr(x_cur), n_x, st))
+                    f = np.where(acc, ft, f)
+                    acc_alpha = np.where(acc, alpha, acc_alpha)
+                    pending &= ~acc
+            alpha = np.where(pending, alpha * cfg.backtrack_factor, alpha)
+        timings["line_search_s"] += time.perf_counter() - tl
+        for b in np.flatnonzero(pending):
+            term[b] = "line_search_failure"
+        accepted = active & ~pending
+        active = accepted
+        if not accepted.any():
+            break
+        tg = time.perf_counter()
+        eng.x.copy_(x_cur)
+        eng.p.copy_(p_cur)
+        gradient_into(accepted)
+        timings["gradient_s"] += time.perf_counter() - tg
+        gn_new = np.sqrt(dot(g, g))
+        gn = np.where(accepted, gn_new, gn)
+        F[accepted, it] = f[accepted]
+        GN[accepted, it] = gn[accepted]
+        AL[accepted, it] = acc_alpha[accepted]
+        RR[accepted, it] = np.asarray(res)[accepted]
+    timings["total_s"] = time.perf_counter() - t0
+    return BatchRun(F, GN, AL, RR, term, p_cur.cpu().numpy(), ndir, timings)

@@ -579,12 +579,18 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
   }
 
   // ---- nodes ----------------------------------------------------------------
-  // node_unk: unknowns of each graph node.  p unknowns are not graph nodes in KKT mode
-  // with p_order 0 (all eliminated last, in the root front); with p_order 1 the pairs
-  // (p_2k, p_2k+1) are nodes of weight 2 (2x2 pivots: the p block's Schur complement is
-  // positive definite when C > 0), and an odd last p alone is eliminated last.
-  const int64_t n_p_nodes = s.p_order ? s.n_p / 2 : 0;
-  const int64_t n_root_p = s.pair_mode ? s.n_p - 2 * n_p_nodes : 0;
+  // node_unk: unknowns of each graph node.  p unknowns are not graph nodes in KKT mode:
+  // with p_order 0 they are all eliminated last, in the root front; with p_order 1 the
+  // pairs (p_2k, p_2k+1) are placed after the dissection (below), and an odd last p is
+  // eliminated last.
+  if (s.p_order) {
+    for (int64_t c = s.n_x; c < s.n_x + s.n_p && s.p_order; ++c)
+      for (int64_t k = s.indptr[c]; k < s.indptr[c + 1]; ++k) {
+        const int64_t r = s.indices[k];
+        if (r != c && r >= s.n_x && r < s.n_x + s.n_p) { s.p_order = 0; break; }
+      }
+  }
+  const int64_t n_pp = s.p_order ? s.n_p / 2 : 0;
   std::vector<int64_t> node_of(n, -1);
   std::vector<std::array<int64_t, 2>> node_unk;
   std::vector<int32_t> node_w;
@@ -604,7 +610,9 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
       node_of[l] = i;
     }
     node_w.assign(s.n_x, 2);
-    for (int64_t k = 0; k < n_p_nodes; ++k) {
+    // p pairs enter the dissection as guide nodes (so separators account for their
+    // couplings); where they are eliminated is decided after it (p placement below)
+    for (int64_t k = 0; k < n_pp; ++k) {
       const int64_t a = s.n_x + 2 * k;
       node_of[a] = node_of[a + 1] = (int64_t)node_unk.size();
       node_unk.push_back({a, a + 1});
@@ -734,6 +742,77 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
     Dissector d(cg, cw, leaf_size);
     nd = d.run();
   }
+  // ---- p placement (p_order 1) -------------------------------------------------
+  // Pair k = (p_2k, p_2k+1) joins the front that is the lowest common ancestor of the
+  // fronts holding its coupled states / multipliers: it is eliminated right after the last
+  // of them, as a 2x2 pivot on the Schur complement of everything it couples to (positive
+  // definite when C > 0), so no early small pivot (C alone) enters the factor -- the
+  // reduced-Hessian structure of the p-last root front, localized.  Pairs without state
+  // couplings (or spanning disconnected components) go to the root p-front.  A p-p
+  // coupling off the diagonal of C would need both p on one root path: p_order falls back to 0.
+  std::vector<int32_t> pfront(n_pp, -1);
+  if (n_pp > 0) {
+    const int32_t NDF = (int32_t)nd.size();
+    std::vector<int32_t> node_front(N, -1), depth(NDF, 0);
+    for (int32_t f = 0; f < NDF; ++f) {
+      for (int32_t sv : nd[f].verts)
+        for (int32_t v : sv_members[sv])
+          if (v < s.n_x) node_front[v] = f;
+      depth[f] = nd[f].parent >= 0 ? depth[nd[f].parent] + 1 : 0;   // parents are created first
+    }
+    auto lca = [&](int32_t a, int32_t b) {
+      while (a != b && a >= 0 && b >= 0) {
+        if (depth[a] >= depth[b]) a = nd[a].parent;
+        else b = nd[b].parent;
+      }
+      return (a == b) ? a : -1;
+    };
+    for (int64_t k = 0; k < n_pp; ++k) {
+      int32_t at = -2;     // -2: no coupling seen yet
+      for (int64_t u = s.n_x + 2 * k; u <= s.n_x + 2 * k + 1 && at != -1; ++u)
+        for (int64_t q = s.indptr[u]; q < s.indptr[u + 1]; ++q) {
+          const int64_t nd_ = node_of[s.indices[q]];
+          if (nd_ < 0 || nd_ >= s.n_x) continue;
+          const int32_t f = node_front[nd_];
+          at = (at == -2) ? f : lca(at, f);
+          if (at < 0) { at = -1; break; }
+        }
+      pfront[k] = at < 0 ? -1 : at;
+    }
+  }
+  int64_t n_root_pairs = 0;
+  for (int32_t f : pfront) n_root_pairs += (f < 0);
+  const int64_t n_root_p = !s.pair_mode ? 0 : (s.p_order ? 2 * n_root_pairs + (s.n_p & 1) : s.n_p);
+  std::vector<std::vector<int32_t>> pairs_of(nd.size());
+  for (int64_t k = 0; k < n_pp; ++k)
+    if (pfront[k] >= 0) pairs_of[pfront[k]].push_back((int32_t)k);
+  if (n_pp > 0) {
+    // drop the guide nodes from the fronts, then the fronts left without pivots (their
+    // children move up to the nearest kept ancestor)
+    const int32_t NDF = (int32_t)nd.size();
+    std::vector<int32_t> keep_id(NDF, -1), eff(NDF, -1);
+    std::vector<NdFront> kept;
+    std::vector<std::vector<int32_t>> kept_pairs;
+    for (int32_t f = 0; f < NDF; ++f) {
+      std::vector<int32_t> vs;
+      for (int32_t sv : nd[f].verts) {
+        bool any = false;
+        for (int32_t v : sv_members[sv]) any |= (v < s.n_x);
+        if (any) vs.push_back(sv);
+      }
+      const int32_t par = nd[f].parent >= 0 ? eff[nd[f].parent] : -1;
+      if (vs.empty() && pairs_of[f].empty()) { eff[f] = par; continue; }
+      NdFront nf;
+      nf.verts.swap(vs);
+      nf.parent = par;
+      keep_id[f] = eff[f] = (int32_t)kept.size();
+      kept.push_back(std::move(nf));
+      kept_pairs.push_back(std::move(pairs_of[f]));
+    }
+    nd.swap(kept);
+    pairs_of.swap(kept_pairs);
+  }
+
   int32_t proot = -1;
   if (s.pair_mode && n_root_p > 0) {
     NdFront pf;
@@ -791,18 +870,23 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
       // 2x2 pivots on consecutive p unknowns halve the serial pivot chain of the root's
       // diagonal blocks (an even count keeps every pair inside one 32-column tile)
       F.pivtype = (s.pair_mode && n_root_p % 2 == 0) ? 2 : 1;
-      for (int64_t u = s.n_x + s.n_p - n_root_p; u < s.n_x + s.n_p; ++u) s.perm[pos++] = u;
+      if (s.p_order) {
+        for (int64_t k = 0; k < n_pp; ++k)
+          if (pfront[k] < 0) { s.perm[pos++] = s.n_x + 2 * k; s.perm[pos++] = s.n_x + 2 * k + 1; }
+        if (s.n_p & 1) s.perm[pos++] = s.n_x + s.n_p - 1;
+      } else {
+        for (int64_t u = s.n_x; u < s.n_x + s.n_p; ++u) s.perm[pos++] = u;
+      }
     } else {
       F.pivtype = s.pair_mode ? 2 : 1;
-      // (x, lambda) pair nodes first, then p pairs: a p pair pivots on the Schur complement
-      // of the front's states (the positive definite reduced Hessian block)
-      for (int pass = 0; pass < (s.p_order ? 2 : 1); ++pass)
-        for (int32_t sv : src.verts)
-          for (int32_t v : sv_members[sv]) {
-            if (s.p_order && ((v >= s.n_x) != (pass == 1))) continue;
-            for (int t = 0; t < 2; ++t)
-              if (node_unk[v][t] >= 0) s.perm[pos++] = node_unk[v][t];
-          }
+      for (int32_t sv : src.verts)
+        for (int32_t v : sv_members[sv]) {
+          if (s.pair_mode && v >= s.n_x) continue;           // guide node (p pair placed below)
+          for (int t = 0; t < 2; ++t)
+            if (node_unk[v][t] >= 0) s.perm[pos++] = node_unk[v][t];
+        }
+      // then the p pairs placed here (after the states they couple to)
+      for (int32_t k : pairs_of[post[k]]) { s.perm[pos++] = s.n_x + 2 * k; s.perm[pos++] = s.n_x + 2 * k + 1; }
     }
     F.npiv = (int32_t)(pos - F.first);
     // generic mode: consecutive unknowns of an even-sized front are pivoted as 2x2 blocks

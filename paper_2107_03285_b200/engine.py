@@ -428,9 +428,30 @@ def _factor_adjoint(eng, st, cur, f0=None, f1=None, events=None):
         ev_adj.record(side)
     cur.wait_event(ev_adj)
     eng.gfac.set_grid(0)
+    eng.kfac.set_grid(0)
     if events is not None:
         events[1].record()
     return res_a, it_a
+
+
+def adjoint_gradient_stage(eng):
+    """Adjoint gradient alone (reference sensitivity.py:160-198): the unshifted LDL^T of
+    dc/dx, one solve, then g = f_p + G_p^T lambda -- no KKT factorization.  A zero pivot of
+    dc/dx raises SingularConstraintJacobian(pivot_index) (_factor_constraint_jac,
+    sensitivity.py:160-164).  The result is in eng.grad; eng.rhs = (0, -g, 0)."""
+    from .errors import SingularConstraintJacobian
+    st = _lib.stream_handle()
+    n_x, n_p = eng.n_x, eng.n_p
+    eng.adjoint_direct(check_pivots=False)
+    piv = eng.gfac.status(st)
+    bad = np.flatnonzero(piv >= 0)
+    if bad.size:
+        raise SingularConstraintJacobian(f"singular state Jacobian dc/dx (instance {int(bad[0])})",
+                                         pivot_index=int(piv[bad[0]]))
+    eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, st)
+    check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
+                                 ptr(eng.grad), st))
+    eng.rhs.copy_(eng.tmp)
 
 
 def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = True, events=None,

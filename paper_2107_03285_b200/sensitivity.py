@@ -6,10 +6,9 @@ Same names and signatures as the reference (pkg/src/sgnopt/sensitivity.py):
 ``adjoint_gradient`` (194-198).
 
 * GPU-native problems (``problems.ElasticDesignProblem``, carrying ``.engine``): the
-  adjoint gradient comes from the device KKT factor -- the leading (x, lambda) block
-  of the stabilized LDL^T preconditions BiCGSTAB on [[A, Gx^T], [Gx, 0]], whose
-  lambda part is Gx^{-T} df/dx -- so no separate factorization of dc/dx is needed
-  (the reference factors dc/dx with SuperLU for this, sensitivity.py:160-164).
+  adjoint gradient comes from a device LDL^T of dc/dx (the reference's SuperLU of dc/dx,
+  sensitivity.py:160-164) and one solve, g = f_p + G_p^T lambda; inside a direction it
+  runs on a side stream next to the KKT factorization (``engine.sgn_solve_stages``).
 * Plugin problems (user subclasses evaluated on the host): Jacobians come from the
   problem's own evaluators and the stacked KKT is solved on the device (``HostKKT``).
 """
@@ -143,12 +142,12 @@ def _host_kkt(prob, x, p, blocks=None):
 
 def adjoint_gradient(prob, x, p, factor=None):
     """Total gradient df/dp by the adjoint method (sensitivity.py:194-198), on the device."""
-    from .engine import sgn_solve_stages
+    from .engine import adjoint_gradient_stage, sgn_solve_stages
     if _is_device_problem(prob):
         eng = prob.engine
         prob._load(x, p)
         eng.assemble()
-        sgn_solve_stages(eng, None, need_direction=False)
+        adjoint_gradient_stage(eng)
         return eng.grad[0].cpu().numpy()
     hk, _ = _host_kkt(prob, x, p)
     sgn_solve_stages(hk, None, need_direction=False)
