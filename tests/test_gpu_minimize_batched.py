@@ -1,0 +1,65 @@
+"""BASELINE config 5 as specified: independent instances of the 100x100 sheet, each running
+20 SGN iterations with its own Armijo line search and termination, all on one device batch
+(paper_2107_03285_b200.batch.minimize_batched).
+
+* every instance's trajectory equals the reference minimize (optimize.py:353-420, 468-488)
+  on the oracle problem to 1e-8 (tests/golden/large_c5.npz, instances 1-3, written by the
+  real reference through tests/golden/make_golden_large.py);
+* an instance's batched trajectory is bitwise the one it has alone (batch of 1).
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def batched_run(cuda):
+    from paper_2107_03285_b200 import OptimizerConfig
+    from paper_2107_03285_b200.batch import minimize_batched
+    from paper_2107_03285_b200.problems import build_sheet_batch
+    bd = build_sheet_batch(2, 0, instances=[1, 2, 3])
+    cfg = OptimizerConfig(method="sgn", max_iterations=20, gradient_tolerance=1e-12)
+    return bd, minimize_batched(bd, bd.p0, cfg)
+
+
+def test_batched_trajectories_match_reference_minimize(batched_run):
+    _, run = batched_run
+    gold = np.load(os.path.join(GOLDEN, "large_c5.npz"))
+    for b, inst in enumerate((1, 2, 3)):
+        ref_f = gold[f"i{inst}_traj_f"]
+        f = run.trajectory(b)
+        assert run.termination[b] == str(gold[f"i{inst}_traj_term"]), (inst, run.termination[b])
+        assert f.size == ref_f.size, (inst, f.size, ref_f.size)
+        np.testing.assert_allclose(f, ref_f, rtol=1e-8, atol=0)
+        ref_a = gold[f"i{inst}_traj_alpha"]
+        np.testing.assert_array_equal(run.alpha[b][:ref_a.size], ref_a)      # same Armijo decisions
+        extra = run.termination[b] in ("line_search_failure", "no_descent", "stationary")
+        assert run.directions[b] == ref_f.size - 1 + extra
+
+
+def test_batched_instance_equals_single_instance_bitwise(batched_run):
+    from paper_2107_03285_b200 import OptimizerConfig
+    from paper_2107_03285_b200.batch import minimize_batched
+    from paper_2107_03285_b200.problems import build_sheet_batch
+    _, run = batched_run
+    one = build_sheet_batch(2, 0, instances=[2])
+    cfg = OptimizerConfig(method="sgn", max_iterations=20, gradient_tolerance=1e-12)
+    r1 = minimize_batched(one, one.p0, cfg)
+    np.testing.assert_array_equal(r1.f[0], run.f[1])
+    np.testing.assert_array_equal(r1.grad_norm[0], run.grad_norm[1])
+    np.testing.assert_array_equal(r1.p[0], run.p[1])
+    assert r1.termination[0] == run.termination[1]
+
+
+def test_pack_roundtrip(batched_run):
+    from paper_2107_03285_b200.batch import BatchRun
+    _, run = batched_run
+    rows = run.pack()
+    for b in range(rows.shape[0]):
+        u = BatchRun.unpack_row(rows[b], 20)
+        np.testing.assert_array_equal(u["f"], run.f[b])
+        assert u["termination"] == run.termination[b] and u["directions"] == run.directions[b]
