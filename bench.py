@@ -1,28 +1,32 @@
 #!/usr/bin/env python
-"""SGN search directions/sec on B200 -- BASELINE.json metric, config 2 (100x100 sheet).
+"""SGN search directions/sec on B200 -- BASELINE.json metric; default workload config 4
+(the 201x201 discrete shell, the largest single-GPU config).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1..5]
 
 One *step* = one SGN search direction (reference direction_sgn, optimize.py:155-165):
 device assembly of the element Hessian / mixed blocks into the KKT pattern, the LDL^T
-factorization, the adjoint gradient and the refined KKT solve, on the 100x100
-neo-Hookean sheet (BASELINE configs[1]; synthetic seeded inputs, oracle/configs.py).
+factorization, the adjoint gradient and the refined KKT solve (synthetic seeded inputs,
+oracle/configs.py, oracle/shell.py).  Config 5 (64 sheet instances) times whole batched
+20-iteration SGN runs (batch.minimize_batched) and counts the directions computed.
 
 * ``value``  -- directions/sec with x, p resident in HBM (device time, CUDA events on
   the launching stream, max over ranks); L2 is flushed (512 MiB memset) before every
   timed step, outside the events.
 * ``e2e``    -- the same metric through the public API direction_sgn(prob, x, p, cfg)
   with host NumPy inputs/outputs (H2D of x, p and D2H of the solution every step).
-* ``roofline`` -- the factorization phase (k_assemble/k_panel/k_update launches) on the
-  FP64 tensor pipe: algorithmic LDL^T flops of the symbolic analysis / its live event
-  time, against the DMMA peak measured in the same run (MEASURED_PEAKS.json has no FP64
-  entry); per-phase HBM fractions in ``phases``.
-* ``cpu_baseline`` -- the CPU oracle (restated reference path: SciPy SuperLU + BiCGSTAB)
-  on 1 host core over a bounded sample of directions.
-* ``--impl reference`` -- the oracle port of the reference's CPU path on all host cores
-  (one single-threaded direction per worker per step).
-With N > 1 (torchrun) every rank runs an independent replica ("replicas only": a single
-sparse factorization does not shard); value = total directions / max-over-ranks time.
+* ``roofline`` -- the factorization (k_factor_dag) on the FP64 tensor pipe: algorithmic
+  LDL^T flops of the symbolic analysis / its live event time, against the DMMA peak
+  measured in the same run (MEASURED_PEAKS.json has no FP64 entry); per-phase HBM
+  fractions in ``phases``.
+* ``cpu_baseline`` -- the CPU oracle (the reference path restated: SciPy SuperLU +
+  BiCGSTAB, oracle/sgn_cpu.py) on 1 host core: SGN and DGN directions (the reference's
+  time_direction, cli.py:189-232).  For config 4 one SGN direction takes minutes: it runs
+  in a separate process from the start of the bench, concurrently with the GPU part.
+* ``--impl reference`` -- the oracle port of the reference's CPU path on the host cores
+  (one single-threaded direction -- config 5: one 20-iteration minimize -- per worker).
+With N > 1 (torchrun) configs 1-4 run independent replicas ("replicas only": a single
+sparse factorization does not shard); config 5 partitions the instances over the ranks.
 """
 from __future__ import annotations
 
@@ -40,17 +44,21 @@ sys.path.insert(0, ROOT)
 
 METRIC = "SGN search directions/sec (assemble+factor+solve)"
 UNIT = "directions/s"
+C5_ITERS = 20
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--cpu-sample", type=int, default=3, help="directions in the cpu_baseline sample")
+    ap.add_argument("--cpu-budget", type=float, default=420.0,
+                    help="seconds the GPU arm waits for a config-4 CPU direction")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-child", default=None, help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -105,102 +113,184 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ CPU legs
-def _cpu_worker_init(config, targets=None):
+def oracle_problem(config, instance=0):
+    """(oracle problem, p0) of a config (test infrastructure restating the reference path)."""
+    if config in (1, 2):
+        from oracle.configs import oracle_sheet
+        return oracle_sheet(config, 0, instance)
+    if config == 3:
+        from oracle.configs import oracle_beam
+        prob, p0 = oracle_beam(0)
+        sag = prob.simulate(p0)                       # targets lift the sagged tip face
+        return oracle_beam(0, targets=sag[prob.target_dofs])
+    if config == 4:
+        from oracle.shell import ShellProblem, shell_spec
+        spec = shell_spec(201, 100)
+        return ShellProblem(spec), spec["p0"]
+    if config == 5:
+        from oracle.configs import oracle_sheet
+        return oracle_sheet(2, 0, max(1, instance))
+    raise ValueError(f"unknown config {config}")
+
+
+def _cpu_worker_init(config):
     global _W
     from threadpoolctl import threadpool_limits
     threadpool_limits(1)
-    if config == 3:
-        from oracle.configs import oracle_beam
-        prob, p0 = oracle_beam(0, targets=targets)
-    else:
-        from oracle.configs import oracle_sheet
-        prob, p0 = oracle_sheet(config)
-    _W = (prob, p0)
+    prob, p0 = oracle_problem(config)
+    x = prob.simulate(p0)
+    _W = (prob, p0, x)
 
 
-def _cpu_worker_direction(x):
+def _cpu_worker_direction(_=None):
     from oracle import sgn_cpu
-    prob, p0 = _W
+    prob, p0, x = _W
     t0 = time.perf_counter()
     d = sgn_cpu.direction_sgn(prob, x, p0)
     return time.perf_counter() - t0, d.timings
 
 
-def cpu_equilibrium(config):
-    from oracle.configs import oracle_sheet
-    prob, p0 = oracle_sheet(config)
-    return prob.simulate(p0)
-
-
-def cpu_baseline(config, x, sample, targets=None):
-    """Oracle port on 1 core: median of `sample` directions (after one warm-up)."""
+def _cpu_worker_minimize(instance):
+    """One reference SGN run of a config-5 instance (minimize, 20 iterations) on 1 core;
+    returns (wall seconds, directions computed)."""
     from threadpoolctl import threadpool_limits
-    _cpu_worker_init(config, targets)
+    from oracle import sgn_cpu
+    threadpool_limits(1)
+    prob, p0 = oracle_problem(5, instance)
+    t0 = time.perf_counter()
+    run = sgn_cpu.minimize_sgn(prob, p0, max_iterations=C5_ITERS, gradient_tolerance=1e-12)
+    n_dir = len(run["f"]) - 1 + (run["termination"] in ("line_search_failure", "no_descent", "stationary"))
+    return time.perf_counter() - t0, n_dir
+
+
+def cpu_baseline(config, sample):
+    """Oracle port on 1 core: median of `sample` SGN directions (after one warm-up) and of
+    DGN directions (the reference's time_direction measures both, cli.py:189-232)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import sgn_cpu
+    _cpu_worker_init(config)
+    prob, p0, x = _W
     with threadpool_limits(1):
-        _cpu_worker_direction(x)
-        ts = [_cpu_worker_direction(x) for _ in range(sample)]
+        _cpu_worker_direction()
+        ts = [_cpu_worker_direction() for _ in range(sample)]
+        td = []
+        for _ in range(sample if config != 3 else 1):
+            t0 = time.perf_counter()
+            sgn_cpu.direction_dgn(prob, x, p0)
+            td.append(time.perf_counter() - t0)
     med = statistics.median([t for t, _ in ts])
     phases = {k: statistics.median([tt[k] for _, tt in ts]) for k in ("assemble_s", "factor_s", "solve_s")}
     return {"value": 1.0 / med, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{sample} directions (median) of config {config} on 1 core after 1 warm-up; "
+            "sample": f"{sample} SGN directions (median) of config {config} on 1 core after 1 warm-up; "
                       f"oracle/sgn_cpu.py restating the reference SuperLU+BiCGSTAB path",
-            "median_s": med, "phases_s": phases}
+            "median_s": med, "phases_s": phases,
+            "dgn": {"value": 1.0 / statistics.median(td), "unit": UNIT, "sample": f"{len(td)} DGN directions"}}
+
+
+def _c4_cpu_child(out_path):
+    """Config-4 cpu_baseline in its own process (spawned before CUDA is initialised):
+    one SGN direction on 1 core; writes JSON to out_path."""
+    _cpu_worker_init(4)
+    dt, tm = _cpu_worker_direction()
+    with open(out_path, "w") as fh:
+        json.dump({"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": "1 SGN direction of config 4 on 1 core (oracle/sgn_cpu.py: SciPy SuperLU + "
+                             "BiCGSTAB restating the reference), run concurrently with the GPU arm",
+                   "median_s": dt, "phases_s": tm,
+                   "dgn": {"value": None, "note": "not attempted: the 121191 x 10000 dense sensitivity matrix "
+                                                  "(9.7 GB) and 10000 sparse solves (BASELINE P5: DGN runs out "
+                                                  "of memory on the shell roof)"}}, fh)
 
 
 WORKLOADS = {1: "config 1: 20x20 neo-Hookean sheet (722 tris), n_p=40",
              2: "config 2: 100x100 neo-Hookean sheet (19602 tris), n_p=400",
-             3: "config 3: 41x11x11 neo-Hookean tet beam (20000 tets)",
-             4: "config 4: 201x201 discrete shell (80000 StVK triangles + 119600 hinges), n_p=10000"}
+             3: "config 3: 41x11x11 neo-Hookean tet beam (20000 tets), n_p=1881",
+             4: "config 4: 201x201 discrete shell (80000 StVK triangles + 119600 hinges), n_p=10000",
+             5: f"config 5: 64 instances of the 100x100 sheet (E ~ U(5e4,2e5), own targets), {C5_ITERS} SGN "
+                f"iterations each with its own Armijo line search"}
 
 
 def run_reference(args):
-    """--impl reference: the oracle port of the reference CPU path on all host cores."""
+    """--impl reference: the oracle port of the reference CPU path on the host cores."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import multiprocessing as mp
-    import numpy as np
     cores = os.cpu_count() or 1
     workers = max(1, min(cores, 64))
-    x = cpu_equilibrium(args.config)
+    steps, warmup = args.steps, args.warmup
+    note = f"each step = {workers} concurrent single-threaded directions (one per worker)"
+    if args.config == 4:
+        # one direction is minutes of SuperLU and several GB: one bounded step, memory-capped
+        try:
+            import psutil
+            workers = max(1, min(workers, int(psutil.virtual_memory().available / 6e9)))
+        except ImportError:
+            workers = max(1, min(workers, 8))
+        steps, warmup = 1, 0
+        note = f"bounded sample: 1 step of {workers} concurrent directions (one per worker, ~6 GB each)"
     ctx = mp.get_context("fork")
-    with ctx.Pool(workers, initializer=_cpu_worker_init, initargs=(args.config,)) as pool:
-        step_t = []
-        for s in range(args.warmup + args.steps):
+    t_all = time.perf_counter()
+    if args.config == 5:
+        # one 20-iteration reference SGN run per worker (instances 1..workers), directions counted
+        with ctx.Pool(workers) as pool:
             t0 = time.perf_counter()
-            pool.map(_cpu_worker_direction, [x] * workers)
-            dt = time.perf_counter() - t0
-            if s >= args.warmup:
-                step_t.append(dt)
-    total = sum(step_t)
-    value = workers * len(step_t) / total
+            res = pool.map(_cpu_worker_minimize, list(range(1, workers + 1)))
+            total = time.perf_counter() - t0
+        n_dir = sum(n for _, n in res)
+        value, step_ms, steps, warmup = n_dir / total, 1e3 * total, 1, 0
+        note = (f"bounded sample: instances 1..{workers} of config 5, one reference minimize "
+                f"({C5_ITERS} iterations) per worker; {n_dir} directions computed")
+    else:
+        with ctx.Pool(workers, initializer=_cpu_worker_init, initargs=(args.config,)) as pool:
+            step_t = []
+            for s_ in range(warmup + steps):
+                t0 = time.perf_counter()
+                pool.map(_cpu_worker_direction, [None] * workers)
+                dt = time.perf_counter() - t0
+                if s_ >= warmup:
+                    step_t.append(dt)
+        total = sum(step_t)
+        value, step_ms = workers * len(step_t) / total, 1e3 * total / len(step_t)
     out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(step_t),
+           "steps": steps, "warmup": warmup, "ms_per_step": step_ms,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (seeded, oracle/configs.py)",
+           "data": "synthetic (seeded, oracle/configs.py, oracle/shell.py)",
            "config": {"workload": WORKLOADS.get(args.config, f"config {args.config}"),
                       "parallelism": f"{workers} single-threaded host processes"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                            "sample": f"each step = {workers} concurrent directions (one per worker)"},
-           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": note},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "wall_s": time.perf_counter() - t_all}
     print(json.dumps(out))
     return 0
 
 
 # ------------------------------------------------------------------------------------ our arm
 def assembly_bytes(pl):
-    """Algorithmic assembly bytes per instance: 8 nnz(tril K_s) + 16 d n_v +
-    4 k n_e + 16 n_p."""
+    """Algorithmic assembly bytes per instance: 8 nnz(tril K_s) written +
+    16 d n_v (x and X read) + 4 k n_e per element group (connectivity) + 16 n_p + 16 per
+    p-map entry (index + coefficient)."""
     import numpy as np
     cols = np.repeat(np.arange(pl.dim), np.diff(pl.K_indptr))
     has_diag = np.zeros(pl.dim, bool)
     has_diag[cols[pl.K_indices == cols]] = True
     shift_rows = np.r_[np.arange(pl.n_x), np.arange(pl.n_x + pl.n_p, pl.dim)]
     nnz_tril = int((pl.K_indices >= cols).sum() + (~has_diag[shift_rows]).sum())   # tril(K_s)
-    return 8 * nnz_tril + 16 * pl.d * pl.n_v + 4 * pl.nv_el * pl.n_e + 16 * pl.n_p
+    conn = sum(4 * g.nv * g.n_e for g in pl.groups)
+    return 8 * nnz_tril + 16 * pl.d * pl.n_v + conn + 16 * pl.n_p + 16 * int(pl.rest_idx.size)
 
 
 def run_ours(args):
+    t_bench = time.perf_counter()
+    rank0_alone = int(os.environ.get("RANK", "0")) == 0 and int(os.environ.get("WORLD_SIZE", "1")) == 1
+    c4_child = None
+    if args.config == 4 and rank0_alone and not args.no_cpu_baseline:
+        # the config-4 CPU direction takes minutes: start it now, in its own process (before
+        # CUDA exists in this one), and collect it after the GPU measurement
+        import tempfile
+        c4_path = os.path.join(tempfile.mkdtemp(prefix="sgn_c4cpu_"), "cpu.json")
+        c4_child = subprocess.Popen([sys.executable, os.path.abspath(__file__), "--cpu-child", c4_path],
+                                    stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
     import numpy as np
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -365,19 +455,39 @@ def run_ours(args):
         "relative_residual": rel_res,
     }
     if refine_note:
-        out["refine"] = dict(refine_note, note="relative residual floor of this KKT system in float64 "
-                             "(sum |K||x| / |b| x eps ~ 1e-9) lies above the 1e-10 contract; the "
-                             "reference's solve_kkt_stabilized raises NoConvergence(best) as well")
-    if rank == 0 and world == 1 and args.config == 4 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "port",
-                               "sample": "skipped: one CPU direction of config 4 exceeds the 30 s sample budget"}
+        out["refine"] = dict(refine_note, note="the refinement raised NoConvergence(best) (timed as run)")
+    if args.config in (1, 2, 3):
+        # the caller-side alternative (reference direction_dgn, optimize.py:168-198) on the device
+        from paper_2107_03285_b200.optimize import direction_dgn
+        direction_dgn(prob, xh, ph_, cfg)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            direction_dgn(prob, xh, ph_, cfg)
+        torch.cuda.synchronize()
+        out["dgn"] = {"value": 3 / (time.perf_counter() - t0), "unit": UNIT,
+                      "note": "device DGN direction (dense reduced Hessian, DMMA GEMM + dense LDL^T), "
+                              "host-timed through direction_dgn with host arrays"}
+    if c4_child is not None:
+        left = args.cpu_budget - (time.perf_counter() - t_bench)
+        try:
+            c4_child.wait(timeout=max(1.0, left))
+            with open(c4_path) as fh:
+                out["cpu_baseline"] = json.load(fh)
+        except (subprocess.TimeoutExpired, OSError, ValueError) as exc:
+            c4_child.kill()
+            out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "port",
+                                   "sample": f"1 SGN direction of config 4 on 1 core did not finish within the "
+                                             f"{args.cpu_budget:.0f} s budget ({type(exc).__name__})"}
     elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            tgt = np.asarray(x)[pl.target_dofs] if args.config == 3 else None   # sagged tip (config 3)
             sample = 1 if args.config == 3 else args.cpu_sample
-            out["cpu_baseline"] = cpu_baseline(args.config, np.asarray(x), sample, tgt)
+            out["cpu_baseline"] = cpu_baseline(args.config, sample)
         except Exception as exc:  # the baseline is reported, never required for the GPU number
             out["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    if out.get("cpu_baseline", {}).get("value"):
+        out["vs_cpu_baseline"] = {"value": value / out["cpu_baseline"]["value"],
+                                  "e2e": e2e_value / out["cpu_baseline"]["value"]}
     if rank == 0:
         print(json.dumps(out))
     if dist is not None:
@@ -397,8 +507,11 @@ def ncu_traffic(config):
 
 
 def run_batch(args):
-    """--config 5: 64 instances of the 100x100 sheet partitioned over the ranks; every rank
-    runs its instances as one device batch; one all-gather of dp at the end (NCCL)."""
+    """--config 5: 64 instances of the 100x100 sheet partitioned over the ranks; each rank
+    runs its instances as one device batch through C5_ITERS SGN iterations with per-instance
+    Armijo line searches (batch.minimize_batched); one all-gather of the per-instance
+    trajectories, termination codes and direction counts at the end (NCCL).  A step is
+    one whole batched run from p0; value = directions computed (all ranks) / max time."""
     import numpy as np
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -409,86 +522,80 @@ def run_batch(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
+    from paper_2107_03285_b200 import OptimizerConfig
     from paper_2107_03285_b200._lib import lib
-    from paper_2107_03285_b200.batch import gather_instances, partition
-    from paper_2107_03285_b200.engine import sgn_solve_stages
+    from paper_2107_03285_b200.batch import BatchRun, gather_instances, minimize_batched, partition
     from paper_2107_03285_b200.problems import build_sheet_batch
     n_total = 64
     rows = partition(n_total, world, rank)
     bd = build_sheet_batch(2, 0, instances=[1 + i for i in rows])
-    X, status = bd.simulate(bd.p0)                   # batched device Newton (setup)
-    eng = bd.engine
-    bd.load(X, bd.p0)
+    cfg = OptimizerConfig(method="sgn", max_iterations=C5_ITERS, gradient_tolerance=1e-12)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
-    for _ in range(args.warmup):
-        bd.directions()
+    warmup, steps = max(1, min(args.warmup, 1)), max(1, min(args.steps, 3))
+    for _ in range(warmup):
+        minimize_batched(bd, bd.p0, cfg)
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     sampler = ClockSampler(local)
     sampler.start()
     l0 = lib().sgn_launch_count()
-    ms, ams = [], []
-    for _ in range(args.steps):
+    ms, ndirs, runs, host_s = [], [], [], []
+    for _ in range(steps):
         flush.zero_()
-        e0, ea, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0 = time.perf_counter()
         e0.record()
-        eng.assemble()
-        ea.record()
-        sgn_solve_stages(eng, None)
+        run = minimize_batched(bd, bd.p0, cfg)            # host inputs in, trajectories out
         e1.record()
         torch.cuda.synchronize()
+        host_s.append(time.perf_counter() - h0)
         ms.append(e0.elapsed_time(e1))
-        ams.append(e0.elapsed_time(ea))
+        ndirs.append(int(run.directions.sum()))
+        runs.append(run)
     launches = lib().sgn_launch_count() - l0
     clocks = sampler.stop()
-    tmax = torch.tensor([sum(ms)], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([sum(ms), float(sum(ndirs))], dtype=torch.float64, device="cuda")
     if dist is not None:
+        tmax = tot[:1].clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    total_ms = float(tmax.item())
-    value = n_total * args.steps / (total_ms * 1e-3)
-    # e2e: host x, p in -> batched directions -> dp back to host (every step)
-    xs, ps = np.asarray(X), np.asarray(bd.p0)
-    t0 = time.perf_counter()
-    e2e_steps = max(2, min(args.steps, 5))
-    for _ in range(e2e_steps):
-        bd.load(xs, ps)
-        bd.directions()
-        dp = eng.sol[:, bd.n_x:bd.n_x + bd.n_p].cpu().numpy()
-    e2e_s = time.perf_counter() - t0
-    et = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    a_ms = statistics.median(ams)
-    a_bytes = len(rows) * assembly_bytes(bd.plan)
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s (B200_PROFILING.md)"
-    # the single collective: gather every instance's dp on every rank
-    tg = time.perf_counter()
-    if dist is not None:
-        full = gather_instances(dp, n_total, world, rank, device="cuda")
+        dsum = tot[1:].clone()
+        dist.all_reduce(dsum, op=dist.ReduceOp.SUM)
+        total_ms, total_dirs = float(tmax.item()), float(dsum.item())
     else:
-        full = dp
+        total_ms, total_dirs = float(tot[0].item()), float(tot[1].item())
+    value = total_dirs / (total_ms * 1e-3)
+    ht = torch.tensor([sum(host_s)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(ht, op=dist.ReduceOp.MAX)
+    e2e_value = total_dirs / float(ht.item())
+    # the single collective: every instance's packed trajectory row on every rank
+    tg = time.perf_counter()
+    packed = runs[-1].pack()
+    full = gather_instances(packed, n_total, world, rank, device="cuda") if dist is not None else packed
     gather_ms = (time.perf_counter() - tg) * 1e3
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+    terms = {}
+    for r in range(full.shape[0]):
+        t = BatchRun.unpack_row(full[r], C5_ITERS)["termination"]
+        terms[t] = terms.get(t, 0) + 1
+    tm = runs[-1].timings
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+           "warmup": warmup, "ms_per_step": total_ms / steps, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded, config-5 instances of oracle/configs.py)",
-           "config": {"workload": "config 5: 64 instances of the 100x100 sheet (E ~ U(5e4,2e5), own targets), "
-                                  "one SGN direction per instance per step",
+           "config": {"workload": WORKLOADS[5],
                       "parallelism": f"instances partitioned {n_total // world}/rank, batched per device",
-                      "l2": "flushed before every timed step", "instances_per_rank": len(rows)},
-           "e2e": {"value": n_total * e2e_steps / float(et.item()), "unit": UNIT,
-                   "h2d_bytes_per_step": 8 * len(rows) * (bd.n_x + bd.n_p),
-                   "d2h_bytes_per_step": 8 * len(rows) * bd.n_p},
+                      "l2": "flushed before every timed step", "instances_per_rank": len(rows),
+                      "step": f"one batched {C5_ITERS}-iteration SGN run from p0 (directions + line-search "
+                              f"forward solves + adjoint gradients), host p0 in, trajectories out"},
+           "directions_per_step": total_dirs / steps,
+           "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * len(rows) * (bd.n_x + bd.n_p),
+                   "d2h_bytes_per_step": int(packed.nbytes),
+                   "note": "host wall clock of the same steps: host p0 in, trajectories out"},
+           "phases_s_per_run": {k: v for k, v in tm.items()},
+           "terminations": terms,
            "gather": {"ms": gather_ms, "bytes": int(full.nbytes), "rows": int(full.shape[0])},
-           "phases": {"assemble": {"ms": a_ms, "bound": "hbm", "algorithmic_bytes": a_bytes,
-                                   "achieved_gbs": a_bytes / (a_ms * 1e-3) / 1e9,
-                                   "frac": a_bytes / (a_ms * 1e-3) / 1e9 / hbm_peak,
-                                   "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,
-                                   "note": f"{len(rows)} instances per launch; median over steps"}},
            "clocks": clocks, "gpu_launches": int(launches)}
     if rank == 0:
         print(json.dumps(out))
@@ -500,6 +607,9 @@ def run_batch(args):
 
 def main():
     args = parse()
+    if args.cpu_child:
+        _c4_cpu_child(args.cpu_child)
+        return 0
     if args.impl == "reference":
         return run_reference(args)
     if args.config == 5:
