@@ -262,7 +262,8 @@ int  sgn_gather_values(int64_t n_out, int32_t batch, const double* d_base, int64
  * energies and norms (sensitivity.py:83-85, forward.py:149,189-203).                */
 int  sgn_reduce(int32_t op, int64_t n, int32_t batch, const double* d_a, const double* d_b,
                 int64_t stride, double* d_out, void* stream);
-/* out = y + alpha[b] * x  (per-instance step length; forward.py:197-199, optimize.py:472) */
+/* out = y + alpha[b] * x  (per-instance step length; forward.py:197-199, optimize.py:472);
+ * d_y = NULL: out = alpha[b] * x (out may alias x)                                    */
 int  sgn_axpy(int64_t n, int32_t batch, const double* d_alpha, const double* d_x,
               const double* d_y, double* d_out, int64_t stride, void* stream);
 /* dst[b] = src[b] for every instance b with mask[b] != 0 (per-instance acceptance in the
@@ -287,6 +288,13 @@ typedef struct {
 } sgn_lsq_args;
 int  sgn_lsq_eval(int32_t batch, const sgn_lsq_args* args, const double* d_x, const double* d_p,
                   double* d_vec, double* d_fobj, void* stream);
+/* rest-length residual blocks of 2-D springs (reference spring bar regularizer,
+ * spring_bar.py:159-184): per spring s (conn 2 x int32, rest positions d_rest, L0 rest
+ * lengths at p0), 21 doubles at d_out + s*21: w j j^T (4x4), w r j (4), r^2 with
+ * r = |X_a - X_b| - L0_s and j = dr/d(X_a, X_b).                                        */
+int  sgn_restlen_blocks(int64_t ns, int32_t batch, const int32_t* d_conn, const double* d_rest,
+                        int64_t rest_stride, const double* d_L0, double w, double* d_out,
+                        int64_t out_stride, void* stream);
 /* adjoint gradient from a leading-block KKT solve (sensitivity.py:181-198, 245-256):
  * mode 0: d_out = (0, 0, d_src[lambda]);  mode 1: g = d_fvec[p] - d_src[p] (d_src = K v),
  * d_out = (0, -g, 0), d_grad = g;  mode 2: d_out = (0, 0, w) for an n_x-vector w = d_src;

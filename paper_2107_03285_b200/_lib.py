@@ -99,6 +99,7 @@ SIGNATURES = {
     "sgn_axpy": (ctypes.c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "sgn_fp64_peak": (ctypes.c_int, [c_i32, c_i32, P_dbl, c_vp]),
     "sgn_lsq_eval": (ctypes.c_int, [c_i32, ctypes.c_void_p, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "sgn_restlen_blocks": (ctypes.c_int, [c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_dbl, c_vp, c_i64, c_vp]),
     "sgn_adjoint_step": (ctypes.c_int, [c_i32, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 

@@ -89,6 +89,7 @@ def minimize_batched(bd, p0, cfg, max_iterations: int | None = None) -> BatchRun
     from .errors import ForwardSimFailure, NoConvergence
     eng = bd.engine
     torch = eng.torch
+    nvtx = torch.cuda.nvtx
     B, n_x, n_p = bd.B, bd.n_x, bd.n_p
     iters = cfg.max_iterations if max_iterations is None else int(max_iterations)
     eng.stab = cfg.stabilization
@@ -144,6 +145,7 @@ def minimize_batched(bd, p0, cfg, max_iterations: int | None = None) -> BatchRun
         if not active.any():
             break
         # one batched SGN direction at every instance's (x, p)
+        nvtx.range_push("sgn.batch.direction")
         td = time.perf_counter()
         eng.x.copy_(x_cur)
         eng.p.copy_(p_cur)
@@ -154,6 +156,7 @@ def minimize_batched(bd, p0, cfg, max_iterations: int | None = None) -> BatchRun
         dp.copy_(eng.sol[:, n_x:n_x + n_p])
         ndir += active
         timings["direction_s"] += time.perf_counter() - td
+        nvtx.range_pop()
         dpn, gdp = dot(dp, dp), dot(g, dp)
         for b in np.flatnonzero(active & (dpn == 0.0)):
             term[b] = "stationary"
@@ -164,6 +167,7 @@ def minimize_batched(bd, p0, cfg, max_iterations: int | None = None) -> BatchRun
         if not active.any():
             break
         # per-instance Armijo backtracking; all pending trial points in one masked batch
+        nvtx.range_push("sgn.batch.line_search")
         tl = time.perf_counter()
         alpha = np.ones(B)
         pending = active.copy()
@@ -194,6 +198,7 @@ def minimize_batched(bd, p0, cfg, max_iterations: int | None = None) -> BatchRun
                     pending &= ~acc
             alpha = np.where(pending, alpha * cfg.backtrack_factor, alpha)
         timings["line_search_s"] += time.perf_counter() - tl
+        nvtx.range_pop()
         for b in np.flatnonzero(pending):
             term[b] = "line_search_failure"
         accepted = active & ~pending

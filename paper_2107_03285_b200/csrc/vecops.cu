@@ -54,7 +54,7 @@ __global__ void k_axpy(int64_t n, const double* __restrict__ alpha, const double
   const double a = alpha[b];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = (int64_t)b * stride + i;
-    out[k] = y[k] + a * x[k];
+    out[k] = (y ? y[k] : 0.0) + a * x[k];
   }
 }
 
@@ -138,6 +138,32 @@ k_lsq_params(int64_t n_x, int64_t n_p, int64_t nt, int nbt, double w_reg, const 
   for (int k = 0; k < nbt; ++k) t += __ldcg(pp + k);
   for (int k = 0; k < (int)gridDim.x; ++k) t += __ldcg(pp + kLsqBlocks + k);
   if (fobj) fobj[b] = 0.5 * t;
+}
+
+// Rest-length residuals of 2-D springs (the reference spring bar's regularizer,
+// spring_bar.py:159-184): r_s = |X_a - X_b| - L0_s, j_s = dr_s/dX = (d, -d), d the unit
+// rest direction.  Per spring, out = [w j j^T (4 x 4, row-major) | w r j (4) | r^2], the
+// element blocks the KKT gather sums into C = J_p^T W J_p and the f_p gather into w J_p^T r.
+__global__ void k_restlen(int64_t ns, const int32_t* __restrict__ conn, const double* __restrict__ rest,
+                          int64_t vstride, const double* __restrict__ L0, double w, double* __restrict__ out,
+                          int64_t ostride) {
+  const int b = blockIdx.y;
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= ns) return;
+  const double* X = rest + (int64_t)b * vstride;
+  const int va = conn[2 * s], vb = conn[2 * s + 1];
+  const double dx = X[2 * va] - X[2 * vb], dy = X[2 * va + 1] - X[2 * vb + 1];
+  const double len = sqrt(dx * dx + dy * dy);
+  const double r = len - L0[s];
+  const double j[4] = {dx / len, dy / len, -dx / len, -dy / len};
+  double* o = out + (int64_t)b * ostride + s * 21;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) o[u * 4 + v] = w * j[u] * j[v];
+    o[16 + u] = w * r * j[u];
+  }
+  o[20] = r * r;
 }
 
 // mode 0: v = (0, 0, src_lambda)
@@ -243,6 +269,17 @@ int sgn_lsq_eval(int32_t batch, const sgn_lsq_args* a, const double* d_x, const 
                                                          a->rscr, a->part);
   k_lsq_params<<<dim3(nbp, batch), kLsqThreads, 0, st>>>(n_x, n_p, nt, nbt, a->w_reg, d_p, d_vec, d_fobj, a->rtptr,
                                                         a->rtidx, a->rtcoef, a->rscr, a->part, a->tickets);
+  VEC_CHECK();
+  return SGN_OK;
+}
+
+int sgn_restlen_blocks(int64_t ns, int32_t batch, const int32_t* d_conn, const double* d_rest,
+                       int64_t rest_stride, const double* d_L0, double w, double* d_out, int64_t out_stride,
+                       void* stream) {
+  if (ns == 0) return SGN_OK;
+  sgn::count_launch();
+  k_restlen<<<dim3((unsigned)((ns + 127) / 128), batch), 128, 0, (cudaStream_t)stream>>>(
+      ns, d_conn, d_rest, rest_stride, d_L0, w, d_out, out_stride);
   VEC_CHECK();
   return SGN_OK;
 }

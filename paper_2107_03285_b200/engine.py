@@ -78,8 +78,12 @@ class MeshPlan:
     """Host precomputation for one mesh / parameterization (shared by all instances)."""
 
     def __init__(self, X0, conn, kind, fixed_verts, pmap, target_dofs, w_target, w_reg,
-                 f_ext=None, rest_base=None, groups=None, R=None, disp_scale=None):
-        """disp_scale = sigma selects the displacement state: x = (pos - X(p)) / sigma on the free
+                 f_ext=None, rest_base=None, groups=None, R=None, disp_scale=None, restlen=None):
+        """restlen = (springs [n_s x 2], L0 [n_s], w) adds the reference spring bar's rest-length
+        residuals r_s = L_s(X(p)) - L0_s with weight w (spring_bar.py:159-184): C = J_p^T W J_p
+        and f_p = J_p^T W r come from per-spring blocks (sgn_restlen_blocks) at every evaluation.
+
+        disp_scale = sigma selects the displacement state: x = (pos - X(p)) / sigma on the free
         dofs (fixed dofs stay at X0).  Then G_x = sigma * dc/dpos, the G_p block gains the
         element-Hessian terms of the free dofs the p-map moves (dc/dp at fixed x), and the
         least-squares residual of a target is sigma * x.  Without it x = positions."""
@@ -100,6 +104,12 @@ class MeshPlan:
             self.groups.append(g)
             hoff += g.size
             goff += g.n_e * g.nd
+        self.restlen = None
+        if restlen is not None:
+            rs, rL0, rw = restlen
+            self.restlen = (np.asarray(rs, dtype=np.int64), np.asarray(rL0, dtype=np.float64), float(rw))
+            self.rl_off = hoff
+            hoff += 21 * len(rs)
         self.ebuf_size, self.egrad_size = hoff, goff
         g0 = self.groups[0]
         self.conn, self.kind, self.elem_code = g0.conn, g0.kind, g0.code     # single-group aliases
@@ -214,6 +224,40 @@ class MeshPlan:
             crow.append(n_x + CtC.row); ccol.append(n_x + CtC.col); cval.append(CtC.data)
         if self.w_reg > 0.0:
             crow.append(n_x + np.arange(n_p)); ccol.append(n_x + np.arange(n_p)); cval.append(np.full(n_p, self.w_reg))
+        if self.restlen is not None:
+            # C block from the per-spring blocks w j j^T; f_p lists from w r j (KKT order)
+            rs = self.restlen[0]
+            ns_ = len(rs)
+            rdof = np.stack([2 * rs[:, 0], 2 * rs[:, 0] + 1, 2 * rs[:, 1], 2 * rs[:, 1] + 1], axis=1)  # (ns, 4)
+            s_idx = np.repeat(np.arange(ns_), 4)
+            u_idx = np.tile(np.arange(4), ns_)
+            d_ = rdof.ravel()
+            cnt = rp[d_ + 1] - rp[d_]
+            sel = np.flatnonzero(cnt)
+            rep_ = cnt[sel]
+            t = np.repeat(sel, rep_)
+            offs = np.arange(int(rep_.sum())) - np.repeat(np.cumsum(rep_) - rep_, rep_)
+            kk = rp[d_[t]] + offs
+            e_s, e_u, e_p, e_c = s_idx[t], u_idx[t], self.rest_idx[kk], self.rest_coef[kk]   # (spring, slot, p, coef)
+            # pairs of entries of the same spring: C[p_i, p_j] += c_i c_j (w j j^T)[u_i, u_j]
+            order = np.argsort(e_s, kind="stable")
+            e_s, e_u, e_p, e_c = e_s[order], e_u[order], e_p[order], e_c[order]
+            starts = np.searchsorted(e_s, np.arange(ns_))
+            ends = np.searchsorted(e_s, np.arange(ns_), side="right")
+            pr, pc, ps, pcf = [], [], [], []
+            for s_ in range(ns_):
+                a0, a1 = starts[s_], ends[s_]
+                for i_ in range(a0, a1):
+                    for j_ in range(a0, a1):
+                        pr.append(n_x + e_p[i_]); pc.append(n_x + e_p[j_])
+                        ps.append(self.rl_off + 21 * s_ + 4 * e_u[i_] + e_u[j_]); pcf.append(e_c[i_] * e_c[j_])
+            rows = np.concatenate([rows, np.asarray(pr, dtype=np.int64)])
+            cols = np.concatenate([cols, np.asarray(pc, dtype=np.int64)])
+            src = np.concatenate([src, np.asarray(ps, dtype=np.int64)])
+            coef = np.concatenate([coef, np.asarray(pcf, dtype=np.float64)])
+            self.rl_fptr, self.rl_fsrc, self.rl_fcoef = _csr_from_lists(
+                n_p, e_p, self.rl_off + 21 * e_s + 16 + e_u, e_c)
+            self.rl_rsrc = self.rl_off + 21 * np.arange(ns_, dtype=np.int64) + 20
         crow, ccol, cval = np.concatenate(crow), np.concatenate(ccol), np.concatenate(cval)
         all_r = np.concatenate([rows, crow])
         all_c = np.concatenate([cols, ccol])
@@ -578,6 +622,15 @@ class DeviceEngine:
         self.K_src, self.K_coef = T(pl.K_src, i64), T(pl.K_coef)
         self.G_ptr, self.G_src = T(pl.G_ptr, i64), T(pl.G_src, i64)
         self.G_coef = None if pl.G_coef is None else T(pl.G_coef)
+        if pl.restlen is not None:
+            self.rl_conn = T(pl.restlen[0].astype(np.int32), torch.int32)
+            self.rl_L0 = T(pl.restlen[1])
+            self.rl_fptr, self.rl_fsrc, self.rl_fcoef = T(pl.rl_fptr, i64), T(pl.rl_fsrc, i64), T(pl.rl_fcoef)
+            self.rl_rptr = T(np.array([0, pl.rl_rsrc.size]), i64)
+            self.rl_rsrc = T(pl.rl_rsrc, i64)
+            self.rl_half = T(np.full(pl.rl_rsrc.size, 0.5))
+            self.rl_obj = torch.zeros(B, 1, dtype=f64, device=dev)
+            self.rl_w = torch.full((B,), pl.restlen[2], dtype=f64, device=dev)
         self.G_diag = T(pl.G_diag, i64)
         self.grad_base, self.grad_ptr, self.grad_src = T(pl.grad_base), T(pl.grad_ptr, i64), T(pl.grad_src, i64)
         self.f_ext = T(pl.f_ext)
@@ -732,8 +785,17 @@ class DeviceEngine:
             self._gx_ready = True
             return
         self.element_blocks()
+        self._restlen_blocks()
         self._gather(pl.nnz, self.K_base, 0, self.K_ptr, self.K_src, self.K_coef, self.ebuf,
                      self.ebuf.stride(0), self.kvals, pl.nnz)
+
+    def _restlen_blocks(self):
+        pl = self.plan
+        if pl.restlen is None:
+            return
+        check(lib().sgn_restlen_blocks(len(pl.restlen[0]), self.batch, ptr(self.rl_conn), ptr(self.rest), pl.n_dof,
+                                       ptr(self.rl_L0), pl.restlen[2], ptr(self.ebuf[:, pl.rl_off:]),
+                                       self.ebuf.stride(0), self.stream))
 
     def gx_values(self, force: bool = False):
         """G_x = dc/dx values (generic pattern) at the current positions into self.gvals."""
@@ -763,22 +825,29 @@ class DeviceEngine:
         solve_kkt_stabilized when any instance's refinement stalls.
         """
         torch = self.torch
+        nvtx = torch.cuda.nvtx
         graphs = self._direction_graphs()
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record()
+        nvtx.range_push("sgn.assemble")
         if graphs is not None:
             # assembly, then KKT factor || adjoint + right-hand side: two graph launches
             # instead of ~30 kernel / memset launches issued from Python
             graphs[0].replay()
             e1.record()
+            nvtx.range_pop()
+            nvtx.range_push("sgn.factor+adjoint")
             graphs[1].replay()
             e2.record()
         else:
             self.assemble()
             e1.record()
+        nvtx.range_pop()
+        nvtx.range_push("sgn.refined_solve")
         try:
             return sgn_solve_stages(self, timings, pre_done=graphs is not None)
         finally:
+            nvtx.range_pop()
             if timings is not None:       # device events, read after the refinement's sync
                 e1.synchronize()
                 timings["assemble_s"] = e0.elapsed_time(e1) * 1e-3
@@ -861,6 +930,17 @@ class DeviceEngine:
             self._lsq_args = a
         check(lib().sgn_lsq_eval(self.batch, ctypes.byref(self._lsq_args), ptr(x), ptr(self.p), ptr(fvec),
                                  ptr(self.fobj), self.stream))
+        if pl.restlen is not None:
+            # rest-length residuals: f_p += w J_p^T r (gather over each p's springs), f += w/2 sum r^2
+            self._restlen_blocks()
+            if fvec is not None:
+                fp = fvec[:, pl.n_x:]
+                self._gather(pl.n_p, fp, pl.dim, self.rl_fptr, self.rl_fsrc, self.rl_fcoef, self.ebuf,
+                             self.ebuf.stride(0), fp, pl.dim)
+            self._gather(1, None, 0, self.rl_rptr, self.rl_rsrc, self.rl_half, self.ebuf, self.ebuf.stride(0),
+                         self.rl_obj, 1)
+            check(lib().sgn_axpy(1, self.batch, ptr(self.rl_w), ptr(self.rl_obj), ptr(self.fobj), ptr(self.fobj), 1,
+                                 self.stream))
 
     # -- objective ---------------------------------------------------------------------
     def objective(self, x=None):
@@ -979,7 +1059,11 @@ class DeviceEngine:
         tau0 = 1e-6 * np.abs(trace) / max(n, 1) + 1e-12
         tau = np.where(bias, tau0 * 1e6, 0.0) * np.ones(B)
         done = ~np.asarray(mask, bool)
-        neg = torch.neg(self.gx)
+        if not hasattr(self, "_neg1"):
+            self._neg1 = torch.full((B,), -1.0, dtype=torch.float64, device="cuda")
+            self._negg = torch.empty_like(self.gx)
+        neg = self._negg
+        check(lib().sgn_axpy(n, B, ptr(self._neg1), ptr(self.gx), None, ptr(neg), n, st))   # -g
         dots = torch.empty(B, dtype=torch.float64, device="cuda")
         amax = torch.empty(B, dtype=torch.float64, device="cuda")
         for _ in range(60):

@@ -293,6 +293,7 @@ class DeviceReducedOperator:
         self.kp, self.ki = eng._kpat
         E = lambda n: torch.empty(n, dtype=torch.float64, device="cuda")
         self.y, self.gy, self.t, self.u, self.u2, self.w = E(self.n_p), E(self.n_x), E(self.n_x), E(self.n_x), E(self.n_x), E(self.n_x)
+        self.pm1 = torch.tensor([1.0, -1.0], dtype=torch.float64, device="cuda")   # axpy step lengths
         self.r1, self.r2, self.r3 = E(self.n_p), E(self.n_p), E(self.n_p)
         self.applications = 0
 
@@ -308,16 +309,22 @@ class DeviceReducedOperator:
         self.y.copy_(self.torch.from_numpy(np.ascontiguousarray(yv, dtype=np.float64)))
         self._spmm(lam0, n_x, p0, n_p, self.y, self.gy, st)                   # G_p y
         self.eng.gfac.solve(self.gy.view(1, -1), self.t.view(1, -1), False, st)
-        self.t.neg_()                                                           # t = S y
+        self._axpy(1, self.t, None, self.t, n_x, st)                          # t = S y = -G_x^{-1} G_p y
         self._spmm(0, n_x, 0, n_x, self.t, self.u, st)                         # A t
         self._spmm(0, n_x, p0, n_p, self.y, self.u2, st)                       # B^T y
-        self.u.add_(self.u2)
+        self._axpy(0, self.u2, self.u, self.u, n_x, st)
         self.eng.gfac.solve(self.u.view(1, -1), self.w.view(1, -1), False, st)   # G_x^{-T} u
         self._spmm(p0, n_p, lam0, n_x, self.w, self.r1, st)                    # G_p^T w
         self._spmm(p0, n_p, 0, n_x, self.t, self.r2, st)                       # B t
         self._spmm(p0, n_p, p0, n_p, self.y, self.r3, st)                      # C y
-        self.r2.sub_(self.r1).add_(self.r3)
+        self._axpy(1, self.r1, self.r2, self.r2, n_p, st)
+        self._axpy(0, self.r3, self.r2, self.r2, n_p, st)
         return self.r2.cpu().numpy()
+
+    def _axpy(self, sign, x, y, out, n, st):
+        """out = y + (+1 | -1) x on the device (sgn_axpy; sign 0: +1, 1: -1; y None: 0)."""
+        self._check(self._lib().sgn_axpy(n, 1, self._ptr(self.pm1[sign:]), self._ptr(x),
+                                         self._ptr(y) if y is not None else None, self._ptr(out), n, st))
 
 
 def cg_reduced(op, rhs: np.ndarray, eta: float = 1e-3, max_iters: int | None = None):

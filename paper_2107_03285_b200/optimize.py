@@ -192,7 +192,9 @@ def direction_dgn(prob, x, p, cfg: OptimizerConfig, grad=None) -> SearchDirectio
     check(lib().sgn_csc_block_dense(dim, ptr(d["kp"]), ptr(d["ki"]), ptr(kv), n_x + n_p, n_x, n_x, n_p,
                                     ptr(d["GP"]), st))                      # G_p, column j = RHS j
     eng.gfac.solve_multi(d["GP"], d["S"], st)
-    d["S"].neg_()
+    if "neg1" not in d:
+        d["neg1"] = torch.full((n_p,), -1.0, dtype=torch.float64, device="cuda")
+    check(lib().sgn_axpy(n_x, n_p, ptr(d["neg1"]), ptr(d["S"]), None, ptr(d["S"]), n_x, st))   # S = -G_x^{-1} G_p
     sync()
     t_sens = time.perf_counter() - t0
     # H = S^T A S + B S + (B S)^T + C

@@ -20,7 +20,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from ..engine import DeviceEngine, MeshPlan
-from ..errors import CapabilityMissing, ForwardSimFailure
+from ..errors import ForwardSimFailure
 from ..sparse import CscMatrix
 
 __all__ = ["ElasticDesignProblem", "BatchedDesign", "beam_spec", "build_beam", "build_sheet", "build_sheet_batch",
@@ -33,9 +33,10 @@ class ElasticDesignProblem:
     def __init__(self, X0, conn, kind, fixed_verts, pmap, target_dofs, target_vals, w_target=1.0,
                  w_reg=0.0, E=1.0, nu=0.3, gload=0.0, stiffness=None, scale=None, tol=1e-12,
                  f_ext=None, rest_base=None, p_offset=None, name=None, stab=None, groups=None,
-                 group_params=None, R=None, disp_scale=None):
+                 group_params=None, R=None, disp_scale=None, restlen=None):
         self.plan = MeshPlan(X0, conn, kind, fixed_verts, pmap, target_dofs, w_target, w_reg,
-                             f_ext=f_ext, rest_base=rest_base, groups=groups, R=R, disp_scale=disp_scale)
+                             f_ext=f_ext, rest_base=rest_base, groups=groups, R=R, disp_scale=disp_scale,
+                             restlen=restlen)
         self.x_scale = 1.0 if disp_scale is None else float(disp_scale)
         mu, lam = (E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu)))
         sc = (1.0 / E) if scale is None else float(scale)
@@ -136,13 +137,27 @@ class ElasticDesignProblem:
         out = [r]
         if pl.w_reg > 0.0:
             out.append(np.asarray(p, dtype=np.float64).copy())
+        if pl.restlen is not None:
+            sp_, L0, _ = pl.restlen
+            X = self._rest_host(p)
+            out.append(np.linalg.norm(X[sp_[:, 0]] - X[sp_[:, 1]], axis=1) - L0)
         return np.concatenate(out)
+
+    def _rest_host(self, p):
+        """Rest positions X(p) on the host (contract accessors only)."""
+        pl = self.plan
+        X = pl.rest_base.copy()
+        rows = np.repeat(np.arange(pl.n_dof), np.diff(pl.rest_ptr))
+        np.add.at(X, rows, pl.rest_coef * np.asarray(p, dtype=np.float64)[pl.rest_idx])
+        return X.reshape(pl.n_v, pl.d)
 
     def weights(self):
         pl = self.plan
         w = [np.full(pl.target_dofs.size, pl.w_target)]
         if pl.w_reg > 0.0:
             w.append(np.full(pl.n_p, pl.w_reg))
+        if pl.restlen is not None:
+            w.append(np.full(len(pl.restlen[0]), pl.restlen[2]))
         return np.concatenate(w)
 
     def residual_jac_x(self, x, p):
@@ -151,15 +166,31 @@ class ElasticDesignProblem:
         sel = sp.csc_matrix((np.full(nt, self.x_scale), (np.arange(nt), pl.target_dofs)), shape=(nt, pl.n_x))
         if pl.w_reg > 0.0:
             sel = sp.vstack([sel, sp.csc_matrix((pl.n_p, pl.n_x))], format="csc")
+        if pl.restlen is not None:
+            sel = sp.vstack([sel, sp.csc_matrix((len(pl.restlen[0]), pl.n_x))], format="csc")
         return CscMatrix.from_scipy(sel)
 
     def residual_jac_p(self, x, p):
         pl = self.plan
         nt = pl.target_dofs.size
         top = -self.R if self.R is not None else sp.csc_matrix((nt, pl.n_p))
+        blocks = [top]
         if pl.w_reg > 0.0:
-            return CscMatrix.from_scipy(sp.vstack([top, sp.identity(pl.n_p, format="csc")], format="csc"))
-        return CscMatrix.from_scipy(sp.csc_matrix(top))
+            blocks.append(sp.identity(pl.n_p, format="csc"))
+        if pl.restlen is not None:
+            sp_ = pl.restlen[0]
+            X = self._rest_host(p)
+            d = X[sp_[:, 0]] - X[sp_[:, 1]]
+            dh = d / np.linalg.norm(d, axis=1)[:, None]
+            ns_ = len(sp_)
+            s_idx = np.repeat(np.arange(ns_), 2)
+            ca = (sp_[:, 0][:, None] * 2 + np.arange(2)).ravel()
+            cb = (sp_[:, 1][:, None] * 2 + np.arange(2)).ravel()
+            dldX = sp.csr_matrix((np.concatenate([dh.ravel(), -dh.ravel()]),
+                                  (np.concatenate([s_idx, s_idx]), np.concatenate([ca, cb]))), shape=(ns_, pl.n_dof))
+            P = sp.csr_matrix((pl.rest_coef, pl.rest_idx, pl.rest_ptr), shape=(pl.n_dof, pl.n_p))
+            blocks.append(sp.csc_matrix(dldX @ P))
+        return CscMatrix.from_scipy(sp.vstack(blocks, format="csc") if len(blocks) > 1 else sp.csc_matrix(top))
 
     def objective(self, x, p) -> float:
         self._load(x, p)
@@ -297,12 +328,11 @@ def build_spring_bar(n_w: int, n_h: int, w_reg: float = 0.0, stiffness: float = 
                      x_target=None, **kw):
     """The reference spring lattice (spring_bar.py:30-207) on the GPU kernels.
 
-    Parameters are the rest positions of the free vertices (n_p == n_x).  The
-    rest-length regularizer (w_reg > 0) makes C = Jp^T W Jp depend on p and is not
-    yet on the device path.
+    Parameters are the rest positions of the free vertices (n_p == n_x).  The rest-length
+    regularizer (w_reg > 0: residuals L_s(p) - L0_s, spring_bar.py:159-184) makes
+    C = J_p^T W J_p depend on p; its per-spring blocks are evaluated on the device
+    (sgn_restlen_blocks) at every assembly.
     """
-    if w_reg > 0.0:
-        raise CapabilityMissing("spring-bar rest-length regularizer on the device path")
     if n_w < 2 or n_h < 2:
         raise ValueError("grid must be at least 2x2")
     ix, iy = np.meshgrid(np.arange(n_w), np.arange(n_h), indexing="ij")
@@ -328,11 +358,13 @@ def build_spring_bar(n_w: int, n_h: int, w_reg: float = 0.0, stiffness: float = 
     rest_base = X0.ravel().copy()
     rest_base[free_dofs] = 0.0          # X[free] = p (absolute rest positions)
     x_target = X0[free_verts].ravel() if x_target is None else np.asarray(x_target, dtype=np.float64)
+    L0 = np.linalg.norm(X0[springs[:, 0]] - X0[springs[:, 1]], axis=1)
     prob = ElasticDesignProblem(X0, springs, "spring", np.arange(n_h),
                                 (free_dofs, np.arange(n_x), np.ones(n_x)), np.arange(n_x), x_target,
                                 w_target=1.0 / n_x, w_reg=0.0, E=1.0, stiffness=np.full(len(springs), stiffness),
                                 scale=1.0, tol=1e-10, f_ext=f_ext, rest_base=rest_base,
-                                p_offset=X0[free_verts].ravel(), name="SpringBarProblem", **kw)
+                                p_offset=X0[free_verts].ravel(), name="SpringBarProblem",
+                                restlen=(springs, L0, w_reg) if w_reg > 0.0 else None, **kw)
     return prob
 
 

@@ -72,6 +72,37 @@ def test_spring_bar_minimize_trajectory_matches_reference(cuda):
     np.testing.assert_allclose(run.f_values()[:n], f_ref[:n], rtol=1e-8, atol=1e-14 * f_ref[0])
 
 
+def test_spring_bar_rest_length_regularizer_matches_reference(cuda):
+    """w_reg > 0 (spring_bar.py:159-184): C = J_p^T W J_p and f_p from the device rest-length
+    blocks; the reference's quasi-definite case.  KKT, direction, gradient and
+    the 5-iteration minimize trajectory against the reference golden (8x4, w_reg 1e-2)."""
+    from paper_2107_03285_b200 import OptimizerConfig, adjoint_gradient, direction_sgn, minimize
+    from paper_2107_03285_b200.problems import build_spring_bar
+    g = _gold("spring_bar_8x4_reg.npz")
+    prob = build_spring_bar(8, 4, w_reg=float(g["w_reg"]))
+    p = prob.default_parameters()
+    np.testing.assert_array_equal(p, g["p"])
+    x = prob.simulate(p)
+    assert _rel(x, g["x"]) <= 1e-9
+    K = prob.kkt_matrix(g["x"], p).to_scipy()
+    Kr = _csc(g, "K")
+    assert _rel(_nz(K).toarray(), _nz(Kr).toarray()) <= 1e-12
+    assert (abs(Kr) > 0).multiply(K == 0).nnz == 0
+    assert _rel(adjoint_gradient(prob, g["x"], p), g["grad"]) <= 1e-9
+    r = prob.residuals(g["x"], p)
+    assert abs(prob.objective(g["x"], p) - 0.5 * prob.weights() @ (r * r)) <= 1e-14 * abs(g["f0"])
+    assert abs(prob.objective(g["x"], p) - float(g["f0"])) <= 1e-12 * abs(float(g["f0"]))
+    sd = direction_sgn(prob, g["x"], p, OptimizerConfig())
+    assert sd.relative_residual <= 1e-10
+    assert _rel(sd.dp, g["dp"]) <= 1e-8
+    prob._x_warm = None
+    run = minimize(prob, p, OptimizerConfig(max_iterations=5, gradient_tolerance=1e-12))
+    f_ref = g["traj_f"]
+    n = min(len(f_ref), len(run.f_values()))
+    assert n >= 3
+    np.testing.assert_allclose(run.f_values()[:n], f_ref[:n], rtol=1e-8, atol=1e-14 * f_ref[0])
+
+
 # ---------------------------------------------------------------- neo-Hookean sheet, config 1
 @pytest.fixture(scope="module")
 def sheet1():
