@@ -265,8 +265,12 @@ def solve_static(energy, gradient, hessian, x0, tol, max_iters=200):
         g = gradient(x)
         if np.linalg.norm(g, np.inf) <= tol:
             return x
-        K = hessian(x).tocsc()
         e0 = energy(x)
+        if not (np.isfinite(e0) and np.all(np.isfinite(g))):
+            # every Armijo comparison with a non-finite e0 / slope is false: the 8 escalations
+            # below would all fail and raise (forward.py:155-164) -- fail now, same outcome
+            raise OracleNoConvergence("static: line search failed (non-finite energy)", float("nan"))
+        K = hessian(x).tocsc()
         step = _reg_newton_step(K, g)
         accepted = False
         for _ in range(8):

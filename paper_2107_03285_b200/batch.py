@@ -67,7 +67,7 @@ class BatchRun:
 
 
 TERMINATIONS = ("max_iterations", "gradient_tolerance", "stationary", "no_descent", "line_search_failure",
-                "forward_failure")
+                "forward_failure", "direction_no_convergence")
 
 
 def minimize_batched(bd, p0, cfg, max_iterations: int | None = None) -> BatchRun:
@@ -151,10 +151,16 @@ def minimize_batched(bd, p0, cfg, max_iterations: int | None = None) -> BatchRun
         eng.p.copy_(p_cur)
         try:
             res, _ = eng.direction()
-        except NoConvergence as exc:       # the reference raises too; every row keeps its best
-            res = np.full(B, float(exc.residual))
+        except NoConvergence as exc:
+            res = np.asarray(exc.instance_residuals)
+        # the reference minimize does not catch a direction's NoConvergence (optimize.py:389,
+        # linear_solvers.py:168): that instance's run ends there
+        failed = active & ~(res <= eng.stab.refine_tolerance)
+        for b in np.flatnonzero(failed):
+            term[b] = "direction_no_convergence"
         dp.copy_(eng.sol[:, n_x:n_x + n_p])
         ndir += active
+        active &= ~failed
         timings["direction_s"] += time.perf_counter() - td
         nvtx.range_pop()
         dpn, gdp = dot(dp, dp), dot(g, dp)

@@ -21,7 +21,11 @@ namespace {
 
 constexpr int kRed = 512;
 
+// max that propagates NaN like numpy's norm(., inf) (fmax would drop it)
+__device__ __forceinline__ double nanmax(double a, double b) { return (a != a || b != b) ? (a + b) : fmax(a, b); }
+
 template <int OP>  // 0 sum, 1 dot, 2 max-abs
+
 __global__ void __launch_bounds__(kRed)
 k_reduce(int64_t n, const double* __restrict__ a, const double* __restrict__ b, int64_t stride,
          double* __restrict__ out) {
@@ -34,13 +38,13 @@ k_reduce(int64_t n, const double* __restrict__ a, const double* __restrict__ b, 
     const double v = ab[i];
     if (OP == 0) acc += v;
     else if (OP == 1) acc += v * bb[i];
-    else acc = fmax(acc, fabs(v));
+    else acc = nanmax(acc, fabs(v));
   }
   sh[threadIdx.x] = acc;
   __syncthreads();
   for (int s = kRed / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) {
-      if (OP == 2) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
+      if (OP == 2) sh[threadIdx.x] = nanmax(sh[threadIdx.x], sh[threadIdx.x + s]);
       else sh[threadIdx.x] += sh[threadIdx.x + s];
     }
     __syncthreads();

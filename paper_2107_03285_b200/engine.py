@@ -581,9 +581,11 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
             timings["main_iters"] = its
     if rc2 == _lib.SGN_NO_CONVERGENCE:
         best = eng.sol.cpu().numpy()
-        raise NoConvergence(f"BiCGSTAB refinement stalled at relative residual {res.max():.3e}",
+        exc = NoConvergence(f"BiCGSTAB refinement stalled at relative residual {res.max():.3e}",
                             residual=float(res.max()), iterations=int(its.max()),
                             best=best[0] if eng.batch == 1 else best)
+        exc.instance_residuals, exc.instance_iterations = res, its      # batched callers
+        raise exc
     return res, its
 
 
@@ -901,6 +903,22 @@ class DeviceEngine:
             self.gfac.check(st)
         check(lib().sgn_adjoint_step(3, self.batch, pl.n_x, pl.n_p, ptr(self.fvec), None, ptr(self.xtry), None, st))
         self.gfac.solve(self.xtry, self.kdir, False, st)
+        # one step of iterative refinement, w += G_x^{-1} (f_x - G_x w): the unpivoted LDL^T
+        # of the (ill-conditioned) shell G_x is not backward stable the way SuperLU's
+        # partial pivoting is; the step restores it (config 4: gradient 5e-9 -> <1e-10 of
+        # the reference's)
+        if not hasattr(self, "_adj_r"):
+            torch = self.torch
+            self._adj_r, self._adj_d = torch.empty_like(self.kdir), torch.empty_like(self.kdir)
+            self._adj_pm = torch.tensor([1.0, -1.0], dtype=torch.float64, device="cuda").repeat_interleave(
+                self.batch).reshape(2, self.batch).contiguous()
+        n = pl.n_x
+        self.gfac.spmv(self.gvals, self.kdir, self._adj_r, False, st)                       # G w
+        check(lib().sgn_axpy(n, self.batch, ptr(self._adj_pm[1]), ptr(self._adj_r), ptr(self.xtry),
+                             ptr(self._adj_r), n, st))                                      # f - G w
+        self.gfac.solve(self._adj_r, self._adj_d, False, st)
+        check(lib().sgn_axpy(n, self.batch, ptr(self._adj_pm[0]), ptr(self._adj_d), ptr(self.kdir),
+                             ptr(self.kdir), n, st))                                        # w += d
         check(lib().sgn_adjoint_step(2, self.batch, pl.n_x, pl.n_p, ptr(self.kdir), None, ptr(self.tmp), None, st))
         return np.zeros(self.batch), np.zeros(self.batch, dtype=np.int32)
 
@@ -1028,6 +1046,10 @@ class DeviceEngine:
             if _DEBUG_NEWTON:
                 print(f"[newton] |g|inf {g_inf[:4]} E {e0[:4]} tol {tol:.3e}", flush=True)
             status[run & (g_inf <= tol)] = 1
+            # a non-finite energy or gradient can never pass the energy Armijo test (every
+            # comparison with NaN is false): the reference's 8 shift escalations would all
+            # fail and raise (forward.py:155-164); fail those instances now
+            status[(status == 0) & ~(np.isfinite(e0) & np.isfinite(g_inf))] = -1
             run = status == 0
             if not run.any():
                 break

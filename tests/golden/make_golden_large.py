@@ -61,13 +61,37 @@ def direction_and_trajectory(prob, p0, iters):
     print(f"  direction: |dp| {np.linalg.norm(out['dp']):.6e} res {out['rel_res']:.3e} "
           f"converged {out['converged']} ({time.time() - t0:.0f} s)", flush=True)
     if iters:
+        # the reference minimize does not catch NoConvergence from a direction's refinement
+        # (optimize.py:389 -> linear_solvers.py:168): it raises.  Count the adjoint
+        # evaluations (1 initial + 2 per completed iteration + 1 in the failing direction)
+        # on our own problem object, then rerun to the last completed iteration and record
+        # the termination as "direction_no_convergence".
+        calls = [0]
+        inner_fx = prob.objective_grad_x
+
+        def counted(x_, p_):
+            calls[0] += 1
+            return inner_fx(x_, p_)
+        prob.objective_grad_x = counted
         if hasattr(prob, "_x_warm"):
             prob._x_warm = None
-        run = minimize(prob, np.asarray(p0, np.float64).copy(), cfg)
+        term = None
+        try:
+            run = minimize(prob, np.asarray(p0, np.float64).copy(), cfg)
+        except NoConvergence as exc:
+            done = calls[0] // 2 - 1
+            print(f"  reference minimize raised at iteration {done + 1}: {exc}", flush=True)
+            if hasattr(prob, "_x_warm"):
+                prob._x_warm = None
+            cfg2 = OptimizerConfig(method="sgn", max_iterations=done, gradient_tolerance=1e-12)
+            run = minimize(prob, np.asarray(p0, np.float64).copy(), cfg2)
+            term = "direction_no_convergence"
+            out["traj_fail_residual"] = float(exc.residual)
+        prob.objective_grad_x = inner_fx
         out.update(traj_f=run.f_values(), traj_g=run.grad_norms(),
                    traj_alpha=np.array([r.step_length for r in run.records]),
-                   traj_term=np.array(run.termination), traj_p=run.p)
-        print(f"  trajectory {run.f_values()} {run.termination} ({time.time() - t0:.0f} s)", flush=True)
+                   traj_term=np.array(term or run.termination), traj_p=run.p)
+        print(f"  trajectory {run.f_values()} {term or run.termination} ({time.time() - t0:.0f} s)", flush=True)
     return out
 
 

@@ -67,7 +67,7 @@ def _pack_oracle_runs(instances, iters):
         a = np.full(iters + 1, np.nan)
         n = len(run["f"])
         f[:n], g[:n], a[:n] = run["f"], run["grad_norm"], run["alpha"]
-        extra = run["termination"] in ("line_search_failure", "no_descent", "stationary")
+        extra = run["termination"] in ("line_search_failure", "no_descent", "stationary", "direction_no_convergence")
         rows.append(np.concatenate([f, g, a, [n - 1 + extra, TERMINATIONS.index(run["termination"])]]))
     return np.array(rows).reshape(len(instances), 3 * (iters + 1) + 2)
 
