@@ -188,10 +188,14 @@ def minimize_batched(bd, p0, cfg, max_iterations: int | None = None) -> BatchRun
             run = pending & (slope < 0.0)
             if run.any():
                 eng.x.copy_(x_cur)                                   # warm start x_init = x
+                t_sim = time.perf_counter()
                 try:
                     stat = eng.simulate(bd.tol, active=run)
                 except ForwardSimFailure:                            # B == 1 raises instead
                     stat = np.full(B, -1)
+                timings.setdefault("trials", []).append(
+                    (it, int(run.sum()), int(getattr(eng, "newton_iters", 0)), int((stat == 1).sum()),
+                     time.perf_counter() - t_sim))
                 ok = run & (stat == 1)
                 ft = eng.objective().cpu().numpy()
                 acc = ok & np.isfinite(ft) & (ft <= f + cfg.armijo_c1 * slope)

@@ -1035,10 +1035,12 @@ class DeviceEngine:
         if active is not None:
             status[~np.asarray(active, bool)] = 1
         self.positions()                       # rest positions for the current p
+        self.newton_iters = 0
         for _ in range(max_iters):
             run = status == 0
             if not run.any():
                 break
+            self.newton_iters += 1
             self._energy_grad(self.x)
             check(lib().sgn_reduce(2, n, B, ptr(self.gx), None, n, ptr(self.scal[3]), st))
             sc = self.scal.cpu().numpy()
