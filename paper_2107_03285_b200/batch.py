@@ -66,6 +66,56 @@ class BatchRun:
                     termination=TERMINATIONS[int(row[3 * n + 1])])
 
 
+class _Compactor:
+    """Forward solves of a few pending instances in a smaller engine.
+
+    A batched Newton iteration launches every kernel over the whole batch, so a line search
+    with one straggler instance would pay for all B.  The pending instances' rows (material
+    parameters, p, x) are copied into a simulate-only engine of the next power-of-two batch
+    (its KKT factor is never allocated), solved there and copied back.  Every kernel treats
+    instance rows independently, so the result is bitwise the one the full batch gives."""
+
+    def __init__(self, eng):
+        self.eng, self.pool = eng, {}
+
+    def simulate(self, tol, run):
+        from .engine import DeviceEngine
+        from .errors import ForwardSimFailure
+        eng = self.eng
+        torch = eng.torch
+        B = eng.batch
+        idx = np.flatnonzero(run)
+        k = int(idx.size)
+        size = 1 << max(0, (k - 1).bit_length())
+        if size * 2 > B:                                  # not worth compacting
+            try:
+                return eng.simulate(tol, active=run)
+            except ForwardSimFailure:
+                return np.full(B, -1)
+            finally:
+                self.last_iters = getattr(eng, "newton_iters", 0)
+        sub = self.pool.get(size)
+        if sub is None:
+            params = [gp[:1].repeat(size, 1).cpu().numpy() for gp in eng.gparams]
+            sub = DeviceEngine(eng.plan, params if len(params) > 1 else params[0],
+                               eng.tvals[:1].repeat(size, 1).cpu().numpy(), batch=size, stab=eng.stab)
+            self.pool[size] = sub
+        rows = torch.as_tensor(np.r_[idx, np.full(size - k, idx[0])], device="cuda")
+        for dst, src in zip(sub.gparams, eng.gparams):
+            dst.copy_(src.index_select(0, rows))
+        sub.p.copy_(eng.p.index_select(0, rows))
+        sub.x.copy_(eng.x.index_select(0, rows))
+        try:
+            st = sub.simulate(tol, active=np.arange(size) < k)
+        except ForwardSimFailure:                          # a batch of one raises instead
+            st = np.full(size, -1)
+        self.last_iters = getattr(sub, "newton_iters", 0)
+        eng.x.index_copy_(0, rows[:k], sub.x[:k])
+        status = np.ones(B, dtype=np.int64)
+        status[idx] = st[:k]
+        return status
+
+
 TERMINATIONS = ("max_iterations", "gradient_tolerance", "stationary", "no_descent", "line_search_failure",
                 "forward_failure", "direction_no_convergence")
 
@@ -116,6 +166,8 @@ def minimize_batched(bd, p0, cfg, max_iterations: int | None = None) -> BatchRun
         adjoint_gradient_stage(eng)
         check(lib().sgn_masked_copy(n_p, B, ptr(mask(sel)), ptr(eng.grad), ptr(g), n_p, st))
 
+    compactor = getattr(bd, "_compactor", None) or _Compactor(eng)
+    bd._compactor = compactor
     t0 = time.perf_counter()
     timings = dict(direction_s=0.0, line_search_s=0.0, gradient_s=0.0)
     term = ["max_iterations"] * B
@@ -189,12 +241,9 @@ def minimize_batched(bd, p0, cfg, max_iterations: int | None = None) -> BatchRun
             if run.any():
                 eng.x.copy_(x_cur)                                   # warm start x_init = x
                 t_sim = time.perf_counter()
-                try:
-                    stat = eng.simulate(bd.tol, active=run)
-                except ForwardSimFailure:                            # B == 1 raises instead
-                    stat = np.full(B, -1)
+                stat = compactor.simulate(bd.tol, run)
                 timings.setdefault("trials", []).append(
-                    (it, int(run.sum()), int(getattr(eng, "newton_iters", 0)), int((stat == 1).sum()),
+                    (it, int(run.sum()), int(compactor.last_iters), int((stat == 1).sum()),
                      time.perf_counter() - t_sim))
                 ok = run & (stat == 1)
                 ft = eng.objective().cpu().numpy()

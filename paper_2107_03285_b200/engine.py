@@ -678,7 +678,7 @@ class DeviceEngine:
         # p unknowns can join the nested dissection (p_order 1); otherwise they stay last
         self.ksym = symbolic_for(pl.dim, pl.K_indptr, pl.K_indices, pl.n_x, pl.n_p, pl.n_x,
                                  p_order=1 if pl.w_reg > 0.0 else 0)
-        self.kfac = DeviceFactor(self.ksym, B)
+        self._kfac = None                    # KKT factor storage: allocated on first use
         self._gfac = None
         from .linear_solvers import StabilizationConfig
         self.stab = stab or StabilizationConfig()
@@ -994,6 +994,12 @@ class DeviceEngine:
 
     def _hessian(self):
         self.gx_values(force=True)
+
+    @property
+    def kfac(self):
+        if self._kfac is None:
+            self._kfac = DeviceFactor(self.ksym, self.batch)
+        return self._kfac
 
     @property
     def gfac(self):
