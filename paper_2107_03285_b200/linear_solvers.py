@@ -149,9 +149,13 @@ def _augmented(m: CscMatrix) -> CscMatrix:
 class SparseFactorization:
     """Sparse factorization of a square matrix on the device (replaces linear_solvers.py:61-97).
 
-    Symmetric input: multifrontal LDL^T (1x1 pivots).  ``fill_nnz`` counts the equivalent LU
-    entries with the unit diagonal excluded (2 * strictly-lower(L) + n), so a factored
-    identity reports exactly n as in the reference's SuperLU accounting.
+    Symmetric input: multifrontal LDL^T (1x1 pivots in a static order), each solve refined
+    by BiCGSTAB against the matrix when its residual exceeds ``refine_tolerance``.
+    ``fill_nnz`` counts the equivalent LU entries with the unit diagonal excluded
+    (2 * strictly-lower(L) + n), so a factored identity reports exactly n as in the
+    reference's SuperLU accounting.  Symmetric indefinite input whose static order meets a
+    zero pivot, or whose refinement stalls, is re-factored in the saddle form below (SuperLU's
+    partial pivoting succeeds on any nonsingular matrix; so does the saddle form).
 
     Unsymmetric input (the reference hands it to SuperLU; here dc/dp in the block solve,
     sensitivity.py:284): the device factors the symmetric saddle form [[0, M^T], [M, 0]]
@@ -161,7 +165,7 @@ class SparseFactorization:
     half).  ``fill_nnz`` is then nnz of the saddle factor's L minus n.
     """
 
-    __slots__ = ("n", "fill_nnz", "_sys", "_unsym", "refine_tolerance", "max_refine_iters", "last_report")
+    __slots__ = ("n", "fill_nnz", "_sys", "_unsym", "_m", "refine_tolerance", "max_refine_iters", "last_report")
 
     def __init__(self, m: CscMatrix, refine_tolerance: float = 1e-12, max_refine_iters: int = 50):
         _structural_checks(m)
@@ -170,14 +174,24 @@ class SparseFactorization:
         self.refine_tolerance = float(refine_tolerance)
         self.max_refine_iters = int(max_refine_iters)
         self.last_report = None
-        if self._unsym:
-            self._sys = _DeviceSystem(_augmented(m), self.n, 0, self.n)
-            self._sys.factorize()
-            self.fill_nnz = int(self._sys.sym.stats()["nnz_l"] - self.n)
-        else:
+        self._m = m
+        if not self._unsym:
             self._sys = _DeviceSystem(m)
-            self._sys.factorize()
-            self.fill_nnz = int(2 * self._sys.sym.stats()["nnz_l"] - self.n)
+            try:
+                self._sys.factorize()
+                self.fill_nnz = int(2 * self._sys.sym.stats()["nnz_l"] - self.n)
+                return
+            except SingularMatrix:
+                # a zero pivot in the static symmetric order (symmetric indefinite input, e.g.
+                # a zero diagonal): SuperLU would pivot past it, so take the saddle form below
+                self._unsym = True
+        self._saddle()
+
+    def _saddle(self) -> None:
+        self._unsym = True
+        self._sys = _DeviceSystem(_augmented(self._m), self.n, 0, self.n)
+        self._sys.factorize()
+        self.fill_nnz = int(self._sys.sym.stats()["nnz_l"] - self.n)
 
     def solve(self, b, transpose: bool = False) -> np.ndarray:
         """x = A^{-1} b, or A^{-T} b with ``transpose`` (a no-op for a symmetric factor;
@@ -186,8 +200,36 @@ class SparseFactorization:
         if b.shape[0] != self.n:
             raise DimensionMismatch(f"rhs has {b.shape[0]} rows, expected {self.n}")
         if not self._unsym:
-            return self._sys.solve_host(b)
+            x = self._solve_symmetric(b)
+            if x is not None:
+                return x
+            self._saddle()        # static pivots too inaccurate for refinement to recover
         return self._solve_saddle(b, transpose)
+
+    def _solve_symmetric(self, b: np.ndarray):
+        """Static-order LDL^T solve, refined by BiCGSTAB against the matrix itself when its
+        residual exceeds ``refine_tolerance`` (0 iterations for well-conditioned SPD input,
+        which is what SuperLU's partial pivoting gives the reference).  None when the
+        refinement stalls: the caller switches to the saddle form."""
+        torch = self._sys.torch
+        cols = b.reshape(self.n, -1)
+        out = np.empty_like(cols)
+        stream = _lib.stream_handle()
+        worst, iters = 0.0, 0
+        for j in range(cols.shape[1]):
+            if not np.any(cols[:, j]):
+                out[:, j] = 0.0
+                continue
+            d_rhs = torch.from_numpy(np.ascontiguousarray(cols[:, j])).to("cuda")
+            d_sol = torch.empty_like(d_rhs)
+            rc, res, its = self._sys.factor.solve_refined(self._sys.values, d_rhs, d_sol, self.refine_tolerance,
+                                                          self.max_refine_iters, False, stream)
+            if rc == _lib.SGN_NO_CONVERGENCE or not np.isfinite(res[0]):
+                return None
+            out[:, j] = d_sol.cpu().numpy()
+            worst, iters = max(worst, float(res[0])), iters + int(its[0])
+        self.last_report = SolveReport(worst, iters)
+        return out.reshape(b.shape)
 
     def _solve_saddle(self, b: np.ndarray, transpose: bool) -> np.ndarray:
         torch = self._sys.torch

@@ -110,3 +110,24 @@ def test_zero_stabilization_is_plain_solve(cuda):
     expect = np.linalg.solve(K.toarray(), rhs)
     assert rep.refine_iterations == 0
     np.testing.assert_allclose(sol, expect, rtol=1e-9, atol=1e-12 * np.abs(expect).max())
+
+
+@pytest.mark.parametrize("n,seed", [(40, 0), (200, 3)])
+def test_symmetric_indefinite_zero_diagonal(cuda, n, seed):
+    """Nonsingular symmetric indefinite input with zero diagonal entries: SuperLU pivots past
+    them (reference linear_solvers.py:87); the device falls back to the saddle form."""
+    from paper_2107_03285_b200 import CscMatrix, factor_sparse
+    rng = np.random.default_rng(seed)
+    a = sp.random(n, n, density=0.08, random_state=rng, data_rvs=rng.standard_normal)
+    m = (a + a.T + sp.diags(rng.standard_normal(n))).tolil()
+    for i in range(0, n, 3):
+        m[i, i] = 0.0                                       # zero pivots in any static order
+    m = m.tocsc()
+    dense = m.toarray()
+    assert abs(np.linalg.det(dense)) > 0
+    b = rng.standard_normal(n)
+    f = factor_sparse(CscMatrix.from_scipy(m))
+    x = f.solve(b)
+    ref = np.linalg.solve(dense, b)
+    assert np.linalg.norm(dense @ x - b) <= 1e-10 * np.linalg.norm(b)
+    assert np.linalg.norm(x - ref) <= 1e-8 * np.linalg.norm(ref) * max(1.0, np.linalg.cond(dense) * 1e-6)
