@@ -437,6 +437,23 @@ def _nan_probe(eng, where):
                   file=sys.stderr, flush=True)
 
 
+def factor_shifts(eng, full: bool = False):
+    """Static shifts of the direction path's KKT factorization.
+
+    The reference factors K + diag(+eps_x, 0, -eps_lambda) with SuperLU and refines against
+    the unshifted K (linear_solvers.py:111-175); the shift keeps its unsymmetric LU of the
+    quasi-definite KKT stable.  The device LDL^T pivots every (x_i, lambda_j) pair as a 2x2
+    block with |det| >= g^2, so it does not need the full shift: it factors with
+    ``eng.factor_shift_scale`` x eps (1e-4: 1e-6 -> 1e-10), which makes the first solve
+    accurate enough that the refinement -- still against the unshifted K, to the same
+    refine_tolerance -- takes 0-1 BiCGSTAB iterations instead of 3-5 (config 2: 5 -> 1,
+    config 4: 3 -> 1; dp unchanged within the contract, profiles/r02_eps_probe.txt).  If the
+    refinement stalls or a pivot is zero with the reduced shift, the direction is recomputed
+    with the full shift (full=True), i.e. exactly the reference's preconditioner."""
+    sc = 1.0 if full else float(getattr(eng, "factor_shift_scale", 1.0))
+    return float(eng.stab.eps_x) * sc, float(eng.stab.eps_lambda) * sc
+
+
 def _factor_adjoint(eng, st, cur, f0=None, f1=None, events=None):
     """KKT factor on `cur` || adjoint gradient and the SGN right-hand side on a side stream,
     joined back into `cur`; no host synchronization (so it can be graph-captured)."""
@@ -456,7 +473,7 @@ def _factor_adjoint(eng, st, cur, f0=None, f1=None, events=None):
     ev_asm.record(cur)
     if f0 is not None:
         f0.record(cur)
-    eng.kfac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda, st)
+    eng.kfac.numeric(eng.kvals, *factor_shifts(eng), st)
     if f1 is not None:
         f1.record(cur)
     if events is not None:
@@ -498,6 +515,30 @@ def adjoint_gradient_stage(eng):
     eng.rhs.copy_(eng.tmp)
 
 
+def _refine_with_fallback(eng, st, tol, mi):
+    """Refined KKT solve (BiCGSTAB against the unshifted K, linear_solvers.py:178-211) on the
+    factor of the reduced shift; on a stall or a zero pivot the KKT is re-factored with the
+    full shift (the reference's own preconditioner) and solved again.  The factor's pivot
+    check is part of this call (SingularMatrix with the full shift, as before)."""
+    from .errors import SingularMatrix
+    rc, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
+    reduced = factor_shifts(eng) != factor_shifts(eng, full=True)
+    singular = False
+    try:
+        eng.kfac.check(st)
+    except SingularMatrix:
+        if not reduced:
+            raise
+        singular = True
+    eng.last_full_shift = False
+    if reduced and (singular or rc == _lib.SGN_NO_CONVERGENCE):
+        eng.kfac.numeric(eng.kvals, *factor_shifts(eng, full=True), st)
+        eng.kfac.check(st)
+        rc, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
+        eng.last_full_shift = True
+    return rc, res, its
+
+
 def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = True, events=None,
                      pre_done: bool = False):
     """factor -> adjoint gradient -> refined KKT solve on an object exposing
@@ -533,11 +574,10 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(cur)
-        rc2, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
+        rc2, res, its = _refine_with_fallback(eng, st, tol, mi)
         s1.record(cur)
         if events is not None:
             events[2].record()
-        eng.kfac.check(st)
         eng.gfac.check(st)
         if timings is not None:         # device events: no host sync between the phases
             s1.synchronize()
@@ -547,10 +587,11 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
             timings["main_iters"] = its
     else:
         _nan_probe(eng, "before factor")
-        eng.kfac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda, st)
+        eng.kfac.numeric(eng.kvals, *factor_shifts(eng), st)
         if events is not None:
             events[0].record()
-        eng.kfac.check(st)
+        if factor_shifts(eng) == factor_shifts(eng, full=True):
+            eng.kfac.check(st)
         t2 = time.perf_counter()
         if timings is not None:
             timings["factor_s"] = t2 - t1
@@ -572,7 +613,7 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
         _nan_probe(eng, "after adjoint")
         if not need_direction:
             return None, None
-        rc2, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
+        rc2, res, its = _refine_with_fallback(eng, st, tol, mi)
         _nan_probe(eng, f"after refine rc={rc2}")
         if events is not None:
             events[2].record()
@@ -863,7 +904,7 @@ class DeviceEngine:
         capture fails (the eager path then stays in use)."""
         if not (_DIR_GRAPH and _SIDE_STREAM and getattr(self, "adjoint_gx", False)):
             return None
-        key = (float(self.stab.eps_x), float(self.stab.eps_lambda))
+        key = factor_shifts(self)
         cached = getattr(self, "_dgraphs", None)
         if cached is not None and cached[0] == key:
             return cached[1]
@@ -890,6 +931,7 @@ class DeviceEngine:
         return self._dgraphs[1]
 
     adjoint_gx = True
+    factor_shift_scale = 1e-4          # see factor_shifts(): 1.0 = the reference's full shift
 
     def adjoint_direct(self, check_pivots: bool = True):
         """w = G_x^{-1} f_x (unshifted LDL^T of the state Jacobian) placed as v = (0, 0, w)
