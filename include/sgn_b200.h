@@ -93,7 +93,8 @@ typedef struct {
     int32_t fat_tiles;     /* fronts of <= fat_tiles tiles factor as one task (default 0)    */
     int32_t fat_solve;     /* small fronts solve as one task (default 1)                     */
     int32_t generic_pairs; /* generic mode: 2x2 pivots on consecutive unknowns (default 1)   */
-    int32_t reserved[7];
+    int32_t upd_pair;      /* grouped Schur updates on 64x64 blocks (2x2 tiles) (default 1)   */
+    int32_t reserved[6];
 } sgn_symbolic_options;
 void sgn_symbolic_options_default(sgn_symbolic_options* o);
 /* as sgn_symbolic_create, with options (NULL = defaults) */
@@ -199,6 +200,16 @@ int  sgn_spmv(sgn_factor f, const double* d_values, int64_t values_stride,
 int  sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_stride,
                        const double* d_rhs, double* d_sol, double tol, int32_t max_iters,
                        int32_t flags, double* rel_res, int32_t* iters, void* stream);
+
+/* Mixed-precision iterative refinement on the factor (the direction path's first solve,
+ * ahead of the BiCGSTAB of linear_solvers.py:178-211): x = F^{-1} rhs, then `steps` times
+ * x += F^{-1}(rhs - K x) with the residual evaluated in double-double (error-free products
+ * and compensated row sums, then rounded).  rel_res[b] = |rhs - K x| / |rhs| of the final x
+ * evaluated the same way (an exact residual, so it cannot be below the truth); corr[b] =
+ * |last correction| / |x|.  The caller falls back to sgn_solve_refined when rel_res > tol. */
+int  sgn_solve_ir(sgn_factor f, const double* d_values, int64_t values_stride,
+                  const double* d_rhs, double* d_sol, int32_t steps, double* rel_res,
+                  double* corr, void* stream);
 
 /* ---- element assembly (device) --------------------------------------------------
  * Replaces the NumPy element kernels + COO->CSC of constraint_jac_x / constraint_jac_p

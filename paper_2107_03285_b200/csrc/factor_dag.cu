@@ -406,6 +406,91 @@ __device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k
   }
 }
 
+// Grouped Schur update of a 64x64 block (F_UPD2): tiles {ti, ti+1} x {tj, tj+1}, steps
+// k0..k.  Each warp owns a 32x32 quarter as 4x4 DMMA fragments (acc in registers), so a
+// streamed step (A 64x32, B 64x32) feeds twice the DMMA work per operand byte of the 32x32
+// body (profiles/micro/upd_bench.cu: 26.5 vs 12.9 TFLOP/s).  Smem: A K-major (stride 68) and
+// B N-major (stride 36): fragment reads and staging stores conflict-free.  Tiles past the
+// front, and the upper tile (ti, tj+1) of a diagonal block, are neither read nor written.
+constexpr int kU2A = 68, kU2B = 36;
+__device__ void f_update2(const sgn::FactorArgs& A, const DFront& F, int b, int k0, int k, int ti, int tj, Smem& S) {
+  static_assert(32 * kU2A + 64 * kU2B <= 5 * kTileWords, "F_UPD2 operands fit the tile buffers");
+  double* As = reinterpret_cast<double*>(&S);   // [32][kU2A] As[c][r] = L21(row(r), j0 + c)  (S.a, S.b)
+  double* Bs = As + 32 * kU2A;                  // [64][kU2B] Bs[j][c] = W(col(j), j0 + c)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  double* Fm = front_ptr(A, F, b);
+  const int64_t ld = F.nrow;
+  const int T = sgn::ntiles_front(F.npiv, F.nrow);
+  // row r of the block -> front row (or -1): tile ti + (r >> 5), row r & 31 of that tile
+  auto brow = [&](int t0, int r) -> int {
+    const int t = t0 + (r >> 5);
+    if (t >= T) return -1;
+    const int lo = sgn::tile_lo(F.npiv, t);
+    return (lo + (r & 31) < sgn::tile_hi(F.npiv, F.nrow, t)) ? lo + (r & 31) : -1;
+  };
+  const int ra = brow(ti, tid & 63);      // this thread's A staging row (fixed)
+  double acc[4][4][2];
+#pragma unroll
+  for (int mf = 0; mf < 4; ++mf)
+#pragma unroll
+    for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
+  for (int s = k0; s <= k; ++s) {
+    const int j0 = s * kTile, w = min(kTile, F.npiv - j0);
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = (tid >> 6) + 2 * (u + 8 * hh);
+        v[u] = (ra >= 0 && c < w) ? __ldcg(Fm + (int64_t)(j0 + c) * ld + ra) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) As[((tid >> 6) + 2 * (u + 8 * hh)) * kU2A + (tid & 63)] = v[u];
+    }
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = (tid >> 5) + 4 * (u + 8 * hh), cb = brow(tj, j);
+        v[u] = (cb >= 0 && lane < w) ? __ldcg(Fm + (int64_t)cb * ld + j0 + lane) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) Bs[((tid >> 5) + 4 * (u + 8 * hh)) * kU2B + lane] = v[u];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kTile; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int mf = 0; mf < 4; ++mf) fa[mf] = As[(kk + q) * kU2A + wm + 8 * mf + g];
+#pragma unroll
+      for (int nf = 0; nf < 4; ++nf) fb[nf] = Bs[(wn + 8 * nf + g) * kU2B + kk + q];
+#pragma unroll
+      for (int mf = 0; mf < 4; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < 4; ++nf) dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], fa[mf], fb[nf]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int mf = 0; mf < 4; ++mf) {
+    const int m = wm + 8 * mf + g, gr = brow(ti, m);
+    if (gr < 0) continue;
+#pragma unroll
+    for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = wn + 8 * nf + 2 * q + h, gc = brow(tj, n);
+        const int tr = ti + (m >> 5), tc = tj + (n >> 5);
+        if (gc < 0 || tr < tc || (tr == tc && (m & 31) < (n & 31))) continue;
+        double* pc = Fm + (int64_t)gc * ld + gr;
+        *pc = __ldcg(pc) - acc[mf][nf][h];
+      }
+  }
+}
+
 // One block Z(t, cb) of the solve panel Z = [I; L21] L11^{-1} (L11 unit lower, the 2x2
 // pivot slots belong to D), t a tile of the split grid, cb a pivot column block:
 //   pivot tile t < P:   Z(t, cb) = L(t,t)^{-1} (delta_{t,cb} I - sum_{j=cb}^{t-1} L(t,j) Z(j,cb))
@@ -578,7 +663,7 @@ k_factor_dag(const sgn::FactorArgs A) {
     }
     const int Tn = sgn::ntiles_front(F.npiv, F.nrow);
     // F_UPDATE: b = tj | (ns << 16) applies steps k-ns+1 .. k (ns = 0 or 1: step k alone)
-    const int tjb = T.b & 0xffff, ns = (kind == sgn::F_UPDATE) ? max(1, T.b >> 16) : 1;
+    const int tjb = T.b & 0xffff, ns = (kind == sgn::F_UPDATE || kind == sgn::F_UPD2) ? max(1, T.b >> 16) : 1;
     if (tid == 0) {
       if (kind == sgn::F_ASM) {
         for (int ci = F.child_begin; ci < F.child_end; ++ci) {
@@ -597,6 +682,14 @@ k_factor_dag(const sgn::FactorArgs A) {
       } else if (kind == sgn::F_UPDATE || kind == sgn::F_DIAGUPD) {   // PAN(k) awaited inside
         const int ti = (kind == sgn::F_DIAGUPD) ? k + 1 : T.a, tj = (kind == sgn::F_DIAGUPD) ? k + 1 : tjb;
         spin_ge(cf + sgn::cnt_tile(P, ti, tj), 2 + k - ns);
+      } else if (kind == sgn::F_UPD2) {           // every tile of the block, then the TRSMs of step k
+        for (int x = T.a; x < min(T.a + 2, Tn); ++x)
+          for (int y = tjb; y < min(tjb + 2, Tn); ++y)
+            if (x >= y) spin_ge(cf + sgn::cnt_tile(P, x, y), 2 + k - ns);
+        for (int x = 0; x < 4; ++x) {
+          const int t = (x < 2) ? T.a + x : tjb + x - 2;
+          if (t < Tn) spin_ge(cf + sgn::cnt_pant(F.npiv, F.nrow, k, sgn::pan_task_of(k, t)), 1);
+        }
       }                                           // Z(t, cb): progressive waits in f_ztask_pre
     }
     __syncthreads();
@@ -617,6 +710,8 @@ k_factor_dag(const sgn::FactorArgs A) {
       const bool dg = (kind == sgn::F_DIAGUPD);
       f_update(A, F, b, k - ns + 1, k, dg ? k + 1 : T.a, dg ? k + 1 : tjb, S, dg);
       if (dg) { fac_k = k + 1; fac_tile = v33(S.b[1]); }
+    } else if (kind == sgn::F_UPD2) {
+      f_update2(A, F, b, k - ns + 1, k, T.a, tjb, S);
     } else {
       f_ztask_pre(A, F, b, T.a, T.b, S);
       nr_trsm = (T.a < P && tid < 32) ? 32 : 0;
@@ -641,6 +736,13 @@ k_factor_dag(const sgn::FactorArgs A) {
         s3 = cf + sgn::cnt_pant(F.npiv, F.nrow, k, T.a);
       }
       else if (kind == sgn::F_DIAGUPD) { s1 = cf + sgn::cnt_tile(P, k + 1, k + 1); s3 = cf + sgn::cnt_diag(P, k + 1); }
+      else if (kind == sgn::F_UPD2) {
+        s1 = nullptr;
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        for (int x = T.a; x < min(T.a + 2, Tn); ++x)
+          for (int y = tjb; y < min(tjb + 2, Tn); ++y)
+            if (x >= y) asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(cf + sgn::cnt_tile(P, x, y)), "r"(ns) : "memory");
+      }
       else {
         s1 = cf + sgn::cnt_tile(P, T.a, tjb);
         if (kind == sgn::F_ASM && T.a == 0 && T.b == 0 && F.npiv > 0) s3 = cf + sgn::cnt_diag(P, 0);

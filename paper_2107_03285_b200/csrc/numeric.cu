@@ -751,6 +751,53 @@ __global__ void k_spmv(const int64_t* __restrict__ ptr, const int32_t* __restric
 }
 
 // ------------------------------------------------------------------------------------
+// r = b - K x with error-free products (fma) and compensated sums: double-double accuracy,
+// rounded once (the residual of the mixed-precision iterative refinement, sgn_solve_ir)
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+__global__ void k_resid_dd(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                           const double* __restrict__ vals, int64_t vstride,
+                           const double* __restrict__ x, const double* __restrict__ bv,
+                           double* __restrict__ r, int64_t n) {
+  const int b = blockIdx.y;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+  const int sub = threadIdx.x & 7;
+  const bool valid = row < n;
+  const double* vb = vals + (int64_t)b * vstride;
+  const double* xb = x + (int64_t)b * n;
+  double s = 0.0, c = 0.0;
+  const int64_t kb = valid ? ptr[row] : 0, ke = valid ? ptr[row + 1] : 0;
+  for (int64_t k = kb + sub; k < ke; k += 8) {
+    const double v = vb[k], xv = xb[idx[k]];
+    const double p = v * xv, e = fma(v, xv, -p);
+    double t;
+    two_sum(s, p, s, t);
+    c += t + e;
+  }
+#pragma unroll
+  for (int off = 1; off < 8; off <<= 1) {
+    const double s2 = __shfl_xor_sync(0xffffffffu, s, off), c2 = __shfl_xor_sync(0xffffffffu, c, off);
+    double t;
+    two_sum(s, s2, s, t);
+    c += c2 + t;
+  }
+  if (valid && sub == 0) {
+    double hi, lo;
+    two_sum(bv[(int64_t)b * n + row], -s, hi, lo);
+    r[(int64_t)b * n + row] = hi + (lo - c);
+  }
+}
+
+__global__ void k_add(double* __restrict__ x, const double* __restrict__ d, int64_t len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] += d[i];
+}
+
+// ------------------------------------------------------------------------------------
 // deterministic batched BLAS-1 for BiCGSTAB (fixed reduction trees)
 // ------------------------------------------------------------------------------------
 constexpr int kDotBlocks = 64;
@@ -990,6 +1037,8 @@ struct sgn_factor_s {
   DevBuf<double> bx, br, brh, bp, bv, bs, bt, btmp, bbest, bb, bscr, partial;
   DevBuf<BiState> bst;
   DevBuf<int> gate, dtick;
+  // mixed-precision iterative refinement workspace (sgn_solve_ir)
+  DevBuf<double> ir_r, ir_d, ir_out;
   bool bicg_ready = false;
   // refinement graphs: prologue + WHILE(any instance iterating){ one BiCGSTAB iteration }
   struct BicgGraph {
@@ -1125,6 +1174,7 @@ void sgn_symbolic_options_default(sgn_symbolic_options* o) {
   o->leaf_size = d.leaf_size; o->p_order = d.p_order; o->upd_group = d.upd_group;
   o->zinline = d.zinline; o->zquota = d.zquota; o->noz_tiles = d.noz_tiles;
   o->fat_tiles = d.fat_tiles; o->fat_solve = d.fat_solve; o->generic_pairs = d.generic_pairs;
+  o->upd_pair = d.upd_pair;
 }
 
 int sgn_symbolic_create(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t n_x,
@@ -1146,6 +1196,7 @@ int sgn_symbolic_create_ex(int64_t n, const int64_t* indptr, const int64_t* indi
       so.zinline = opts->zinline; so.zquota = opts->zquota; so.noz_tiles = opts->noz_tiles;
       so.fat_tiles = opts->fat_tiles; so.fat_solve = opts->fat_solve;
       so.generic_pairs = opts->generic_pairs;
+      so.upd_pair = opts->upd_pair;
     }
     if (!out || !indptr || n < 0) { sgn::last_error() = "bad arguments"; return SGN_INVALID; }
     auto h = std::make_unique<sgn_symbolic_s>();
@@ -1661,6 +1712,51 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
   if (fail) {
     sgn::last_error() = "BiCGSTAB refinement stalled above tolerance";
     return SGN_NO_CONVERGENCE;
+  }
+  return SGN_OK;
+}
+
+// Mixed-precision iterative refinement on the factor: x = M^-1 b, then `steps` times
+// x += M^-1 (b - K x) with the residual in double-double (k_resid_dd); the final residual
+// is evaluated the same way.  rel_res[b] = |b - K x| / |b| (exact residual, rounded),
+// corr[b] = |last correction| / |x|.  One host synchronisation.
+int sgn_solve_ir(sgn_factor f, const double* d_values, int64_t values_stride, const double* d_rhs,
+                 double* d_sol, int32_t steps, double* rel_res, double* corr, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const sgn::Symbolic& s = f->sym->s;
+  const int64_t n = s.n;
+  const int B = f->batch;
+  const size_t N = (size_t)B * std::max<int64_t>(n, 1);
+  int rc;
+  if (!f->ir_r.p && ((rc = f->ir_r.alloc(N)) || (rc = f->ir_d.alloc(N)) || (rc = f->ir_out.alloc(4 * (size_t)B))))
+    return rc;
+  if ((rc = launch_solve(f, d_rhs, d_sol, 0, st))) return rc;
+  const unsigned rb = (unsigned)((n * 8 + 255) / 256);
+  CUDA_TRY(cudaMemsetAsync(f->ir_d.p, 0, N * sizeof(double), st));
+  for (int it = 0; it <= steps; ++it) {
+    sgn::count_launch();
+    k_resid_dd<<<dim3(rb, B), 256, 0, st>>>(f->indptr.p, f->idx32.p, d_values, values_stride, d_sol, d_rhs,
+                                            f->ir_r.p, n);
+    CUDA_TRY(cudaGetLastError());
+    if (it == steps) break;
+    if ((rc = launch_solve(f, f->ir_r.p, f->ir_d.p, 0, st))) return rc;
+    sgn::count_launch();
+    k_add<<<(unsigned)std::min<size_t>((N + 255) / 256, 4096), 256, 0, st>>>(d_sol, f->ir_d.p, (int64_t)N);
+    CUDA_TRY(cudaGetLastError());
+  }
+  double* o = f->ir_out.p;
+  if ((rc = sgn_reduce(1, n, B, f->ir_r.p, f->ir_r.p, n, o, st)) ||
+      (rc = sgn_reduce(1, n, B, d_rhs, d_rhs, n, o + B, st)) ||
+      (rc = sgn_reduce(1, n, B, f->ir_d.p, f->ir_d.p, n, o + 2 * B, st)) ||
+      (rc = sgn_reduce(1, n, B, d_sol, d_sol, n, o + 3 * B, st)))
+    return rc;
+  std::vector<double> h(4 * (size_t)B);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), o, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int b = 0; b < B; ++b) {
+    const double bn = std::sqrt(h[B + b]), xn = std::sqrt(h[3 * B + b]);
+    if (rel_res) rel_res[b] = bn > 0.0 ? std::sqrt(h[b]) / bn : 0.0;
+    if (corr) corr[b] = xn > 0.0 ? std::sqrt(h[2 * B + b]) / xn : 0.0;
   }
   return SGN_OK;
 }

@@ -1194,12 +1194,25 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
         const int32_t P = ptiles(F.npiv);
         // column tj: step tj-1 is the look-ahead update, step tj-2 stays a single-step
         // task (it sits one chain step from the pivot block tj), steps <= tj-3 are grouped
+        // grouped columns emitting at this step with the same step range pair up: their
+        // tiles are updated as 64x64 blocks {ti, ti+1} x {tj, tj+1} (F_UPD2, twice the
+        // DMMA work per operand byte; profiles/micro/upd_bench.cu)
+        auto grouped_ns = [&](int32_t tj) -> int32_t {   // 0: no grouped emission at k
+          if (tj >= T || k > tj - 3) return 0;
+          const int32_t kmax = std::min(tj - 3, P - 1);
+          if ((k + 1) % kUpdGroup != 0 && k != kmax) return 0;
+          return k - (k / kUpdGroup) * kUpdGroup + 1;
+        };
         for (int32_t tj = k + 2; tj < T; ++tj) {
           int32_t ns = 1;
           if (k <= tj - 3) {
-            const int32_t kmax = std::min(tj - 3, P - 1);
-            if ((k + 1) % kUpdGroup != 0 && k != kmax) continue;
-            ns = k - (k / kUpdGroup) * kUpdGroup + 1;
+            ns = grouped_ns(tj);
+            if (ns == 0) continue;
+            if (opt.upd_pair && grouped_ns(tj + 1) == ns) {
+              for (int32_t ti = tj; ti < T; ti += 2) ft(F_UPD2, k, f, ti, tj | (ns << 16));
+              ++tj;
+              continue;
+            }
           }
           for (int32_t ti = tj; ti < T; ++ti) ft(F_UPDATE, k, f, ti, tj | (ns << 16));
         }

@@ -26,7 +26,8 @@ def _i64(a) -> np.ndarray:
 # profiling sweeps only; the product path passes options explicitly)
 _OPTION_ENV = {"leaf_size": "SGN_LEAF_SIZE", "upd_group": "SGN_UPD_GROUP", "zinline": "SGN_ZINLINE",
                "zquota": "SGN_ZQUOTA", "noz_tiles": "SGN_NOZ_TILES", "fat_tiles": "SGN_FAT_TILES",
-               "fat_solve": "SGN_FAT_SOLVE", "generic_pairs": "SGN_GENERIC_PAIRS", "p_order": "SGN_P_ORDER"}
+               "fat_solve": "SGN_FAT_SOLVE", "generic_pairs": "SGN_GENERIC_PAIRS", "p_order": "SGN_P_ORDER",
+               "upd_pair": "SGN_UPD_PAIR"}
 
 
 def symbolic_options(**kw) -> "_lib.SymbolicOptions":
@@ -164,6 +165,16 @@ class DeviceFactor:
         stride = values.stride(0) if values.dim() == 2 else 0
         flags = _lib.SGN_SOLVE_LEADING if leading else 0
         check(lib().sgn_spmv(self._h, ptr(values), stride, ptr(x), ptr(y), flags, stream), what="spmv")
+
+    def solve_ir(self, values, rhs, sol, steps: int, stream: int = 0):
+        """Mixed-precision iterative refinement (sgn_solve_ir); returns (rel_res[batch],
+        corr[batch]) -- exact residuals of the final iterate and the last correction."""
+        stride = values.stride(0) if values.dim() == 2 else 0
+        res = np.zeros(self.batch)
+        corr = np.zeros(self.batch)
+        check(lib().sgn_solve_ir(self._h, ptr(values), stride, ptr(rhs), ptr(sol), int(steps),
+                                 res.ctypes.data_as(P_dbl), corr.ctypes.data_as(P_dbl), stream), what="refinement")
+        return res, corr
 
     def solve_refined(self, values, rhs, sol, tol: float, max_iters: int, leading: bool = False,
                       stream: int = 0):

@@ -11,7 +11,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-KIND = {0: "asm", 1: "panel", 2: "update", 3: "zpanel", 4: "diagupd"}
+KIND = {0: "asm", 1: "panel", 2: "update", 3: "zpanel", 4: "diagupd", 6: "upd2"}
 
 
 def main():
@@ -80,7 +80,15 @@ def summarize(a, fac):
     np.savez(a.out, T=T, M=M, sm=tr[:, 3], meta=meta)
     kind, step, front, lvl = meta[:, 0], meta[:, 1], meta[:, 2], meta[:, 3]
     print("span us %.1f tasks %d" % (T[:, 2].max(), len(T)))
-    for k in range(5):
+    try:
+        npiv = np.asarray(fac.sym.fronts()["npiv"])
+        zp = (kind == 3) & (meta[:, 4] < (npiv[front] + 31) // 32)
+        zs = (kind == 3) & ~zp
+        for nm, m in (("z(piv tiles)", zp), ("z(struct tiles)", zs)):
+            print(f"{nm:16s} n={m.sum():7d} busy_sum_us={np.sum(T[m, 2] - T[m, 1]):9.1f}")
+    except Exception as exc:  # noqa: BLE001
+        print("z split unavailable:", exc)
+    for k in KIND:
         m = kind == k
         if m.any():
             print(f"{KIND[k]:7s} n={m.sum():6d} busy_med={np.median(T[m, 2] - T[m, 1]):6.2f} "
