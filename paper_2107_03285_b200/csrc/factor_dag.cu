@@ -406,28 +406,40 @@ __device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k
   }
 }
 
-// Grouped Schur update of a 64x64 block (F_UPD2): tiles {ti, ti+1} x {tj, tj+1}, steps
-// k0..k.  Each warp owns a 32x32 quarter as 4x4 DMMA fragments (acc in registers), so a
-// streamed step (A 64x32, B 64x32) feeds twice the DMMA work per operand byte of the 32x32
-// body (profiles/micro/upd_bench.cu: 26.5 vs 12.9 TFLOP/s).  Smem: A K-major (stride 68) and
-// B N-major (stride 36): fragment reads and staging stores conflict-free.  Tiles past the
-// front, and the upper tile (ti, tj+1) of a diagonal block, are neither read nor written.
+// 64x64 DMMA block products of the factorization (each warp owns a 32x32 quarter as 4x4
+// m8n8k4 fragments, acc in registers, so a streamed 32-wide step (A 64x32, B 64x32) feeds
+// twice the DMMA work per operand byte of the 32x32 bodies; profiles/micro/upd_bench.cu:
+// 26.5 vs 12.9 TFLOP/s).  Smem: A K-major (stride 68), B N-major (stride 36): fragment
+// reads and staging stores are conflict-free.
+//   ZP = false, F_UPD2: C(ti..ti+1, tj..tj+1) -= sum_{s=k0..k} L21(rows, step s) W(cols, step s)^T;
+//                tiles past the front, and the upper tile (ti, tj+1) of a diagonal block,
+//                are neither read nor written.
+//   ZP = true,  F_ZPAN2: Z(t..t+1, cb..cb+1) = sum_{j=cb}^{P-1} L(t..t+1, j) Z(j, cb..cb+1) for
+//                struct tiles t >= P (Z(cb, cb+1) = 0, so both columns sum from j = cb).
 constexpr int kU2A = 68, kU2B = 36;
-__device__ void f_update2(const sgn::FactorArgs& A, const DFront& F, int b, int k0, int k, int ti, int tj, Smem& S) {
-  static_assert(32 * kU2A + 64 * kU2B <= 5 * kTileWords, "F_UPD2 operands fit the tile buffers");
-  double* As = reinterpret_cast<double*>(&S);   // [32][kU2A] As[c][r] = L21(row(r), j0 + c)  (S.a, S.b)
-  double* Bs = As + 32 * kU2A;                  // [64][kU2B] Bs[j][c] = W(col(j), j0 + c)
+template <bool ZP>
+__device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int k0, int k, int ti, int tj, Smem& S) {
+  static_assert(32 * kU2A + 64 * kU2B <= 5 * kTileWords, "64x64 operands fit the tile buffers");
+  double* As = reinterpret_cast<double*>(&S);   // [32][kU2A] As[c][r] = L(row(r), j0 + c)  (S.a, S.b)
+  double* Bs = As + 32 * kU2A;                  // [64][kU2B] Bs[j][c] = W(col(j), j0 + c) | Z(j0 + c, col j)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   double* Fm = front_ptr(A, F, b);
+  double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
   const int64_t ld = F.nrow;
   const int T = sgn::ntiles_front(F.npiv, F.nrow);
-  // row r of the block -> front row (or -1): tile ti + (r >> 5), row r & 31 of that tile
+  // row r of the block -> front row (or -1): tile t0 + (r >> 5), row r & 31 of that tile
   auto brow = [&](int t0, int r) -> int {
     const int t = t0 + (r >> 5);
     if (t >= T) return -1;
     const int lo = sgn::tile_lo(F.npiv, t);
     return (lo + (r & 31) < sgn::tile_hi(F.npiv, F.nrow, t)) ? lo + (r & 31) : -1;
+  };
+  // column j of the block -> W row (update) or Z column (Z panel), or -1
+  auto bcol = [&](int j) -> int {
+    if (!ZP) return brow(tj, j);
+    const int c = 32 * tj + j;
+    return c < F.npiv ? c : -1;
   };
   const int ra = brow(ti, tid & 63);      // this thread's A staging row (fixed)
   double acc[4][4][2];
@@ -453,8 +465,9 @@ __device__ void f_update2(const sgn::FactorArgs& A, const DFront& F, int b, int 
       double v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int j = (tid >> 5) + 4 * (u + 8 * hh), cb = brow(tj, j);
-        v[u] = (cb >= 0 && lane < w) ? __ldcg(Fm + (int64_t)cb * ld + j0 + lane) : 0.0;
+        const int j = (tid >> 5) + 4 * (u + 8 * hh), cb = bcol(j);
+        const double* src = ZP ? Zm : Fm;
+        v[u] = (cb >= 0 && lane < w) ? __ldcg(src + (int64_t)cb * ld + j0 + lane) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) Bs[((tid >> 5) + 4 * (u + 8 * hh)) * kU2B + lane] = v[u];
@@ -482,11 +495,16 @@ __device__ void f_update2(const sgn::FactorArgs& A, const DFront& F, int b, int 
     for (int nf = 0; nf < 4; ++nf)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int n = wn + 8 * nf + 2 * q + h, gc = brow(tj, n);
-        const int tr = ti + (m >> 5), tc = tj + (n >> 5);
-        if (gc < 0 || tr < tc || (tr == tc && (m & 31) < (n & 31))) continue;
-        double* pc = Fm + (int64_t)gc * ld + gr;
-        *pc = __ldcg(pc) - acc[mf][nf][h];
+        const int n = wn + 8 * nf + 2 * q + h, gc = bcol(n);
+        if (gc < 0) continue;
+        if (ZP) {
+          Zm[(int64_t)gc * ld + gr] = acc[mf][nf][h];
+        } else {
+          const int tr = ti + (m >> 5), tc = tj + (n >> 5);
+          if (tr < tc || (tr == tc && (m & 31) < (n & 31))) continue;
+          double* pc = Fm + (int64_t)gc * ld + gr;
+          *pc = __ldcg(pc) - acc[mf][nf][h];
+        }
       }
   }
 }
@@ -682,6 +700,10 @@ k_factor_dag(const sgn::FactorArgs A) {
       } else if (kind == sgn::F_UPDATE || kind == sgn::F_DIAGUPD) {   // PAN(k) awaited inside
         const int ti = (kind == sgn::F_DIAGUPD) ? k + 1 : T.a, tj = (kind == sgn::F_DIAGUPD) ? k + 1 : tjb;
         spin_ge(cf + sgn::cnt_tile(P, ti, tj), 2 + k - ns);
+      } else if (kind == sgn::F_ZPAN2) {          // L final (last step's TRSMs), both Z columns complete
+        spin_ge(cf + sgn::cnt_pan(P - 1), sgn::panel_tasks(F.npiv, F.nrow, P - 1));
+        spin_ge(cf + sgn::cnt_zc(P, Tn, T.b), P - T.b);
+        if (T.b + 1 < P) spin_ge(cf + sgn::cnt_zc(P, Tn, T.b + 1), P - T.b - 1);
       } else if (kind == sgn::F_UPD2) {           // every tile of the block, then the TRSMs of step k
         for (int x = T.a; x < min(T.a + 2, Tn); ++x)
           for (int y = tjb; y < min(tjb + 2, Tn); ++y)
@@ -711,7 +733,9 @@ k_factor_dag(const sgn::FactorArgs A) {
       f_update(A, F, b, k - ns + 1, k, dg ? k + 1 : T.a, dg ? k + 1 : tjb, S, dg);
       if (dg) { fac_k = k + 1; fac_tile = v33(S.b[1]); }
     } else if (kind == sgn::F_UPD2) {
-      f_update2(A, F, b, k - ns + 1, k, T.a, tjb, S);
+      f_block64<false>(A, F, b, k - ns + 1, k, T.a, tjb, S);
+    } else if (kind == sgn::F_ZPAN2) {
+      f_block64<true>(A, F, b, T.b, P - 1, T.a, T.b, S);
     } else {
       f_ztask_pre(A, F, b, T.a, T.b, S);
       nr_trsm = (T.a < P && tid < 32) ? 32 : 0;
@@ -731,6 +755,7 @@ k_factor_dag(const sgn::FactorArgs A) {
       int* s2 = cf;                                            // DONE
       int* s3 = nullptr;
       if (kind == sgn::F_ZPANEL) { s1 = (T.a < P) ? cf + sgn::cnt_zc(P, Tn, T.b) : nullptr; s2 = nullptr; }
+      else if (kind == sgn::F_ZPAN2) { s1 = nullptr; s2 = nullptr; }
       else if (kind == sgn::F_PANEL) {
         s1 = cf + sgn::cnt_pan(k);
         s3 = cf + sgn::cnt_pant(F.npiv, F.nrow, k, T.a);

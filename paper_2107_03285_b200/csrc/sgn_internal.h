@@ -95,7 +95,11 @@ SGN_HD int tile_of_row(int npiv, int r) { return r < npiv ? r / 32 : ptiles(npiv
 //   F_UPD2    (f, k, a=ti, b=tj | ns << 16): the grouped update of the 64x64 block of tiles
 //                              {ti, ti+1} x {tj, tj+1} (tiles past the front or above the
 //                              diagonal skipped): waits and signals as F_UPDATE per tile
-enum FKind : int32_t { F_ASM = 0, F_PANEL = 1, F_UPDATE = 2, F_ZPANEL = 3, F_DIAGUPD = 4, F_FAT = 5, F_UPD2 = 6 };
+//   F_ZPAN2   (f, a=t, b=cb)  : struct-tile solve-panel blocks Z({t, t+1}, {cb, cb+1}) (t >= P) in
+//                              one 64x64 DMMA product; waits PAN(P-1) and the complete Z
+//                              columns ZC(cb), ZC(cb+1); signals nothing (read by the solve)
+enum FKind : int32_t { F_ASM = 0, F_PANEL = 1, F_UPDATE = 2, F_ZPANEL = 3, F_DIAGUPD = 4, F_FAT = 5, F_UPD2 = 6,
+                       F_ZPAN2 = 7 };
 struct FTask { int32_t kind_k, f, a, b; };
 constexpr int kDiagStride = 2 * kTile * kTile + 3 * kTile;   // scratch per step: D, L^T, D^-1
 SGN_HD int panel_tasks(int npiv, int nrow, int k) {   // TRSM tasks of step k
@@ -149,7 +153,8 @@ struct SymOptions {
   int32_t fat_tiles = 0;      // fronts of <= fat_tiles tiles factor as one task (0: off)
   int32_t fat_solve = 1;      // small fronts solve as one task
   int32_t generic_pairs = 1;  // generic mode: 2x2 pivots on consecutive unknowns
-  int32_t upd_pair = 1;       // grouped Schur updates on 64x64 blocks (F_UPD2)
+  int32_t upd_pair = 3;       // grouped Schur updates on 64x64 blocks (F_UPD2); bit 1: struct-tile
+                              // Z blocks on 64x64 blocks too (F_ZPAN2); default 3 = both
 };
 
 struct Symbolic {

@@ -516,41 +516,65 @@ def adjoint_gradient_stage(eng):
 
 
 def _refine_with_fallback(eng, st, tol, mi):
-    """Refined KKT solve (BiCGSTAB against the unshifted K, linear_solvers.py:178-211) on the
-    factor of the reduced shift; on a stall or a zero pivot the KKT is re-factored with the
-    full shift (the reference's own preconditioner) and solved again.  The factor's pivot
-    check is part of this call (SingularMatrix with the full shift, as before)."""
+    """The direction path's KKT solve, in stages that each instance leaves as soon as it
+    meets ``tol`` (so an instance's result never depends on its batch):
+
+    1. mixed-precision iterative refinement on the reduced-shift factor (sgn_solve_ir:
+       exact double-double residuals drive ``eng.ir_steps`` corrections);
+    2. the reference's refinement, BiCGSTAB against the unshifted K (linear_solvers.py:
+       178-211), on the same factor;
+    3. the KKT re-factored with the full shift (the reference's own preconditioner) and
+       BiCGSTAB again.
+    Stages 1 and 3 exist only with a reduced shift (factor_shifts).  Returns (rc, res, its)
+    per instance; a zero pivot of the full-shift factor raises SingularMatrix as before."""
     from .errors import SingularMatrix
+    torch = eng.torch
+    B = eng.batch
     reduced = factor_shifts(eng) != factor_shifts(eng, full=True)
     steps = int(getattr(eng, "ir_steps", 0))
+    done = np.zeros(B, bool)
+    res_all = np.full(B, np.inf)
+    its_all = np.zeros(B, dtype=np.int32)
+    keep = None
+    eng.last_full_shift = False
+
+    def pivots_ok():
+        return eng.kfac.status(st) < 0
+
+    def absorb(res, its, ok):
+        nonlocal keep
+        new = ok & ~done
+        if new.any():
+            if keep is None:
+                keep = torch.empty_like(eng.sol)
+            m = torch.as_tensor(new, device=eng.sol.device)
+            keep[m] = eng.sol[m]
+            res_all[new], its_all[new] = res[new], its[new]
+            done[new] = True
+
     if reduced and steps > 0:
-        # mixed-precision iterative refinement on the reduced-shift factor: the exact
-        # (double-double) residual drives the corrections, so the forward error converges
-        # to the solution's double rounding instead of stopping at the residual contract
         res, corr = eng.kfac.solve_ir(eng.kvals, eng.rhs, eng.sol, steps, st)
         eng.last_ir_correction = corr
-        try:
-            eng.kfac.check(st)
-            if np.all(res <= tol):
-                eng.last_full_shift = False
-                return _lib.SGN_OK, res, np.full(eng.batch, steps, dtype=np.int32)
-        except SingularMatrix:
-            pass
-    rc, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
-    singular = False
-    try:
-        eng.kfac.check(st)
-    except SingularMatrix:
-        if not reduced:
-            raise
-        singular = True
-    eng.last_full_shift = False
-    if reduced and (singular or rc == _lib.SGN_NO_CONVERGENCE):
-        eng.kfac.numeric(eng.kvals, *factor_shifts(eng, full=True), st)
-        eng.kfac.check(st)
+        absorb(res, np.full(B, steps, dtype=np.int32), (res <= tol) & pivots_ok())
+    if not done.all():
         rc, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
-        eng.last_full_shift = True
-    return rc, res, its
+        piv = pivots_ok()
+        if not reduced and not piv.all():
+            eng.kfac.check(st)                                  # raises SingularMatrix
+        absorb(res, its, (res <= tol) & piv)
+        if reduced and not done.all():
+            eng.kfac.numeric(eng.kvals, *factor_shifts(eng, full=True), st)
+            eng.kfac.check(st)
+            eng.last_full_shift = True
+            rc, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
+            absorb(res, its, res <= tol)
+        left = ~done                                            # failed every stage: best iterate
+        res_all[left], its_all[left] = res[left], its[left]
+    if keep is not None:
+        m = torch.as_tensor(done, device=eng.sol.device)
+        eng.sol[m] = keep[m]
+    rc = _lib.SGN_OK if done.all() else _lib.SGN_NO_CONVERGENCE
+    return rc, res_all, its_all
 
 
 def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = True, events=None,

@@ -69,9 +69,36 @@ def test_shell_simulate_kkt_and_direction(shell):
     rhs = np.zeros_like(rhs_r)
     rhs[prob.n_x:prob.n_x + prob.n_p] = -g
     assert np.linalg.norm(Kr.to_scipy() @ sol - rhs) <= 2e-10 * np.linalg.norm(rhs)
+    # dp against the EXACT solution of the oracle's KKT for the same right-hand side (dense
+    # LU + refinement with double-double residuals): the device path refines to the
+    # solution's double rounding, so 1e-8 holds against the exact dp; the reference
+    # algorithm (oracle) stops at its 1e-10 residual contract, which on this shell leaves
+    # it ~1e-7 from its own exact dp -- the device result may differ from it by that much
     ref = sgn_cpu.direction_sgn(oprob, x, p)
-    assert _rel(sd.dp, ref.dp) <= 1e-8
+    exact = _exact_solve(Kr.to_scipy(), rhs)
+    n_x, n_p = prob.n_x, prob.n_p
+    assert _rel(sd.dp, exact[n_x:n_x + n_p]) <= 1e-8
+    rhs_o = np.zeros_like(rhs_r)
+    rhs_o[n_x:n_x + n_p] = -g_r
+    exact_o = _exact_solve(Kr.to_scipy(), rhs_o)
+    oracle_err = _rel(ref.dp, exact_o[n_x:n_x + n_p])
+    print(f"small shell: device dp vs exact {_rel(sd.dp, exact[n_x:n_x + n_p]):.2e}, oracle dp vs its exact "
+          f"{oracle_err:.2e}, device vs oracle {_rel(sd.dp, ref.dp):.2e}")
+    assert _rel(sd.dp, ref.dp) <= max(1e-8, 2.0 * oracle_err + 1e-8)
     assert abs(prob.objective(x, p) - oprob.objective(x, p)) <= 1e-12 * max(1.0, abs(oprob.objective(x, p)))
+
+
+def _exact_solve(K, rhs):
+    """Dense LU of K with iterative refinement on double-double residuals (test helper)."""
+    import sys
+    import scipy.linalg as sla
+    sys.path.insert(0, GOLDEN)
+    from make_golden_exact import dd_residual
+    lu = sla.lu_factor(K.toarray())
+    x = sla.lu_solve(lu, rhs)
+    for _ in range(6):
+        x = x + sla.lu_solve(lu, dd_residual(K.tocsr(), x, rhs))
+    return x
 
 
 def test_shell_full_size_direction_matches_reference_golden():
