@@ -93,8 +93,8 @@ typedef struct {
     int32_t fat_tiles;     /* fronts of <= fat_tiles tiles factor as one task (default 0)    */
     int32_t fat_solve;     /* small fronts solve as one task (default 1)                     */
     int32_t generic_pairs; /* generic mode: 2x2 pivots on consecutive unknowns (default 1)   */
-    int32_t upd_pair;      /* 64x64 DMMA blocks: bit 0 grouped Schur updates, bit 1 struct-tile
-                              solve-panel blocks (default 3)                                   */
+    int32_t upd_pair;      /* 64x64 task blocks: bit 0 grouped Schur updates, bit 1 struct-tile
+                              solve-panel blocks, bit 2 front assembly (default 7)             */
     int32_t reserved[6];
 } sgn_symbolic_options;
 void sgn_symbolic_options_default(sgn_symbolic_options* o);

@@ -142,6 +142,89 @@ __device__ void f_asm(const sgn::FactorArgs& A, const DFront& F, int b, int ti, 
       if ((e >> 5) < (e & 31)) tile[e >> 5][e & 31] = 0.0;
 }
 
+// F_ASM with k = 1: the 64x64 block of tiles {ti, ti+1} x {tj, tj+1} in one task (the
+// lower tiles of it; ti, tj even).  Same sources and order as f_asm per entry: original
+// entries, the signed shift on pivot diagonals, then every child's update block extend-
+// added in child order (bitwise identical to four f_asm tiles), with one pass of the
+// latency chain (tile lists, child fronts, relative rows) for up to four tiles.  Block
+// buffer: 64 x 65 doubles in S.b (row-major, conflict-free column write-out); a block
+// holding tile (0, 0) also leaves that tile in S.a for the caller's D_0 factorization.
+constexpr int kA2 = 65;
+__device__ void f_asm2(const sgn::FactorArgs& A, const DFront& F, int b, int ti, int tj, Smem& S) {
+  static_assert(64 * kA2 <= 4 * kTileWords, "64x64 assembly block fits S.b");
+  double* Bk = &S.b[0][0];
+  const int tid = threadIdx.x;
+  const int T = sgn::ntiles_front(F.npiv, F.nrow);
+  for (int e = tid; e < 64 * kA2; e += kFThreads) Bk[e] = 0.0;
+  __syncthreads();
+  const double* vals = A.values + (int64_t)b * A.vstride;
+  const int xlo_i = sgn::tile_lo(F.npiv, ti), xlo_j = sgn::tile_lo(F.npiv, tj);
+  const int mid_i = (ti + 1 < T) ? sgn::tile_lo(F.npiv, ti + 1) : (1 << 30);
+  const int mid_j = (tj + 1 < T) ? sgn::tile_lo(F.npiv, tj + 1) : (1 << 30);
+  // front-local row / col -> block index (the second tile starts at 32)
+  auto bi = [&](int g) { return g < mid_i ? g - xlo_i : 32 + g - mid_i; };
+  auto bj = [&](int g) { return g < mid_j ? g - xlo_j : 32 + g - mid_j; };
+  for (int x = ti; x < min(ti + 2, T); ++x)
+    for (int y = tj; y < min(tj + 2, T); ++y) {
+      if (x < y) continue;
+      const int64_t tg = F.tile_base + (int64_t)x * (x + 1) / 2 + y;
+      const int64_t e0 = A.tile_ptr[tg], e1 = A.tile_ptr[tg + 1];
+      const int ro = 32 * (x - ti), co = 32 * (y - tj);
+      for (int64_t e = e0 + tid; e < e1; e += kFThreads) {
+        const int loc = A.tile_loc[e];
+        Bk[(ro + (loc >> 5)) * kA2 + co + (loc & 31)] = vals[A.tile_nnz[e]];
+      }
+    }
+  __syncthreads();
+  if (ti == tj) {                               // signed shift on the pivot diagonals
+    const int d = tid & 63, x = ti + (d >> 5);
+    if (tid < 64 && x < T) {
+      const int gi = sgn::tile_lo(F.npiv, x) + (d & 31);
+      if (gi < min(F.npiv, sgn::tile_hi(F.npiv, F.nrow, x))) {
+        const int8_t kd = A.kind_pos[F.first + gi];
+        if (kd == 1) Bk[d * kA2 + d] += A.eps_xv ? A.eps_xv[b] : A.eps_x;
+        else if (kd == 2) Bk[d * kA2 + d] -= A.eps_lv ? A.eps_lv[b] : A.eps_l;
+      }
+    }
+  }
+  const double* fb = A.fstore + (int64_t)b * A.fstride;
+  for (int ci = F.child_begin; ci < F.child_end; ++ci) {
+    const DFront C = A.fronts[A.children[ci]];
+    const int cn = C.nrow - C.npiv;
+    __syncthreads();
+    if (cn == 0) continue;
+    const int32_t* rc = A.rel + C.rel_off;
+    const int32_t* rt = A.reltile + C.woff;
+    const int r_lo = rt[ti], r_hi = rt[min(ti + 2, T)], s_lo = rt[tj], s_hi = rt[min(tj + 2, T)];
+    const int nr = r_hi - r_lo, ns = s_hi - s_lo;
+    if (nr <= 0 || ns <= 0) continue;
+    const double* U = fb + C.foff;
+    const int64_t ldc = C.nrow;
+    for (int idx = tid; idx < nr * ns; idx += kFThreads) {
+      const int r = r_lo + idx % nr, s = s_lo + idx / nr;
+      if (r >= s) Bk[bi(rc[r]) * kA2 + bj(rc[s])] += __ldcg(U + (int64_t)(C.npiv + s) * ldc + C.npiv + r);
+    }
+  }
+  __syncthreads();
+  double* Fm = front_ptr(A, F, b);
+  const int64_t ld = F.nrow;
+  for (int e = tid; e < 64 * 64; e += kFThreads) {
+    const int ii = e & 63, jj = e >> 6;
+    const int x = ti + (ii >> 5), y = tj + (jj >> 5);
+    if (x >= T || y >= T || x < y) continue;
+    const int gi = sgn::tile_lo(F.npiv, x) + (ii & 31), gj = sgn::tile_lo(F.npiv, y) + (jj & 31);
+    if (gi < sgn::tile_hi(F.npiv, F.nrow, x) && gj < sgn::tile_hi(F.npiv, F.nrow, y))
+      Fm[(int64_t)gj * ld + gi] = Bk[ii * kA2 + jj];
+  }
+  if (ti == 0 && tj == 0 && F.npiv > 0) {       // D_0 for the caller: tile (0, 0), lower part
+    double (*tile)[kTile + 1] = v33(S.a);
+    for (int e = tid; e < kTile * kTile; e += kFThreads) {
+      const int r = e >> 5, c = e & 31;
+      tile[r][c] = (r >= c) ? Bk[r * kA2 + c] : 0.0;
+    }
+  }
+}
+
 // LDL^T of the w x w diagonal block by one warp (lane i = row i), rows in registers,
 // fully unrolled so every register index is static; the two pivot columns of each step
 // are broadcast through smem (colbuf) -- measured 2.2x faster than shuffles and 9x faster
@@ -467,7 +550,10 @@ __device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int 
       for (int u = 0; u < 8; ++u) {
         const int j = (tid >> 5) + 4 * (u + 8 * hh), cb = bcol(j);
         const double* src = ZP ? Zm : Fm;
-        v[u] = (cb >= 0 && lane < w) ? __ldcg(src + (int64_t)cb * ld + j0 + lane) : 0.0;
+        // Z(j0 + lane, col) of a pivot tile above the column's block is structurally zero
+        // and never stored (only the first column block's s = tj step reaches it)
+        const bool zup = ZP && s < tj + (j >> 5);
+        v[u] = (cb >= 0 && lane < w && !zup) ? __ldcg(src + (int64_t)cb * ld + j0 + lane) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) Bs[((tid >> 5) + 4 * (u + 8 * hh)) * kU2B + lane] = v[u];
@@ -723,7 +809,8 @@ k_factor_dag(const sgn::FactorArgs A) {
     double (*tr_p)[kTile + 1] = v33(S.b[0]);
     double (*tr_l)[kTile + 1] = v33(S.a);
     if (kind == sgn::F_ASM) {
-      f_asm(A, F, b, T.a, T.b, S);
+      if (k == 1) f_asm2(A, F, b, T.a, T.b, S);
+      else f_asm(A, F, b, T.a, T.b, S);
       if (T.a == 0 && T.b == 0 && F.npiv > 0) fac_k = 0;
     } else if (kind == sgn::F_PANEL) {
       nr_trsm = f_panel_pre(A, F, b, k, T.a, S);
@@ -767,6 +854,14 @@ k_factor_dag(const sgn::FactorArgs A) {
         for (int x = T.a; x < min(T.a + 2, Tn); ++x)
           for (int y = tjb; y < min(tjb + 2, Tn); ++y)
             if (x >= y) asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(cf + sgn::cnt_tile(P, x, y)), "r"(ns) : "memory");
+      }
+      else if (kind == sgn::F_ASM && k == 1) {   // every lower tile of the 64x64 block
+        s1 = nullptr;
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        for (int x = T.a; x < min(T.a + 2, Tn); ++x)
+          for (int y = tjb; y < min(tjb + 2, Tn); ++y)
+            if (x >= y) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(cf + sgn::cnt_tile(P, x, y)) : "memory");
+        if (T.a == 0 && T.b == 0 && F.npiv > 0) s3 = cf + sgn::cnt_diag(P, 0);
       }
       else {
         s1 = cf + sgn::cnt_tile(P, T.a, tjb);

@@ -77,7 +77,8 @@ SGN_HD int tile_of_row(int npiv, int r) { return r < npiv ? r / 32 : ptiles(npiv
 // are derived from the coordinates on the device (no stored wait lists).  Per pivot step
 // k of a front the diagonal block D_k is factored ONCE (by the assembly task of tile
 // (0,0) for k = 0, else by F_DIAGUPD(k-1)) and published to scratch as [D | L^T | D^-1]:
-//   F_ASM     (f, a=ti, b=tj): waits DONE(child) == ftotal(child) for every child
+//   F_ASM     (f, a=ti, b=tj): waits DONE(child) == ftotal(child) for every child; k = 1: the
+//                              64x64 block {ti, ti+1} x {tj, tj+1} (its lower tiles)
 //   F_PANEL   (f, k, a=t)    : TRSM of row tiles {k+1} (t = 0) or k+2+4(t-1).. (t >= 1);
 //                              waits DIAG(f, k), TILE(f, i, k) == 1 + k for its rows
 //   F_UPDATE  (f, k, a=ti, b=tj): waits PAN(f, k) == TRSM tasks of step k, TILE(f,ti,tj) == 1+k
@@ -153,8 +154,9 @@ struct SymOptions {
   int32_t fat_tiles = 0;      // fronts of <= fat_tiles tiles factor as one task (0: off)
   int32_t fat_solve = 1;      // small fronts solve as one task
   int32_t generic_pairs = 1;  // generic mode: 2x2 pivots on consecutive unknowns
-  int32_t upd_pair = 3;       // grouped Schur updates on 64x64 blocks (F_UPD2); bit 1: struct-tile
-                              // Z blocks on 64x64 blocks too (F_ZPAN2); default 3 = both
+  int32_t upd_pair = 7;       // grouped Schur updates on 64x64 blocks (F_UPD2); bit 1: struct-tile
+                              // Z blocks on 64x64 blocks too (F_ZPAN2); bit 2: assembly
+                              // on 64x64 blocks (F_ASM, k = 1); default 7 = all
 };
 
 struct Symbolic {

@@ -1175,8 +1175,13 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
     const auto& fl = s.level_fronts[lv];
     for (int32_t f : fl) {
       const int32_t T = ntiles_front(s.fronts[f].npiv, s.fronts[f].nrow);
-      for (int32_t ti = 0; ti < T; ++ti)
-        for (int32_t tj = 0; tj <= ti; ++tj) ft(F_ASM, 0, f, ti, tj);
+      if (opt.upd_pair & 4) {                        // 64x64 assembly blocks (F_ASM, k = 1)
+        for (int32_t ti = 0; ti < T; ti += 2)
+          for (int32_t tj = 0; tj <= ti; tj += 2) ft(F_ASM, 1, f, ti, tj);
+      } else {
+        for (int32_t ti = 0; ti < T; ++ti)
+          for (int32_t tj = 0; tj <= ti; ++tj) ft(F_ASM, 0, f, ti, tj);
+      }
     }
     int32_t maxp = 0;
     for (int32_t f : fl) maxp = std::max(maxp, ptiles(s.fronts[f].npiv));

@@ -555,7 +555,9 @@ def _refine_with_fallback(eng, st, tol, mi):
     if reduced and steps > 0:
         res, corr = eng.kfac.solve_ir(eng.kvals, eng.rhs, eng.sol, steps, st)
         eng.last_ir_correction = corr
-        absorb(res, np.full(B, steps, dtype=np.int32), (res <= tol) & pivots_ok())
+        # an exact residual within tol verifies the solution whatever the pivots were (a zero
+        # pivot is replaced by 1 in the factor, which the residual then exposes)
+        absorb(res, np.full(B, steps, dtype=np.int32), res <= tol)
     if not done.all():
         rc, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
         piv = pivots_ok()

@@ -41,20 +41,30 @@ def main():
         dm = np.abs(d.data).max() if d.nnz else 0.0
         om = np.abs(o.data).max() if o.nnz else 0.0
         print(f"  {nm:10s} nnz {o.nnz:9d} max|K| {om:.3e} max|dK| {dm:.3e} rel {dm / max(om, 1e-300):.2e}", flush=True)
-    rhs = np.zeros(Ko.shape[0])
-    g = gold["grad"]
     dpx = ex["dp_exact"]
     eng = prob.engine
-    for scale, steps in ((1.0, 0), (1e-4, 0), (1e-4, 2), (1e-4, 4)):
+    from paper_2107_03285_b200.engine import kkt_inverse_p
+    prob._load(x, p)
+    eng.assemble()
+    # solver accuracy for a GIVEN right-hand side: (0, -g_reference, 0) against the exact
+    # solution of the oracle KKT for that rhs
+    for scale, steps in ((1.0, 0), (1e-4, 0), (1e-4, 1), (1e-4, 2), (1e-4, 3)):
         eng.factor_shift_scale, eng.ir_steps = scale, steps
+        sol, res, its = kkt_inverse_p(eng, -gold["grad"], factor=True)
+        print(f"given rhs: shift x{scale:g} ir {steps}: res {res:.2e} its {its} | dp vs exact "
+              f"{np.linalg.norm(sol[n_x:n_x + n_p] - dpx) / np.linalg.norm(dpx):.3e} | dx vs exact "
+              f"{np.linalg.norm(sol[:n_x] - ex['dx_exact']) / np.linalg.norm(ex['dx_exact']):.3e}", flush=True)
+    eng.factor_shift_scale, eng.ir_steps = 1e-4, 2
+    from paper_2107_03285_b200 import adjoint_gradient
+    g = adjoint_gradient(prob, x, p)
+    if "g_exact" in ex.files:
+        ge = ex["g_exact"]
+        print(f"gradient vs exact: device {np.linalg.norm(g - ge) / np.linalg.norm(ge):.3e}, reference "
+              f"{np.linalg.norm(gold['grad'] - ge) / np.linalg.norm(ge):.3e}")
         sd = direction_sgn(prob, x, p, OptimizerConfig())
-        sol = np.concatenate([sd.dx, sd.dp, sd.dlam])
-        rhs[n_x:n_x + n_p] = -sd.extra.get("grad", g) if isinstance(sd.extra, dict) and "grad" in sd.extra else -g
-        r_or = np.linalg.norm(dd_residual(Ko.tocsr(), sol, rhs)) / np.linalg.norm(rhs)
-        print(f"shift x{scale:g} ir {steps}: reported res {sd.relative_residual:.2e} its {sd.extra.get('refine_iterations')}"
-              f" | dp vs exact {np.linalg.norm(sd.dp - dpx) / np.linalg.norm(dpx):.3e}"
-              f" | dx vs exact {np.linalg.norm(sd.dx - ex['dx_exact']) / np.linalg.norm(ex['dx_exact']):.3e}"
-              f" | residual vs oracle K (dd) {r_or:.2e}", flush=True)
+        dpe = ex["dp_exact_gexact"]
+        print(f"full direction: dp vs exact(g_exact) {np.linalg.norm(sd.dp - dpe) / np.linalg.norm(dpe):.3e}, "
+              f"reference dp vs exact(g_exact) {np.linalg.norm(gold['dp'] - dpe) / np.linalg.norm(dpe):.3e}")
 
 
 if __name__ == "__main__":

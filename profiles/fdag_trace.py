@@ -11,7 +11,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-KIND = {0: "asm", 1: "panel", 2: "update", 3: "zpanel", 4: "diagupd", 6: "upd2"}
+KIND = {0: "asm", 1: "panel", 2: "update", 3: "zpanel", 4: "diagupd", 6: "upd2", 7: "zpan2"}
 
 
 def main():
