@@ -95,7 +95,9 @@ typedef struct {
     int32_t generic_pairs; /* generic mode: 2x2 pivots on consecutive unknowns (default 1)   */
     int32_t upd_pair;      /* 64x64 task blocks: bit 0 grouped Schur updates, bit 1 struct-tile
                               solve-panel blocks, bit 2 front assembly (default 7)             */
-    int32_t reserved[6];
+    int32_t pair_min_tiles;/* bits 0-1 of upd_pair apply to fronts of >= this many 32-row tiles
+                              (smaller fronts are dependency-chain bound; default 32)          */
+    int32_t reserved[5];
 } sgn_symbolic_options;
 void sgn_symbolic_options_default(sgn_symbolic_options* o);
 /* as sgn_symbolic_create, with options (NULL = defaults) */

@@ -761,22 +761,24 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
 }
 __global__ void k_resid_dd(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                            const double* __restrict__ vals, int64_t vstride,
-                           const double* __restrict__ x, const double* __restrict__ bv,
-                           double* __restrict__ r, int64_t n) {
+                           const double* __restrict__ x, const double* __restrict__ xlo,
+                           const double* __restrict__ bv, double* __restrict__ r, int64_t n) {
   const int b = blockIdx.y;
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
   const int sub = threadIdx.x & 7;
   const bool valid = row < n;
   const double* vb = vals + (int64_t)b * vstride;
   const double* xb = x + (int64_t)b * n;
+  const double* xl = xlo + (int64_t)b * n;
   double s = 0.0, c = 0.0;
   const int64_t kb = valid ? ptr[row] : 0, ke = valid ? ptr[row + 1] : 0;
   for (int64_t k = kb + sub; k < ke; k += 8) {
-    const double v = vb[k], xv = xb[idx[k]];
+    const int32_t j = idx[k];
+    const double v = vb[k], xv = xb[j];
     const double p = v * xv, e = fma(v, xv, -p);
     double t;
     two_sum(s, p, s, t);
-    c += t + e;
+    c += t + e + v * xl[j];      // the low word of x: its product only needs double
   }
 #pragma unroll
   for (int off = 1; off < 8; off <<= 1) {
@@ -792,9 +794,16 @@ __global__ void k_resid_dd(const int64_t* __restrict__ ptr, const int32_t* __res
   }
 }
 
-__global__ void k_add(double* __restrict__ x, const double* __restrict__ d, int64_t len) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
-    x[i] += d[i];
+// (hi, lo) += d, renormalised: the refined solution is carried in double-double
+__global__ void k_add_dd(double* __restrict__ hi, double* __restrict__ lo, const double* __restrict__ d, int64_t len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    double s, e;
+    two_sum(hi[i], d[i], s, e);
+    e += lo[i];
+    const double h = s + e;
+    hi[i] = h;
+    lo[i] = e - (h - s);
+  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -1038,7 +1047,7 @@ struct sgn_factor_s {
   DevBuf<BiState> bst;
   DevBuf<int> gate, dtick;
   // mixed-precision iterative refinement workspace (sgn_solve_ir)
-  DevBuf<double> ir_r, ir_d, ir_out;
+  DevBuf<double> ir_r, ir_d, ir_lo, ir_out;
   bool bicg_ready = false;
   // refinement graphs: prologue + WHILE(any instance iterating){ one BiCGSTAB iteration }
   struct BicgGraph {
@@ -1174,7 +1183,7 @@ void sgn_symbolic_options_default(sgn_symbolic_options* o) {
   o->leaf_size = d.leaf_size; o->p_order = d.p_order; o->upd_group = d.upd_group;
   o->zinline = d.zinline; o->zquota = d.zquota; o->noz_tiles = d.noz_tiles;
   o->fat_tiles = d.fat_tiles; o->fat_solve = d.fat_solve; o->generic_pairs = d.generic_pairs;
-  o->upd_pair = d.upd_pair;
+  o->upd_pair = d.upd_pair; o->pair_min_tiles = d.pair_min_tiles;
 }
 
 int sgn_symbolic_create(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t n_x,
@@ -1197,6 +1206,7 @@ int sgn_symbolic_create_ex(int64_t n, const int64_t* indptr, const int64_t* indi
       so.fat_tiles = opts->fat_tiles; so.fat_solve = opts->fat_solve;
       so.generic_pairs = opts->generic_pairs;
       so.upd_pair = opts->upd_pair;
+      so.pair_min_tiles = opts->pair_min_tiles;
     }
     if (!out || !indptr || n < 0) { sgn::last_error() = "bad arguments"; return SGN_INVALID; }
     auto h = std::make_unique<sgn_symbolic_s>();
@@ -1716,10 +1726,13 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
   return SGN_OK;
 }
 
-// Mixed-precision iterative refinement on the factor: x = M^-1 b, then `steps` times
-// x += M^-1 (b - K x) with the residual in double-double (k_resid_dd); the final residual
-// is evaluated the same way.  rel_res[b] = |b - K x| / |b| (exact residual, rounded),
-// corr[b] = |last correction| / |x|.  One host synchronisation.
+// Extra-precise iterative refinement on the factor: x = M^-1 b, then `steps` times
+// x += M^-1 (b - K x) with the residual in double-double (k_resid_dd) and x itself carried
+// as a double-double (hi, lo) pair -- otherwise the rounding of the large multiplier
+// block alone leaves a residual in the parameter rows that the corrections keep chasing,
+// and dp (which the reduced Hessian amplifies ~1e6-fold on the shell) never settles.  The
+// final residual is evaluated the same way: rel_res[b] = |b - K (hi + lo)| / |b|, corr[b]
+// = |last correction| / |x|; d_sol receives hi.  One host synchronisation.
 int sgn_solve_ir(sgn_factor f, const double* d_values, int64_t values_stride, const double* d_rhs,
                  double* d_sol, int32_t steps, double* rel_res, double* corr, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -1728,20 +1741,23 @@ int sgn_solve_ir(sgn_factor f, const double* d_values, int64_t values_stride, co
   const int B = f->batch;
   const size_t N = (size_t)B * std::max<int64_t>(n, 1);
   int rc;
-  if (!f->ir_r.p && ((rc = f->ir_r.alloc(N)) || (rc = f->ir_d.alloc(N)) || (rc = f->ir_out.alloc(4 * (size_t)B))))
+  if (!f->ir_r.p && ((rc = f->ir_r.alloc(N)) || (rc = f->ir_d.alloc(N)) || (rc = f->ir_lo.alloc(N)) ||
+                      (rc = f->ir_out.alloc(4 * (size_t)B))))
     return rc;
   if ((rc = launch_solve(f, d_rhs, d_sol, 0, st))) return rc;
   const unsigned rb = (unsigned)((n * 8 + 255) / 256);
   CUDA_TRY(cudaMemsetAsync(f->ir_d.p, 0, N * sizeof(double), st));
+  CUDA_TRY(cudaMemsetAsync(f->ir_lo.p, 0, N * sizeof(double), st));
   for (int it = 0; it <= steps; ++it) {
     sgn::count_launch();
-    k_resid_dd<<<dim3(rb, B), 256, 0, st>>>(f->indptr.p, f->idx32.p, d_values, values_stride, d_sol, d_rhs,
-                                            f->ir_r.p, n);
+    k_resid_dd<<<dim3(rb, B), 256, 0, st>>>(f->indptr.p, f->idx32.p, d_values, values_stride, d_sol, f->ir_lo.p,
+                                            d_rhs, f->ir_r.p, n);
     CUDA_TRY(cudaGetLastError());
     if (it == steps) break;
     if ((rc = launch_solve(f, f->ir_r.p, f->ir_d.p, 0, st))) return rc;
     sgn::count_launch();
-    k_add<<<(unsigned)std::min<size_t>((N + 255) / 256, 4096), 256, 0, st>>>(d_sol, f->ir_d.p, (int64_t)N);
+    k_add_dd<<<(unsigned)std::min<size_t>((N + 255) / 256, 4096), 256, 0, st>>>(d_sol, f->ir_lo.p, f->ir_d.p,
+                                                                               (int64_t)N);
     CUDA_TRY(cudaGetLastError());
   }
   double* o = f->ir_out.p;

@@ -1146,13 +1146,14 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
           zq.push_back(FTask{F_ZPANEL, f, t, cb});
           zq_level.push_back(lv);
         }
-      for (int32_t t = P; t < T; t += (opt.upd_pair & 2) ? 2 : 1)   // struct tiles: after every pivot tile
+      const bool zpair = (opt.upd_pair & 2) && T >= opt.pair_min_tiles;
+      for (int32_t t = P; t < T; t += zpair ? 2 : 1)   // struct tiles: after every pivot tile
         for (int32_t cb = 0; cb < P; ++cb) {
-          if ((opt.upd_pair & 2) && cb + 1 < P) {
+          if (zpair && cb + 1 < P) {
             zq.push_back(FTask{F_ZPAN2, f, t, cb++});
           } else {
             zq.push_back(FTask{F_ZPANEL, f, t, cb});
-            if ((opt.upd_pair & 2) && t + 1 < T) {
+            if (zpair && t + 1 < T) {
               zq.push_back(FTask{F_ZPANEL, f, t + 1, cb});
               zq_level.push_back(lv);
             }
@@ -1226,7 +1227,7 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
           if (k <= tj - 3) {
             ns = grouped_ns(tj);
             if (ns == 0) continue;
-            if ((opt.upd_pair & 1) && grouped_ns(tj + 1) == ns) {
+            if ((opt.upd_pair & 1) && T >= opt.pair_min_tiles && grouped_ns(tj + 1) == ns) {
               for (int32_t ti = tj; ti < T; ti += 2) ft(F_UPD2, k, f, ti, tj | (ns << 16));
               ++tj;
               continue;

@@ -27,7 +27,7 @@ def _i64(a) -> np.ndarray:
 _OPTION_ENV = {"leaf_size": "SGN_LEAF_SIZE", "upd_group": "SGN_UPD_GROUP", "zinline": "SGN_ZINLINE",
                "zquota": "SGN_ZQUOTA", "noz_tiles": "SGN_NOZ_TILES", "fat_tiles": "SGN_FAT_TILES",
                "fat_solve": "SGN_FAT_SOLVE", "generic_pairs": "SGN_GENERIC_PAIRS", "p_order": "SGN_P_ORDER",
-               "upd_pair": "SGN_UPD_PAIR"}
+               "upd_pair": "SGN_UPD_PAIR", "pair_min_tiles": "SGN_PAIR_MIN_TILES"}
 
 
 def symbolic_options(**kw) -> "_lib.SymbolicOptions":

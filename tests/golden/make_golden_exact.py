@@ -62,9 +62,10 @@ def _two_sum(a, b):
     return s, (a - (s - bb)) + (b - bb)
 
 
-def dd_residual(a: sp.csr_matrix, x: np.ndarray, b: np.ndarray) -> np.ndarray:
-    """b - a @ x with double-double accuracy, rounded to double (rows padded to the max
-    row length, summed column by column with TwoSum and a compensation term)."""
+def dd_residual(a: sp.csr_matrix, x: np.ndarray, b: np.ndarray, x_lo=None) -> np.ndarray:
+    """b - a @ (x + x_lo) with double-double accuracy, rounded to double (rows padded to the
+    max row length, summed column by column with TwoSum and a compensation term; the low
+    word x_lo of a double-double x only needs double products)."""
     a = a.tocsr()
     n = a.shape[0]
     cnt = np.diff(a.indptr)
@@ -76,7 +77,7 @@ def dd_residual(a: sp.csr_matrix, x: np.ndarray, b: np.ndarray) -> np.ndarray:
     P[np.repeat(np.arange(n), cnt), pos] = -p
     E[np.repeat(np.arange(n), cnt), pos] = -e
     s = b.astype(np.float64).copy()
-    comp = np.zeros(n)
+    comp = np.zeros(n) if x_lo is None else -(a @ x_lo)
     for k in range(width):
         s, err = _two_sum(s, P[:, k])
         comp += err + E[:, k]
@@ -93,21 +94,24 @@ def exact_solve(a, M, rhs, max_outer=12, log=print):
     bnorm = np.linalg.norm(rhs)
     x = M.solve(rhs)
     x, res, it = sgn_cpu.bicgstab_refine(ac, rhs, x, M, 1e-10, 50)
+    lo = np.zeros_like(x)                 # x is carried as a double-double (x, lo)
     hist = [(0, res, it, float("nan"))]
     log(f"reference-style solve: residual {res:.3e} after {it} BiCGSTAB iterations")
     for k in range(1, max_outer + 1):
-        r = dd_residual(a, x, rhs)
+        r = dd_residual(a, x, rhs, lo)
         rr = np.linalg.norm(r) / bnorm
         d0 = M.solve(r)
         d, dres, dit = sgn_cpu.bicgstab_refine(ac, r, d0, M, 1e-10, 50)
-        x_new = x + d
-        step = np.linalg.norm(x_new - x) / np.linalg.norm(x_new)
-        x = x_new
+        s, e = _two_sum(x, d)
+        e = e + lo
+        x = s + e
+        lo = e - (x - s)
+        step = np.linalg.norm(d) / np.linalg.norm(x)
         hist.append((k, rr, dit, step))
         log(f"outer {k}: exact residual before {rr:.3e}, correction {step:.3e} ({dit} BiCGSTAB its)")
-        if step < 1e-15:
+        if step < 1e-22:
             break
-    rr = np.linalg.norm(dd_residual(a, x, rhs)) / bnorm
+    rr = np.linalg.norm(dd_residual(a, x, rhs, lo)) / bnorm
     hist.append((-1, rr, 0, 0.0))
     log(f"final exact residual {rr:.3e}")
     return x, np.array(hist)
@@ -124,17 +128,21 @@ def exact_gradient(prob, x, p, log=print):
     fx, fp = sgn_cpu.objective_grads(prob, x, p)
     GT = Gx.T.tocsr()
     lam = -F.solve(fx, transpose=True)
-    for k in range(8):
-        r = dd_residual(GT, lam, -fx)
+    lo = np.zeros_like(lam)
+    for k in range(12):
+        r = dd_residual(GT, lam, -fx, lo)
         d = F.solve(r, transpose=True)
-        lam = lam + d
+        s, e = _two_sum(lam, d)
+        e = e + lo
+        lam = s + e
+        lo = e - (lam - s)
         step = np.linalg.norm(d) / np.linalg.norm(lam)
         log(f"adjoint refinement {k + 1}: correction {step:.3e}")
-        if step < 1e-16:
+        if step < 1e-22:
             break
     Gp = prob.constraint_jac_p(x, p).to_scipy().tocsr()
     # f_p + G_p^T lambda with exact products and compensated sums (rows of G_p^T)
-    g = -dd_residual(Gp.T.tocsr(), lam, -fp)
+    g = -dd_residual(Gp.T.tocsr(), lam, -fp, lo)
     return g
 
 

@@ -96,8 +96,13 @@ def _exact_solve(K, rhs):
     from make_golden_exact import dd_residual
     lu = sla.lu_factor(K.toarray())
     x = sla.lu_solve(lu, rhs)
-    for _ in range(6):
-        x = x + sla.lu_solve(lu, dd_residual(K.tocsr(), x, rhs))
+    lo = np.zeros_like(x)               # x carried as a double-double
+    for _ in range(8):
+        d = sla.lu_solve(lu, dd_residual(K.tocsr(), x, rhs, lo))
+        s = x + d
+        e = (x - (s - (s - x))) + (d - (s - x)) + lo
+        x = s + e
+        lo = e - (x - s)
     return x
 
 
