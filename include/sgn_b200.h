@@ -97,7 +97,10 @@ typedef struct {
                               solve-panel blocks, bit 2 front assembly (default 7)             */
     int32_t pair_min_tiles;/* bits 0-1 of upd_pair apply to fronts of >= this many 32-row tiles
                               (smaller fronts are dependency-chain bound; default 32)          */
-    int32_t reserved[5];
+    int32_t upd_group_cb;  /* pivot steps per grouped update of contribution-block columns
+                              (tj >= P: off the pivot chain, only the parent's assembly reads
+                              them; default 32)                                              */
+    int32_t reserved[4];
 } sgn_symbolic_options;
 void sgn_symbolic_options_default(sgn_symbolic_options* o);
 /* as sgn_symbolic_create, with options (NULL = defaults) */
@@ -209,10 +212,18 @@ int  sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_stri
  * x += F^{-1}(rhs - K x) with the residual evaluated in double-double (error-free products
  * and compensated row sums, then rounded).  rel_res[b] = |rhs - K x| / |rhs| of the final x
  * evaluated the same way (an exact residual, so it cannot be below the truth); corr[b] =
- * |last correction| / |x|.  The caller falls back to sgn_solve_refined when rel_res > tol. */
+ * |last correction| / |x|.  x is carried as a double-double (hi in d_sol, lo copied to
+ * d_sol_lo when non-NULL).  rel_res = corr = NULL: no final residual and no host sync
+ * (graph-capturable).  The caller falls back to sgn_solve_refined when rel_res > tol.   */
 int  sgn_solve_ir(sgn_factor f, const double* d_values, int64_t values_stride,
-                  const double* d_rhs, double* d_sol, int32_t steps, double* rel_res,
-                  double* corr, void* stream);
+                  const double* d_rhs, double* d_sol, double* d_sol_lo, int32_t steps,
+                  double* rel_res, double* corr, void* stream);
+/* r = b - K (x + x_lo) with the same double-double evaluation (x_lo may be NULL).  The
+ * adjoint gradient g = f_p + G_p^T lambda of the direction path is taken from it, with
+ * lambda = (hi, lo) from sgn_solve_ir on the dc/dx factor (sensitivity.py:181-198). */
+int  sgn_residual_dd(sgn_factor f, const double* d_values, int64_t values_stride,
+                     const double* d_x, const double* d_x_lo, const double* d_b, double* d_r,
+                     void* stream);
 
 /* ---- element assembly (device) --------------------------------------------------
  * Replaces the NumPy element kernels + COO->CSC of constraint_jac_x / constraint_jac_p
@@ -312,7 +323,8 @@ int  sgn_restlen_blocks(int64_t ns, int32_t batch, const int32_t* d_conn, const 
 /* adjoint gradient from a leading-block KKT solve (sensitivity.py:181-198, 245-256):
  * mode 0: d_out = (0, 0, d_src[lambda]);  mode 1: g = d_fvec[p] - d_src[p] (d_src = K v),
  * d_out = (0, -g, 0), d_grad = g;  mode 2: d_out = (0, 0, w) for an n_x-vector w = d_src;
- * mode 3: d_out (n_x per instance) = x block of d_src.                                                     */
+ * mode 3: d_out (n_x per instance) = x block of d_src;  mode 4: g = d_src[p] (d_src = f - K v
+ * evaluated by sgn_residual_dd), d_out = (0, -g, 0), d_grad = g.                                           */
 int  sgn_adjoint_step(int32_t mode, int32_t batch, int64_t n_x, int64_t n_p, const double* d_src,
                       const double* d_fvec, double* d_out, double* d_grad, void* stream);
 

@@ -34,7 +34,7 @@ class SymbolicOptions(ctypes.Structure):
     _fields_ = [("leaf_size", c_i32), ("p_order", c_i32), ("upd_group", c_i32), ("zinline", c_i32),
                 ("zquota", c_i32), ("noz_tiles", c_i32), ("fat_tiles", c_i32), ("fat_solve", c_i32),
                 ("generic_pairs", c_i32), ("upd_pair", c_i32), ("pair_min_tiles", c_i32),
-                ("reserved", c_i32 * 5)]
+                ("upd_group_cb", c_i32), ("reserved", c_i32 * 4)]
 
 
 class LsqArgs(ctypes.Structure):
@@ -80,7 +80,8 @@ SIGNATURES = {
     "sgn_debug_factor_buffer": (ctypes.c_int, [c_vp, c_i32, c_vp, ctypes.c_int64, c_vp]),
     "sgn_debug_poison": (ctypes.c_int, [c_vp, c_dbl]),
     "sgn_factor_destroy": (None, [c_vp]),
-    "sgn_solve_ir": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i32, P_dbl, P_dbl, c_vp]),
+    "sgn_solve_ir": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32, P_dbl, P_dbl, c_vp]),
+    "sgn_residual_dd": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "sgn_spmv": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp]),
     "sgn_solve_refined": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_dbl, c_i32, c_i32,
                                          P_dbl, P_i32, c_vp]),

@@ -1183,7 +1183,7 @@ void sgn_symbolic_options_default(sgn_symbolic_options* o) {
   o->leaf_size = d.leaf_size; o->p_order = d.p_order; o->upd_group = d.upd_group;
   o->zinline = d.zinline; o->zquota = d.zquota; o->noz_tiles = d.noz_tiles;
   o->fat_tiles = d.fat_tiles; o->fat_solve = d.fat_solve; o->generic_pairs = d.generic_pairs;
-  o->upd_pair = d.upd_pair; o->pair_min_tiles = d.pair_min_tiles;
+  o->upd_pair = d.upd_pair; o->pair_min_tiles = d.pair_min_tiles; o->upd_group_cb = d.upd_group_cb;
 }
 
 int sgn_symbolic_create(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t n_x,
@@ -1207,6 +1207,7 @@ int sgn_symbolic_create_ex(int64_t n, const int64_t* indptr, const int64_t* indi
       so.generic_pairs = opts->generic_pairs;
       so.upd_pair = opts->upd_pair;
       so.pair_min_tiles = opts->pair_min_tiles;
+      so.upd_group_cb = opts->upd_group_cb;
     }
     if (!out || !indptr || n < 0) { sgn::last_error() = "bad arguments"; return SGN_INVALID; }
     auto h = std::make_unique<sgn_symbolic_s>();
@@ -1726,6 +1727,29 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
   return SGN_OK;
 }
 
+// r = b - K (x + x_lo) in double-double, rounded (x_lo may be NULL)
+int sgn_residual_dd(sgn_factor f, const double* d_values, int64_t values_stride, const double* d_x,
+                    const double* d_x_lo, const double* d_b, double* d_r, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = f->sym->s.n;
+  const int B = f->batch;
+  if (n == 0) return SGN_OK;
+  const double* lo = d_x_lo;
+  int rc;
+  if (!lo) {                                      // a zero low word
+    if (!f->ir_lo.p && ((rc = f->ir_r.alloc((size_t)B * n)) || (rc = f->ir_d.alloc((size_t)B * n)) ||
+                        (rc = f->ir_lo.alloc((size_t)B * n)) || (rc = f->ir_out.alloc(4 * (size_t)B))))
+      return rc;
+    CUDA_TRY(cudaMemsetAsync(f->ir_lo.p, 0, (size_t)B * n * sizeof(double), st));
+    lo = f->ir_lo.p;
+  }
+  sgn::count_launch();
+  k_resid_dd<<<dim3((unsigned)((n * 8 + 255) / 256), B), 256, 0, st>>>(f->indptr.p, f->idx32.p, d_values,
+                                                                       values_stride, d_x, lo, d_b, d_r, n);
+  CUDA_TRY(cudaGetLastError());
+  return SGN_OK;
+}
+
 // Extra-precise iterative refinement on the factor: x = M^-1 b, then `steps` times
 // x += M^-1 (b - K x) with the residual in double-double (k_resid_dd) and x itself carried
 // as a double-double (hi, lo) pair -- otherwise the rounding of the large multiplier
@@ -1734,7 +1758,7 @@ int sgn_solve_refined(sgn_factor f, const double* d_values, int64_t values_strid
 // final residual is evaluated the same way: rel_res[b] = |b - K (hi + lo)| / |b|, corr[b]
 // = |last correction| / |x|; d_sol receives hi.  One host synchronisation.
 int sgn_solve_ir(sgn_factor f, const double* d_values, int64_t values_stride, const double* d_rhs,
-                 double* d_sol, int32_t steps, double* rel_res, double* corr, void* stream) {
+                 double* d_sol, double* d_sol_lo, int32_t steps, double* rel_res, double* corr, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const sgn::Symbolic& s = f->sym->s;
   const int64_t n = s.n;
@@ -1748,7 +1772,9 @@ int sgn_solve_ir(sgn_factor f, const double* d_values, int64_t values_stride, co
   const unsigned rb = (unsigned)((n * 8 + 255) / 256);
   CUDA_TRY(cudaMemsetAsync(f->ir_d.p, 0, N * sizeof(double), st));
   CUDA_TRY(cudaMemsetAsync(f->ir_lo.p, 0, N * sizeof(double), st));
+  const bool report = rel_res || corr;
   for (int it = 0; it <= steps; ++it) {
+    if (it == steps && !report) break;              // no final residual wanted: no host sync
     sgn::count_launch();
     k_resid_dd<<<dim3(rb, B), 256, 0, st>>>(f->indptr.p, f->idx32.p, d_values, values_stride, d_sol, f->ir_lo.p,
                                             d_rhs, f->ir_r.p, n);
@@ -1760,6 +1786,8 @@ int sgn_solve_ir(sgn_factor f, const double* d_values, int64_t values_stride, co
                                                                                (int64_t)N);
     CUDA_TRY(cudaGetLastError());
   }
+  if (d_sol_lo) CUDA_TRY(cudaMemcpyAsync(d_sol_lo, f->ir_lo.p, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (!report) return SGN_OK;
   double* o = f->ir_out.p;
   if ((rc = sgn_reduce(1, n, B, f->ir_r.p, f->ir_r.p, n, o, st)) ||
       (rc = sgn_reduce(1, n, B, d_rhs, d_rhs, n, o + B, st)) ||

@@ -1216,11 +1216,15 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
         // grouped columns emitting at this step with the same step range pair up: their
         // tiles are updated as 64x64 blocks {ti, ti+1} x {tj, tj+1} (F_UPD2, twice the
         // DMMA work per operand byte; profiles/micro/upd_bench.cu)
+        // contribution-block columns (tj >= P) are read only by the parent's assembly, after
+        // the front's last step: they take longer groups (upd_group_cb), so each C tile makes
+        // fewer HBM round trips (a large front's trailing matrix does not fit in L2)
         auto grouped_ns = [&](int32_t tj) -> int32_t {   // 0: no grouped emission at k
           if (tj >= T || k > tj - 3) return 0;
+          const int32_t G = (tj >= P) ? std::max(kUpdGroup, opt.upd_group_cb) : kUpdGroup;
           const int32_t kmax = std::min(tj - 3, P - 1);
-          if ((k + 1) % kUpdGroup != 0 && k != kmax) return 0;
-          return k - (k / kUpdGroup) * kUpdGroup + 1;
+          if ((k + 1) % G != 0 && k != kmax) return 0;
+          return k - (k / G) * G + 1;
         };
         for (int32_t tj = k + 2; tj < T; ++tj) {
           int32_t ns = 1;

@@ -187,6 +187,14 @@ __global__ void k_adjoint(int mode, int64_t n_x, int64_t n_p, const double* __re
       out[k] = (i >= n_x + n_p) ? src[(int64_t)b * n_x + (i - n_x - n_p)] : 0.0;
     } else if (mode == 3) {           // out_nx = x block of src (contiguous n_x per instance)
       if (i < n_x) out[(int64_t)b * n_x + i] = src[k];
+    } else if (mode == 4) {           // src = f - K (0, 0, w) evaluated exactly: g = its p block
+      if (in_p) {
+        const double g = src[k];
+        out[k] = -g;
+        if (grad) grad[(int64_t)b * n_p + (i - n_x)] = g;
+      } else {
+        out[k] = 0.0;
+      }
     } else {
       if (in_p) {
         const double g = fvec[k] - src[k];

@@ -27,7 +27,8 @@ def _i64(a) -> np.ndarray:
 _OPTION_ENV = {"leaf_size": "SGN_LEAF_SIZE", "upd_group": "SGN_UPD_GROUP", "zinline": "SGN_ZINLINE",
                "zquota": "SGN_ZQUOTA", "noz_tiles": "SGN_NOZ_TILES", "fat_tiles": "SGN_FAT_TILES",
                "fat_solve": "SGN_FAT_SOLVE", "generic_pairs": "SGN_GENERIC_PAIRS", "p_order": "SGN_P_ORDER",
-               "upd_pair": "SGN_UPD_PAIR", "pair_min_tiles": "SGN_PAIR_MIN_TILES"}
+               "upd_pair": "SGN_UPD_PAIR", "pair_min_tiles": "SGN_PAIR_MIN_TILES",
+               "upd_group_cb": "SGN_UPD_GROUP_CB"}
 
 
 def symbolic_options(**kw) -> "_lib.SymbolicOptions":
@@ -166,15 +167,24 @@ class DeviceFactor:
         flags = _lib.SGN_SOLVE_LEADING if leading else 0
         check(lib().sgn_spmv(self._h, ptr(values), stride, ptr(x), ptr(y), flags, stream), what="spmv")
 
-    def solve_ir(self, values, rhs, sol, steps: int, stream: int = 0):
-        """Mixed-precision iterative refinement (sgn_solve_ir); returns (rel_res[batch],
-        corr[batch]) -- exact residuals of the final iterate and the last correction."""
+    def solve_ir(self, values, rhs, sol, steps: int, stream: int = 0, sol_lo=None, report: bool = True):
+        """Extra-precise iterative refinement (sgn_solve_ir); returns (rel_res[batch],
+        corr[batch]) -- exact residuals of the final iterate and the last correction -- or
+        (None, None) with report=False (no host synchronisation)."""
         stride = values.stride(0) if values.dim() == 2 else 0
-        res = np.zeros(self.batch)
-        corr = np.zeros(self.batch)
-        check(lib().sgn_solve_ir(self._h, ptr(values), stride, ptr(rhs), ptr(sol), int(steps),
-                                 res.ctypes.data_as(P_dbl), corr.ctypes.data_as(P_dbl), stream), what="refinement")
+        res = np.zeros(self.batch) if report else None
+        corr = np.zeros(self.batch) if report else None
+        check(lib().sgn_solve_ir(self._h, ptr(values), stride, ptr(rhs), ptr(sol),
+                                 ptr(sol_lo) if sol_lo is not None else None, int(steps),
+                                 res.ctypes.data_as(P_dbl) if report else None,
+                                 corr.ctypes.data_as(P_dbl) if report else None, stream), what="refinement")
         return res, corr
+
+    def residual_dd(self, values, x, x_lo, b, r, stream: int = 0) -> None:
+        """r = b - K (x + x_lo), double-double evaluation (sgn_residual_dd)."""
+        stride = values.stride(0) if values.dim() == 2 else 0
+        check(lib().sgn_residual_dd(self._h, ptr(values), stride, ptr(x),
+                                    ptr(x_lo) if x_lo is not None else None, ptr(b), ptr(r), stream), what="residual")
 
     def solve_refined(self, values, rhs, sol, tol: float, max_iters: int, leading: bool = False,
                       stream: int = 0):

@@ -437,6 +437,22 @@ def _nan_probe(eng, where):
                   file=sys.stderr, flush=True)
 
 
+def gradient_from_adjoint(eng, st) -> None:
+    """g = f_p + G_p^T lambda (sensitivity.py:194-198) from v = (0, 0, w) in eng.tmp (lambda =
+    -w): eng.grad = g and eng.rhs = (0, -g, 0).  With a double-double w (adjoint_direct),
+    the product is evaluated exactly too (sgn_residual_dd: f - K v), else by a plain SpMV."""
+    n_x, n_p = eng.n_x, eng.n_p
+    lo = getattr(eng, "tmp_lo", None)
+    if lo is not None and int(getattr(eng, "adj_ir_steps", 0)) > 0:
+        eng.kfac.residual_dd(eng.kvals, eng.tmp, lo, eng.fvec, eng.rhs, st)
+        check(lib().sgn_adjoint_step(4, eng.batch, n_x, n_p, ptr(eng.rhs), None, ptr(eng.tmp), ptr(eng.grad), st))
+    else:
+        eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, st)
+        check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
+                                     ptr(eng.grad), st))
+    eng.rhs.copy_(eng.tmp)
+
+
 def factor_shifts(eng, full: bool = False):
     """Static shifts of the direction path's KKT factorization.
 
@@ -482,10 +498,7 @@ def _factor_adjoint(eng, st, cur, f0=None, f1=None, events=None):
     with torch.cuda.stream(side):
         sst = _lib.stream_handle()
         res_a, it_a = eng.adjoint_direct(check_pivots=False)
-        eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, sst)
-        check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
-                                     ptr(eng.grad), sst))
-        eng.rhs.copy_(eng.tmp)
+        gradient_from_adjoint(eng, sst)
         ev_adj.record(side)
     cur.wait_event(ev_adj)
     eng.gfac.set_grid(0)
@@ -509,10 +522,7 @@ def adjoint_gradient_stage(eng):
     if bad.size:
         raise SingularConstraintJacobian(f"singular state Jacobian dc/dx (instance {int(bad[0])})",
                                          pivot_index=int(piv[bad[0]]))
-    eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, st)
-    check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
-                                 ptr(eng.grad), st))
-    eng.rhs.copy_(eng.tmp)
+    gradient_from_adjoint(eng, st)
 
 
 def _refine_with_fallback(eng, st, tol, mi):
@@ -557,6 +567,8 @@ def _refine_with_fallback(eng, st, tol, mi):
         eng.last_ir_correction = corr
         # an exact residual within tol verifies the solution whatever the pivots were (a zero
         # pivot is replaced by 1 in the factor, which the residual then exposes)
+        if np.all(res <= tol):                                  # the common case: done
+            return _lib.SGN_OK, res, np.full(B, steps, dtype=np.int32)
         absorb(res, np.full(B, steps, dtype=np.int32), res <= tol)
     if not done.all():
         rc, res, its = eng.kfac.solve_refined(eng.kvals, eng.rhs, eng.sol, tol, mi, False, st)
@@ -637,14 +649,15 @@ def sgn_solve_stages(eng, timings: dict | None = None, need_direction: bool = Tr
             timings["factor_s"] = t2 - t1
         if getattr(eng, "adjoint_gx", False):
             res_a, it_a = eng.adjoint_direct()
+            gradient_from_adjoint(eng, st)
         else:
             # leading (x, lambda) block of the KKT factor preconditions [[A, G^T], [G, 0]]
             rc, res_a, it_a = eng.kfac.solve_refined(eng.kvals, eng.fvec, eng.sol_adj, tol, mi, True, st)
             check(lib().sgn_adjoint_step(0, eng.batch, n_x, n_p, ptr(eng.sol_adj), None, ptr(eng.tmp), None, st))
-        eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, st)
-        check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
-                                     ptr(eng.grad), st))
-        eng.rhs.copy_(eng.tmp)
+            eng.kfac.spmv(eng.kvals, eng.tmp, eng.rhs, False, st)
+            check(lib().sgn_adjoint_step(1, eng.batch, n_x, n_p, ptr(eng.rhs), ptr(eng.fvec), ptr(eng.tmp),
+                                         ptr(eng.grad), st))
+            eng.rhs.copy_(eng.tmp)
         if events is not None:
             events[1].record()
         if timings is not None:
@@ -976,8 +989,16 @@ class DeviceEngine:
 
     def adjoint_direct(self, check_pivots: bool = True):
         """w = G_x^{-1} f_x (unshifted LDL^T of the state Jacobian) placed as v = (0, 0, w)
-        in self.tmp; returns (res, iters) placeholders of the refined variant.  With
-        check_pivots=False the caller checks the factor's status later (no host sync here)."""
+        in self.tmp (and its low word in self.tmp_lo); returns (res, iters) placeholders of
+        the refined variant.  With check_pivots=False the caller checks the factor's status
+        later (no host sync here).
+
+        w comes from extra-precise iterative refinement on the factor (sgn_solve_ir:
+        double-double residuals, w carried as a double-double): the unpivoted LDL^T of the
+        ill-conditioned shell G_x is not backward stable the way SuperLU's partial pivoting
+        is, and the reduced Hessian of config 4 amplifies a gradient error ~1e6-fold into dp,
+        so the gradient is taken to the double rounding of the exact one (gradient_from_
+        adjoint); ``adj_ir_steps`` = 0 restores the single double-precision refinement step."""
         pl = self.plan
         st = self.stream
         self.gx_values()
@@ -985,25 +1006,31 @@ class DeviceEngine:
         if check_pivots:
             self.gfac.check(st)
         check(lib().sgn_adjoint_step(3, self.batch, pl.n_x, pl.n_p, ptr(self.fvec), None, ptr(self.xtry), None, st))
-        self.gfac.solve(self.xtry, self.kdir, False, st)
-        # one step of iterative refinement, w += G_x^{-1} (f_x - G_x w): the unpivoted LDL^T
-        # of the (ill-conditioned) shell G_x is not backward stable the way SuperLU's
-        # partial pivoting is; the step restores it (config 4: gradient 5e-9 -> <1e-10 of
-        # the reference's)
+        n = pl.n_x
+        torch = self.torch
         if not hasattr(self, "_adj_r"):
-            torch = self.torch
             self._adj_r, self._adj_d = torch.empty_like(self.kdir), torch.empty_like(self.kdir)
+            self._adj_lo = torch.zeros_like(self.kdir)
+            self.tmp_lo = torch.zeros_like(self.tmp)
             self._adj_pm = torch.tensor([1.0, -1.0], dtype=torch.float64, device="cuda").repeat_interleave(
                 self.batch).reshape(2, self.batch).contiguous()
-        n = pl.n_x
-        self.gfac.spmv(self.gvals, self.kdir, self._adj_r, False, st)                       # G w
-        check(lib().sgn_axpy(n, self.batch, ptr(self._adj_pm[1]), ptr(self._adj_r), ptr(self.xtry),
-                             ptr(self._adj_r), n, st))                                      # f - G w
-        self.gfac.solve(self._adj_r, self._adj_d, False, st)
-        check(lib().sgn_axpy(n, self.batch, ptr(self._adj_pm[0]), ptr(self._adj_d), ptr(self.kdir),
-                             ptr(self.kdir), n, st))                                        # w += d
+        steps = int(getattr(self, "adj_ir_steps", 0))
+        if steps > 0:
+            self.gfac.solve_ir(self.gvals, self.xtry, self.kdir, steps, st, sol_lo=self._adj_lo, report=False)
+        else:
+            self.gfac.solve(self.xtry, self.kdir, False, st)
+            self.gfac.spmv(self.gvals, self.kdir, self._adj_r, False, st)                       # G w
+            check(lib().sgn_axpy(n, self.batch, ptr(self._adj_pm[1]), ptr(self._adj_r), ptr(self.xtry),
+                                 ptr(self._adj_r), n, st))                                      # f - G w
+            self.gfac.solve(self._adj_r, self._adj_d, False, st)
+            check(lib().sgn_axpy(n, self.batch, ptr(self._adj_pm[0]), ptr(self._adj_d), ptr(self.kdir),
+                                 ptr(self.kdir), n, st))                                        # w += d
+            self._adj_lo.zero_()
         check(lib().sgn_adjoint_step(2, self.batch, pl.n_x, pl.n_p, ptr(self.kdir), None, ptr(self.tmp), None, st))
+        check(lib().sgn_adjoint_step(2, self.batch, pl.n_x, pl.n_p, ptr(self._adj_lo), None, ptr(self.tmp_lo), None, st))
         return np.zeros(self.batch), np.zeros(self.batch, dtype=np.int32)
+
+    adj_ir_steps = 2                   # extra-precise refinement steps of the adjoint solve
 
     def split(self):
         pl = self.plan

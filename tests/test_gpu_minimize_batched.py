@@ -29,8 +29,8 @@ def batched_run(cuda):
 def test_batched_trajectories_match_reference_minimize(batched_run):
     """The reference run of each instance ends when a direction's refinement stalls above
     1e-10 (its minimize raises NoConvergence, optimize.py:389; after 7-10 iterations here),
-    so the trajectories are compared over the iterations both runs completed; where a run
-    stopped, the other must stop within two iterations for the same reason."""
+    so the trajectories are compared over the iterations both runs completed; the device run
+    evaluates that residual exactly (double-double) and continues past the reference's stop."""
     _, run = batched_run
     gold = np.load(os.path.join(GOLDEN, "large_c5.npz"))
     for b, inst in enumerate((1, 2, 3)):
@@ -52,8 +52,10 @@ def test_batched_trajectories_match_reference_minimize(batched_run):
         ratio = run.alpha[b][6:n] / ref_alpha[6:n]
         assert np.all(np.isin(np.log2(ratio), np.arange(-6, 7))), (inst, run.alpha[b][:n], ref_alpha[:n])
         if f.size != ref_f.size:
-            assert abs(f.size - ref_f.size) <= 2
-            assert "direction_no_convergence" in (run.termination[b], ref_term)
+            # the reference's run ends when its refinement stalls above 1e-10 on the double-
+            # precision residual floor (linear_solvers.py:168); the device refinement evaluates
+            # the residual exactly (sgn_solve_ir), meets 1e-10 and carries on
+            assert ref_term == "direction_no_convergence" and f.size > ref_f.size, (ref_term, f.size, ref_f.size)
         extra = run.termination[b] in ("line_search_failure", "no_descent", "stationary", "direction_no_convergence")
         assert run.directions[b] == f.size - 1 + extra
 
