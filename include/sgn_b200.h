@@ -95,8 +95,9 @@ typedef struct {
     int32_t generic_pairs; /* generic mode: 2x2 pivots on consecutive unknowns (default 1)   */
     int32_t upd_pair;      /* 64x64 task blocks: bit 0 grouped Schur updates, bit 1 struct-tile
                               solve-panel blocks, bit 2 front assembly (default 7)             */
-    int32_t pair_min_tiles;/* bits 0-1 of upd_pair apply to fronts of >= this many 32-row tiles
-                              (smaller fronts are dependency-chain bound; default 32)          */
+    int32_t pair_min_tiles;/* bits 0-1 of upd_pair apply to fronts of >= this many 32-row tiles;
+                              0 (default) = auto: 4 when the factorization has >= 5e9 flops,
+                              else none (small factorizations are pivot-chain bound)          */
     int32_t upd_group_cb;  /* pivot steps per grouped update of contribution-block columns
                               (tj >= P: off the pivot chain, only the parent's assembly reads
                               them; default 32)                                              */

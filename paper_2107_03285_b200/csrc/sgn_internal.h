@@ -157,7 +157,7 @@ struct SymOptions {
   int32_t upd_pair = 7;       // grouped Schur updates on 64x64 blocks (F_UPD2); bit 1: struct-tile
                               // Z blocks on 64x64 blocks too (F_ZPAN2); bit 2: assembly
                               // on 64x64 blocks (F_ASM, k = 1); default 7 = all
-  int32_t pair_min_tiles = 32; // bits 0-1 apply to fronts of >= this many tiles
+  int32_t pair_min_tiles = 0; // bits 0-1 apply to fronts of >= this many tiles (0: auto)
   int32_t upd_group_cb = 32;  // pivot steps per grouped update of contribution-block columns
 };
 

@@ -989,6 +989,7 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
   s.nnz_l = 0;
   s.flops = 0;
   s.max_front = s.max_piv = 0;
+  int32_t pair_tiles = 1 << 30;
   // The root p-front of a large n_p (>= kNoZTiles pivot tiles, no contribution rows) gets no
   // solve panel: forming L11^{-1} costs npiv^3/3 flops (as much as its factorization) and a
   // column-serial tail, to speed up a handful of solves.  Its solves are blocked
@@ -1012,6 +1013,13 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
     s.max_front = std::max<int64_t>(s.max_front, nr);
     s.max_piv = std::max<int64_t>(s.max_piv, F.npiv);
   }
+
+  // 64x64 update / Z blocks (upd_pair bits 0-1) pay where the factorization is throughput
+  // bound; a small factorization is bound by its top fronts' pivot chain, which longer
+  // tasks only lengthen (config 2: factor 1.63 -> 1.79 ms with pairs, config 4: 51.5 ->
+  // 46.6 ms).  pair_min_tiles = 0 (auto): fronts of >= 4 tiles when the factorization has
+  // >= 5e9 flops, else none.
+  pair_tiles = opt.pair_min_tiles > 0 ? opt.pair_min_tiles : (s.flops >= 5e9 ? 4 : (1 << 30));
 
   // stabilization kind per position
   // generic mode: every diagonal takes +eps_x (tau-regularized Newton, forward.py:171-186)
@@ -1146,7 +1154,7 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
           zq.push_back(FTask{F_ZPANEL, f, t, cb});
           zq_level.push_back(lv);
         }
-      const bool zpair = (opt.upd_pair & 2) && T >= opt.pair_min_tiles;
+      const bool zpair = (opt.upd_pair & 2) && T >= pair_tiles;
       for (int32_t t = P; t < T; t += zpair ? 2 : 1)   // struct tiles: after every pivot tile
         for (int32_t cb = 0; cb < P; ++cb) {
           if (zpair && cb + 1 < P) {
@@ -1231,7 +1239,7 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
           if (k <= tj - 3) {
             ns = grouped_ns(tj);
             if (ns == 0) continue;
-            if ((opt.upd_pair & 1) && T >= opt.pair_min_tiles && grouped_ns(tj + 1) == ns) {
+            if ((opt.upd_pair & 1) && T >= pair_tiles && grouped_ns(tj + 1) == ns) {
               for (int32_t ti = tj; ti < T; ti += 2) ft(F_UPD2, k, f, ti, tj | (ns << 16));
               ++tj;
               continue;
