@@ -200,9 +200,28 @@ __device__ void f_asm2(const sgn::FactorArgs& A, const DFront& F, int b, int ti,
     if (nr <= 0 || ns <= 0) continue;
     const double* U = fb + C.foff;
     const int64_t ldc = C.nrow;
-    for (int idx = tid; idx < nr * ns; idx += kFThreads) {
-      const int r = r_lo + idx % nr, s = s_lo + idx / nr;
-      if (r >= s) Bk[bi(rc[r]) * kA2 + bj(rc[s])] += __ldcg(U + (int64_t)(C.npiv + s) * ldc + C.npiv + r);
+    // 8 entries per thread in flight: the loads (child update block, relative rows) first,
+    // then the shared-memory adds (every entry of one child lands on its own position)
+    const int tot = nr * ns;
+    for (int base = tid; base < tot; base += 8 * kFThreads) {
+      double u[8];
+      int di[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int idx = base + q * kFThreads;
+        di[q] = -1;
+        u[q] = 0.0;
+        if (idx < tot) {
+          const int r = r_lo + idx % nr, s = s_lo + idx / nr;
+          if (r >= s) {
+            u[q] = __ldcg(U + (int64_t)(C.npiv + s) * ldc + C.npiv + r);
+            di[q] = bi(rc[r]) * kA2 + bj(rc[s]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (di[q] >= 0) Bk[di[q]] += u[q];
     }
   }
   __syncthreads();

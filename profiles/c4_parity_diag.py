@@ -51,7 +51,12 @@ def main():
     for scale, steps in ((1.0, 0), (1e-4, 0), (1e-4, 1), (1e-4, 2), (1e-4, 3)):
         eng.factor_shift_scale, eng.ir_steps = scale, steps
         sol, res, its = kkt_inverse_p(eng, -gold["grad"], factor=True)
-        print(f"given rhs: shift x{scale:g} ir {steps}: res {res:.2e} its {its} | dp vs exact "
+        rhs = np.zeros(Ko.shape[0])
+        rhs[n_x:n_x + n_p] = -gold["grad"]
+        r_o = np.linalg.norm(dd_residual(Ko.tocsr(), sol, rhs)) / np.linalg.norm(rhs)
+        r_d = np.linalg.norm(dd_residual(Kd.tocsr(), sol, rhs)) / np.linalg.norm(rhs)
+        print(f"given rhs: shift x{scale:g} ir {steps}: res {res:.2e} (dd vs device K {r_d:.2e}, vs oracle K "
+              f"{r_o:.2e}) its {its} | dp vs exact "
               f"{np.linalg.norm(sol[n_x:n_x + n_p] - dpx) / np.linalg.norm(dpx):.3e} | dx vs exact "
               f"{np.linalg.norm(sol[:n_x] - ex['dx_exact']) / np.linalg.norm(ex['dx_exact']):.3e}", flush=True)
     eng.factor_shift_scale, eng.ir_steps = 1e-4, 2
@@ -62,6 +67,13 @@ def main():
         print(f"gradient vs exact: device {np.linalg.norm(g - ge) / np.linalg.norm(ge):.3e}, reference "
               f"{np.linalg.norm(gold['grad'] - ge) / np.linalg.norm(ge):.3e}")
         sd = direction_sgn(prob, x, p, OptimizerConfig())
+        gd = eng.grad[0].cpu().numpy()
+        rhs = np.zeros(Ko.shape[0])
+        rhs[n_x:n_x + n_p] = -gd
+        sol = np.concatenate([sd.dx, sd.dp, sd.dlam])
+        print(f"full direction: residual (own gradient) vs oracle K "
+              f"{np.linalg.norm(dd_residual(Ko.tocsr(), sol, rhs)) / np.linalg.norm(rhs):.2e}, vs device K "
+              f"{np.linalg.norm(dd_residual(Kd.tocsr(), sol, rhs)) / np.linalg.norm(rhs):.2e}")
         dpe = ex["dp_exact_gexact"]
         print(f"full direction: dp vs exact(g_exact) {np.linalg.norm(sd.dp - dpe) / np.linalg.norm(dpe):.3e}, "
               f"reference dp vs exact(g_exact) {np.linalg.norm(gold['dp'] - dpe) / np.linalg.norm(dpe):.3e}")

@@ -39,6 +39,11 @@ def main():
         rhs = np.zeros(2 * n_x + n_p)
         rhs[n_x:n_x + n_p] = -gd
         ex = _exact_solve(K, rhs)
+        Kd = prob.kkt_matrix(x, p).to_scipy().tocsr()
+        exd = _exact_solve(Kd, rhs)
+        print(f"   exact(device K) vs exact(oracle K): dp {rel(exd[n_x:n_x + n_p], ex[n_x:n_x + n_p]):.2e}; "
+              f"device dp vs exact(device K) {rel(sd.dp, exd[n_x:n_x + n_p]):.2e}; |K_dev - K_or| max "
+              f"{np.abs((Kd - K).data).max() if (Kd - K).nnz else 0.0:.2e} of max|K| {np.abs(K.data).max():.2e}")
         sol = np.concatenate([sd.dx, sd.dp, sd.dlam])
         r = dd_residual(K, sol, rhs)
         print(f"shift {scale:g} ir {steps} adj {adj}: g_dir vs g_adj {rel(gd, g1):.2e}, g vs oracle {rel(gd, g_r):.2e} | "
