@@ -220,6 +220,10 @@ def _repair_rest(X0, tris, pm_dof, p0, half, rng, n_w, n_h):
         p0[redo] = rng.uniform(-half, half, int(redo.sum()))
 
 
+# forward tolerance of the sheets (oracle/configs.py SHEET_TOL: the reference's default 1e-10)
+SHEET_TOL = 1e-10
+
+
 def sheet_spec(config: int, seed: int = 0, instance: int = 0) -> dict:
     """BASELINE sheet spec (configs 1, 2; config-5 instances) -- see oracle/configs.py docs.
 
@@ -262,7 +266,7 @@ def sheet_spec(config: int, seed: int = 0, instance: int = 0) -> dict:
     return dict(X0=X0, conn=tris, kind="tri", fixed_verts=fixed,
                 pmap=(pm_dof, np.arange(pm_dof.size), np.ones(pm_dof.size)), target_dofs=tdofs,
                 target_vals=tvals, target_verts=tv, w_target=1.0, w_reg=2e-6, E=E, nu=nu, gload=100.0 * 9.81, p0=p0,
-                name=f"sheet_c{config}")
+                name=f"sheet_c{config}", tol=SHEET_TOL)
 
 
 def build_sheet(config: int, seed: int = 0, instance: int = 0, **kw):
@@ -282,7 +286,7 @@ class BatchedDesign:
     materials (1/E scaling), targets and parameters.
     """
 
-    def __init__(self, specs, stab=None, tol=1e-12):
+    def __init__(self, specs, stab=None, tol=None):
         s0 = specs[0]
         self.specs = specs
         self.B = len(specs)
@@ -298,7 +302,7 @@ class BatchedDesign:
         self.engine = DeviceEngine(self.plan, np.asarray(params), tvals, batch=self.B, stab=stab)
         self.p0 = np.stack([s["p0"] for s in specs])
         self.n_x, self.n_p = self.plan.n_x, self.plan.n_p
-        self.tol = tol
+        self.tol = float(s0.get("tol", 1e-12) if tol is None else tol)
 
     def load(self, x=None, p=None):
         self.engine.load(x=x, p=p)
