@@ -94,7 +94,8 @@ typedef struct {
     int32_t fat_solve;     /* small fronts solve as one task (default 1)                     */
     int32_t generic_pairs; /* generic mode: 2x2 pivots on consecutive unknowns (default 1)   */
     int32_t upd_pair;      /* 64x64 task blocks: bit 0 grouped Schur updates, bit 1 struct-tile
-                              solve-panel blocks, bit 2 front assembly (default 7)             */
+                              solve-panel blocks, bit 2 front assembly, bit 3 single-column
+                              updates as 64x32 row pairs (default 15)                         */
     int32_t pair_min_tiles;/* bits 0-1 of upd_pair apply to fronts of >= this many 32-row tiles;
                               0 (default) = auto: 4 when the factorization has >= 5e9 flops,
                               else none (small factorizations are pivot-chain bound)          */

@@ -519,13 +519,17 @@ __device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k
 //   ZP = true,  F_ZPAN2: Z(t..t+1, cb..cb+1) = sum_{j=cb}^{P-1} L(t..t+1, j) Z(j, cb..cb+1) for
 //                struct tiles t >= P (Z(cb, cb+1) = 0, so both columns sum from j = cb).
 constexpr int kU2A = 68, kU2B = 36;
-template <bool ZP>
+// NB = 32: one column tile (the row-paired single-column updates: look-ahead and single-step
+// columns, unpaired groups); warps own 32x16 quarters (4x2 fragments).
+template <bool ZP, int NB>
 __device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int k0, int k, int ti, int tj, Smem& S) {
+  static_assert(NB == 64 || NB == 32, "block width");
+  constexpr int NF = NB / 16;             // n fragments per warp
   static_assert(32 * kU2A + 64 * kU2B <= 5 * kTileWords, "64x64 operands fit the tile buffers");
   double* As = reinterpret_cast<double*>(&S);   // [32][kU2A] As[c][r] = L(row(r), j0 + c)  (S.a, S.b)
   double* Bs = As + 32 * kU2A;                  // [64][kU2B] Bs[j][c] = W(col(j), j0 + c) | Z(j0 + c, col j)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * (NB / 2);
   double* Fm = front_ptr(A, F, b);
   double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
   const int64_t ld = F.nrow;
@@ -544,11 +548,11 @@ __device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int 
     return c < F.npiv ? c : -1;
   };
   const int ra = brow(ti, tid & 63);      // this thread's A staging row (fixed)
-  double acc[4][4][2];
+  double acc[4][NF][2];
 #pragma unroll
   for (int mf = 0; mf < 4; ++mf)
 #pragma unroll
-    for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
+    for (int nf = 0; nf < NF; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
   for (int s = k0; s <= k; ++s) {
     const int j0 = s * kTile, w = min(kTile, F.npiv - j0);
 #pragma unroll
@@ -563,7 +567,7 @@ __device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int 
       for (int u = 0; u < 8; ++u) As[((tid >> 6) + 2 * (u + 8 * hh)) * kU2A + (tid & 63)] = v[u];
     }
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
+    for (int hh = 0; hh < NB / 32; ++hh) {
       double v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -580,15 +584,15 @@ __device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int 
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < kTile; kk += 4) {
-      double fa[4], fb[4];
+      double fa[4], fb[NF];
 #pragma unroll
       for (int mf = 0; mf < 4; ++mf) fa[mf] = As[(kk + q) * kU2A + wm + 8 * mf + g];
 #pragma unroll
-      for (int nf = 0; nf < 4; ++nf) fb[nf] = Bs[(wn + 8 * nf + g) * kU2B + kk + q];
+      for (int nf = 0; nf < NF; ++nf) fb[nf] = Bs[(wn + 8 * nf + g) * kU2B + kk + q];
 #pragma unroll
       for (int mf = 0; mf < 4; ++mf)
 #pragma unroll
-        for (int nf = 0; nf < 4; ++nf) dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], fa[mf], fb[nf]);
+        for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], fa[mf], fb[nf]);
     }
     __syncthreads();
   }
@@ -597,7 +601,7 @@ __device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int 
     const int m = wm + 8 * mf + g, gr = brow(ti, m);
     if (gr < 0) continue;
 #pragma unroll
-    for (int nf = 0; nf < 4; ++nf)
+    for (int nf = 0; nf < NF; ++nf)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int n = wn + 8 * nf + 2 * q + h, gc = bcol(n);
@@ -786,7 +790,11 @@ k_factor_dag(const sgn::FactorArgs A) {
     }
     const int Tn = sgn::ntiles_front(F.npiv, F.nrow);
     // F_UPDATE: b = tj | (ns << 16) applies steps k-ns+1 .. k (ns = 0 or 1: step k alone)
-    const int tjb = T.b & 0xffff, ns = (kind == sgn::F_UPDATE || kind == sgn::F_UPD2) ? max(1, T.b >> 16) : 1;
+    // F_UPD2: bit 15 of b = one column tile (rows paired only)
+    const bool u2single = (kind == sgn::F_UPD2) && (T.b & 0x8000);
+    const int tjb = (kind == sgn::F_UPD2) ? (T.b & 0x7fff) : (T.b & 0xffff);
+    const int ns = (kind == sgn::F_UPDATE || kind == sgn::F_UPD2) ? max(1, T.b >> 16) : 1;
+    const int tjw = u2single ? 1 : 2;       // column tiles of an F_UPD2 block
     if (tid == 0) {
       if (kind == sgn::F_ASM) {
         for (int ci = F.child_begin; ci < F.child_end; ++ci) {
@@ -811,9 +819,9 @@ k_factor_dag(const sgn::FactorArgs A) {
         if (T.b + 1 < P) spin_ge(cf + sgn::cnt_zc(P, Tn, T.b + 1), P - T.b - 1);
       } else if (kind == sgn::F_UPD2) {           // every tile of the block, then the TRSMs of step k
         for (int x = T.a; x < min(T.a + 2, Tn); ++x)
-          for (int y = tjb; y < min(tjb + 2, Tn); ++y)
+          for (int y = tjb; y < min(tjb + tjw, Tn); ++y)
             if (x >= y) spin_ge(cf + sgn::cnt_tile(P, x, y), 2 + k - ns);
-        for (int x = 0; x < 4; ++x) {
+        for (int x = 0; x < 2 + tjw; ++x) {
           const int t = (x < 2) ? T.a + x : tjb + x - 2;
           if (t < Tn) spin_ge(cf + sgn::cnt_pant(F.npiv, F.nrow, k, sgn::pan_task_of(k, t)), 1);
         }
@@ -839,9 +847,10 @@ k_factor_dag(const sgn::FactorArgs A) {
       f_update(A, F, b, k - ns + 1, k, dg ? k + 1 : T.a, dg ? k + 1 : tjb, S, dg);
       if (dg) { fac_k = k + 1; fac_tile = v33(S.b[1]); }
     } else if (kind == sgn::F_UPD2) {
-      f_block64<false>(A, F, b, k - ns + 1, k, T.a, tjb, S);
+      if (u2single) f_block64<false, 32>(A, F, b, k - ns + 1, k, T.a, tjb, S);
+      else f_block64<false, 64>(A, F, b, k - ns + 1, k, T.a, tjb, S);
     } else if (kind == sgn::F_ZPAN2) {
-      f_block64<true>(A, F, b, T.b, P - 1, T.a, T.b, S);
+      f_block64<true, 64>(A, F, b, T.b, P - 1, T.a, T.b, S);
     } else {
       f_ztask_pre(A, F, b, T.a, T.b, S);
       nr_trsm = (T.a < P && tid < 32) ? 32 : 0;
@@ -871,7 +880,7 @@ k_factor_dag(const sgn::FactorArgs A) {
         s1 = nullptr;
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
         for (int x = T.a; x < min(T.a + 2, Tn); ++x)
-          for (int y = tjb; y < min(tjb + 2, Tn); ++y)
+          for (int y = tjb; y < min(tjb + tjw, Tn); ++y)
             if (x >= y) asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(cf + sgn::cnt_tile(P, x, y)), "r"(ns) : "memory");
       }
       else if (kind == sgn::F_ASM && k == 1) {   // every lower tile of the 64x64 block

@@ -93,7 +93,7 @@ SGN_HD int tile_of_row(int npiv, int r) { return r < npiv ? r / 32 : ptiles(npiv
 //   F_FAT     (f, a, b)      : a whole small front in one CTA: runs fat[a .. b) (its tasks in the
 //                              order above, then its Z blocks) back to back; the sub-tasks signal
 //                              their own counters, so the waits between them pass at once
-//   F_UPD2    (f, k, a=ti, b=tj | ns << 16): the grouped update of the 64x64 block of tiles
+//   F_UPD2    (f, k, a=ti, b=tj | ns << 16 [| 0x8000: one column tile, 64x32]): the update of the 64x64 block of tiles
 //                              {ti, ti+1} x {tj, tj+1} (tiles past the front or above the
 //                              diagonal skipped): waits and signals as F_UPDATE per tile
 //   F_ZPAN2   (f, a=t, b=cb)  : struct-tile solve-panel blocks Z({t, t+1}, {cb, cb+1}) (t >= P) in
@@ -154,9 +154,11 @@ struct SymOptions {
   int32_t fat_tiles = 0;      // fronts of <= fat_tiles tiles factor as one task (0: off)
   int32_t fat_solve = 1;      // small fronts solve as one task
   int32_t generic_pairs = 1;  // generic mode: 2x2 pivots on consecutive unknowns
-  int32_t upd_pair = 7;       // grouped Schur updates on 64x64 blocks (F_UPD2); bit 1: struct-tile
+  int32_t upd_pair = 15;      // grouped Schur updates on 64x64 blocks (F_UPD2); bit 1: struct-tile
                               // Z blocks on 64x64 blocks too (F_ZPAN2); bit 2: assembly
-                              // on 64x64 blocks (F_ASM, k = 1); default 7 = all
+                              // on 64x64 blocks (F_ASM, k = 1); bit 3: single-column updates
+                              // (look-ahead, single-step, unpaired groups) as row pairs
+                              // (F_UPD2 with b bit 15, 64x32); default 15 = all
   int32_t pair_min_tiles = 0; // bits 0-1 apply to fronts of >= this many tiles (0: auto)
   int32_t upd_group_cb = 32;  // pivot steps per grouped update of contribution-block columns
 };

@@ -1105,7 +1105,7 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
     const int64_t P = ptiles(F.npiv), T = ntiles_front(F.npiv, F.nrow);
     F.cbase = s.n_fcnt;
     s.n_fcnt += 1 + 2 * P + T * (T + 1) / 2 + (F.nrow + kTile - 1) / kTile + P * T;   // ... ZC, PANT
-    if (T >= (1 << 16)) { last_error() = "front too large for the task schedule"; return 5; }
+    if (T >= (1 << 15)) { last_error() = "front too large for the task schedule"; return 5; }
     F.ftotal = 0;                                         // counted as the tasks are emitted
   }
   // Schur updates off the look-ahead column are applied in groups of up to kUpdGroup
@@ -1210,9 +1210,14 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
         if (k >= ptiles(F.npiv)) continue;
         const int32_t T = ntiles_front(F.npiv, F.nrow);
         const bool diag_next = k + 1 < ptiles(F.npiv);
-        if (k + 1 < T)
-          for (int32_t ti = k + 1; ti < T; ++ti)
-            if (!(diag_next && ti == k + 1)) ft(F_UPDATE, k, f, ti, k + 1);
+        if (k + 1 < T) {
+          const int32_t t0 = diag_next ? k + 2 : k + 1;
+          if ((opt.upd_pair & 8) && T >= pair_tiles) {       // row pairs (F_UPD2, one column)
+            for (int32_t ti = t0; ti < T; ti += 2) ft(F_UPD2, k, f, ti, (k + 1) | 0x8000 | (1 << 16));
+          } else {
+            for (int32_t ti = t0; ti < T; ++ti) ft(F_UPDATE, k, f, ti, k + 1);
+          }
+        }
       }
       for (int32_t f : fl) {
         const Front& F = s.fronts[f];
@@ -1245,7 +1250,11 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
               continue;
             }
           }
-          for (int32_t ti = tj; ti < T; ++ti) ft(F_UPDATE, k, f, ti, tj | (ns << 16));
+          if ((opt.upd_pair & 8) && T >= pair_tiles) {         // row pairs (F_UPD2, one column)
+            for (int32_t ti = tj; ti < T; ti += 2) ft(F_UPD2, k, f, ti, tj | 0x8000 | (ns << 16));
+          } else {
+            for (int32_t ti = tj; ti < T; ++ti) ft(F_UPDATE, k, f, ti, tj | (ns << 16));
+          }
         }
       }
       for (int32_t f : fl) {                                 // inline Z row of pivot tile k
