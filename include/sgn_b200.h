@@ -295,6 +295,12 @@ int  sgn_axpy(int64_t n, int32_t batch, const double* d_alpha, const double* d_x
               const double* d_y, double* d_out, int64_t stride, void* stream);
 /* dst[b] = src[b] for every instance b with mask[b] != 0 (per-instance acceptance in the
  * batched Newton / line search, forward.py:197-201, optimize.py:485-486)               */
+/* 64-bit fingerprint of each instance's n-vector (XOR of mixed bit patterns; deterministic):
+ * the forward Newton detects an iterate that repeats bitwise -- a deterministic iteration
+ * is then periodic and can never meet its tolerance (forward.py:135-168 would fail after
+ * max_iters; the device fails at once, with the same outcome).                         */
+int  sgn_fingerprint(int64_t n, int32_t batch, const double* d_x, int64_t stride, uint64_t* d_out,
+                     void* stream);
 int  sgn_masked_copy(int64_t n, int32_t batch, const int32_t* d_mask, const double* d_src,
                      double* d_dst, int64_t stride, void* stream);
 /* least-squares terms (sensitivity.py:83-93): d_vec (KKT order, dim = 2 n_x + n_p per

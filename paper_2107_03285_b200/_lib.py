@@ -66,6 +66,7 @@ SIGNATURES = {
     "sgn_factor_check": (ctypes.c_int, [c_vp, c_vp, P_i64]),
     "sgn_factor_status": (ctypes.c_int, [c_vp, c_vp, P_i64]),
     "sgn_masked_copy": (ctypes.c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "sgn_fingerprint": (ctypes.c_int, [c_i64, c_i32, c_vp, c_i64, c_vp, c_vp]),
     "sgn_factor_solve": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
     "sgn_factor_solve_multi": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
     "sgn_factor_set_grid": (ctypes.c_int, [c_vp, c_i32, ctypes.POINTER(ctypes.c_int32)]),

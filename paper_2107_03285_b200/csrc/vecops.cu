@@ -252,6 +252,39 @@ int sgn_axpy(int64_t n, int32_t batch, const double* d_alpha, const double* d_x,
   return SGN_OK;
 }
 
+// 64-bit fingerprint of each instance's vector: XOR over i of splitmix64(bits(x_i) ^ golden*i)
+// (XOR is order-free, so the value is deterministic whatever the block schedule)
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__global__ void k_fingerprint(int64_t n, const double* __restrict__ x, int64_t stride,
+                              unsigned long long* __restrict__ out) {
+  const int b = blockIdx.y;
+  unsigned long long h = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    h ^= mix64((unsigned long long)__double_as_longlong(x[(int64_t)b * stride + i]) ^ (0x632be59bd9b4e019ull * (unsigned long long)i));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0 && h) atomicXor(out + b, h);
+}
+
+int sgn_fingerprint(int64_t n, int32_t batch, const double* d_x, int64_t stride, uint64_t* d_out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(d_out, 0, (size_t)batch * sizeof(uint64_t), st) != cudaSuccess) {
+    sgn::last_error() = "fingerprint memset";
+    return SGN_CUDA_ERROR;
+  }
+  if (n == 0) return SGN_OK;
+  const dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 256), batch);
+  sgn::count_launch();
+  k_fingerprint<<<g, 256, 0, st>>>(n, d_x, stride, reinterpret_cast<unsigned long long*>(d_out));
+  VEC_CHECK();
+  return SGN_OK;
+}
+
 int sgn_masked_copy(int64_t n, int32_t batch, const int32_t* d_mask, const double* d_src,
                     double* d_dst, int64_t stride, void* stream) {
   if (n == 0) return SGN_OK;

@@ -1152,6 +1152,9 @@ class DeviceEngine:
             status[~np.asarray(active, bool)] = 1
         self.positions()                       # rest positions for the current p
         self.newton_iters = 0
+        if getattr(self, "_fp", None) is None:
+            self._fp = torch.zeros(B, dtype=torch.int64, device="cuda")
+        seen = [set() for _ in range(B)]
         for _ in range(max_iters):
             run = status == 0
             if not run.any():
@@ -1159,8 +1162,21 @@ class DeviceEngine:
             self.newton_iters += 1
             self._energy_grad(self.x)
             check(lib().sgn_reduce(2, n, B, ptr(self.gx), None, n, ptr(self.scal[3]), st))
+            check(lib().sgn_fingerprint(n, B, ptr(self.x), n, ptr(self._fp), st))
             sc = self.scal.cpu().numpy()
+            fp = self._fp.cpu().numpy()
             g_inf, e0 = sc[3], self._energies(sc)
+            # a bitwise-repeated iterate (fingerprint, |g|_inf and energy all equal) makes the
+            # deterministic iteration periodic through states that all failed the tolerance:
+            # the reference would run out its max_iters and raise; fail now, same outcome
+            # (config-5 line searches: trial states whose float floor is above tol cycle
+            # through ~4 states for the remaining ~190 iterations)
+            for b in np.flatnonzero(run & (g_inf > tol)):
+                key = (int(fp[b]), float(g_inf[b]), float(e0[b]))
+                if key in seen[b]:
+                    status[b] = -1
+                else:
+                    seen[b].add(key)
             if _DEBUG_NEWTON:
                 print(f"[newton] |g|inf {g_inf[:4]} E {e0[:4]} tol {tol:.3e}", flush=True)
             status[run & (g_inf <= tol)] = 1
