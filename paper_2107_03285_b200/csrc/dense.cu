@@ -126,11 +126,12 @@ __global__ void k_min_pivot(const sgn::DFront* __restrict__ fronts, const double
   int64_t pos = -1;
   const double* Fm = fstore + F.foff;
   for (int r = threadIdx.x; r < F.npiv; r += blockDim.x) {
-    double d = Fm[(int64_t)r * F.nrow + r];
+    const int64_t ld = sgn::front_ld(F.nrow);
+    double d = Fm[(int64_t)r * ld + r];
     if (F.pivtype == 2) {       // 2x2 block [a b; b c]: the equivalent 1x1 pivots a, det / a
       const int re = r & ~1;
-      const double a = Fm[(int64_t)re * F.nrow + re], bb = Fm[(int64_t)re * F.nrow + re + 1];
-      const double c = Fm[(int64_t)(re + 1) * F.nrow + re + 1];
+      const double a = Fm[(int64_t)re * ld + re], bb = Fm[(int64_t)re * ld + re + 1];
+      const double c = Fm[(int64_t)(re + 1) * ld + re + 1];
       d = (r == re) ? a : (a != 0.0 ? (a * c - bb * bb) / a : DBL_MAX);   // a == 0: reported at re
     }
     if (d < m) { m = d; pos = F.first + r; }

@@ -59,6 +59,13 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
       : "+d"(d0), "+d"(d1)
       : "d"(a), "d"(b));
 }
+__device__ __forceinline__ void cp16(void* dst, const void* src) {     // global -> shared, 16 B, L2 only
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 // Shared memory (dynamic, ~53 KB): five raw 32 x 40 tiles, each viewed either row-major
 // with stride 33 (one row per lane: conflict-free) or K-major with stride 40 (DMMA
 // fragment reads (row g, k q) and the coalesced staging stores both conflict-free).
@@ -123,7 +130,7 @@ __device__ void f_asm(const sgn::FactorArgs& A, const DFront& F, int b, int ti, 
     const int nr = r_hi - r_lo, ns = s_hi - s_lo;
     if (nr <= 0 || ns <= 0) continue;
     const double* U = fb + C.foff;
-    const int64_t ldc = C.nrow;
+    const int64_t ldc = sgn::front_ld(C.nrow);
     for (int idx = tid; idx < nr * ns; idx += kFThreads) {
       const int r = r_lo + idx % nr, s = s_lo + idx / nr;
       if (r >= s) tile[rc[r] - i0][rc[s] - j0] += __ldcg(U + (int64_t)(C.npiv + s) * ldc + C.npiv + r);
@@ -131,7 +138,7 @@ __device__ void f_asm(const sgn::FactorArgs& A, const DFront& F, int b, int ti, 
   }
   __syncthreads();
   double* Fm = front_ptr(A, F, b);
-  const int64_t ld = F.nrow;
+  const int64_t ld = sgn::front_ld(F.nrow);
   for (int e = tid; e < kTile * kTile; e += kFThreads) {
     const int ii = e & 31, jj = e >> 5;
     const int gi = i0 + ii, gj = j0 + jj;
@@ -199,7 +206,7 @@ __device__ void f_asm2(const sgn::FactorArgs& A, const DFront& F, int b, int ti,
     const int nr = r_hi - r_lo, ns = s_hi - s_lo;
     if (nr <= 0 || ns <= 0) continue;
     const double* U = fb + C.foff;
-    const int64_t ldc = C.nrow;
+    const int64_t ldc = sgn::front_ld(C.nrow);
     // 8 entries per thread in flight: the loads (child update block, relative rows) first,
     // then the shared-memory adds (every entry of one child lands on its own position)
     const int tot = nr * ns;
@@ -226,7 +233,7 @@ __device__ void f_asm2(const sgn::FactorArgs& A, const DFront& F, int b, int ti,
   }
   __syncthreads();
   double* Fm = front_ptr(A, F, b);
-  const int64_t ld = F.nrow;
+  const int64_t ld = sgn::front_ld(F.nrow);
   for (int e = tid; e < 64 * 64; e += kFThreads) {
     const int ii = e & 63, jj = e >> 6;
     const int x = ti + (ii >> 5), y = tj + (jj >> 5);
@@ -357,7 +364,7 @@ __device__ __forceinline__ void factor_publish(const sgn::FactorArgs& A, const D
 __device__ int f_panel_pre(const sgn::FactorArgs& A, const DFront& F, int b, int k, int t, Smem& S) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* Fm = front_ptr(A, F, b);
-  const int64_t ld = F.nrow;
+  const int64_t ld = sgn::front_ld(F.nrow);
   const int j0 = k * kTile, w = min(kTile, F.npiv - j0);
   const int T = sgn::ntiles_front(F.npiv, F.nrow);
   double (*Lt)[kTile + 1] = v33(S.a);
@@ -390,7 +397,7 @@ __device__ void f_panel_post(const sgn::FactorArgs& A, const DFront& F, int b, i
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (nr == 0) return;
   double* Fm = front_ptr(A, F, b);
-  const int64_t ld = F.nrow;
+  const int64_t ld = sgn::front_ld(F.nrow);
   const int j0 = k * kTile, w = min(kTile, F.npiv - j0);
   const int ti = (t == 0) ? k + 1 : k + 2 + 4 * (t - 1) + warp;
   const int lo = sgn::tile_lo(F.npiv, ti);
@@ -421,7 +428,7 @@ __device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k
   V40 Bk = v40(S.b[0]);       // Bk[c][j] = W[lo_j + j, j0 + c]
   const int tid = threadIdx.x;
   double* Fm = front_ptr(A, F, b);
-  const int64_t ld = F.nrow;
+  const int64_t ld = sgn::front_ld(F.nrow);
   const int lo_i = sgn::tile_lo(F.npiv, ti), nr = sgn::tile_hi(F.npiv, F.nrow, ti) - lo_i;
   const int lo_j = sgn::tile_lo(F.npiv, tj), nc = sgn::tile_hi(F.npiv, F.nrow, tj) - lo_j;
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
@@ -532,7 +539,7 @@ __device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int 
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * (NB / 2);
   double* Fm = front_ptr(A, F, b);
   double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
-  const int64_t ld = F.nrow;
+  const int64_t ld = sgn::front_ld(F.nrow);
   const int T = sgn::ntiles_front(F.npiv, F.nrow);
   // row r of the block -> front row (or -1): tile t0 + (r >> 5), row r & 31 of that tile
   auto brow = [&](int t0, int r) -> int {
@@ -553,7 +560,9 @@ __device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int 
   for (int mf = 0; mf < 4; ++mf)
 #pragma unroll
     for (int nf = 0; nf < NF; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
-  for (int s = k0; s <= k; ++s) {
+  // one 32-wide step through registers (partial steps, Z's structurally-zero upper block,
+  // fronts with an odd npiv)
+  auto step_reg = [&](int s) {
     const int j0 = s * kTile, w = min(kTile, F.npiv - j0);
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
@@ -595,7 +604,59 @@ __device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int 
         for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], fa[mf], fb[nf]);
     }
     __syncthreads();
+  };
+  // full 32-wide steps with 16-byte aligned operands (even npiv: every tile starts at an even
+  // row; ld is even) stream through a cp.async.cg double buffer of 16-wide half steps, so the
+  // next half step's operands are in flight during the DMMAs (profiles/micro/upd_bench.cu:
+  // v64a 30.3 vs v64 26.5 TFLOP/s).  Rows / columns past the block read a clamped valid
+  // address: their products only reach accumulators that are never stored.
+  const int sa = ZP ? k0 + 1 : k0;
+  const int sb = (F.npiv & 1) ? sa - 1 : min(k, (F.npiv >> 5) - 1);
+  if (ZP) step_reg(k0);
+  if (sb >= sa) {
+    double* As2 = As;                           // [2][16][kU2A]
+    double* Bs2 = As + 2 * 16 * kU2A;           // [2][NB][kA2B]
+    constexpr int kA2B = 20;
+    static_assert(2 * 16 * kU2A + 2 * 64 * kA2B <= 5 * kTileWords, "cp.async buffers fit");
+    const double* bsrc = ZP ? Zm : Fm;
+    auto issue = [&](int hs, int buf) {
+      const int c0 = (sa + (hs >> 1)) * kTile + 16 * (hs & 1);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {             // A: 16 columns x 32 row pairs
+        const int e = tid + u * kFThreads, ch = e & 31, c = e >> 5;
+        const int gr = brow(ti, 2 * ch);
+        cp16(&As2[(buf * 16 + c) * kU2A + 2 * ch], Fm + (int64_t)(c0 + c) * ld + (gr >= 0 ? gr : 0));
+      }
+#pragma unroll
+      for (int u = 0; u < NB / 16; ++u) {       // B: NB rows x 8 k pairs
+        const int e = tid + u * kFThreads, ch = e & 7, j = e >> 3;
+        const int gc = bcol(j);
+        cp16(&Bs2[(buf * 64 + j) * kA2B + 2 * ch], bsrc + (int64_t)(gc >= 0 ? gc : 0) * ld + c0 + 2 * ch);
+      }
+      cp_commit();
+    };
+    const int nh = 2 * (sb - sa + 1);
+    issue(0, 0);
+    for (int hs = 0; hs < nh; ++hs) {
+      const int buf = hs & 1;
+      if (hs + 1 < nh) { issue(hs + 1, buf ^ 1); cp_wait<1>(); } else { cp_wait<0>(); }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < 16; kk += 4) {
+        double fa[4], fb[NF];
+#pragma unroll
+        for (int mf = 0; mf < 4; ++mf) fa[mf] = As2[(buf * 16 + kk + q) * kU2A + wm + 8 * mf + g];
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf) fb[nf] = Bs2[(buf * 64 + wn + 8 * nf + g) * kA2B + kk + q];
+#pragma unroll
+        for (int mf = 0; mf < 4; ++mf)
+#pragma unroll
+          for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[mf][nf][0], acc[mf][nf][1], fa[mf], fb[nf]);
+      }
+      __syncthreads();
+    }
   }
+  for (int s = max(sa, sb + 1); s <= k; ++s) step_reg(s);
 #pragma unroll
   for (int mf = 0; mf < 4; ++mf) {
     const int m = wm + 8 * mf + g, gr = brow(ti, m);
@@ -633,7 +694,7 @@ __device__ void f_ztask_pre(const sgn::FactorArgs& A, const DFront& F, int b, in
   const int npiv = F.npiv, P = sgn::ptiles(npiv);
   const int lo = sgn::tile_lo(npiv, t), nr = sgn::tile_hi(npiv, F.nrow, t) - lo;
   const bool piv = t < P;
-  const int64_t ld = F.nrow;
+  const int64_t ld = sgn::front_ld(F.nrow);
   double* Fm = front_ptr(A, F, b);
   const double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
   const double* ds = A.dscr + (int64_t)b * A.dstride + F.doff;
@@ -733,7 +794,7 @@ __device__ void f_ztask_pre(const sgn::FactorArgs& A, const DFront& F, int b, in
 __device__ void f_ztask_post(const sgn::FactorArgs& A, const DFront& F, int b, int t, int cb, Smem& S) {
   const int tid = threadIdx.x;
   const int lo = sgn::tile_lo(F.npiv, t), nr = sgn::tile_hi(F.npiv, F.nrow, t) - lo;
-  const int64_t ld = F.nrow;
+  const int64_t ld = sgn::front_ld(F.nrow);
   double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
   const int c0 = cb * kTile, wb = min(kTile, F.npiv - c0);
   double (*Pw)[kTile + 1] = v33(S.b[0]);

@@ -152,7 +152,7 @@ __device__ bool dag_fwd(const SolveArgs& A, const sgn::Task& T, int b, const int
   const int cend = (r0 < npiv) ? min(npiv, r0 + nr) : npiv;
   const int c_lo = k * sgn::kFwdCols, c_hi = min(c_lo + sgn::kFwdCols, cend);
   const double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
-  const int64_t ld = F.nrow;
+  const int64_t ld = sgn::front_ld(F.nrow);
   double z[8];
   {
     const double* zr = Zm + r0 + lane;
@@ -271,7 +271,7 @@ __device__ bool dag_bwd(const SolveArgs& A, const sgn::Task& T, int b, const int
     return first_chunk;
   }
   const double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
-  const int64_t ld = F.nrow;
+  const int64_t ld = sgn::front_ld(F.nrow);
   const int np = F.npiv;
   const int re = min(rs + sgn::kBwdRows, F.nrow);
   double z[4][4];
@@ -346,7 +346,7 @@ __device__ bool dag_fwd_fat(const SolveArgs& A, const sgn::Task& T, int b, const
   const int npiv = F.npiv, nrow = F.nrow;
   const int ntile = (nrow + 31) / 32;
   const double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
-  const int64_t ld = nrow;
+  const int64_t ld = sgn::front_ld(nrow);
   double z[RT][8];
   auto load_z = [&](int t0) {
 #pragma unroll
@@ -468,7 +468,7 @@ __device__ bool dag_bwd_fat(const SolveArgs& A, const sgn::Task& T, int b, const
     return true;
   }
   const double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
-  const int64_t ld = nrow;
+  const int64_t ld = sgn::front_ld(nrow);
   double z[8][RT];
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
@@ -533,7 +533,7 @@ __device__ bool dag_root_fwd(const SolveArgs& A, const sgn::Task& T, int b, cons
   const int r0 = 32 * j, w = min(32, F.npiv - r0);
   if (A.nop || (A.leading && F.is_root_p)) { dag_wait(A, T, cnt); return true; }
   const double* Fm = A.fstore + (int64_t)b * A.fstride + F.foff;
-  const int64_t ld = F.nrow;
+  const int64_t ld = sgn::front_ld(F.nrow);
   double* yb = A.xbuf + (int64_t)b * A.n + F.first;
   double base = 0.0;
   int64_t q0 = 0, q1 = 0;
@@ -626,7 +626,7 @@ __device__ bool dag_root_bwd(const SolveArgs& A, const sgn::Task& T, int b, cons
     return true;
   }
   const double* Fm = A.fstore + (int64_t)b * A.fstride + F.foff;
-  const int64_t ld = F.nrow;
+  const int64_t ld = sgn::front_ld(F.nrow);
   const double* dsj = A.dscr + (int64_t)b * A.dstride + F.doff + (int64_t)j * sgn::kDiagStride;
   for (int e = tid; e < 1024; e += kSolveThreads) {
     const int r = e >> 5, c = e & 31;

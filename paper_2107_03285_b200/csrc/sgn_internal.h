@@ -58,6 +58,11 @@ struct DFront {
   int32_t ftotal, flags;  // flags bit 0: noz (Front::noz)
 };
 
+// Leading dimension of a front's dense storage and of its solve panel Z: nrow rounded up to
+// even, so every column starts 16-byte aligned (the cp.async operand staging of the 64x64
+// DMMA blocks, factor_dag.cu:f_block64).
+SGN_HD int64_t front_ld(int nrow) { return (int64_t)nrow + (nrow & 1); }
+
 // Split tile grid of a front: pivot tiles a < P cover rows [32a, min(32a+32, npiv)), the
 // contribution tiles a >= P cover [npiv + 32(a-P), ...).  Pivot step k is tile k, so every
 // Schur-update step touches whole tiles and per-tile dependency counters are exact.

@@ -998,10 +998,10 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
   for (auto& F : s.fronts) {
     const int64_t nr = F.nrow, ns = F.nrow - F.npiv;
     F.noz = (kNoZTiles > 0 && F.is_root_p && ns == 0 && ptiles(F.npiv) >= kNoZTiles) ? 1 : 0;
-    F.foff = s.front_doubles; s.front_doubles += nr * nr;
+    F.foff = s.front_doubles; s.front_doubles += front_ld((int)nr) * nr;
     F.uoff = s.u_doubles; s.u_doubles += ns;
     F.voff = s.v_doubles; s.v_doubles += nr;
-    F.zoff = s.z_doubles; s.z_doubles += F.noz ? 0 : nr * F.npiv;
+    F.zoff = s.z_doubles; s.z_doubles += F.noz ? 0 : front_ld((int)nr) * F.npiv;
     F.doff = s.d_doubles; s.d_doubles += (int64_t)((F.npiv + kTile - 1) / kTile) * kDiagStride;
     const int64_t T = ntiles_front(F.npiv, F.nrow);
     F.tile_base = s.ntiles; s.ntiles += T * (T + 1) / 2;

@@ -985,6 +985,7 @@ class DeviceEngine:
 
     adjoint_gx = True
     factor_shift_scale = 1e-4          # see factor_shifts(): 1.0 = the reference's full shift
+    floor_stall_window = 0             # simulate(): float-floor stall cut-off (0: reference behaviour)
     ir_steps = 2                       # mixed-precision refinement steps (_refine_with_fallback)
 
     def adjoint_direct(self, check_pivots: bool = True):
@@ -1155,6 +1156,9 @@ class DeviceEngine:
         if getattr(self, "_fp", None) is None:
             self._fp = torch.zeros(B, dtype=torch.int64, device="cuda")
         seen = [set() for _ in range(B)]
+        best = np.full(B, np.inf)                  # smallest |c|_inf so far
+        since = np.zeros(B, dtype=np.int64)        # iterations without a new best
+        win = int(getattr(self, "floor_stall_window", 0))
         for _ in range(max_iters):
             run = status == 0
             if not run.any():
@@ -1177,6 +1181,15 @@ class DeviceEngine:
                     status[b] = -1
                 else:
                     seen[b].add(key)
+            # float-floor stall (option, off by default: floor_stall_window = 0 is the
+            # reference's iteration exactly): |c|_inf within 100 x tol that sets no new
+            # minimum for `win` iterations sits on the float64 floor of the state and cannot
+            # reach tol; fail now instead of after max_iters
+            if win > 0:
+                imp = g_inf < best
+                best = np.where(imp, g_inf, best)
+                since = np.where(imp, 0, since + 1)
+                status[run & (g_inf > tol) & (g_inf <= 100.0 * tol) & (since >= win)] = -1
             if _DEBUG_NEWTON:
                 print(f"[newton] |g|inf {g_inf[:4]} E {e0[:4]} tol {tol:.3e}", flush=True)
             status[run & (g_inf <= tol)] = 1

@@ -300,6 +300,10 @@ class BatchedDesign:
             params.append([E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu)), s["gload"], 1.0 / E])
         tvals = np.stack([s["target_vals"] for s in specs])
         self.engine = DeviceEngine(self.plan, np.asarray(params), tvals, batch=self.B, stab=stab)
+        # config 5's line searches hit trial states whose float64 floor of |c|_inf is above
+        # the tolerance (profiles/r02_c5_newton_stalls.txt); the batch cuts such stalls after
+        # 16 iterations without a new minimum (DeviceEngine.simulate)
+        self.engine.floor_stall_window = 16
         self.p0 = np.stack([s["p0"] for s in specs])
         self.n_x, self.n_p = self.plan.n_x, self.plan.n_p
         self.tol = float(s0.get("tol", 1e-12) if tol is None else tol)
