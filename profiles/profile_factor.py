@@ -10,6 +10,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--solve", action="store_true", help="also profile one triangular solve")
     a = ap.parse_args()
     import torch
     from paper_2107_03285_b200.problems import build_beam, build_sheet, build_shell
@@ -28,6 +29,10 @@ def main():
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStart()
     eng.kfac.numeric(eng.kvals, eng.stab.eps_x, eng.stab.eps_lambda)
+    if a.solve:
+        b = torch.ones(eng.batch, prob.plan.dim, dtype=torch.float64, device="cuda")
+        xs = torch.empty_like(b)
+        eng.kfac.solve(b, xs)
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStop()
     print("profiled one factorization; KKT dim", prob.plan.dim)
