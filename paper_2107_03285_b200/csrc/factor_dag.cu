@@ -207,23 +207,28 @@ __device__ void f_asm2(const sgn::FactorArgs& A, const DFront& F, int b, int ti,
     if (nr <= 0 || ns <= 0) continue;
     const double* U = fb + C.foff;
     const int64_t ldc = sgn::front_ld(C.nrow);
-    // 8 entries per thread in flight: the loads (child update block, relative rows) first,
-    // then the shared-memory adds (every entry of one child lands on its own position)
-    const int tot = nr * ns;
-    for (int base = tid; base < tot; base += 8 * kFThreads) {
+    // A warp per child column, a lane per child row (nr <= 64: two rows per lane, their block
+    // rows looked up once per child); four columns = 8 entries per thread in flight: the loads
+    // (child update block, coalesced along the column) first, then the shared-memory adds
+    // (every entry of one child lands on its own position)
+    const int lane = tid & 31, warp = tid >> 5;
+    const int ra = r_lo + lane, rb = ra + 32;
+    const int ba = (ra < r_hi) ? bi(rc[ra]) * kA2 : -1;
+    const int bb = (rb < r_hi) ? bi(rc[rb]) * kA2 : -1;
+    const double* Ur = U + (int64_t)C.npiv * ldc + C.npiv;
+    for (int sb = warp; sb < ns; sb += 16) {
       double u[8];
       int di[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int idx = base + q * kFThreads;
-        di[q] = -1;
-        u[q] = 0.0;
-        if (idx < tot) {
-          const int r = r_lo + idx % nr, s = s_lo + idx / nr;
-          if (r >= s) {
-            u[q] = __ldcg(U + (int64_t)(C.npiv + s) * ldc + C.npiv + r);
-            di[q] = bi(rc[r]) * kA2 + bj(rc[s]);
-          }
+      for (int q = 0; q < 4; ++q) {
+        const int so = sb + 4 * q, s = s_lo + so;
+        di[2 * q] = di[2 * q + 1] = -1;
+        u[2 * q] = u[2 * q + 1] = 0.0;
+        if (so < ns) {
+          const int cj = bj(rc[s]);
+          const double* col = Ur + (int64_t)s * ldc;
+          if (ba >= 0 && ra >= s) { u[2 * q] = __ldcg(col + ra); di[2 * q] = ba + cj; }
+          if (bb >= 0 && rb >= s) { u[2 * q + 1] = __ldcg(col + rb); di[2 * q + 1] = bb + cj; }
         }
       }
 #pragma unroll
@@ -657,25 +662,43 @@ __device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int 
     }
   }
   for (int s = max(sa, sb + 1); s <= k; ++s) step_reg(s);
+  // C -= acc: the C loads of one fragment row (2 NF values per thread) are issued together,
+  // then subtracted and stored -- a load / store pair per value would serialize one memory
+  // latency per value behind the possibly-aliasing store before it (ncu: 19 % of the
+  // config-4 factorization's stall samples sat on that line)
+  int gcn[NF][2];
+#pragma unroll
+  for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) gcn[nf][h] = bcol(wn + 8 * nf + 2 * q + h);
 #pragma unroll
   for (int mf = 0; mf < 4; ++mf) {
     const int m = wm + 8 * mf + g, gr = brow(ti, m);
     if (gr < 0) continue;
+    if (ZP) {
 #pragma unroll
-    for (int nf = 0; nf < NF; ++nf)
+      for (int nf = 0; nf < NF; ++nf)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int n = wn + 8 * nf + 2 * q + h, gc = bcol(n);
-        if (gc < 0) continue;
-        if (ZP) {
-          Zm[(int64_t)gc * ld + gr] = acc[mf][nf][h];
-        } else {
-          const int tr = ti + (m >> 5), tc = tj + (n >> 5);
-          if (tr < tc || (tr == tc && (m & 31) < (n & 31))) continue;
-          double* pc = Fm + (int64_t)gc * ld + gr;
-          *pc = __ldcg(pc) - acc[mf][nf][h];
+        for (int h = 0; h < 2; ++h)
+          if (gcn[nf][h] >= 0) Zm[(int64_t)gcn[nf][h] * ld + gr] = acc[mf][nf][h];
+    } else {
+      double cv[NF][2];
+      bool ok[NF][2];
+      const int tr = ti + (m >> 5);
+#pragma unroll
+      for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int n = wn + 8 * nf + 2 * q + h, tc = tj + (n >> 5);
+          ok[nf][h] = gcn[nf][h] >= 0 && !(tr < tc || (tr == tc && (m & 31) < (n & 31)));
+          cv[nf][h] = ok[nf][h] ? __ldcg(Fm + (int64_t)gcn[nf][h] * ld + gr) : 0.0;
         }
-      }
+#pragma unroll
+      for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (ok[nf][h]) Fm[(int64_t)gcn[nf][h] * ld + gr] = cv[nf][h] - acc[mf][nf][h];
+    }
   }
 }
 
