@@ -216,16 +216,20 @@ __device__ void f_asm2(const sgn::FactorArgs& A, const DFront& F, int b, int ti,
     const int ba = (ra < r_hi) ? bi(rc[ra]) * kA2 : -1;
     const int bb = (rb < r_hi) ? bi(rc[rb]) * kA2 : -1;
     const double* Ur = U + (int64_t)C.npiv * ldc + C.npiv;
-    for (int sb = warp; sb < ns; sb += 16) {
+    // the warp's <= 16 columns (warp + 4 i): their block columns are loaded by lanes i next to
+    // the row lookups above (one latency) and handed out by shuffles
+    const int myc = warp + 4 * (lane & 15);
+    const int cjl = (myc < ns) ? bj(rc[s_lo + myc]) : 0;
+    for (int sb = warp, pass = 0; sb < ns; sb += 16, ++pass) {
       double u[8];
       int di[8];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int so = sb + 4 * q, s = s_lo + so;
+        const int cj = __shfl_sync(0xffffffffu, cjl, 4 * pass + q);
         di[2 * q] = di[2 * q + 1] = -1;
         u[2 * q] = u[2 * q + 1] = 0.0;
         if (so < ns) {
-          const int cj = bj(rc[s]);
           const double* col = Ur + (int64_t)s * ldc;
           if (ba >= 0 && ra >= s) { u[2 * q] = __ldcg(col + ra); di[2 * q] = ba + cj; }
           if (bb >= 0 && rb >= s) { u[2 * q + 1] = __ldcg(col + rb); di[2 * q + 1] = bb + cj; }
@@ -531,6 +535,10 @@ __device__ void f_update(const sgn::FactorArgs& A, const DFront& F, int b, int k
 //   ZP = true,  F_ZPAN2: Z(t..t+1, cb..cb+1) = sum_{j=cb}^{P-1} L(t..t+1, j) Z(j, cb..cb+1) for
 //                struct tiles t >= P (Z(cb, cb+1) = 0, so both columns sum from j = cb).
 constexpr int kU2A = 68, kU2B = 36;
+#ifndef SGN_UPD_RED
+#define SGN_UPD_RED 1
+#endif
+constexpr bool kUpdRed = SGN_UPD_RED != 0;   // C -= acc by red.global.add.f64 (1) or load / subtract / store (0)
 // NB = 32: one column tile (the row-paired single-column updates: look-ahead and single-step
 // columns, unpaired groups); warps own 32x16 quarters (4x2 fragments).
 template <bool ZP, int NB>
@@ -681,6 +689,20 @@ __device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int 
 #pragma unroll
         for (int h = 0; h < 2; ++h)
           if (gcn[nf][h] >= 0) Zm[(int64_t)gcn[nf][h] * ld + gr] = acc[mf][nf][h];
+    } else if (kUpdRed) {
+      // C += (-acc) as L2 reductions (no return value, no load latency in the task): the block
+      // has exactly one writer at a time (tile counters), so the result is the same rounded
+      // difference C - acc and the order of updates per entry stays the task order
+      const int tr = ti + (m >> 5);
+#pragma unroll
+      for (int nf = 0; nf < NF; ++nf)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int n = wn + 8 * nf + 2 * q + h, tc = tj + (n >> 5);
+          if (gcn[nf][h] >= 0 && !(tr < tc || (tr == tc && (m & 31) < (n & 31))))
+            asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(Fm + (int64_t)gcn[nf][h] * ld + gr),
+                         "d"(-acc[mf][nf][h]) : "memory");
+        }
     } else {
       double cv[NF][2];
       bool ok[NF][2];
@@ -879,33 +901,36 @@ k_factor_dag(const sgn::FactorArgs A) {
     const int tjb = (kind == sgn::F_UPD2) ? (T.b & 0x7fff) : (T.b & 0xffff);
     const int ns = (kind == sgn::F_UPDATE || kind == sgn::F_UPD2) ? max(1, T.b >> 16) : 1;
     const int tjw = u2single ? 1 : 2;       // column tiles of an F_UPD2 block
-    if (tid == 0) {
+    // the task's dependency counters, one per lane of warp 0: the acquire loads of up to 8
+    // counters are in flight together instead of one L2 round trip after another (the
+    // barrier below orders every thread of the CTA after all of them)
+    if (tid < 32) {
+      const int lane = tid;
       if (kind == sgn::F_ASM) {
-        for (int ci = F.child_begin; ci < F.child_end; ++ci) {
+        for (int ci = F.child_begin + lane; ci < F.child_end; ci += 32) {
           const DFront C = A.fronts[A.children[ci]];
           spin_ge(cnt + C.cbase, C.ftotal);
         }
       } else if (kind == sgn::F_PANEL) {          // DIAG(k) is awaited inside (after P loads)
         if (T.a == 0) {
-          spin_ge(cf + sgn::cnt_tile(P, k + 1, k), 1 + k);
-        } else {
-          for (int qd = 0; qd < 4; ++qd) {
-            const int i = k + 2 + 4 * (T.a - 1) + qd;
-            if (i < Tn) spin_ge(cf + sgn::cnt_tile(P, i, k), 1 + k);
-          }
+          if (lane == 0) spin_ge(cf + sgn::cnt_tile(P, k + 1, k), 1 + k);
+        } else if (lane < 4) {
+          const int i = k + 2 + 4 * (T.a - 1) + lane;
+          if (i < Tn) spin_ge(cf + sgn::cnt_tile(P, i, k), 1 + k);
         }
       } else if (kind == sgn::F_UPDATE || kind == sgn::F_DIAGUPD) {   // PAN(k) awaited inside
         const int ti = (kind == sgn::F_DIAGUPD) ? k + 1 : T.a, tj = (kind == sgn::F_DIAGUPD) ? k + 1 : tjb;
-        spin_ge(cf + sgn::cnt_tile(P, ti, tj), 2 + k - ns);
+        if (lane == 0) spin_ge(cf + sgn::cnt_tile(P, ti, tj), 2 + k - ns);
       } else if (kind == sgn::F_ZPAN2) {          // L final (last step's TRSMs), both Z columns complete
-        spin_ge(cf + sgn::cnt_pan(P - 1), sgn::panel_tasks(F.npiv, F.nrow, P - 1));
-        spin_ge(cf + sgn::cnt_zc(P, Tn, T.b), P - T.b);
-        if (T.b + 1 < P) spin_ge(cf + sgn::cnt_zc(P, Tn, T.b + 1), P - T.b - 1);
+        if (lane == 0) spin_ge(cf + sgn::cnt_pan(P - 1), sgn::panel_tasks(F.npiv, F.nrow, P - 1));
+        if (lane == 1) spin_ge(cf + sgn::cnt_zc(P, Tn, T.b), P - T.b);
+        if (lane == 2 && T.b + 1 < P) spin_ge(cf + sgn::cnt_zc(P, Tn, T.b + 1), P - T.b - 1);
       } else if (kind == sgn::F_UPD2) {           // every tile of the block, then the TRSMs of step k
-        for (int x = T.a; x < min(T.a + 2, Tn); ++x)
-          for (int y = tjb; y < min(tjb + tjw, Tn); ++y)
-            if (x >= y) spin_ge(cf + sgn::cnt_tile(P, x, y), 2 + k - ns);
-        for (int x = 0; x < 2 + tjw; ++x) {
+        if (lane < 4) {
+          const int x = T.a + (lane >> 1), y = tjb + (lane & 1);
+          if (x < min(T.a + 2, Tn) && y < min(tjb + tjw, Tn) && x >= y) spin_ge(cf + sgn::cnt_tile(P, x, y), 2 + k - ns);
+        } else if (lane < 6 + tjw) {
+          const int x = lane - 4;
           const int t = (x < 2) ? T.a + x : tjb + x - 2;
           if (t < Tn) spin_ge(cf + sgn::cnt_pant(F.npiv, F.nrow, k, sgn::pan_task_of(k, t)), 1);
         }

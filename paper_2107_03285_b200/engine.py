@@ -411,14 +411,16 @@ def _gx_share(eng, full: int) -> int:
     if eng.batch > 1:      # batched instances are throughput-bound: 1/4 (config 5 sweep, 111..222 CTAs)
         return max(1, full // 4)
     # single instance: proportional to the G_x factor's share of the flops, 1.85 x
-    # flops(G_x) / flops(KKT), within [1/16, 1/4] of the grid.  Sweeps (SGN_GX_CTAS):
-    # config 2 (ratio 0.119) best at 129 of 592, config 3 (0.066) at 74, config 4 (~0.03)
-    # at 37 (factor 208 -> 174 ms against the fixed 7/32)
+    # flops(G_x) / flops(KKT), within [3/16, 1/4] of the grid.  Sweeps (SGN_GX_CTAS):
+    # config 2 (ratio 0.119) best at 129 of 592; with the round-2 KKT factorization (config 4:
+    # 33 ms) a smaller share leaves the adjoint as a tail after the KKT factor: config 3
+    # 158 / 174 / 172 directions/s at 74 / 111 / 148, config 4 23.4 / 23.3 / 24.2 / 23.7 at
+    # 37 / 92 / 111 / 130 (profiles/r02_gx_share_sweep.txt)
     if not hasattr(eng, "_gx_frac"):
         fk = float(eng.ksym.stats()["flops"])
         eng.gfac                                   # builds gsym
         fg = float(eng.gsym.stats()["flops"])
-        eng._gx_frac = min(0.25, max(1.0 / 16.0, 1.85 * fg / max(fk, 1.0)))
+        eng._gx_frac = min(0.25, max(3.0 / 16.0, 1.85 * fg / max(fk, 1.0)))
     return max(1, int(round(eng._gx_frac * full)))
 _DEBUG_NAN = os.environ.get("SGN_DEBUG_NAN", "0") == "1"
 _DEBUG_NEWTON = os.environ.get("SGN_DEBUG_NEWTON", "0") == "1"
