@@ -244,6 +244,14 @@ int  sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch,
                         int64_t vert_stride, const double* d_params, int64_t param_stride,
                         double* d_hess, double* d_mixed, const int32_t* d_mslot,
                         int64_t buf_stride, void* stream);
+/* as sgn_element_derivs; rest_comp_mask (bit i = rest coordinate component i is moved by the
+ * parameter map) lets the shell kinds skip the mixed columns of components the p-map never
+ * reads (config 4: heights only, 4 of a hinge's 12 columns); those entries are not written. */
+int  sgn_element_derivs_ex(int32_t elem_type, int64_t n_elems, int32_t batch,
+                           const int32_t* d_conn, const double* d_pos, const double* d_rest,
+                           int64_t vert_stride, const double* d_params, int64_t param_stride,
+                           double* d_hess, double* d_mixed, const int32_t* d_mslot,
+                           int64_t buf_stride, int32_t rest_comp_mask, void* stream);
 /* element energies / gradients for the forward solve and line search
  * (spring_energy/spring_gradient analog, forward.py:34-48) */
 int  sgn_element_energy_grad(int32_t elem_type, int64_t n_elems, int32_t batch,

@@ -88,6 +88,8 @@ SIGNATURES = {
                                          P_dbl, P_i32, c_vp]),
     "sgn_element_derivs": (ctypes.c_int, [c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp,
                                           c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "sgn_element_derivs_ex": (ctypes.c_int, [c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp,
+                                             c_i64, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
     "sgn_element_energy_grad": (ctypes.c_int, [c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_i64,
                                                c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
     "sgn_gather_values": (ctypes.c_int, [c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp,

@@ -609,6 +609,15 @@ int sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch, const 
                        const double* d_pos, const double* d_rest, int64_t vert_stride,
                        const double* d_params, int64_t param_stride, double* d_hess,
                        double* d_mixed, const int32_t* d_mslot, int64_t buf_stride, void* stream) {
+  return sgn_element_derivs_ex(elem_type, n_elems, batch, d_conn, d_pos, d_rest, vert_stride, d_params,
+                               param_stride, d_hess, d_mixed, d_mslot, buf_stride, 7, stream);
+}
+
+int sgn_element_derivs_ex(int32_t elem_type, int64_t n_elems, int32_t batch, const int32_t* d_conn,
+                          const double* d_pos, const double* d_rest, int64_t vert_stride,
+                          const double* d_params, int64_t param_stride, double* d_hess,
+                          double* d_mixed, const int32_t* d_mslot, int64_t buf_stride,
+                          int32_t rest_comp_mask, void* stream) {
   if (d_mslot && elem_type != SGN_ELEM_NH_TRI && elem_type != SGN_ELEM_NH_TET) {
     sgn::last_error() = "mixed slots are supported for neo-Hookean simplices only";
     return SGN_INVALID;
@@ -654,7 +663,7 @@ int sgn_element_derivs(int32_t elem_type, int64_t n_elems, int32_t batch, const 
     case SGN_ELEM_SHELL_MEMBRANE:
     case SGN_ELEM_HINGE:
       return sgn::launch_shell(true, elem_type, n_elems, batch, d_conn, d_pos, d_rest, vert_stride,
-                               d_params, param_stride, d_hess, d_mixed, buf_stride, stream);
+                               d_params, param_stride, d_hess, d_mixed, buf_stride, stream, rest_comp_mask);
     default:
       sgn::last_error() = "unknown element type";
       return SGN_INVALID;

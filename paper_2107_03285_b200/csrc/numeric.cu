@@ -806,6 +806,42 @@ __global__ void k_add_dd(double* __restrict__ hi, double* __restrict__ lo, const
   }
 }
 
+// The four squared norms the refinement reports (|r|^2, |b|^2, |d|^2, |x|^2) in one pass:
+// kIrBlocks block partials per instance (fixed strided slices, fixed trees), then one block
+// per instance adds them in block order -- deterministic, 2 launches instead of four
+// single-CTA reductions over n.
+constexpr int kIrBlocks = 64, kIrThreads = 256;
+__global__ void __launch_bounds__(kIrThreads)
+k_ir_norms_partial(int64_t n, const double* __restrict__ r, const double* __restrict__ b,
+                   const double* __restrict__ d, const double* __restrict__ x, double* __restrict__ part) {
+  __shared__ double sh[4][kIrThreads];
+  const int inst = blockIdx.y, tid = threadIdx.x;
+  const int64_t o = (int64_t)inst * n;
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)kIrThreads + tid; i < n; i += (int64_t)kIrBlocks * kIrThreads) {
+    const double v0 = r[o + i], v1 = b[o + i], v2 = d[o + i], v3 = x[o + i];
+    a[0] += v0 * v0; a[1] += v1 * v1; a[2] += v2 * v2; a[3] += v3 * v3;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sh[q][tid] = a[q];
+  __syncthreads();
+  for (int s = kIrThreads / 2; s > 0; s >>= 1) {
+    if (tid < s) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sh[q][tid] += sh[q][tid + s];
+    }
+    __syncthreads();
+  }
+  if (tid < 4) part[((int64_t)inst * kIrBlocks + blockIdx.x) * 4 + tid] = sh[tid][0];
+}
+__global__ void k_ir_norms_final(const double* __restrict__ part, double* __restrict__ out, int B) {
+  const int inst = blockIdx.x, q = threadIdx.x;       // 4 threads: one norm each, block order
+  if (q >= 4) return;
+  double t = 0.0;
+  for (int k = 0; k < kIrBlocks; ++k) t += part[((int64_t)inst * kIrBlocks + k) * 4 + q];
+  out[(int64_t)q * B + inst] = t;
+}
+
 // ------------------------------------------------------------------------------------
 // deterministic batched BLAS-1 for BiCGSTAB (fixed reduction trees)
 // ------------------------------------------------------------------------------------
@@ -1738,7 +1774,7 @@ int sgn_residual_dd(sgn_factor f, const double* d_values, int64_t values_stride,
   int rc;
   if (!lo) {                                      // a zero low word
     if (!f->ir_lo.p && ((rc = f->ir_r.alloc((size_t)B * n)) || (rc = f->ir_d.alloc((size_t)B * n)) ||
-                        (rc = f->ir_lo.alloc((size_t)B * n)) || (rc = f->ir_out.alloc(4 * (size_t)B))))
+                        (rc = f->ir_lo.alloc((size_t)B * n)) || (rc = f->ir_out.alloc(4 * (size_t)B * (1 + kIrBlocks)))))
       return rc;
     CUDA_TRY(cudaMemsetAsync(f->ir_lo.p, 0, (size_t)B * n * sizeof(double), st));
     lo = f->ir_lo.p;
@@ -1766,7 +1802,7 @@ int sgn_solve_ir(sgn_factor f, const double* d_values, int64_t values_stride, co
   const size_t N = (size_t)B * std::max<int64_t>(n, 1);
   int rc;
   if (!f->ir_r.p && ((rc = f->ir_r.alloc(N)) || (rc = f->ir_d.alloc(N)) || (rc = f->ir_lo.alloc(N)) ||
-                      (rc = f->ir_out.alloc(4 * (size_t)B))))
+                      (rc = f->ir_out.alloc(4 * (size_t)B * (1 + kIrBlocks)))))
     return rc;
   if ((rc = launch_solve(f, d_rhs, d_sol, 0, st))) return rc;
   const unsigned rb = (unsigned)((n * 8 + 255) / 256);
@@ -1789,11 +1825,12 @@ int sgn_solve_ir(sgn_factor f, const double* d_values, int64_t values_stride, co
   if (d_sol_lo) CUDA_TRY(cudaMemcpyAsync(d_sol_lo, f->ir_lo.p, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
   if (!report) return SGN_OK;
   double* o = f->ir_out.p;
-  if ((rc = sgn_reduce(1, n, B, f->ir_r.p, f->ir_r.p, n, o, st)) ||
-      (rc = sgn_reduce(1, n, B, d_rhs, d_rhs, n, o + B, st)) ||
-      (rc = sgn_reduce(1, n, B, f->ir_d.p, f->ir_d.p, n, o + 2 * B, st)) ||
-      (rc = sgn_reduce(1, n, B, d_sol, d_sol, n, o + 3 * B, st)))
-    return rc;
+  sgn::count_launch();
+  k_ir_norms_partial<<<dim3(kIrBlocks, B), kIrThreads, 0, st>>>(n, f->ir_r.p, d_rhs, f->ir_d.p, d_sol, o + 4 * (size_t)B);
+  CUDA_TRY(cudaGetLastError());
+  sgn::count_launch();
+  k_ir_norms_final<<<B, 32, 0, st>>>(o + 4 * (size_t)B, o, B);
+  CUDA_TRY(cudaGetLastError());
   std::vector<double> h(4 * (size_t)B);
   CUDA_TRY(cudaMemcpyAsync(h.data(), o, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));

@@ -241,7 +241,8 @@ int64_t launch_count();
 
 int launch_shell(bool derivs, int32_t elem_type, int64_t n_elems, int32_t batch, const int32_t* conn,
                  const double* pos, const double* rest, int64_t vstride, const double* params,
-                 int64_t pstride, double* out1, double* out2, int64_t bstride, void* stream);
+                 int64_t pstride, double* out1, double* out2, int64_t bstride, void* stream,
+                 int rest_comp_mask = 7);
 
 // returns 0 ok, 1 singular (pivot_index set), 5 invalid
 int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index);

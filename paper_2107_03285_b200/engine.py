@@ -99,6 +99,9 @@ class MeshPlan:
         hoff = goff = 0
         rest_used = np.zeros(self.n_v * d, bool)
         rest_used[np.asarray(pmap[0], dtype=np.int64)] = True
+        # rest coordinate components the p-map moves at all (bit i): the shell kernels skip the
+        # mixed columns of the others (config 4: heights only)
+        self.rest_comp_mask = int(sum(1 << i for i in range(d) if rest_used[i::d].any()))
         for gk, gc in groups:
             g = ElemGroup(gk, gc, d, hoff, goff, rest_used)
             self.groups.append(g)
@@ -847,11 +850,12 @@ class DeviceEngine:
             self._mslots = [None if g.mslot is None else
                             self.torch.as_tensor(g.mslot, dtype=self.torch.int32, device="cuda") for g in pl.groups]
         for g, conn, prm, ms in zip(pl.groups, self.conns, self.gparams, self._mslots):
-            check(lib().sgn_element_derivs(g.code, g.n_e, self.batch, ptr(conn), ptr(self.pos), ptr(self.rest),
-                                           pl.n_dof, ptr(prm), prm.stride(0),
-                                           ptr(self.ebuf[:, g.hoff:]) if (hess or g.mslot is None) else None,
-                                           ptr(self.ebuf[:, g.moff:]) if (mixed or g.mslot is None) else None,
-                                           ptr(ms) if ms is not None else None, pl.ebuf_size, self.stream))
+            check(lib().sgn_element_derivs_ex(g.code, g.n_e, self.batch, ptr(conn), ptr(self.pos), ptr(self.rest),
+                                              pl.n_dof, ptr(prm), prm.stride(0),
+                                              ptr(self.ebuf[:, g.hoff:]) if (hess or g.mslot is None) else None,
+                                              ptr(self.ebuf[:, g.moff:]) if (mixed or g.mslot is None) else None,
+                                              ptr(ms) if ms is not None else None, pl.ebuf_size,
+                                              pl.rest_comp_mask, self.stream))
 
     def _vertex(self, kv, gv):
         pl, vp = self.plan, self.vplan
@@ -988,7 +992,7 @@ class DeviceEngine:
     adjoint_gx = True
     factor_shift_scale = 1e-4          # see factor_shifts(): 1.0 = the reference's full shift
     floor_stall_window = 0             # simulate(): float-floor stall cut-off (0: reference behaviour)
-    ir_steps = 2                       # mixed-precision refinement steps (_refine_with_fallback)
+    ir_steps = int(os.environ.get("SGN_IR_STEPS", "2"))   # mixed-precision refinement steps (_refine_with_fallback)
 
     def adjoint_direct(self, check_pivots: bool = True):
         """w = G_x^{-1} f_x (unshifted LDL^T of the state Jacobian) placed as v = (0, 0, w)
