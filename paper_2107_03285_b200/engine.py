@@ -157,6 +157,7 @@ class MeshPlan:
         rows, cols, src, coef = [], [], [], []
         gx_r_all, gx_c_all, gx_s_all = [], [], []
         g_rows, g_src = [], []
+        ts_row, ts_cdof, ts_m, ts_h = [], [], [], []      # two-stage G_p: entries before the p expansion
         rp = self.rest_ptr
         for g in self.groups:
             nd = g.nd
@@ -181,6 +182,9 @@ class MeshPlan:
             cnt = (rp[c_dof + 1] - rp[c_dof]) * (rx >= 0)
             sel = np.flatnonzero(cnt)
             if sel.size:
+                ts_row.append(rx[sel]); ts_cdof.append(c_dof[sel]); ts_m.append(midx[sel])
+                ts_h.append(np.where(cx[sel] >= 0, hidx[sel], -1) if self.disp_scale is not None
+                            else np.full(sel.size, -1, dtype=np.int64))
                 rep = cnt[sel]
                 base_t = np.repeat(sel, rep)
                 starts = np.zeros(rep.size, dtype=np.int64)
@@ -298,6 +302,65 @@ class MeshPlan:
         # --- gradient gather: free dof <- element-gradient entries ------------------------
         self.grad_ptr, self.grad_src = _csr_from_lists(n_x, np.concatenate(g_rows), np.concatenate(g_src))
         self.grad_base = self.f_ext[self.free_dofs].copy()
+
+        # --- two-stage assembly (multi-group meshes with a wide p-map: the shell) -----------
+        # The one-stage gather expands every element entry over the parameters of its rest dof
+        # and over both symmetric copies (config 4: 173 M terms, 5 GB read per assembly).  Two
+        # stages instead: G_x values once (the G lists above) copied to both K blocks; the
+        # mixed matrix Mz = d2E/dx dX (+ H on free columns, displacement state) summed per
+        # (row, rest dof), then G_p = Mz P over the p-map rows, written to both K blocks; the
+        # constant entries (A, B, C) are written once.  ~50 M terms for config 4.
+        self.two_stage = None
+        if self.restlen is None and R is None and ts_row and len(self.groups) > 1:
+            self.two_stage = self._two_stage_lists(ukey, oL, np.concatenate(ts_row), np.concatenate(ts_cdof),
+                                                   np.concatenate(ts_m), np.concatenate(ts_h), gu)
+
+    def _two_stage_lists(self, ukey, oL, t_row, t_cdof, t_m, t_h, gu):
+        dim, n_x, n_p = self.dim, self.n_x, self.n_p
+
+        def kpos(row, col):
+            key = col * dim + row
+            pos = np.searchsorted(ukey, key)
+            assert np.array_equal(ukey[pos], key)
+            return pos.astype(np.int64)
+
+        ts = {}
+        # G_x block: the G pattern's nnz q = (row gu % n_x, col gu // n_x) -> K[oL + row, col] and its transpose
+        g_row, g_col = gu % n_x, gu // n_x
+        ts["gx_dst"] = np.concatenate([kpos(oL + g_row, g_col), kpos(g_col, oL + g_row)])
+        ts["gx_src"] = np.concatenate([np.arange(self.G_nnz, dtype=np.int64)] * 2)
+        # stage 1: Mz entries (rest dof, row) <- element mixed (+ Hessian) entries
+        key1 = t_cdof * n_x + t_row
+        u1, inv1 = np.unique(key1, return_inverse=True)
+        hv = t_h >= 0
+        ts["mz_ptr"], ts["mz_src"] = _csr_from_lists(u1.size, np.concatenate([inv1, inv1[hv]]),
+                                                     np.concatenate([t_m, t_h[hv]]))
+        ts["n_mz"] = int(u1.size)
+        # stage 2: G_p[row, p] = sum_c Mz[row, c] P[c, p]
+        m_cdof, m_row = u1 // n_x, u1 % n_x
+        rp = self.rest_ptr
+        rep = rp[m_cdof + 1] - rp[m_cdof]
+        src = np.repeat(np.arange(u1.size, dtype=np.int64), rep)
+        offs = np.arange(int(rep.sum()), dtype=np.int64) - np.repeat(np.cumsum(rep) - rep, rep)
+        kk = rp[m_cdof[src]] + offs
+        pj, pc = self.rest_idx[kk], self.rest_coef[kk]
+        key2 = pj * n_x + m_row[src]
+        u2, inv2 = np.unique(key2, return_inverse=True)
+        gp_ptr, gp_src, gp_coef = _csr_from_lists(u2.size, inv2, src, pc)
+        p_of, r_of = u2 // n_x, u2 % n_x
+        n2 = u2.size
+        ts["gp_dst"] = np.concatenate([kpos(oL + r_of, n_x + p_of), kpos(n_x + p_of, oL + r_of)])
+        ts["gp_ptr"] = np.concatenate([gp_ptr, gp_ptr[-1] + gp_ptr[1:]])
+        ts["gp_src"] = np.concatenate([gp_src, gp_src])
+        ts["gp_coef"] = np.concatenate([gp_coef, gp_coef])
+        # every structural entry is either constant (written once from K_base) or covered above
+        covered = np.zeros(self.nnz, bool)
+        covered[ts["gx_dst"]] = True
+        covered[ts["gp_dst"]] = True
+        assert (self.K_base[covered] == 0.0).all()
+        assert np.array_equal(np.diff(self.K_ptr) > 0, covered), "two-stage lists cover the variable entries"
+        ts["n_gp"] = int(2 * n2)
+        return ts
 
 
 class VertexPlan:
@@ -719,8 +782,17 @@ class DeviceEngine:
             self.X0_flat = T(pl.X0.ravel())
         self.rest_base, self.rest_ptr = T(pl.rest_base), T(pl.rest_ptr, i64)
         self.rest_idx, self.rest_coef = T(pl.rest_idx, i64), T(pl.rest_coef)
-        self.K_base, self.K_ptr = T(pl.K_base), T(pl.K_ptr, i64)
-        self.K_src, self.K_coef = T(pl.K_src, i64), T(pl.K_coef)
+        self.K_base = T(pl.K_base)
+        self.ts = None
+        if pl.two_stage is not None:           # two-stage assembly lists instead of the one-stage gather's
+            t2 = pl.two_stage
+            self.ts = {k: (T(v, i64) if v.dtype.kind == "i" else T(v)) for k, v in t2.items()
+                       if isinstance(v, np.ndarray)}
+            self.ts["unit_ptr"] = torch.arange(max(t2["gx_dst"].size, 1) + 1, dtype=i64, device=dev)
+            self.mz = torch.zeros(B, max(t2["n_mz"], 1), dtype=f64, device=dev)
+        else:
+            self.K_ptr = T(pl.K_ptr, i64)
+            self.K_src, self.K_coef = T(pl.K_src, i64), T(pl.K_coef)
         self.G_ptr, self.G_src = T(pl.G_ptr, i64), T(pl.G_src, i64)
         self.G_coef = None if pl.G_coef is None else T(pl.G_coef)
         if pl.restlen is not None:
@@ -748,6 +820,8 @@ class DeviceEngine:
         self.eener = self.eeners[0]
         self.rscr = z(B, max(int(pl.target_dofs.size), 1))
         self.kvals = z(B, pl.nnz)
+        if self.ts is not None:                # constant entries (A, B, C) once; the rest every assembly
+            self.kvals.copy_(self.K_base.reshape(1, -1).expand(B, -1))
         self.gvals = z(B, pl.G_nnz)
         self.fvec = z(B, pl.dim)
         self.rhs = z(B, pl.dim)
@@ -790,6 +864,11 @@ class DeviceEngine:
     def _gather(self, n_out, base, base_stride, ptr_, idx, coef, buf, buf_stride, out, out_stride):
         check(lib().sgn_gather_values(n_out, self.batch, ptr(base), base_stride, ptr(ptr_), ptr(idx),
                                       ptr(coef), ptr(buf), buf_stride, ptr(out), out_stride, self.stream))
+
+    def _gather_to(self, dst, base, ptr_, idx, coef, buf, buf_stride):
+        """kvals[dst[k]] = base[k] + sum coef * buf[idx] over ptr_[k] .. ptr_[k + 1] (restricted gather)."""
+        check(lib().sgn_gather_to(dst.numel(), self.batch, ptr(dst), ptr(base), ptr(ptr_), ptr(idx), ptr(coef),
+                                  ptr(buf), buf_stride, ptr(self.kvals), self.plan.nnz, self.stream))
 
     def load(self, x=None, p=None):
         """Host (x, p) -> device through pinned staging buffers: the host->device copies are
@@ -887,6 +966,18 @@ class DeviceEngine:
             self._gx_ready = True
             return
         self.element_blocks()
+        if self.ts is not None:
+            # two-stage path (MeshPlan._two_stage_lists): G_x once -> both K blocks; Mz, then
+            # G_p = Mz P -> both K blocks
+            ts = self.ts
+            self._gather(pl.G_nnz, None, 0, self.G_ptr, self.G_src, self.G_coef, self.ebuf, self.ebuf.stride(0),
+                         self.gvals, pl.G_nnz)
+            self._gather_to(ts["gx_dst"], None, ts["unit_ptr"], ts["gx_src"], None, self.gvals, pl.G_nnz)
+            self._gather(self.mz.shape[1], None, 0, ts["mz_ptr"], ts["mz_src"], None, self.ebuf,
+                         self.ebuf.stride(0), self.mz, self.mz.shape[1])
+            self._gather_to(ts["gp_dst"], None, ts["gp_ptr"], ts["gp_src"], ts["gp_coef"], self.mz, self.mz.shape[1])
+            self._gx_ready = True
+            return
         self._restlen_blocks()
         self._gather(pl.nnz, self.K_base, 0, self.K_ptr, self.K_src, self.K_coef, self.ebuf,
                      self.ebuf.stride(0), self.kvals, pl.nnz)
