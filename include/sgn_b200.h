@@ -147,6 +147,14 @@ void sgn_factor_destroy(sgn_factor f);
  * factor of one direction (sensitivity.py:194-198 next to linear_solvers.py:130-175) --
  * split the SMs' CTA slots instead of queueing.                                        */
 int  sgn_factor_set_grid(sgn_factor f, int32_t ctas, int32_t* grid);
+/* Late hand-over of CTA slots to a concurrent launch: the factorization starts on its full
+ * grid, and once its task list reaches the first of the top levels that hold at most
+ * max_level_fronts fronts each (the dependency-chain-bound end of the elimination tree), the
+ * CTAs with index >= keep_ctas leave.  A launch queued on another stream (the adjoint's G_x
+ * factorization, sensitivity.py:194-198) then becomes resident in their slots.  keep_ctas <=
+ * 0 or max_level_fronts <= 0 turns it off; *retire_task (may be NULL) = the task index of
+ * the hand-over, -1 when off or when no level qualifies. */
+int  sgn_factor_set_retire(sgn_factor f, int32_t keep_ctas, int32_t max_level_fronts, int64_t* retire_task);
 
 /* X[:, j] = (L D L^T)^{-1} B[:, j] for nrhs right-hand sides against ONE factor (batch 1),
  * column j at B + j*n.  Replaces the n_p back-substitutions of sensitivity_matrix

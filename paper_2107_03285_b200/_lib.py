@@ -70,6 +70,7 @@ SIGNATURES = {
     "sgn_factor_solve": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
     "sgn_factor_solve_multi": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
     "sgn_factor_set_grid": (ctypes.c_int, [c_vp, c_i32, ctypes.POINTER(ctypes.c_int32)]),
+    "sgn_factor_set_retire": (ctypes.c_int, [c_vp, c_i32, c_i32, ctypes.POINTER(ctypes.c_int64)]),
     "sgn_factor_min_pivot": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "sgn_csc_block_dense": (ctypes.c_int, [c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp]),
     "sgn_csc_spmm": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,

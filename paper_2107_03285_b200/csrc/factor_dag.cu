@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <string>
 
 #include "../../include/sgn_b200.h"
@@ -861,12 +862,16 @@ k_factor_dag(const sgn::FactorArgs A) {
   // the earliest unfinished task is still always running (deadlock freedom unchanged).
   // An F_FAT task (a whole small front) runs its sub-tasks fat[a .. b) back to back under
   // the same index before the next grab.
-  if (tid == 0) { s_left = 0; s_sub = 0; s_subend = 0; }
+  if (tid == 0) { s_left = 0; s_sub = 0; s_subend = 0; s_idx = -1; }
+  const bool retiring = (int)blockIdx.x >= A.retire_from;
   for (;;) {
     __syncthreads();
     if (tid == 0) {
       if (s_sub < s_subend) {
         s_cur = s_sub++;
+      } else if (retiring && s_left == 0 && s_idx >= A.retire_at) {
+        s_idx = INT_MAX;                     // leave: the slot goes to the concurrent launch
+        s_cur = -1;
       } else {
         if (s_left == 0) { s_base = atomicAdd(A.head, A.run); s_left = A.run; }
         s_idx = s_base + (A.run - s_left);

@@ -11,6 +11,8 @@
 // solve panels Z = [I; L21] L11^{-1} built by the factorization.
 #include <cuda_runtime.h>
 
+#include <climits>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -1067,6 +1069,8 @@ struct sgn_factor_s {
   DevBuf<int64_t> ftrace;       // SGN_FDAG_TRACE=1: 4 words per factor task (diagnostics)
   DevBuf<int> fcnt;             // [head | batch x n_fcnt counters] of the persistent factorization
   int factor_grid = 0;
+  int retire_from = INT_MAX;       // sgn_factor_set_retire
+  int64_t retire_at = INT64_MAX;
   DevBuf<sgn::Task> stasks;
   DevBuf<int32_t> swaits, gsrc;
   DevBuf<int64_t> gptr;
@@ -1415,6 +1419,7 @@ static int factor_numeric_impl(sgn_factor f, const double* d_values, int64_t val
     const int r = atoi(e);
     if (r >= 1 && f->batch % r == 0) A.run = r;
   }
+  A.retire_from = f->retire_from; A.retire_at = f->retire_at;
   A.trace = nullptr;
   { const char* e = getenv("SGN_FDAG_TRACE");
     if (e && *e == '1') {
@@ -1536,6 +1541,24 @@ int sgn_factor_set_grid(sgn_factor f, int32_t ctas, int32_t* grid) {
   if (full <= 0) { sgn::last_error() = "set_grid: no CUDA device"; return SGN_CUDA_ERROR; }
   f->factor_grid = (ctas > 0) ? std::min(ctas, full) : full;
   if (grid) *grid = f->factor_grid;
+  return SGN_OK;
+}
+
+int sgn_factor_set_retire(sgn_factor f, int32_t keep_ctas, int32_t max_level_fronts, int64_t* retire_task) {
+  if (!f) { sgn::last_error() = "set_retire: invalid argument"; return SGN_INVALID; }
+  const sgn::Symbolic& s = f->sym->s;
+  f->retire_from = INT_MAX;
+  f->retire_at = INT64_MAX;
+  if (keep_ctas > 0 && max_level_fronts > 0) {
+    // the first level from which every level has at most max_level_fronts fronts
+    int32_t lv = s.n_levels;
+    while (lv > 0 && (int32_t)s.level_fronts[lv - 1].size() <= max_level_fronts) --lv;
+    if (lv < s.n_levels && lv > 0) {
+      f->retire_from = keep_ctas;
+      f->retire_at = s.level_task_off[lv] * (int64_t)f->batch;
+    }
+  }
+  if (retire_task) *retire_task = (f->retire_at == INT64_MAX) ? -1 : f->retire_at;
   return SGN_OK;
 }
 

@@ -189,6 +189,7 @@ struct Symbolic {
   // schedule
   int32_t n_levels = 0;
   std::vector<std::vector<int32_t>> level_fronts;
+  std::vector<int64_t> level_task_off;         // first factorization task of each level (ftasks index)
   std::vector<Work> work;                      // all work items
   std::vector<Launch> launches;                // factorization launch schedule
   // solve work lists per level (items into `work`): forward (f, row0), backward (f, col0)
@@ -227,6 +228,10 @@ struct FactorArgs {
   double* dscr; int64_t dstride; long long* status;
   unsigned long long* trace;   // optional (SGN_FDAG_TRACE=1): 4 words per task
   int32_t run;                 // instances per grab (divides batch; 1 for a single instance)
+  // CTAs with blockIdx >= retire_from leave once a task index >= retire_at has been reached
+  // (sgn_factor_set_retire): a concurrent launch takes over their SM slots for the
+  // dependency-bound top levels
+  int32_t retire_from; int64_t retire_at;
 };
 int factor_dag_grid();   // persistent CTAs: SMs x occupancy limit
 int min_pivot(const DFront* d_fronts, int32_t n_fronts, const double* d_fstore, double* out_min,

@@ -1180,8 +1180,10 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
     for (int64_t q = 0; q < zquota && zhead < zq.size() && zq_level[zhead] <= lv - 2; ++q)
       s.ftasks.push_back(zq[zhead++]);
   };
+  s.level_task_off.assign(s.n_levels, 0);
   for (int32_t lv = 0; lv < s.n_levels; ++lv) {
     const auto& fl = s.level_fronts[lv];
+    s.level_task_off[lv] = (int64_t)s.ftasks.size();
     for (int32_t f : fl) {
       const int32_t T = ntiles_front(s.fronts[f].npiv, s.fronts[f].nrow);
       if (opt.upd_pair & 4) {                        // 64x64 assembly blocks (F_ASM, k = 1)

@@ -158,6 +158,14 @@ class DeviceFactor:
         check(lib().sgn_factor_set_grid(self._h, int(ctas), ctypes.byref(out)), what="factor grid")
         return out.value
 
+    def set_retire(self, keep_ctas: int, max_level_fronts: int) -> int:
+        """CTAs >= keep_ctas leave the persistent factorization at the first top level of <=
+        max_level_fronts fronts (sgn_factor_set_retire); returns the hand-over task index (-1: off)."""
+        out = ctypes.c_int64()
+        check(lib().sgn_factor_set_retire(self._h, int(keep_ctas), int(max_level_fronts), ctypes.byref(out)),
+              what="factor retire")
+        return out.value
+
     def solve_multi(self, B, X, stream: int = 0) -> None:
         """X[j] = A^{-1} B[j] for the rows j of a (nrhs, n) float64 CUDA tensor (batch-1 factor)."""
         check(lib().sgn_factor_solve_multi(self._h, ptr(B), ptr(X), int(B.shape[0]), stream), what="multi solve")

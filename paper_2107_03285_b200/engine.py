@@ -488,6 +488,7 @@ def _gx_share(eng, full: int) -> int:
         fg = float(eng.gsym.stats()["flops"])
         eng._gx_frac = min(0.25, max(3.0 / 16.0, 1.85 * fg / max(fk, 1.0)))
     return max(1, int(round(eng._gx_frac * full)))
+_GX_RETIRE = int(os.environ.get("SGN_GX_RETIRE", "-1"))     # sweeps: top levels of <= k fronts hand CTAs over (0: off)
 _DEBUG_NAN = os.environ.get("SGN_DEBUG_NAN", "0") == "1"
 _DEBUG_NEWTON = os.environ.get("SGN_DEBUG_NEWTON", "0") == "1"
 
@@ -551,7 +552,18 @@ def _factor_adjoint(eng, st, cur, f0=None, f1=None, events=None):
     full = eng.kfac.set_grid(0)
     gx = _gx_share(eng, full)
     eng.gfac.set_grid(gx)
-    eng.kfac.set_grid(full - gx)
+    # option (SGN_GX_RETIRE=k, off by default): the KKT factor starts on the full grid and hands
+    # gx CTA slots over when it reaches its top levels of <= k fronts (sgn_factor_set_retire);
+    # the G_x launch, queued on the side stream, becomes resident then.  Measured on config 4
+    # (profiles/r02_gx_handover_sweep.txt): the KKT factor gains 1.3 ms, but the adjoint (G_x
+    # factor + 3 refined solves, ~6 ms on 111 CTAs) no longer fits in the tail: 27.3 -> 25.0
+    # directions/s at k = 8; configs 2 and 3 lose 10-20 %.  The two split the slots from the start.
+    handover = -1
+    lvf = max(_GX_RETIRE, 0)
+    if lvf > 0 and eng.batch == 1:
+        handover = eng.kfac.set_retire(full - gx, lvf)
+    if handover < 0:
+        eng.kfac.set_grid(full - gx)
     side = eng._side_stream
     ev_asm, ev_adj = torch.cuda.Event(), torch.cuda.Event()
     ev_asm.record(cur)
@@ -571,6 +583,7 @@ def _factor_adjoint(eng, st, cur, f0=None, f1=None, events=None):
     cur.wait_event(ev_adj)
     eng.gfac.set_grid(0)
     eng.kfac.set_grid(0)
+    eng.kfac.set_retire(0, 0)
     if events is not None:
         events[1].record()
     return res_a, it_a
