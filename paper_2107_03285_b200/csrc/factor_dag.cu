@@ -244,13 +244,20 @@ __device__ void f_asm2(const sgn::FactorArgs& A, const DFront& F, int b, int ti,
   __syncthreads();
   double* Fm = front_ptr(A, F, b);
   const int64_t ld = sgn::front_ld(F.nrow);
-  for (int e = tid; e < 64 * 64; e += kFThreads) {
-    const int ii = e & 63, jj = e >> 6;
-    const int x = ti + (ii >> 5), y = tj + (jj >> 5);
-    if (x >= T || y >= T || x < y) continue;
-    const int gi = sgn::tile_lo(F.npiv, x) + (ii & 31), gj = sgn::tile_lo(F.npiv, y) + (jj & 31);
-    if (gi < sgn::tile_hi(F.npiv, F.nrow, x) && gj < sgn::tile_hi(F.npiv, F.nrow, y))
-      Fm[(int64_t)gj * ld + gi] = Bk[ii * kA2 + jj];
+  {   // write-out: this thread's block row is fixed (kFThreads = 2 x 64), columns tid >> 6, +2, ...
+    const int ii = tid & 63, x = ti + (ii >> 5);
+    const int gi = (x < T) ? sgn::tile_lo(F.npiv, x) + (ii & 31) : 0;
+    const bool rok = x < T && gi < sgn::tile_hi(F.npiv, F.nrow, x);
+    for (int yh = 0; yh < 2; ++yh) {
+      const int y = tj + yh;
+      if (!rok || y >= T || x < y) continue;
+      const int lo = sgn::tile_lo(F.npiv, y), hi = sgn::tile_hi(F.npiv, F.nrow, y);
+      double* col = Fm + (int64_t)lo * ld + gi;
+      const double* brow_ = Bk + ii * kA2 + 32 * yh;
+#pragma unroll 4
+      for (int jl = tid >> 6; jl < 32; jl += 2)
+        if (lo + jl < hi) col[(int64_t)jl * ld] = brow_[jl];
+    }
   }
   if (ti == 0 && tj == 0 && F.npiv > 0) {       // D_0 for the caller: tile (0, 0), lower part
     double (*tile)[kTile + 1] = v33(S.a);
@@ -633,19 +640,25 @@ __device__ void f_block64(const sgn::FactorArgs& A, const DFront& F, int b, int 
     constexpr int kA2B = 20;
     static_assert(2 * 16 * kU2A + 2 * 64 * kA2B <= 5 * kTileWords, "cp.async buffers fit");
     const double* bsrc = ZP ? Zm : Fm;
+    // this thread's staging addresses are fixed for the task (kFThreads is a multiple of 32 and
+    // of 8): the A row pair and the NB / 16 B rows are resolved once, not per half step
+    const int cha = tid & 31, chb = tid & 7;
+    const int gra = max(brow(ti, 2 * cha), 0);
+    const double* asrc = Fm + gra;
+    const double* bsrcu[NB / 16];
+#pragma unroll
+    for (int u = 0; u < NB / 16; ++u) bsrcu[u] = bsrc + (int64_t)max(bcol((tid >> 3) + 16 * u), 0) * ld + 2 * chb;
     auto issue = [&](int hs, int buf) {
       const int c0 = (sa + (hs >> 1)) * kTile + 16 * (hs & 1);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {             // A: 16 columns x 32 row pairs
-        const int e = tid + u * kFThreads, ch = e & 31, c = e >> 5;
-        const int gr = brow(ti, 2 * ch);
-        cp16(&As2[(buf * 16 + c) * kU2A + 2 * ch], Fm + (int64_t)(c0 + c) * ld + (gr >= 0 ? gr : 0));
+        const int c = (tid >> 5) + 4 * u;
+        cp16(&As2[(buf * 16 + c) * kU2A + 2 * cha], asrc + (int64_t)(c0 + c) * ld);
       }
 #pragma unroll
       for (int u = 0; u < NB / 16; ++u) {       // B: NB rows x 8 k pairs
-        const int e = tid + u * kFThreads, ch = e & 7, j = e >> 3;
-        const int gc = bcol(j);
-        cp16(&Bs2[(buf * 64 + j) * kA2B + 2 * ch], bsrc + (int64_t)(gc >= 0 ? gc : 0) * ld + c0 + 2 * ch);
+        const int j = (tid >> 3) + 16 * u;
+        cp16(&Bs2[(buf * 64 + j) * kA2B + 2 * chb], bsrcu[u] + c0);
       }
       cp_commit();
     };
