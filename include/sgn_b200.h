@@ -102,7 +102,9 @@ typedef struct {
     int32_t upd_group_cb;  /* pivot steps per grouped update of contribution-block columns
                               (tj >= P: off the pivot chain, only the parent's assembly reads
                               them; default 32)                                              */
-    int32_t reserved[4];
+    int32_t defer_groups;  /* 1: grouped updates of step k are listed after the panels and the diagonal
+                            * update of step k + 1 (CTAs run them while that step's TRSMs are in flight) */
+    int32_t reserved[3];
 } sgn_symbolic_options;
 void sgn_symbolic_options_default(sgn_symbolic_options* o);
 /* as sgn_symbolic_create, with options (NULL = defaults) */

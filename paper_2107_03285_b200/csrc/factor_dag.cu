@@ -163,6 +163,27 @@ __device__ void f_asm2(const sgn::FactorArgs& A, const DFront& F, int b, int ti,
   double* Bk = &S.b[0][0];
   const int tid = threadIdx.x;
   const int T = sgn::ntiles_front(F.npiv, F.nrow);
+  // children's metadata (front, relative-row ranges of this block), one child per thread, into
+  // S.a while the block is cleared and the original entries load: the per-child chain
+  // children[] -> fronts[] -> reltile[] is paid once, in parallel, not once per child in turn
+  struct AsmChild { const double* Ur; const int32_t* rc; int64_t ldc; int r_lo, r_hi, s_lo, s_hi; };
+  constexpr int kMaxMeta = (int)(kTileWords * sizeof(double) / sizeof(AsmChild));
+  AsmChild* cm = reinterpret_cast<AsmChild*>(S.a);
+  const int nch = F.child_end - F.child_begin;
+  const double* fb = A.fstore + (int64_t)b * A.fstride;
+  for (int c = tid; c < min(nch, kMaxMeta); c += kFThreads) {
+    const DFront C = A.fronts[A.children[F.child_begin + c]];
+    AsmChild m;
+    m.Ur = nullptr; m.rc = nullptr; m.ldc = 0; m.r_lo = m.r_hi = m.s_lo = m.s_hi = 0;
+    if (C.nrow > C.npiv) {
+      const int32_t* rt = A.reltile + C.woff;
+      m.r_lo = rt[ti]; m.r_hi = rt[min(ti + 2, T)]; m.s_lo = rt[tj]; m.s_hi = rt[min(tj + 2, T)];
+      m.rc = A.rel + C.rel_off;
+      m.ldc = sgn::front_ld(C.nrow);
+      m.Ur = fb + C.foff + (int64_t)C.npiv * m.ldc + C.npiv;
+    }
+    cm[c] = m;
+  }
   for (int e = tid; e < 64 * kA2; e += kFThreads) Bk[e] = 0.0;
   __syncthreads();
   const double* vals = A.values + (int64_t)b * A.vstride;
@@ -195,19 +216,30 @@ __device__ void f_asm2(const sgn::FactorArgs& A, const DFront& F, int b, int ti,
       }
     }
   }
-  const double* fb = A.fstore + (int64_t)b * A.fstride;
-  for (int ci = F.child_begin; ci < F.child_end; ++ci) {
-    const DFront C = A.fronts[A.children[ci]];
-    const int cn = C.nrow - C.npiv;
-    __syncthreads();
-    if (cn == 0) continue;
-    const int32_t* rc = A.rel + C.rel_off;
-    const int32_t* rt = A.reltile + C.woff;
-    const int r_lo = rt[ti], r_hi = rt[min(ti + 2, T)], s_lo = rt[tj], s_hi = rt[min(tj + 2, T)];
+  __syncthreads();                              // original entries and the shift are in place
+  bool dirty = false;                           // adds of a child in flight since the last barrier
+  for (int ci = 0; ci < nch; ++ci) {
+    AsmChild m;
+    if (ci < kMaxMeta) {
+      m = cm[ci];
+    } else {                                    // (more children than metadata slots: direct loads)
+      const DFront C = A.fronts[A.children[F.child_begin + ci]];
+      m.Ur = nullptr; m.rc = nullptr; m.ldc = 0; m.r_lo = m.r_hi = m.s_lo = m.s_hi = 0;
+      if (C.nrow > C.npiv) {
+        const int32_t* rt = A.reltile + C.woff;
+        m.r_lo = rt[ti]; m.r_hi = rt[min(ti + 2, T)]; m.s_lo = rt[tj]; m.s_hi = rt[min(tj + 2, T)];
+        m.rc = A.rel + C.rel_off;
+        m.ldc = sgn::front_ld(C.nrow);
+        m.Ur = fb + C.foff + (int64_t)C.npiv * m.ldc + C.npiv;
+      }
+    }
+    const int32_t* rc = m.rc;
+    const int r_lo = m.r_lo, r_hi = m.r_hi, s_lo = m.s_lo, s_hi = m.s_hi;
     const int nr = r_hi - r_lo, ns = s_hi - s_lo;
-    if (nr <= 0 || ns <= 0) continue;
-    const double* U = fb + C.foff;
-    const int64_t ldc = sgn::front_ld(C.nrow);
+    if (nr <= 0 || ns <= 0) continue;           // (uniform: the metadata is the same for every thread)
+    if (dirty) __syncthreads();                 // children are added one after another, in child order
+    dirty = true;
+    const int64_t ldc = m.ldc;
     // A warp per child column, a lane per child row (nr <= 64: two rows per lane, their block
     // rows looked up once per child); four columns = 8 entries per thread in flight: the loads
     // (child update block, coalesced along the column) first, then the shared-memory adds
@@ -216,7 +248,7 @@ __device__ void f_asm2(const sgn::FactorArgs& A, const DFront& F, int b, int ti,
     const int ra = r_lo + lane, rb = ra + 32;
     const int ba = (ra < r_hi) ? bi(rc[ra]) * kA2 : -1;
     const int bb = (rb < r_hi) ? bi(rc[rb]) * kA2 : -1;
-    const double* Ur = U + (int64_t)C.npiv * ldc + C.npiv;
+    const double* Ur = m.Ur;
     // the warp's <= 16 columns (warp + 4 i): their block columns are loaded by lanes i next to
     // the row lookups above (one latency) and handed out by shuffles
     const int myc = warp + 4 * (lane & 15);

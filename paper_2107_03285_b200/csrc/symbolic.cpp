@@ -1181,6 +1181,23 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
       s.ftasks.push_back(zq[zhead++]);
   };
   s.level_task_off.assign(s.n_levels, 0);
+  // defer_groups: the grouped updates emitted at step k are held back until the panels and the
+  // diagonal update of step k + 1 are in the list.  They are ready when grabbed (their last step's
+  // TRSMs finished a step ago), so CTAs run them while step k + 1's TRSMs are in flight, instead of
+  // grabbing that step's look-ahead updates early and spinning on the TRSM counters.  Every task
+  // that consumes a deferred update (the column's single-step / look-ahead task, the next group,
+  // the parent's assembly) still comes later in the list.
+  struct Deferred { int32_t kind, k, f, a, b; };
+  std::vector<Deferred> deferred;
+  const bool defer_groups = opt.defer_groups != 0;
+  auto flush_deferred = [&]() {
+    for (const Deferred& d : deferred) ft(d.kind, d.k, d.f, d.a, d.b);
+    deferred.clear();
+  };
+  auto fg = [&](int32_t kind, int32_t k, int32_t f, int32_t a, int32_t b) {   // a grouped update
+    if (defer_groups) deferred.push_back(Deferred{kind, k, f, a, b});
+    else ft(kind, k, f, a, b);
+  };
   for (int32_t lv = 0; lv < s.n_levels; ++lv) {
     const auto& fl = s.level_fronts[lv];
     s.level_task_off[lv] = (int64_t)s.ftasks.size();
@@ -1207,6 +1224,7 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
         const Front& F = s.fronts[f];
         if (k + 1 < ptiles(F.npiv)) ft(F_DIAGUPD, k, f, 0, 0);
       }
+      flush_deferred();                                      // grouped updates of step k - 1
       for (int32_t f : fl) {                                 // look-ahead column first
         const Front& F = s.fronts[f];
         if (k >= ptiles(F.npiv)) continue;
@@ -1247,15 +1265,18 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
             ns = grouped_ns(tj);
             if (ns == 0) continue;
             if ((opt.upd_pair & 1) && T >= pair_tiles && grouped_ns(tj + 1) == ns) {
-              for (int32_t ti = tj; ti < T; ti += 2) ft(F_UPD2, k, f, ti, tj | (ns << 16));
+              for (int32_t ti = tj; ti < T; ti += 2) fg(F_UPD2, k, f, ti, tj | (ns << 16));
               ++tj;
               continue;
             }
           }
+          const bool grouped = k <= tj - 3;
           if ((opt.upd_pair & 8) && T >= pair_tiles) {         // row pairs (F_UPD2, one column)
-            for (int32_t ti = tj; ti < T; ti += 2) ft(F_UPD2, k, f, ti, tj | 0x8000 | (ns << 16));
+            for (int32_t ti = tj; ti < T; ti += 2)
+              grouped ? fg(F_UPD2, k, f, ti, tj | 0x8000 | (ns << 16)) : ft(F_UPD2, k, f, ti, tj | 0x8000 | (ns << 16));
           } else {
-            for (int32_t ti = tj; ti < T; ++ti) ft(F_UPDATE, k, f, ti, tj | (ns << 16));
+            for (int32_t ti = tj; ti < T; ++ti)
+              grouped ? fg(F_UPDATE, k, f, ti, tj | (ns << 16)) : ft(F_UPDATE, k, f, ti, tj | (ns << 16));
           }
         }
       }
@@ -1266,6 +1287,7 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
       }
       emit_z(lv);
     }
+    flush_deferred();                                        // before the parents' assembly
   }
   while (zhead < zq.size()) s.ftasks.push_back(zq[zhead++]);
   for (int32_t f = 0; f < NFr; ++f) {                    // fat fronts: sub-tasks, then their Z blocks

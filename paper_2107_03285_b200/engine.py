@@ -1226,7 +1226,10 @@ class DeviceEngine:
     def gfac(self):
         if self._gfac is None:
             pl = self.plan
-            self.gsym = symbolic_for(pl.n_x, pl.G_indptr, pl.G_indices)
+            # sweeps: SGN_GX_FAT_TILES / SGN_GX_LEAF_SIZE apply to the G_x analysis only
+            gopt = {k: int(os.environ[e]) for k, e in (("fat_tiles", "SGN_GX_FAT_TILES"), ("leaf_size", "SGN_GX_LEAF_SIZE"))
+                    if os.environ.get(e)}
+            self.gsym = symbolic_for(pl.n_x, pl.G_indptr, pl.G_indices, **gopt)
             self._gfac = DeviceFactor(self.gsym, self.batch)
         return self._gfac
 
