@@ -104,7 +104,10 @@ typedef struct {
                               them; default 32)                                              */
     int32_t defer_groups;  /* 1: grouped updates of step k are listed after the panels and the diagonal
                             * update of step k + 1 (CTAs run them while that step's TRSMs are in flight) */
-    int32_t reserved[3];
+    int32_t zdist;         /* queued solve-panel blocks of fronts at levels <= lv - zdist are interleaved into
+                            * the pivot steps of level lv (2: their fronts are finished by then; 1: the level
+                            * below, whose fronts may still be finishing) */
+    int32_t reserved[2];
 } sgn_symbolic_options;
 void sgn_symbolic_options_default(sgn_symbolic_options* o);
 /* as sgn_symbolic_create, with options (NULL = defaults) */

@@ -34,7 +34,7 @@ class SymbolicOptions(ctypes.Structure):
     _fields_ = [("leaf_size", c_i32), ("p_order", c_i32), ("upd_group", c_i32), ("zinline", c_i32),
                 ("zquota", c_i32), ("noz_tiles", c_i32), ("fat_tiles", c_i32), ("fat_solve", c_i32),
                 ("generic_pairs", c_i32), ("upd_pair", c_i32), ("pair_min_tiles", c_i32),
-                ("upd_group_cb", c_i32), ("defer_groups", c_i32), ("reserved", c_i32 * 3)]
+                ("upd_group_cb", c_i32), ("defer_groups", c_i32), ("zdist", c_i32), ("reserved", c_i32 * 2)]
 
 
 class LsqArgs(ctypes.Structure):

@@ -1224,7 +1224,7 @@ void sgn_symbolic_options_default(sgn_symbolic_options* o) {
   o->zinline = d.zinline; o->zquota = d.zquota; o->noz_tiles = d.noz_tiles;
   o->fat_tiles = d.fat_tiles; o->fat_solve = d.fat_solve; o->generic_pairs = d.generic_pairs;
   o->upd_pair = d.upd_pair; o->pair_min_tiles = d.pair_min_tiles; o->upd_group_cb = d.upd_group_cb;
-  o->defer_groups = d.defer_groups;
+  o->defer_groups = d.defer_groups; o->zdist = d.zdist;
 }
 
 int sgn_symbolic_create(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t n_x,
@@ -1250,6 +1250,7 @@ int sgn_symbolic_create_ex(int64_t n, const int64_t* indptr, const int64_t* indi
       so.pair_min_tiles = opts->pair_min_tiles;
       so.upd_group_cb = opts->upd_group_cb;
       so.defer_groups = opts->defer_groups;
+      so.zdist = std::max(1, opts->zdist);
     }
     if (!out || !indptr || n < 0) { sgn::last_error() = "bad arguments"; return SGN_INVALID; }
     auto h = std::make_unique<sgn_symbolic_s>();

@@ -166,7 +166,8 @@ struct SymOptions {
                               // (F_UPD2 with b bit 15, 64x32); default 15 = all
   int32_t pair_min_tiles = 0; // bits 0-1 apply to fronts of >= this many tiles (0: auto)
   int32_t upd_group_cb = 32;  // pivot steps per grouped update of contribution-block columns
-  int32_t defer_groups = 0;   // grouped updates of step k listed after the panels / diagonal update of step k + 1
+  int32_t defer_groups = 1;   // grouped updates of step k listed after the panels / diagonal update of step k + 1
+  int32_t zdist = 2;          // queued Z blocks of fronts at levels <= lv - zdist are interleaved into level lv
 };
 
 struct Symbolic {

@@ -1177,7 +1177,7 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
   size_t zhead = 0;
   const int64_t zquota = std::max(0, opt.zquota);
   auto emit_z = [&](int32_t lv) {
-    for (int64_t q = 0; q < zquota && zhead < zq.size() && zq_level[zhead] <= lv - 2; ++q)
+    for (int64_t q = 0; q < zquota && zhead < zq.size() && zq_level[zhead] <= lv - std::max(1, opt.zdist); ++q)
       s.ftasks.push_back(zq[zhead++]);
   };
   s.level_task_off.assign(s.n_levels, 0);

@@ -28,7 +28,7 @@ _OPTION_ENV = {"leaf_size": "SGN_LEAF_SIZE", "upd_group": "SGN_UPD_GROUP", "zinl
                "zquota": "SGN_ZQUOTA", "noz_tiles": "SGN_NOZ_TILES", "fat_tiles": "SGN_FAT_TILES",
                "fat_solve": "SGN_FAT_SOLVE", "generic_pairs": "SGN_GENERIC_PAIRS", "p_order": "SGN_P_ORDER",
                "upd_pair": "SGN_UPD_PAIR", "pair_min_tiles": "SGN_PAIR_MIN_TILES",
-               "upd_group_cb": "SGN_UPD_GROUP_CB", "defer_groups": "SGN_DEFER_GROUPS"}
+               "upd_group_cb": "SGN_UPD_GROUP_CB", "defer_groups": "SGN_DEFER_GROUPS", "zdist": "SGN_ZDIST"}
 
 
 def symbolic_options(**kw) -> "_lib.SymbolicOptions":
