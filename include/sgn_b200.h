@@ -95,7 +95,9 @@ typedef struct {
     int32_t generic_pairs; /* generic mode: 2x2 pivots on consecutive unknowns (default 1)   */
     int32_t upd_pair;      /* 64x64 task blocks: bit 0 grouped Schur updates, bit 1 struct-tile
                               solve-panel blocks, bit 2 front assembly, bit 3 single-column
-                              updates as 64x32 row pairs (default 15)                         */
+                              updates as 64x32 row pairs, bit 4 the look-ahead and single-step
+                              columns of a step as one 64x64 block per row pair below the
+                              chain rows (default 31)                                         */
     int32_t pair_min_tiles;/* bits 0-1 of upd_pair apply to fronts of >= this many 32-row tiles;
                               0 (default) = auto: 4 when the factorization has >= 5e9 flops,
                               else none (small factorizations are pivot-chain bound)          */

@@ -159,11 +159,13 @@ struct SymOptions {
   int32_t fat_tiles = 0;      // fronts of <= fat_tiles tiles factor as one task (0: off)
   int32_t fat_solve = 1;      // small fronts solve as one task
   int32_t generic_pairs = 1;  // generic mode: 2x2 pivots on consecutive unknowns
-  int32_t upd_pair = 15;      // grouped Schur updates on 64x64 blocks (F_UPD2); bit 1: struct-tile
+  int32_t upd_pair = 31;      // grouped Schur updates on 64x64 blocks (F_UPD2); bit 1: struct-tile
                               // Z blocks on 64x64 blocks too (F_ZPAN2); bit 2: assembly
                               // on 64x64 blocks (F_ASM, k = 1); bit 3: single-column updates
                               // (look-ahead, single-step, unpaired groups) as row pairs
-                              // (F_UPD2 with b bit 15, 64x32); default 15 = all
+                              // (F_UPD2 with b bit 15, 64x32); bit 4: look-ahead column k + 1 and
+                              // single-step column k + 2 of step k as one 64x64 block per row pair
+                              // below the chain rows; default 31 = all
   int32_t pair_min_tiles = 0; // bits 0-1 apply to fronts of >= this many tiles (0: auto)
   int32_t upd_group_cb = 32;  // pivot steps per grouped update of contribution-block columns
   int32_t defer_groups = 1;   // grouped updates of step k listed after the panels / diagonal update of step k + 1

@@ -1233,7 +1233,14 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
         if (k + 1 < T) {
           const int32_t t0 = diag_next ? k + 2 : k + 1;
           if ((opt.upd_pair & 8) && T >= pair_tiles) {       // row pairs (F_UPD2, one column)
-            for (int32_t ti = t0; ti < T; ti += 2) ft(F_UPD2, k, f, ti, (k + 1) | 0x8000 | (1 << 16));
+            // bit 4: below the first row pair (the chain's tiles), the look-ahead column k + 1
+            // and the single-step column k + 2 -- both take exactly step k -- go as one 64x64
+            // block per row pair: half the tasks of the two most numerous task kinds
+            const bool merge = (opt.upd_pair & 16) && diag_next && k + 2 < T;
+            for (int32_t ti = t0; ti < T; ti += 2) {
+              if (merge && ti > t0) ft(F_UPD2, k, f, ti, (k + 1) | (1 << 16));
+              else ft(F_UPD2, k, f, ti, (k + 1) | 0x8000 | (1 << 16));
+            }
           } else {
             for (int32_t ti = t0; ti < T; ++ti) ft(F_UPDATE, k, f, ti, k + 1);
           }
@@ -1272,7 +1279,9 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
           }
           const bool grouped = k <= tj - 3;
           if ((opt.upd_pair & 8) && T >= pair_tiles) {         // row pairs (F_UPD2, one column)
-            for (int32_t ti = tj; ti < T; ti += 2)
+            // (bit 4: column k + 2's rows below its first pair went with the look-ahead column)
+            const bool merged = (opt.upd_pair & 16) && !grouped && tj == k + 2 && k + 1 < P;
+            for (int32_t ti = tj; ti < (merged ? std::min(tj + 2, T) : T); ti += 2)
               grouped ? fg(F_UPD2, k, f, ti, tj | 0x8000 | (ns << 16)) : ft(F_UPD2, k, f, ti, tj | 0x8000 | (ns << 16));
           } else {
             for (int32_t ti = tj; ti < T; ++ti)
