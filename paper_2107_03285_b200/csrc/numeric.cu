@@ -94,8 +94,11 @@ __device__ __forceinline__ void dag_mark(const SolveArgs& A, int64_t idx, int sl
 }
 
 __device__ __forceinline__ void dag_wait(const SolveArgs& A, const sgn::Task& T, const int* cnt) {
-  if (threadIdx.x == 0) {
-    for (int w = T.w0; w < T.w1; ++w) {
+  // one (counter, target) pair per lane of warp 0: the acquire loads of a task's waits are in
+  // flight together instead of one L2 round trip after another; the barrier orders every
+  // thread of the CTA after all of them
+  if (threadIdx.x < 32) {
+    for (int w = T.w0 + (int)threadIdx.x; w < T.w1; w += 32) {
       const int* c = cnt + A.waits[2 * w];
       const int target = A.waits[2 * w + 1];
       if (A.mode & 1) { while (ld_acquire(c) < target) { } }

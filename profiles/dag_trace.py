@@ -23,8 +23,13 @@ def main():
     os.environ["SGN_BICG_GRAPH"] = "0"      # trace buffers are allocated lazily (not under capture)
     import torch
     from paper_2107_03285_b200._lib import lib
-    from paper_2107_03285_b200.problems import build_sheet
-    prob, p0 = build_sheet(a.config)
+    from paper_2107_03285_b200.problems import build_beam, build_sheet, build_shell
+    if a.config == 3:
+        prob, p0, _ = build_beam(0)
+    elif a.config == 4:
+        prob, p0 = build_shell(201, 100)
+    else:
+        prob, p0 = build_sheet(a.config)
     x = prob.simulate(p0)
     prob._load(x, p0)
     eng = prob.engine
