@@ -432,12 +432,14 @@ __device__ bool dag_fwd_fat(const SolveArgs& A, const sgn::Task& T, int b, const
     }
   }
   __syncthreads();
-  if (warp < ntile) {
+  // warp w finishes row tiles w, w + 8, ...; pivot rows (npiv <= kFwdCols = 64) are all in
+  // tiles 0 and 1, whose D entries warps 0 and 1 loaded above
+  for (int tt = warp; tt < ntile; tt += kSolveThreads / 32) {
     double t = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) t += redf[warp][w][lane];
+    for (int w = 0; w < 8; ++w) t += redf[tt][w][lane];
     const double tp = __shfl_xor_sync(0xffffffffu, t, 1);   // 2x2 pivot partner row
-    const int r = 32 * warp + lane;
+    const int r = 32 * tt + lane;
     if (r < npiv) {
       double* zb = A.zbuf + (int64_t)b * A.n;
       if (F.pivtype == 2) {

@@ -135,7 +135,7 @@ constexpr int kFwdRows = 32;    // rows per CTA of the forward-solve GEMV
 constexpr int kFwdCols = 64;    // columns (K chunk) per CTA of the forward-solve GEMV
 constexpr int kBwdCols = 32;    // columns per CTA of the backward-solve dots
 constexpr int kBwdRows = 128;   // rows (K chunk) per CTA of the backward-solve dots
-constexpr int kFatRows = 256;     // rows of a one-task ("fat") forward front solve
+constexpr int kFatRows = 512;     // rows of a one-task ("fat") forward front solve
 constexpr int kFatRowsBwd = 128;  // rows of a one-task backward front solve (Z prefetched whole)
 // Persistent dependency-driven (DAG) schedule: a task runs after every (counter, target)
 // wait in waits[w0, w1) is met, then bumps counter `sig` (-1: none).  Tasks are listed in a
