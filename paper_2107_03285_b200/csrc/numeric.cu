@@ -140,14 +140,14 @@ __device__ __forceinline__ double dag_combine(const double* pp, int nch, double 
   return s;
 }
 
-// Forward GEMV task (front, 32-row tile, 64-column chunk).  Before waiting it prefetches
-// its Z tile (8 values per thread) and the inverse gather map of the v entries it needs
-// (64 chunk columns + its own struct rows); after the children are done it forms those v
+// Forward GEMV task (front, 32-row tile, kFwdChunk = 128-column chunk).  Before waiting it prefetches
+// its Z tile (16 values per thread) and the inverse gather map of the v entries it needs
+// (the chunk columns + its own struct rows); after the children are done it forms those v
 // entries (b + children updates in child order), multiplies, and the group's last CTA
 // emits z = D^{-1} y1 (pivot rows) or u = v2 - t (struct rows, the parent's update).
 __device__ bool dag_fwd(const SolveArgs& A, const sgn::Task& T, int b, const int* cnt, int64_t idx) {
   __shared__ double red[8][33];
-  __shared__ double vs[sgn::kFwdCols + sgn::kFwdRows];
+  __shared__ double vs[sgn::kFwdChunk + sgn::kFwdRows];
   const DFront F = A.fronts[T.f];
   const int r0 = T.a, k = T.b, g = T.c;
   if (A.nop || (A.leading && F.is_root_p)) { dag_wait(A, T, cnt); return k == 0; }
@@ -155,23 +155,24 @@ __device__ bool dag_fwd(const SolveArgs& A, const sgn::Task& T, int b, const int
   const int nr = min(sgn::kFwdRows, F.nrow - r0);
   const int npiv = F.npiv;
   const int cend = (r0 < npiv) ? min(npiv, r0 + nr) : npiv;
-  const int c_lo = k * sgn::kFwdCols, c_hi = min(c_lo + sgn::kFwdCols, cend);
+  const int c_lo = k * sgn::kFwdChunk, c_hi = min(c_lo + sgn::kFwdChunk, cend);
   const double* Zm = A.zstore + (int64_t)b * A.zstride + F.zoff;
   const int64_t ld = sgn::front_ld(F.nrow);
-  double z[8];
+  constexpr int NZ = sgn::kFwdChunk / 8;
+  double z[NZ];
   {
     const double* zr = Zm + r0 + lane;
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
+    for (int m = 0; m < NZ; ++m) {
       const int c = c_lo + warp + 8 * m;
       z[m] = (lane < nr && c < c_hi) ? zr[(int64_t)c * ld] : 0.0;
     }
   }
   int vr = -1;
-  if (tid < sgn::kFwdCols) {
+  if (tid < sgn::kFwdChunk) {
     if (c_lo + tid < c_hi) vr = c_lo + tid;
-  } else if (tid < sgn::kFwdCols + sgn::kFwdRows) {
-    const int r = r0 + tid - sgn::kFwdCols;
+  } else if (tid < sgn::kFwdChunk + sgn::kFwdRows) {
+    const int r = r0 + tid - sgn::kFwdChunk;
     if (r < F.nrow && r >= npiv) vr = r;
   }
   double base = 0.0;
@@ -200,7 +201,7 @@ __device__ bool dag_fwd(const SolveArgs& A, const sgn::Task& T, int b, const int
   dag_mark(A, idx, 2);
   dag_wait(A, T, cnt);
   dag_mark(A, idx, 3);
-  if (tid < sgn::kFwdCols + sgn::kFwdRows) {
+  if (tid < sgn::kFwdChunk + sgn::kFwdRows) {
     double v = 0.0;
     if (vr >= 0) {
       const double* ub = A.ubuf + (int64_t)b * A.ustride;
@@ -217,7 +218,7 @@ __device__ bool dag_fwd(const SolveArgs& A, const sgn::Task& T, int b, const int
   __syncthreads();
   double acc = 0.0;
 #pragma unroll
-  for (int m = 0; m < 8; ++m) acc += z[m] * vs[warp + 8 * m];
+  for (int m = 0; m < NZ; ++m) acc += z[m] * vs[warp + 8 * m];
   red[warp][lane] = acc;
   __syncthreads();
   const int nch = A.grp_nchunk[g];
@@ -246,7 +247,7 @@ __device__ bool dag_fwd(const SolveArgs& A, const sgn::Task& T, int b, const int
           zb[F.first + r] = t / da;
         }
       } else {
-        A.ubuf[(int64_t)b * A.ustride + F.uoff + (r - npiv)] = vs[sgn::kFwdCols + lane] - t;
+        A.ubuf[(int64_t)b * A.ustride + F.uoff + (r - npiv)] = vs[sgn::kFwdChunk + lane] - t;
       }
     }
   }

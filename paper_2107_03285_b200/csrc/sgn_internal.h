@@ -132,7 +132,8 @@ struct Work { int32_t f, a, b, c; };   // generic work item
 
 enum LaunchKind : int32_t { L_ASM = 0, L_PANEL = 1, L_UPDATE = 2, L_ZPANEL = 3 };
 constexpr int kFwdRows = 32;    // rows per CTA of the forward-solve GEMV
-constexpr int kFwdCols = 64;    // columns (K chunk) per CTA of the forward-solve GEMV
+constexpr int kFwdCols = 64;    // pivot columns of a one-task ("fat") forward front solve
+constexpr int kFwdChunk = 128;  // columns (K chunk) per CTA of the tiled forward-solve GEMV
 constexpr int kBwdCols = 32;    // columns per CTA of the backward-solve dots
 constexpr int kBwdRows = 128;   // rows (K chunk) per CTA of the backward-solve dots
 constexpr int kFatRows = 512;     // rows of a one-task ("fat") forward front solve

@@ -1355,7 +1355,7 @@ int build_symbolic(Symbolic& s, const SymOptions& opt, int64_t* pivot_index) {
       if (fat_front(F, fat_rows)) { s.work.push_back({f, -1, 0, new_group(1)}); continue; }
       for (int32_t r0 = 0; r0 < F.nrow; r0 += kFwdRows) {
         const int32_t cend = (r0 < F.npiv) ? std::min(F.npiv, r0 + kFwdRows) : F.npiv;
-        const int32_t nch = std::max(1, (cend + kFwdCols - 1) / kFwdCols);
+        const int32_t nch = std::max(1, (cend + kFwdChunk - 1) / kFwdChunk);
         const int32_t g = new_group(nch);
         for (int32_t k = 0; k < nch; ++k) s.work.push_back({f, r0, k, g});
       }
