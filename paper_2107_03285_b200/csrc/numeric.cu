@@ -254,8 +254,9 @@ __device__ bool dag_fwd(const SolveArgs& A, const sgn::Task& T, int b, const int
   return true;
 }
 
-// Backward task (front, 32-column tile, 128-row chunk): x1 = Z^T [z1; -x2] as column dots.
-// Z (16 values per thread) and the struct-row map are prefetched before the wait.
+// Backward task (front, 32-column tile, kBwdRows = 256-row chunk): x1 = Z^T [z1; -x2] as column
+// dots.  Z of the first 128 rows (16 values per thread) and the struct-row map are prefetched
+// before the wait; the second 128 rows stream through the same registers afterwards.
 __device__ bool dag_bwd(const SolveArgs& A, const sgn::Task& T, int b, const int* cnt, int64_t idx) {
   __shared__ double colsum[32];
   __shared__ double vs[sgn::kBwdRows];
@@ -303,11 +304,34 @@ __device__ bool dag_bwd(const SolveArgs& A, const sgn::Task& T, int b, const int
     vs[tid] = v;
   }
   __syncthreads();
+  // rows rs .. rs + 127 from the prefetched Z values, then (chunks of more than 128 rows) the
+  // second half through the same registers: one task, one wait and one ticket per 256 rows
+  double acc[4];
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
-    double a = 0.0;
+    acc[m] = 0.0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a += z[m][i] * vs[lane + 32 * i];
+    for (int i = 0; i < 4; ++i) acc[m] += z[m][i] * vs[lane + 32 * i];
+  }
+  if (re - rs > 128) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int j = c0 + warp + 8 * m;
+      const bool colok = (warp + 8 * m < ncol);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = rs + 128 + lane + 32 * i;
+        z[m][i] = (colok && r < re && r >= j) ? Zm[(int64_t)j * ld + r] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[m] += z[m][i] * vs[128 + lane + 32 * i];
+  }
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    double a = acc[m];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if (lane == 0) colsum[warp + 8 * m] = a;

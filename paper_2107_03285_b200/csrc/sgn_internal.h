@@ -135,7 +135,7 @@ constexpr int kFwdRows = 32;    // rows per CTA of the forward-solve GEMV
 constexpr int kFwdCols = 64;    // pivot columns of a one-task ("fat") forward front solve
 constexpr int kFwdChunk = 128;  // columns (K chunk) per CTA of the tiled forward-solve GEMV
 constexpr int kBwdCols = 32;    // columns per CTA of the backward-solve dots
-constexpr int kBwdRows = 128;   // rows (K chunk) per CTA of the backward-solve dots
+constexpr int kBwdRows = 256;   // rows (K chunk) per CTA of the backward-solve dots (two 128-row halves)
 constexpr int kFatRows = 512;     // rows of a one-task ("fat") forward front solve
 constexpr int kFatRowsBwd = 128;  // rows of a one-task backward front solve (Z prefetched whole)
 // Persistent dependency-driven (DAG) schedule: a task runs after every (counter, target)
