@@ -131,3 +131,31 @@ def test_symmetric_indefinite_zero_diagonal(cuda, n, seed):
     ref = np.linalg.solve(dense, b)
     assert np.linalg.norm(dense @ x - b) <= 1e-10 * np.linalg.norm(b)
     assert np.linalg.norm(x - ref) <= 1e-8 * np.linalg.norm(ref) * max(1.0, np.linalg.cond(dense) * 1e-6)
+
+
+def test_cta_hand_over_option_keeps_the_factorization(cuda):
+    """sgn_factor_set_retire: CTAs past the kept share leave at the top levels; the task
+    order per tile is unchanged, so the factor and the solve are bitwise the same."""
+    import torch
+    from paper_2107_03285_b200.device import DeviceFactor, symbolic_for
+    g = grid_laplacian(60, 50, 2, seed=5).tocsc()
+    g.sort_indices()
+    sym = symbolic_for(g.shape[0], g.indptr, g.indices)
+    fac = DeviceFactor(sym, 1)
+    vals = torch.as_tensor(g.data, dtype=torch.float64, device="cuda").reshape(1, -1)
+    b = torch.as_tensor(np.random.default_rng(6).standard_normal(g.shape[0]), device="cuda").reshape(1, -1)
+    x0, x1 = torch.empty_like(b), torch.empty_like(b)
+    fac.numeric(vals)
+    fac.check()
+    fac.solve(b, x0)
+    full = fac.set_grid(0)
+    task = fac.set_retire(max(1, full // 4), 4)
+    assert task >= 0                                   # a hand-over point exists (top levels of <= 4 fronts)
+    fac.numeric(vals)
+    fac.check()
+    fac.solve(b, x1)
+    assert fac.set_retire(0, 0) == -1
+    torch.cuda.synchronize()
+    assert torch.equal(x0, x1)
+    expect = sp.linalg.spsolve(g, b[0].cpu().numpy())
+    assert np.linalg.norm(x1[0].cpu().numpy() - expect) <= 1e-10 * np.linalg.norm(expect)
